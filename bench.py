@@ -1,0 +1,424 @@
+#!/usr/bin/env python
+"""Benchmark: LJ FP64 pair-interactions/s on B200 (BASELINE.json metric).
+
+Workload (N=1): BASELINE config 2 at rho = 0.8 -- 1,000,000 particles,
+uniform random (RSA, min distance 0.9, seed 42) in a periodic cube, LJ
+cutoff 2.5, FP64.  A step is one force phase over the resident particles
+(the reference's metric region, driver.py:203-207: traversal + kernel);
+the neighbor structure is built before the timed region.  The L2 is
+flushed (256 MiB write) before every timed step; only the force phase is
+inside the CUDA-event bracket.  With --gpus N > 1 every rank runs its own
+1M-particle box (replicas, weak scaling, no data-path collective).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config LABEL]
+    python bench.py --impl reference ...   # the reference algorithm on host cores
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FLOPS_PER_PAIR = {False: 22, True: 25}   # SURVEY.md §8(d), counted on executor.py:93-111
+DEFAULT_CONFIG = "lc,lc_c01,false,two_by_half"
+METRIC = "LJ FP64 pair-interactions/sec"
+UNIT = "pair-interactions/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default=DEFAULT_CONFIG)
+    ap.add_argument("--rho", type=float, default=0.8)
+    ap.add_argument("--n", type=int, default=1_000_000)
+    ap.add_argument("--vector-width", type=int, default=8)
+    ap.add_argument("--energy", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sweep", action="store_true", help="time every config, write gpurun_out/sweep.json")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ clocks
+REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+           0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+           0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+           0x100: "display_clock_setting"}
+
+
+class ClockSampler:
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        self.proc.wait()
+        sm, mx, reasons = [], [], set()
+        with open(self.path) as fh:
+            for line in fh:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 3:
+                    continue
+                try:
+                    sm.append(float(parts[0]))
+                    mx.append(float(parts[1]))
+                    mask = int(parts[2], 16)
+                except ValueError:
+                    continue
+                for bit, name in REASONS.items():
+                    if mask & bit and name != "gpu_idle":
+                        reasons.add(name)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------------- workload
+def make_workload(args, device, seed):
+    from paper_2512_03565_b200 import workloads
+    return workloads.config2(args.rho, n=args.n, seed=seed, device=device)
+
+
+def params_for(cfg, w):
+    from paper_2512_03565_b200 import LJParams
+    # linked cells with cell size = cutoff (skin 0); Verlet/cluster lists skin 0.3
+    skin = 0.0 if cfg.container.value == "lc" else w.skin
+    return LJParams(cutoff=w.cutoff, skin=skin)
+
+
+def fp64_peak_tflops(torch, N) -> float:
+    """Measured FP64 DFMA peak on this GPU (lmd_dfma_burn, best of 5)."""
+    sms = N.load().lmd_device_sm_count()
+    blocks, threads, iters = sms * 8, 256, 400
+    scratch = torch.empty(threads, dtype=torch.float64, device="cuda")
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    best = 1e30
+    for rep in range(7):
+        e0.record()
+        N.call("lmd_dfma_burn", blocks, threads, iters, N.ptr(scratch), N.stream())
+        e1.record()
+        e1.synchronize()
+        if rep >= 2:
+            best = min(best, e0.elapsed_time(e1) * 1e-3)
+    flops = blocks * threads * iters * 128 * 2.0
+    return flops / best / 1e12
+
+
+class LCStepper:
+    """Holds a built container and launches one force phase per step."""
+
+    def __init__(self, cont, pattern, energy, torch, N):
+        self.cont = cont
+        self.pattern = pattern
+        self.energy = energy
+        dev = cont._pos4.device
+        self.stats_t = N.new_stats(dev)
+        slots = int(N.load().lmd_lc_ev_slots(cont.grid))
+        self.ev_t = torch.empty(2 * slots, dtype=torch.float64, device=dev)
+
+    def launch(self):
+        return self.cont.launch_force(self.pattern, self.energy, self.stats_t, self.ev_t)
+
+    launches_per_step = 1
+
+
+def build_stepper(cfg, w, args, torch, N):
+    import paper_2512_03565_b200 as B
+    params = params_for(cfg, w)
+    box = B.SimulationBox.cube(w.box_length, periodic=True)
+    buf = B.ParticleBuffer.from_positions(w.positions.cpu().numpy(), device="cuda")
+    cont = B.make_container(cfg.container, box, params, cluster_size=args.vector_width)
+    cont.rebuild(buf)
+    cont.refresh(buf)
+    if cfg.container.value != "lc":
+        raise SystemExit(f"bench: container {cfg.container.value} not wired yet")
+    stepper = LCStepper(cont, cfg.pattern, args.energy, torch, N)
+    a, b = cfg.pattern.shape(args.vector_width)
+    inv, slots, useful = cont._lc_stats(B.traversals.traversal_code(cfg.traversal), cfg.newton3,
+                                        cfg.pattern, args.vector_width)
+    return stepper, cont, buf, box, params, (inv, slots, useful)
+
+
+def time_steps(stepper, steps, flush, torch):
+    """Per-step CUDA-event brackets around the force phase; L2 flushed before each."""
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(steps)]
+    for k in range(steps):
+        flush.fill_(k & 0xFF)
+        evs[k][0].record()
+        stepper.launch()
+        evs[k][1].record()
+    torch.cuda.synchronize()
+    return [a.elapsed_time(b) * 1e-3 for a, b in evs]
+
+
+def cpu_baseline_lc(w, cfg, params, threads):
+    from oracle import oracle as O
+    span = w.box_length
+    pos = w.positions.cpu().numpy() if hasattr(w.positions, "cpu") else w.positions
+    trav = cfg.traversal.value
+    n3 = cfg.newton3
+    if threads > 1 and n3:
+        trav, n3 = "lc_c01", False       # the parallel baseline sweeps Newton3-off units
+    t0 = time.perf_counter()
+    h = O.PreparedLC(pos, np.zeros(3), np.full(3, span), [True] * 3, params, trav, n3,
+                     cfg.pattern.value, 8, omp=threads > 1)
+    prep = time.perf_counter() - t0
+    return h, prep, trav, n3
+
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2512_03565_b200 as B
+    from paper_2512_03565_b200 import _native as N
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = B.Configuration.parse(args.config)
+    w = make_workload(args, "cuda", 42 + rank)
+    stepper, cont, buf, box, params, geo = build_stepper(cfg, w, args, torch, N)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    peak = fp64_peak_tflops(torch, N)
+
+    for _ in range(max(args.warmup, 3)):
+        flush.fill_(1)
+        stepper.launch()
+    torch.cuda.synchronize()
+    st = N.read_stats(stepper.stats_t)
+    stats = cont.finish_stats(st, cfg.newton3, *geo)
+    pairs = stats.pair_interactions
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    per_step = time_steps(stepper, args.steps, flush, torch)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    t_force = sum(per_step)
+    t_max = t_force
+    if world > 1:
+        t = torch.tensor([t_force], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_max = float(t.item())
+    # results must not have changed across the timed steps (deterministic counts)
+    st2 = N.read_stats(stepper.stats_t)
+    assert st2.pair_interactions == st.pair_interactions and not st2.overlap
+
+    value = pairs * args.steps * world / t_max
+    avg_launch = t_force / args.steps
+    flops = pairs * FLOPS_PER_PAIR[cfg.newton3]
+    achieved = flops / avg_launch / 1e12
+
+    # ------------------------------------------------ e2e through the public API
+    e2e = None
+    if args.e2e_steps > 0:
+        host = {k: np.ascontiguousarray(v) for k, v in
+                zip(("pos_x", "pos_y", "pos_z"), w.positions.cpu().numpy().T)}
+        n = len(host["pos_x"])
+
+        class HostBuffer:
+            pass
+
+        hb = HostBuffer()
+        for k, v in host.items():
+            setattr(hb, k, torch.from_numpy(v).pin_memory())
+        for k in ("vel_x", "vel_y", "vel_z", "old_force_x", "old_force_y", "old_force_z"):
+            setattr(hb, k, None)
+        for k in ("force_x", "force_y", "force_z"):
+            setattr(hb, k, torch.zeros(n, dtype=torch.float64).pin_memory())
+        hb.id = None
+        hb.ownership = torch.zeros(n, dtype=torch.int8).pin_memory()
+        B.force_phase(hb, box, params, cfg, args.vector_width)       # warm
+        torch.cuda.synchronize()
+        times = []
+        for _ in range(args.e2e_steps):
+            flush.fill_(3)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            s_e2e = B.force_phase(hb, box, params, cfg, args.vector_width)
+            torch.cuda.synchronize()
+            times.append(time.perf_counter() - t0)
+            assert s_e2e.pair_interactions == pairs
+        t_e2e = max(times) if world == 1 else max(times)
+        tt = torch.tensor([sum(times)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e = {"value": pairs * args.e2e_steps * world / float(tt.item()), "unit": UNIT,
+               "h2d_bytes_per_step": int(n * (3 * 8 + 1)),
+               "d2h_bytes_per_step": int(n * 3 * 8),
+               "steps": args.e2e_steps,
+               "note": "force_phase() on pinned host SoA buffers: H2D positions, device "
+                       "binning/halo/sort, force kernel, D2H forces"}
+
+    # ------------------------------------------------------------ CPU baseline
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            h, prep, trav, n3 = cpu_baseline_lc(w, cfg, params, 1)
+            t0 = time.perf_counter()
+            _, ost = h.execute(1)
+            dt = time.perf_counter() - t0
+            h.close()
+            cpu = {"value": ost.pair_interactions / dt, "unit": UNIT, "cores": 1, "kind": "port",
+                   "sample": f"one full force phase of the same {w.n}-particle workload, "
+                             f"{trav} newton3={n3}, oracle/lj_oracle.c (bitwise restatement of "
+                             f"the reference's numba sweep), 1 thread; prepare {prep:.1f}s "
+                             f"untimed, sweep {dt:.2f}s",
+                   "cpu_pairs_match_gpu": ost.pair_interactions == pairs}
+        except Exception as exc:  # pragma: no cover - reported, not fatal
+            cpu = {"value": None, "error": repr(exc)}
+
+    if args.sweep and rank == 0:
+        sweep(args, w, torch, N, flush)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": t_max / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": w.name, "particles_per_gpu": w.n, "rho": args.rho,
+                       "box_length": w.box_length, "cutoff": w.cutoff, "skin": params.skin,
+                       "configuration": cfg.label, "vector_width": args.vector_width,
+                       "pairs_per_step_per_gpu": pairs,
+                       "useful_interactions": stats.useful_interactions,
+                       "candidate_efficiency": pairs / max(stats.useful_interactions, 1),
+                       "l2": "flushed (256 MiB write) before every timed step",
+                       "parallelism": "replicas" if world > 1 else "single",
+                       "inputs": w.note},
+            "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak,
+                         "unit": "TFLOP/s", "frac": achieved / peak,
+                         "flops_per_pair": FLOPS_PER_PAIR[cfg.newton3],
+                         "peak_source": "measured in this run: lmd_dfma_burn (DFMA, 2 flop)",
+                         "traffic": None},
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "gpu_launches": args.steps * stepper.launches_per_step,
+            "clocks": clocks,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def sweep(args, w, torch, N, flush):
+    import paper_2512_03565_b200 as B
+    rows = []
+    labels = [c.label for c in B.enumerate_search_space(
+        [B.ContainerKind.LINKED_CELLS], [B.TraversalKind.LC_C01, B.TraversalKind.LC_C18],
+        [False, True], list(B.PATTERN_ORDER))]
+    for label in labels:
+        cfg = B.Configuration.parse(label)
+        stepper, cont, *_ = build_stepper(cfg, w, args, torch, N)
+        for _ in range(3):
+            stepper.launch()
+        t = time_steps(stepper, 5, flush, torch)
+        st = N.read_stats(stepper.stats_t)
+        pairs = st.pair_interactions if not cfg.newton3 else \
+            (st.pair_interactions - st.pairs_owned_halo) // 2 + st.pairs_owned_halo
+        rows.append({"config": label, "ms": min(t) * 1e3, "pairs": pairs,
+                     "pairs_per_s": pairs / min(t)})
+        print(f"sweep {label:36s} {min(t) * 1e3:8.3f} ms  {pairs / min(t):.3e} pairs/s",
+              file=sys.stderr)
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    with open(os.path.join(ROOT, "gpurun_out", "sweep.json"), "w") as fh:
+        json.dump(rows, fh, indent=1)
+
+
+def run_reference(args):
+    """The reference algorithm (oracle port of lanemd's execute_packed, all host
+    threads) on this arm's workload/config/metric; rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import torch
+
+    import paper_2512_03565_b200 as B
+    from oracle import oracle as O
+    cfg = B.Configuration.parse(args.config)
+    device = "cuda" if torch.cuda.is_available() else "cpu"
+    w = make_workload(args, device, 42)
+    params = params_for(cfg, w)
+    threads = O.max_threads()
+    h, prep, trav, n3 = cpu_baseline_lc(w, cfg, params, threads)
+    for _ in range(max(args.warmup, 1)):
+        h.execute(threads)
+    times = []
+    pairs = None
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        _, st = h.execute(threads)
+        times.append(time.perf_counter() - t0)
+        pairs = st.pair_interactions
+    h.close()
+    value = pairs * args.steps / sum(times)
+    sample = (f"{args.steps} force phases (execute only) of {w.name}, {trav} newton3={n3}, "
+              f"oracle/lj_oracle.c with OpenMP over i-cell unit groups (bitwise the "
+              f"sequential reference sweep); prepare {prep:.1f}s untimed")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": sum(times) / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": w.name, "configuration": cfg.label,
+                       "executed": f"lc,{trav},{str(n3).lower()}", "pairs_per_step": pairs},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

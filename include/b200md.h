@@ -1,0 +1,228 @@
+/*
+ * b200md.h -- C ABI of the B200-native Lennard-Jones 12-6 force path.
+ *
+ * The reference (lanemd, pure Python + numba) has no foreign-function boundary;
+ * its hot path crosses from Python into numba-compiled machine code at two
+ * call sites, which these entry points replace:
+ *   - executor.py:146-171  execute_packed -> _batch_sweep -> _sweep_span
+ *   - kernels.py:377-424   compute_pair_vectorized -> _pair_sweep
+ * together with the container/traversal work that feeds them
+ * (containers.py:61-479, domain.py:97-144, traversals.py:108-305).
+ *
+ * Conventions
+ *   - every pointer is caller-owned DEVICE memory (torch.Tensor.data_ptr());
+ *     `stream` is a cudaStream_t passed as void*; all work is stream-ordered
+ *     and asynchronous: results are valid after the caller synchronises.
+ *   - no hidden allocation: scratch is sized by the *_bytes queries and
+ *     passed in by the caller.
+ *   - status codes map onto the reference's exception hierarchy
+ *     (errors.py:4-25); see LMD_ERR_*.  A zero-distance in-cutoff pair is
+ *     detected inside the kernels and reported through lmd_stats.overlap
+ *     (the numba -1 sentinel, executor.py:99-100, 163-164).
+ *   - particle positions inside the library are packed double4
+ *     {x, y, z, ownership} ("pos4"), 32 B per particle, one sector each.
+ */
+#ifndef B200MD_H
+#define B200MD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LMD_OK 0
+#define LMD_ERR_CONFIG 1     /* ConfigurationError      (kernels.py:92-95, traversals.py:110-119) */
+#define LMD_ERR_DEGENERATE 2 /* DegenerateDomainError   (containers.py:78-80) */
+#define LMD_ERR_CUDA 3       /* RuntimeError: a CUDA launch or API call failed */
+#define LMD_ERR_OVERLAP 4    /* ParticleOverlapError    (kernels.py:176-178) */
+
+/* ownership codes (particles.py:17-19) */
+#define LMD_OWNED 0
+#define LMD_HALO 1
+#define LMD_DUMMY 2
+
+/* interaction orders / register-fill patterns (kernels.py:40-64) */
+#define LMD_ONE_BY_V 0
+#define LMD_V_BY_ONE 1
+#define LMD_TWO_BY_HALF 2
+#define LMD_HALF_BY_TWO 3
+
+/* traversals (traversals.py:40-48) + the Verlet-list extension */
+#define LMD_LC_C01 0
+#define LMD_LC_C08 1
+#define LMD_LC_C18 2
+#define LMD_VCL 3
+#define LMD_VL 4
+
+/* kernel flags */
+#define LMD_FLAG_ENERGY 1 /* accumulate potential energy and virial */
+
+/* KernelStats (kernels.py:67-89) + extensions.  Device resident; kernels
+ * accumulate into it, the caller zeroes it (cudaMemsetAsync) beforehand. */
+typedef struct {
+  int64_t kernel_invocations;
+  int64_t lane_slots;
+  int64_t useful_interactions;
+  int64_t pair_interactions;
+  double epot;                /* extension: sum of 4 eps (s^12 - s^6) over pairs */
+  double virial;              /* extension: sum of r . F_ij over pairs */
+  int64_t pairs_owned_halo;   /* subset of pair_interactions with a halo j */
+  int32_t overlap;            /* 1 if an in-cutoff pair sat at r2 == 0 */
+  int32_t overflow;           /* 1 if a capacity-bounded output overflowed */
+} lmd_stats;
+
+/* SimulationBox (domain.py:20-42) */
+typedef struct {
+  double lo[3];
+  double hi[3];
+  int32_t periodic[3];
+  int32_t pad;
+} lmd_box;
+
+/* LJParams (domain.py:45-66) */
+typedef struct {
+  double epsilon, sigma, cutoff, skin;
+} lmd_lj;
+
+/* ring-padded cell grid (containers.py:71-98): dims = floor(L / length),
+ * cell_len = L / dims, tdims = dims + 2. */
+typedef struct {
+  int64_t dims[3];
+  int64_t tdims[3];
+  double cell_len[3];
+  double lo[3];
+  int64_t ncell; /* tdims[0] * tdims[1] * tdims[2] */
+} lmd_grid;
+
+/* ------------------------------------------------------------ library */
+int lmd_version(void);
+const char* lmd_status_string(int status);
+int lmd_device_sm_count(void);
+
+/* ------------------------------------------------------------ geometry */
+/* containers.py:71-98; LMD_ERR_DEGENERATE if any axis has dims < 1. */
+int lmd_grid_init(const lmd_box* box, double length, lmd_grid* out);
+
+/* ----------------------------------------------- K1 cell binning + sort */
+/* containers.py:104-115 (cell_coords + linear_index), bit-exact:
+ * floor((pos - lo) / cell_len) + 1 clipped to [1, dims] (ring = 0) or
+ * [0, dims + 1] (ring = 1), IEEE division.  Positions are SoA. */
+int lmd_cell_index(const lmd_grid* g, int ring, int64_t n, const double* x, const double* y,
+                   const double* z, int32_t* cell, void* stream);
+
+/* Stable radix sort of (cell, index) -> (cell_sorted, perm): the GPU
+ * equivalent of np.argsort(kind="stable") (containers.py:125, 158).
+ * temp_bytes from lmd_sort_temp_bytes(n). */
+size_t lmd_sort_temp_bytes(int64_t n);
+int lmd_sort_by_cell(int64_t n, int64_t ncell, const int32_t* cell, int32_t* cell_sorted,
+                     int32_t* perm, int32_t* scratch_iota, void* temp, size_t temp_bytes,
+                     void* stream);
+
+/* cell_start/cell_count over a sorted key array (np.unique(..., return_index)
+ * at containers.py:128, 164); `base` is added to every start.  Both arrays
+ * are fully overwritten (empty cells get count 0). */
+int lmd_cell_ranges(int64_t n, int64_t ncell, int32_t base, const int32_t* cell_sorted,
+                    int32_t* cell_start, int32_t* cell_count, void* stream);
+
+/* buffer_at semantics (containers.py:178-184): the owned view of a cell if it
+ * holds owned particles, else its halo view.  Writes the merged tables. */
+int lmd_merge_cell_tables(int64_t ncell, const int32_t* o_start, const int32_t* o_count,
+                          const int32_t* h_start, const int32_t* h_count, int32_t* start,
+                          int32_t* count, void* stream);
+
+/* pos4[k] = {x[perm[k]], y[perm[k]], z[perm[k]], own[perm[k]]}; own may be
+ * NULL (then `own_value` is used for every entry). */
+int lmd_gather_pos4(int64_t n, const int32_t* perm, const double* x, const double* y,
+                    const double* z, const int8_t* own, double own_value, double* pos4,
+                    void* stream);
+
+/* ---------------------------------------- K9 periodic images (halo) */
+/* domain.py:97-144: number of images per owned particle within `margin` of
+ * a periodic face (every non-zero shift combination). */
+int lmd_halo_count(const lmd_box* box, double margin, int64_t n, const double* x,
+                   const double* y, const double* z, const int8_t* own, int32_t* count,
+                   void* stream);
+size_t lmd_scan_temp_bytes(int64_t n);
+int lmd_exclusive_scan_i32(int64_t n, const int32_t* in, int32_t* out, void* temp,
+                           size_t temp_bytes, void* stream);
+/* Emit the images: positions pos + (hi - lo) / + (lo - hi) per shifted axis,
+ * exactly as domain.py:118-121; owner index and a shift code (base-3 digits,
+ * 0 none / 1 plus / 2 minus, x least significant) per image. */
+int lmd_halo_emit(const lmd_box* box, double margin, int64_t n, const double* x,
+                  const double* y, const double* z, const int8_t* own, const int32_t* offset,
+                  double* hx, double* hy, double* hz, int32_t* owner, int8_t* shift,
+                  void* stream);
+/* Refresh image positions from their owners between rebuilds (sorted halo
+ * slots, written straight into pos4 at `pos4_halo`). */
+int lmd_halo_refresh_pos4(const lmd_box* box, int64_t nh, const int32_t* owner,
+                          const int8_t* shift, const double* x, const double* y,
+                          const double* z, double* pos4_halo, void* stream);
+
+/* ---------------------------------- K2 linked-cell force (N3 off, full shell) */
+/* One warp per owned cell, the 27-cell shell as j (owned and halo views),
+ * lanes mapped by `pattern` at warp width 32.  Forces are written (not
+ * accumulated) into f{x,y,z}[k] for k in the owned backing (sorted order).
+ * Accumulates pair_interactions (ordered pairs), pairs_owned_halo, overlap,
+ * and with LMD_FLAG_ENERGY epot/virial into *stats (deterministically).
+ * ev_scratch: 2 * lmd_lc_ev_slots(g) doubles. */
+int64_t lmd_lc_ev_slots(const lmd_grid* g);
+int lmd_force_lc(const lmd_grid* g, const lmd_lj* lj, int pattern, int flags,
+                 const double* pos4, const int32_t* cell_start, const int32_t* cell_count,
+                 double* fx, double* fy, double* fz, double* ev_scratch, lmd_stats* stats,
+                 void* stream);
+
+/* Geometric KernelStats of the reference schedules (traversals.py:108-266,
+ * executor.py:38-69, 165-171) for lc_c01 / lc_c08 / lc_c18: kernel
+ * invocations, lane slots and useful interactions for shape (a, b) and
+ * width V, from per-cell owned/halo counts.  Adds into *stats. */
+int lmd_lc_stats(const lmd_grid* g, int traversal, int newton3, int a, int b, int vector_width,
+                 const int32_t* o_count, const int32_t* h_count, lmd_stats* stats,
+                 void* stream);
+
+/* collect_forces (containers.py:186-189): out[perm[k]] = sorted[k]. */
+int lmd_scatter_forces(int64_t n, const int32_t* perm, const double* fx, const double* fy,
+                       const double* fz, double* ox, double* oy, double* oz, void* stream);
+
+
+/* ------------------------------------------------ the functor (two buffers) */
+/* compute_pair_vectorized (kernels.py:377-424) on device buffers given as
+ * pos4 (ownership in .w).  Forces ACCUMULATE (+=) into the SoA force arrays.
+ * same = 1 requires pos4_i == pos4_j (kernels.py:398-399).  newton3 = 1
+ * also subtracts the reaction from the j buffer via a second, transposed
+ * pass (deterministic, no floating-point atomics).  ev_scratch holds
+ * 2 * lmd_pair_sweep_ev_slots(ni, pattern) doubles. */
+int64_t lmd_pair_sweep_ev_slots(int64_t ni, int pattern);
+int lmd_pair_sweep(int64_t ni, const double* pos4_i, int64_t nj, const double* pos4_j,
+                   int same, int newton3, int pattern, int flags, const lmd_lj* lj,
+                   double* fxi, double* fyi, double* fzi, double* fxj, double* fyj, double* fzj,
+                   double* ev_scratch, lmd_stats* stats, void* stream);
+/* {owned, non-dummy, self_pair_slots(newton3=1)} of a pos4 buffer
+ * (particles.py:111-143), as three int64 on the device. */
+int lmd_buffer_counts(int64_t n, const double* pos4, int64_t* out3, void* stream);
+
+/* --------------------------------------- K11 integrator + boundaries */
+/* domain.py:69-94 (apply_boundaries): periodic wrap with numpy's np.mod
+ * semantics, reflective mirror with velocity flip; *diverged |= 1 if a
+ * particle is more than one box length outside (SimulationDivergedError). */
+int lmd_apply_boundaries(const lmd_box* box, int64_t n, double* x, double* y, double* z,
+                         double* vx, double* vy, double* vz, int32_t* diverged, void* stream);
+
+/* integrator.py:21-48: phase 0 = pre-force (drift, stash old force, zero
+ * force), 1 = post-force (kick).  *nonfinite |= 1 on non-finite state. */
+int lmd_verlet_step(int64_t n, int phase, double dt, double mass, double* x, double* y,
+                    double* z, double* vx, double* vy, double* vz, double* fx, double* fy,
+                    double* fz, double* ox, double* oy, double* oz, int32_t* nonfinite,
+                    void* stream);
+
+/* ------------------------------------------------------------- tools */
+/* FP64 pipe peak microbenchmark: blocks x threads threads, each running
+ * iters x 128 independent-chain DFMAs (2 flops each).  Time it with CUDA
+ * events on `stream`; scratch needs `threads` doubles. */
+int lmd_dfma_burn(int blocks, int threads, int iters, double* scratch, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* B200MD_H */

@@ -22,6 +22,9 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 
 #define OWNED 0
 #define HALO 1
@@ -1111,4 +1114,132 @@ int orc_apply_boundaries(int64_t n, const double* lo, const double* hi, const in
     }
   }
   return 0;
+}
+
+/* ------------------------------------------- prepared execution (baseline) */
+/* The reference's metric region covers execute_packed only (driver.py:203-207);
+ * rebuild / halo / schedule / pack happen before it.  orc_lc_prepare does the
+ * latter once; orc_lc_execute times like execute_packed.  With Newton3 off the
+ * units of one i-cell write only that cell, so they are grouped per i-cell and
+ * the groups run in parallel (OpenMP) -- in unit order within a group, which
+ * keeps every particle's summation order, i.e. bitwise the sequential result. */
+typedef struct {
+  lc_t c; pbuf halo; unitvec v; ljk k;
+  int a, b, V, newton3;
+  int64_t n; int64_t* ids;
+  int64_t ngroups; int64_t* gstart; int64_t* gunits;
+  int64_t inv, useful;
+} orc_lc_handle;
+
+static int unit_by_i(const void* x, const void* y) {
+  const unit* const* a = x; const unit* const* b = y;
+  if ((*a)->i_off != (*b)->i_off) return (*a)->i_off < (*b)->i_off ? -1 : 1;
+  return (*a)->seq < (*b)->seq ? -1 : ((*a)->seq > (*b)->seq);
+}
+
+void* orc_lc_prepare(int64_t n, const double* x, const double* y, const double* z,
+                     const int8_t* own, const double* lo, const double* hi, const int32_t* periodic,
+                     double eps, double sigma, double cutoff, double skin,
+                     int trav, int newton3, int a, int b, int V, int* status) {
+  orc_lc_handle* h = calloc(1, sizeof(orc_lc_handle));
+  *status = check_pattern(a, b, V);
+  if (*status) { free(h); return NULL; }
+  obox bx; make_box(&bx, lo, hi, periodic);
+  pbuf in; wrap_input(&in, n, x, y, z, own);
+  h->ids = malloc((n + 1) * 8);
+  for (int64_t k = 0; k < n; ++k) h->ids[k] = k;
+  in.id = h->ids;
+  h->n = n; h->a = a; h->b = b; h->V = V; h->newton3 = newton3;
+  if ((*status = lc_init(&h->c, &bx, cutoff + skin))) { free(h->ids); free(h); return NULL; }
+  if ((*status = build_halo(&in, &bx, cutoff + skin, &h->halo))) { free(h->ids); free(h); return NULL; }
+  if ((*status = lc_build(&h->c, &in, &h->halo))) return h;
+  if ((*status = schedule_lc(&h->c, trav, newton3, &h->v))) return h;
+  h->k = make_ljk(eps, sigma, cutoff);
+  /* geometric stats once (they do not change between executions) */
+  for (int64_t u = 0; u < h->v.n; ++u) {
+    const unit* w = &h->v.u[u];
+    const pbuf* J = w->j_halo ? &h->c.hb : &h->c.ob;
+    h->inv += cdiv(w->i_len, a) * cdiv(w->j_len, b);
+    if (w->same) h->useful += self_pair_slots(&h->c.ob, w->i_off, w->i_len, w->newton3);
+    else {
+      int64_t io, in_, jo, jn;
+      span_counts(&h->c.ob, w->i_off, w->i_len, &io, &in_);
+      span_counts(J, w->j_off, w->j_len, &jo, &jn);
+      h->useful += io * jn;
+    }
+  }
+  if (!newton3) {
+    unit** ptrs = malloc((h->v.n + 1) * sizeof(unit*));
+    for (int64_t u = 0; u < h->v.n; ++u) ptrs[u] = &h->v.u[u];
+    qsort(ptrs, h->v.n, sizeof(unit*), unit_by_i);
+    h->gunits = malloc((h->v.n + 1) * 8);
+    h->gstart = malloc((h->v.n + 2) * 8);
+    int64_t g = 0;
+    for (int64_t u = 0; u < h->v.n; ++u) {
+      h->gunits[u] = ptrs[u] - h->v.u;
+      if (u == 0 || ptrs[u]->i_off != ptrs[u - 1]->i_off) h->gstart[g++] = u;
+    }
+    h->gstart[g] = h->v.n;
+    h->ngroups = g;
+    free(ptrs);
+  }
+  *status = ORC_OK;
+  return h;
+}
+
+int orc_lc_execute(void* hv, int threads, orc_stats* st, double* fx, double* fy, double* fz) {
+  orc_lc_handle* h = hv;
+  memset(st, 0, sizeof(*st));
+  pbuf* ob = &h->c.ob;
+  memset(ob->fx, 0, ob->n * 8); memset(ob->fy, 0, ob->n * 8); memset(ob->fz, 0, ob->n * 8);
+  int64_t total = 0; int bad = 0;
+  if (h->newton3 || threads <= 1) {
+    for (int64_t u = 0; u < h->v.n && !bad; ++u) {
+      const unit* w = &h->v.u[u];
+      const pbuf* J = w->j_halo ? &h->c.hb : ob;
+      int64_t p = sweep_span(ob, J, w->i_off, w->i_len, w->j_off, w->j_len, w->newton3, w->same,
+                             &h->k, NULL, NULL);
+      if (p < 0) bad = 1; else total += p;
+    }
+  } else {
+#ifdef _OPENMP
+#pragma omp parallel for schedule(dynamic, 64) num_threads(threads) reduction(+:total) reduction(|:bad)
+#endif
+    for (int64_t g = 0; g < h->ngroups; ++g) {
+      for (int64_t t = h->gstart[g]; t < h->gstart[g + 1]; ++t) {
+        const unit* w = &h->v.u[h->gunits[t]];
+        const pbuf* J = w->j_halo ? &h->c.hb : ob;
+        int64_t p = sweep_span(ob, J, w->i_off, w->i_len, w->j_off, w->j_len, 0, w->same,
+                               &h->k, NULL, NULL);
+        if (p < 0) bad = 1; else total += p;
+      }
+    }
+  }
+  if (bad) { st->overlap = 1; return ORC_OVERLAP; }
+  st->kernel_invocations = h->inv;
+  st->lane_slots = h->inv * h->V;
+  st->useful_interactions = h->useful;
+  st->pair_interactions = total;
+  if (fx) {
+    for (int64_t q = 0; q < h->n; ++q) {
+      int64_t s = h->c.perm[q];
+      fx[s] = ob->fx[q]; fy[s] = ob->fy[q]; fz[s] = ob->fz[q];
+    }
+  }
+  return ORC_OK;
+}
+
+void orc_lc_free(void* hv) {
+  orc_lc_handle* h = hv;
+  if (!h) return;
+  lc_free(&h->c); pbuf_free(&h->halo); free(h->v.u); free(h->ids);
+  free(h->gstart); free(h->gunits); free(h);
+}
+
+int orc_omp_max_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
 }

@@ -307,3 +307,56 @@ def apply_boundaries(state: dict, lo, hi, periodic) -> bool:
     rc = lib().orc_apply_boundaries(C.c_int64(len(state["x"])), _p(lo), _p(hi), _p(per, C.c_int32),
                                     *[_p(a) for a in arrs])
     return bool(rc)
+
+
+class PreparedLC:
+    """orc_lc_prepare / orc_lc_execute: the reference's execute_packed timed
+    apart from rebuild/halo/schedule (driver.py:203-207).  ``threads > 1``
+    (Newton3 off only) runs per-i-cell unit groups in parallel, bitwise
+    identical to the sequential sweep."""
+
+    def __init__(self, pos, lo, hi, periodic, params, traversal: str, newton3: bool,
+                 pattern: str, vector_width: int, omp: bool = True):
+        x, y, z = _xyz(pos)
+        self._keep = (x, y, z)
+        n = len(x)
+        self.n = n
+        own = np.zeros(n, dtype=np.int8)
+        self._own = own
+        lo, hi, per = _box_args(lo, hi, periodic)
+        a, b = PATTERN_SHAPES[pattern](vector_width)
+        self.L = lib(omp)
+        self.L.orc_lc_prepare.restype = C.c_void_p
+        self.L.orc_lc_execute.argtypes = [C.c_void_p, C.c_int, C.POINTER(_Stats),
+                                          C.c_void_p, C.c_void_p, C.c_void_p]
+        self.L.orc_lc_free.argtypes = [C.c_void_p]
+        status = C.c_int(0)
+        self.h = self.L.orc_lc_prepare(
+            C.c_int64(n), _p(x), _p(y), _p(z), _p(own, C.c_int8), _p(lo), _p(hi),
+            _p(per, C.c_int32), C.c_double(params.epsilon), C.c_double(params.sigma),
+            C.c_double(params.cutoff), C.c_double(params.skin), C.c_int(TRAVERSAL_CODES[traversal]),
+            C.c_int(int(newton3)), C.c_int(a), C.c_int(b), C.c_int(vector_width), C.byref(status))
+        if status.value:
+            self.close()
+            raise OracleError(status.value, "orc_lc_prepare")
+
+    def execute(self, threads: int = 1, want_forces: bool = False):
+        st = _Stats()
+        f = np.zeros((3, self.n)) if want_forces else None
+        ptrs = [f[k].ctypes.data for k in range(3)] if want_forces else [None] * 3
+        rc = self.L.orc_lc_execute(self.h, int(threads), C.byref(st), *ptrs)
+        if rc:
+            raise OracleError(rc, "orc_lc_execute")
+        return (f.T.copy() if want_forces else None), _stats(st)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.orc_lc_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+
+def max_threads() -> int:
+    return int(lib(True).orc_omp_max_threads())

@@ -1,0 +1,141 @@
+// Shared device helpers for the LJ 12-6 force path (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "b200md.h"
+
+#define LMD_CHECK_LAUNCH()                                   \
+  do {                                                       \
+    cudaError_t e_ = cudaGetLastError();                     \
+    if (e_ != cudaSuccess) return lmd::set_cuda_error(e_);   \
+  } while (0)
+
+namespace lmd {
+
+int set_cuda_error(cudaError_t e);
+
+// Kernel constants derived from LJParams exactly as the reference does
+// (executor.py:160-161): eps24 = 24*eps, sigma2 = sigma*sigma, rc2 = cutoff*cutoff.
+struct LJK {
+  double rc2, sigma2, eps24, eps48, eps4;
+};
+
+inline LJK make_ljk(const lmd_lj* p) {
+  LJK k;
+  k.rc2 = p->cutoff * p->cutoff;
+  k.sigma2 = p->sigma * p->sigma;
+  k.eps24 = 24.0 * p->epsilon;
+  k.eps48 = 48.0 * p->epsilon;
+  k.eps4 = 4.0 * p->epsilon;
+  return k;
+}
+
+// r2 exactly as the reference computes it ((dx*dx + dy*dy) + dz*dz, no FMA;
+// executor.py:93-94), so every cutoff decision is bit-identical.
+__device__ __forceinline__ double r2_exact(double dx, double dy, double dz) {
+  return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+}
+
+// 1/x for normal positive x: MUFU.RCP64H seed + one cubic Newton step
+// (3 DFMA), ~1 ulp; the force tolerance is 1e-12 relative.
+__device__ __forceinline__ double rcp_fast(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  e = fma(e, e, e);
+  return fma(y, e, y);
+}
+
+// Force scalar f with F_i += f * d (d = r_i - r_j), for r2 < rc2:
+// f = 24 eps (2 s6^2 - s6) / r2, s6 = (sigma^2 / r2)^3 (kernels.py:112-126).
+__device__ __forceinline__ double lj_scalar(double r2, const LJK& k, double& s6) {
+  double inv = rcp_fast(r2);
+  double s2 = k.sigma2 * inv;
+  s6 = s2 * s2 * s2;
+  return (s6 * inv) * fma(k.eps48, s6, -k.eps24);
+}
+
+// pattern (a, b) at warp width 32, lane -> (i_off, j_off) exactly as
+// kernels.py:250-265 (_lane_templates).
+template <int P>
+struct Pattern;
+template <>
+struct Pattern<LMD_ONE_BY_V> {
+  static constexpr int A = 1, B = 32;
+  __device__ static int ioff(int l) { return 0; }
+  __device__ static int joff(int l) { return l; }
+};
+template <>
+struct Pattern<LMD_V_BY_ONE> {
+  static constexpr int A = 32, B = 1;
+  __device__ static int ioff(int l) { return l; }
+  __device__ static int joff(int l) { return 0; }
+};
+template <>
+struct Pattern<LMD_TWO_BY_HALF> {
+  static constexpr int A = 2, B = 16;
+  __device__ static int ioff(int l) { return l >> 4; }
+  __device__ static int joff(int l) { return l & 15; }
+};
+template <>
+struct Pattern<LMD_HALF_BY_TWO> {
+  static constexpr int A = 16, B = 2;
+  __device__ static int ioff(int l) { return l & 15; }
+  __device__ static int joff(int l) { return l >> 4; }
+};
+
+// Sum over the lanes that share an i (i.e. over the j_off lanes).
+template <int P>
+__device__ __forceinline__ double reduce_j(double v) {
+  if (P == LMD_ONE_BY_V) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  } else if (P == LMD_TWO_BY_HALF) {
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  } else if (P == LMD_HALF_BY_TWO) {
+    v += __shfl_xor_sync(0xffffffffu, v, 16);
+  }
+  return v;
+}
+
+// Sum over the lanes that share a j (i.e. over the i_off lanes): the
+// transposed store of the Newton3 j-side (kernels.py:9-16).
+template <int P>
+__device__ __forceinline__ double reduce_i(double v) {
+  if (P == LMD_V_BY_ONE) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  } else if (P == LMD_TWO_BY_HALF) {
+    v += __shfl_xor_sync(0xffffffffu, v, 16);
+  } else if (P == LMD_HALF_BY_TWO) {
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  }
+  return v;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ long long warp_sum_ll(long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ double4 ld_pos4(const double* pos4, long long k) {
+  const double2* p = reinterpret_cast<const double2*>(pos4) + 2 * k;
+  const double2 a = __ldg(p), b = __ldg(p + 1);
+  return make_double4(a.x, a.y, b.x, b.y);
+}
+
+// Deterministic fixed-order reduction of per-warp (epot, virial) partials.
+int reduce_ev(const double* partials, int64_t nslots, lmd_stats* stats, cudaStream_t s);
+
+inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace lmd

@@ -1,0 +1,66 @@
+"""Force-phase entry points (the drop-in seam, driver.py:107-129).
+
+``force_phase`` keeps the reference's signature and semantics: it builds the
+configured container around the owned particles, derives the periodic
+images, runs one force computation and OVERWRITES ``owned.force_*`` with the
+total forces, returning the KernelStats.  Buffers may live on the host
+(numpy SoA with the reference's field names, e.g. a reference
+``ParticleBuffer``) or on the device (our ``ParticleBuffer`` on CUDA); host
+buffers are copied to HBM and the forces copied back inside the call.
+"""
+
+from __future__ import annotations
+
+from .containers import LinkedCellsContainer, device_soa
+from .domain import as_box
+from .errors import ConfigurationError
+from .kernels import KernelStats, as_pattern, validate_vector_width
+from .tuning import Configuration, ContainerKind
+
+
+def make_container(kind, box, params, cluster_size=None, rebuild_period=None, device=None):
+    kind = ContainerKind(getattr(kind, "value", kind))
+    kw = {} if rebuild_period is None else {"rebuild_period": rebuild_period}
+    if kind is ContainerKind.LINKED_CELLS:
+        return LinkedCellsContainer(box, params, device=device, **kw)
+    if kind is ContainerKind.VERLET_LISTS:
+        from .verlet_lists import VerletListContainer
+        return VerletListContainer(box, params, device=device, **kw)
+    from .clusters import VerletClusterContainer
+    if cluster_size is None:
+        raise ConfigurationError("cluster container needs a cluster size")
+    return VerletClusterContainer(box, params, cluster_size, device=device, **kw)
+
+
+def force_phase(owned, box, params, config: Configuration, vector_width: int,
+                cluster_size: int | None = None, energy: bool = False) -> KernelStats:
+    """One standalone force computation through the device container pipeline."""
+    validate_vector_width(vector_width)
+    if not isinstance(config, Configuration):
+        config = Configuration(config.container, config.traversal, config.newton3,
+                               config.pattern)
+    if not config.is_valid():
+        raise ConfigurationError(f"invalid configuration {config.label!r}")
+    box = as_box(box)
+    dev_owned = device_soa(owned)
+    cont = make_container(config.container, box, params,
+                          cluster_size=cluster_size or vector_width)
+    cont.rebuild(dev_owned)
+    cont.refresh(dev_owned)
+    stats = cont.compute_forces(config.traversal, config.newton3, as_pattern(config.pattern),
+                                vector_width, energy=energy)
+    cont.collect_forces(dev_owned)
+    if dev_owned is not owned:
+        _write_forces_back(owned, dev_owned)
+    return stats
+
+
+def _write_forces_back(host, dev) -> None:
+    import torch
+    for name in ("force_x", "force_y", "force_z"):
+        dst = getattr(host, name)
+        val = getattr(dev, name)
+        if isinstance(dst, torch.Tensor):
+            dst.copy_(val.to(dst.device))
+        else:
+            dst[...] = val.cpu().numpy()
