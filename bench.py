@@ -140,8 +140,9 @@ def fp64_peak_tflops(torch, N) -> float:
 class LCStepper:
     """Holds a built container and launches one force phase per step."""
 
-    def __init__(self, cont, pattern, energy, torch, N):
+    def __init__(self, cont, pattern, energy, torch, N, traversal):
         self.cont = cont
+        self.traversal = traversal
         self.pattern = pattern
         self.energy = energy
         dev = cont._pos4.device
@@ -150,9 +151,34 @@ class LCStepper:
         self.ev_t = torch.empty(2 * slots, dtype=torch.float64, device=dev)
 
     def launch(self):
-        return self.cont.launch_force(self.pattern, self.energy, self.stats_t, self.ev_t)
+        return self.cont.launch_force(self.pattern, self.energy, self.stats_t, self.ev_t,
+                                      self.traversal)
 
     launches_per_step = 1
+
+
+class VLStepper:
+    """Verlet-list force phase on resident lists (built before the timed region)."""
+
+    def __init__(self, cont, pattern, newton3, energy, torch, N):
+        self.cont = cont
+        self.pattern = pattern
+        self.newton3 = newton3
+        self.energy = energy
+        dev = cont._pos4.device
+        self.stats_t = N.new_stats(dev)
+        slots = int(N.load().lmd_vl_ev_slots(cont.n_owned, pattern.code))
+        self.ev_t = torch.empty(2 * max(slots, 1), dtype=torch.float64, device=dev)
+        cont.launch_force(pattern, newton3, energy, self.stats_t, self.ev_t)  # builds the list
+
+    def launch(self):
+        return self.cont.launch_force(self.pattern, self.newton3, self.energy, self.stats_t,
+                                      self.ev_t)
+
+    # N3 zeroes the force arrays first (3 torch fills) before the kernel
+    @property
+    def launches_per_step(self):
+        return 1
 
 
 def build_stepper(cfg, w, args, torch, N):
@@ -163,13 +189,26 @@ def build_stepper(cfg, w, args, torch, N):
     cont = B.make_container(cfg.container, box, params, cluster_size=args.vector_width)
     cont.rebuild(buf)
     cont.refresh(buf)
+    if cfg.container.value == "vl":
+        stepper = VLStepper(cont, cfg.pattern, cfg.newton3, args.energy, torch, N)
+        geo = cont.vl_stats(cfg.newton3, cfg.pattern, args.vector_width)
+        return stepper, cont, buf, box, params, geo
     if cfg.container.value != "lc":
         raise SystemExit(f"bench: container {cfg.container.value} not wired yet")
-    stepper = LCStepper(cont, cfg.pattern, args.energy, torch, N)
+    stepper = LCStepper(cont, cfg.pattern, args.energy, torch, N,
+                        B.traversals.traversal_code(cfg.traversal))
     a, b = cfg.pattern.shape(args.vector_width)
     inv, slots, useful = cont._lc_stats(B.traversals.traversal_code(cfg.traversal), cfg.newton3,
                                         cfg.pattern, args.vector_width)
     return stepper, cont, buf, box, params, (inv, slots, useful)
+
+
+def finish(cfg, st, geo):
+    from paper_2512_03565_b200 import KernelStats
+    from paper_2512_03565_b200.containers import LinkedCellsContainer
+    if cfg.container.value == "lc":
+        return LinkedCellsContainer.finish_stats(st, cfg.newton3, *geo)
+    return KernelStats(geo[0], geo[1], geo[2], int(st.pair_interactions))
 
 
 def time_steps(stepper, steps, flush, torch):
@@ -224,7 +263,7 @@ def run_b200(args):
         stepper.launch()
     torch.cuda.synchronize()
     st = N.read_stats(stepper.stats_t)
-    stats = cont.finish_stats(st, cfg.newton3, *geo)
+    stats = finish(cfg, st, geo)
     pairs = stats.pair_interactions
 
     sampler = ClockSampler(local)
@@ -349,7 +388,8 @@ def sweep(args, w, torch, N, flush):
     import paper_2512_03565_b200 as B
     rows = []
     labels = [c.label for c in B.enumerate_search_space(
-        [B.ContainerKind.LINKED_CELLS], [B.TraversalKind.LC_C01, B.TraversalKind.LC_C18],
+        [B.ContainerKind.LINKED_CELLS, B.ContainerKind.VERLET_LISTS],
+        [B.TraversalKind.LC_C01, B.TraversalKind.LC_C18, B.TraversalKind.VL],
         [False, True], list(B.PATTERN_ORDER))]
     for label in labels:
         cfg = B.Configuration.parse(label)
@@ -358,8 +398,7 @@ def sweep(args, w, torch, N, flush):
             stepper.launch()
         t = time_steps(stepper, 5, flush, torch)
         st = N.read_stats(stepper.stats_t)
-        pairs = st.pair_interactions if not cfg.newton3 else \
-            (st.pair_interactions - st.pairs_owned_halo) // 2 + st.pairs_owned_halo
+        pairs = finish(cfg, st, (0, 0, 0)).pair_interactions
         rows.append({"config": label, "ms": min(t) * 1e3, "pairs": pairs,
                      "pairs_per_s": pairs / min(t)})
         print(f"sweep {label:36s} {min(t) * 1e3:8.3f} ms  {pairs / min(t):.3e} pairs/s",

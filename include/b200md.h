@@ -127,10 +127,13 @@ int lmd_cell_ranges(int64_t n, int64_t ncell, int32_t base, const int32_t* cell_
                     int32_t* cell_start, int32_t* cell_count, void* stream);
 
 /* buffer_at semantics (containers.py:178-184): the owned view of a cell if it
- * holds owned particles, else its halo view.  Writes the merged tables. */
+ * holds owned particles, else its halo view.  Writes the merged tables and
+ * (if dup != NULL) dup[c] = 1 for cells holding both owned particles and
+ * images: the reference's _occupied_pairs (traversals.py:133) then lists the
+ * cell twice as an anchor, which lc_c08 / lc_c18 turn into duplicated units. */
 int lmd_merge_cell_tables(int64_t ncell, const int32_t* o_start, const int32_t* o_count,
                           const int32_t* h_start, const int32_t* h_count, int32_t* start,
-                          int32_t* count, void* stream);
+                          int32_t* count, uint8_t* dup, void* stream);
 
 /* pos4[k] = {x[perm[k]], y[perm[k]], z[perm[k]], own[perm[k]]}; own may be
  * NULL (then `own_value` is used for every entry). */
@@ -160,18 +163,29 @@ int lmd_halo_refresh_pos4(const lmd_box* box, int64_t nh, const int32_t* owner,
                           const int8_t* shift, const double* x, const double* y,
                           const double* z, double* pos4_halo, void* stream);
 
+/* The same into SoA arrays (Verlet-list gathers read x, y, z separately). */
+int lmd_halo_refresh_soa(const lmd_box* box, int64_t nh, const int32_t* owner,
+                         const int8_t* shift, const double* x, const double* y, const double* z,
+                         double* ox, double* oy, double* oz, void* stream);
+/* ox[k] = x[perm[k]] (perm may be NULL = identity), likewise y, z. */
+int lmd_gather_soa(int64_t n, const int32_t* perm, const double* x, const double* y,
+                   const double* z, double* ox, double* oy, double* oz, void* stream);
+
 /* ---------------------------------- K2 linked-cell force (N3 off, full shell) */
 /* One warp per owned cell, the 27-cell shell as j (owned and halo views),
  * lanes mapped by `pattern` at warp width 32.  Forces are written (not
  * accumulated) into f{x,y,z}[k] for k in the owned backing (sorted order).
  * Accumulates pair_interactions (ordered pairs), pairs_owned_halo, overlap,
  * and with LMD_FLAG_ENERGY epot/virial into *stats (deterministically).
+ * dup (may be NULL = lc_c01 semantics): per-cell flags from
+ * lmd_merge_cell_tables; a cell pair (C, D != C) then counts 1 + dup[min(C, D)]
+ * times, reproducing the reference's lc_c08 / lc_c18 unit multiplicity.
  * ev_scratch: 2 * lmd_lc_ev_slots(g) doubles. */
 int64_t lmd_lc_ev_slots(const lmd_grid* g);
 int lmd_force_lc(const lmd_grid* g, const lmd_lj* lj, int pattern, int flags,
                  const double* pos4, const int32_t* cell_start, const int32_t* cell_count,
-                 double* fx, double* fy, double* fz, double* ev_scratch, lmd_stats* stats,
-                 void* stream);
+                 const uint8_t* dup, double* fx, double* fy, double* fz, double* ev_scratch,
+                 lmd_stats* stats, void* stream);
 
 /* Geometric KernelStats of the reference schedules (traversals.py:108-266,
  * executor.py:38-69, 165-171) for lc_c01 / lc_c08 / lc_c18: kernel
@@ -185,6 +199,43 @@ int lmd_lc_stats(const lmd_grid* g, int traversal, int newton3, int a, int b, in
 int lmd_scatter_forces(int64_t n, const int32_t* perm, const double* fx, const double* fy,
                        const double* fz, double* ox, double* oy, double* oz, void* stream);
 
+
+/* --------------------------------------------- K3/K4 Verlet lists (extension) */
+/* Build on the rc+skin cell grid over a combined backing pos4 = [owned sorted
+ * by cell | images sorted by cell], with SEPARATE owned and image cell tables
+ * (o_*, h_*; image starts include the n_owned base).  Candidates: owned
+ * particles and images of the 27 cells; listed iff r2 < rl2 with the
+ * reference's exact r2.  newton3 = 1 builds half lists (owned j > i).
+ * 1) lmd_vl_count -> count[i];  2) lmd_vl_layout -> per-tile kmax / offsets
+ * for `pattern` (tiles of A = distinct i per fill; kmax padded to B);
+ * 3) lmd_vl_fill -> nbr (interleaved, padded with `sentinel`, the index of a
+ * far-away dummy position).  Total entries = tile_off[last] + tile_len[last]. */
+int lmd_vl_count(const lmd_grid* g, double rl2, int newton3, int64_t n_owned, const double* pos4,
+                 const int32_t* o_start, const int32_t* o_count, const int32_t* h_start,
+                 const int32_t* h_count, int32_t* count, void* stream);
+int64_t lmd_vl_num_tiles(int64_t n_owned, int pattern);
+size_t lmd_vl_scan_temp_bytes(int64_t ntiles);
+int lmd_vl_layout(int64_t n_owned, int pattern, const int32_t* count, int64_t* tile_len,
+                  int64_t* tile_off, int32_t* kmax, void* temp, size_t temp_bytes,
+                  void* stream);
+int lmd_vl_fill(const lmd_grid* g, double rl2, int newton3, int pattern, int64_t n_owned,
+                int32_t sentinel, const double* pos4, const int32_t* o_start,
+                const int32_t* o_count, const int32_t* h_start, const int32_t* h_count,
+                const int64_t* tile_off, const int32_t* kmax, int32_t* nbr, void* stream);
+/* Force over the lists: one warp per i-tile, lanes by `pattern`; positions
+ * are SoA x, y, z over the combined backing (+ sentinel).  newton3 = 0
+ * writes f[i]; newton3 = 1 accumulates with FP64 atomics into zeroed f
+ * (j-side reactions; summation order is then not deterministic).
+ * ev_scratch: 2 * lmd_vl_ev_slots(n_owned, pattern) doubles. */
+int64_t lmd_vl_ev_slots(int64_t n_owned, int pattern);
+int lmd_force_vl(int pattern, int newton3, int flags, const lmd_lj* lj, int64_t n_owned,
+                 const double* x, const double* y, const double* z, const int64_t* tile_off,
+                 const int32_t* kmax, const int32_t* nbr, double* fx, double* fy, double* fz,
+                 double* ev_scratch, lmd_stats* stats, void* stream);
+/* KernelStats of a Verlet-list force phase: i-tiles of `a` consecutive owned
+ * particles, each tile's j-stream its longest list chunked by b. */
+int lmd_vl_stats(int64_t n_owned, int a, int b, int vector_width, const int32_t* count,
+                 lmd_stats* stats, void* stream);
 
 /* ------------------------------------------------ the functor (two buffers) */
 /* compute_pair_vectorized (kernels.py:377-424) on device buffers given as

@@ -911,9 +911,13 @@ int orc_vcl_structure(int64_t n, const double* x, const double* y, const double*
  * come from the linked-cells grid built with interaction_length = rc + skin
  * (containers.py:71-139); a pair (i, j) is listed iff r2 < (rc+skin)^2 with r2
  * evaluated exactly as executor.py:93-94.  Lists are per owned particle in the
- * cell-sorted order; candidate order = 27 directions (itertools.product order)
- * then cell order.  Half lists (newton3): owned j only if j's sorted index > i;
- * halo j always (the owned side is i, traversals.py:157-160). */
+ * cell-sorted order; candidates are the owned particles of the 27 cells
+ * (itertools.product order, cell order) followed by the images binned to
+ * those cells.  Unlike buffer_at (containers.py:178-184) no image is shadowed
+ * by owned particles of the same cell, so images of particles that sit
+ * outside [lo, hi) still interact (the physically exact pair set).  Half
+ * lists (newton3): owned j only if j's sorted index > i; images always (the
+ * owned side is i, traversals.py:157-160). */
 static int vl_build(const lc_t* c, double rl2, int newton3, int64_t** off_o, int64_t** nbr_o, int8_t** halo_o) {
   init_dirs();
   int64_t n = c->ob.n;
@@ -926,22 +930,24 @@ static int vl_build(const lc_t* c, double rl2, int newton3, int64_t** off_o, int
     if (c->ob.own[p] != OWNED) continue;
     int64_t cell = lc_cell_of(c, c->ob.x[p], c->ob.y[p], c->ob.z[p], 0);
     int64_t x, y, z; coords_of(c, cell, &x, &y, &z);
-    for (int d = 0; d < 27; ++d) {
-      int64_t nlin = (x + ALL[d][0]) + c->tdims[0] * ((y + ALL[d][1]) + c->tdims[1] * (z + ALL[d][2]));
-      int ih; int64_t o, l;
-      lc_buffer_at(c, nlin, &ih, &o, &l);
-      const pbuf* J = ih ? &c->hb : &c->ob;
-      for (int64_t q = o; q < o + l; ++q) {
-        if (!ih && q == p) continue;
-        if (J->own[q] == DUMMY) continue;
-        if (newton3 && !ih && q < p) continue;
-        double dx = c->ob.x[p] - J->x[q];
-        double dy = c->ob.y[p] - J->y[q];
-        double dz = c->ob.z[p] - J->z[q];
-        double r2 = dx * dx + dy * dy + dz * dz;
-        if (!(r2 < rl2)) continue;
-        if (cnt == cap) { cap *= 2; nbr = realloc(nbr, cap * 8); hal = realloc(hal, cap); }
-        nbr[cnt] = q; hal[cnt] = (int8_t)ih; ++cnt;
+    for (int ih = 0; ih < 2; ++ih) {
+      for (int d = 0; d < 27; ++d) {
+        int64_t nlin = (x + ALL[d][0]) + c->tdims[0] * ((y + ALL[d][1]) + c->tdims[1] * (z + ALL[d][2]));
+        int64_t o = ih ? c->h_start[nlin] : c->o_start[nlin];
+        int64_t l = ih ? c->h_count[nlin] : c->o_count[nlin];
+        const pbuf* J = ih ? &c->hb : &c->ob;
+        for (int64_t q = o; q < o + l; ++q) {
+          if (!ih && q == p) continue;
+          if (J->own[q] == DUMMY) continue;
+          if (newton3 && !ih && q < p) continue;
+          double dx = c->ob.x[p] - J->x[q];
+          double dy = c->ob.y[p] - J->y[q];
+          double dz = c->ob.z[p] - J->z[q];
+          double r2 = dx * dx + dy * dy + dz * dz;
+          if (!(r2 < rl2)) continue;
+          if (cnt == cap) { cap *= 2; nbr = realloc(nbr, cap * 8); hal = realloc(hal, cap); }
+          nbr[cnt] = q; hal[cnt] = (int8_t)ih; ++cnt;
+        }
       }
     }
   }

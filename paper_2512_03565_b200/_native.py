@@ -116,7 +116,7 @@ _sig("lmd_cell_index", _INT, C.POINTER(Grid), _INT, _I64, _VP, _VP, _VP, _VP, _V
 _sig("lmd_sort_temp_bytes", _SZ, _I64)
 _sig("lmd_sort_by_cell", _INT, _I64, _I64, _VP, _VP, _VP, _VP, _VP, _SZ, _VP)
 _sig("lmd_cell_ranges", _INT, _I64, _I64, _I32, _VP, _VP, _VP, _VP)
-_sig("lmd_merge_cell_tables", _INT, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP)
+_sig("lmd_merge_cell_tables", _INT, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP)
 _sig("lmd_gather_pos4", _INT, _I64, _VP, _VP, _VP, _VP, _VP, _D, _VP, _VP)
 _sig("lmd_halo_count", _INT, C.POINTER(Box), _D, _I64, _VP, _VP, _VP, _VP, _VP, _VP)
 _sig("lmd_scan_temp_bytes", _SZ, _I64)
@@ -126,7 +126,7 @@ _sig("lmd_halo_emit", _INT, C.POINTER(Box), _D, _I64, _VP, _VP, _VP, _VP, _VP,
 _sig("lmd_halo_refresh_pos4", _INT, C.POINTER(Box), _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP)
 _sig("lmd_lc_ev_slots", _I64, C.POINTER(Grid))
 _sig("lmd_force_lc", _INT, C.POINTER(Grid), C.POINTER(LJ), _INT, _INT, _VP, _VP, _VP,
-     _VP, _VP, _VP, _VP, _VP, _VP)
+     _VP, _VP, _VP, _VP, _VP, _VP, _VP)
 _sig("lmd_lc_stats", _INT, C.POINTER(Grid), _INT, _INT, _INT, _INT, _INT, _VP, _VP, _VP, _VP)
 _sig("lmd_apply_boundaries", _INT, C.POINTER(Box), _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP)
 _sig("lmd_verlet_step", _INT, _I64, _INT, _D, _D, *([_VP] * 13), _VP)
@@ -135,6 +135,19 @@ _sig("lmd_pair_sweep", _INT, _I64, _VP, _I64, _VP, _INT, _INT, _INT, _INT, C.POI
      *([_VP] * 6), _VP, _VP, _VP)
 _sig("lmd_buffer_counts", _INT, _I64, _VP, _VP, _VP)
 _sig("lmd_dfma_burn", _INT, _INT, _INT, _INT, _VP, _VP)
+_sig("lmd_halo_refresh_soa", _INT, C.POINTER(Box), _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP,
+     _VP, _VP)
+_sig("lmd_gather_soa", _INT, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP)
+_sig("lmd_vl_count", _INT, C.POINTER(Grid), _D, _INT, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP)
+_sig("lmd_vl_num_tiles", _I64, _I64, _INT)
+_sig("lmd_vl_scan_temp_bytes", _SZ, _I64)
+_sig("lmd_vl_layout", _INT, _I64, _INT, _VP, _VP, _VP, _VP, _VP, _SZ, _VP)
+_sig("lmd_vl_fill", _INT, C.POINTER(Grid), _D, _INT, _INT, _I64, _I32, _VP, _VP, _VP, _VP, _VP,
+     _VP, _VP, _VP, _VP)
+_sig("lmd_vl_ev_slots", _I64, _I64, _INT)
+_sig("lmd_force_vl", _INT, _INT, _INT, _INT, C.POINTER(LJ), _I64, _VP, _VP, _VP, _VP, _VP, _VP,
+     _VP, _VP, _VP, _VP, _VP, _VP)
+_sig("lmd_vl_stats", _INT, _I64, _INT, _INT, _INT, _VP, _VP, _VP)
 _sig("lmd_scatter_forces", _INT, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP)
 
 

@@ -196,6 +196,7 @@ class LinkedCellsContainer:
         self._h_count = torch.zeros(nc, dtype=torch.int32, device=dev)
         self._start = torch.empty(nc, dtype=torch.int32, device=dev)
         self._count = torch.empty(nc, dtype=torch.int32, device=dev)
+        self._dup = torch.zeros(nc, dtype=torch.uint8, device=dev)
 
     def rebuild(self, owned) -> None:
         d = device_soa(owned)
@@ -260,7 +261,7 @@ class LinkedCellsContainer:
             self._halo_ids = torch.zeros(0, dtype=torch.int64, device=dev)
         N.call("lmd_merge_cell_tables", self._n_total, N.ptr(self._o_start), N.ptr(self._o_count),
                N.ptr(self._h_start), N.ptr(self._h_count), N.ptr(self._start), N.ptr(self._count),
-               s)
+               N.ptr(self._dup), s)
         self._tables_ready = True
 
     def refresh_positions(self, owned) -> None:
@@ -358,9 +359,12 @@ class LinkedCellsContainer:
         self._stats_cache[key] = hit
         return hit
 
-    def launch_force(self, pattern, energy: bool = False, stats_t=None, ev_t=None):
+    def launch_force(self, pattern, energy: bool = False, stats_t=None, ev_t=None,
+                     traversal=N.LC_C01):
         """Launch K2 on the current stream without synchronising; returns the
-        device stats tensor (pair counts, overlap flag, energy)."""
+        device stats tensor (pair counts, overlap flag, energy).  lc_c08 /
+        lc_c18 weight cells that hold both owned particles and images the way
+        the reference's duplicated anchor units do (traversals.py:133)."""
         if not self._tables_ready:
             raise ConfigurationError("container has not been refreshed")
         pattern = as_pattern(pattern)
@@ -374,7 +378,8 @@ class LinkedCellsContainer:
             ev_t = torch.empty(2 * slots, dtype=torch.float64, device=dev)
         N.call("lmd_force_lc", self.grid, N.make_lj(self.params), pattern.code,
                N.FLAG_ENERGY if energy else 0, N.ptr(self._pos4), N.ptr(self._start),
-               N.ptr(self._count), N.ptr(self._fx), N.ptr(self._fy), N.ptr(self._fz), N.ptr(ev_t),
+               N.ptr(self._count), None if traversal == N.LC_C01 else N.ptr(self._dup),
+               N.ptr(self._fx), N.ptr(self._fy), N.ptr(self._fz), N.ptr(ev_t),
                N.ptr(stats_t), N.stream())
         return stats_t
 
@@ -391,7 +396,7 @@ class LinkedCellsContainer:
         if code == N.LC_C01 and newton3:
             raise ConfigurationError("lc_c01 cannot exploit Newton's third law")
         inv, slots, useful = self._lc_stats(code, newton3, pattern, vector_width)
-        st = N.read_stats(self.launch_force(pattern, energy))
+        st = N.read_stats(self.launch_force(pattern, energy, traversal=code))
         return self.finish_stats(st, newton3, inv, slots, useful)
 
     @staticmethod

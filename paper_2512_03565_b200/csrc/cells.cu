@@ -80,9 +80,12 @@ __global__ void merge_tables_kernel(int64_t ncell, const int32_t* __restrict__ o
                                     const int32_t* __restrict__ oc,
                                     const int32_t* __restrict__ hs,
                                     const int32_t* __restrict__ hc, int32_t* __restrict__ s,
-                                    int32_t* __restrict__ c) {
+                                    int32_t* __restrict__ c, uint8_t* __restrict__ dup) {
   int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (q >= ncell) return;
+  // a cell holding owned particles AND images (images of particles that sit
+  // outside [lo, hi) mid-step): the reference lists it twice as an anchor
+  if (dup) dup[q] = (oc[q] > 0 && hc[q] > 0) ? 1 : 0;
   if (oc[q] > 0) {
     s[q] = os[q];
     c[q] = oc[q];
@@ -205,6 +208,30 @@ __global__ void halo_refresh_kernel(BoxK b, int64_t nh, const int32_t* __restric
     q[ax] = __dadd_rn(p[ax], sh);
   }
   pos4[k] = make_double4(q[0], q[1], q[2], (double)LMD_HALO);
+}
+
+__global__ void halo_refresh_soa_kernel(BoxK b, int64_t nh, const int32_t* __restrict__ owner,
+                                        const int8_t* __restrict__ shift,
+                                        const double* __restrict__ x, const double* __restrict__ y,
+                                        const double* __restrict__ z, double* __restrict__ ox,
+                                        double* __restrict__ oy, double* __restrict__ oz) {
+  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= nh) return;
+  int32_t o = owner[k];
+  int s = shift[k];
+  const double p[3] = {x[o], y[o], z[o]};
+  double q[3];
+#pragma unroll
+  for (int ax = 0; ax < 3; ++ax) {
+    int d = s % 3;
+    s /= 3;
+    double sh = d == 1 ? __dadd_rn(b.hi[ax], -b.lo[ax])
+                       : (d == 2 ? __dadd_rn(b.lo[ax], -b.hi[ax]) : 0.0);
+    q[ax] = __dadd_rn(p[ax], sh);
+  }
+  ox[k] = q[0];
+  oy[k] = q[1];
+  oz[k] = q[2];
 }
 
 // ------------------------------------------------ deterministic reductions
@@ -352,9 +379,9 @@ int lmd_cell_ranges(int64_t n, int64_t ncell, int32_t base, const int32_t* cell_
 
 int lmd_merge_cell_tables(int64_t ncell, const int32_t* o_start, const int32_t* o_count,
                           const int32_t* h_start, const int32_t* h_count, int32_t* start,
-                          int32_t* count, void* stream) {
+                          int32_t* count, uint8_t* dup, void* stream) {
   merge_tables_kernel<<<grid1d(ncell, 256), 256, 0, (cudaStream_t)stream>>>(
-      ncell, o_start, o_count, h_start, h_count, start, count);
+      ncell, o_start, o_count, h_start, h_count, start, count, dup);
   LMD_CHECK_LAUNCH();
   return LMD_OK;
 }
@@ -413,6 +440,16 @@ int lmd_halo_refresh_pos4(const lmd_box* box, int64_t nh, const int32_t* owner,
   if (nh <= 0) return LMD_OK;
   halo_refresh_kernel<<<grid1d(nh, 256), 256, 0, (cudaStream_t)stream>>>(
       make_boxk(box), nh, owner, shift, x, y, z, reinterpret_cast<double4*>(pos4_halo));
+  LMD_CHECK_LAUNCH();
+  return LMD_OK;
+}
+
+int lmd_halo_refresh_soa(const lmd_box* box, int64_t nh, const int32_t* owner,
+                         const int8_t* shift, const double* x, const double* y, const double* z,
+                         double* ox, double* oy, double* oz, void* stream) {
+  if (nh <= 0) return LMD_OK;
+  halo_refresh_soa_kernel<<<grid1d(nh, 256), 256, 0, (cudaStream_t)stream>>>(
+      make_boxk(box), nh, owner, shift, x, y, z, ox, oy, oz);
   LMD_CHECK_LAUNCH();
   return LMD_OK;
 }

@@ -22,7 +22,8 @@ template <int P, bool EV>
 __global__ void __launch_bounds__(32 * kWarpsPerBlock)
     lc_force_kernel(long long d0, long long d1, long long d2, long long t0, long long t1,
                     LJK k, const double* __restrict__ pos4, const int32_t* __restrict__ cstart,
-                    const int32_t* __restrict__ ccount, double* __restrict__ fx,
+                    const int32_t* __restrict__ ccount, const uint8_t* __restrict__ dup,
+                    double* __restrict__ fx,
                     double* __restrict__ fy, double* __restrict__ fz, double* __restrict__ ev,
                     lmd_stats* __restrict__ stats) {
   using Pat = Pattern<P>;
@@ -40,12 +41,14 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
     const int ns = ccount[lin];
     const int ss = cstart[lin];
     // lane d < 27 holds neighbour cell d (itertools.product order, traversals.py:84)
-    int nb_s = 0, nb_n = 0;
+    int nb_s = 0, nb_n = 0, nb_m = 1;
     if (lane < 27) {
       const int dx = lane / 9 - 1, dy = (lane / 3) % 3 - 1, dz = lane % 3 - 1;
       const long long nl = (cx + dx) + t0 * ((cy + dy) + t1 * (cz + dz));
       nb_s = cstart[nl];
       nb_n = ccount[nl];
+      // reference unit multiplicity of the cell pair (lc_c08 / lc_c18 only)
+      if (dup && nl != lin) nb_m = 1 + dup[nl < lin ? nl : lin];
     }
     const int io = Pat::ioff(lane), jo = Pat::joff(lane);
     for (int ci = 0; ci < ns; ci += Pat::A) {
@@ -57,6 +60,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
       for (int d = 0; d < 27; ++d) {
         const int js = __shfl_sync(0xffffffffu, nb_s, d);
         const int jn = __shfl_sync(0xffffffffu, nb_n, d);
+        const int mult = __shfl_sync(0xffffffffu, nb_m, d);
         for (int cj = 0; cj < jn; cj += Pat::B) {
           const int jl = cj + jo;
           const int j = js + jl;
@@ -71,14 +75,14 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
             continue;
           }
           double s6;
-          const double f = lj_scalar(r2, k, s6);
+          const double f = lj_scalar(r2, k, s6) * (double)mult;
           ax = fma(f, dx, ax);
           ay = fma(f, dy, ay);
           az = fma(f, dz, az);
-          ++pairs;
-          pairs_halo += pj.w != (double)LMD_OWNED;
+          pairs += mult;
+          if (pj.w != (double)LMD_OWNED) pairs_halo += mult;
           if (EV) {
-            e_acc = fma(0.5 * s6, fma(k.eps4, s6, -k.eps4), e_acc);
+            e_acc = fma((0.5 * mult) * s6, fma(k.eps4, s6, -k.eps4), e_acc);
             v_acc = fma(0.5 * f, r2, v_acc);
           }
         }
@@ -143,6 +147,9 @@ __device__ __forceinline__ void c08_ranks(int dx, int dy, int dz, int& r1, int& 
 __global__ void lc_stats_kernel(long long t0, long long t1, long long t2, int trav, int newton3,
                                 int a, int b, const int32_t* __restrict__ oc,
                                 const int32_t* __restrict__ hc, lmd_stats* __restrict__ stats) {
+  // A cell holding owned particles and images appears twice in the
+  // reference's anchor list (traversals.py:133), so its forward pairs are
+  // emitted twice; pair_mult carries that multiplicity.
   const long long ncell = t0 * t1 * t2;
   const long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   long long inv = 0, useful = 0;
@@ -163,6 +170,7 @@ __global__ void lc_stats_kernel(long long t0, long long t1, long long t2, int tr
         }
       }
     } else if (A.state != 0) {
+      const long long pair_mult = (oc[q] > 0 && hc[q] > 0) ? 2 : 1;
       // traversals.py:190-241: self unit per owned cell, then each unordered
       // occupied adjacent pair once from its lower-linear-index anchor
       if (A.state == 1) {
@@ -183,8 +191,8 @@ __global__ void lc_stats_kernel(long long t0, long long t1, long long t2, int tr
               // _emit_pair halo rule: the owned side is i, never N3
               const CellView& I = A.state == 2 ? B : A;
               const CellView& J = A.state == 2 ? A : B;
-              inv += cdivd(I.n, a) * cdivd(J.n, b);
-              useful += (long long)I.owned * J.n;
+              inv += pair_mult * cdivd(I.n, a) * cdivd(J.n, b);
+              useful += pair_mult * I.owned * J.n;
             } else if (newton3) {
               bool swap = false;
               if (trav == LMD_LC_C08) {
@@ -194,11 +202,11 @@ __global__ void lc_stats_kernel(long long t0, long long t1, long long t2, int tr
               }
               const CellView& I = swap ? B : A;
               const CellView& J = swap ? A : B;
-              inv += cdivd(I.n, a) * cdivd(J.n, b);
-              useful += (long long)I.owned * J.n;
+              inv += pair_mult * cdivd(I.n, a) * cdivd(J.n, b);
+              useful += pair_mult * I.owned * J.n;
             } else {
-              inv += cdivd(A.n, a) * cdivd(B.n, b) + cdivd(B.n, a) * cdivd(A.n, b);
-              useful += (long long)A.owned * B.n + (long long)B.owned * A.n;
+              inv += pair_mult * (cdivd(A.n, a) * cdivd(B.n, b) + cdivd(B.n, a) * cdivd(A.n, b));
+              useful += pair_mult * ((long long)A.owned * B.n + (long long)B.owned * A.n);
             }
           }
     }
@@ -228,8 +236,8 @@ int64_t lmd_lc_ev_slots(const lmd_grid* g) {
 
 int lmd_force_lc(const lmd_grid* g, const lmd_lj* lj, int pattern, int flags,
                  const double* pos4, const int32_t* cell_start, const int32_t* cell_count,
-                 double* fx, double* fy, double* fz, double* ev_scratch, lmd_stats* stats,
-                 void* stream) {
+                 const uint8_t* dup, double* fx, double* fy, double* fz, double* ev_scratch,
+                 lmd_stats* stats, void* stream) {
   const LJK k = make_ljk(lj);
   const int64_t nowned = g->dims[0] * g->dims[1] * g->dims[2];
   const unsigned blocks = (unsigned)cdiv(nowned, kWarpsPerBlock);
@@ -240,11 +248,11 @@ int lmd_force_lc(const lmd_grid* g, const lmd_lj* lj, int pattern, int flags,
     if (ev)                                                                                  \
       lc_force_kernel<P, true><<<blocks, 32 * kWarpsPerBlock, 0, s>>>(                       \
           g->dims[0], g->dims[1], g->dims[2], g->tdims[0], g->tdims[1], k, pos4, cell_start, \
-          cell_count, fx, fy, fz, ev_scratch, stats);                                        \
+          cell_count, dup, fx, fy, fz, ev_scratch, stats);                                   \
     else                                                                                     \
       lc_force_kernel<P, false><<<blocks, 32 * kWarpsPerBlock, 0, s>>>(                      \
           g->dims[0], g->dims[1], g->dims[2], g->tdims[0], g->tdims[1], k, pos4, cell_start, \
-          cell_count, fx, fy, fz, ev_scratch, stats);                                        \
+          cell_count, dup, fx, fy, fz, ev_scratch, stats);                                   \
   } while (0)
   switch (pattern) {
     case LMD_ONE_BY_V: LMD_LAUNCH_LC(LMD_ONE_BY_V); break;

@@ -1,0 +1,425 @@
+// K3/K4: Verlet lists with a skin -- build and force (sm_100a).
+//
+// Extension: the reference excludes plain Verlet lists; the
+// north star adds them.  Semantics (mirrored by oracle/lj_oracle.c:vl_build):
+// candidates are the owned particles and the images of the 27 cells of the
+// rc+skin grid (no buffer_at shadowing), listed iff r2 < (rc+skin)^2 with the
+// reference's exact r2.  Half lists (Newton3): owned j > i only, images always.
+//
+// List layout = the interaction order: owned particles (cell-sorted) form
+// i-tiles of A consecutive particles (A = distinct i per warp fill); tile t
+// stores its entries interleaved, entry (k, il) at tile_off[t] + k*A + il,
+// padded to kmax[t] (a multiple of B) with a sentinel particle far away.  A
+// warp fill (A i's x B consecutive k's) therefore reads 32 consecutive ints.
+// Lists are ascending in j, so lanes of a tile gather nearby particles.
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+
+namespace lmd {
+
+constexpr int kVLWarps = 4;
+
+template <int P>
+struct Tile {
+  static constexpr int A = Pattern<P>::A, B = Pattern<P>::B;
+};
+
+// visits every candidate j (index into the combined backing) of owned i
+template <typename F>
+__device__ __forceinline__ void for_candidates(int i, const double4& pi, int newton3, long long t0,
+                                               long long t1, long long lin,
+                                               const int32_t* __restrict__ os,
+                                               const int32_t* __restrict__ oc,
+                                               const int32_t* __restrict__ hs,
+                                               const int32_t* __restrict__ hc,
+                                               const double* __restrict__ pos4, double rl2,
+                                               F&& visit) {
+  for (int view = 0; view < 2; ++view) {
+    const int32_t* vs = view ? hs : os;
+    const int32_t* vc = view ? hc : oc;
+    for (int dz = -1; dz <= 1; ++dz)
+      for (int dy = -1; dy <= 1; ++dy)
+        for (int dx = -1; dx <= 1; ++dx) {
+          const long long nl = lin + dx + t0 * (dy + t1 * dz);
+          const int s = vs[nl], c = vc[nl];
+          for (int j = s; j < s + c; ++j) {
+            if (!view && (j == i || (newton3 && j < i))) continue;
+            const double4 pj = ld_pos4(pos4, j);
+            if (pj.w == (double)LMD_DUMMY) continue;
+            const double r2 = r2_exact(pi.x - pj.x, pi.y - pj.y, pi.z - pj.z);
+            if (r2 < rl2) visit(j);
+          }
+        }
+  }
+}
+
+__device__ __forceinline__ long long cell_of_owned(const double4& p, double lo0, double lo1,
+                                                   double lo2, double cl0, double cl1, double cl2,
+                                                   long long d0, long long d1, long long d2,
+                                                   long long t0, long long t1) {
+  const double pp[3] = {p.x, p.y, p.z};
+  const double lo[3] = {lo0, lo1, lo2}, cl[3] = {cl0, cl1, cl2};
+  const long long d[3] = {d0, d1, d2};
+  long long q[3];
+#pragma unroll
+  for (int ax = 0; ax < 3; ++ax) {
+    double s = floor(__ddiv_rn(__dadd_rn(pp[ax], -lo[ax]), cl[ax]));
+    long long v = !(s >= -4.0) ? -3 : (s > 1.0e15 ? 1000000000000000LL : (long long)s + 1);
+    q[ax] = v < 1 ? 1 : (v > d[ax] ? d[ax] : v);
+  }
+  return q[0] + t0 * (q[1] + t1 * q[2]);
+}
+
+struct GridK {
+  double lo0, lo1, lo2, cl0, cl1, cl2;
+  long long d0, d1, d2, t0, t1;
+};
+
+__global__ void vl_count_kernel(GridK g, int n, int newton3, double rl2,
+                                const double* __restrict__ pos4, const int32_t* __restrict__ os,
+                                const int32_t* __restrict__ oc, const int32_t* __restrict__ hs,
+                                const int32_t* __restrict__ hc, int32_t* __restrict__ count) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double4 pi = ld_pos4(pos4, i);
+  int c = 0;
+  if (pi.w == (double)LMD_OWNED) {
+    const long long lin = cell_of_owned(pi, g.lo0, g.lo1, g.lo2, g.cl0, g.cl1, g.cl2, g.d0, g.d1,
+                                        g.d2, g.t0, g.t1);
+    for_candidates(i, pi, newton3, g.t0, g.t1, lin, os, oc, hs, hc, pos4, rl2,
+                   [&](int) { ++c; });
+  }
+  count[i] = c;
+}
+
+__global__ void vl_tile_kernel(int n, int A, int B, const int32_t* __restrict__ count,
+                               long long* __restrict__ tile_len, int32_t* __restrict__ kmax) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int ntiles = (n + A - 1) / A;
+  if (t >= ntiles) return;
+  int m = 0;
+  for (int k = t * A; k < t * A + A && k < n; ++k) m = max(m, count[k]);
+  m = (m + B - 1) / B * B;
+  kmax[t] = m;
+  tile_len[t] = (long long)m * A;
+}
+
+__global__ void vl_fill_kernel(GridK g, int n, int A, int newton3, double rl2, int sentinel,
+                               const double* __restrict__ pos4, const int32_t* __restrict__ os,
+                               const int32_t* __restrict__ oc, const int32_t* __restrict__ hs,
+                               const int32_t* __restrict__ hc, const long long* __restrict__ toff,
+                               const int32_t* __restrict__ kmax, int32_t* __restrict__ nbr) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int t = i / A, il = i - t * A;
+  int32_t* out = nbr + toff[t] + il;
+  int k = 0;
+  const double4 pi = ld_pos4(pos4, i);
+  if (pi.w == (double)LMD_OWNED) {
+    const long long lin = cell_of_owned(pi, g.lo0, g.lo1, g.lo2, g.cl0, g.cl1, g.cl2, g.d0, g.d1,
+                                        g.d2, g.t0, g.t1);
+    for_candidates(i, pi, newton3, g.t0, g.t1, lin, os, oc, hs, hc, pos4, rl2, [&](int j) {
+      out[(long long)k * A] = j;
+      ++k;
+    });
+  }
+  const int km = kmax[t];
+  for (; k < km; ++k) out[(long long)k * A] = sentinel;
+}
+
+// padding entries of lanes past the last owned particle of the last tile
+__global__ void vl_tail_pad_kernel(int n, int A, int sentinel, const long long* __restrict__ toff,
+                                   const int32_t* __restrict__ kmax, int32_t* __restrict__ nbr) {
+  const int ntiles = (n + A - 1) / A;
+  const int t = ntiles - 1;
+  const int first_missing = n - t * A;
+  const int km = kmax[t];
+  for (int e = threadIdx.x; e < km * A; e += blockDim.x) {
+    const int il = e % A;
+    if (il >= first_missing) nbr[toff[t] + e] = sentinel;
+  }
+}
+
+// ------------------------------------------------------------------ force
+template <int P, bool EV, bool N3>
+__global__ void __launch_bounds__(32 * kVLWarps)
+    vl_force_kernel(int n_owned, int ntiles, const double* __restrict__ x,
+                    const double* __restrict__ y, const double* __restrict__ z,
+                    const long long* __restrict__ toff, const int32_t* __restrict__ kmax,
+                    const int32_t* __restrict__ nbr, LJK k, double* __restrict__ fx,
+                    double* __restrict__ fy, double* __restrict__ fz, double* __restrict__ ev,
+                    lmd_stats* __restrict__ stats) {
+  using Pat = Pattern<P>;
+  const int lane = threadIdx.x & 31;
+  const int t = blockIdx.x * kVLWarps + (threadIdx.x >> 5);
+  long long pairs = 0, pairs_halo = 0;
+  int overlap = 0;
+  double e_acc = 0.0, v_acc = 0.0;
+  if (t < ntiles) {
+    const int io = Pat::ioff(lane), jo = Pat::joff(lane);
+    const int i = t * Pat::A + io;
+    const bool iact = i < n_owned;
+    const double xi = iact ? x[i] : 0.0, yi = iact ? y[i] : 0.0, zi = iact ? z[i] : 0.0;
+    const int32_t* list = nbr + toff[t] + jo * Pat::A + io;
+    const int steps = kmax[t] / Pat::B;
+    double ax = 0.0, ay = 0.0, az = 0.0;
+#pragma unroll 2
+    for (int s = 0; s < steps; ++s) {
+      const int j = __ldg(list + (long long)s * (Pat::A * Pat::B));
+      const double dx = xi - __ldg(x + j), dy = yi - __ldg(y + j), dz = zi - __ldg(z + j);
+      const double r2 = r2_exact(dx, dy, dz);
+      if (r2 < k.rc2) {
+        if (r2 == 0.0) {
+          overlap = 1;
+          continue;
+        }
+        double s6;
+        const double f = lj_scalar(r2, k, s6);
+        ax = fma(f, dx, ax);
+        ay = fma(f, dy, ay);
+        az = fma(f, dz, az);
+        ++pairs;
+        const bool jhalo = j >= n_owned;
+        pairs_halo += jhalo;
+        if (N3 && !jhalo) {
+          atomicAdd(fx + j, -f * dx);
+          atomicAdd(fy + j, -f * dy);
+          atomicAdd(fz + j, -f * dz);
+        }
+        if (EV) {
+          const double w = (N3 && !jhalo) ? 1.0 : 0.5;
+          e_acc = fma(w * s6, fma(k.eps4, s6, -k.eps4), e_acc);
+          v_acc = fma(w * f, r2, v_acc);
+        }
+      }
+    }
+    ax = reduce_j<P>(ax);
+    ay = reduce_j<P>(ay);
+    az = reduce_j<P>(az);
+    if (iact && jo == 0) {
+      if (N3) {
+        atomicAdd(fx + i, ax);
+        atomicAdd(fy + i, ay);
+        atomicAdd(fz + i, az);
+      } else {
+        fx[i] = ax;
+        fy[i] = ay;
+        fz[i] = az;
+      }
+    }
+  }
+  pairs = warp_sum_ll(pairs);
+  pairs_halo = warp_sum_ll(pairs_halo);
+  overlap = __any_sync(0xffffffffu, overlap);
+  if (lane == 0 && t < ntiles) {
+    if (pairs) atomicAdd((unsigned long long*)&stats->pair_interactions, (unsigned long long)pairs);
+    if (pairs_halo)
+      atomicAdd((unsigned long long*)&stats->pairs_owned_halo, (unsigned long long)pairs_halo);
+    if (overlap) atomicOr(&stats->overlap, 1);
+  }
+  if (EV) {
+    e_acc = warp_sum(e_acc);
+    v_acc = warp_sum(v_acc);
+    if (lane == 0) {
+      const long long w = (long long)blockIdx.x * kVLWarps + (threadIdx.x >> 5);
+      ev[2 * w] = e_acc;
+      ev[2 * w + 1] = v_acc;
+    }
+  }
+}
+
+__global__ void vl_stats_kernel(int n, int a, int b, const int32_t* __restrict__ count,
+                                lmd_stats* __restrict__ stats) {
+  // i-tiles of `a` consecutive backing slots; each tile's j-stream is its
+  // longest list, chunked by b (oracle/lj_oracle.c: orc_force_phase_vl)
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int ntiles = (n + a - 1) / a;
+  long long inv = 0, useful = 0;
+  if (t < ntiles) {
+    int m = 0;
+    for (int q = t * a; q < t * a + a && q < n; ++q) {
+      m = max(m, count[q]);
+      useful += count[q];
+    }
+    inv = (m + b - 1) / b;
+  }
+  inv = warp_sum_ll(inv);
+  useful = warp_sum_ll(useful);
+  if ((threadIdx.x & 31) == 0 && (inv || useful)) {
+    atomicAdd((unsigned long long*)&stats->kernel_invocations, (unsigned long long)inv);
+    atomicAdd((unsigned long long*)&stats->useful_interactions, (unsigned long long)useful);
+  }
+}
+
+__global__ void lane_slots_kernel_vl(lmd_stats* stats, int V) {
+  stats->lane_slots = stats->kernel_invocations * (long long)V;
+}
+
+__global__ void gather_soa_kernel(int64_t n, const int32_t* __restrict__ perm,
+                                  const double* __restrict__ x, const double* __restrict__ y,
+                                  const double* __restrict__ z, double* __restrict__ ox,
+                                  double* __restrict__ oy, double* __restrict__ oz) {
+  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int32_t s = perm ? perm[k] : (int32_t)k;
+  ox[k] = x[s];
+  oy[k] = y[s];
+  oz[k] = z[s];
+}
+
+static GridK make_gridk(const lmd_grid* g) {
+  GridK k;
+  k.lo0 = g->lo[0];
+  k.lo1 = g->lo[1];
+  k.lo2 = g->lo[2];
+  k.cl0 = g->cell_len[0];
+  k.cl1 = g->cell_len[1];
+  k.cl2 = g->cell_len[2];
+  k.d0 = g->dims[0];
+  k.d1 = g->dims[1];
+  k.d2 = g->dims[2];
+  k.t0 = g->tdims[0];
+  k.t1 = g->tdims[1];
+  return k;
+}
+
+static int pattern_A(int p) {
+  return p == LMD_ONE_BY_V ? 1 : p == LMD_V_BY_ONE ? 32 : p == LMD_TWO_BY_HALF ? 2 : 16;
+}
+static int pattern_B(int p) { return 32 / pattern_A(p); }
+
+}  // namespace lmd
+
+using namespace lmd;
+
+extern "C" {
+
+int lmd_vl_count(const lmd_grid* g, double rl2, int newton3, int64_t n_owned, const double* pos4,
+                 const int32_t* o_start, const int32_t* o_count, const int32_t* h_start,
+                 const int32_t* h_count, int32_t* count, void* stream) {
+  if (n_owned <= 0) return LMD_OK;
+  if (n_owned > 0x7fffffffLL) return LMD_ERR_CONFIG;
+  vl_count_kernel<<<(unsigned)cdiv(n_owned, 128), 128, 0, (cudaStream_t)stream>>>(
+      make_gridk(g), (int)n_owned, newton3, rl2, pos4, o_start, o_count, h_start, h_count, count);
+  LMD_CHECK_LAUNCH();
+  return LMD_OK;
+}
+
+int64_t lmd_vl_num_tiles(int64_t n_owned, int pattern) {
+  return cdiv(n_owned, pattern_A(pattern));
+}
+
+size_t lmd_vl_scan_temp_bytes(int64_t ntiles) {
+  size_t bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, bytes, (const long long*)nullptr, (long long*)nullptr,
+                                (int)(ntiles > 0 ? ntiles : 1));
+  return bytes;
+}
+
+int lmd_vl_layout(int64_t n_owned, int pattern, const int32_t* count, int64_t* tile_len,
+                  int64_t* tile_off, int32_t* kmax, void* temp, size_t temp_bytes,
+                  void* stream) {
+  if (n_owned <= 0) return LMD_OK;
+  const int A = pattern_A(pattern), B = pattern_B(pattern);
+  const int64_t ntiles = cdiv(n_owned, A);
+  cudaStream_t s = (cudaStream_t)stream;
+  vl_tile_kernel<<<(unsigned)cdiv(ntiles, 256), 256, 0, s>>>((int)n_owned, A, B, count,
+                                                             (long long*)tile_len, kmax);
+  LMD_CHECK_LAUNCH();
+  size_t bytes = temp_bytes;
+  cudaError_t e = cub::DeviceScan::ExclusiveSum(temp, bytes, (const long long*)tile_len,
+                                                (long long*)tile_off, (int)ntiles, s);
+  if (e != cudaSuccess) return set_cuda_error(e);
+  return LMD_OK;
+}
+
+int lmd_vl_fill(const lmd_grid* g, double rl2, int newton3, int pattern, int64_t n_owned,
+                int32_t sentinel, const double* pos4, const int32_t* o_start,
+                const int32_t* o_count, const int32_t* h_start, const int32_t* h_count,
+                const int64_t* tile_off, const int32_t* kmax, int32_t* nbr, void* stream) {
+  if (n_owned <= 0) return LMD_OK;
+  const int A = pattern_A(pattern);
+  cudaStream_t s = (cudaStream_t)stream;
+  vl_fill_kernel<<<(unsigned)cdiv(n_owned, 128), 128, 0, s>>>(
+      make_gridk(g), (int)n_owned, A, newton3, rl2, sentinel, pos4, o_start, o_count, h_start,
+      h_count, (const long long*)tile_off, kmax, nbr);
+  LMD_CHECK_LAUNCH();
+  if (n_owned % A) {
+    vl_tail_pad_kernel<<<1, 256, 0, s>>>((int)n_owned, A, sentinel, (const long long*)tile_off,
+                                         kmax, nbr);
+    LMD_CHECK_LAUNCH();
+  }
+  return LMD_OK;
+}
+
+int64_t lmd_vl_ev_slots(int64_t n_owned, int pattern) {
+  return cdiv(lmd_vl_num_tiles(n_owned, pattern), kVLWarps) * kVLWarps;
+}
+
+int lmd_force_vl(int pattern, int newton3, int flags, const lmd_lj* lj, int64_t n_owned,
+                 const double* x, const double* y, const double* z, const int64_t* tile_off,
+                 const int32_t* kmax, const int32_t* nbr, double* fx, double* fy, double* fz,
+                 double* ev_scratch, lmd_stats* stats, void* stream) {
+  if (n_owned <= 0) return LMD_OK;
+  const LJK k = make_ljk(lj);
+  const int64_t ntiles = lmd_vl_num_tiles(n_owned, pattern);
+  const unsigned blocks = (unsigned)cdiv(ntiles, kVLWarps);
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool ev = (flags & LMD_FLAG_ENERGY) != 0;
+  if (newton3) {
+    // forces accumulate through atomics; the caller zeroes them
+  }
+#define LMD_VL(P, EVB, N3B)                                                                    \
+  vl_force_kernel<P, EVB, N3B><<<blocks, 32 * kVLWarps, 0, s>>>(                               \
+      (int)n_owned, (int)ntiles, x, y, z, (const long long*)tile_off, kmax, nbr, k, fx, fy, fz, \
+      ev_scratch, stats)
+#define LMD_VL_P(P)                         \
+  do {                                      \
+    if (ev) {                               \
+      if (newton3) LMD_VL(P, true, true);   \
+      else LMD_VL(P, true, false);          \
+    } else {                                \
+      if (newton3) LMD_VL(P, false, true);  \
+      else LMD_VL(P, false, false);         \
+    }                                       \
+  } while (0)
+  switch (pattern) {
+    case LMD_ONE_BY_V: LMD_VL_P(LMD_ONE_BY_V); break;
+    case LMD_V_BY_ONE: LMD_VL_P(LMD_V_BY_ONE); break;
+    case LMD_TWO_BY_HALF: LMD_VL_P(LMD_TWO_BY_HALF); break;
+    case LMD_HALF_BY_TWO: LMD_VL_P(LMD_HALF_BY_TWO); break;
+    default: return LMD_ERR_CONFIG;
+  }
+#undef LMD_VL_P
+#undef LMD_VL
+  LMD_CHECK_LAUNCH();
+  if (ev) return reduce_ev(ev_scratch, lmd_vl_ev_slots(n_owned, pattern), stats, s);
+  return LMD_OK;
+}
+
+int lmd_vl_stats(int64_t n_owned, int a, int b, int vector_width, const int32_t* count,
+                 lmd_stats* stats, void* stream) {
+  if (vector_width < 4 || (vector_width & (vector_width - 1)) != 0) return LMD_ERR_CONFIG;
+  if (a < 1 || b < 1 || a * b != vector_width) return LMD_ERR_CONFIG;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (n_owned > 0) {
+    const int64_t ntiles = cdiv(n_owned, a);
+    vl_stats_kernel<<<(unsigned)cdiv(ntiles, 256), 256, 0, s>>>((int)n_owned, a, b, count, stats);
+    LMD_CHECK_LAUNCH();
+  }
+  lane_slots_kernel_vl<<<1, 1, 0, s>>>(stats, vector_width);
+  LMD_CHECK_LAUNCH();
+  return LMD_OK;
+}
+
+int lmd_gather_soa(int64_t n, const int32_t* perm, const double* x, const double* y,
+                   const double* z, double* ox, double* oy, double* oz, void* stream) {
+  if (n <= 0) return LMD_OK;
+  gather_soa_kernel<<<(unsigned)cdiv(n, 256), 256, 0, (cudaStream_t)stream>>>(n, perm, x, y, z,
+                                                                             ox, oy, oz);
+  LMD_CHECK_LAUNCH();
+  return LMD_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,266 @@
+"""Verlet lists with a skin on the device (north-star extension; the reference
+excludes them).
+
+The container follows the reference's container protocol (driver.py:179-208):
+``needs_rebuild`` (displacement >= skin/2 or the rebuild period),
+``rebuild`` (bin + images + lists), ``refresh`` (between rebuilds: reload
+positions into the rebuild-time order and move the images with their owners
+-- no re-binning, no host synchronisation), ``collect_forces``.  Lists are
+built by K3 on the rc+skin cell grid and laid out per interaction order
+(see csrc/vl.cu); the force kernel K4 gathers SoA positions.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .containers import _Sorter, _check_all_owned, _grid, device_soa, needs_rebuild
+from .domain import as_box, build_halo
+from .errors import ConfigurationError, ParticleOverlapError
+from .kernels import KernelStats, as_pattern, validate_vector_width
+from .particles import HALO, OWNED
+
+VL_REBUILD_PERIOD_DEFAULT = 10
+SENTINEL_POSITION = 1.0e30
+
+
+class VerletListContainer:
+    kind = "vl"
+
+    def __init__(self, box, params, rebuild_period: int = VL_REBUILD_PERIOD_DEFAULT, device=None):
+        self.box = as_box(box)
+        self.params = params
+        self.rebuild_period = rebuild_period
+        self.device = torch.device(device) if device is not None else (
+            torch.device("cuda") if torch.cuda.is_available() else torch.device("cpu"))
+        self.grid = _grid(self.box, params.interaction_length)
+        g = self.grid
+        self.dims = np.array(list(g.dims), dtype=np.int64)
+        self.total_dims = self.dims + 2
+        self.reference_positions = None
+        self.steps_since_rebuild = 0
+        self.structure_version = 0
+        self.n_owned = 0
+        self.n_halo = 0
+        self._sorter = None
+        self._lists: dict = {}
+        self._counts: dict = {}
+        self._stats_cache: dict = {}
+
+    # ------------------------------------------------------------ protocol
+    def needs_rebuild(self, owned) -> bool:
+        d = device_soa(owned)
+        return needs_rebuild(d.positions(), self.reference_positions, self.params.skin,
+                             self.steps_since_rebuild, self.rebuild_period)
+
+    def rebuild(self, owned) -> None:
+        d = device_soa(owned)
+        _check_all_owned(d)
+        dev = d.device
+        nc = int(self.grid.ncell)
+        if self._sorter is None or self._sorter.device != dev:
+            self._sorter = _Sorter(dev)
+            self._o_start = torch.empty(nc, dtype=torch.int32, device=dev)
+            self._o_count = torch.empty(nc, dtype=torch.int32, device=dev)
+            self._h_start = torch.zeros(nc, dtype=torch.int32, device=dev)
+            self._h_count = torch.zeros(nc, dtype=torch.int32, device=dev)
+        n = len(d)
+        s = N.stream()
+        self._perm = self._sorter.bin(self.grid, 0, d.pos_x, d.pos_y, d.pos_z, 0,
+                                      self._o_start, self._o_count)
+        halo = build_halo(d, self.box, self.params.interaction_length)
+        nh = len(halo)
+        self.n_owned, self.n_halo = n, nh
+        self._pos4 = torch.empty((n + nh, 4), dtype=torch.float64, device=dev)
+        if n:
+            N.call("lmd_gather_pos4", n, N.ptr(self._perm), N.ptr(d.pos_x), N.ptr(d.pos_y),
+                   N.ptr(d.pos_z), None, float(OWNED), N.ptr(self._pos4), s)
+        if nh:
+            hperm = self._sorter.bin(self.grid, 1, halo.pos_x, halo.pos_y, halo.pos_z, n,
+                                     self._h_start, self._h_count)
+            N.call("lmd_gather_pos4", nh, N.ptr(hperm), N.ptr(halo.pos_x), N.ptr(halo.pos_y),
+                   N.ptr(halo.pos_z), None, float(HALO), N.ptr(self._pos4[n:]), s)
+            hp = hperm.long()
+            self._halo_owner = halo.extra["owner"][hp].contiguous()
+            self._halo_shift = halo.extra["shift"][hp].contiguous()
+        else:
+            self._h_start.zero_()
+            self._h_count.zero_()
+            self._halo_owner = torch.zeros(0, dtype=torch.int32, device=dev)
+            self._halo_shift = torch.zeros(0, dtype=torch.int8, device=dev)
+        # SoA positions for the force gathers, + one sentinel far away
+        tot = n + nh + 1
+        self._x = torch.empty(tot, dtype=torch.float64, device=dev)
+        self._y = torch.empty(tot, dtype=torch.float64, device=dev)
+        self._z = torch.empty(tot, dtype=torch.float64, device=dev)
+        self._x[-1] = SENTINEL_POSITION
+        self._y[-1] = SENTINEL_POSITION
+        self._z[-1] = SENTINEL_POSITION
+        self._fx = torch.zeros(max(n, 1), dtype=torch.float64, device=dev)
+        self._fy = torch.zeros(max(n, 1), dtype=torch.float64, device=dev)
+        self._fz = torch.zeros(max(n, 1), dtype=torch.float64, device=dev)
+        self._load_positions(d)
+        self._lists.clear()
+        self._counts.clear()
+        self._stats_cache.clear()
+        self.reference_positions = d.positions().clone()
+        self.steps_since_rebuild = 0
+        self.structure_version += 1
+
+    def _load_positions(self, d) -> None:
+        n, nh = self.n_owned, self.n_halo
+        s = N.stream()
+        if n:
+            N.call("lmd_gather_soa", n, N.ptr(self._perm), N.ptr(d.pos_x), N.ptr(d.pos_y),
+                   N.ptr(d.pos_z), N.ptr(self._x), N.ptr(self._y), N.ptr(self._z), s)
+        if nh:
+            N.call("lmd_halo_refresh_soa", N.make_box(self.box), nh, N.ptr(self._halo_owner),
+                   N.ptr(self._halo_shift), N.ptr(d.pos_x), N.ptr(d.pos_y), N.ptr(d.pos_z),
+                   N.ptr(self._x[n:]), N.ptr(self._y[n:]), N.ptr(self._z[n:]), s)
+
+    def refresh(self, owned, halo=None) -> None:
+        """Reload current positions (rebuild-time order) and move the images
+        with their owners; ``halo`` is accepted for protocol compatibility --
+        images are derived from the rebuild-time set, which covers every pair
+        within the cutoff while displacements stay below skin/2."""
+        if self.reference_positions is None:
+            raise ConfigurationError("container has not been rebuilt")
+        self._load_positions(device_soa(owned))
+
+    refresh_positions = refresh
+
+    # ----------------------------------------------------------------- lists
+    def _count(self, newton3: bool) -> torch.Tensor:
+        c = self._counts.get(newton3)
+        if c is None:
+            n = self.n_owned
+            c = torch.zeros(max(n, 1), dtype=torch.int32, device=self._pos4.device)
+            rl2 = self.params.interaction_length * self.params.interaction_length
+            N.call("lmd_vl_count", self.grid, float(rl2), int(newton3), n, N.ptr(self._pos4),
+                   N.ptr(self._o_start), N.ptr(self._o_count), N.ptr(self._h_start),
+                   N.ptr(self._h_count), N.ptr(c), N.stream())
+            self._counts[newton3] = c
+        return c
+
+    def _list(self, pattern, newton3: bool):
+        key = (pattern.code, bool(newton3))
+        hit = self._lists.get(key)
+        if hit is not None:
+            return hit
+        n = self.n_owned
+        dev = self._pos4.device
+        count = self._count(newton3)
+        L = N.load()
+        ntiles = int(L.lmd_vl_num_tiles(n, pattern.code))
+        tile_len = torch.empty(max(ntiles, 1), dtype=torch.int64, device=dev)
+        tile_off = torch.empty(max(ntiles, 1), dtype=torch.int64, device=dev)
+        kmax = torch.zeros(max(ntiles, 1), dtype=torch.int32, device=dev)
+        tb = int(L.lmd_vl_scan_temp_bytes(ntiles))
+        temp = torch.empty(max(tb, 1), dtype=torch.uint8, device=dev)
+        s = N.stream()
+        total = 0
+        if n:
+            N.call("lmd_vl_layout", n, pattern.code, N.ptr(count), N.ptr(tile_len),
+                   N.ptr(tile_off), N.ptr(kmax), N.ptr(temp), tb, s)
+            total = int((tile_off[ntiles - 1] + tile_len[ntiles - 1]).item())
+        nbr = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
+        if n:
+            rl2 = self.params.interaction_length * self.params.interaction_length
+            N.call("lmd_vl_fill", self.grid, float(rl2), int(newton3), pattern.code, n,
+                   self.n_owned + self.n_halo, N.ptr(self._pos4), N.ptr(self._o_start),
+                   N.ptr(self._o_count), N.ptr(self._h_start), N.ptr(self._h_count),
+                   N.ptr(tile_off), N.ptr(kmax), N.ptr(nbr), s)
+        hit = (tile_off, kmax, nbr, total)
+        self._lists[key] = hit
+        return hit
+
+    def list_entries(self, pattern, newton3: bool) -> int:
+        """Padded list entries of the layout for `pattern` (4 B each)."""
+        return self._list(as_pattern(pattern), newton3)[3]
+
+    def pairs(self, newton3: bool = False):
+        """(id_i, id_j, j_is_image) of every list entry, for exact set checks."""
+        pattern = as_pattern("one_by_v")
+        tile_off, kmax, nbr, total = self._list(pattern, newton3)
+        count = self._count(newton3)[: self.n_owned].long()
+        n = self.n_owned
+        perm = self._perm.long()
+        owner = self._halo_owner.long()
+        # ONE_BY_V tiles hold one i each: entries are contiguous per i
+        offs = tile_off[:n].long()
+        i_idx = torch.repeat_interleave(torch.arange(n, device=count.device), count)
+        first = torch.repeat_interleave(torch.cumsum(count, 0) - count, count)
+        k = torch.arange(int(count.sum()), device=count.device) - first
+        j = nbr[(offs[i_idx] + k)].long()
+        is_img = j >= n
+        jid = torch.where(is_img, perm[owner[(j - n).clamp(min=0)]], perm[j.clamp(max=n - 1)])
+        return perm[i_idx], jid, is_img
+
+    # ----------------------------------------------------------------- force
+    def launch_force(self, pattern, newton3: bool, energy: bool = False, stats_t=None,
+                     ev_t=None):
+        pattern = as_pattern(pattern)
+        tile_off, kmax, nbr, _ = self._list(pattern, newton3)
+        dev = self._pos4.device
+        if stats_t is None:
+            stats_t = N.new_stats(dev)
+        else:
+            stats_t.zero_()
+        if ev_t is None:
+            slots = int(N.load().lmd_vl_ev_slots(self.n_owned, pattern.code))
+            ev_t = torch.empty(2 * max(slots, 1), dtype=torch.float64, device=dev)
+        if newton3:
+            self._fx.zero_()
+            self._fy.zero_()
+            self._fz.zero_()
+        N.call("lmd_force_vl", pattern.code, int(newton3), N.FLAG_ENERGY if energy else 0,
+               N.make_lj(self.params), self.n_owned, N.ptr(self._x), N.ptr(self._y),
+               N.ptr(self._z), N.ptr(tile_off), N.ptr(kmax), N.ptr(nbr), N.ptr(self._fx),
+               N.ptr(self._fy), N.ptr(self._fz), N.ptr(ev_t), N.ptr(stats_t), N.stream())
+        return stats_t
+
+    def vl_stats(self, newton3: bool, pattern, V: int):
+        key = (self.structure_version, bool(newton3), pattern, V)
+        hit = self._stats_cache.get(key)
+        if hit is None:
+            a, b = pattern.shape(V)
+            t = N.new_stats(self._pos4.device)
+            N.call("lmd_vl_stats", self.n_owned, a, b, V, N.ptr(self._count(newton3)), N.ptr(t),
+                   N.stream())
+            st = N.read_stats(t)
+            hit = (int(st.kernel_invocations), int(st.lane_slots), int(st.useful_interactions))
+            self._stats_cache[key] = hit
+        return hit
+
+    def compute_forces(self, traversal, newton3: bool, pattern, vector_width: int,
+                       energy: bool = False) -> KernelStats:
+        from .traversals import TraversalKind, as_traversal
+        validate_vector_width(vector_width)
+        if as_traversal(traversal) is not TraversalKind.VL:
+            raise ConfigurationError(f"{traversal} traversal requires the verlet-list container")
+        pattern = as_pattern(pattern)
+        inv, slots, useful = self.vl_stats(newton3, pattern, vector_width)
+        st = N.read_stats(self.launch_force(pattern, newton3, energy))
+        if st.overlap:
+            raise ParticleOverlapError("zero distance between interacting particles")
+        return KernelStats(kernel_invocations=inv, lane_slots=slots, useful_interactions=useful,
+                           pair_interactions=int(st.pair_interactions), epot=st.epot,
+                           virial=st.virial)
+
+    def collect_forces(self, owned) -> None:
+        d = device_soa(owned)
+        n = self.n_owned
+        if n:
+            N.call("lmd_scatter_forces", n, N.ptr(self._perm), N.ptr(self._fx), N.ptr(self._fy),
+                   N.ptr(self._fz), N.ptr(d.force_x), N.ptr(d.force_y), N.ptr(d.force_z),
+                   N.stream())
+        if d is not owned:
+            for name in ("force_x", "force_y", "force_z"):
+                dst = getattr(owned, name)
+                val = getattr(d, name)
+                if isinstance(dst, torch.Tensor):
+                    dst.copy_(val.to(dst.device))
+                else:
+                    dst[...] = val.cpu().numpy()

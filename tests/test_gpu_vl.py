@@ -1,0 +1,93 @@
+"""GPU Verlet lists (north-star extension) against the oracle.
+
+Bars: the neighbor-pair set is EXACTLY the oracle's (same exact-r2 rule);
+forces within forces_close of the oracle; pair counts and lane statistics
+exact; energy/virial 1e-12 relative; lists reused between rebuilds track a
+from-scratch linked-cell evaluation at the moved positions.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import forces_close, jittered_lattice
+from oracle import oracle as O
+
+import paper_2512_03565_b200 as B
+from paper_2512_03565_b200 import Configuration, LJParams, ParticleBuffer, PatternKind, SimulationBox
+
+pytestmark = pytest.mark.gpu
+
+
+def _state(rng, n, rho):
+    side = int(round((n / rho) ** (1 / 3) / 1.0))
+    span = (n / rho) ** (1 / 3)
+    k = int(np.ceil(n ** (1 / 3)))
+    pos = jittered_lattice(rng, (k, k, k), span / k, 0.3 * span / k)[:n]
+    return pos, span
+
+
+@pytest.mark.parametrize("periodic", [True, False])
+def test_pair_sets_exact(rng, periodic):
+    pos, span = _state(rng, 3000, 0.6)
+    params = LJParams(cutoff=2.5, skin=0.3)
+    box = SimulationBox.cube(span, periodic=periodic)
+    cont = B.VerletListContainer(box, params)
+    buf = ParticleBuffer.from_positions(pos, device="cuda")
+    cont.rebuild(buf)
+    for n3 in (False, True):
+        gi, gj, gh = (t.cpu().numpy() for t in cont.pairs(n3))
+        oi, oj, oh = O.vl_pairs(pos, np.zeros(3), np.full(3, span), [periodic] * 3, 2.8, n3)
+        got = sorted(zip(gi.tolist(), gj.tolist(), gh.astype(int).tolist()))
+        want = sorted(zip(oi.tolist(), oj.tolist(), oh.astype(int).tolist()))
+        assert got == want
+
+
+@pytest.mark.parametrize("pattern", list(PatternKind))
+def test_forces_stats_energy_vs_oracle(rng, pattern):
+    pos, span = _state(rng, 4000, 0.8)
+    params = LJParams(cutoff=2.5, skin=0.3)
+    box = SimulationBox.cube(span, periodic=True)
+    lo, hi = np.zeros(3), np.full(3, span)
+    for n3 in (False, True):
+        for V in (8, 16):
+            of, ost = O.force_phase_vl(pos, lo, hi, [True] * 3, params, n3, pattern.value, V)
+            buf = ParticleBuffer.from_positions(pos, device="cuda")
+            cfg = Configuration(B.ContainerKind.VERLET_LISTS, B.TraversalKind.VL, n3, pattern)
+            st = B.force_phase(buf, box, params, cfg, V, energy=True)
+            assert st == B.KernelStats(*ost.as_tuple()), (n3, V)
+            assert forces_close(buf.forces().cpu().numpy(), of), (n3, V)
+            assert abs(st.epot - ost.epot) <= 1e-12 * abs(ost.epot)
+            assert abs(st.virial - ost.virial) <= 1e-12 * abs(ost.virial)
+
+
+def test_lists_reused_between_rebuilds_match_fresh_linked_cells(rng):
+    pos, span = _state(rng, 6000, 0.8)
+    params = LJParams(cutoff=2.5, skin=0.3)
+    box = SimulationBox.cube(span, periodic=True)
+    cont = B.VerletListContainer(box, params)
+    buf = ParticleBuffer.from_positions(pos, device="cuda")
+    cont.rebuild(buf)
+    moved = pos + rng.uniform(-0.07, 0.07, pos.shape)   # |disp| < skin/2
+    moved = np.mod(moved, span)
+    buf2 = ParticleBuffer.from_positions(moved, device="cuda")
+    assert not cont.needs_rebuild(buf2)
+    cont.refresh(buf2)
+    st = cont.compute_forces("vl", False, PatternKind.TWO_BY_HALF, 8)
+    cont.collect_forces(buf2)
+    of, ost = O.force_phase_lc(moved, np.zeros(3), np.full(3, span), [True] * 3,
+                               LJParams(cutoff=2.5, skin=0.0), "lc_c01", False, "one_by_v", 8)
+    assert st.pair_interactions == ost.pair_interactions
+    assert forces_close(buf2.forces().cpu().numpy(), of)
+
+
+def test_vl_overlap_raises():
+    pos = np.random.default_rng(3).uniform(0, 9, (40, 3))
+    pos[7] = pos[3]
+    cfg = Configuration.parse("vl,vl,false,one_by_v")
+    with pytest.raises(B.ParticleOverlapError):
+        B.force_phase(ParticleBuffer.from_positions(pos, device="cuda"),
+                      SimulationBox.cube(9.0, periodic=False), LJParams(cutoff=2.2, skin=0.4),
+                      cfg, 8)
