@@ -62,7 +62,7 @@ GPU_LANES = 32
 def as_pattern(pattern) -> PatternKind:
     if isinstance(pattern, PatternKind):
         return pattern
-    value = getattr(pattern, "value", None)
+    value = pattern if isinstance(pattern, str) else getattr(pattern, "value", None)
     if isinstance(value, str):
         try:
             return PatternKind(value)
