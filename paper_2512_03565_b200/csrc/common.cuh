@@ -19,11 +19,20 @@ int set_cuda_error(cudaError_t e);
 // (executor.py:160-161): eps24 = 24*eps, sigma2 = sigma*sigma, rc2 = cutoff*cutoff.
 struct LJK {
   double rc2, sigma2, eps24, eps48, eps4;
+  long long rc2_bits;  // bit pattern of rc2 (positive doubles order like int64)
 };
 
 inline LJK make_ljk(const lmd_lj* p) {
   LJK k;
   k.rc2 = p->cutoff * p->cutoff;
+  {
+    union {
+      double d;
+      long long i;
+    } u;
+    u.d = k.rc2;
+    k.rc2_bits = u.i;
+  }
   k.sigma2 = p->sigma * p->sigma;
   k.eps24 = 24.0 * p->epsilon;
   k.eps48 = 48.0 * p->epsilon;
@@ -35,6 +44,22 @@ inline LJK make_ljk(const lmd_lj* p) {
 // executor.py:93-94), so every cutoff decision is bit-identical.
 __device__ __forceinline__ double r2_exact(double dx, double dy, double dz) {
   return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+}
+
+// Cutoff decision identical to the reference's `r2 >= rc2` test at two FP64
+// slots less than r2_exact: r2 is formed with FMAs (|error| of a few ulp), the
+// comparison happens on the bit patterns on the integer pipes, and only
+// candidates within kR2Band ulps of rc2 are re-evaluated with the exact,
+// unfused reference expression.  Returns the r2 used for the force.
+constexpr long long kR2Band = 64;
+__device__ __forceinline__ bool within_cutoff(double dx, double dy, double dz, const LJK& k,
+                                              double& r2) {
+  r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+  const long long b = __double_as_longlong(r2);
+  if (b < k.rc2_bits - kR2Band) return true;
+  if (b > k.rc2_bits + kR2Band) return false;
+  r2 = r2_exact(dx, dy, dz);
+  return r2 < k.rc2;
 }
 
 // 1/x for normal positive x: MUFU.RCP64H seed + one cubic Newton step
@@ -127,10 +152,14 @@ __device__ __forceinline__ long long warp_sum_ll(long long v) {
   return v;
 }
 
+// One 256-bit read-only load per particle (LDG.E.ENL2.256 on sm_100a): a
+// pos4 record is exactly one 32-byte sector.
 __device__ __forceinline__ double4 ld_pos4(const double* pos4, long long k) {
-  const double2* p = reinterpret_cast<const double2*>(pos4) + 2 * k;
-  const double2 a = __ldg(p), b = __ldg(p + 1);
-  return make_double4(a.x, a.y, b.x, b.y);
+  double4 r;
+  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+      : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w)
+      : "l"(pos4 + 4 * k));
+  return r;
 }
 
 // Deterministic fixed-order reduction of per-warp (epot, virial) partials.

@@ -142,76 +142,101 @@ __global__ void vl_tail_pad_kernel(int n, int A, int sentinel, const long long* 
 }
 
 // ------------------------------------------------------------------ force
+struct Acc {
+  double ax, ay, az, e, v;
+  long long pairs, halo;
+  int overlap;
+};
+
+template <bool EV, bool N3>
+__device__ __forceinline__ void vl_pair(const double4& pi, const double4& pj, int j, int n_owned,
+                                        const LJK& k, Acc& a, double* __restrict__ fx,
+                                        double* __restrict__ fy, double* __restrict__ fz) {
+  const double dx = pi.x - pj.x, dy = pi.y - pj.y, dz = pi.z - pj.z;
+  double r2;
+  if (!within_cutoff(dx, dy, dz, k, r2)) return;
+  if (r2 == 0.0) {
+    a.overlap = 1;
+    return;
+  }
+  double s6;
+  const double f = lj_scalar(r2, k, s6);
+  a.ax = fma(f, dx, a.ax);
+  a.ay = fma(f, dy, a.ay);
+  a.az = fma(f, dz, a.az);
+  ++a.pairs;
+  const bool jhalo = j >= n_owned;
+  a.halo += jhalo;
+  if (N3 && !jhalo) {
+    atomicAdd(fx + j, -f * dx);
+    atomicAdd(fy + j, -f * dy);
+    atomicAdd(fz + j, -f * dz);
+  }
+  if (EV) {
+    const double w = (N3 && !jhalo) ? 1.0 : 0.5;
+    a.e = fma(w * s6, fma(k.eps4, s6, -k.eps4), a.e);
+    a.v = fma(w * f, r2, a.v);
+  }
+}
+
+// One warp per i-tile; lane (io, jo) walks entries k = jo, jo + B, ... of
+// particle t*A + io.  Indices for U fills are loaded first, then the U
+// positions (256-bit gathers), then the U interactions, so each lane keeps
+// 2U loads in flight.
 template <int P, bool EV, bool N3>
-__global__ void __launch_bounds__(32 * kVLWarps)
-    vl_force_kernel(int n_owned, int ntiles, const double* __restrict__ x,
-                    const double* __restrict__ y, const double* __restrict__ z,
+__global__ void __launch_bounds__(32 * kVLWarps, 4)
+    vl_force_kernel(int n_owned, int ntiles, const double* __restrict__ pos4,
                     const long long* __restrict__ toff, const int32_t* __restrict__ kmax,
                     const int32_t* __restrict__ nbr, LJK k, double* __restrict__ fx,
                     double* __restrict__ fy, double* __restrict__ fz, double* __restrict__ ev,
                     lmd_stats* __restrict__ stats) {
   using Pat = Pattern<P>;
+  constexpr int U = 4;
+  constexpr int STRIDE = Pat::A * Pat::B;  // = 32 ints per fill
   const int lane = threadIdx.x & 31;
   const int t = blockIdx.x * kVLWarps + (threadIdx.x >> 5);
-  long long pairs = 0, pairs_halo = 0;
-  int overlap = 0;
-  double e_acc = 0.0, v_acc = 0.0;
+  Acc a = {0.0, 0.0, 0.0, 0.0, 0.0, 0, 0, 0};
   if (t < ntiles) {
     const int io = Pat::ioff(lane), jo = Pat::joff(lane);
     const int i = t * Pat::A + io;
     const bool iact = i < n_owned;
-    const double xi = iact ? x[i] : 0.0, yi = iact ? y[i] : 0.0, zi = iact ? z[i] : 0.0;
+    const double4 pi = ld_pos4(pos4, iact ? i : 0);
     const int32_t* list = nbr + toff[t] + jo * Pat::A + io;
     const int steps = kmax[t] / Pat::B;
-    double ax = 0.0, ay = 0.0, az = 0.0;
-#pragma unroll 2
-    for (int s = 0; s < steps; ++s) {
-      const int j = __ldg(list + (long long)s * (Pat::A * Pat::B));
-      const double dx = xi - __ldg(x + j), dy = yi - __ldg(y + j), dz = zi - __ldg(z + j);
-      const double r2 = r2_exact(dx, dy, dz);
-      if (r2 < k.rc2) {
-        if (r2 == 0.0) {
-          overlap = 1;
-          continue;
-        }
-        double s6;
-        const double f = lj_scalar(r2, k, s6);
-        ax = fma(f, dx, ax);
-        ay = fma(f, dy, ay);
-        az = fma(f, dz, az);
-        ++pairs;
-        const bool jhalo = j >= n_owned;
-        pairs_halo += jhalo;
-        if (N3 && !jhalo) {
-          atomicAdd(fx + j, -f * dx);
-          atomicAdd(fy + j, -f * dy);
-          atomicAdd(fz + j, -f * dz);
-        }
-        if (EV) {
-          const double w = (N3 && !jhalo) ? 1.0 : 0.5;
-          e_acc = fma(w * s6, fma(k.eps4, s6, -k.eps4), e_acc);
-          v_acc = fma(w * f, r2, v_acc);
-        }
-      }
+    int s = 0;
+    for (; s + U <= steps; s += U) {
+      int j[U];
+      double4 pj[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) j[u] = __ldg(list + (long long)(s + u) * STRIDE);
+#pragma unroll
+      for (int u = 0; u < U; ++u) pj[u] = ld_pos4(pos4, j[u]);
+#pragma unroll
+      for (int u = 0; u < U; ++u) vl_pair<EV, N3>(pi, pj[u], j[u], n_owned, k, a, fx, fy, fz);
     }
-    ax = reduce_j<P>(ax);
-    ay = reduce_j<P>(ay);
-    az = reduce_j<P>(az);
+    for (; s < steps; ++s) {
+      const int j = __ldg(list + (long long)s * STRIDE);
+      vl_pair<EV, N3>(pi, ld_pos4(pos4, j), j, n_owned, k, a, fx, fy, fz);
+    }
+    if (!iact) a.ax = a.ay = a.az = 0.0;
+    a.ax = reduce_j<P>(a.ax);
+    a.ay = reduce_j<P>(a.ay);
+    a.az = reduce_j<P>(a.az);
     if (iact && jo == 0) {
       if (N3) {
-        atomicAdd(fx + i, ax);
-        atomicAdd(fy + i, ay);
-        atomicAdd(fz + i, az);
+        atomicAdd(fx + i, a.ax);
+        atomicAdd(fy + i, a.ay);
+        atomicAdd(fz + i, a.az);
       } else {
-        fx[i] = ax;
-        fy[i] = ay;
-        fz[i] = az;
+        fx[i] = a.ax;
+        fy[i] = a.ay;
+        fz[i] = a.az;
       }
     }
   }
-  pairs = warp_sum_ll(pairs);
-  pairs_halo = warp_sum_ll(pairs_halo);
-  overlap = __any_sync(0xffffffffu, overlap);
+  const long long pairs = warp_sum_ll(a.pairs);
+  const long long pairs_halo = warp_sum_ll(a.halo);
+  const int overlap = __any_sync(0xffffffffu, a.overlap);
   if (lane == 0 && t < ntiles) {
     if (pairs) atomicAdd((unsigned long long*)&stats->pair_interactions, (unsigned long long)pairs);
     if (pairs_halo)
@@ -219,12 +244,11 @@ __global__ void __launch_bounds__(32 * kVLWarps)
     if (overlap) atomicOr(&stats->overlap, 1);
   }
   if (EV) {
-    e_acc = warp_sum(e_acc);
-    v_acc = warp_sum(v_acc);
+    const double e = warp_sum(a.e), v = warp_sum(a.v);
     if (lane == 0) {
       const long long w = (long long)blockIdx.x * kVLWarps + (threadIdx.x >> 5);
-      ev[2 * w] = e_acc;
-      ev[2 * w + 1] = v_acc;
+      ev[2 * w] = e;
+      ev[2 * w + 1] = v;
     }
   }
 }
@@ -358,7 +382,7 @@ int64_t lmd_vl_ev_slots(int64_t n_owned, int pattern) {
 }
 
 int lmd_force_vl(int pattern, int newton3, int flags, const lmd_lj* lj, int64_t n_owned,
-                 const double* x, const double* y, const double* z, const int64_t* tile_off,
+                 const double* pos4, const int64_t* tile_off,
                  const int32_t* kmax, const int32_t* nbr, double* fx, double* fy, double* fz,
                  double* ev_scratch, lmd_stats* stats, void* stream) {
   if (n_owned <= 0) return LMD_OK;
@@ -372,7 +396,7 @@ int lmd_force_vl(int pattern, int newton3, int flags, const lmd_lj* lj, int64_t 
   }
 #define LMD_VL(P, EVB, N3B)                                                                    \
   vl_force_kernel<P, EVB, N3B><<<blocks, 32 * kVLWarps, 0, s>>>(                               \
-      (int)n_owned, (int)ntiles, x, y, z, (const long long*)tile_off, kmax, nbr, k, fx, fy, fz, \
+      (int)n_owned, (int)ntiles, pos4, (const long long*)tile_off, kmax, nbr, k, fx, fy, fz,     \
       ev_scratch, stats)
 #define LMD_VL_P(P)                         \
   do {                                      \

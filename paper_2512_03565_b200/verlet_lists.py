@@ -7,7 +7,7 @@ The container follows the reference's container protocol (driver.py:179-208):
 positions into the rebuild-time order and move the images with their owners
 -- no re-binning, no host synchronisation), ``collect_forces``.  Lists are
 built by K3 on the rc+skin cell grid and laid out per interaction order
-(see csrc/vl.cu); the force kernel K4 gathers SoA positions.
+(see csrc/vl.cu); the force kernel K4 gathers 32-byte pos4 records.
 """
 
 from __future__ import annotations
@@ -73,7 +73,9 @@ class VerletListContainer:
         halo = build_halo(d, self.box, self.params.interaction_length)
         nh = len(halo)
         self.n_owned, self.n_halo = n, nh
-        self._pos4 = torch.empty((n + nh, 4), dtype=torch.float64, device=dev)
+        # combined backing [owned | images | sentinel] as pos4 (32 B records)
+        self._pos4 = torch.empty((n + nh + 1, 4), dtype=torch.float64, device=dev)
+        self._pos4[-1] = torch.tensor([SENTINEL_POSITION] * 3 + [2.0], dtype=torch.float64)
         if n:
             N.call("lmd_gather_pos4", n, N.ptr(self._perm), N.ptr(d.pos_x), N.ptr(d.pos_y),
                    N.ptr(d.pos_z), None, float(OWNED), N.ptr(self._pos4), s)
@@ -90,18 +92,9 @@ class VerletListContainer:
             self._h_count.zero_()
             self._halo_owner = torch.zeros(0, dtype=torch.int32, device=dev)
             self._halo_shift = torch.zeros(0, dtype=torch.int8, device=dev)
-        # SoA positions for the force gathers, + one sentinel far away
-        tot = n + nh + 1
-        self._x = torch.empty(tot, dtype=torch.float64, device=dev)
-        self._y = torch.empty(tot, dtype=torch.float64, device=dev)
-        self._z = torch.empty(tot, dtype=torch.float64, device=dev)
-        self._x[-1] = SENTINEL_POSITION
-        self._y[-1] = SENTINEL_POSITION
-        self._z[-1] = SENTINEL_POSITION
         self._fx = torch.zeros(max(n, 1), dtype=torch.float64, device=dev)
         self._fy = torch.zeros(max(n, 1), dtype=torch.float64, device=dev)
         self._fz = torch.zeros(max(n, 1), dtype=torch.float64, device=dev)
-        self._load_positions(d)
         self._lists.clear()
         self._counts.clear()
         self._stats_cache.clear()
@@ -113,12 +106,12 @@ class VerletListContainer:
         n, nh = self.n_owned, self.n_halo
         s = N.stream()
         if n:
-            N.call("lmd_gather_soa", n, N.ptr(self._perm), N.ptr(d.pos_x), N.ptr(d.pos_y),
-                   N.ptr(d.pos_z), N.ptr(self._x), N.ptr(self._y), N.ptr(self._z), s)
+            N.call("lmd_gather_pos4", n, N.ptr(self._perm), N.ptr(d.pos_x), N.ptr(d.pos_y),
+                   N.ptr(d.pos_z), None, float(OWNED), N.ptr(self._pos4), s)
         if nh:
-            N.call("lmd_halo_refresh_soa", N.make_box(self.box), nh, N.ptr(self._halo_owner),
+            N.call("lmd_halo_refresh_pos4", N.make_box(self.box), nh, N.ptr(self._halo_owner),
                    N.ptr(self._halo_shift), N.ptr(d.pos_x), N.ptr(d.pos_y), N.ptr(d.pos_z),
-                   N.ptr(self._x[n:]), N.ptr(self._y[n:]), N.ptr(self._z[n:]), s)
+                   N.ptr(self._pos4[n:]), s)
 
     def refresh(self, owned, halo=None) -> None:
         """Reload current positions (rebuild-time order) and move the images
@@ -216,8 +209,8 @@ class VerletListContainer:
             self._fy.zero_()
             self._fz.zero_()
         N.call("lmd_force_vl", pattern.code, int(newton3), N.FLAG_ENERGY if energy else 0,
-               N.make_lj(self.params), self.n_owned, N.ptr(self._x), N.ptr(self._y),
-               N.ptr(self._z), N.ptr(tile_off), N.ptr(kmax), N.ptr(nbr), N.ptr(self._fx),
+               N.make_lj(self.params), self.n_owned, N.ptr(self._pos4),
+               N.ptr(tile_off), N.ptr(kmax), N.ptr(nbr), N.ptr(self._fx),
                N.ptr(self._fy), N.ptr(self._fz), N.ptr(ev_t), N.ptr(stats_t), N.stream())
         return stats_t
 
