@@ -179,78 +179,115 @@ __device__ __forceinline__ void vl_pair(const double4& pi, const double4& pj, in
   }
 }
 
-// One warp per i-tile; lane (io, jo) walks entries k = jo, jo + B, ... of
-// particle t*A + io.  Indices for U fills are loaded first, then the U
-// positions (256-bit gathers), then the U interactions, so each lane keeps
-// 2U loads in flight.
-template <int P, bool EV, bool N3>
+// One i-tile: lane (io, jo) walks entries k = jo, jo + B, ... of particle
+// t*A + io.  Indices for U fills are loaded first, then the U positions
+// (256-bit gathers), then the U interactions, so each lane keeps 2U loads in
+// flight.  Writes the tile's i forces; pair counts etc. accumulate in `a`.
+template <int P, bool EV, bool N3, int U>
+__device__ __forceinline__ void vl_tile(int t, int lane, int n_owned,
+                                        const double* __restrict__ pos4,
+                                        const long long* __restrict__ toff,
+                                        const int32_t* __restrict__ kmax,
+                                        const int32_t* __restrict__ nbr, const LJK& k, Acc& a,
+                                        double* __restrict__ fx, double* __restrict__ fy,
+                                        double* __restrict__ fz) {
+  using Pat = Pattern<P>;
+  constexpr int STRIDE = Pat::A * Pat::B;  // = 32 ints per fill
+  const int io = Pat::ioff(lane), jo = Pat::joff(lane);
+  const int i = t * Pat::A + io;
+  const bool iact = i < n_owned;
+  const double4 pi = ld_pos4(pos4, iact ? i : 0);
+  const int32_t* list = nbr + toff[t] + jo * Pat::A + io;
+  const int steps = kmax[t] / Pat::B;
+  const double ax0 = a.ax, ay0 = a.ay, az0 = a.az;
+  a.ax = a.ay = a.az = 0.0;
+  int s = 0;
+  for (; s + U <= steps; s += U) {
+    int j[U];
+    double4 pj[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) j[u] = __ldg(list + (long long)(s + u) * STRIDE);
+#pragma unroll
+    for (int u = 0; u < U; ++u) pj[u] = ld_pos4(pos4, j[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) vl_pair<EV, N3>(pi, pj[u], j[u], n_owned, k, a, fx, fy, fz);
+  }
+  for (; s < steps; ++s) {
+    const int j = __ldg(list + (long long)s * STRIDE);
+    vl_pair<EV, N3>(pi, ld_pos4(pos4, j), j, n_owned, k, a, fx, fy, fz);
+  }
+  if (!iact) a.ax = a.ay = a.az = 0.0;
+  const double rx = reduce_j<P>(a.ax), ry = reduce_j<P>(a.ay), rz = reduce_j<P>(a.az);
+  if (iact && jo == 0) {
+    if (N3) {
+      atomicAdd(fx + i, rx);
+      atomicAdd(fy + i, ry);
+      atomicAdd(fz + i, rz);
+    } else {
+      fx[i] = rx;
+      fy[i] = ry;
+      fz[i] = rz;
+    }
+  }
+  a.ax = ax0;
+  a.ay = ay0;
+  a.az = az0;
+}
+
+__device__ __forceinline__ void flush_acc(const Acc& a, int lane, bool live, bool ev_on,
+                                          long long warp_slot, double* __restrict__ ev,
+                                          lmd_stats* __restrict__ stats) {
+  const long long pairs = warp_sum_ll(a.pairs);
+  const long long pairs_halo = warp_sum_ll(a.halo);
+  const int overlap = __any_sync(0xffffffffu, a.overlap);
+  if (lane == 0 && live) {
+    if (pairs) atomicAdd((unsigned long long*)&stats->pair_interactions, (unsigned long long)pairs);
+    if (pairs_halo)
+      atomicAdd((unsigned long long*)&stats->pairs_owned_halo, (unsigned long long)pairs_halo);
+    if (overlap) atomicOr(&stats->overlap, 1);
+  }
+  if (ev_on) {
+    const double e = warp_sum(a.e), v = warp_sum(a.v);
+    if (lane == 0) {
+      ev[2 * warp_slot] = e;
+      ev[2 * warp_slot + 1] = v;
+    }
+  }
+}
+
+// One warp per i-tile.
+template <int P, bool EV, bool N3, int U>
 __global__ void __launch_bounds__(32 * kVLWarps, 4)
     vl_force_kernel(int n_owned, int ntiles, const double* __restrict__ pos4,
                     const long long* __restrict__ toff, const int32_t* __restrict__ kmax,
                     const int32_t* __restrict__ nbr, LJK k, double* __restrict__ fx,
                     double* __restrict__ fy, double* __restrict__ fz, double* __restrict__ ev,
                     lmd_stats* __restrict__ stats) {
-  using Pat = Pattern<P>;
-  constexpr int U = 4;
-  constexpr int STRIDE = Pat::A * Pat::B;  // = 32 ints per fill
   const int lane = threadIdx.x & 31;
   const int t = blockIdx.x * kVLWarps + (threadIdx.x >> 5);
   Acc a = {0.0, 0.0, 0.0, 0.0, 0.0, 0, 0, 0};
-  if (t < ntiles) {
-    const int io = Pat::ioff(lane), jo = Pat::joff(lane);
-    const int i = t * Pat::A + io;
-    const bool iact = i < n_owned;
-    const double4 pi = ld_pos4(pos4, iact ? i : 0);
-    const int32_t* list = nbr + toff[t] + jo * Pat::A + io;
-    const int steps = kmax[t] / Pat::B;
-    int s = 0;
-    for (; s + U <= steps; s += U) {
-      int j[U];
-      double4 pj[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) j[u] = __ldg(list + (long long)(s + u) * STRIDE);
-#pragma unroll
-      for (int u = 0; u < U; ++u) pj[u] = ld_pos4(pos4, j[u]);
-#pragma unroll
-      for (int u = 0; u < U; ++u) vl_pair<EV, N3>(pi, pj[u], j[u], n_owned, k, a, fx, fy, fz);
-    }
-    for (; s < steps; ++s) {
-      const int j = __ldg(list + (long long)s * STRIDE);
-      vl_pair<EV, N3>(pi, ld_pos4(pos4, j), j, n_owned, k, a, fx, fy, fz);
-    }
-    if (!iact) a.ax = a.ay = a.az = 0.0;
-    a.ax = reduce_j<P>(a.ax);
-    a.ay = reduce_j<P>(a.ay);
-    a.az = reduce_j<P>(a.az);
-    if (iact && jo == 0) {
-      if (N3) {
-        atomicAdd(fx + i, a.ax);
-        atomicAdd(fy + i, a.ay);
-        atomicAdd(fz + i, a.az);
-      } else {
-        fx[i] = a.ax;
-        fy[i] = a.ay;
-        fz[i] = a.az;
-      }
-    }
-  }
-  const long long pairs = warp_sum_ll(a.pairs);
-  const long long pairs_halo = warp_sum_ll(a.halo);
-  const int overlap = __any_sync(0xffffffffu, a.overlap);
-  if (lane == 0 && t < ntiles) {
-    if (pairs) atomicAdd((unsigned long long*)&stats->pair_interactions, (unsigned long long)pairs);
-    if (pairs_halo)
-      atomicAdd((unsigned long long*)&stats->pairs_owned_halo, (unsigned long long)pairs_halo);
-    if (overlap) atomicOr(&stats->overlap, 1);
-  }
-  if (EV) {
-    const double e = warp_sum(a.e), v = warp_sum(a.v);
-    if (lane == 0) {
-      const long long w = (long long)blockIdx.x * kVLWarps + (threadIdx.x >> 5);
-      ev[2 * w] = e;
-      ev[2 * w + 1] = v;
-    }
-  }
+  if (t < ntiles) vl_tile<P, EV, N3, U>(t, lane, n_owned, pos4, toff, kmax, nbr, k, a, fx, fy, fz);
+  flush_acc(a, lane, t < ntiles, EV, (long long)blockIdx.x * kVLWarps + (threadIdx.x >> 5), ev,
+            stats);
+}
+
+// Persistent variant: each block owns a contiguous (spatially coherent) run
+// of tiles, so the j positions its warps gather stay resident in its SM's L1.
+template <int P, bool EV, bool N3, int U>
+__global__ void __launch_bounds__(32 * kVLWarps, 4)
+    vl_force_persistent_kernel(int n_owned, int ntiles, const double* __restrict__ pos4,
+                               const long long* __restrict__ toff,
+                               const int32_t* __restrict__ kmax, const int32_t* __restrict__ nbr,
+                               LJK k, double* __restrict__ fx, double* __restrict__ fy,
+                               double* __restrict__ fz, double* __restrict__ ev,
+                               lmd_stats* __restrict__ stats) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int per = (ntiles + gridDim.x - 1) / gridDim.x;
+  const int t0 = blockIdx.x * per, t1 = min(ntiles, t0 + per);
+  Acc a = {0.0, 0.0, 0.0, 0.0, 0.0, 0, 0, 0};
+  for (int t = t0 + w; t < t1; t += kVLWarps)
+    vl_tile<P, EV, N3, U>(t, lane, n_owned, pos4, toff, kmax, nbr, k, a, fx, fy, fz);
+  flush_acc(a, lane, true, EV, (long long)blockIdx.x * kVLWarps + w, ev, stats);
 }
 
 __global__ void vl_stats_kernel(int n, int a, int b, const int32_t* __restrict__ count,
@@ -378,8 +415,58 @@ int lmd_vl_fill(const lmd_grid* g, double rl2, int newton3, int pattern, int64_t
 }
 
 int64_t lmd_vl_ev_slots(int64_t n_owned, int pattern) {
-  return cdiv(lmd_vl_num_tiles(n_owned, pattern), kVLWarps) * kVLWarps;
+  // enough for both the one-tile-per-warp grid and the persistent grid
+  return cdiv(lmd_vl_num_tiles(n_owned, pattern), kVLWarps) * kVLWarps + 148 * 64 * kVLWarps;
 }
+
+}  // extern "C"
+
+static int g_persistent_blocks = 0;
+
+template <int P, bool EV, bool N3, int U>
+static void launch_vl(bool persistent, int64_t n_owned, int64_t ntiles, const double* pos4,
+                      const int64_t* tile_off, const int32_t* kmax, const int32_t* nbr,
+                      const LJK& k, double* fx, double* fy, double* fz, double* ev,
+                      lmd_stats* stats, cudaStream_t s) {
+  if (persistent) {
+    int sms = 148;
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess)
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, vl_force_persistent_kernel<P, EV, N3, U>,
+                                                  32 * kVLWarps, 0);
+    int blocks = sms * (per_sm > 0 ? per_sm : 1);
+    if (blocks > 148 * 64) blocks = 148 * 64;
+    g_persistent_blocks = blocks;
+    vl_force_persistent_kernel<P, EV, N3, U><<<blocks, 32 * kVLWarps, 0, s>>>(
+        (int)n_owned, (int)ntiles, pos4, (const long long*)tile_off, kmax, nbr, k, fx, fy, fz, ev,
+        stats);
+  } else {
+    const unsigned blocks = (unsigned)cdiv(ntiles, kVLWarps);
+    vl_force_kernel<P, EV, N3, U><<<blocks, 32 * kVLWarps, 0, s>>>(
+        (int)n_owned, (int)ntiles, pos4, (const long long*)tile_off, kmax, nbr, k, fx, fy, fz, ev,
+        stats);
+  }
+}
+
+template <int P, bool EV, bool N3>
+static void launch_vl_u(int u, bool persistent, int64_t n_owned, int64_t ntiles,
+                        const double* pos4, const int64_t* tile_off, const int32_t* kmax,
+                        const int32_t* nbr, const LJK& k, double* fx, double* fy, double* fz,
+                        double* ev, lmd_stats* stats, cudaStream_t s) {
+  if (u == 1)
+    launch_vl<P, EV, N3, 1>(persistent, n_owned, ntiles, pos4, tile_off, kmax, nbr, k, fx, fy, fz,
+                            ev, stats, s);
+  else if (u == 2)
+    launch_vl<P, EV, N3, 2>(persistent, n_owned, ntiles, pos4, tile_off, kmax, nbr, k, fx, fy, fz,
+                            ev, stats, s);
+  else
+    launch_vl<P, EV, N3, 4>(persistent, n_owned, ntiles, pos4, tile_off, kmax, nbr, k, fx, fy, fz,
+                            ev, stats, s);
+}
+
+extern "C" {
 
 int lmd_force_vl(int pattern, int newton3, int flags, const lmd_lj* lj, int64_t n_owned,
                  const double* pos4, const int64_t* tile_off,
@@ -388,16 +475,15 @@ int lmd_force_vl(int pattern, int newton3, int flags, const lmd_lj* lj, int64_t 
   if (n_owned <= 0) return LMD_OK;
   const LJK k = make_ljk(lj);
   const int64_t ntiles = lmd_vl_num_tiles(n_owned, pattern);
-  const unsigned blocks = (unsigned)cdiv(ntiles, kVLWarps);
   cudaStream_t s = (cudaStream_t)stream;
   const bool ev = (flags & LMD_FLAG_ENERGY) != 0;
-  if (newton3) {
-    // forces accumulate through atomics; the caller zeroes them
-  }
-#define LMD_VL(P, EVB, N3B)                                                                    \
-  vl_force_kernel<P, EVB, N3B><<<blocks, 32 * kVLWarps, 0, s>>>(                               \
-      (int)n_owned, (int)ntiles, pos4, (const long long*)tile_off, kmax, nbr, k, fx, fy, fz,     \
-      ev_scratch, stats)
+  // tuning knobs: bits 4-5 unroll (0 -> 4, 1 -> 1, 2 -> 2), bit 6 persistent grid
+  const int ucode = (flags >> 4) & 3;
+  const int u = ucode == 1 ? 1 : ucode == 2 ? 2 : 4;
+  const bool persistent = (flags >> 6) & 1;
+#define LMD_VL(P, EVB, N3B)                                                                  \
+  launch_vl_u<P, EVB, N3B>(u, persistent, n_owned, ntiles, pos4, tile_off, kmax, nbr, k, fx, \
+                           fy, fz, ev_scratch, stats, s)
 #define LMD_VL_P(P)                         \
   do {                                      \
     if (ev) {                               \
@@ -418,7 +504,11 @@ int lmd_force_vl(int pattern, int newton3, int flags, const lmd_lj* lj, int64_t 
 #undef LMD_VL_P
 #undef LMD_VL
   LMD_CHECK_LAUNCH();
-  if (ev) return reduce_ev(ev_scratch, lmd_vl_ev_slots(n_owned, pattern), stats, s);
+  if (ev) {
+    const int64_t slots = persistent ? (int64_t)g_persistent_blocks * kVLWarps
+                                     : cdiv(ntiles, kVLWarps) * kVLWarps;
+    return reduce_ev(ev_scratch, slots, stats, s);
+  }
   return LMD_OK;
 }
 

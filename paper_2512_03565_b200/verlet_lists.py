@@ -48,6 +48,8 @@ class VerletListContainer:
         self._lists: dict = {}
         self._counts: dict = {}
         self._stats_cache: dict = {}
+        # kernel tuning knobs (csrc/vl.cu lmd_force_vl flags bits 4-6)
+        self.knobs = 0
 
     # ------------------------------------------------------------ protocol
     def needs_rebuild(self, owned) -> bool:
@@ -188,7 +190,10 @@ class VerletListContainer:
         k = torch.arange(int(count.sum()), device=count.device) - first
         j = nbr[(offs[i_idx] + k)].long()
         is_img = j >= n
-        jid = torch.where(is_img, perm[owner[(j - n).clamp(min=0)]], perm[j.clamp(max=n - 1)])
+        jid = torch.empty_like(j)
+        jid[~is_img] = perm[j[~is_img]]
+        if bool(is_img.any()):
+            jid[is_img] = owner[j[is_img] - n]   # owner indices are caller order
         return perm[i_idx], jid, is_img
 
     # ----------------------------------------------------------------- force
@@ -208,7 +213,7 @@ class VerletListContainer:
             self._fx.zero_()
             self._fy.zero_()
             self._fz.zero_()
-        N.call("lmd_force_vl", pattern.code, int(newton3), N.FLAG_ENERGY if energy else 0,
+        N.call("lmd_force_vl", pattern.code, int(newton3), (N.FLAG_ENERGY if energy else 0) | self.knobs,
                N.make_lj(self.params), self.n_owned, N.ptr(self._pos4),
                N.ptr(tile_off), N.ptr(kmax), N.ptr(nbr), N.ptr(self._fx),
                N.ptr(self._fy), N.ptr(self._fz), N.ptr(ev_t), N.ptr(stats_t), N.stream())
