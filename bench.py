@@ -31,7 +31,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 FLOPS_PER_PAIR = {False: 22, True: 25}   # SURVEY.md §8(d), counted on executor.py:93-111
-DEFAULT_CONFIG = "lc,lc_c01,false,two_by_half"
+DEFAULT_CONFIG = "vl,vl,false,v_by_one"
 METRIC = "LJ FP64 pair-interactions/sec"
 UNIT = "pair-interactions/s"
 
@@ -230,6 +230,12 @@ def cpu_baseline_lc(w, cfg, params, threads):
     pos = w.positions.cpu().numpy() if hasattr(w.positions, "cpu") else w.positions
     trav = cfg.traversal.value
     n3 = cfg.newton3
+    if cfg.container.value != "lc":
+        # the reference has no Verlet lists: its own algorithm for
+        # the same pairs is linked cells with cell size = cutoff
+        from paper_2512_03565_b200 import LJParams
+        trav, n3 = "lc_c01", False
+        params = LJParams(cutoff=params.cutoff, skin=0.0)
     if threads > 1 and n3:
         trav, n3 = "lc_c01", False       # the parallel baseline sweeps Newton3-off units
     t0 = time.perf_counter()

@@ -49,7 +49,7 @@ class VerletListContainer:
         self._counts: dict = {}
         self._stats_cache: dict = {}
         # kernel tuning knobs (csrc/vl.cu lmd_force_vl flags bits 4-6)
-        self.knobs = 0
+        self.knobs = 0x40   # persistent coherent grid, unroll 4 (tools/vl_variants.py)
 
     # ------------------------------------------------------------ protocol
     def needs_rebuild(self, owned) -> bool:
