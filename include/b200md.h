@@ -224,13 +224,15 @@ int lmd_vl_fill(const lmd_grid* g, double rl2, int newton3, int pattern, int64_t
                 const int64_t* tile_off, const int32_t* kmax, int32_t* nbr, void* stream);
 /* Force over the lists: one warp per i-tile, lanes by `pattern`; positions
  * are pos4 over the combined backing plus one sentinel record (256-bit
- * gathers).  newton3 = 0
+ * gathers), or, if soa != NULL, SoA copies x = soa[0..ntot), y, z of the
+ * same ntot records (three 64-bit gathers that share sectors between
+ * neighbouring lanes).  flags bits 4-6 select unroll / grid variants.  newton3 = 0
  * writes f[i]; newton3 = 1 accumulates with FP64 atomics into zeroed f
  * (j-side reactions; summation order is then not deterministic).
  * ev_scratch: 2 * lmd_vl_ev_slots(n_owned, pattern) doubles. */
 int64_t lmd_vl_ev_slots(int64_t n_owned, int pattern);
 int lmd_force_vl(int pattern, int newton3, int flags, const lmd_lj* lj, int64_t n_owned,
-                 const double* pos4, const int64_t* tile_off,
+                 const double* pos4, const double* soa, int64_t ntot, const int64_t* tile_off,
                  const int32_t* kmax, const int32_t* nbr, double* fx, double* fy, double* fz,
                  double* ev_scratch, lmd_stats* stats, void* stream);
 /* KernelStats of a Verlet-list force phase: i-tiles of `a` consecutive owned

@@ -183,9 +183,21 @@ __device__ __forceinline__ void vl_pair(const double4& pi, const double4& pj, in
 // t*A + io.  Indices for U fills are loaded first, then the U positions
 // (256-bit gathers), then the U interactions, so each lane keeps 2U loads in
 // flight.  Writes the tile's i forces; pair counts etc. accumulate in `a`.
-template <int P, bool EV, bool N3, int U>
+struct SoA {
+  const double* __restrict__ x;
+  const double* __restrict__ y;
+  const double* __restrict__ z;
+};
+
+template <bool SOA>
+__device__ __forceinline__ double4 ld_j(const double* __restrict__ pos4, const SoA& q, int j) {
+  if (SOA) return make_double4(__ldg(q.x + j), __ldg(q.y + j), __ldg(q.z + j), 0.0);
+  return ld_pos4(pos4, j);
+}
+
+template <int P, bool EV, bool N3, int U, bool SOA>
 __device__ __forceinline__ void vl_tile(int t, int lane, int n_owned,
-                                        const double* __restrict__ pos4,
+                                        const double* __restrict__ pos4, const SoA& q,
                                         const long long* __restrict__ toff,
                                         const int32_t* __restrict__ kmax,
                                         const int32_t* __restrict__ nbr, const LJK& k, Acc& a,
@@ -208,13 +220,13 @@ __device__ __forceinline__ void vl_tile(int t, int lane, int n_owned,
 #pragma unroll
     for (int u = 0; u < U; ++u) j[u] = __ldg(list + (long long)(s + u) * STRIDE);
 #pragma unroll
-    for (int u = 0; u < U; ++u) pj[u] = ld_pos4(pos4, j[u]);
+    for (int u = 0; u < U; ++u) pj[u] = ld_j<SOA>(pos4, q, j[u]);
 #pragma unroll
     for (int u = 0; u < U; ++u) vl_pair<EV, N3>(pi, pj[u], j[u], n_owned, k, a, fx, fy, fz);
   }
   for (; s < steps; ++s) {
     const int j = __ldg(list + (long long)s * STRIDE);
-    vl_pair<EV, N3>(pi, ld_pos4(pos4, j), j, n_owned, k, a, fx, fy, fz);
+    vl_pair<EV, N3>(pi, ld_j<SOA>(pos4, q, j), j, n_owned, k, a, fx, fy, fz);
   }
   if (!iact) a.ax = a.ay = a.az = 0.0;
   const double rx = reduce_j<P>(a.ax), ry = reduce_j<P>(a.ay), rz = reduce_j<P>(a.az);
@@ -256,9 +268,9 @@ __device__ __forceinline__ void flush_acc(const Acc& a, int lane, bool live, boo
 }
 
 // One warp per i-tile.
-template <int P, bool EV, bool N3, int U>
+template <int P, bool EV, bool N3, int U, bool SOA>
 __global__ void __launch_bounds__(32 * kVLWarps, 4)
-    vl_force_kernel(int n_owned, int ntiles, const double* __restrict__ pos4,
+    vl_force_kernel(int n_owned, int ntiles, const double* __restrict__ pos4, SoA q,
                     const long long* __restrict__ toff, const int32_t* __restrict__ kmax,
                     const int32_t* __restrict__ nbr, LJK k, double* __restrict__ fx,
                     double* __restrict__ fy, double* __restrict__ fz, double* __restrict__ ev,
@@ -266,16 +278,17 @@ __global__ void __launch_bounds__(32 * kVLWarps, 4)
   const int lane = threadIdx.x & 31;
   const int t = blockIdx.x * kVLWarps + (threadIdx.x >> 5);
   Acc a = {0.0, 0.0, 0.0, 0.0, 0.0, 0, 0, 0};
-  if (t < ntiles) vl_tile<P, EV, N3, U>(t, lane, n_owned, pos4, toff, kmax, nbr, k, a, fx, fy, fz);
+  if (t < ntiles)
+    vl_tile<P, EV, N3, U, SOA>(t, lane, n_owned, pos4, q, toff, kmax, nbr, k, a, fx, fy, fz);
   flush_acc(a, lane, t < ntiles, EV, (long long)blockIdx.x * kVLWarps + (threadIdx.x >> 5), ev,
             stats);
 }
 
 // Persistent variant: each block owns a contiguous (spatially coherent) run
 // of tiles, so the j positions its warps gather stay resident in its SM's L1.
-template <int P, bool EV, bool N3, int U>
+template <int P, bool EV, bool N3, int U, bool SOA>
 __global__ void __launch_bounds__(32 * kVLWarps, 4)
-    vl_force_persistent_kernel(int n_owned, int ntiles, const double* __restrict__ pos4,
+    vl_force_persistent_kernel(int n_owned, int ntiles, const double* __restrict__ pos4, SoA q,
                                const long long* __restrict__ toff,
                                const int32_t* __restrict__ kmax, const int32_t* __restrict__ nbr,
                                LJK k, double* __restrict__ fx, double* __restrict__ fy,
@@ -286,7 +299,7 @@ __global__ void __launch_bounds__(32 * kVLWarps, 4)
   const int t0 = blockIdx.x * per, t1 = min(ntiles, t0 + per);
   Acc a = {0.0, 0.0, 0.0, 0.0, 0.0, 0, 0, 0};
   for (int t = t0 + w; t < t1; t += kVLWarps)
-    vl_tile<P, EV, N3, U>(t, lane, n_owned, pos4, toff, kmax, nbr, k, a, fx, fy, fz);
+    vl_tile<P, EV, N3, U, SOA>(t, lane, n_owned, pos4, q, toff, kmax, nbr, k, a, fx, fy, fz);
   flush_acc(a, lane, true, EV, (long long)blockIdx.x * kVLWarps + w, ev, stats);
 }
 
@@ -423,53 +436,55 @@ int64_t lmd_vl_ev_slots(int64_t n_owned, int pattern) {
 
 static int g_persistent_blocks = 0;
 
-template <int P, bool EV, bool N3, int U>
+template <int P, bool EV, bool N3, int U, bool SOA>
 static void launch_vl(bool persistent, int64_t n_owned, int64_t ntiles, const double* pos4,
-                      const int64_t* tile_off, const int32_t* kmax, const int32_t* nbr,
-                      const LJK& k, double* fx, double* fy, double* fz, double* ev,
-                      lmd_stats* stats, cudaStream_t s) {
+                      const SoA& q, const int64_t* tile_off, const int32_t* kmax,
+                      const int32_t* nbr, const LJK& k, double* fx, double* fy, double* fz,
+                      double* ev, lmd_stats* stats, cudaStream_t s) {
   if (persistent) {
     int sms = 148;
     int dev = 0;
     if (cudaGetDevice(&dev) == cudaSuccess)
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, vl_force_persistent_kernel<P, EV, N3, U>,
-                                                  32 * kVLWarps, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per_sm, vl_force_persistent_kernel<P, EV, N3, U, SOA>, 32 * kVLWarps, 0);
     int blocks = sms * (per_sm > 0 ? per_sm : 1);
     if (blocks > 148 * 64) blocks = 148 * 64;
     g_persistent_blocks = blocks;
-    vl_force_persistent_kernel<P, EV, N3, U><<<blocks, 32 * kVLWarps, 0, s>>>(
-        (int)n_owned, (int)ntiles, pos4, (const long long*)tile_off, kmax, nbr, k, fx, fy, fz, ev,
-        stats);
+    vl_force_persistent_kernel<P, EV, N3, U, SOA><<<blocks, 32 * kVLWarps, 0, s>>>(
+        (int)n_owned, (int)ntiles, pos4, q, (const long long*)tile_off, kmax, nbr, k, fx, fy, fz,
+        ev, stats);
   } else {
     const unsigned blocks = (unsigned)cdiv(ntiles, kVLWarps);
-    vl_force_kernel<P, EV, N3, U><<<blocks, 32 * kVLWarps, 0, s>>>(
-        (int)n_owned, (int)ntiles, pos4, (const long long*)tile_off, kmax, nbr, k, fx, fy, fz, ev,
-        stats);
+    vl_force_kernel<P, EV, N3, U, SOA><<<blocks, 32 * kVLWarps, 0, s>>>(
+        (int)n_owned, (int)ntiles, pos4, q, (const long long*)tile_off, kmax, nbr, k, fx, fy, fz,
+        ev, stats);
   }
 }
 
 template <int P, bool EV, bool N3>
-static void launch_vl_u(int u, bool persistent, int64_t n_owned, int64_t ntiles,
-                        const double* pos4, const int64_t* tile_off, const int32_t* kmax,
-                        const int32_t* nbr, const LJK& k, double* fx, double* fy, double* fz,
-                        double* ev, lmd_stats* stats, cudaStream_t s) {
-  if (u == 1)
-    launch_vl<P, EV, N3, 1>(persistent, n_owned, ntiles, pos4, tile_off, kmax, nbr, k, fx, fy, fz,
-                            ev, stats, s);
-  else if (u == 2)
-    launch_vl<P, EV, N3, 2>(persistent, n_owned, ntiles, pos4, tile_off, kmax, nbr, k, fx, fy, fz,
-                            ev, stats, s);
-  else
-    launch_vl<P, EV, N3, 4>(persistent, n_owned, ntiles, pos4, tile_off, kmax, nbr, k, fx, fy, fz,
-                            ev, stats, s);
+static void launch_vl_u(int u, bool persistent, bool soa, int64_t n_owned, int64_t ntiles,
+                        const double* pos4, const SoA& q, const int64_t* tile_off,
+                        const int32_t* kmax, const int32_t* nbr, const LJK& k, double* fx,
+                        double* fy, double* fz, double* ev, lmd_stats* stats, cudaStream_t s) {
+#define LMD_VLU(UU, SS)                                                                          \
+  launch_vl<P, EV, N3, UU, SS>(persistent, n_owned, ntiles, pos4, q, tile_off, kmax, nbr, k, fx, \
+                               fy, fz, ev, stats, s)
+  if (soa) {
+    if (u == 2) LMD_VLU(2, true);
+    else LMD_VLU(4, true);
+  } else {
+    if (u == 2) LMD_VLU(2, false);
+    else LMD_VLU(4, false);
+  }
+#undef LMD_VLU
 }
 
 extern "C" {
 
 int lmd_force_vl(int pattern, int newton3, int flags, const lmd_lj* lj, int64_t n_owned,
-                 const double* pos4, const int64_t* tile_off,
+                 const double* pos4, const double* soa, int64_t ntot, const int64_t* tile_off,
                  const int32_t* kmax, const int32_t* nbr, double* fx, double* fy, double* fz,
                  double* ev_scratch, lmd_stats* stats, void* stream) {
   if (n_owned <= 0) return LMD_OK;
@@ -477,13 +492,14 @@ int lmd_force_vl(int pattern, int newton3, int flags, const lmd_lj* lj, int64_t 
   const int64_t ntiles = lmd_vl_num_tiles(n_owned, pattern);
   cudaStream_t s = (cudaStream_t)stream;
   const bool ev = (flags & LMD_FLAG_ENERGY) != 0;
-  // tuning knobs: bits 4-5 unroll (0 -> 4, 1 -> 1, 2 -> 2), bit 6 persistent grid
-  const int ucode = (flags >> 4) & 3;
-  const int u = ucode == 1 ? 1 : ucode == 2 ? 2 : 4;
+  // tuning knobs: bits 4-5 unroll (2 -> 2, else 4), bit 6 persistent grid;
+  // soa != NULL gathers x, y, z from SoA arrays soa[0..ntot), soa[ntot..), ...
+  const int u = ((flags >> 4) & 3) == 2 ? 2 : 4;
   const bool persistent = (flags >> 6) & 1;
+  const SoA q = {soa, soa ? soa + ntot : nullptr, soa ? soa + 2 * ntot : nullptr};
 #define LMD_VL(P, EVB, N3B)                                                                  \
-  launch_vl_u<P, EVB, N3B>(u, persistent, n_owned, ntiles, pos4, tile_off, kmax, nbr, k, fx, \
-                           fy, fz, ev_scratch, stats, s)
+  launch_vl_u<P, EVB, N3B>(u, persistent, soa != nullptr, n_owned, ntiles, pos4, q, tile_off,  \
+                           kmax, nbr, k, fx, fy, fz, ev_scratch, stats, s)
 #define LMD_VL_P(P)                         \
   do {                                      \
     if (ev) {                               \

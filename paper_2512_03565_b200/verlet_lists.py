@@ -50,6 +50,7 @@ class VerletListContainer:
         self._stats_cache: dict = {}
         # kernel tuning knobs (csrc/vl.cu lmd_force_vl flags bits 4-6)
         self.knobs = 0x40   # persistent coherent grid, unroll 4 (tools/vl_variants.py)
+        self.use_soa = True  # gather SoA x, y, z (sector sharing) instead of pos4
 
     # ------------------------------------------------------------ protocol
     def needs_rebuild(self, owned) -> bool:
@@ -94,9 +95,12 @@ class VerletListContainer:
             self._h_count.zero_()
             self._halo_owner = torch.zeros(0, dtype=torch.int32, device=dev)
             self._halo_shift = torch.zeros(0, dtype=torch.int8, device=dev)
+        self._soa = torch.empty((3, n + nh + 1), dtype=torch.float64, device=dev)
+        self._soa[:, -1] = SENTINEL_POSITION
         self._fx = torch.zeros(max(n, 1), dtype=torch.float64, device=dev)
         self._fy = torch.zeros(max(n, 1), dtype=torch.float64, device=dev)
         self._fz = torch.zeros(max(n, 1), dtype=torch.float64, device=dev)
+        self._load_positions(d)
         self._lists.clear()
         self._counts.clear()
         self._stats_cache.clear()
@@ -107,6 +111,15 @@ class VerletListContainer:
     def _load_positions(self, d) -> None:
         n, nh = self.n_owned, self.n_halo
         s = N.stream()
+        ntot = n + nh + 1
+        sx, sy, sz = self._soa[0], self._soa[1], self._soa[2]
+        if n:
+            N.call("lmd_gather_soa", n, N.ptr(self._perm), N.ptr(d.pos_x), N.ptr(d.pos_y),
+                   N.ptr(d.pos_z), N.ptr(sx), N.ptr(sy), N.ptr(sz), s)
+        if nh:
+            N.call("lmd_halo_refresh_soa", N.make_box(self.box), nh, N.ptr(self._halo_owner),
+                   N.ptr(self._halo_shift), N.ptr(d.pos_x), N.ptr(d.pos_y), N.ptr(d.pos_z),
+                   N.ptr(sx[n:]), N.ptr(sy[n:]), N.ptr(sz[n:]), s)
         if n:
             N.call("lmd_gather_pos4", n, N.ptr(self._perm), N.ptr(d.pos_x), N.ptr(d.pos_y),
                    N.ptr(d.pos_z), None, float(OWNED), N.ptr(self._pos4), s)
@@ -215,6 +228,7 @@ class VerletListContainer:
             self._fz.zero_()
         N.call("lmd_force_vl", pattern.code, int(newton3), (N.FLAG_ENERGY if energy else 0) | self.knobs,
                N.make_lj(self.params), self.n_owned, N.ptr(self._pos4),
+               N.ptr(self._soa) if self.use_soa else None, self._soa.shape[1],
                N.ptr(tile_off), N.ptr(kmax), N.ptr(nbr), N.ptr(self._fx),
                N.ptr(self._fy), N.ptr(self._fz), N.ptr(ev_t), N.ptr(stats_t), N.stream())
         return stats_t

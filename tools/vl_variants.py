@@ -20,9 +20,10 @@ patterns = os.environ.get("PATTERNS", "v_by_one,half_by_two").split(",")
 for pname in patterns:
     pat = B.PatternKind(pname)
     for n3 in (False,):
-        for ucode, u in ((1, 1), (2, 2), (0, 4)):
+        for ucode, u, soa in ((2, 2, 0), (0, 4, 0), (2, 2, 1), (0, 4, 1)):
             for pers in (0, 1):
                 cont.knobs = (ucode << 4) | (pers << 6)
+                cont.use_soa = bool(soa)
                 st = cont.launch_force(pat, n3)
                 ts = []
                 for _ in range(6):
@@ -36,5 +37,5 @@ for pname in patterns:
                     ts.append(e0.elapsed_time(e1))
                 from paper_2512_03565_b200 import _native as N
                 s = N.read_stats(st)
-                print(f"{pname:12s} n3={int(n3)} U={u} persistent={pers}  {min(ts)*1e3:8.1f} us  "
+                print(f"{pname:12s} n3={int(n3)} U={u} soa={soa} persistent={pers}  {min(ts)*1e3:8.1f} us  "
                       f"pairs={s.pair_interactions}", flush=True)
