@@ -49,8 +49,8 @@ class VerletListContainer:
         self._counts: dict = {}
         self._stats_cache: dict = {}
         # kernel tuning knobs (csrc/vl.cu lmd_force_vl flags bits 4-6)
-        self.knobs = 0x40   # persistent coherent grid, unroll 4 (tools/vl_variants.py)
-        self.use_soa = True  # gather SoA x, y, z (sector sharing) instead of pos4
+        self.knobs = 0      # unroll 4, one warp per tile (tools/vl_variants.py)
+        self.use_soa = False  # True: gather SoA x, y, z instead of 256-bit pos4
 
     # ------------------------------------------------------------ protocol
     def needs_rebuild(self, owned) -> bool:
