@@ -240,6 +240,47 @@ int lmd_force_vl(int pattern, int newton3, int flags, const lmd_lj* lj, int64_t 
 int lmd_vl_stats(int64_t n_owned, int a, int b, int vector_width, const int32_t* count,
                  lmd_stats* stats, void* stream);
 
+/* --------------------------------------------- K5-K7 Verlet cluster lists */
+/* VerletClusterContainer (containers.py:302-479) on the device.  Build:
+ * lmd_vcl_order (column key cx + width*cy, lexsort((z, col)) as two stable
+ * radix sorts), lmd_vcl_chunk (M-slot clusters per column; synchronises to
+ * return the cluster count), lmd_vcl_backing (padded pos4 with dummies parked
+ * at the AABB minimum), lmd_vcl_column_table, lmd_vcl_pairs (AABB gap^2 <=
+ * limit, binned; ascending ids).  Force: lmd_force_vcl (warp per owned
+ * cluster over itself, its owned list and its halo links; Newton3 off).
+ * Stats: lmd_vcl_stats (units of traversals.py:244-266). */
+size_t lmd_vcl_temp_bytes(int64_t n);
+int lmd_vcl_order(int64_t n, const double* x, const double* y, const double* z, double lo0,
+                  double lo1, double col, int64_t width, int32_t* colkey, int32_t* ckey2,
+                  uint64_t* zkey, uint64_t* zkey2, int32_t* tmp_idx, int32_t* order,
+                  int32_t* sorted_colkey, void* temp, size_t temp_bytes, void* stream);
+int lmd_vcl_chunk(int64_t n, int M, const int32_t* sorted_colkey, int32_t* flag, int32_t* run_id,
+                  int32_t* run_start, int32_t* run_nclu, int32_t* run_coff, int32_t* slot,
+                  int32_t* cluster_key, int64_t* ncl_out, void* temp, size_t temp_bytes,
+                  void* stream);
+int lmd_vcl_backing(int64_t n, int64_t ncl, int M, const int32_t* order, const int32_t* slot,
+                    const double* x, const double* y, const double* z, double own_value,
+                    double* pos4, double* amin, double* amax, void* stream);
+int lmd_vcl_column_table(int64_t ncl, const int32_t* cluster_key, int32_t* tbeg, int32_t* tend,
+                         int64_t tsize, void* stream);
+int lmd_vcl_pairs(int64_t ncl, const int32_t* cluster_key, const double* amin, const double* amax,
+                  const double* bmin, const double* bmax, const int32_t* tbeg,
+                  const int32_t* tend, int64_t width, int64_t tsize, int exclude_self, double rl,
+                  double limit, int32_t* count, int32_t* n3count, const int64_t* off,
+                  int32_t* list, void* stream);
+int64_t lmd_vcl_ev_slots(int64_t ncl);
+int lmd_force_vcl(int64_t ncl, int M, int flags, const lmd_lj* lj, const double* pos4,
+                  const int64_t* off, const int32_t* nlist, const int32_t* list,
+                  const int64_t* hoff, const int32_t* hnlist, const int32_t* hlist, double* fx,
+                  double* fy, double* fz, double* ev_scratch, lmd_stats* stats, void* stream);
+int lmd_vcl_stats(int64_t ncl, int M, int newton3, int a, int b, int vector_width,
+                  const double* pos4, const int64_t* off, const int32_t* nlist,
+                  const int32_t* n3count, const int32_t* list, const int64_t* hoff,
+                  const int32_t* hcount, const int32_t* hlist, lmd_stats* stats, void* stream);
+int lmd_vcl_collect(int64_t n, const int32_t* order, const int32_t* slot, const double* fx,
+                    const double* fy, const double* fz, double* ox, double* oy, double* oz,
+                    void* stream);
+
 /* ------------------------------------------------ the functor (two buffers) */
 /* compute_pair_vectorized (kernels.py:377-424) on device buffers given as
  * pos4 (ownership in .w).  Forces ACCUMULATE (+=) into the SoA force arrays.

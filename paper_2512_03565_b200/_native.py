@@ -148,6 +148,17 @@ _sig("lmd_vl_ev_slots", _I64, _I64, _INT)
 _sig("lmd_force_vl", _INT, _INT, _INT, _INT, C.POINTER(LJ), _I64, _VP, _VP, _I64, _VP, _VP,
      _VP, _VP, _VP, _VP, _VP, _VP, _VP)
 _sig("lmd_vl_stats", _INT, _I64, _INT, _INT, _INT, _VP, _VP, _VP)
+_sig("lmd_vcl_temp_bytes", _SZ, _I64)
+_sig("lmd_vcl_order", _INT, _I64, _VP, _VP, _VP, _D, _D, _D, _I64, *([_VP] * 8), _VP, _SZ, _VP)
+_sig("lmd_vcl_chunk", _INT, _I64, _INT, *([_VP] * 9), C.POINTER(_I64), _VP, _SZ, _VP)
+_sig("lmd_vcl_backing", _INT, _I64, _I64, _INT, _VP, _VP, _VP, _VP, _VP, _D, _VP, _VP, _VP, _VP)
+_sig("lmd_vcl_column_table", _INT, _I64, _VP, _VP, _VP, _I64, _VP)
+_sig("lmd_vcl_pairs", _INT, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _I64, _I64, _INT, _D, _D,
+     _VP, _VP, _VP, _VP, _VP)
+_sig("lmd_vcl_ev_slots", _I64, _I64)
+_sig("lmd_force_vcl", _INT, _I64, _INT, _INT, C.POINTER(LJ), *([_VP] * 13), _VP)
+_sig("lmd_vcl_stats", _INT, _I64, _INT, _INT, _INT, _INT, _INT, *([_VP] * 8), _VP, _VP)
+_sig("lmd_vcl_collect", _INT, _I64, *([_VP] * 8), _VP)
 _sig("lmd_scatter_forces", _INT, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP)
 
 
@@ -203,3 +214,8 @@ def new_stats(device) -> torch.Tensor:
 def read_stats(t: torch.Tensor) -> Stats:
     raw = t.cpu().numpy().tobytes()
     return Stats.from_buffer_copy(raw)
+
+
+def I64_out() -> C.c_int64:
+    """An int64 out-parameter (passed by reference through POINTER argtypes)."""
+    return C.c_int64(0)

@@ -1,0 +1,313 @@
+"""Verlet cluster lists on the device (VerletClusterContainer, containers.py:302-479).
+
+Clusters follow the reference exactly: x-y columns of side rc + skin, each
+column sorted by z (``np.lexsort((z, col))``) and chunked into M-slot
+clusters, the last one dummy-padded with its dummies parked at the AABB
+minimum.  Cluster pairs are those whose AABB gap^2 <= (rc+skin)^2, found by a
+binned search (K6) instead of the reference's dense O(C^2) matrix.  Halo
+clusters and halo links are re-derived on every ``refresh`` as the reference
+does; the owned lists stay fixed between rebuilds.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .containers import _check_all_owned, device_soa, needs_rebuild
+from .domain import as_box, build_halo
+from .errors import ConfigurationError, ParticleOverlapError
+from .kernels import KernelStats, as_pattern, validate_vector_width
+from .particles import DUMMY, HALO, OWNED, ParticleBuffer
+
+REBUILD_PERIOD_DEFAULT = 20
+
+
+@dataclass
+class Cluster:
+    """Fixed-size particle group (containers.py:201-213), as a host view."""
+
+    cluster_id: int
+    buffer: object
+    aabb_min: np.ndarray
+    aabb_max: np.ndarray
+    n_real: int
+
+    @property
+    def size(self) -> int:
+        return len(self.buffer)
+
+
+class _Clustered:
+    """Device clustering of one particle set (owned or halo)."""
+
+    def __init__(self, n, M, dev):
+        self.n = n
+        self.M = M
+        self.ncl = 0
+        self.order = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        self.slot = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        self.ckey = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+
+
+def _cluster(x, y, z, box, col, width, M, dev) -> _Clustered:
+    n = int(x.shape[0])
+    out = _Clustered(n, M, dev)
+    if n == 0:
+        return out
+    L = N.load()
+    tb = int(L.lmd_vcl_temp_bytes(n))
+    temp = torch.empty(max(tb, 1), dtype=torch.uint8, device=dev)
+    i32 = lambda: torch.empty(n, dtype=torch.int32, device=dev)  # noqa: E731
+    colkey, ckey2, tmp_idx, sorted_key = i32(), i32(), i32(), i32()
+    zkey = torch.empty(n, dtype=torch.int64, device=dev)
+    zkey2 = torch.empty(n, dtype=torch.int64, device=dev)
+    s = N.stream()
+    N.call("lmd_vcl_order", n, N.ptr(x), N.ptr(y), N.ptr(z), float(box.min[0]), float(box.min[1]),
+           float(col), int(width), N.ptr(colkey), N.ptr(ckey2), N.ptr(zkey), N.ptr(zkey2),
+           N.ptr(tmp_idx), N.ptr(out.order), N.ptr(sorted_key), N.ptr(temp), tb, s)
+    flag, run_id, run_start, run_nclu, run_coff = i32(), i32(), i32(), i32(), i32()
+    ncl = N.I64_out()
+    N.call("lmd_vcl_chunk", n, M, N.ptr(sorted_key), N.ptr(flag), N.ptr(run_id), N.ptr(run_start),
+           N.ptr(run_nclu), N.ptr(run_coff), N.ptr(out.slot), N.ptr(out.ckey), ncl, N.ptr(temp),
+           tb, s)
+    out.ncl = int(ncl.value)
+    out.ckey = out.ckey[: out.ncl].contiguous()
+    return out
+
+
+class VerletClusterContainer:
+    """Cluster-list container on the GPU: owned clusters plus per-refresh halo clusters."""
+
+    kind = "vcl"
+
+    def __init__(self, box, params, cluster_size: int,
+                 rebuild_period: int = REBUILD_PERIOD_DEFAULT, device=None):
+        if cluster_size < 2:
+            raise ConfigurationError(f"cluster size must be >= 2, got {cluster_size}")
+        self.box = as_box(box)
+        self.params = params
+        self.cluster_size = int(cluster_size)
+        self.rebuild_period = rebuild_period
+        self.column_length = params.interaction_length
+        self.device = torch.device(device) if device is not None else (
+            torch.device("cuda") if torch.cuda.is_available() else torch.device("cpu"))
+        L = self.box.lengths
+        self.width = int(L[0] / self.column_length) + 4            # containers.py:340
+        self.height = int(L[1] / self.column_length) + 4
+        self.tsize = self.width * self.height
+        self.reference_positions = None
+        self.steps_since_rebuild = 0
+        self.structure_version = 0
+        self._own = None
+        self._stats_cache: dict = {}
+
+    # ------------------------------------------------------------ protocol
+    def needs_rebuild(self, owned) -> bool:
+        d = device_soa(owned)
+        return needs_rebuild(d.positions(), self.reference_positions, self.params.skin,
+                             self.steps_since_rebuild, self.rebuild_period)
+
+    def _table(self, cl: _Clustered, dev):
+        tbeg = torch.zeros(self.tsize, dtype=torch.int32, device=dev)
+        tend = torch.zeros(self.tsize, dtype=torch.int32, device=dev)
+        N.call("lmd_vcl_column_table", cl.ncl, N.ptr(cl.ckey), N.ptr(tbeg), N.ptr(tend),
+               self.tsize, N.stream())
+        return tbeg, tend
+
+    def _lists(self, a_min, a_max, b_min, b_max, tbeg, tend, exclude_self, want_n3, dev):
+        ncl = self._own.ncl
+        rl = self.params.interaction_length
+        limit = rl * rl                                   # containers.py:291
+        count = torch.zeros(max(ncl, 1), dtype=torch.int32, device=dev)
+        n3 = torch.zeros(max(ncl, 1), dtype=torch.int32, device=dev) if want_n3 else None
+        s = N.stream()
+        N.call("lmd_vcl_pairs", ncl, N.ptr(self._own.ckey), N.ptr(a_min), N.ptr(a_max),
+               N.ptr(b_min), N.ptr(b_max), N.ptr(tbeg), N.ptr(tend), self.width, self.tsize,
+               int(exclude_self), float(rl), float(limit), N.ptr(count), N.ptr(n3), None, None, s)
+        c64 = count[:ncl].to(torch.int64)
+        off = torch.zeros(max(ncl, 1), dtype=torch.int64, device=dev)
+        if ncl > 1:
+            off[1:ncl] = torch.cumsum(c64, 0)[:-1]
+        total = int(c64.sum().item()) if ncl else 0
+        lst = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
+        if total:
+            N.call("lmd_vcl_pairs", ncl, N.ptr(self._own.ckey), N.ptr(a_min), N.ptr(a_max),
+                   N.ptr(b_min), N.ptr(b_max), N.ptr(tbeg), N.ptr(tend), self.width, self.tsize,
+                   int(exclude_self), float(rl), float(limit), N.ptr(count), None, N.ptr(off),
+                   N.ptr(lst), s)
+        return count, n3, off, lst
+
+    def rebuild(self, owned) -> None:
+        d = device_soa(owned)
+        _check_all_owned(d)
+        dev = d.device
+        M = self.cluster_size
+        self._own = _cluster(d.pos_x, d.pos_y, d.pos_z, self.box, self.column_length, self.width,
+                             M, dev)
+        self._owned_pos4 = torch.empty((max(self._own.ncl * M, 1), 4), dtype=torch.float64,
+                                       device=dev)
+        ncl = self._own.ncl
+        self._amin = torch.empty((max(ncl, 1), 3), dtype=torch.float64, device=dev)
+        self._amax = torch.empty((max(ncl, 1), 3), dtype=torch.float64, device=dev)
+        self._load_owned(d)
+        self._tbeg, self._tend = self._table(self._own, dev)
+        self._count, self._n3count, self._off, self._list = self._lists(
+            self._amin, self._amax, self._amin, self._amax, self._tbeg, self._tend, True, True,
+            dev)
+        self.reference_positions = d.positions().clone()
+        self.steps_since_rebuild = 0
+        self.structure_version += 1
+        self._stats_cache.clear()
+        self._halo_ready = False
+
+    def _load_owned(self, d) -> None:
+        M = self.cluster_size
+        N.call("lmd_vcl_backing", self._own.n, self._own.ncl, M, N.ptr(self._own.order),
+               N.ptr(self._own.slot), N.ptr(d.pos_x), N.ptr(d.pos_y), N.ptr(d.pos_z),
+               float(OWNED), N.ptr(self._owned_pos4), N.ptr(self._amin), N.ptr(self._amax),
+               N.stream())
+
+    def refresh(self, owned, halo=None) -> None:
+        """Reload positions into the clusters, recompute the AABBs (dummies
+        re-parked) and re-derive the halo clusters and links (containers.py:431-469)."""
+        if self._own is None:
+            raise ConfigurationError("cluster container has not been rebuilt")
+        d = device_soa(owned)
+        dev = d.device
+        M = self.cluster_size
+        self._load_owned(d)
+        if halo is None:
+            halo = build_halo(d, self.box, self.params.interaction_length)
+        h = device_soa(halo, dev)
+        self._hal = _cluster(h.pos_x, h.pos_y, h.pos_z, self.box, self.column_length, self.width,
+                             M, dev)
+        nh = self._hal.ncl
+        ncl = self._own.ncl
+        self._pos4 = torch.empty(((ncl + nh) * M + 1, 4), dtype=torch.float64, device=dev)
+        self._pos4[: ncl * M] = self._owned_pos4[: ncl * M]
+        self._hmin = torch.empty((max(nh, 1), 3), dtype=torch.float64, device=dev)
+        self._hmax = torch.empty((max(nh, 1), 3), dtype=torch.float64, device=dev)
+        if nh:
+            N.call("lmd_vcl_backing", self._hal.n, nh, M, N.ptr(self._hal.order),
+                   N.ptr(self._hal.slot), N.ptr(h.pos_x), N.ptr(h.pos_y), N.ptr(h.pos_z),
+                   float(HALO), N.ptr(self._pos4[ncl * M:]), N.ptr(self._hmin), N.ptr(self._hmax),
+                   N.stream())
+            htb, hte = self._table(self._hal, dev)
+            self._hcount, _, self._hoff, self._hlist = self._lists(
+                self._amin, self._amax, self._hmin, self._hmax, htb, hte, False, False, dev)
+        else:
+            self._hcount = torch.zeros(max(ncl, 1), dtype=torch.int32, device=dev)
+            self._hoff = torch.zeros(max(ncl, 1), dtype=torch.int64, device=dev)
+            self._hlist = torch.zeros(1, dtype=torch.int32, device=dev)
+        n = self._own.ncl * M
+        self._fx = torch.zeros(max(n, 1), dtype=torch.float64, device=dev)
+        self._fy = torch.zeros(max(n, 1), dtype=torch.float64, device=dev)
+        self._fz = torch.zeros(max(n, 1), dtype=torch.float64, device=dev)
+        self.structure_version += 1
+        self._stats_cache.clear()
+        self._halo_ready = True
+
+    # --------------------------------------------------------------- views
+    @property
+    def n_clusters(self) -> int:
+        return self._own.ncl if self._own else 0
+
+    @property
+    def neighbor_lists(self) -> dict:
+        """{newton3: list of neighbour-id lists} as in containers.py:421-426 (host copy)."""
+        off = self._off.cpu().numpy()
+        cnt = self._count.cpu().numpy()
+        lst = self._list.cpu().numpy()
+        full = [lst[off[k]:off[k] + cnt[k]].tolist() for k in range(self.n_clusters)]
+        return {False: full, True: [[z for z in zs if z > k] for k, zs in enumerate(full)]}
+
+    @property
+    def halo_links(self) -> list:
+        off = self._hoff.cpu().numpy()
+        cnt = self._hcount.cpu().numpy()
+        lst = self._hlist.cpu().numpy()
+        return [lst[off[k]:off[k] + cnt[k]].tolist() for k in range(self.n_clusters)]
+
+    def structure(self) -> dict:
+        """perm / slots / real counts / AABBs / padded positions (host copies)."""
+        M = self.cluster_size
+        ncl = self.n_clusters
+        slots = self._own.slot[: self._own.n].cpu().numpy().astype(np.int64)
+        counts = np.bincount(slots // M, minlength=ncl)
+        return dict(perm=self._own.order[: self._own.n].cpu().numpy().astype(np.int64),
+                    slots=slots, counts=counts,
+                    aabb_min=self._amin[:ncl].cpu().numpy(), aabb_max=self._amax[:ncl].cpu().numpy(),
+                    padded=self._owned_pos4[: ncl * M, :3].cpu().numpy())
+
+    # ---------------------------------------------------------------- force
+    def launch_force(self, energy: bool = False, stats_t=None, ev_t=None):
+        if not self._halo_ready:
+            raise ConfigurationError("cluster container has not been refreshed")
+        dev = self._pos4.device
+        if stats_t is None:
+            stats_t = N.new_stats(dev)
+        else:
+            stats_t.zero_()
+        ncl = self._own.ncl
+        if ev_t is None:
+            ev_t = torch.empty(2 * max(int(N.load().lmd_vcl_ev_slots(ncl)), 1),
+                               dtype=torch.float64, device=dev)
+        N.call("lmd_force_vcl", ncl, self.cluster_size, N.FLAG_ENERGY if energy else 0,
+               N.make_lj(self.params), N.ptr(self._pos4), N.ptr(self._off), N.ptr(self._count),
+               N.ptr(self._list), N.ptr(self._hoff), N.ptr(self._hcount), N.ptr(self._hlist),
+               N.ptr(self._fx), N.ptr(self._fy), N.ptr(self._fz), N.ptr(ev_t), N.ptr(stats_t),
+               N.stream())
+        return stats_t
+
+    def vcl_stats(self, newton3: bool, pattern, V: int):
+        key = (self.structure_version, bool(newton3), pattern, V)
+        hit = self._stats_cache.get(key)
+        if hit is None:
+            a, b = pattern.shape(V)
+            t = N.new_stats(self._pos4.device)
+            N.call("lmd_vcl_stats", self._own.ncl, self.cluster_size, int(newton3), a, b, V,
+                   N.ptr(self._pos4), N.ptr(self._off), N.ptr(self._count), N.ptr(self._n3count),
+                   N.ptr(self._list), N.ptr(self._hoff), N.ptr(self._hcount), N.ptr(self._hlist),
+                   N.ptr(t), N.stream())
+            st = N.read_stats(t)
+            hit = (int(st.kernel_invocations), int(st.lane_slots), int(st.useful_interactions))
+            self._stats_cache[key] = hit
+        return hit
+
+    def compute_forces(self, traversal, newton3: bool, pattern, vector_width: int,
+                       energy: bool = False) -> KernelStats:
+        from .traversals import TraversalKind, as_traversal
+        validate_vector_width(vector_width)
+        if as_traversal(traversal) is not TraversalKind.VCL:
+            raise ConfigurationError(f"{traversal} traversal requires linked cells")
+        pattern = as_pattern(pattern)
+        inv, slots, useful = self.vcl_stats(newton3, pattern, vector_width)
+        st = N.read_stats(self.launch_force(energy))
+        if st.overlap:
+            raise ParticleOverlapError("zero distance between interacting particles")
+        pairs = int(st.pair_interactions)
+        if newton3:
+            oh = int(st.pairs_owned_halo)
+            pairs = (pairs - oh) // 2 + oh
+        return KernelStats(kernel_invocations=inv, lane_slots=slots, useful_interactions=useful,
+                           pair_interactions=pairs, epot=st.epot, virial=st.virial)
+
+    def collect_forces(self, owned) -> None:
+        d = device_soa(owned)
+        n = self._own.n
+        if n:
+            N.call("lmd_vcl_collect", n, N.ptr(self._own.order), N.ptr(self._own.slot),
+                   N.ptr(self._fx), N.ptr(self._fy), N.ptr(self._fz), N.ptr(d.force_x),
+                   N.ptr(d.force_y), N.ptr(d.force_z), N.stream())
+        if d is not owned:
+            for name in ("force_x", "force_y", "force_z"):
+                dst = getattr(owned, name)
+                val = getattr(d, name)
+                if isinstance(dst, torch.Tensor):
+                    dst.copy_(val.to(dst.device))
+                else:
+                    dst[...] = val.cpu().numpy()
