@@ -76,6 +76,19 @@ def declared_symbols() -> list[str]:
     return _parse_header()
 
 
+def declared_arity() -> dict[str, int]:
+    """Parameter count of every function the public header declares."""
+    hdr = os.path.join(_build.ROOT, "include", "b200md.h")
+    with open(hdr, encoding="utf-8") as fh:
+        text = fh.read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    out = {}
+    for m in re.finditer(r"\b(lmd_[a-z0-9_]+)\s*\(([^)]*)\)\s*;", text):
+        params = m.group(2).strip()
+        out[m.group(1)] = 0 if params in ("", "void") else params.count(",") + 1
+    return out
+
+
 _lib: C.CDLL | None = None
 
 
@@ -149,14 +162,14 @@ _sig("lmd_force_vl", _INT, _INT, _INT, _INT, C.POINTER(LJ), _I64, _VP, _VP, _I64
      _VP, _VP, _VP, _VP, _VP, _VP, _VP)
 _sig("lmd_vl_stats", _INT, _I64, _INT, _INT, _INT, _VP, _VP, _VP)
 _sig("lmd_vcl_temp_bytes", _SZ, _I64)
-_sig("lmd_vcl_order", _INT, _I64, _VP, _VP, _VP, _D, _D, _D, _I64, *([_VP] * 8), _VP, _SZ, _VP)
-_sig("lmd_vcl_chunk", _INT, _I64, _INT, *([_VP] * 9), C.POINTER(_I64), _VP, _SZ, _VP)
+_sig("lmd_vcl_order", _INT, _I64, _VP, _VP, _VP, _D, _D, _D, _I64, *([_VP] * 8), _SZ, _VP)
+_sig("lmd_vcl_chunk", _INT, _I64, _INT, *([_VP] * 8), C.POINTER(_I64), _VP, _SZ, _VP)
 _sig("lmd_vcl_backing", _INT, _I64, _I64, _INT, _VP, _VP, _VP, _VP, _VP, _D, _VP, _VP, _VP, _VP)
 _sig("lmd_vcl_column_table", _INT, _I64, _VP, _VP, _VP, _I64, _VP)
 _sig("lmd_vcl_pairs", _INT, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _I64, _I64, _INT, _D, _D,
      _VP, _VP, _VP, _VP, _VP)
 _sig("lmd_vcl_ev_slots", _I64, _I64)
-_sig("lmd_force_vcl", _INT, _I64, _INT, _INT, C.POINTER(LJ), *([_VP] * 13), _VP)
+_sig("lmd_force_vcl", _INT, _I64, _INT, _INT, C.POINTER(LJ), *([_VP] * 12), _VP)
 _sig("lmd_vcl_stats", _INT, _I64, _INT, _INT, _INT, _INT, _INT, *([_VP] * 8), _VP, _VP)
 _sig("lmd_vcl_collect", _INT, _I64, *([_VP] * 8), _VP)
 _sig("lmd_scatter_forces", _INT, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP)

@@ -24,6 +24,14 @@ def test_library_exports_every_declared_symbol():
     assert set(names) <= set(N._SIGNATURES)
 
 
+def test_binding_arity_matches_header():
+    arity = N.declared_arity()
+    assert set(arity) == set(N.declared_symbols())
+    bad = {name: (arity[name], len(N._SIGNATURES[name][1])) for name in arity
+           if arity[name] != len(N._SIGNATURES[name][1])}
+    assert bad == {}
+
+
 def test_version_and_status_strings():
     lib = N.load()
     assert lib.lmd_version() >= 1
