@@ -58,7 +58,12 @@ class VerletListContainer:
         return needs_rebuild(d.positions(), self.reference_positions, self.params.skin,
                              self.steps_since_rebuild, self.rebuild_period)
 
-    def rebuild(self, owned) -> None:
+    def rebuild(self, owned, halo=None) -> None:
+        """Bin the owned particles and their images and drop the lists.
+
+        ``halo=None`` derives the periodic images on the device (K9).  A
+        domain decomposition passes its ghost layer instead; later refreshes
+        must then pass the ghosts again, in the same order."""
         d = device_soa(owned)
         _check_all_owned(d)
         dev = d.device
@@ -73,7 +78,11 @@ class VerletListContainer:
         s = N.stream()
         self._perm = self._sorter.bin(self.grid, 0, d.pos_x, d.pos_y, d.pos_z, 0,
                                       self._o_start, self._o_count)
-        halo = build_halo(d, self.box, self.params.interaction_length)
+        self._external_halo = halo is not None
+        if halo is None:
+            halo = build_halo(d, self.box, self.params.interaction_length)
+        else:
+            halo = device_soa(halo, dev)
         nh = len(halo)
         self.n_owned, self.n_halo = n, nh
         # combined backing [owned | images | sentinel] as pos4 (32 B records)
@@ -87,9 +96,11 @@ class VerletListContainer:
                                      self._h_start, self._h_count)
             N.call("lmd_gather_pos4", nh, N.ptr(hperm), N.ptr(halo.pos_x), N.ptr(halo.pos_y),
                    N.ptr(halo.pos_z), None, float(HALO), N.ptr(self._pos4[n:]), s)
-            hp = hperm.long()
-            self._halo_owner = halo.extra["owner"][hp].contiguous()
-            self._halo_shift = halo.extra["shift"][hp].contiguous()
+            self._hperm = hperm
+            if not self._external_halo:
+                hp = hperm.long()
+                self._halo_owner = halo.extra["owner"][hp].contiguous()
+                self._halo_shift = halo.extra["shift"][hp].contiguous()
         else:
             self._h_start.zero_()
             self._h_count.zero_()
@@ -100,7 +111,7 @@ class VerletListContainer:
         self._fx = torch.zeros(max(n, 1), dtype=torch.float64, device=dev)
         self._fy = torch.zeros(max(n, 1), dtype=torch.float64, device=dev)
         self._fz = torch.zeros(max(n, 1), dtype=torch.float64, device=dev)
-        self._load_positions(d)
+        self._load_positions(d, halo if self._external_halo else None)
         self._lists.clear()
         self._counts.clear()
         self._stats_cache.clear()
@@ -108,25 +119,34 @@ class VerletListContainer:
         self.steps_since_rebuild = 0
         self.structure_version += 1
 
-    def _load_positions(self, d) -> None:
+    def _load_positions(self, d, ghosts=None) -> None:
+        """Current positions into pos4 and the SoA copies, in rebuild-time order:
+        owned via the cell permutation; images either moved with their owners
+        (shift codes) or, for an external ghost layer, gathered from it."""
         n, nh = self.n_owned, self.n_halo
         s = N.stream()
-        ntot = n + nh + 1
         sx, sy, sz = self._soa[0], self._soa[1], self._soa[2]
         if n:
             N.call("lmd_gather_soa", n, N.ptr(self._perm), N.ptr(d.pos_x), N.ptr(d.pos_y),
                    N.ptr(d.pos_z), N.ptr(sx), N.ptr(sy), N.ptr(sz), s)
-        if nh:
-            N.call("lmd_halo_refresh_soa", N.make_box(self.box), nh, N.ptr(self._halo_owner),
-                   N.ptr(self._halo_shift), N.ptr(d.pos_x), N.ptr(d.pos_y), N.ptr(d.pos_z),
-                   N.ptr(sx[n:]), N.ptr(sy[n:]), N.ptr(sz[n:]), s)
-        if n:
             N.call("lmd_gather_pos4", n, N.ptr(self._perm), N.ptr(d.pos_x), N.ptr(d.pos_y),
                    N.ptr(d.pos_z), None, float(OWNED), N.ptr(self._pos4), s)
-        if nh:
-            N.call("lmd_halo_refresh_pos4", N.make_box(self.box), nh, N.ptr(self._halo_owner),
-                   N.ptr(self._halo_shift), N.ptr(d.pos_x), N.ptr(d.pos_y), N.ptr(d.pos_z),
+        if not nh:
+            return
+        if ghosts is not None:
+            N.call("lmd_gather_soa", nh, N.ptr(self._hperm), N.ptr(ghosts.pos_x),
+                   N.ptr(ghosts.pos_y), N.ptr(ghosts.pos_z), N.ptr(sx[n:]), N.ptr(sy[n:]),
+                   N.ptr(sz[n:]), s)
+            N.call("lmd_gather_pos4", nh, N.ptr(self._hperm), N.ptr(ghosts.pos_x),
+                   N.ptr(ghosts.pos_y), N.ptr(ghosts.pos_z), None, float(HALO),
                    N.ptr(self._pos4[n:]), s)
+            return
+        box = N.make_box(self.box)
+        N.call("lmd_halo_refresh_soa", box, nh, N.ptr(self._halo_owner), N.ptr(self._halo_shift),
+               N.ptr(d.pos_x), N.ptr(d.pos_y), N.ptr(d.pos_z), N.ptr(sx[n:]), N.ptr(sy[n:]),
+               N.ptr(sz[n:]), s)
+        N.call("lmd_halo_refresh_pos4", box, nh, N.ptr(self._halo_owner), N.ptr(self._halo_shift),
+               N.ptr(d.pos_x), N.ptr(d.pos_y), N.ptr(d.pos_z), N.ptr(self._pos4[n:]), s)
 
     def refresh(self, owned, halo=None) -> None:
         """Reload current positions (rebuild-time order) and move the images
@@ -135,6 +155,11 @@ class VerletListContainer:
         within the cutoff while displacements stay below skin/2."""
         if self.reference_positions is None:
             raise ConfigurationError("container has not been rebuilt")
+        if self._external_halo:
+            if halo is None or len(halo) != self.n_halo:
+                raise ConfigurationError("refresh needs the same ghost layer as the rebuild")
+            self._load_positions(device_soa(owned), device_soa(halo, self._pos4.device))
+            return
         self._load_positions(device_soa(owned))
 
     refresh_positions = refresh
