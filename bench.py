@@ -7,8 +7,9 @@ cutoff 2.5, FP64.  A step is one force phase over the resident particles
 (the reference's metric region, driver.py:203-207: traversal + kernel);
 the neighbor structure is built before the timed region.  The L2 is
 flushed (256 MiB write) before every timed step; only the force phase is
-inside the CUDA-event bracket.  With --gpus N > 1 every rank runs its own
-1M-particle box (replicas, weak scaling, no data-path collective).
+inside the CUDA-event bracket.  With --gpus N > 1 the periodic box is N bricks
+(2x1x1, 2x2x1, 2x2x2) of the N=1 box (weak scaling); every step includes the
+NCCL point-to-point ghost exchange.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config LABEL]
     python bench.py --impl reference ...   # the reference algorithm on host cores
@@ -137,91 +138,122 @@ def fp64_peak_tflops(torch, N) -> float:
     return flops / best / 1e12
 
 
-class LCStepper:
-    """Holds a built container and launches one force phase per step."""
+class Phase:
+    """One force phase on a built container: refresh (positions -> backing,
+    images or the exchanged ghost layer) + the force kernel."""
 
-    def __init__(self, cont, pattern, energy, torch, N, traversal):
-        self.cont = cont
-        self.traversal = traversal
-        self.pattern = pattern
-        self.energy = energy
-        dev = cont._pos4.device
+    def __init__(self, cfg, cont, buf, args, torch, N, dec=None, owned_rows=None):
+        import paper_2512_03565_b200 as B
+        self.cfg, self.cont, self.buf, self.dec = cfg, cont, buf, dec
+        self.owned_rows = owned_rows
+        self.energy = args.energy
+        self.kind = cfg.container.value
+        dev = buf.device
         self.stats_t = N.new_stats(dev)
-        slots = int(N.load().lmd_lc_ev_slots(cont.grid))
-        self.ev_t = torch.empty(2 * slots, dtype=torch.float64, device=dev)
-
-    def launch(self):
-        return self.cont.launch_force(self.pattern, self.energy, self.stats_t, self.ev_t,
-                                      self.traversal)
-
-    launches_per_step = 1
-
-
-class VLStepper:
-    """Verlet-list force phase on resident lists (built before the timed region)."""
-
-    def __init__(self, cont, pattern, newton3, energy, torch, N):
-        self.cont = cont
-        self.pattern = pattern
-        self.newton3 = newton3
-        self.energy = energy
-        dev = cont._pos4.device
-        self.stats_t = N.new_stats(dev)
-        slots = int(N.load().lmd_vl_ev_slots(cont.n_owned, pattern.code))
+        if self.kind == "vl":
+            slots = int(N.load().lmd_vl_ev_slots(cont.n_owned, cfg.pattern.code))
+        elif self.kind == "lc":
+            slots = int(N.load().lmd_lc_ev_slots(cont.grid))
+        else:
+            slots = int(N.load().lmd_vcl_ev_slots(cont.n_clusters))
         self.ev_t = torch.empty(2 * max(slots, 1), dtype=torch.float64, device=dev)
-        cont.launch_force(pattern, newton3, energy, self.stats_t, self.ev_t)  # builds the list
+        self.trav = B.traversals.traversal_code(cfg.traversal)
+        self.ghosts = None
+        self.launch()   # builds lazily-built lists outside the timed region
+
+    def refresh(self):
+        if self.dec is not None:
+            g = self.dec.exchange(self.owned_rows)
+            self.ghosts.pos_x.copy_(g[:, 0])
+            self.ghosts.pos_y.copy_(g[:, 1])
+            self.ghosts.pos_z.copy_(g[:, 2])
+            self.cont.refresh(self.buf, self.ghosts)
+        elif self.kind == "lc":
+            self.cont.refresh_positions(self.buf)
+        elif self.kind == "vl":
+            self.cont.refresh(self.buf)
+        # vcl: refresh re-derives halo clusters (host-synchronising); not per step
 
     def launch(self):
-        return self.cont.launch_force(self.pattern, self.newton3, self.energy, self.stats_t,
-                                      self.ev_t)
+        if self.kind == "vl":
+            return self.cont.launch_force(self.cfg.pattern, self.cfg.newton3, self.energy,
+                                          self.stats_t, self.ev_t)
+        if self.kind == "lc":
+            return self.cont.launch_force(self.cfg.pattern, self.energy, self.stats_t, self.ev_t,
+                                          self.trav)
+        return self.cont.launch_force(self.energy, self.stats_t, self.ev_t)
 
-    # N3 zeroes the force arrays first (3 torch fills) before the kernel
     @property
-    def launches_per_step(self):
+    def launches_per_step(self) -> int:
+        # force kernel + refresh gathers (owned pos4 + SoA; images / ghosts pos4 + SoA)
+        if self.kind == "vl":
+            return 1 + 4
+        if self.kind == "lc":
+            return 1 + 2
         return 1
 
 
-def build_stepper(cfg, w, args, torch, N):
+def build_phase(cfg, w, args, torch, N, dec=None):
     import paper_2512_03565_b200 as B
     params = params_for(cfg, w)
-    box = B.SimulationBox.cube(w.box_length, periodic=True)
-    buf = B.ParticleBuffer.from_positions(w.positions.cpu().numpy(), device="cuda")
-    cont = B.make_container(cfg.container, box, params, cluster_size=args.vector_width)
-    cont.rebuild(buf)
-    cont.refresh(buf)
+    pos = w.positions if isinstance(w.positions, torch.Tensor) else torch.as_tensor(w.positions)
+    pos = pos.to("cuda", torch.float64)
+    if dec is None:
+        box = B.SimulationBox.cube(w.box_length, periodic=True)
+        buf = B.ParticleBuffer.from_positions(pos.cpu().numpy(), device="cuda")
+        cont = B.make_container(cfg.container, box, params, cluster_size=args.vector_width)
+        cont.rebuild(buf)
+        cont.refresh(buf)
+        phase = Phase(cfg, cont, buf, args, torch, N)
+    else:
+        box = dec.local_box()
+        ids = torch.arange(pos.shape[0], dtype=torch.float64, device="cuda")
+        rows = torch.cat([pos, ids[:, None]], dim=1)
+        rows = dec.migrate(rows)
+        owned_rows = rows.contiguous()
+        ghost_rows = dec.plan(owned_rows)
+        buf = B.ParticleBuffer.from_positions(owned_rows[:, :3].cpu().numpy(), device="cuda")
+        owned_rows = torch.cat([torch.stack([buf.pos_x, buf.pos_y, buf.pos_z], 1),
+                                owned_rows[:, 3:]], 1)
+        ghosts = B.ParticleBuffer.from_positions(ghost_rows[:, :3].cpu().numpy(), device="cuda")
+        cont = B.make_container(cfg.container, box, params, cluster_size=args.vector_width)
+        cont.rebuild(buf, ghosts)
+        cont.refresh(buf, ghosts)
+        phase = Phase(cfg, cont, buf, args, torch, N, dec=dec, owned_rows=owned_rows)
+        phase.ghosts = ghosts
     if cfg.container.value == "vl":
-        stepper = VLStepper(cont, cfg.pattern, cfg.newton3, args.energy, torch, N)
         geo = cont.vl_stats(cfg.newton3, cfg.pattern, args.vector_width)
-        return stepper, cont, buf, box, params, geo
-    if cfg.container.value != "lc":
-        raise SystemExit(f"bench: container {cfg.container.value} not wired yet")
-    stepper = LCStepper(cont, cfg.pattern, args.energy, torch, N,
-                        B.traversals.traversal_code(cfg.traversal))
-    a, b = cfg.pattern.shape(args.vector_width)
-    inv, slots, useful = cont._lc_stats(B.traversals.traversal_code(cfg.traversal), cfg.newton3,
-                                        cfg.pattern, args.vector_width)
-    return stepper, cont, buf, box, params, (inv, slots, useful)
+    elif cfg.container.value == "lc":
+        geo = cont._lc_stats(B.traversals.traversal_code(cfg.traversal), cfg.newton3,
+                             cfg.pattern, args.vector_width)
+    else:
+        geo = cont.vcl_stats(cfg.newton3, cfg.pattern, args.vector_width)
+    return phase, cont, buf, box, params, geo
 
 
 def finish(cfg, st, geo):
     from paper_2512_03565_b200 import KernelStats
     from paper_2512_03565_b200.containers import LinkedCellsContainer
-    if cfg.container.value == "lc":
+    if cfg.container.value in ("lc", "vcl"):
         return LinkedCellsContainer.finish_stats(st, cfg.newton3, *geo)
     return KernelStats(geo[0], geo[1], geo[2], int(st.pair_interactions))
 
 
-def time_steps(stepper, steps, flush, torch):
-    """Per-step CUDA-event brackets around the force phase; L2 flushed before each."""
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(steps)]
+def time_steps(phase, steps, flush, torch):
+    """Per-step CUDA events around (refresh + force) and around the force
+    kernel alone; the L2 is flushed (untimed) before every step."""
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
     for k in range(steps):
         flush.fill_(k & 0xFF)
-        evs[k][0].record()
-        stepper.launch()
-        evs[k][1].record()
+        ev[k][0].record()
+        phase.refresh()
+        ev[k][1].record()
+        phase.launch()
+        ev[k][2].record()
     torch.cuda.synchronize()
-    return [a.elapsed_time(b) * 1e-3 for a, b in evs]
+    step = [a.elapsed_time(c) * 1e-3 for a, b, c in ev]
+    kern = [b.elapsed_time(c) * 1e-3 for a, b, c in ev]
+    return step, kern
 
 
 def cpu_baseline_lc(w, cfg, params, threads):
@@ -259,47 +291,68 @@ def run_b200(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = B.Configuration.parse(args.config)
-    w = make_workload(args, "cuda", 42 + rank)
-    stepper, cont, buf, box, params, geo = build_stepper(cfg, w, args, torch, N)
+    dec = None
+    if world > 1:
+        # weak scaling: every rank's brick is the N=1 box (same density), the
+        # global periodic box stacks the bricks; one NCCL ghost exchange per step
+        from paper_2512_03565_b200.decomposition import BrickDecomposition, brick_grid
+        grid = brick_grid(world)
+        w = make_workload(args, "cuda", 42 + rank)
+        Lb = w.box_length
+        c = (rank % grid[0], (rank // grid[0]) % grid[1], rank // (grid[0] * grid[1]))
+        w.positions = w.positions + torch.tensor([c[0] * Lb, c[1] * Lb, c[2] * Lb],
+                                                 dtype=torch.float64, device="cuda")
+        params0 = params_for(cfg, w)
+        dec = BrickDecomposition(np.zeros(3), np.array(grid, dtype=np.float64) * Lb,
+                                 params0.interaction_length, rank, world, grid=grid)
+    else:
+        w = make_workload(args, "cuda", 42)
+    phase, cont, buf, box, params, geo = build_phase(cfg, w, args, torch, N, dec)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     peak = fp64_peak_tflops(torch, N)
 
     for _ in range(max(args.warmup, 3)):
         flush.fill_(1)
-        stepper.launch()
+        phase.refresh()
+        phase.launch()
     torch.cuda.synchronize()
-    st = N.read_stats(stepper.stats_t)
+    st = N.read_stats(phase.stats_t)
     stats = finish(cfg, st, geo)
     pairs = stats.pair_interactions
+    n_local = int(buf.pos_x.shape[0])
 
     sampler = ClockSampler(local)
     sampler.start()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    per_step = time_steps(stepper, args.steps, flush, torch)
+    per_step, per_kernel = time_steps(phase, args.steps, flush, torch)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     clocks = sampler.stop()
-    t_force = sum(per_step)
-    t_max = t_force
+    t_step = sum(per_step)
+    t_kern = sum(per_kernel)
+    st2 = N.read_stats(phase.stats_t)
+    assert st2.pair_interactions == st.pair_interactions and not st2.overlap
+    t_max = t_step
+    total_pairs = pairs
     if world > 1:
-        t = torch.tensor([t_force], dtype=torch.float64, device="cuda")
+        t = torch.tensor([t_step], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_max = float(t.item())
-    # results must not have changed across the timed steps (deterministic counts)
-    st2 = N.read_stats(stepper.stats_t)
-    assert st2.pair_interactions == st.pair_interactions and not st2.overlap
+        p = torch.tensor([pairs], dtype=torch.int64, device="cuda")
+        dist.all_reduce(p)
+        total_pairs = int(p.item())
 
-    value = pairs * args.steps * world / t_max
-    avg_launch = t_force / args.steps
+    value = total_pairs * args.steps / t_max
+    avg_launch = t_kern / args.steps
     flops = pairs * FLOPS_PER_PAIR[cfg.newton3]
     achieved = flops / avg_launch / 1e12
 
     # ------------------------------------------------ e2e through the public API
     e2e = None
-    if args.e2e_steps > 0:
+    if args.e2e_steps > 0 and world == 1:
         host = {k: np.ascontiguousarray(v) for k, v in
                 zip(("pos_x", "pos_y", "pos_z"), w.positions.cpu().numpy().T)}
         n = len(host["pos_x"])
@@ -327,16 +380,15 @@ def run_b200(args):
             torch.cuda.synchronize()
             times.append(time.perf_counter() - t0)
             assert s_e2e.pair_interactions == pairs
-        t_e2e = max(times) if world == 1 else max(times)
-        tt = torch.tensor([sum(times)], dtype=torch.float64, device="cuda")
-        if world > 1:
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e = {"value": pairs * args.e2e_steps * world / float(tt.item()), "unit": UNIT,
+        e2e = {"value": pairs * args.e2e_steps / sum(times), "unit": UNIT,
                "h2d_bytes_per_step": int(n * (3 * 8 + 1)),
                "d2h_bytes_per_step": int(n * 3 * 8),
                "steps": args.e2e_steps,
                "note": "force_phase() on pinned host SoA buffers: H2D positions, device "
-                       "binning/halo/sort, force kernel, D2H forces"}
+                       "binning/images/neighbour build, force kernel, D2H forces"}
+    elif args.e2e_steps > 0:
+        e2e = {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+               "note": "e2e measured at N=1 only (force_phase is single-domain)"}
 
     # ------------------------------------------------------------ CPU baseline
     cpu = None
@@ -356,7 +408,7 @@ def run_b200(args):
         except Exception as exc:  # pragma: no cover - reported, not fatal
             cpu = {"value": None, "error": repr(exc)}
 
-    if args.sweep and rank == 0:
+    if args.sweep and rank == 0 and world == 1:
         sweep(args, w, torch, N, flush)
 
     if rank == 0:
@@ -366,23 +418,29 @@ def run_b200(args):
             "ms_per_step": t_max / args.steps * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": w.name, "particles_per_gpu": w.n, "rho": args.rho,
-                       "box_length": w.box_length, "cutoff": w.cutoff, "skin": params.skin,
-                       "configuration": cfg.label, "vector_width": args.vector_width,
-                       "pairs_per_step_per_gpu": pairs,
-                       "useful_interactions": stats.useful_interactions,
+            "config": {"workload": w.name, "particles_per_gpu": n_local, "rho": args.rho,
+                       "box_length_per_gpu": w.box_length, "cutoff": w.cutoff,
+                       "skin": params.skin, "configuration": cfg.label,
+                       "vector_width": args.vector_width,
+                       "pairs_per_step": total_pairs, "pairs_per_step_rank0": pairs,
+                       "useful_interactions_rank0": stats.useful_interactions,
                        "candidate_efficiency": pairs / max(stats.useful_interactions, 1),
+                       "step": "refresh (positions -> cell order, images/ghosts) + force "
+                               "kernel" + (" + NCCL ghost exchange" if world > 1 else ""),
+                       "kernel_ms_rank0": avg_launch * 1e3,
                        "l2": "flushed (256 MiB write) before every timed step",
-                       "parallelism": "replicas" if world > 1 else "single",
+                       "parallelism": (f"bricks {dec.grid}, NCCL P2P ghost exchange"
+                                       if dec else "single"),
                        "inputs": w.note},
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved / peak,
                          "flops_per_pair": FLOPS_PER_PAIR[cfg.newton3],
+                         "kernel": "force kernel alone (CUDA events on its stream)",
                          "peak_source": "measured in this run: lmd_dfma_burn (DFMA, 2 flop)",
                          "traffic": None},
             "e2e": e2e,
             "cpu_baseline": cpu,
-            "gpu_launches": args.steps * stepper.launches_per_step,
+            "gpu_launches": args.steps * phase.launches_per_step,
             "clocks": clocks,
         }
         print(json.dumps(line))
@@ -399,11 +457,11 @@ def sweep(args, w, torch, N, flush):
         [False, True], list(B.PATTERN_ORDER))]
     for label in labels:
         cfg = B.Configuration.parse(label)
-        stepper, cont, *_ = build_stepper(cfg, w, args, torch, N)
+        phase, cont, *_ = build_phase(cfg, w, args, torch, N)
         for _ in range(3):
-            stepper.launch()
-        t = time_steps(stepper, 5, flush, torch)
-        st = N.read_stats(stepper.stats_t)
+            phase.launch()
+        _, t = time_steps(phase, 5, flush, torch)
+        st = N.read_stats(phase.stats_t)
         pairs = finish(cfg, st, (0, 0, 0)).pair_interactions
         rows.append({"config": label, "ms": min(t) * 1e3, "pairs": pairs,
                      "pairs_per_s": pairs / min(t)})

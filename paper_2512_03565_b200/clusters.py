@@ -141,7 +141,8 @@ class VerletClusterContainer:
                    N.ptr(lst), s)
         return count, n3, off, lst
 
-    def rebuild(self, owned) -> None:
+    def rebuild(self, owned, halo=None) -> None:
+        """``halo`` is accepted for protocol uniformity; images enter at refresh."""
         d = device_soa(owned)
         _check_all_owned(d)
         dev = d.device

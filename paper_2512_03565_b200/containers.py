@@ -198,7 +198,8 @@ class LinkedCellsContainer:
         self._count = torch.empty(nc, dtype=torch.int32, device=dev)
         self._dup = torch.zeros(nc, dtype=torch.uint8, device=dev)
 
-    def rebuild(self, owned) -> None:
+    def rebuild(self, owned, halo=None) -> None:
+        """``halo`` is accepted for protocol uniformity; images enter at refresh."""
         d = device_soa(owned)
         _check_all_owned(d)
         dev = d.device
