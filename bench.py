@@ -153,7 +153,8 @@ class Phase:
         if self.kind == "vl":
             slots = int(N.load().lmd_vl_ev_slots(cont.n_owned, cfg.pattern.code))
         elif self.kind == "lc":
-            slots = int(N.load().lmd_lc_ev_slots(cont.grid))
+            slots = max(int(N.load().lmd_lc_ev_slots(cont.grid)),
+                        int(N.load().lmd_lc_n3_ev_slots(cont.grid)))
         else:
             slots = int(N.load().lmd_vcl_ev_slots(cont.n_clusters))
         self.ev_t = torch.empty(2 * max(slots, 1), dtype=torch.float64, device=dev)
@@ -180,14 +181,14 @@ class Phase:
                                           self.stats_t, self.ev_t)
         if self.kind == "lc":
             return self.cont.launch_force(self.cfg.pattern, self.energy, self.stats_t, self.ev_t,
-                                          self.trav)
+                                          self.trav, self.cfg.newton3)
         return self.cont.launch_force(self.energy, self.stats_t, self.ev_t)
 
     @property
     def launches_per_step(self) -> int:
-        # force kernel + refresh gathers (owned pos4 + SoA; images / ghosts pos4 + SoA)
+        # force kernel + refresh gathers (owned pos4; images / ghosts pos4)
         if self.kind == "vl":
-            return 1 + 4
+            return 1 + 2
         if self.kind == "lc":
             return 1 + 2
         return 1
@@ -234,7 +235,10 @@ def build_phase(cfg, w, args, torch, N, dec=None):
 def finish(cfg, st, geo):
     from paper_2512_03565_b200 import KernelStats
     from paper_2512_03565_b200.containers import LinkedCellsContainer
-    if cfg.container.value in ("lc", "vcl"):
+    if cfg.container.value == "lc":
+        once = cfg.newton3 and cfg.traversal.value in ("lc_c08", "lc_c18")
+        return LinkedCellsContainer.finish_stats(st, cfg.newton3 and not once, *geo)
+    if cfg.container.value == "vcl":
         return LinkedCellsContainer.finish_stats(st, cfg.newton3, *geo)
     return KernelStats(geo[0], geo[1], geo[2], int(st.pair_interactions))
 

@@ -187,6 +187,20 @@ int lmd_force_lc(const lmd_grid* g, const lmd_lj* lj, int pattern, int flags,
                  const uint8_t* dup, double* fx, double* fy, double* fz, double* ev_scratch,
                  lmd_stats* stats, void* stream);
 
+/* Newton3 lc_c08 / lc_c18 as colored passes (traversals.py:190-241, the
+ * concurrency contract of traversals.py:1-6): one launch per color, one warp
+ * per base; the base's units dual-write into its shared-memory write set
+ * (c08: its 2x2x2 block, c18: its cell + 13 forward neighbours), flushed to
+ * f once per base.  Zeroes f first; deterministic.  pair_interactions is
+ * counted in the reference's Newton3 convention.  max_cell >= the largest
+ * owned cell count; ev_scratch: 2 * lmd_lc_n3_ev_slots(g) doubles. */
+int64_t lmd_lc_n3_ev_slots(const lmd_grid* g);
+int lmd_force_lc_n3(const lmd_grid* g, const lmd_lj* lj, int traversal, int pattern, int flags,
+                    const double* pos4, int64_t n_owned, const int32_t* cell_start,
+                    const int32_t* cell_count, const int32_t* o_count, const int32_t* h_count,
+                    const uint8_t* dup, int max_cell, double* fx, double* fy, double* fz,
+                    double* ev_scratch, lmd_stats* stats, void* stream);
+
 /* Geometric KernelStats of the reference schedules (traversals.py:108-266,
  * executor.py:38-69, 165-171) for lc_c01 / lc_c08 / lc_c18: kernel
  * invocations, lane slots and useful interactions for shape (a, b) and

@@ -156,6 +156,9 @@ class LinkedCellsContainer:
         self._sorter = None
         self._stats_cache: dict = {}
         self._tables_ready = False
+        # Newton3 on lc_c08/lc_c18: "colored" dual-write passes, or "full_shell"
+        self.n3_mode = "colored"
+        self._max_cell = 1
 
     # ------------------------------------------------------------ geometry
     def linear_index(self, coords: np.ndarray) -> np.ndarray:
@@ -210,6 +213,7 @@ class LinkedCellsContainer:
         self.n_owned = n
         self._perm = self._sorter.bin(self.grid, 0, d.pos_x, d.pos_y, d.pos_z, 0,
                                       self._o_start, self._o_count)
+        self._max_cell = max(1, int(self._o_count.max().item())) if n else 1
         self.reference_positions = d.positions().clone()
         self.steps_since_rebuild = 0
         self.structure_version += 1
@@ -360,12 +364,19 @@ class LinkedCellsContainer:
         self._stats_cache[key] = hit
         return hit
 
+    def uses_colored_n3(self, traversal, newton3: bool) -> bool:
+        return bool(newton3) and traversal in (N.LC_C08, N.LC_C18) and self.n3_mode == "colored"
+
     def launch_force(self, pattern, energy: bool = False, stats_t=None, ev_t=None,
-                     traversal=N.LC_C01):
-        """Launch K2 on the current stream without synchronising; returns the
-        device stats tensor (pair counts, overlap flag, energy).  lc_c08 /
-        lc_c18 weight cells that hold both owned particles and images the way
-        the reference's duplicated anchor units do (traversals.py:133)."""
+                     traversal=N.LC_C01, newton3: bool = False):
+        """Launch the force phase on the current stream without synchronising;
+        returns the device stats tensor (pair counts, overlap flag, energy).
+
+        Newton3 on lc_c08 / lc_c18 runs the colored dual-write traversal
+        (lmd_force_lc_n3: one launch per color, deterministic); otherwise the
+        27-cell full shell (lmd_force_lc).  Both weight cells that hold owned
+        particles and images the way the reference's duplicated anchor units
+        do (traversals.py:133)."""
         if not self._tables_ready:
             raise ConfigurationError("container has not been refreshed")
         pattern = as_pattern(pattern)
@@ -374,6 +385,16 @@ class LinkedCellsContainer:
             stats_t = N.new_stats(dev)
         else:
             stats_t.zero_()
+        if self.uses_colored_n3(traversal, newton3):
+            if ev_t is None or ev_t.numel() < 2 * int(N.load().lmd_lc_n3_ev_slots(self.grid)):
+                slots = int(N.load().lmd_lc_n3_ev_slots(self.grid))
+                ev_t = torch.empty(2 * slots, dtype=torch.float64, device=dev)
+            N.call("lmd_force_lc_n3", self.grid, N.make_lj(self.params), traversal, pattern.code,
+                   N.FLAG_ENERGY if energy else 0, N.ptr(self._pos4), self.n_owned,
+                   N.ptr(self._start), N.ptr(self._count), N.ptr(self._o_count),
+                   N.ptr(self._h_count), N.ptr(self._dup), self._max_cell, N.ptr(self._fx),
+                   N.ptr(self._fy), N.ptr(self._fz), N.ptr(ev_t), N.ptr(stats_t), N.stream())
+            return stats_t
         if ev_t is None:
             slots = int(N.load().lmd_lc_ev_slots(self.grid))
             ev_t = torch.empty(2 * slots, dtype=torch.float64, device=dev)
@@ -397,11 +418,14 @@ class LinkedCellsContainer:
         if code == N.LC_C01 and newton3:
             raise ConfigurationError("lc_c01 cannot exploit Newton's third law")
         inv, slots, useful = self._lc_stats(code, newton3, pattern, vector_width)
-        st = N.read_stats(self.launch_force(pattern, energy, traversal=code))
-        return self.finish_stats(st, newton3, inv, slots, useful)
+        st = N.read_stats(self.launch_force(pattern, energy, traversal=code, newton3=newton3))
+        once = self.uses_colored_n3(code, newton3)
+        return self.finish_stats(st, newton3 and not once, inv, slots, useful)
 
     @staticmethod
     def finish_stats(st, newton3, inv, slots, useful) -> KernelStats:
+        """KernelStats from a device stats record; ``newton3`` converts ordered
+        full-shell pair counts to the reference's Newton3 convention."""
         from .errors import ParticleOverlapError
         if st.overlap:
             raise ParticleOverlapError("zero distance between interacting particles")

@@ -126,25 +126,29 @@ class VerletListContainer:
         n, nh = self.n_owned, self.n_halo
         s = N.stream()
         sx, sy, sz = self._soa[0], self._soa[1], self._soa[2]
+        soa = self.use_soa
         if n:
-            N.call("lmd_gather_soa", n, N.ptr(self._perm), N.ptr(d.pos_x), N.ptr(d.pos_y),
-                   N.ptr(d.pos_z), N.ptr(sx), N.ptr(sy), N.ptr(sz), s)
+            if soa:
+                N.call("lmd_gather_soa", n, N.ptr(self._perm), N.ptr(d.pos_x), N.ptr(d.pos_y),
+                       N.ptr(d.pos_z), N.ptr(sx), N.ptr(sy), N.ptr(sz), s)
             N.call("lmd_gather_pos4", n, N.ptr(self._perm), N.ptr(d.pos_x), N.ptr(d.pos_y),
                    N.ptr(d.pos_z), None, float(OWNED), N.ptr(self._pos4), s)
         if not nh:
             return
         if ghosts is not None:
-            N.call("lmd_gather_soa", nh, N.ptr(self._hperm), N.ptr(ghosts.pos_x),
-                   N.ptr(ghosts.pos_y), N.ptr(ghosts.pos_z), N.ptr(sx[n:]), N.ptr(sy[n:]),
-                   N.ptr(sz[n:]), s)
+            if soa:
+                N.call("lmd_gather_soa", nh, N.ptr(self._hperm), N.ptr(ghosts.pos_x),
+                       N.ptr(ghosts.pos_y), N.ptr(ghosts.pos_z), N.ptr(sx[n:]), N.ptr(sy[n:]),
+                       N.ptr(sz[n:]), s)
             N.call("lmd_gather_pos4", nh, N.ptr(self._hperm), N.ptr(ghosts.pos_x),
                    N.ptr(ghosts.pos_y), N.ptr(ghosts.pos_z), None, float(HALO),
                    N.ptr(self._pos4[n:]), s)
             return
         box = N.make_box(self.box)
-        N.call("lmd_halo_refresh_soa", box, nh, N.ptr(self._halo_owner), N.ptr(self._halo_shift),
-               N.ptr(d.pos_x), N.ptr(d.pos_y), N.ptr(d.pos_z), N.ptr(sx[n:]), N.ptr(sy[n:]),
-               N.ptr(sz[n:]), s)
+        if soa:
+            N.call("lmd_halo_refresh_soa", box, nh, N.ptr(self._halo_owner),
+                   N.ptr(self._halo_shift), N.ptr(d.pos_x), N.ptr(d.pos_y), N.ptr(d.pos_z),
+                   N.ptr(sx[n:]), N.ptr(sy[n:]), N.ptr(sz[n:]), s)
         N.call("lmd_halo_refresh_pos4", box, nh, N.ptr(self._halo_owner), N.ptr(self._halo_shift),
                N.ptr(d.pos_x), N.ptr(d.pos_y), N.ptr(d.pos_z), N.ptr(self._pos4[n:]), s)
 

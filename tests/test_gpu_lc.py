@@ -221,3 +221,32 @@ def test_lc_random_medium_vs_oracle(rng):
                                          PatternKind(pat)), 8)
         assert st == B.KernelStats(*ost.as_tuple())
         assert forces_close(buf.forces().cpu().numpy(), of)
+
+
+@pytest.mark.parametrize("trav", ["lc_c08", "lc_c18"])
+def test_colored_newton3_matches_full_shell_and_is_deterministic(rng, trav):
+    pos = jittered_lattice(rng, (14, 14, 14), 1.08, 0.12)
+    span = 14 * 1.08
+    params = LJParams(cutoff=2.5, skin=0.0)
+    box = _box(span, True)
+    results = {}
+    for mode in ("colored", "full_shell", "colored"):
+        cont = B.LinkedCellsContainer(box, params)
+        cont.n3_mode = mode
+        buf = _buf(pos)
+        cont.rebuild(buf)
+        cont.refresh(buf)
+        for pat in PATTERNS:
+            st = cont.compute_forces(trav, True, pat, 8, energy=True)
+            cont.collect_forces(buf)
+            f = buf.forces().cpu().numpy()
+            key = (mode, pat)
+            if key in results:
+                assert np.array_equal(results[key][0], f)        # bitwise deterministic
+            results[key] = (f, st)
+    for pat in PATTERNS:
+        fc, sc = results[("colored", pat)]
+        ff, sf = results[("full_shell", pat)]
+        assert forces_close(fc, ff)
+        assert sc == sf
+        assert abs(sc.epot - sf.epot) <= 1e-12 * abs(sf.epot)
