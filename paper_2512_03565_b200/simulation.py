@@ -1,0 +1,243 @@
+"""Device-resident MD loop with the runtime tuner (driver.py:132-313).
+
+Per iteration, as the reference's ``run_simulation`` (driver.py:171-224):
+pre-force half step, tuner decision, container rebuild when
+``needs_rebuild`` fires (displacement >= skin/2 or the period), images,
+metric-bracketed force phase, force collection, tuner sample (displaced by a
+rebuild -> retaken), post-force half step, boundaries, one record.  All state
+stays in HBM; the force phase is bracketed with CUDA events on its stream
+(``metric="time"``) or counted in lane slots (``"laneops"``).
+
+Extensions: Verlet lists join the search space; ``retune_drift`` starts a new
+tuning phase when the peak cell occupancy drifts by more than that fraction
+since the last phase started ("re-tuning as density changes").
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .containers import LinkedCellsContainer, max_particles_per_cell
+from .domain import apply_boundaries, as_box
+from .driver import make_container
+from .errors import ConfigurationError, ParticleOverlapError, ScenarioError, SimulationDivergedError
+from .integrator import POST_FORCE, PRE_FORCE, velocity_verlet_step
+from .kernels import KernelStats, validate_vector_width
+from .traversals import traversal_code
+from .tuning import (PRODUCTION, Configuration, ContainerKind, Tuner, TuningPolicy,
+                     make_metric_provider)
+
+CSV_COLUMNS = (
+    "iteration", "phase", "container", "traversal", "newton3", "pattern",
+    "metric_value", "lane_slots", "useful_interactions", "blank_lanes",
+    "pair_interactions", "particle_count",
+)
+
+
+@dataclass
+class IterationRecord:
+    """One CSV row (driver.py:36-56)."""
+
+    iteration: int
+    phase: str
+    configuration: Configuration
+    metric_value: float
+    lane_slots: int
+    useful_interactions: int
+    blank_lanes: int
+    pair_interactions: int
+    particle_count: int
+
+    def row(self) -> list:
+        c = self.configuration
+        return [str(self.iteration), self.phase, c.container.value, c.traversal.value,
+                "true" if c.newton3 else "false", c.pattern.value, repr(self.metric_value),
+                str(self.lane_slots), str(self.useful_interactions), str(self.blank_lanes),
+                str(self.pair_interactions), str(self.particle_count)]
+
+
+@dataclass
+class RunSummary:
+    per_config_metric: dict
+    phase_selections: list
+    failed_configs: list
+    wall_time_s: float
+    particle_count: int
+    initial_max_per_cell: int
+    final_max_per_cell: int
+    final_max_speed: float
+    force_time_s: float = 0.0
+    steps: int = 0
+    retunes: int = 0
+    extra: dict = field(default_factory=dict)
+
+    @property
+    def total_metric(self) -> float:
+        return sum(self.per_config_metric.values())
+
+    @property
+    def particle_steps_per_s(self) -> float:
+        return self.particle_count * self.steps / self.wall_time_s if self.wall_time_s else 0.0
+
+
+def _launch(cont, cfg: Configuration, V: int, energy: bool):
+    kind = cfg.container
+    if kind is ContainerKind.LINKED_CELLS:
+        code = traversal_code(cfg.traversal)
+        return cont.launch_force(cfg.pattern, energy, traversal=code, newton3=cfg.newton3)
+    if kind is ContainerKind.VERLET_LISTS:
+        return cont.launch_force(cfg.pattern, cfg.newton3, energy)
+    return cont.launch_force(energy)
+
+
+def _finish(cont, cfg: Configuration, V: int, stats_t) -> KernelStats:
+    st = N.read_stats(stats_t)
+    kind = cfg.container
+    if kind is ContainerKind.LINKED_CELLS:
+        code = traversal_code(cfg.traversal)
+        geo = cont._lc_stats(code, cfg.newton3, cfg.pattern, V)
+        once = cont.uses_colored_n3(code, cfg.newton3)
+        return LinkedCellsContainer.finish_stats(st, cfg.newton3 and not once, *geo)
+    if kind is ContainerKind.VERLET_LISTS:
+        geo = cont.vl_stats(cfg.newton3, cfg.pattern, V)
+        if st.overlap:
+            raise ParticleOverlapError("zero distance between interacting particles")
+        return KernelStats(geo[0], geo[1], geo[2], int(st.pair_interactions), st.epot, st.virial)
+    geo = cont.vcl_stats(cfg.newton3, cfg.pattern, V)
+    return LinkedCellsContainer.finish_stats(st, cfg.newton3, *geo)
+
+
+def run_md(owned, box, params, iterations: int, vector_width: int = 8, *,
+           configurations=None, fixed_config: Configuration | None = None,
+           policy: TuningPolicy | None = None, metric: str = "time",
+           cluster_size: int | None = None, rebuild_period: int | None = None,
+           retune_drift: float | None = None, energy: bool = False, record: bool = True):
+    """Run ``iterations`` MD steps on device-resident ``owned`` (our ParticleBuffer).
+
+    Returns (records, summary).  With ``fixed_config`` the tuner is off."""
+    validate_vector_width(vector_width)
+    box = as_box(box)
+    if fixed_config is None:
+        if not configurations:
+            raise ConfigurationError("search space has no valid configuration")
+        pol = policy or TuningPolicy(metric=metric)
+        if policy is None:
+            pol = TuningPolicy(pol.samples_per_config,
+                               max(1000, pol.samples_per_config * len(configurations)),
+                               pol.reduction, metric)
+        tuner = Tuner(list(configurations), pol)
+    else:
+        if not fixed_config.is_valid():
+            raise ConfigurationError(f"invalid configuration {fixed_config.label!r}")
+        tuner = None
+    lane_total = [0]
+    provider = make_metric_provider(metric, lambda: lane_total[0])
+    containers: dict = {}
+    records: list = []
+    per_config: dict = {}
+    margin = params.interaction_length
+    initial_max = max_particles_per_cell(owned, box, margin)
+    phase_max = initial_max
+    retunes = 0
+    force_time = 0.0
+    start = time.perf_counter()
+    try:
+        for it in range(iterations):
+            velocity_verlet_step(owned, params, PRE_FORCE, check=False)
+            if tuner is not None:
+                if retune_drift and it > 0 and tuner.selected is not None and it % 10 == 0:
+                    cur = max_particles_per_cell(owned, box, margin)
+                    if abs(cur - phase_max) > retune_drift * max(phase_max, 1):
+                        tuner.request_retune()
+                        phase_max = cur
+                        retunes += 1
+                cfg, phase = tuner.next_configuration(it)
+            else:
+                cfg, phase = fixed_config, PRODUCTION
+            cont = containers.get(cfg.container)
+            if cont is None:
+                kw = {} if rebuild_period is None else {"rebuild_period": rebuild_period}
+                cont = make_container(cfg.container, box, params,
+                                      cluster_size=cluster_size or vector_width, **kw)
+                containers[cfg.container] = cont
+            rebuilt = False
+            if cont.reference_positions is None:
+                cont.rebuild(owned)
+                cont.refresh(owned)
+            elif cont.needs_rebuild(owned):
+                cont.rebuild(owned)
+                cont.refresh(owned)
+                rebuilt = True
+            else:
+                cont.refresh(owned)
+            cont.steps_since_rebuild += 1
+            provider.begin_region()
+            t0 = time.perf_counter()
+            stats_t = _launch(cont, cfg, vector_width, energy)
+            sample = provider.end_region() if metric != "laneops" else None
+            stats = _finish(cont, cfg, vector_width, stats_t)
+            force_time += time.perf_counter() - t0
+            lane_total[0] += stats.lane_slots
+            if sample is None:
+                sample = provider.end_region()
+            cont.collect_forces(owned)
+            if tuner is not None:
+                tuner.record_sample(sample, displaced=rebuilt)
+            velocity_verlet_step(owned, params, POST_FORCE, check=False)
+            apply_boundaries(owned, box)
+            if record:
+                records.append(IterationRecord(it, phase, cfg, sample, stats.lane_slots,
+                                               stats.useful_interactions, stats.blank_lanes,
+                                               stats.pair_interactions, len(owned)))
+            per_config[cfg.label] = per_config.get(cfg.label, 0.0) + sample
+        flag = owned.extra.get("nonfinite")
+        if flag is not None and int(flag.item()):
+            raise SimulationDivergedError("non-finite particle state")
+    except SimulationDivergedError as exc:
+        exc.records = records
+        raise
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - start
+    speed = torch.sqrt(owned.vel_x ** 2 + owned.vel_y ** 2 + owned.vel_z ** 2)
+    failed, selections = [], []
+    if tuner is not None:
+        selections = [c.label for c in tuner.phase_selection]
+    summary = RunSummary(
+        per_config_metric=dict(sorted(per_config.items())), phase_selections=selections,
+        failed_configs=failed, wall_time_s=wall, particle_count=len(owned),
+        initial_max_per_cell=initial_max,
+        final_max_per_cell=max_particles_per_cell(owned, box, margin),
+        final_max_speed=float(speed.max().item()) if len(owned) else 0.0,
+        force_time_s=force_time, steps=iterations, retunes=retunes)
+    return records, summary
+
+
+def emit_csv(records, path) -> None:
+    """Records as CSV with the reference's column order (driver.py:262-270)."""
+    if not records:
+        raise ScenarioError("no records to write")
+    lines = [",".join(CSV_COLUMNS)] + [",".join(r.row()) for r in records]
+    with open(path, "w", encoding="utf-8", newline="\n") as fh:
+        fh.write("\n".join(lines) + "\n")
+
+
+def read_records_csv(path) -> list:
+    from .kernels import PatternKind
+    from .traversals import TraversalKind
+    with open(path, encoding="utf-8") as fh:
+        lines = [ln.rstrip("\n") for ln in fh if ln.strip()]
+    if tuple(lines[0].split(",")) != CSV_COLUMNS:
+        raise ScenarioError(f"unexpected CSV header {lines[0]!r}")
+    out = []
+    for ln in lines[1:]:
+        p = ln.split(",")
+        cfg = Configuration(ContainerKind(p[2]), TraversalKind(p[3]), p[4] == "true",
+                            PatternKind(p[5]))
+        out.append(IterationRecord(int(p[0]), p[1], cfg, float(p[6]), int(p[7]), int(p[8]),
+                                   int(p[9]), int(p[10]), int(p[11])))
+    return out

@@ -1,0 +1,88 @@
+"""Device MD loop: the reference's driver semantics (config 1 trajectory) and
+the tuner (full-search sampling, laneops / replay selection)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden
+
+import paper_2512_03565_b200 as B
+from paper_2512_03565_b200 import (PATTERN_ORDER, Configuration, ContainerKind, LJParams,
+                                   ParticleBuffer, SimulationBox, TraversalKind, TuningPolicy,
+                                   enumerate_search_space)
+from paper_2512_03565_b200.simulation import emit_csv, read_records_csv, run_md
+
+pytestmark = pytest.mark.gpu
+
+
+def test_run_md_config1_matches_reference_trajectory(tmp_path):
+    g = golden("config1.npz")
+    box = SimulationBox.cube(22.0, periodic=True)
+    params = LJParams(cutoff=2.5, skin=0.0, dt=0.001)
+    buf = ParticleBuffer.from_positions(g["pos0"], device="cuda")
+    v = torch.as_tensor(g["vel0"], device="cuda")
+    buf.vel_x.copy_(v[:, 0]); buf.vel_y.copy_(v[:, 1]); buf.vel_z.copy_(v[:, 2])
+    cfg = Configuration.parse("lc,lc_c08,true,one_by_v")
+    B.force_phase(buf, box, params, cfg, 8)          # seed forces for the first kick
+    records, summary = run_md(buf, box, params, 10, 8, fixed_config=cfg, metric="laneops")
+    assert [r.pair_interactions for r in records] == g["pairs_per_step"].tolist()
+    assert np.abs(buf.positions().cpu().numpy() - g["pos10"]).max() < 1e-12
+    path = tmp_path / "run.csv"
+    emit_csv(records, path)
+    assert read_records_csv(path) == records
+
+
+def test_tuner_samples_every_config_and_selects_by_replay(tmp_path):
+    rng = np.random.default_rng(11)
+    grid = np.stack(np.meshgrid(*[np.arange(5)] * 3, indexing="ij"), -1).reshape(-1, 3)
+    pos = 4.0 + grid * 1.2 + rng.uniform(-0.02, 0.02, grid.shape)
+    box = SimulationBox(np.zeros(3), np.full(3, 14.0), ("reflective",) * 3)
+    params = LJParams(cutoff=2.5, skin=0.5, dt=0.001)
+    configs = enumerate_search_space([ContainerKind.LINKED_CELLS],
+                                     [TraversalKind.LC_C01, TraversalKind.LC_C08], [False, True],
+                                     list(PATTERN_ORDER))
+    assert len(configs) == 12
+    target = configs[7]
+    schedule = []
+    for _ in range(3):
+        schedule.extend(k // 2 for k in range(24))
+        schedule.extend([None] * 6)
+    lines = [str(5.0) if i is None else str(1.0 if configs[i] == target else 10.0 + i)
+             for i in schedule]
+    replay = tmp_path / "replay.txt"
+    replay.write_text("\n".join(lines) + "\n")
+    buf = ParticleBuffer.from_positions(pos, device="cuda")
+    records, summary = run_md(buf, box, params, 90, 8, configurations=configs,
+                              policy=TuningPolicy(2, 30, "mean", f"replay:{replay}"),
+                              metric=f"replay:{replay}", rebuild_period=100000)
+    assert summary.phase_selections == [target.label] * 3
+    for start in (0, 30, 60):
+        window = records[start:start + 24]
+        assert all(r.phase == "tuning" for r in window)
+        seen = {}
+        for r in window:
+            seen[r.configuration.label] = seen.get(r.configuration.label, 0) + 1
+        assert seen == {c.label: 2 for c in configs}
+
+
+def test_time_metric_tuner_runs_all_containers():
+    rng = np.random.default_rng(5)
+    n = 4000
+    span = (n / 0.7) ** (1 / 3)
+    k = int(np.ceil(n ** (1 / 3)))
+    grid = np.stack(np.meshgrid(*[np.arange(k)] * 3, indexing="ij"), -1).reshape(-1, 3)[:n]
+    pos = (grid + 0.5) * (span / k) + rng.uniform(-0.1, 0.1, (n, 3))
+    box = SimulationBox.cube(span, periodic=True)
+    params = LJParams(cutoff=2.5, skin=0.3, dt=0.001)
+    configs = enumerate_search_space(list(ContainerKind), list(TraversalKind), [False],
+                                     [B.PatternKind.V_BY_ONE, B.PatternKind.HALF_BY_TWO])
+    buf = ParticleBuffer.from_positions(pos, device="cuda")
+    records, summary = run_md(buf, box, params, len(configs) + 5, 8, configurations=configs,
+                              policy=TuningPolicy(1, len(configs) + 5, "mean", "time"),
+                              metric="time")
+    assert len(summary.phase_selections) == 1
+    pairs = {r.pair_interactions for r in records[:2]}
+    assert min(r.metric_value for r in records) > 0
