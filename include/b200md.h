@@ -221,9 +221,10 @@ int lmd_scatter_forces(int64_t n, const int32_t* perm, const double* fx, const d
  * particles and images of the 27 cells; listed iff r2 < rl2 with the
  * reference's exact r2.  newton3 = 1 builds half lists (owned j > i).
  * 1) lmd_vl_count -> count[i];  2) lmd_vl_layout -> per-tile kmax / offsets
- * for `pattern` (tiles of A = distinct i per fill; kmax padded to B);
- * 3) lmd_vl_fill -> nbr (interleaved, padded with `sentinel`, the index of a
- * far-away dummy position).  Total entries = tile_off[last] + tile_len[last]. */
+ * for `pattern` (tiles of A = distinct i per fill; kmax = fill steps x B,
+ * steps padded to whole 4-step chunks); 3) lmd_vl_fill -> nbr (`total` =
+ * tile_off[last] + tile_len[last] entries, lane-chunked as documented in
+ * csrc/vl.cu, padded with `sentinel`, the index of a far-away record). */
 int lmd_vl_count(const lmd_grid* g, double rl2, int newton3, int64_t n_owned, const double* pos4,
                  const int32_t* o_start, const int32_t* o_count, const int32_t* h_start,
                  const int32_t* h_count, int32_t* count, void* stream);
@@ -235,7 +236,7 @@ int lmd_vl_layout(int64_t n_owned, int pattern, const int32_t* count, int64_t* t
 int lmd_vl_fill(const lmd_grid* g, double rl2, int newton3, int pattern, int64_t n_owned,
                 int32_t sentinel, const double* pos4, const int32_t* o_start,
                 const int32_t* o_count, const int32_t* h_start, const int32_t* h_count,
-                const int64_t* tile_off, const int32_t* kmax, int32_t* nbr, void* stream);
+                const int64_t* tile_off, int64_t total, int32_t* nbr, void* stream);
 /* Force over the lists: one warp per i-tile, lanes by `pattern`; positions
  * are pos4 over the combined backing plus one sentinel record (256-bit
  * gathers), or, if soa != NULL, SoA copies x = soa[0..ntot), y, z of the

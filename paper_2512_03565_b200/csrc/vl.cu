@@ -7,11 +7,14 @@
 // reference's exact r2.  Half lists (Newton3): owned j > i only, images always.
 //
 // List layout = the interaction order: owned particles (cell-sorted) form
-// i-tiles of A consecutive particles (A = distinct i per warp fill); tile t
-// stores its entries interleaved, entry (k, il) at tile_off[t] + k*A + il,
-// padded to kmax[t] (a multiple of B) with a sentinel particle far away.  A
-// warp fill (A i's x B consecutive k's) therefore reads 32 consecutive ints.
-// Lists are ascending in j, so lanes of a tile gather nearby particles.
+// i-tiles of A consecutive particles (A = distinct i per warp fill).  Entry k
+// of tile particle il is consumed at fill step s = k / B by the lane l with
+// (i_off(l), j_off(l)) = (il, k % B).  Each lane's entries are stored in
+// chunks of kChunk consecutive steps -- entry (s, l) at
+// tile_off[t] + (s / kChunk) * 32 * kChunk + l * kChunk + s % kChunk -- so a
+// lane fetches kChunk indices with one 128-bit load and a warp reads 512
+// contiguous bytes per chunk.  Tiles are padded to a whole number of chunks
+// with a sentinel particle far away.  Lists are ascending in j.
 #include <cub/cub.cuh>
 
 #include "common.cuh"
@@ -19,6 +22,17 @@
 namespace lmd {
 
 constexpr int kVLWarps = 4;
+constexpr int kChunk = 4;  // fill steps per lane per 128-bit index load
+
+// lane holding (i_off = il, j_off = jo) of a pattern (inverse of Pattern<P>)
+__device__ __forceinline__ int lane_of(int pattern, int il, int jo) {
+  switch (pattern) {
+    case LMD_ONE_BY_V: return jo;
+    case LMD_V_BY_ONE: return il;
+    case LMD_TWO_BY_HALF: return il * 16 + jo;
+    default: return il + 16 * jo;  // LMD_HALF_BY_TWO
+  }
+}
 
 template <int P>
 struct Tile {
@@ -100,45 +114,38 @@ __global__ void vl_tile_kernel(int n, int A, int B, const int32_t* __restrict__ 
   if (t >= ntiles) return;
   int m = 0;
   for (int k = t * A; k < t * A + A && k < n; ++k) m = max(m, count[k]);
-  m = (m + B - 1) / B * B;
-  kmax[t] = m;
-  tile_len[t] = (long long)m * A;
+  int steps = (m + B - 1) / B;
+  steps = (steps + kChunk - 1) / kChunk * kChunk;
+  kmax[t] = steps * B;
+  tile_len[t] = (long long)steps * 32;
 }
 
-__global__ void vl_fill_kernel(GridK g, int n, int A, int newton3, double rl2, int sentinel,
+__global__ void vl_fill_kernel(GridK g, int n, int A, int B, int pattern, int newton3, double rl2,
                                const double* __restrict__ pos4, const int32_t* __restrict__ os,
                                const int32_t* __restrict__ oc, const int32_t* __restrict__ hs,
                                const int32_t* __restrict__ hc, const long long* __restrict__ toff,
-                               const int32_t* __restrict__ kmax, int32_t* __restrict__ nbr) {
+                               int32_t* __restrict__ nbr) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int t = i / A, il = i - t * A;
-  int32_t* out = nbr + toff[t] + il;
+  int32_t* out = nbr + toff[t];
   int k = 0;
   const double4 pi = ld_pos4(pos4, i);
   if (pi.w == (double)LMD_OWNED) {
     const long long lin = cell_of_owned(pi, g.lo0, g.lo1, g.lo2, g.cl0, g.cl1, g.cl2, g.d0, g.d1,
                                         g.d2, g.t0, g.t1);
     for_candidates(i, pi, newton3, g.t0, g.t1, lin, os, oc, hs, hc, pos4, rl2, [&](int j) {
-      out[(long long)k * A] = j;
+      const int st = k / B, l = lane_of(pattern, il, k % B);
+      out[(long long)(st / kChunk) * (32 * kChunk) + l * kChunk + st % kChunk] = j;
       ++k;
     });
   }
-  const int km = kmax[t];
-  for (; k < km; ++k) out[(long long)k * A] = sentinel;
 }
 
-// padding entries of lanes past the last owned particle of the last tile
-__global__ void vl_tail_pad_kernel(int n, int A, int sentinel, const long long* __restrict__ toff,
-                                   const int32_t* __restrict__ kmax, int32_t* __restrict__ nbr) {
-  const int ntiles = (n + A - 1) / A;
-  const int t = ntiles - 1;
-  const int first_missing = n - t * A;
-  const int km = kmax[t];
-  for (int e = threadIdx.x; e < km * A; e += blockDim.x) {
-    const int il = e % A;
-    if (il >= first_missing) nbr[toff[t] + e] = sentinel;
-  }
+__global__ void fill_i32_kernel(int64_t n, int32_t v, int32_t* __restrict__ out) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x)
+    out[k] = v;
 }
 
 // ------------------------------------------------------------------ force
@@ -204,29 +211,27 @@ __device__ __forceinline__ void vl_tile(int t, int lane, int n_owned,
                                         double* __restrict__ fx, double* __restrict__ fy,
                                         double* __restrict__ fz) {
   using Pat = Pattern<P>;
-  constexpr int STRIDE = Pat::A * Pat::B;  // = 32 ints per fill
+  static_assert(U == kChunk || U == 2 * kChunk, "unroll must be one or two index chunks");
   const int io = Pat::ioff(lane), jo = Pat::joff(lane);
   const int i = t * Pat::A + io;
   const bool iact = i < n_owned;
   const double4 pi = ld_pos4(pos4, iact ? i : 0);
-  const int32_t* list = nbr + toff[t] + jo * Pat::A + io;
-  const int steps = kmax[t] / Pat::B;
+  const int4* chunks = reinterpret_cast<const int4*>(nbr + toff[t]) + lane;
+  const int nchunks = kmax[t] / Pat::B / kChunk;
   const double ax0 = a.ax, ay0 = a.ay, az0 = a.az;
   a.ax = a.ay = a.az = 0.0;
-  int s = 0;
-  for (; s + U <= steps; s += U) {
-    int j[U];
-    double4 pj[U];
+  // software pipeline: the next chunk's indices are in flight while the
+  // current chunk's positions are gathered and evaluated
+  int4 nxt = nchunks > 0 ? __ldg(chunks) : make_int4(0, 0, 0, 0);
+  for (int c = 0; c < nchunks; ++c) {
+    const int4 cur = nxt;
+    if (c + 1 < nchunks) nxt = __ldg(chunks + (long long)(c + 1) * 32);
+    const int j[4] = {cur.x, cur.y, cur.z, cur.w};
+    double4 pj[4];
 #pragma unroll
-    for (int u = 0; u < U; ++u) j[u] = __ldg(list + (long long)(s + u) * STRIDE);
+    for (int u = 0; u < 4; ++u) pj[u] = ld_j<SOA>(pos4, q, j[u]);
 #pragma unroll
-    for (int u = 0; u < U; ++u) pj[u] = ld_j<SOA>(pos4, q, j[u]);
-#pragma unroll
-    for (int u = 0; u < U; ++u) vl_pair<EV, N3>(pi, pj[u], j[u], n_owned, k, a, fx, fy, fz);
-  }
-  for (; s < steps; ++s) {
-    const int j = __ldg(list + (long long)s * STRIDE);
-    vl_pair<EV, N3>(pi, ld_j<SOA>(pos4, q, j), j, n_owned, k, a, fx, fy, fz);
+    for (int u = 0; u < 4; ++u) vl_pair<EV, N3>(pi, pj[u], j[u], n_owned, k, a, fx, fy, fz);
   }
   if (!iact) a.ax = a.ay = a.az = 0.0;
   const double rx = reduce_j<P>(a.ax), ry = reduce_j<P>(a.ay), rz = reduce_j<P>(a.az);
@@ -411,19 +416,16 @@ int lmd_vl_layout(int64_t n_owned, int pattern, const int32_t* count, int64_t* t
 int lmd_vl_fill(const lmd_grid* g, double rl2, int newton3, int pattern, int64_t n_owned,
                 int32_t sentinel, const double* pos4, const int32_t* o_start,
                 const int32_t* o_count, const int32_t* h_start, const int32_t* h_count,
-                const int64_t* tile_off, const int32_t* kmax, int32_t* nbr, void* stream) {
+                const int64_t* tile_off, int64_t total, int32_t* nbr, void* stream) {
   if (n_owned <= 0) return LMD_OK;
-  const int A = pattern_A(pattern);
+  const int A = pattern_A(pattern), B = pattern_B(pattern);
   cudaStream_t s = (cudaStream_t)stream;
-  vl_fill_kernel<<<(unsigned)cdiv(n_owned, 128), 128, 0, s>>>(
-      make_gridk(g), (int)n_owned, A, newton3, rl2, sentinel, pos4, o_start, o_count, h_start,
-      h_count, (const long long*)tile_off, kmax, nbr);
+  fill_i32_kernel<<<1184, 256, 0, s>>>(total, sentinel, nbr);
   LMD_CHECK_LAUNCH();
-  if (n_owned % A) {
-    vl_tail_pad_kernel<<<1, 256, 0, s>>>((int)n_owned, A, sentinel, (const long long*)tile_off,
-                                         kmax, nbr);
-    LMD_CHECK_LAUNCH();
-  }
+  vl_fill_kernel<<<(unsigned)cdiv(n_owned, 128), 128, 0, s>>>(
+      make_gridk(g), (int)n_owned, A, B, pattern, newton3, rl2, pos4, o_start, o_count, h_start,
+      h_count, (const long long*)tile_off, nbr);
+  LMD_CHECK_LAUNCH();
   return LMD_OK;
 }
 
@@ -471,13 +473,9 @@ static void launch_vl_u(int u, bool persistent, bool soa, int64_t n_owned, int64
 #define LMD_VLU(UU, SS)                                                                          \
   launch_vl<P, EV, N3, UU, SS>(persistent, n_owned, ntiles, pos4, q, tile_off, kmax, nbr, k, fx, \
                                fy, fz, ev, stats, s)
-  if (soa) {
-    if (u == 2) LMD_VLU(2, true);
-    else LMD_VLU(4, true);
-  } else {
-    if (u == 2) LMD_VLU(2, false);
-    else LMD_VLU(4, false);
-  }
+  (void)u;
+  if (soa) LMD_VLU(4, true);
+  else LMD_VLU(4, false);
 #undef LMD_VLU
 }
 
@@ -492,9 +490,9 @@ int lmd_force_vl(int pattern, int newton3, int flags, const lmd_lj* lj, int64_t 
   const int64_t ntiles = lmd_vl_num_tiles(n_owned, pattern);
   cudaStream_t s = (cudaStream_t)stream;
   const bool ev = (flags & LMD_FLAG_ENERGY) != 0;
-  // tuning knobs: bits 4-5 unroll (2 -> 2, else 4), bit 6 persistent grid;
+  // tuning knobs: bit 6 persistent grid;
   // soa != NULL gathers x, y, z from SoA arrays soa[0..ntot), soa[ntot..), ...
-  const int u = ((flags >> 4) & 3) == 2 ? 2 : 4;
+  const int u = 4;
   const bool persistent = (flags >> 6) & 1;
   const SoA q = {soa, soa ? soa + ntot : nullptr, soa ? soa + 2 * ntot : nullptr};
 #define LMD_VL(P, EVB, N3B)                                                                  \

@@ -208,7 +208,7 @@ class VerletListContainer:
             N.call("lmd_vl_fill", self.grid, float(rl2), int(newton3), pattern.code, n,
                    self.n_owned + self.n_halo, N.ptr(self._pos4), N.ptr(self._o_start),
                    N.ptr(self._o_count), N.ptr(self._h_start), N.ptr(self._h_count),
-                   N.ptr(tile_off), N.ptr(kmax), N.ptr(nbr), s)
+                   N.ptr(tile_off), total, N.ptr(nbr), s)
         hit = (tile_off, kmax, nbr, total)
         self._lists[key] = hit
         return hit
@@ -230,7 +230,9 @@ class VerletListContainer:
         i_idx = torch.repeat_interleave(torch.arange(n, device=count.device), count)
         first = torch.repeat_interleave(torch.cumsum(count, 0) - count, count)
         k = torch.arange(int(count.sum()), device=count.device) - first
-        j = nbr[(offs[i_idx] + k)].long()
+        # ONE_BY_V: step s = k // 32 on lane k % 32, lane-chunked by 4 steps
+        s_, lane = k // 32, k % 32
+        j = nbr[offs[i_idx] + (s_ // 4) * 128 + lane * 4 + s_ % 4].long()
         is_img = j >= n
         jid = torch.empty_like(j)
         jid[~is_img] = perm[j[~is_img]]
