@@ -211,7 +211,8 @@ __device__ __forceinline__ void vl_tile(int t, int lane, int n_owned,
                                         double* __restrict__ fx, double* __restrict__ fy,
                                         double* __restrict__ fz) {
   using Pat = Pattern<P>;
-  static_assert(U == kChunk || U == 2 * kChunk, "unroll must be one or two index chunks");
+  // U = positions gathered per group (2 or 4) within a 4-step index chunk
+  static_assert(U == 2 || U == 4, "gather group must divide the index chunk");
   const int io = Pat::ioff(lane), jo = Pat::joff(lane);
   const int i = t * Pat::A + io;
   const bool iact = i < n_owned;
@@ -227,11 +228,15 @@ __device__ __forceinline__ void vl_tile(int t, int lane, int n_owned,
     const int4 cur = nxt;
     if (c + 1 < nchunks) nxt = __ldg(chunks + (long long)(c + 1) * 32);
     const int j[4] = {cur.x, cur.y, cur.z, cur.w};
-    double4 pj[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) pj[u] = ld_j<SOA>(pos4, q, j[u]);
+    for (int g = 0; g < 4; g += U) {
+      double4 pj[U];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) vl_pair<EV, N3>(pi, pj[u], j[u], n_owned, k, a, fx, fy, fz);
+      for (int u = 0; u < U; ++u) pj[u] = ld_j<SOA>(pos4, q, j[g + u]);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        vl_pair<EV, N3>(pi, pj[u], j[g + u], n_owned, k, a, fx, fy, fz);
+    }
   }
   if (!iact) a.ax = a.ay = a.az = 0.0;
   const double rx = reduce_j<P>(a.ax), ry = reduce_j<P>(a.ay), rz = reduce_j<P>(a.az);
@@ -272,9 +277,10 @@ __device__ __forceinline__ void flush_acc(const Acc& a, int lane, bool live, boo
   }
 }
 
-// One warp per i-tile.
+// One warp per i-tile.  The 2-wide gather variant trades memory-level
+// parallelism per warp for occupancy (64 registers, 8 blocks per SM).
 template <int P, bool EV, bool N3, int U, bool SOA>
-__global__ void __launch_bounds__(32 * kVLWarps, 4)
+__global__ void __launch_bounds__(32 * kVLWarps, U == 2 ? 8 : 4)
     vl_force_kernel(int n_owned, int ntiles, const double* __restrict__ pos4, SoA q,
                     const long long* __restrict__ toff, const int32_t* __restrict__ kmax,
                     const int32_t* __restrict__ nbr, LJK k, double* __restrict__ fx,
@@ -292,7 +298,7 @@ __global__ void __launch_bounds__(32 * kVLWarps, 4)
 // Persistent variant: each block owns a contiguous (spatially coherent) run
 // of tiles, so the j positions its warps gather stay resident in its SM's L1.
 template <int P, bool EV, bool N3, int U, bool SOA>
-__global__ void __launch_bounds__(32 * kVLWarps, 4)
+__global__ void __launch_bounds__(32 * kVLWarps, U == 2 ? 8 : 4)
     vl_force_persistent_kernel(int n_owned, int ntiles, const double* __restrict__ pos4, SoA q,
                                const long long* __restrict__ toff,
                                const int32_t* __restrict__ kmax, const int32_t* __restrict__ nbr,
@@ -473,9 +479,13 @@ static void launch_vl_u(int u, bool persistent, bool soa, int64_t n_owned, int64
 #define LMD_VLU(UU, SS)                                                                          \
   launch_vl<P, EV, N3, UU, SS>(persistent, n_owned, ntiles, pos4, q, tile_off, kmax, nbr, k, fx, \
                                fy, fz, ev, stats, s)
-  (void)u;
-  if (soa) LMD_VLU(4, true);
-  else LMD_VLU(4, false);
+  if (soa) {
+    if (u == 2) LMD_VLU(2, true);
+    else LMD_VLU(4, true);
+  } else {
+    if (u == 2) LMD_VLU(2, false);
+    else LMD_VLU(4, false);
+  }
 #undef LMD_VLU
 }
 
@@ -490,9 +500,9 @@ int lmd_force_vl(int pattern, int newton3, int flags, const lmd_lj* lj, int64_t 
   const int64_t ntiles = lmd_vl_num_tiles(n_owned, pattern);
   cudaStream_t s = (cudaStream_t)stream;
   const bool ev = (flags & LMD_FLAG_ENERGY) != 0;
-  // tuning knobs: bit 6 persistent grid;
+  // tuning knobs: bits 4-5 == 2 -> 2-wide gathers (else 4), bit 6 persistent grid;
   // soa != NULL gathers x, y, z from SoA arrays soa[0..ntot), soa[ntot..), ...
-  const int u = 4;
+  const int u = ((flags >> 4) & 3) == 2 ? 2 : 4;
   const bool persistent = (flags >> 6) & 1;
   const SoA q = {soa, soa ? soa + ntot : nullptr, soa ? soa + 2 * ntot : nullptr};
 #define LMD_VL(P, EVB, N3B)                                                                  \

@@ -20,7 +20,7 @@ patterns = os.environ.get("PATTERNS", "v_by_one,half_by_two").split(",")
 for pname in patterns:
     pat = B.PatternKind(pname)
     for n3 in (False,):
-        for ucode, u, soa in ((0, 4, 0), (0, 4, 1)):
+        for ucode, u, soa in ((0, 4, 0), (2, 2, 0), (2, 2, 1)):
             for pers in (0, 1):
                 cont.knobs = (ucode << 4) | (pers << 6)
                 cont.use_soa = bool(soa)
