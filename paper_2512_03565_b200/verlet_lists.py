@@ -49,7 +49,7 @@ class VerletListContainer:
         self._counts: dict = {}
         self._stats_cache: dict = {}
         # kernel tuning knobs (csrc/vl.cu lmd_force_vl flags bits 4-6)
-        self.knobs = 0      # unroll 4, one warp per tile (tools/vl_variants.py)
+        self.knobs = 0x20   # 2-wide gathers at 8 blocks/SM (tools/vl_variants.py)
         self.use_soa = False  # True: gather SoA x, y, z instead of 256-bit pos4
 
     # ------------------------------------------------------------ protocol
