@@ -232,6 +232,27 @@ def build_phase(cfg, w, args, torch, N, dec=None):
     return phase, cont, buf, box, params, geo
 
 
+def committed_traffic(label):
+    """DRAM bytes per launch of this configuration's force kernel, from the
+    committed ncu capture (profiles/traffic.json), else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            return json.load(fh).get(label, {}).get("bytes")
+    except (OSError, ValueError):
+        return None
+
+
+def algorithmic_bytes(cfg, cont, stats, n):
+    """Bytes one force launch must move: positions (32 B pos4 per particle and
+    image), forces (24 B per owned particle) and, for Verlet lists, 4 B per
+    list entry (useful interactions)."""
+    images = getattr(cont, "n_halo", 0) or 0
+    b = 32 * (n + images) + 24 * n
+    if cfg.container.value == "vl":
+        b += 4 * stats.useful_interactions
+    return int(b)
+
+
 def finish(cfg, st, geo):
     from paper_2512_03565_b200 import KernelStats
     from paper_2512_03565_b200.containers import LinkedCellsContainer
@@ -441,7 +462,10 @@ def run_b200(args):
                          "flops_per_pair": FLOPS_PER_PAIR[cfg.newton3],
                          "kernel": "force kernel alone (CUDA events on its stream)",
                          "peak_source": "measured in this run: lmd_dfma_burn (DFMA, 2 flop)",
-                         "traffic": None},
+                         "traffic": committed_traffic(cfg.label),
+                         "algorithmic_bytes": algorithmic_bytes(cfg, cont, stats, n_local),
+                         "hbm_gbs_achieved": algorithmic_bytes(cfg, cont, stats, n_local)
+                         / avg_launch / 1e9},
             "e2e": e2e,
             "cpu_baseline": cpu,
             "gpu_launches": args.steps * phase.launches_per_step,
