@@ -296,6 +296,26 @@ int lmd_vcl_collect(int64_t n, const int32_t* order, const int32_t* slot, const 
                     const double* fy, const double* fz, double* ox, double* oy, double* oz,
                     void* stream);
 
+/* ----------------------------------------------- execute_packed (batched) */
+/* The reference's batched operator (executor.py:118-171) over an explicit
+ * unit list: unit u sweeps owned-backing i-span [i_off, i_off + i_len) x
+ * j-span [j_off, j_off + j_len) of the owned (j_halo = 0) or halo backing,
+ * Newton3 dual-write if newton3[u], self exclusion if same[u]
+ * (_sweep_span, executor.py:72-115).  Units are grouped by base: the bases of
+ * color c are [color_base_start[c], color_base_start[c+1]) (HOST array of
+ * n_colors + 1 entries); base b's units are base_units[base_start[b] ..
+ * base_start[b+1]) (device).  One launch per color, one warp per base.
+ * Forces ACCUMULATE (+=) into the SoA force arrays; pair_interactions and
+ * overlap accumulate into *stats.  own4 / halo4: pos4 backings. */
+int lmd_execute_packed(int64_t n_units, const int64_t* i_off, const int64_t* i_len,
+                       const int64_t* j_off, const int64_t* j_len, const uint8_t* j_halo,
+                       const uint8_t* newton3, const uint8_t* same, int n_colors,
+                       const int64_t* color_base_start, const int64_t* base_units,
+                       const int64_t* base_start, int pattern, const lmd_lj* lj,
+                       const double* own4, const double* halo4, double* ofx, double* ofy,
+                       double* ofz, double* hfx, double* hfy, double* hfz, lmd_stats* stats,
+                       void* stream);
+
 /* ------------------------------------------------ the functor (two buffers) */
 /* compute_pair_vectorized (kernels.py:377-424) on device buffers given as
  * pos4 (ownership in .w).  Forces ACCUMULATE (+=) into the SoA force arrays.

@@ -175,6 +175,9 @@ _sig("lmd_vcl_collect", _INT, _I64, *([_VP] * 8), _VP)
 _sig("lmd_lc_n3_ev_slots", _I64, C.POINTER(Grid))
 _sig("lmd_force_lc_n3", _INT, C.POINTER(Grid), C.POINTER(LJ), _INT, _INT, _INT, _VP, _I64,
      _VP, _VP, _VP, _VP, _VP, _INT, _VP, _VP, _VP, _VP, _VP, _VP)
+_sig("lmd_execute_packed", _INT, _I64, *([_VP] * 7), _INT, C.POINTER(C.c_int64), _VP, _VP, _INT,
+     C.POINTER(LJ),
+     *([_VP] * 9), _VP)
 _sig("lmd_scatter_forces", _INT, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP)
 
 

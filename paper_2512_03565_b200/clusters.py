@@ -213,6 +213,28 @@ class VerletClusterContainer:
         self._halo_ready = True
 
     # --------------------------------------------------------------- views
+    def kernel_backings(self):
+        """(owned, halo) padded backings as device views (containers.py:471-473)."""
+        M = self.cluster_size
+        n = self._own.ncl * M
+        nh = self._hal.ncl * M if self._halo_ready else 0
+        dev = self._pos4.device
+
+        def mk(a, b, fx, fy, fz):
+            p = self._pos4[a:b]
+            z = torch.zeros(b - a, dtype=torch.float64, device=dev)
+            return ParticleBuffer(pos_x=p[:, 0], pos_y=p[:, 1], pos_z=p[:, 2], vel_x=z, vel_y=z,
+                                  vel_z=z, force_x=fx, force_y=fy, force_z=fz, old_force_x=z,
+                                  old_force_y=z, old_force_z=z,
+                                  id=torch.full((b - a,), -1, dtype=torch.int64, device=dev),
+                                  ownership=p[:, 3].to(torch.int8))
+        if not hasattr(self, "_hfx") or self._hfx.shape[0] != max(nh, 1):
+            self._hfx = torch.zeros(max(nh, 1), dtype=torch.float64, device=dev)
+            self._hfy = torch.zeros(max(nh, 1), dtype=torch.float64, device=dev)
+            self._hfz = torch.zeros(max(nh, 1), dtype=torch.float64, device=dev)
+        return (mk(0, n, self._fx[:n], self._fy[:n], self._fz[:n]),
+                mk(n, n + nh, self._hfx[:nh], self._hfy[:nh], self._hfz[:nh]))
+
     @property
     def n_clusters(self) -> int:
         return self._own.ncl if self._own else 0
