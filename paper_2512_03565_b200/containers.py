@@ -294,7 +294,8 @@ class LinkedCellsContainer:
         m = b - a
         dev = self._pos4.device
         z = torch.zeros(m, dtype=torch.float64, device=dev)
-        ids = self._halo_ids if a >= self.n_owned else self._perm.long()
+        n = self.n_owned
+        ids = self._halo_ids[a - n:b - n] if a >= n else self._perm[a:b].long()
         return ParticleBuffer(pos_x=p[:, 0], pos_y=p[:, 1], pos_z=p[:, 2], vel_x=z, vel_y=z,
                               vel_z=z, force_x=self._fx[a:b], force_y=self._fy[a:b],
                               force_z=self._fz[a:b], old_force_x=z, old_force_y=z, old_force_z=z,
