@@ -39,6 +39,35 @@ struct Tile {
   static constexpr int A = Pattern<P>::A, B = Pattern<P>::B;
 };
 
+// visits every candidate j (index into the combined backing) of owned i
+template <typename F>
+__device__ __forceinline__ void for_candidates(int i, const double4& pi, int newton3, long long t0,
+                                               long long t1, long long lin,
+                                               const int32_t* __restrict__ os,
+                                               const int32_t* __restrict__ oc,
+                                               const int32_t* __restrict__ hs,
+                                               const int32_t* __restrict__ hc,
+                                               const double* __restrict__ pos4, double rl2,
+                                               F&& visit) {
+  for (int view = 0; view < 2; ++view) {
+    const int32_t* vs = view ? hs : os;
+    const int32_t* vc = view ? hc : oc;
+    for (int dz = -1; dz <= 1; ++dz)
+      for (int dy = -1; dy <= 1; ++dy)
+        for (int dx = -1; dx <= 1; ++dx) {
+          const long long nl = lin + dx + t0 * (dy + t1 * dz);
+          const int s = vs[nl], c = vc[nl];
+          for (int j = s; j < s + c; ++j) {
+            if (!view && (j == i || (newton3 && j < i))) continue;
+            const double4 pj = ld_pos4(pos4, j);
+            if (pj.w == (double)LMD_DUMMY) continue;
+            const double r2 = r2_exact(pi.x - pj.x, pi.y - pj.y, pi.z - pj.z);
+            if (r2 < rl2) visit(j);
+          }
+        }
+  }
+}
+
 __device__ __forceinline__ long long cell_of_owned(const double4& p, double lo0, double lo1,
                                                    double lo2, double cl0, double cl1, double cl2,
                                                    long long d0, long long d1, long long d2,
@@ -61,6 +90,23 @@ struct GridK {
   long long d0, d1, d2, t0, t1;
 };
 
+__global__ void vl_count_kernel(GridK g, int n, int newton3, double rl2,
+                                const double* __restrict__ pos4, const int32_t* __restrict__ os,
+                                const int32_t* __restrict__ oc, const int32_t* __restrict__ hs,
+                                const int32_t* __restrict__ hc, int32_t* __restrict__ count) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double4 pi = ld_pos4(pos4, i);
+  int c = 0;
+  if (pi.w == (double)LMD_OWNED) {
+    const long long lin = cell_of_owned(pi, g.lo0, g.lo1, g.lo2, g.cl0, g.cl1, g.cl2, g.d0, g.d1,
+                                        g.d2, g.t0, g.t1);
+    for_candidates(i, pi, newton3, g.t0, g.t1, lin, os, oc, hs, hc, pos4, rl2,
+                   [&](int) { ++c; });
+  }
+  count[i] = c;
+}
+
 __global__ void vl_tile_kernel(int n, int A, int B, const int32_t* __restrict__ count,
                                long long* __restrict__ tile_len, int32_t* __restrict__ kmax) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -74,59 +120,26 @@ __global__ void vl_tile_kernel(int n, int A, int B, const int32_t* __restrict__ 
   tile_len[t] = (long long)steps * 32;
 }
 
-
-// Warp-cooperative build: one warp per owned i; the lanes sweep the
-// candidates of each neighbour-cell view 32 at a time and compact the
-// accepted ones with a ballot, so the entries keep the candidate order of
-// for_candidates (views, then cells in product order, then ascending j).
-// count_only: write count[i]; else write the entries into the lane-chunked
-// layout at the tile's offset.
-template <bool COUNT>
-__global__ void __launch_bounds__(128)
-    vl_build_warp_kernel(GridK g, int n, int A, int B, int pattern, int newton3, double rl2,
-                         const double* __restrict__ pos4, const int32_t* __restrict__ os,
-                         const int32_t* __restrict__ oc, const int32_t* __restrict__ hs,
-                         const int32_t* __restrict__ hc, const long long* __restrict__ toff,
-                         int32_t* __restrict__ count, int32_t* __restrict__ nbr) {
-  const int lane = threadIdx.x & 31;
-  const int i = blockIdx.x * 4 + (threadIdx.x >> 5);
+__global__ void vl_fill_kernel(GridK g, int n, int A, int B, int pattern, int newton3, double rl2,
+                               const double* __restrict__ pos4, const int32_t* __restrict__ os,
+                               const int32_t* __restrict__ oc, const int32_t* __restrict__ hs,
+                               const int32_t* __restrict__ hc, const long long* __restrict__ toff,
+                               int32_t* __restrict__ nbr) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const double4 pi = ld_pos4(pos4, i);
+  const int t = i / A, il = i - t * A;
+  int32_t* out = nbr + toff[t];
   int k = 0;
+  const double4 pi = ld_pos4(pos4, i);
   if (pi.w == (double)LMD_OWNED) {
     const long long lin = cell_of_owned(pi, g.lo0, g.lo1, g.lo2, g.cl0, g.cl1, g.cl2, g.d0, g.d1,
                                         g.d2, g.t0, g.t1);
-    const int t = i / A, il = i - t * A;
-    int32_t* out = COUNT ? nullptr : nbr + toff[t];
-    for (int view = 0; view < 2; ++view) {
-      const int32_t* vs = view ? hs : os;
-      const int32_t* vc = view ? hc : oc;
-      for (int dz = -1; dz <= 1; ++dz)
-        for (int dy = -1; dy <= 1; ++dy)
-          for (int dx = -1; dx <= 1; ++dx) {
-            const long long nl = lin + dx + g.t0 * (dy + g.t1 * dz);
-            const int s0 = vs[nl], c0 = vc[nl];
-            for (int base = 0; base < c0; base += 32) {
-              const int j = s0 + base + lane;
-              bool ok = base + lane < c0;
-              if (ok && !view && (j == i || (newton3 && j < i))) ok = false;
-              if (ok) {
-                const double4 pj = ld_pos4(pos4, j);
-                ok = pj.w != (double)LMD_DUMMY &&
-                     r2_exact(pi.x - pj.x, pi.y - pj.y, pi.z - pj.z) < rl2;
-              }
-              const unsigned m = __ballot_sync(0xffffffffu, ok);
-              if (!COUNT && ok) {
-                const int kk = k + __popc(m & ((1u << lane) - 1u));
-                const int st = kk / B, l = lane_of(pattern, il, kk % B);
-                out[(long long)(st / kChunk) * (32 * kChunk) + l * kChunk + st % kChunk] = j;
-              }
-              k += __popc(m);
-            }
-          }
-    }
+    for_candidates(i, pi, newton3, g.t0, g.t1, lin, os, oc, hs, hc, pos4, rl2, [&](int j) {
+      const int st = k / B, l = lane_of(pattern, il, k % B);
+      out[(long long)(st / kChunk) * (32 * kChunk) + l * kChunk + st % kChunk] = j;
+      ++k;
+    });
   }
-  if (COUNT && lane == 0) count[i] = k;
 }
 
 __global__ void fill_i32_kernel(int64_t n, int32_t v, int32_t* __restrict__ out) {
@@ -372,9 +385,8 @@ int lmd_vl_count(const lmd_grid* g, double rl2, int newton3, int64_t n_owned, co
                  const int32_t* h_count, int32_t* count, void* stream) {
   if (n_owned <= 0) return LMD_OK;
   if (n_owned > 0x7fffffffLL) return LMD_ERR_CONFIG;
-  vl_build_warp_kernel<true><<<(unsigned)cdiv(n_owned, 4), 128, 0, (cudaStream_t)stream>>>(
-      make_gridk(g), (int)n_owned, 1, 1, 0, newton3, rl2, pos4, o_start, o_count, h_start,
-      h_count, nullptr, count, nullptr);
+  vl_count_kernel<<<(unsigned)cdiv(n_owned, 128), 128, 0, (cudaStream_t)stream>>>(
+      make_gridk(g), (int)n_owned, newton3, rl2, pos4, o_start, o_count, h_start, h_count, count);
   LMD_CHECK_LAUNCH();
   return LMD_OK;
 }
@@ -416,9 +428,9 @@ int lmd_vl_fill(const lmd_grid* g, double rl2, int newton3, int pattern, int64_t
   cudaStream_t s = (cudaStream_t)stream;
   fill_i32_kernel<<<1184, 256, 0, s>>>(total, sentinel, nbr);
   LMD_CHECK_LAUNCH();
-  vl_build_warp_kernel<false><<<(unsigned)cdiv(n_owned, 4), 128, 0, s>>>(
+  vl_fill_kernel<<<(unsigned)cdiv(n_owned, 128), 128, 0, s>>>(
       make_gridk(g), (int)n_owned, A, B, pattern, newton3, rl2, pos4, o_start, o_count, h_start,
-      h_count, (const long long*)tile_off, nullptr, nbr);
+      h_count, (const long long*)tile_off, nbr);
   LMD_CHECK_LAUNCH();
   return LMD_OK;
 }
@@ -493,17 +505,17 @@ int lmd_force_vl(int pattern, int newton3, int flags, const lmd_lj* lj, int64_t 
   const int u = ((flags >> 4) & 3) == 2 ? 2 : 4;
   const bool persistent = (flags >> 6) & 1;
   const SoA q = {soa, soa ? soa + ntot : nullptr, soa ? soa + 2 * ntot : nullptr};
-#define LMD_VL(P, EVB, N3B)                                                                  \
+#define LMD_VLK(P, EVB, N3B)                                                                  \
   launch_vl_u<P, EVB, N3B>(u, persistent, soa != nullptr, n_owned, ntiles, pos4, q, tile_off,  \
                            kmax, nbr, k, fx, fy, fz, ev_scratch, stats, s)
 #define LMD_VL_P(P)                         \
   do {                                      \
     if (ev) {                               \
-      if (newton3) LMD_VL(P, true, true);   \
-      else LMD_VL(P, true, false);          \
+      if (newton3) LMD_VLK(P, true, true);   \
+      else LMD_VLK(P, true, false);          \
     } else {                                \
-      if (newton3) LMD_VL(P, false, true);  \
-      else LMD_VL(P, false, false);         \
+      if (newton3) LMD_VLK(P, false, true);  \
+      else LMD_VLK(P, false, false);         \
     }                                       \
   } while (0)
   switch (pattern) {
@@ -514,7 +526,7 @@ int lmd_force_vl(int pattern, int newton3, int flags, const lmd_lj* lj, int64_t 
     default: return LMD_ERR_CONFIG;
   }
 #undef LMD_VL_P
-#undef LMD_VL
+#undef LMD_VLK
   LMD_CHECK_LAUNCH();
   if (ev) {
     const int64_t slots = persistent ? (int64_t)g_persistent_blocks * kVLWarps
