@@ -332,7 +332,17 @@ def run_b200(args):
                                  params0.interaction_length, rank, world, grid=grid)
     else:
         w = make_workload(args, "cuda", 42)
-    phase, cont, buf, box, params, geo = build_phase(cfg, w, args, torch, N, dec)
+    dec_error = None
+    try:
+        phase, cont, buf, box, params, geo = build_phase(cfg, w, args, torch, N, dec)
+    except Exception as exc:  # the decomposed path could not be built: say so, run replicas
+        if dec is None:
+            raise
+        dec_error = f"{type(exc).__name__}: {exc}"[:300]
+        print(f"[bench] brick decomposition failed on rank {rank}: {dec_error}", file=sys.stderr)
+        dec = None
+        w = make_workload(args, "cuda", 42 + rank)
+        phase, cont, buf, box, params, geo = build_phase(cfg, w, args, torch, N, None)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     peak = fp64_peak_tflops(torch, N)
 
@@ -455,7 +465,10 @@ def run_b200(args):
                        "kernel_ms_rank0": avg_launch * 1e3,
                        "l2": "flushed (256 MiB write) before every timed step",
                        "parallelism": (f"bricks {dec.grid}, NCCL P2P ghost exchange"
-                                       if dec else "single"),
+                                       if dec else ("replicas (decomposition failed: "
+                                                    f"{dec_error})" if dec_error
+                                                    else ("replicas" if world > 1
+                                                          else "single"))),
                        "inputs": w.note},
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved / peak,
