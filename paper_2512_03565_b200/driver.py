@@ -44,7 +44,7 @@ def force_phase(owned, box, params, config: Configuration, vector_width: int,
     box = as_box(box)
     dev_owned = device_soa(owned)
     cont = make_container(config.container, box, params,
-                          cluster_size=cluster_size or vector_width)
+                          cluster_size=config.cluster_size or cluster_size or vector_width)
     cont.rebuild(dev_owned)
     cont.refresh(dev_owned)
     stats = cont.compute_forces(config.traversal, config.newton3, as_pattern(config.pattern),

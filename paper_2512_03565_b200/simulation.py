@@ -159,12 +159,13 @@ def run_md(owned, box, params, iterations: int, vector_width: int = 8, *,
                 cfg, phase = tuner.next_configuration(it)
             else:
                 cfg, phase = fixed_config, PRODUCTION
-            cont = containers.get(cfg.container)
+            ckey = (cfg.container, cfg.cluster_size)
+            cont = containers.get(ckey)
             if cont is None:
                 kw = {} if rebuild_period is None else {"rebuild_period": rebuild_period}
-                cont = make_container(cfg.container, box, params,
-                                      cluster_size=cluster_size or vector_width, **kw)
-                containers[cfg.container] = cont
+                m = cfg.cluster_size or cluster_size or vector_width
+                cont = make_container(cfg.container, box, params, cluster_size=m, **kw)
+                containers[ckey] = cont
             rebuilt = False
             if cont.reference_positions is None:
                 cont.rebuild(owned)

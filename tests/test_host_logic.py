@@ -162,3 +162,15 @@ def test_lane_ops_and_replay_metrics(tmp_path):
     path.write_text("1.5\n\n2\n")
     r = ReplayMetric(str(path))
     assert r.end_region() == 1.5 and r.end_region() == 2.0
+
+
+def test_cluster_size_is_a_tuning_dimension():
+    space = enumerate_search_space([ContainerKind.LINKED_CELLS, ContainerKind.VERLET_CLUSTER_LISTS],
+                                   [TraversalKind.LC_C08, TraversalKind.VCL], [False],
+                                   [PatternKind.ONE_BY_V], cluster_sizes=[4, 8, 32])
+    assert [c.label for c in space] == ["lc,lc_c08,false,one_by_v",
+                                        "vcl,vcl,false,one_by_v,m4", "vcl,vcl,false,one_by_v,m8",
+                                        "vcl,vcl,false,one_by_v,m32"]
+    assert Configuration.parse("vcl,vcl,true,half_by_two,m8").cluster_size == 8
+    with pytest.raises(ConfigurationError):
+        Configuration.parse("lc,lc_c08,true,half_by_two,m8")
