@@ -1,0 +1,98 @@
+"""Run the BASELINE MD configurations on one GPU and report particle-steps/s.
+
+    python tools/md_configs.py --config 1            # 8,000 lattice, LC c08 N3, 1 + 10 steps
+    python tools/md_configs.py --config 3 --steps 300 # droplet, VCL M in {4,8,32}, tuner / 100
+    python tools/md_configs.py --config 5 --steps 400 # 8.4M gas, tuner / 200 over LC x VL
+
+Every step runs the whole velocity-Verlet step on the device (integrator,
+boundaries, neighbour maintenance, images, force phase) through
+``paper_2512_03565_b200.run_md``.  One JSON line per run.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2512_03565_b200 as B  # noqa: E402
+from paper_2512_03565_b200 import workloads  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=None)
+    ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--metric", default="time")
+    args = ap.parse_args()
+    torch.cuda.set_device(0)
+    t_gen = time.perf_counter()
+    if args.config == 1:
+        w = workloads.config1()
+        params = B.LJParams(cutoff=2.5, skin=0.0, dt=0.001)
+        fixed = B.Configuration.parse("lc,lc_c08,true,one_by_v")
+        configs, interval, steps = None, None, args.steps or 10
+    elif args.config == 3:
+        w = workloads.config3(n=args.n or 2_000_000, device="cuda")
+        params = B.LJParams(cutoff=3.0, skin=0.3, dt=0.001)
+        fixed = None
+        configs = B.enumerate_search_space([B.ContainerKind.VERLET_CLUSTER_LISTS],
+                                           [B.TraversalKind.VCL], [False],
+                                           [B.PatternKind.V_BY_ONE, B.PatternKind.HALF_BY_TWO],
+                                           cluster_sizes=[4, 8, 32])
+        interval, steps = 100, args.steps or 1000
+    elif args.config == 5:
+        w = workloads.config5(n=args.n or 8_388_608, device="cuda")
+        params = B.LJParams(cutoff=2.5, skin=0.3, dt=0.001)
+        fixed = None
+        configs = B.enumerate_search_space([B.ContainerKind.LINKED_CELLS,
+                                            B.ContainerKind.VERLET_LISTS],
+                                           [B.TraversalKind.LC_C01, B.TraversalKind.VL],
+                                           [False], [B.PatternKind.V_BY_ONE,
+                                                     B.PatternKind.HALF_BY_TWO,
+                                                     B.PatternKind.TWO_BY_HALF])
+        interval, steps = 200, args.steps or 2000
+    else:
+        raise SystemExit("configs 1, 3 and 5 run here (2 is bench.py, 4 is multi-GPU)")
+    t_gen = time.perf_counter() - t_gen
+    box = B.SimulationBox.cube(w.box_length, periodic=True)
+    pos = w.positions if isinstance(w.positions, torch.Tensor) else torch.as_tensor(w.positions)
+    buf = B.ParticleBuffer.from_positions(pos.cpu().numpy(), device="cuda")
+    v = torch.as_tensor(w.velocities).to("cuda", torch.float64)
+    buf.vel_x.copy_(v[:, 0]); buf.vel_y.copy_(v[:, 1]); buf.vel_z.copy_(v[:, 2])
+    seed_cfg = fixed or configs[0]
+    B.force_phase(buf, box, params, seed_cfg, 8)            # forces for the first kick
+    torch.cuda.synchronize()
+    policy = None
+    if configs:
+        policy = B.TuningPolicy(1, interval, "mean", args.metric)
+    records, summary = B.run_md(buf, box, params, steps, 8, configurations=configs,
+                                fixed_config=fixed, policy=policy, metric=args.metric,
+                                retune_drift=0.2 if configs else None)
+    pairs = sum(r.pair_interactions for r in records)
+    out = {
+        "config": args.config, "workload": w.name, "particles": len(buf), "steps": steps,
+        "particle_steps_per_s": summary.particle_steps_per_s,
+        "wall_s": summary.wall_time_s, "force_time_s": summary.force_time_s,
+        "pair_interactions_per_s_force": pairs / max(summary.force_time_s, 1e-12),
+        "pair_interactions_per_step_last": records[-1].pair_interactions,
+        "phase_selections": summary.phase_selections, "retunes": summary.retunes,
+        "initial_max_per_cell": summary.initial_max_per_cell,
+        "final_max_per_cell": summary.final_max_per_cell,
+        "generation_s": t_gen, "note": w.note,
+    }
+    if args.config == 1:
+        out["pairs_per_step"] = [r.pair_interactions for r in records]
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
