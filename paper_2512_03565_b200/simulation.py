@@ -116,10 +116,22 @@ def run_md(owned, box, params, iterations: int, vector_width: int = 8, *,
            configurations=None, fixed_config: Configuration | None = None,
            policy: TuningPolicy | None = None, metric: str = "time",
            cluster_size: int | None = None, rebuild_period: int | None = None,
-           retune_drift: float | None = None, energy: bool = False, record: bool = True):
+           retune_drift: float | None = None, energy: bool = False, record: bool = True,
+           wrap: str = "always"):
     """Run ``iterations`` MD steps on device-resident ``owned`` (our ParticleBuffer).
 
-    Returns (records, summary).  With ``fixed_config`` the tuner is off."""
+    Returns (records, summary).  With ``fixed_config`` the tuner is off.
+
+    ``wrap="always"`` applies the boundaries after every step as the
+    reference does (driver.py:214); in a large periodic system some particle
+    then wraps every step, its displacement looks like a box length and
+    ``needs_rebuild`` fires every step, so every tuning sample is displaced.
+    ``wrap="at_rebuild"`` keeps positions unwrapped between rebuilds and
+    wraps them just before a rebuild (the usual MD practice): rebuilds follow
+    the skin/period rule and the tuner can finish its phases.  Forces are the
+    same up to rounding of the unwrapped coordinates."""
+    if wrap not in ("always", "at_rebuild"):
+        raise ConfigurationError(f"unknown wrap policy {wrap!r}")
     validate_vector_width(vector_width)
     box = as_box(box)
     if fixed_config is None:
@@ -167,13 +179,13 @@ def run_md(owned, box, params, iterations: int, vector_width: int = 8, *,
                 cont = make_container(cfg.container, box, params, cluster_size=m, **kw)
                 containers[ckey] = cont
             rebuilt = False
-            if cont.reference_positions is None:
+            fresh = cont.reference_positions is None
+            if fresh or cont.needs_rebuild(owned):
+                if wrap == "at_rebuild":
+                    apply_boundaries(owned, box)
                 cont.rebuild(owned)
                 cont.refresh(owned)
-            elif cont.needs_rebuild(owned):
-                cont.rebuild(owned)
-                cont.refresh(owned)
-                rebuilt = True
+                rebuilt = not fresh
             else:
                 cont.refresh(owned)
             cont.steps_since_rebuild += 1
@@ -190,7 +202,8 @@ def run_md(owned, box, params, iterations: int, vector_width: int = 8, *,
             if tuner is not None:
                 tuner.record_sample(sample, displaced=rebuilt)
             velocity_verlet_step(owned, params, POST_FORCE, check=False)
-            apply_boundaries(owned, box)
+            if wrap == "always":
+                apply_boundaries(owned, box)
             if record:
                 records.append(IterationRecord(it, phase, cfg, sample, stats.lane_slots,
                                                stats.useful_interactions, stats.blank_lanes,
@@ -202,6 +215,8 @@ def run_md(owned, box, params, iterations: int, vector_width: int = 8, *,
     except SimulationDivergedError as exc:
         exc.records = records
         raise
+    if wrap == "at_rebuild":
+        apply_boundaries(owned, box)
     torch.cuda.synchronize()
     wall = time.perf_counter() - start
     speed = torch.sqrt(owned.vel_x ** 2 + owned.vel_y ** 2 + owned.vel_z ** 2)

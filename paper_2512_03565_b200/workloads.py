@@ -36,11 +36,12 @@ class Workload:
 
 def maxwell_boltzmann(n: int, temperature: float, seed: int, mass: float = 1.0,
                       device="cpu") -> torch.Tensor:
-    """N(0, sqrt(T/m)) per component, centre-of-mass velocity removed."""
-    g = torch.Generator(device="cpu").manual_seed(int(seed))
-    v = torch.randn((n, 3), generator=g, dtype=torch.float64) * math.sqrt(temperature / mass)
-    v -= v.mean(dim=0, keepdim=True)
-    return v.to(device)
+    """N(0, sqrt(T/m)) per component (numpy default_rng(seed)), centre-of-mass
+    velocity removed -- the construction of SURVEY.md §8(d)."""
+    rng = np.random.default_rng(int(seed))
+    v = rng.normal(0.0, math.sqrt(temperature / mass), (n, 3))
+    v -= v.mean(axis=0)
+    return torch.from_numpy(v).to(device)
 
 
 def rsa_positions(n: int, length: float, dmin: float, seed: int, device="cpu",

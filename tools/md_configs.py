@@ -76,7 +76,8 @@ def main():
         policy = B.TuningPolicy(1, interval, "mean", args.metric)
     records, summary = B.run_md(buf, box, params, steps, 8, configurations=configs,
                                 fixed_config=fixed, policy=policy, metric=args.metric,
-                                retune_drift=0.2 if configs else None)
+                                retune_drift=0.2 if configs else None,
+                                wrap="always" if args.config == 1 else "at_rebuild")
     pairs = sum(r.pair_interactions for r in records)
     out = {
         "config": args.config, "workload": w.name, "particles": len(buf), "steps": steps,
@@ -88,6 +89,8 @@ def main():
         "initial_max_per_cell": summary.initial_max_per_cell,
         "final_max_per_cell": summary.final_max_per_cell,
         "generation_s": t_gen, "note": w.note,
+        "tuning_iterations": sum(r.phase == "tuning" for r in records),
+        "configs_seen": sorted({r.configuration.label for r in records}),
     }
     if args.config == 1:
         out["pairs_per_step"] = [r.pair_interactions for r in records]
