@@ -112,6 +112,9 @@ class VerletListContainer:
         self._fy = torch.zeros(max(n, 1), dtype=torch.float64, device=dev)
         self._fz = torch.zeros(max(n, 1), dtype=torch.float64, device=dev)
         self._load_positions(d, halo if self._external_halo else None)
+        # lists are built lazily per interaction order: always from the
+        # rebuild-time positions, whatever the particles did since
+        self._build_pos4 = self._pos4.clone()
         self._lists.clear()
         self._counts.clear()
         self._stats_cache.clear()
@@ -175,7 +178,8 @@ class VerletListContainer:
             n = self.n_owned
             c = torch.zeros(max(n, 1), dtype=torch.int32, device=self._pos4.device)
             rl2 = self.params.interaction_length * self.params.interaction_length
-            N.call("lmd_vl_count", self.grid, float(rl2), int(newton3), n, N.ptr(self._pos4),
+            N.call("lmd_vl_count", self.grid, float(rl2), int(newton3), n,
+                   N.ptr(self._build_pos4),
                    N.ptr(self._o_start), N.ptr(self._o_count), N.ptr(self._h_start),
                    N.ptr(self._h_count), N.ptr(c), N.stream())
             self._counts[newton3] = c
@@ -206,7 +210,7 @@ class VerletListContainer:
         if n:
             rl2 = self.params.interaction_length * self.params.interaction_length
             N.call("lmd_vl_fill", self.grid, float(rl2), int(newton3), pattern.code, n,
-                   self.n_owned + self.n_halo, N.ptr(self._pos4), N.ptr(self._o_start),
+                   self.n_owned + self.n_halo, N.ptr(self._build_pos4), N.ptr(self._o_start),
                    N.ptr(self._o_count), N.ptr(self._h_start), N.ptr(self._h_count),
                    N.ptr(tile_off), total, N.ptr(nbr), s)
         hit = (tile_off, kmax, nbr, total)

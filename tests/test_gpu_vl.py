@@ -91,3 +91,25 @@ def test_vl_overlap_raises():
         B.force_phase(ParticleBuffer.from_positions(pos, device="cuda"),
                       SimulationBox.cube(9.0, periodic=False), LJParams(cutoff=2.2, skin=0.4),
                       cfg, 8)
+
+
+def test_lists_for_a_new_pattern_use_rebuild_positions(rng):
+    """A list built lazily after the particles moved must still be the
+    rebuild-time list (tile sizes were counted then)."""
+    pos, span = _state(rng, 5000, 0.8)
+    params = LJParams(cutoff=2.5, skin=0.3)
+    box = SimulationBox.cube(span, periodic=True)
+    cont = B.VerletListContainer(box, params)
+    buf = ParticleBuffer.from_positions(pos, device="cuda")
+    cont.rebuild(buf)
+    cont.refresh(buf)
+    st1 = cont.compute_forces("vl", False, PatternKind.V_BY_ONE, 8)
+    moved = np.mod(pos + rng.uniform(-0.07, 0.07, pos.shape), span)
+    buf2 = ParticleBuffer.from_positions(moved, device="cuda")
+    cont.refresh(buf2)
+    for pat in PatternKind:
+        st = cont.compute_forces("vl", False, pat, 8)
+        assert st.useful_interactions == st1.useful_interactions
+        of, ost = O.force_phase_lc(moved, np.zeros(3), np.full(3, span), [True] * 3,
+                                   LJParams(cutoff=2.5, skin=0.0), "lc_c01", False, "one_by_v", 8)
+        assert st.pair_interactions == ost.pair_interactions
