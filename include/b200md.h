@@ -237,6 +237,38 @@ int lmd_vl_fill(const lmd_grid* g, double rl2, int newton3, int pattern, int64_t
                 int32_t sentinel, const double* pos4, const int32_t* o_start,
                 const int32_t* o_count, const int32_t* h_start, const int32_t* h_count,
                 const int64_t* tile_off, int64_t total, int32_t* nbr, void* stream);
+/* Single-pass build (what the containers use): same lists and lane layout
+ * as count/layout/fill, but tile t starts at tile_off[t] = t * cap_steps * 32
+ * (cap_steps a multiple of 4), so no count pass, scan or prefill is needed;
+ * nbr holds ceil(n_owned / A) * cap_steps * 32 entries.  Writes count[i],
+ * tile_off, kmax and *max_count = the longest list; if *max_count >
+ * cap_steps * B the lists were truncated and the caller must rebuild with a
+ * larger capacity. */
+int lmd_vl_build(const lmd_grid* g, double rl2, int newton3, int pattern, int64_t n_owned,
+                 int32_t sentinel, const double* pos4, const int32_t* o_start,
+                 const int32_t* o_count, const int32_t* h_start, const int32_t* h_count,
+                 int32_t cap_steps, int32_t* count, int64_t* tile_off, int32_t* kmax,
+                 int32_t* max_count, int32_t* nbr, void* stream);
+/* i-cluster lists (csrc/vl_ci.cu), full lists only: each cell's owned
+ * particles are cut into clusters of up to ci (2 or 4) consecutive backing
+ * slots, cluster c = [cl_first[c], cl_first[c] + cl_len[c]); its list is the
+ * union of its members' lists.  Layout and capacity as lmd_vl_build with
+ * clusters in place of particles; count[i] = each member's own list length.
+ * The force entry tests every entry against all members: same pairs, forces
+ * and counts as lmd_force_vl with newton3 = 0; ev_scratch holds
+ * 2 * lmd_vl_ci_ev_slots(n_clusters, pattern) doubles. */
+int lmd_vl_ci_build(const lmd_grid* g, double rl2, int pattern, int ci, int64_t n_clusters,
+                    const int32_t* cl_first, const int32_t* cl_len, int32_t sentinel,
+                    const double* pos4, const int32_t* o_start, const int32_t* o_count,
+                    const int32_t* h_start, const int32_t* h_count, int32_t cap_steps,
+                    int32_t* count, int64_t* tile_off, int32_t* kmax, int32_t* max_count,
+                    int32_t* nbr, void* stream);
+int64_t lmd_vl_ci_ev_slots(int64_t n_clusters, int pattern);
+int lmd_force_vl_ci(int pattern, int ci, int flags, const lmd_lj* lj, int64_t n_owned,
+                    int64_t n_clusters, const int32_t* cl_first, const int32_t* cl_len,
+                    const double* pos4, const int64_t* tile_off, const int32_t* kmax,
+                    const int32_t* nbr, double* fx, double* fy, double* fz, double* ev_scratch,
+                    lmd_stats* stats, void* stream);
 /* Force over the lists: one warp per i-tile, lanes by `pattern`; positions
  * are pos4 over the combined backing plus one sentinel record (256-bit
  * gathers), or, if soa != NULL, SoA copies x = soa[0..ntot), y, z of the

@@ -157,7 +157,14 @@ _sig("lmd_vl_scan_temp_bytes", _SZ, _I64)
 _sig("lmd_vl_layout", _INT, _I64, _INT, _VP, _VP, _VP, _VP, _VP, _SZ, _VP)
 _sig("lmd_vl_fill", _INT, C.POINTER(Grid), _D, _INT, _INT, _I64, _I32, _VP, _VP, _VP, _VP, _VP,
      _VP, _I64, _VP, _VP)
+_sig("lmd_vl_build", _INT, C.POINTER(Grid), _D, _INT, _INT, _I64, _I32, _VP, _VP, _VP, _VP, _VP,
+     _I32, _VP, _VP, _VP, _VP, _VP, _VP)
 _sig("lmd_vl_ev_slots", _I64, _I64, _INT)
+_sig("lmd_vl_ci_build", _INT, C.POINTER(Grid), _D, _INT, _INT, _I64, _VP, _VP, _I32, _VP, _VP,
+     _VP, _VP, _VP, _I32, _VP, _VP, _VP, _VP, _VP, _VP)
+_sig("lmd_vl_ci_ev_slots", _I64, _I64, _INT)
+_sig("lmd_force_vl_ci", _INT, _INT, _INT, _INT, C.POINTER(LJ), _I64, _I64, _VP, _VP, _VP, _VP,
+     _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP)
 _sig("lmd_force_vl", _INT, _INT, _INT, _INT, C.POINTER(LJ), _I64, _VP, _VP, _I64, _VP, _VP,
      _VP, _VP, _VP, _VP, _VP, _VP, _VP)
 _sig("lmd_vl_stats", _INT, _I64, _INT, _INT, _INT, _VP, _VP, _VP)

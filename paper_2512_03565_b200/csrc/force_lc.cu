@@ -31,8 +31,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
   const long long warp = (long long)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
   const long long nowned = d0 * d1 * d2;
   double e_acc = 0.0, v_acc = 0.0;
-  long long pairs = 0, pairs_halo = 0;
-  int overlap = 0;
+  int pairs = 0, pairs_halo = 0, overlap = 0;   // per lane; widened in the warp sums
   if (warp < nowned) {
     const long long cx = warp % d0 + 1;
     const long long cy = (warp / d0) % d1 + 1;
@@ -61,6 +60,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
         const int js = __shfl_sync(0xffffffffu, nb_s, d);
         const int jn = __shfl_sync(0xffffffffu, nb_n, d);
         const int mult = __shfl_sync(0xffffffffu, nb_m, d);
+        const double fm = (double)mult;
         for (int cj = 0; cj < jn; cj += Pat::B) {
           const int jl = cj + jo;
           const int j = js + jl;
@@ -75,14 +75,14 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
             continue;
           }
           double s6;
-          const double f = lj_scalar(r2, k, s6) * (double)mult;
+          const double f = lj_scalar(r2, k, s6) * fm;
           ax = fma(f, dx, ax);
           ay = fma(f, dy, ay);
           az = fma(f, dz, az);
           pairs += mult;
           if (pj.w != (double)LMD_OWNED) pairs_halo += mult;
           if (EV) {
-            e_acc = fma((0.5 * mult) * s6, fma(k.eps4, s6, -k.eps4), e_acc);
+            e_acc = fma((0.5 * fm) * s6, fma(k.eps4, s6, -k.eps4), e_acc);
             v_acc = fma(0.5 * f, r2, v_acc);
           }
         }
@@ -97,13 +97,12 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
       }
     }
   }
-  pairs = warp_sum_ll(pairs);
-  pairs_halo = warp_sum_ll(pairs_halo);
+  const long long pr = warp_sum_ll((long long)pairs);
+  const long long ph = warp_sum_ll((long long)pairs_halo);
   overlap = __any_sync(0xffffffffu, overlap);
   if (lane == 0 && warp < nowned) {
-    if (pairs) atomicAdd((unsigned long long*)&stats->pair_interactions, (unsigned long long)pairs);
-    if (pairs_halo)
-      atomicAdd((unsigned long long*)&stats->pairs_owned_halo, (unsigned long long)pairs_halo);
+    if (pr) atomicAdd((unsigned long long*)&stats->pair_interactions, (unsigned long long)pr);
+    if (ph) atomicAdd((unsigned long long*)&stats->pairs_owned_halo, (unsigned long long)ph);
     if (overlap) atomicOr(&stats->overlap, 1);
   }
   if (EV) {
@@ -243,16 +242,13 @@ int lmd_force_lc(const lmd_grid* g, const lmd_lj* lj, int pattern, int flags,
   const unsigned blocks = (unsigned)cdiv(nowned, kWarpsPerBlock);
   const bool ev = (flags & LMD_FLAG_ENERGY) != 0;
   cudaStream_t s = (cudaStream_t)stream;
-#define LMD_LAUNCH_LC(P)                                                                     \
-  do {                                                                                       \
-    if (ev)                                                                                  \
-      lc_force_kernel<P, true><<<blocks, 32 * kWarpsPerBlock, 0, s>>>(                       \
-          g->dims[0], g->dims[1], g->dims[2], g->tdims[0], g->tdims[1], k, pos4, cell_start, \
-          cell_count, dup, fx, fy, fz, ev_scratch, stats);                                   \
-    else                                                                                     \
-      lc_force_kernel<P, false><<<blocks, 32 * kWarpsPerBlock, 0, s>>>(                      \
-          g->dims[0], g->dims[1], g->dims[2], g->tdims[0], g->tdims[1], k, pos4, cell_start, \
-          cell_count, dup, fx, fy, fz, ev_scratch, stats);                                   \
+#define LMD_LC_ARGS                                                                           \
+  g->dims[0], g->dims[1], g->dims[2], g->tdims[0], g->tdims[1], k, pos4, cell_start,          \
+      cell_count, dup, fx, fy, fz, ev_scratch, stats
+#define LMD_LAUNCH_LC(P)                                                                      \
+  do {                                                                                        \
+    if (ev) lc_force_kernel<P, true><<<blocks, 32 * kWarpsPerBlock, 0, s>>>(LMD_LC_ARGS);        \
+    else lc_force_kernel<P, false><<<blocks, 32 * kWarpsPerBlock, 0, s>>>(LMD_LC_ARGS);          \
   } while (0)
   switch (pattern) {
     case LMD_ONE_BY_V: LMD_LAUNCH_LC(LMD_ONE_BY_V); break;
@@ -262,6 +258,7 @@ int lmd_force_lc(const lmd_grid* g, const lmd_lj* lj, int pattern, int flags,
     default: return LMD_ERR_CONFIG;
   }
 #undef LMD_LAUNCH_LC
+#undef LMD_LC_ARGS
   LMD_CHECK_LAUNCH();
   if (ev) return reduce_ev(ev_scratch, lmd_lc_ev_slots(g), stats, s);
   return LMD_OK;

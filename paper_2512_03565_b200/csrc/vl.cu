@@ -17,22 +17,9 @@
 // with a sentinel particle far away.  Lists are ascending in j.
 #include <cub/cub.cuh>
 
-#include "common.cuh"
+#include "vl_common.cuh"
 
 namespace lmd {
-
-constexpr int kVLWarps = 4;
-constexpr int kChunk = 4;  // fill steps per lane per 128-bit index load
-
-// lane holding (i_off = il, j_off = jo) of a pattern (inverse of Pattern<P>)
-__device__ __forceinline__ int lane_of(int pattern, int il, int jo) {
-  switch (pattern) {
-    case LMD_ONE_BY_V: return jo;
-    case LMD_V_BY_ONE: return il;
-    case LMD_TWO_BY_HALF: return il * 16 + jo;
-    default: return il + 16 * jo;  // LMD_HALF_BY_TWO
-  }
-}
 
 template <int P>
 struct Tile {
@@ -67,28 +54,6 @@ __device__ __forceinline__ void for_candidates(int i, const double4& pi, int new
         }
   }
 }
-
-__device__ __forceinline__ long long cell_of_owned(const double4& p, double lo0, double lo1,
-                                                   double lo2, double cl0, double cl1, double cl2,
-                                                   long long d0, long long d1, long long d2,
-                                                   long long t0, long long t1) {
-  const double pp[3] = {p.x, p.y, p.z};
-  const double lo[3] = {lo0, lo1, lo2}, cl[3] = {cl0, cl1, cl2};
-  const long long d[3] = {d0, d1, d2};
-  long long q[3];
-#pragma unroll
-  for (int ax = 0; ax < 3; ++ax) {
-    double s = floor(__ddiv_rn(__dadd_rn(pp[ax], -lo[ax]), cl[ax]));
-    long long v = !(s >= -4.0) ? -3 : (s > 1.0e15 ? 1000000000000000LL : (long long)s + 1);
-    q[ax] = v < 1 ? 1 : (v > d[ax] ? d[ax] : v);
-  }
-  return q[0] + t0 * (q[1] + t1 * q[2]);
-}
-
-struct GridK {
-  double lo0, lo1, lo2, cl0, cl1, cl2;
-  long long d0, d1, d2, t0, t1;
-};
 
 __global__ void vl_count_kernel(GridK g, int n, int newton3, double rl2,
                                 const double* __restrict__ pos4, const int32_t* __restrict__ os,
@@ -142,6 +107,82 @@ __global__ void vl_fill_kernel(GridK g, int n, int A, int B, int pattern, int ne
   }
 }
 
+// Single-pass build into a fixed per-tile capacity: tile t owns the slots
+// [t * cap_steps * 32, (t + 1) * cap_steps * 32), so no count pass and no
+// prefix scan are needed.  Thread per owned particle; a tile's A particles
+// are A aligned lanes of one warp, which agree on the tile's step count with
+// a shuffle reduction, and each thread pads its own slots with the sentinel
+// up to that count.  Entries past the capacity are dropped and reported
+// through *max_count (the caller rebuilds with a larger capacity).
+__global__ void vl_build_kernel(GridK g, int n, int ntiles, int A, int B, int pattern, int newton3,
+                                double rl2, int32_t sentinel, const double* __restrict__ pos4,
+                                const int32_t* __restrict__ os, const int32_t* __restrict__ oc,
+                                const int32_t* __restrict__ hs, const int32_t* __restrict__ hc,
+                                int cap_steps, int32_t* __restrict__ count,
+                                long long* __restrict__ toff, int32_t* __restrict__ kmax,
+                                int32_t* __restrict__ max_count, int32_t* __restrict__ nbr) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int t = i / A, il = i - t * A;
+  const long long stride = (long long)cap_steps * 32;
+  int32_t* out = nbr + (long long)t * stride;
+  const int cap = cap_steps * B;
+  int k = 0;
+  if (i < n) {
+    const double4 pi = ld_pos4(pos4, i);
+    if (pi.w == (double)LMD_OWNED) {
+      const long long lin = cell_of_owned(pi, g.lo0, g.lo1, g.lo2, g.cl0, g.cl1, g.cl2, g.d0,
+                                          g.d1, g.d2, g.t0, g.t1);
+      for (int view = 0; view < 2; ++view) {
+        const int32_t* vs = view ? hs : os;
+        const int32_t* vc = view ? hc : oc;
+        for (int dz = -1; dz <= 1; ++dz)
+          for (int dy = -1; dy <= 1; ++dy)
+            for (int dx = -1; dx <= 1; ++dx) {
+              const long long nl = lin + dx + g.t0 * (dy + g.t1 * dz);
+              const int c = vc[nl];
+              if (c == 0) continue;
+              int j = vs[nl];
+              const int e = j + c;
+              if (!view && newton3) j = max(j, i + 1);
+              for (; j < e; ++j) {
+                if (!view && j == i) continue;
+                const double4 pj = ld_pos4(pos4, j);
+                if (pj.w == (double)LMD_DUMMY) continue;
+                const double r2 = r2_exact(pi.x - pj.x, pi.y - pj.y, pi.z - pj.z);
+                if (r2 < rl2) {
+                  if (k < cap) {
+                    const int st = k / B, l = lane_of(pattern, il, k % B);
+                    out[(long long)(st / kChunk) * (32 * kChunk) + l * kChunk + st % kChunk] = j;
+                  }
+                  ++k;
+                }
+              }
+            }
+      }
+    }
+    count[i] = k;
+  }
+  // the tile's longest list (aligned groups of A lanes)
+  int m = k;
+  for (int off = 1; off < A; off <<= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, off));
+  int steps = (m + B - 1) / B;
+  steps = (steps + kChunk - 1) / kChunk * kChunk;
+  if (steps > cap_steps) steps = cap_steps;
+  if (t < ntiles) {
+    for (int q = min(k, cap); q < steps * B; ++q) {
+      const int st = q / B, l = lane_of(pattern, il, q % B);
+      out[(long long)(st / kChunk) * (32 * kChunk) + l * kChunk + st % kChunk] = sentinel;
+    }
+    if (il == 0) {
+      kmax[t] = steps * B;
+      toff[t] = (long long)t * stride;
+    }
+  }
+  int w = m;
+  for (int off = 16; off > 0; off >>= 1) w = max(w, __shfl_xor_sync(0xffffffffu, w, off));
+  if ((threadIdx.x & 31) == 0 && w > 0) atomicMax(max_count, w);
+}
+
 __global__ void fill_i32_kernel(int64_t n, int32_t v, int32_t* __restrict__ out) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
        k += (int64_t)gridDim.x * blockDim.x)
@@ -149,12 +190,6 @@ __global__ void fill_i32_kernel(int64_t n, int32_t v, int32_t* __restrict__ out)
 }
 
 // ------------------------------------------------------------------ force
-struct Acc {
-  double ax, ay, az, e, v;
-  long long pairs, halo;
-  int overlap;
-};
-
 template <bool EV, bool N3>
 __device__ __forceinline__ void vl_pair(const double4& pi, const double4& pj, int j, int n_owned,
                                         const LJK& k, Acc& a, double* __restrict__ fx,
@@ -173,7 +208,6 @@ __device__ __forceinline__ void vl_pair(const double4& pi, const double4& pj, in
   a.az = fma(f, dz, a.az);
   ++a.pairs;
   const bool jhalo = j >= n_owned;
-  a.halo += jhalo;
   if (N3 && !jhalo) {
     atomicAdd(fx + j, -f * dx);
     atomicAdd(fy + j, -f * dy);
@@ -256,27 +290,6 @@ __device__ __forceinline__ void vl_tile(int t, int lane, int n_owned,
   a.az = az0;
 }
 
-__device__ __forceinline__ void flush_acc(const Acc& a, int lane, bool live, bool ev_on,
-                                          long long warp_slot, double* __restrict__ ev,
-                                          lmd_stats* __restrict__ stats) {
-  const long long pairs = warp_sum_ll(a.pairs);
-  const long long pairs_halo = warp_sum_ll(a.halo);
-  const int overlap = __any_sync(0xffffffffu, a.overlap);
-  if (lane == 0 && live) {
-    if (pairs) atomicAdd((unsigned long long*)&stats->pair_interactions, (unsigned long long)pairs);
-    if (pairs_halo)
-      atomicAdd((unsigned long long*)&stats->pairs_owned_halo, (unsigned long long)pairs_halo);
-    if (overlap) atomicOr(&stats->overlap, 1);
-  }
-  if (ev_on) {
-    const double e = warp_sum(a.e), v = warp_sum(a.v);
-    if (lane == 0) {
-      ev[2 * warp_slot] = e;
-      ev[2 * warp_slot + 1] = v;
-    }
-  }
-}
-
 // One warp per i-tile.  The 2-wide gather variant trades memory-level
 // parallelism per warp for occupancy (64 registers, 8 blocks per SM).
 template <int P, bool EV, bool N3, int U, bool SOA>
@@ -288,7 +301,7 @@ __global__ void __launch_bounds__(32 * kVLWarps, U == 2 ? 8 : 4)
                     lmd_stats* __restrict__ stats) {
   const int lane = threadIdx.x & 31;
   const int t = blockIdx.x * kVLWarps + (threadIdx.x >> 5);
-  Acc a = {0.0, 0.0, 0.0, 0.0, 0.0, 0, 0, 0};
+  Acc a = {0.0, 0.0, 0.0, 0.0, 0.0, 0, 0};
   if (t < ntiles)
     vl_tile<P, EV, N3, U, SOA>(t, lane, n_owned, pos4, q, toff, kmax, nbr, k, a, fx, fy, fz);
   flush_acc(a, lane, t < ntiles, EV, (long long)blockIdx.x * kVLWarps + (threadIdx.x >> 5), ev,
@@ -308,7 +321,7 @@ __global__ void __launch_bounds__(32 * kVLWarps, U == 2 ? 8 : 4)
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int per = (ntiles + gridDim.x - 1) / gridDim.x;
   const int t0 = blockIdx.x * per, t1 = min(ntiles, t0 + per);
-  Acc a = {0.0, 0.0, 0.0, 0.0, 0.0, 0, 0, 0};
+  Acc a = {0.0, 0.0, 0.0, 0.0, 0.0, 0, 0};
   for (int t = t0 + w; t < t1; t += kVLWarps)
     vl_tile<P, EV, N3, U, SOA>(t, lane, n_owned, pos4, q, toff, kmax, nbr, k, a, fx, fy, fz);
   flush_acc(a, lane, true, EV, (long long)blockIdx.x * kVLWarps + w, ev, stats);
@@ -352,27 +365,6 @@ __global__ void gather_soa_kernel(int64_t n, const int32_t* __restrict__ perm,
   oy[k] = y[s];
   oz[k] = z[s];
 }
-
-static GridK make_gridk(const lmd_grid* g) {
-  GridK k;
-  k.lo0 = g->lo[0];
-  k.lo1 = g->lo[1];
-  k.lo2 = g->lo[2];
-  k.cl0 = g->cell_len[0];
-  k.cl1 = g->cell_len[1];
-  k.cl2 = g->cell_len[2];
-  k.d0 = g->dims[0];
-  k.d1 = g->dims[1];
-  k.d2 = g->dims[2];
-  k.t0 = g->tdims[0];
-  k.t1 = g->tdims[1];
-  return k;
-}
-
-static int pattern_A(int p) {
-  return p == LMD_ONE_BY_V ? 1 : p == LMD_V_BY_ONE ? 32 : p == LMD_TWO_BY_HALF ? 2 : 16;
-}
-static int pattern_B(int p) { return 32 / pattern_A(p); }
 
 }  // namespace lmd
 
@@ -431,6 +423,26 @@ int lmd_vl_fill(const lmd_grid* g, double rl2, int newton3, int pattern, int64_t
   vl_fill_kernel<<<(unsigned)cdiv(n_owned, 128), 128, 0, s>>>(
       make_gridk(g), (int)n_owned, A, B, pattern, newton3, rl2, pos4, o_start, o_count, h_start,
       h_count, (const long long*)tile_off, nbr);
+  LMD_CHECK_LAUNCH();
+  return LMD_OK;
+}
+
+int lmd_vl_build(const lmd_grid* g, double rl2, int newton3, int pattern, int64_t n_owned,
+                 int32_t sentinel, const double* pos4, const int32_t* o_start,
+                 const int32_t* o_count, const int32_t* h_start, const int32_t* h_count,
+                 int32_t cap_steps, int32_t* count, int64_t* tile_off, int32_t* kmax,
+                 int32_t* max_count, int32_t* nbr, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(max_count, 0, sizeof(int32_t), s);
+  if (e != cudaSuccess) return set_cuda_error(e);
+  if (n_owned <= 0) return LMD_OK;
+  if (n_owned > 0x7fffffffLL || cap_steps <= 0 || cap_steps % kChunk) return LMD_ERR_CONFIG;
+  const int A = pattern_A(pattern), B = pattern_B(pattern);
+  const int64_t ntiles = cdiv(n_owned, A);
+  vl_build_kernel<<<(unsigned)cdiv(ntiles * A, 128), 128, 0, s>>>(
+      make_gridk(g), (int)n_owned, (int)ntiles, A, B, pattern, newton3, rl2, sentinel, pos4,
+      o_start, o_count, h_start, h_count, cap_steps, count, (long long*)tile_off, kmax,
+      max_count, nbr);
   LMD_CHECK_LAUNCH();
   return LMD_OK;
 }

@@ -1,0 +1,93 @@
+// Shared pieces of the Verlet-list build and force kernels (vl.cu, vl_ci.cu).
+#pragma once
+
+#include "common.cuh"
+
+namespace lmd {
+
+constexpr int kVLWarps = 4;
+constexpr int kChunk = 4;  // fill steps per lane per 128-bit index load
+
+// lane holding (i_off = il, j_off = jo) of a pattern (inverse of Pattern<P>)
+__device__ __forceinline__ int lane_of(int pattern, int il, int jo) {
+  switch (pattern) {
+    case LMD_ONE_BY_V: return jo;
+    case LMD_V_BY_ONE: return il;
+    case LMD_TWO_BY_HALF: return il * 16 + jo;
+    default: return il + 16 * jo;  // LMD_HALF_BY_TWO
+  }
+}
+
+__device__ __forceinline__ long long cell_of_owned(const double4& p, double lo0, double lo1,
+                                                   double lo2, double cl0, double cl1, double cl2,
+                                                   long long d0, long long d1, long long d2,
+                                                   long long t0, long long t1) {
+  const double pp[3] = {p.x, p.y, p.z};
+  const double lo[3] = {lo0, lo1, lo2}, cl[3] = {cl0, cl1, cl2};
+  const long long d[3] = {d0, d1, d2};
+  long long q[3];
+#pragma unroll
+  for (int ax = 0; ax < 3; ++ax) {
+    double s = floor(__ddiv_rn(__dadd_rn(pp[ax], -lo[ax]), cl[ax]));
+    long long v = !(s >= -4.0) ? -3 : (s > 1.0e15 ? 1000000000000000LL : (long long)s + 1);
+    q[ax] = v < 1 ? 1 : (v > d[ax] ? d[ax] : v);
+  }
+  return q[0] + t0 * (q[1] + t1 * q[2]);
+}
+
+struct GridK {
+  double lo0, lo1, lo2, cl0, cl1, cl2;
+  long long d0, d1, d2, t0, t1;
+};
+
+// ------------------------------------------------------------------ force
+// per-lane accumulators; counts are 32-bit (a lane sees at most a few
+// thousand pairs per launch) and widened once in flush_acc.  The Verlet-list
+// kernels leave pairs_owned_halo at 0 (only the cell kernels' Newton3
+// bookkeeping needs it).
+struct Acc {
+  double ax, ay, az, e, v;
+  int pairs, overlap;
+};
+
+__device__ __forceinline__ void flush_acc(const Acc& a, int lane, bool live, bool ev_on,
+                                          long long warp_slot, double* __restrict__ ev,
+                                          lmd_stats* __restrict__ stats) {
+  const long long pairs = warp_sum_ll((long long)a.pairs);
+  const int overlap = __any_sync(0xffffffffu, a.overlap);
+  if (lane == 0 && live) {
+    if (pairs) atomicAdd((unsigned long long*)&stats->pair_interactions, (unsigned long long)pairs);
+    if (overlap) atomicOr(&stats->overlap, 1);
+  }
+  if (ev_on) {
+    const double e = warp_sum(a.e), v = warp_sum(a.v);
+    if (lane == 0) {
+      ev[2 * warp_slot] = e;
+      ev[2 * warp_slot + 1] = v;
+    }
+  }
+}
+
+static inline GridK make_gridk(const lmd_grid* g) {
+  GridK k;
+  k.lo0 = g->lo[0];
+  k.lo1 = g->lo[1];
+  k.lo2 = g->lo[2];
+  k.cl0 = g->cell_len[0];
+  k.cl1 = g->cell_len[1];
+  k.cl2 = g->cell_len[2];
+  k.d0 = g->dims[0];
+  k.d1 = g->dims[1];
+  k.d2 = g->dims[2];
+  k.t0 = g->tdims[0];
+  k.t1 = g->tdims[1];
+  return k;
+}
+
+static inline int pattern_A(int p) {
+  return p == LMD_ONE_BY_V ? 1 : p == LMD_V_BY_ONE ? 32 : p == LMD_TWO_BY_HALF ? 2 : 16;
+}
+static inline int pattern_B(int p) { return 32 / pattern_A(p); }
+
+
+}  // namespace lmd

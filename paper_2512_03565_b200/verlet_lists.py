@@ -22,7 +22,7 @@ from .errors import ConfigurationError, ParticleOverlapError
 from .kernels import KernelStats, as_pattern, validate_vector_width
 from .particles import HALO, OWNED
 
-VL_REBUILD_PERIOD_DEFAULT = 10
+VL_REBUILD_PERIOD_DEFAULT = 20   # the reference scenario default (scenario.py:55)
 SENTINEL_POSITION = 1.0e30
 
 
@@ -48,9 +48,14 @@ class VerletListContainer:
         self._lists: dict = {}
         self._counts: dict = {}
         self._stats_cache: dict = {}
+        self._max_seen: dict = {}
         # kernel tuning knobs (csrc/vl.cu lmd_force_vl flags bits 4-6)
         self.knobs = 0x20   # 2-wide gathers at 8 blocks/SM (tools/vl_variants.py)
         self.use_soa = False  # True: gather SoA x, y, z instead of 256-bit pos4
+        # particles per lane sharing one union list (csrc/vl_ci.cu) for full
+        # lists; 1 = one list per particle (csrc/vl.cu)
+        self.i_cluster = 1   # CI = 2 or 4 measured 2-3x slower
+        self._clusters_cache: dict = {}
 
     # ------------------------------------------------------------ protocol
     def needs_rebuild(self, owned) -> bool:
@@ -117,6 +122,7 @@ class VerletListContainer:
         self._build_pos4 = self._pos4.clone()
         self._lists.clear()
         self._counts.clear()
+        self._clusters_cache.clear()
         self._stats_cache.clear()
         self.reference_positions = d.positions().clone()
         self.steps_since_rebuild = 0
@@ -172,59 +178,110 @@ class VerletListContainer:
     refresh_positions = refresh
 
     # ----------------------------------------------------------------- lists
-    def _count(self, newton3: bool) -> torch.Tensor:
-        c = self._counts.get(newton3)
+    def _count(self, newton3: bool, pattern=None) -> torch.Tensor:
+        """Per-particle list lengths (written by the first list build)."""
+        c = self._counts.get(bool(newton3))
         if c is None:
-            n = self.n_owned
-            c = torch.zeros(max(n, 1), dtype=torch.int32, device=self._pos4.device)
-            rl2 = self.params.interaction_length * self.params.interaction_length
-            N.call("lmd_vl_count", self.grid, float(rl2), int(newton3), n,
-                   N.ptr(self._build_pos4),
-                   N.ptr(self._o_start), N.ptr(self._o_count), N.ptr(self._h_start),
-                   N.ptr(self._h_count), N.ptr(c), N.stream())
-            self._counts[newton3] = c
+            self._list(pattern or as_pattern("v_by_one"), newton3)
+            c = self._counts[bool(newton3)]
         return c
 
-    def _list(self, pattern, newton3: bool):
-        key = (pattern.code, bool(newton3))
+    def _clusters(self, ci: int):
+        """(first, len) of the i-clusters: each cell's owned particles (one
+        contiguous run of the cell-sorted backing) cut into runs of ci."""
+        hit = self._clusters_cache.get(ci)
+        if hit is not None:
+            return hit
+        dev = self._pos4.device
+        oc = self._o_count.long()
+        per_cell = (oc + ci - 1) // ci
+        k = int(per_cell.sum().item())
+        cell = torch.repeat_interleave(torch.arange(len(oc), device=dev), per_cell, output_size=k)
+        first_of_cell = torch.cumsum(per_cell, 0) - per_cell
+        idx = torch.arange(k, device=dev) - first_of_cell[cell]
+        first = (self._o_start.long()[cell] + idx * ci).to(torch.int32)
+        ln = torch.clamp(oc[cell] - idx * ci, max=ci).to(torch.int32)
+        hit = (first.contiguous(), ln.contiguous(), k)
+        self._clusters_cache[ci] = hit
+        return hit
+
+    def _ci_for(self, newton3: bool) -> int:
+        return 1 if newton3 else int(self.i_cluster)
+
+    def _capacity_guess(self, newton3: bool, ci: int = 1) -> int:
+        """Entries per particle to reserve: the last build's longest list
+        (+25 %), else twice the mean-density estimate."""
+        seen = self._max_seen.get((bool(newton3), ci))
+        if seen is not None:
+            return int(seen * 1.25) + 8
+        rl = self.params.interaction_length
+        vol = float(np.prod(self.box.lengths))
+        est = (self.n_owned + self.n_halo) / vol * (4.0 / 3.0) * np.pi * rl ** 3
+        if newton3:
+            est *= 0.5
+        if ci > 1:   # union of ci nearby spheres
+            est *= 1.0 + 0.45 * (ci - 1)
+        return int(2.0 * est) + 32
+
+    def _list(self, pattern, newton3: bool, ci: int | None = None):
+        ci = self._ci_for(newton3) if ci is None else ci
+        key = (pattern.code, bool(newton3), ci)
         hit = self._lists.get(key)
         if hit is not None:
             return hit
         n = self.n_owned
         dev = self._pos4.device
-        count = self._count(newton3)
-        L = N.load()
-        ntiles = int(L.lmd_vl_num_tiles(n, pattern.code))
-        tile_len = torch.empty(max(ntiles, 1), dtype=torch.int64, device=dev)
+        if ci > 1:
+            cl_first, cl_len, units = self._clusters(ci)
+        else:
+            units = n
+        ntiles = int(N.load().lmd_vl_num_tiles(units, pattern.code))
+        b_ = pattern.shape(32)[1]
         tile_off = torch.empty(max(ntiles, 1), dtype=torch.int64, device=dev)
         kmax = torch.zeros(max(ntiles, 1), dtype=torch.int32, device=dev)
-        tb = int(L.lmd_vl_scan_temp_bytes(ntiles))
-        temp = torch.empty(max(tb, 1), dtype=torch.uint8, device=dev)
+        count = torch.zeros(max(n, 1), dtype=torch.int32, device=dev)
+        mx = torch.zeros(1, dtype=torch.int32, device=dev)
+        rl2 = self.params.interaction_length * self.params.interaction_length
+        cap = self._capacity_guess(newton3, ci)
         s = N.stream()
-        total = 0
-        if n:
-            N.call("lmd_vl_layout", n, pattern.code, N.ptr(count), N.ptr(tile_len),
-                   N.ptr(tile_off), N.ptr(kmax), N.ptr(temp), tb, s)
-            total = int((tile_off[ntiles - 1] + tile_len[ntiles - 1]).item())
-        nbr = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
-        if n:
-            rl2 = self.params.interaction_length * self.params.interaction_length
-            N.call("lmd_vl_fill", self.grid, float(rl2), int(newton3), pattern.code, n,
-                   self.n_owned + self.n_halo, N.ptr(self._build_pos4), N.ptr(self._o_start),
-                   N.ptr(self._o_count), N.ptr(self._h_start), N.ptr(self._h_count),
-                   N.ptr(tile_off), total, N.ptr(nbr), s)
-        hit = (tile_off, kmax, nbr, total)
+        tables = (N.ptr(self._build_pos4), N.ptr(self._o_start), N.ptr(self._o_count),
+                  N.ptr(self._h_start), N.ptr(self._h_count))
+        sentinel = self.n_owned + self.n_halo
+        while True:
+            steps = (cap + b_ - 1) // b_
+            cap_steps = max(4, (steps + 3) // 4 * 4)
+            nbr = torch.empty(max(ntiles * cap_steps * 32, 1), dtype=torch.int32, device=dev)
+            if ci > 1:
+                N.call("lmd_vl_ci_build", self.grid, float(rl2), pattern.code, ci, units,
+                       N.ptr(cl_first), N.ptr(cl_len), sentinel, *tables, cap_steps,
+                       N.ptr(count), N.ptr(tile_off), N.ptr(kmax), N.ptr(mx), N.ptr(nbr), s)
+            else:
+                N.call("lmd_vl_build", self.grid, float(rl2), int(newton3), pattern.code, n,
+                       sentinel, *tables, cap_steps, N.ptr(count), N.ptr(tile_off),
+                       N.ptr(kmax), N.ptr(mx), N.ptr(nbr), s)
+            longest = int(mx.item()) if n else 0
+            if longest <= cap_steps * b_:
+                break
+            del nbr
+            cap = longest
+        self._max_seen[(bool(newton3), ci)] = longest
+        self._counts.setdefault(bool(newton3), count)
+        hit = (tile_off, kmax, nbr, ntiles * cap_steps * 32)
         self._lists[key] = hit
         return hit
 
     def list_entries(self, pattern, newton3: bool) -> int:
-        """Padded list entries of the layout for `pattern` (4 B each)."""
-        return self._list(as_pattern(pattern), newton3)[3]
+        """List entries the force kernel reads for `pattern` (padded to whole
+        fill steps and 4-step chunks; 4 B each)."""
+        pattern = as_pattern(pattern)
+        _, kmax, _, _ = self._list(pattern, newton3)
+        b = pattern.shape(32)[1]
+        return int((kmax.long() // b).sum().item()) * 32
 
     def pairs(self, newton3: bool = False):
         """(id_i, id_j, j_is_image) of every list entry, for exact set checks."""
         pattern = as_pattern("one_by_v")
-        tile_off, kmax, nbr, total = self._list(pattern, newton3)
+        tile_off, kmax, nbr, total = self._list(pattern, newton3, ci=1)
         count = self._count(newton3)[: self.n_owned].long()
         n = self.n_owned
         perm = self._perm.long()
@@ -248,12 +305,23 @@ class VerletListContainer:
     def launch_force(self, pattern, newton3: bool, energy: bool = False, stats_t=None,
                      ev_t=None):
         pattern = as_pattern(pattern)
+        ci = self._ci_for(newton3)
         tile_off, kmax, nbr, _ = self._list(pattern, newton3)
         dev = self._pos4.device
         if stats_t is None:
             stats_t = N.new_stats(dev)
         else:
             stats_t.zero_()
+        if ci > 1:
+            cl_first, cl_len, units = self._clusters(ci)
+            if ev_t is None:
+                slots = int(N.load().lmd_vl_ci_ev_slots(units, pattern.code))
+                ev_t = torch.empty(2 * max(slots, 1), dtype=torch.float64, device=dev)
+            N.call("lmd_force_vl_ci", pattern.code, ci, N.FLAG_ENERGY if energy else 0,
+                   N.make_lj(self.params), self.n_owned, units, N.ptr(cl_first), N.ptr(cl_len),
+                   N.ptr(self._pos4), N.ptr(tile_off), N.ptr(kmax), N.ptr(nbr), N.ptr(self._fx),
+                   N.ptr(self._fy), N.ptr(self._fz), N.ptr(ev_t), N.ptr(stats_t), N.stream())
+            return stats_t
         if ev_t is None:
             slots = int(N.load().lmd_vl_ev_slots(self.n_owned, pattern.code))
             ev_t = torch.empty(2 * max(slots, 1), dtype=torch.float64, device=dev)
@@ -274,7 +342,7 @@ class VerletListContainer:
         if hit is None:
             a, b = pattern.shape(V)
             t = N.new_stats(self._pos4.device)
-            N.call("lmd_vl_stats", self.n_owned, a, b, V, N.ptr(self._count(newton3)), N.ptr(t),
+            N.call("lmd_vl_stats", self.n_owned, a, b, V, N.ptr(self._count(newton3, pattern)), N.ptr(t),
                    N.stream())
             st = N.read_stats(t)
             hit = (int(st.kernel_invocations), int(st.lane_slots), int(st.useful_interactions))

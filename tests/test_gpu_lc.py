@@ -250,3 +250,35 @@ def test_colored_newton3_matches_full_shell_and_is_deterministic(rng, trav):
         assert forces_close(fc, ff)
         assert sc == sf
         assert abs(sc.epot - sf.epot) <= 1e-12 * abs(sf.epot)
+
+
+def test_full_shell_dup_cells_energy_and_determinism(rng):
+    """Full-shell kernel against the oracle with dup-weighted cells (images
+    mid-step in owned cells), energy/virial, and run-to-run bitwise
+    determinism, for every pattern."""
+    n = 6000
+    span = (n / 0.7) ** (1 / 3)
+    pos = jittered_lattice(rng, (19, 19, 19), span / 19, 0.3)[:n]
+    pos[:40] = np.mod(pos[:40] - 0.02 * span, span)      # a few near the faces
+    pos[40:45, 0] = span + 1e-3                           # outside [lo, hi): dup anchors
+    params = LJParams(cutoff=2.5, skin=0.0)
+    lo, hi = np.zeros(3), np.full(3, span)
+    for pat in PATTERNS:
+        of, ost = O.force_phase_lc(pos, lo, hi, [True] * 3, params, "lc_c18", False, pat.value,
+                                   8)
+        prev = None
+        for _ in range(2):
+            cont = B.LinkedCellsContainer(_box(span, True), params)
+            buf = _buf(pos)
+            cont.rebuild(buf)
+            cont.refresh(buf)
+            st = cont.compute_forces("lc_c18", False, pat, 8, energy=True)
+            cont.collect_forces(buf)
+            f = buf.forces().cpu().numpy()
+            assert st == B.KernelStats(*ost.as_tuple()), pat
+            assert forces_close(f, of), pat
+            assert abs(st.epot - ost.epot) <= 1e-12 * abs(ost.epot)
+            assert abs(st.virial - ost.virial) <= 1e-12 * abs(ost.virial)
+            if prev is not None:
+                assert np.array_equal(prev, f)
+            prev = f

@@ -113,3 +113,59 @@ def test_lists_for_a_new_pattern_use_rebuild_positions(rng):
         of, ost = O.force_phase_lc(moved, np.zeros(3), np.full(3, span), [True] * 3,
                                    LJParams(cutoff=2.5, skin=0.0), "lc_c01", False, "one_by_v", 8)
         assert st.pair_interactions == ost.pair_interactions
+
+
+@pytest.mark.parametrize("ci", [1, 2, 4])
+@pytest.mark.parametrize("pattern", list(PatternKind))
+def test_i_cluster_lists_match_oracle(rng, ci, pattern):
+    """Union lists over i-clusters (csrc/vl_ci.cu) give the same pairs,
+    forces, per-particle counts and statistics as per-particle lists."""
+    pos, span = _state(rng, 3500, 0.8)
+    pos[::97] = pos[::97] * 0.999     # ragged cells
+    params = LJParams(cutoff=2.5, skin=0.3)
+    box = SimulationBox.cube(span, periodic=True)
+    of, ost = O.force_phase_vl(pos, np.zeros(3), np.full(3, span), [True] * 3, params, False,
+                               pattern.value, 8)
+    cont = B.VerletListContainer(box, params)
+    cont.i_cluster = ci
+    buf = ParticleBuffer.from_positions(pos, device="cuda")
+    cont.rebuild(buf)
+    cont.refresh(buf)
+    st = cont.compute_forces("vl", False, pattern, 8, energy=True)
+    cont.collect_forces(buf)
+    assert st == B.KernelStats(*ost.as_tuple())
+    assert forces_close(buf.forces().cpu().numpy(), of)
+    assert abs(st.epot - ost.epot) <= 1e-12 * abs(ost.epot)
+    assert abs(st.virial - ost.virial) <= 1e-12 * abs(ost.virial)
+
+
+def test_i_cluster_capacity_retry_and_overlap(rng):
+    """A clustered droplet overflows the density-based capacity guess (the
+    build retries with the observed longest list); zero distance raises."""
+    pos, span = _state(rng, 3000, 0.3)
+    pos[:600] = pos[:600] * 0.25 + span * 0.3     # dense blob
+    params = LJParams(cutoff=2.5, skin=0.3)
+    box = SimulationBox.cube(span, periodic=True)
+    of, ost = O.force_phase_vl(pos, np.zeros(3), np.full(3, span), [True] * 3, params, False,
+                               "v_by_one", 8)
+    for ci in (1, 2, 4):
+        buf = ParticleBuffer.from_positions(pos, device="cuda")
+        cfg = Configuration(B.ContainerKind.VERLET_LISTS, B.TraversalKind.VL, False,
+                            PatternKind.V_BY_ONE)
+        cont = B.VerletListContainer(box, params)
+        cont.i_cluster = ci
+        cont.rebuild(buf)
+        cont.refresh(buf)
+        st = cont.compute_forces("vl", False, PatternKind.V_BY_ONE, 8)
+        cont.collect_forces(buf)
+        assert st == B.KernelStats(*ost.as_tuple()), ci
+        assert forces_close(buf.forces().cpu().numpy(), of), ci
+    bad = pos.copy()
+    bad[11] = bad[10]
+    cont = B.VerletListContainer(box, params)
+    cont.i_cluster = 2
+    buf = ParticleBuffer.from_positions(bad, device="cuda")
+    cont.rebuild(buf)
+    cont.refresh(buf)
+    with pytest.raises(B.ParticleOverlapError):
+        cont.compute_forces("vl", False, PatternKind.V_BY_ONE, 8)

@@ -39,6 +39,16 @@ def main(path):
                 parts.append(f"{short}={r[idx[key]]}{units[idx[key]] if short in ('dur', 'dram_rd', 'dram_wr') else ''}")
         print(name)
         print("   " + "  ".join(parts))
+        stalls = []
+        for h, k in idx.items():
+            if h.startswith("smsp__average_warps_issue_stalled_") and h.endswith("_per_issue_active.ratio"):
+                try:
+                    stalls.append((float(r[k]), h[len("smsp__average_warps_issue_stalled_"):-len("_per_issue_active.ratio")]))
+                except ValueError:
+                    pass
+        if stalls:
+            stalls.sort(reverse=True)
+            print("   stalls/issue: " + "  ".join(f"{n}={v:.2f}" for v, n in stalls[:6]))
 
 
 if __name__ == "__main__":
