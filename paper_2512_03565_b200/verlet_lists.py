@@ -22,7 +22,7 @@ from .errors import ConfigurationError, ParticleOverlapError
 from .kernels import KernelStats, as_pattern, validate_vector_width
 from .particles import HALO, OWNED
 
-VL_REBUILD_PERIOD_DEFAULT = 20   # the reference scenario default (scenario.py:55)
+VL_REBUILD_PERIOD_DEFAULT = 10   # BASELINE config 2: lists rebuilt every 10 steps
 SENTINEL_POSITION = 1.0e30
 
 

@@ -3,6 +3,9 @@
     python tools/md_configs.py --config 1            # 8,000 lattice, LC c08 N3, 1 + 10 steps
     python tools/md_configs.py --config 3 --steps 300 # droplet, VCL M in {4,8,32}, tuner / 100
     python tools/md_configs.py --config 5 --steps 400 # 8.4M gas, tuner / 200 over LC x VL
+    python tools/md_configs.py --config 2             # 1M at rho 0.2/0.5/0.8: every order x
+                                                      # {LC c01/c08/c18, VL} x Newton3, 100 steps
+    python tools/md_configs.py --config 4             # 16.8M perturbed lattice, VL, 200 steps
 
 Every step runs the whole velocity-Verlet step on the device (integrator,
 boundaries, neighbour maintenance, images, force phase) through
@@ -32,8 +35,11 @@ def main():
     ap.add_argument("--steps", type=int, default=None)
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--metric", default="time")
+    ap.add_argument("--rho", default="0.2,0.5,0.8")
     args = ap.parse_args()
     torch.cuda.set_device(0)
+    if args.config == 2:
+        return sweep_config2(args)
     t_gen = time.perf_counter()
     if args.config == 1:
         w = workloads.config1()
@@ -49,6 +55,11 @@ def main():
                                            [B.PatternKind.V_BY_ONE, B.PatternKind.HALF_BY_TWO],
                                            cluster_sizes=[4, 8, 32])
         interval, steps = 100, args.steps or 1000
+    elif args.config == 4:
+        w = workloads.config4(device="cuda")
+        params = B.LJParams(cutoff=2.5, skin=0.3, dt=0.001)
+        fixed = B.Configuration.parse("vl,vl,false,v_by_one")
+        configs, interval, steps = None, None, args.steps or 200
     elif args.config == 5:
         w = workloads.config5(n=args.n or 8_388_608, device="cuda")
         params = B.LJParams(cutoff=2.5, skin=0.3, dt=0.001)
@@ -61,7 +72,7 @@ def main():
                                                      B.PatternKind.TWO_BY_HALF])
         interval, steps = 200, args.steps or 2000
     else:
-        raise SystemExit("configs 1, 3 and 5 run here (2 is bench.py, 4 is multi-GPU)")
+        raise SystemExit("configs 1-5 only")
     t_gen = time.perf_counter() - t_gen
     box = B.SimulationBox.cube(w.box_length, periodic=True)
     pos = w.positions if isinstance(w.positions, torch.Tensor) else torch.as_tensor(w.positions)
@@ -78,6 +89,7 @@ def main():
                                 fixed_config=fixed, policy=policy, metric=args.metric,
                                 retune_drift=0.2 if configs else None,
                                 wrap="always" if args.config == 1 else "at_rebuild")
+    torch.cuda.synchronize()
     pairs = sum(r.pair_interactions for r in records)
     out = {
         "config": args.config, "workload": w.name, "particles": len(buf), "steps": steps,
@@ -95,6 +107,41 @@ def main():
     if args.config == 1:
         out["pairs_per_step"] = [r.pair_interactions for r in records]
     print(json.dumps(out))
+
+
+def sweep_config2(args):
+    """BASELINE config 2: every interaction order x {linked cells (cell = rc),
+    Verlet lists (skin 0.3, rebuilt every 10 steps)} x Newton3, 100 MD steps
+    each, at each density; one JSON line per run."""
+    steps = args.steps or 100
+    for rho in [float(r) for r in args.rho.split(",")]:
+        w = workloads.config2(rho, n=args.n or 1_000_000, device="cuda")
+        box = B.SimulationBox.cube(w.box_length, periodic=True)
+        pos0 = w.positions.cpu().numpy()
+        v0 = torch.as_tensor(w.velocities).to("cuda", torch.float64)
+        cfgs = B.enumerate_search_space(
+            [B.ContainerKind.LINKED_CELLS, B.ContainerKind.VERLET_LISTS],
+            [B.TraversalKind.LC_C01, B.TraversalKind.LC_C08, B.TraversalKind.LC_C18,
+             B.TraversalKind.VL], [False, True], list(B.PATTERN_ORDER))
+        for cfg in cfgs:
+            skin = 0.0 if cfg.container is B.ContainerKind.LINKED_CELLS else 0.3
+            params = B.LJParams(cutoff=2.5, skin=skin, dt=0.001)
+            buf = B.ParticleBuffer.from_positions(pos0, device="cuda")
+            buf.vel_x.copy_(v0[:, 0]); buf.vel_y.copy_(v0[:, 1]); buf.vel_z.copy_(v0[:, 2])
+            B.force_phase(buf, box, params, cfg, 8)
+            torch.cuda.synchronize()
+            records, summary = B.run_md(buf, box, params, steps, 8, fixed_config=cfg,
+                                        rebuild_period=10 if skin else None,
+                                        wrap="at_rebuild")
+            torch.cuda.synchronize()
+            pairs = sum(r.pair_interactions for r in records)
+            print(json.dumps({
+                "config": 2, "rho": rho, "configuration": cfg.label, "particles": len(buf),
+                "steps": steps, "particle_steps_per_s": summary.particle_steps_per_s,
+                "wall_s": summary.wall_time_s, "force_time_s": summary.force_time_s,
+                "pair_interactions_per_s_force": pairs / max(summary.force_time_s, 1e-12),
+                "pair_interactions_per_s_wall": pairs / max(summary.wall_time_s, 1e-12),
+                "pairs_per_step_last": records[-1].pair_interactions}), flush=True)
 
 
 if __name__ == "__main__":
