@@ -114,13 +114,15 @@ __global__ void vl_fill_kernel(GridK g, int n, int A, int B, int pattern, int ne
 // a shuffle reduction, and each thread pads its own slots with the sentinel
 // up to that count.  Entries past the capacity are dropped and reported
 // through *max_count (the caller rebuilds with a larger capacity).
-__global__ void vl_build_kernel(GridK g, int n, int ntiles, int A, int B, int pattern, int newton3,
+template <int P>
+__global__ void vl_build_kernel(GridK g, int n, int ntiles, int newton3,
                                 double rl2, int32_t sentinel, const double* __restrict__ pos4,
                                 const int32_t* __restrict__ os, const int32_t* __restrict__ oc,
                                 const int32_t* __restrict__ hs, const int32_t* __restrict__ hc,
                                 int cap_steps, int32_t* __restrict__ count,
                                 long long* __restrict__ toff, int32_t* __restrict__ kmax,
                                 int32_t* __restrict__ max_count, int32_t* __restrict__ nbr) {
+  constexpr int A = Pattern<P>::A, B = Pattern<P>::B, pattern = P;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int t = i / A, il = i - t * A;
   const long long stride = (long long)cap_steps * 32;
@@ -144,15 +146,26 @@ __global__ void vl_build_kernel(GridK g, int n, int ntiles, int A, int B, int pa
               int j = vs[nl];
               const int e = j + c;
               if (!view && newton3) j = max(j, i + 1);
-              for (; j < e; ++j) {
-                if (!view && j == i) continue;
-                const double4 pj = ld_pos4(pos4, j);
-                if (pj.w == (double)LMD_DUMMY) continue;
-                const double r2 = r2_exact(pi.x - pj.x, pi.y - pj.y, pi.z - pj.z);
-                if (r2 < rl2) {
+              // hits of up to 32 consecutive candidates are collected as a
+              // bit mask and emitted afterwards in ascending order, so the
+              // (warp-divergent) emit path runs once per hit, not once per
+              // candidate that some lane of the warp accepted
+              for (int j0 = j; j0 < e; j0 += 32) {
+                const int j1 = min(e, j0 + 32);
+                unsigned mask = 0u;
+                for (int jj = j0; jj < j1; ++jj) {
+                  if (!view && jj == i) continue;
+                  const double4 pj = ld_pos4(pos4, jj);
+                  if (pj.w == (double)LMD_DUMMY) continue;
+                  const double r2 = r2_exact(pi.x - pj.x, pi.y - pj.y, pi.z - pj.z);
+                  if (r2 < rl2) mask |= 1u << (jj - j0);
+                }
+                while (mask) {
+                  const int jj = j0 + __ffs(mask) - 1;
+                  mask &= mask - 1u;
                   if (k < cap) {
                     const int st = k / B, l = lane_of(pattern, il, k % B);
-                    out[(long long)(st / kChunk) * (32 * kChunk) + l * kChunk + st % kChunk] = j;
+                    out[(long long)(st / kChunk) * (32 * kChunk) + l * kChunk + st % kChunk] = jj;
                   }
                   ++k;
                 }
@@ -439,10 +452,20 @@ int lmd_vl_build(const lmd_grid* g, double rl2, int newton3, int pattern, int64_
   if (n_owned > 0x7fffffffLL || cap_steps <= 0 || cap_steps % kChunk) return LMD_ERR_CONFIG;
   const int A = pattern_A(pattern), B = pattern_B(pattern);
   const int64_t ntiles = cdiv(n_owned, A);
-  vl_build_kernel<<<(unsigned)cdiv(ntiles * A, 128), 128, 0, s>>>(
-      make_gridk(g), (int)n_owned, (int)ntiles, A, B, pattern, newton3, rl2, sentinel, pos4,
-      o_start, o_count, h_start, h_count, cap_steps, count, (long long*)tile_off, kmax,
-      max_count, nbr);
+  const unsigned blocks = (unsigned)cdiv(ntiles * A, 128);
+#define LMD_VLB(P)                                                                             \
+  vl_build_kernel<P><<<blocks, 128, 0, s>>>(make_gridk(g), (int)n_owned, (int)ntiles, newton3, \
+                                            rl2, sentinel, pos4, o_start, o_count, h_start,    \
+                                            h_count, cap_steps, count, (long long*)tile_off,   \
+                                            kmax, max_count, nbr)
+  switch (pattern) {
+    case LMD_ONE_BY_V: LMD_VLB(LMD_ONE_BY_V); break;
+    case LMD_V_BY_ONE: LMD_VLB(LMD_V_BY_ONE); break;
+    case LMD_TWO_BY_HALF: LMD_VLB(LMD_TWO_BY_HALF); break;
+    case LMD_HALF_BY_TWO: LMD_VLB(LMD_HALF_BY_TWO); break;
+    default: return LMD_ERR_CONFIG;
+  }
+#undef LMD_VLB
   LMD_CHECK_LAUNCH();
   return LMD_OK;
 }
