@@ -331,6 +331,6 @@ class VerletClusterContainer:
                 dst = getattr(owned, name)
                 val = getattr(d, name)
                 if isinstance(dst, torch.Tensor):
-                    dst.copy_(val.to(dst.device))
+                    dst.copy_(val)   # direct device -> (pinned) host DMA
                 else:
-                    dst[...] = val.cpu().numpy()
+                    torch.from_numpy(dst).copy_(val)

@@ -204,7 +204,6 @@ class LinkedCellsContainer:
     def rebuild(self, owned, halo=None) -> None:
         """``halo`` is accepted for protocol uniformity; images enter at refresh."""
         d = device_soa(owned)
-        _check_all_owned(d)
         dev = d.device
         if self._sorter is None or self._sorter.device != dev:
             self._sorter = _Sorter(dev)
@@ -213,7 +212,17 @@ class LinkedCellsContainer:
         self.n_owned = n
         self._perm = self._sorter.bin(self.grid, 0, d.pos_x, d.pos_y, d.pos_z, 0,
                                       self._o_start, self._o_count)
-        self._max_cell = max(1, int(self._o_count.max().item())) if n else 1
+        if n:
+            # one host read for the ownership check and the peak occupancy
+            bad, peak = torch.stack([(d.ownership != OWNED).any().to(torch.int32),
+                                     self._o_count.max()]).tolist()
+            if bad:
+                raise ConfigurationError(
+                    "device containers take an all-OWNED particle buffer (halo images are "
+                    "derived)")
+            self._max_cell = max(1, int(peak))
+        else:
+            self._max_cell = 1
         self.reference_positions = d.positions().clone()
         self.steps_since_rebuild = 0
         self.structure_version += 1
@@ -314,9 +323,9 @@ class LinkedCellsContainer:
                 dst = getattr(owned, name)
                 val = getattr(d, name)
                 if isinstance(dst, torch.Tensor):
-                    dst.copy_(val.to(dst.device))
+                    dst.copy_(val)   # direct device -> (pinned) host DMA
                 else:
-                    dst[...] = val.cpu().numpy()
+                    torch.from_numpy(dst).copy_(val)
 
     # --------------------------------------------------------------- views
     @property

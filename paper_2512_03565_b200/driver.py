@@ -61,6 +61,6 @@ def _write_forces_back(host, dev) -> None:
         dst = getattr(host, name)
         val = getattr(dev, name)
         if isinstance(dst, torch.Tensor):
-            dst.copy_(val.to(dst.device))
+            dst.copy_(val)   # direct device -> (pinned) host DMA
         else:
-            dst[...] = val.cpu().numpy()
+            torch.from_numpy(dst).copy_(val)

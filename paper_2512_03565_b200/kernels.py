@@ -156,9 +156,9 @@ class _DeviceView:
             dst = getattr(self.src, name)
             val = getattr(self.dev, name)
             if isinstance(dst, torch.Tensor):
-                dst.copy_(val.to(dst.device))
+                dst.copy_(val)   # direct device -> (pinned) host DMA
             else:
-                dst[...] = val.cpu().numpy()
+                torch.from_numpy(dst).copy_(val)
 
 
 def _device_for(*bufs) -> torch.device:

@@ -101,8 +101,9 @@ class ParticleBuffer:
     @classmethod
     def empty(cls, n: int, device=None) -> "ParticleBuffer":
         device = torch.device(device) if device is not None else default_device()
-        kw = {name: torch.zeros(n, dtype=torch.float64, device=device)
-              for name in FLOAT_FIELDS}
+        # one zeroed allocation, one row per float field (one fill launch)
+        block = torch.zeros((len(FLOAT_FIELDS), n), dtype=torch.float64, device=device)
+        kw = {name: block[k] for k, name in enumerate(FLOAT_FIELDS)}
         kw["id"] = torch.zeros(n, dtype=torch.int64, device=device)
         kw["ownership"] = torch.full((n,), OWNED, dtype=torch.int8, device=device)
         return cls(**kw)

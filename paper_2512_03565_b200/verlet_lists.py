@@ -16,7 +16,7 @@ import numpy as np
 import torch
 
 from . import _native as N
-from .containers import _Sorter, _check_all_owned, _grid, device_soa, needs_rebuild
+from .containers import _Sorter, _grid, device_soa, needs_rebuild
 from .domain import as_box, build_halo
 from .errors import ConfigurationError, ParticleOverlapError
 from .kernels import KernelStats, as_pattern, validate_vector_width
@@ -70,7 +70,8 @@ class VerletListContainer:
         domain decomposition passes its ghost layer instead; later refreshes
         must then pass the ghosts again, in the same order."""
         d = device_soa(owned)
-        _check_all_owned(d)
+        # the all-OWNED check is read after the halo count's host sync
+        not_owned = (d.ownership != OWNED).any() if len(d) else None
         dev = d.device
         nc = int(self.grid.ncell)
         if self._sorter is None or self._sorter.device != dev:
@@ -79,8 +80,9 @@ class VerletListContainer:
             self._o_count = torch.empty(nc, dtype=torch.int32, device=dev)
             self._h_start = torch.zeros(nc, dtype=torch.int32, device=dev)
             self._h_count = torch.zeros(nc, dtype=torch.int32, device=dev)
+            self._sentinel_row = torch.tensor([SENTINEL_POSITION] * 3 + [2.0],
+                                              dtype=torch.float64, device=dev)
         n = len(d)
-        s = N.stream()
         self._perm = self._sorter.bin(self.grid, 0, d.pos_x, d.pos_y, d.pos_z, 0,
                                       self._o_start, self._o_count)
         self._external_halo = halo is not None
@@ -88,22 +90,20 @@ class VerletListContainer:
             halo = build_halo(d, self.box, self.params.interaction_length)
         else:
             halo = device_soa(halo, dev)
+        if not_owned is not None and bool(not_owned):
+            raise ConfigurationError(
+                "device containers take an all-OWNED particle buffer (halo images are derived)")
         nh = len(halo)
         self.n_owned, self.n_halo = n, nh
-        # combined backing [owned | images | sentinel] as pos4 (32 B records)
+        # combined backing [owned | images | sentinel] as pos4 (32 B records),
+        # filled by _load_positions in the rebuild-time order
         self._pos4 = torch.empty((n + nh + 1, 4), dtype=torch.float64, device=dev)
-        self._pos4[-1] = torch.tensor([SENTINEL_POSITION] * 3 + [2.0], dtype=torch.float64)
-        if n:
-            N.call("lmd_gather_pos4", n, N.ptr(self._perm), N.ptr(d.pos_x), N.ptr(d.pos_y),
-                   N.ptr(d.pos_z), None, float(OWNED), N.ptr(self._pos4), s)
+        self._pos4[-1].copy_(self._sentinel_row)
         if nh:
-            hperm = self._sorter.bin(self.grid, 1, halo.pos_x, halo.pos_y, halo.pos_z, n,
-                                     self._h_start, self._h_count)
-            N.call("lmd_gather_pos4", nh, N.ptr(hperm), N.ptr(halo.pos_x), N.ptr(halo.pos_y),
-                   N.ptr(halo.pos_z), None, float(HALO), N.ptr(self._pos4[n:]), s)
-            self._hperm = hperm
+            self._hperm = self._sorter.bin(self.grid, 1, halo.pos_x, halo.pos_y, halo.pos_z, n,
+                                           self._h_start, self._h_count)
             if not self._external_halo:
-                hp = hperm.long()
+                hp = self._hperm.long()
                 self._halo_owner = halo.extra["owner"][hp].contiguous()
                 self._halo_shift = halo.extra["shift"][hp].contiguous()
         else:
@@ -111,11 +111,15 @@ class VerletListContainer:
             self._h_count.zero_()
             self._halo_owner = torch.zeros(0, dtype=torch.int32, device=dev)
             self._halo_shift = torch.zeros(0, dtype=torch.int8, device=dev)
-        self._soa = torch.empty((3, n + nh + 1), dtype=torch.float64, device=dev)
-        self._soa[:, -1] = SENTINEL_POSITION
-        self._fx = torch.zeros(max(n, 1), dtype=torch.float64, device=dev)
-        self._fy = torch.zeros(max(n, 1), dtype=torch.float64, device=dev)
-        self._fz = torch.zeros(max(n, 1), dtype=torch.float64, device=dev)
+        if self.use_soa:
+            self._soa = torch.empty((3, n + nh + 1), dtype=torch.float64, device=dev)
+            self._soa[:, -1] = SENTINEL_POSITION
+        else:
+            self._soa = torch.empty((3, 1), dtype=torch.float64, device=dev)
+        # every owned slot is written by the force kernel (Newton3 zeroes first)
+        self._fx = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
+        self._fy = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
+        self._fz = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
         self._load_positions(d, halo if self._external_halo else None)
         # lists are built lazily per interaction order: always from the
         # rebuild-time positions, whatever the particles did since
@@ -134,8 +138,9 @@ class VerletListContainer:
         (shift codes) or, for an external ghost layer, gathered from it."""
         n, nh = self.n_owned, self.n_halo
         s = N.stream()
-        sx, sy, sz = self._soa[0], self._soa[1], self._soa[2]
         soa = self.use_soa
+        if soa:
+            sx, sy, sz = self._soa[0], self._soa[1], self._soa[2]
         if n:
             if soa:
                 N.call("lmd_gather_soa", n, N.ptr(self._perm), N.ptr(d.pos_x), N.ptr(d.pos_y),
@@ -376,6 +381,6 @@ class VerletListContainer:
                 dst = getattr(owned, name)
                 val = getattr(d, name)
                 if isinstance(dst, torch.Tensor):
-                    dst.copy_(val.to(dst.device))
+                    dst.copy_(val)   # direct device -> (pinned) host DMA
                 else:
-                    dst[...] = val.cpu().numpy()
+                    torch.from_numpy(dst).copy_(val)
