@@ -493,8 +493,10 @@ def sweep(args, w, torch, N, flush):
     import paper_2512_03565_b200 as B
     rows = []
     labels = [c.label for c in B.enumerate_search_space(
-        [B.ContainerKind.LINKED_CELLS, B.ContainerKind.VERLET_LISTS],
-        [B.TraversalKind.LC_C01, B.TraversalKind.LC_C18, B.TraversalKind.VL],
+        [B.ContainerKind.LINKED_CELLS, B.ContainerKind.VERLET_LISTS,
+         B.ContainerKind.VERLET_CLUSTER_LISTS],
+        [B.TraversalKind.LC_C01, B.TraversalKind.LC_C08, B.TraversalKind.LC_C18,
+         B.TraversalKind.VL, B.TraversalKind.VCL],
         [False, True], list(B.PATTERN_ORDER))]
     for label in labels:
         cfg = B.Configuration.parse(label)
