@@ -312,9 +312,16 @@ def run_b200(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # LMD_DEVICE / LMD_DIST_BACKEND=gloo: run the multi-rank path on one GPU
+    # (host-staged communication) to exercise it where only one GPU exists
+    local = int(os.environ.get("LMD_DEVICE", local))
+    backend = os.environ.get("LMD_DIST_BACKEND", "nccl")
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     cfg = B.Configuration.parse(args.config)
     dec = None
     if world > 1:
@@ -461,10 +468,10 @@ def run_b200(args):
                        "useful_interactions_rank0": stats.useful_interactions,
                        "candidate_efficiency": pairs / max(stats.useful_interactions, 1),
                        "step": "refresh (positions -> cell order, images/ghosts) + force "
-                               "kernel" + (" + NCCL ghost exchange" if world > 1 else ""),
+                               "kernel" + (f" + {backend} ghost exchange" if world > 1 else ""),
                        "kernel_ms_rank0": avg_launch * 1e3,
                        "l2": "flushed (256 MiB write) before every timed step",
-                       "parallelism": (f"bricks {dec.grid}, NCCL P2P ghost exchange"
+                       "parallelism": (f"bricks {dec.grid}, {backend} P2P ghost exchange"
                                        if dec else ("replicas (decomposition failed: "
                                                     f"{dec_error})" if dec_error
                                                     else ("replicas" if world > 1

@@ -127,13 +127,16 @@ class BrickDecomposition:
         order = torch.argsort(dest, stable=True)
         state = state[order]
         counts = torch.bincount(dest, minlength=self.nranks).to(torch.int64)
+        dev = state.device
+        if self._host_staged(state):
+            state, counts = state.cpu(), counts.cpu()
         recv_counts = torch.empty_like(counts)
         dist.all_to_all_single(recv_counts, counts, group=self.group)
         out = torch.empty((int(recv_counts.sum()), state.shape[1]), dtype=state.dtype,
                           device=state.device)
         dist.all_to_all_single(out, state.contiguous(), recv_counts.tolist(), counts.tolist(),
                                group=self.group)
-        return out
+        return out.to(dev)
 
     # ------------------------------------------------------------ exchange
     def _neighbour(self, axis: int, direction: int) -> int:
@@ -146,15 +149,31 @@ class BrickDecomposition:
         return (self.coords[axis] == 0 and direction == 0) or (
             self.coords[axis] == self.grid[axis] - 1 and direction == 1)
 
+    def _host_staged(self, t: torch.Tensor) -> bool:
+        """gloo moves CPU tensors only: device tensors go through host copies
+        (used to run the multi-rank path on one GPU; NCCL moves them directly)."""
+        return t.device.type == "cuda" and dist.get_backend(self.group) == "gloo"
+
     def _p2p(self, sends: list, recvs: list) -> None:
         """sends / recvs: lists of (peer, tensor), matched per peer in list
         order; issued as one batch (one NCCL group), so no ordering deadlock."""
-        ops = [dist.P2POp(dist.irecv, t, peer, self.group) for peer, t in recvs if t.numel()]
-        ops += [dist.P2POp(dist.isend, t, peer, self.group) for peer, t in sends if t.numel()]
+        sends = [(p, t) for p, t in sends if t.numel()]
+        recvs = [(p, t) for p, t in recvs if t.numel()]
+        staged = any(self._host_staged(t) for _, t in sends + recvs)
+        if staged:
+            sends = [(p, t.cpu()) for p, t in sends]
+            host_recvs = [(p, torch.empty(t.shape, dtype=t.dtype)) for p, t in recvs]
+        else:
+            host_recvs = recvs
+        ops = [dist.P2POp(dist.irecv, t, peer, self.group) for peer, t in host_recvs]
+        ops += [dist.P2POp(dist.isend, t, peer, self.group) for peer, t in sends]
         if not ops:
             return
         for r in dist.batch_isend_irecv(ops):
             r.wait()
+        if staged:
+            for (_, dst), (_, src) in zip(recvs, host_recvs):
+                dst.copy_(src)
 
     def plan(self, owned_pos: torch.Tensor) -> torch.Tensor:
         """Build the ghost layer for the current owned rows (N, k), columns

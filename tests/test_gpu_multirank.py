@@ -1,0 +1,38 @@
+"""The multi-rank bench path (brick decomposition, ghost exchange, weak
+scaling) run with the real kernels: two ranks share the one GPU, the ghost
+exchange goes host-staged through gloo (NCCL on a multi-GPU node moves the
+same tensors directly).  The global pair count must be twice the single
+box's up to the brick interface (each brick sees its neighbour instead of
+its own periodic image)."""
+
+from __future__ import annotations
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_two_ranks_on_one_gpu_gloo():
+    env = dict(os.environ, LMD_DIST_BACKEND="gloo", LMD_DEVICE="0")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29561", "bench.py", "--gpus", "2",
+           "--steps", "2", "--warmup", "3", "--n=200000"]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = [ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1]
+    d = json.loads(line)
+    assert d["n_gpus"] == 2 and d["config"]["parallelism"].startswith("bricks (2, 1, 1)")
+    single = subprocess.run([sys.executable, "bench.py", "--steps", "2", "--warmup", "3",
+                             "--n=200000", "--e2e-steps", "0", "--no-cpu-baseline"], cwd=ROOT,
+                            capture_output=True, text=True, timeout=600)
+    assert single.returncode == 0, single.stderr[-2000:]
+    s = json.loads([ln for ln in single.stdout.splitlines() if ln.startswith("{")][-1])
+    one = s["config"]["pairs_per_step"]
+    assert abs(d["config"]["pairs_per_step"] - 2 * one) < 1e-3 * one
