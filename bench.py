@@ -45,7 +45,8 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default=DEFAULT_CONFIG)
     ap.add_argument("--rho", type=float, default=0.8)
-    ap.add_argument("--n", type=int, default=1_000_000)
+    ap.add_argument("--n", "--particles", dest="n", type=int, default=1_000_000,
+                    help="particles per GPU (--particles under torchrun: --n is ambiguous there)")
     ap.add_argument("--vector-width", type=int, default=8)
     ap.add_argument("--energy", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)

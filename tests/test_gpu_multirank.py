@@ -23,7 +23,7 @@ def test_two_ranks_on_one_gpu_gloo():
     env = dict(os.environ, LMD_DIST_BACKEND="gloo", LMD_DEVICE="0")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", "29561", "bench.py", "--gpus", "2",
-           "--steps", "2", "--warmup", "3", "--n=200000"]
+           "--steps", "2", "--warmup", "3", "--particles", "200000"]
     r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     line = [ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1]
