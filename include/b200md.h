@@ -249,6 +249,14 @@ int lmd_vl_build(const lmd_grid* g, double rl2, int newton3, int pattern, int64_
                  const int32_t* o_count, const int32_t* h_start, const int32_t* h_count,
                  int32_t cap_steps, int32_t* count, int64_t* tile_off, int32_t* kmax,
                  int32_t* max_count, int32_t* nbr, void* stream);
+/* Optional pass after lmd_vl_build / lmd_vl_ci_build: permutes every lane's
+ * own slot sequence of every tile so that the lanes of a fill gather from
+ * shared 128-B lines (window of `window` = 8, 16 or 32 entries per lane,
+ * see csrc/vl.cu vl_align_kernel).  Same entries per lane, so forces, pair
+ * counts and statistics are unchanged up to summation order.  n_units = owned
+ * particles (or clusters for the i-cluster lists). */
+int lmd_vl_align(int pattern, int64_t n_units, int window, const int64_t* tile_off,
+                 const int32_t* kmax, int32_t* nbr, void* stream);
 /* i-cluster lists (csrc/vl_ci.cu), full lists only: each cell's owned
  * particles are cut into clusters of up to ci (2 or 4) consecutive backing
  * slots, cluster c = [cl_first[c], cl_first[c] + cl_len[c]); its list is the
@@ -273,7 +281,7 @@ int lmd_force_vl_ci(int pattern, int ci, int flags, const lmd_lj* lj, int64_t n_
  * are pos4 over the combined backing plus one sentinel record (256-bit
  * gathers), or, if soa != NULL, SoA copies x = soa[0..ntot), y, z of the
  * same ntot records (three 64-bit gathers that share sectors between
- * neighbouring lanes).  flags bits 4-6 select unroll / grid variants.  newton3 = 0
+ * neighbouring lanes).  newton3 = 0
  * writes f[i]; newton3 = 1 accumulates with FP64 atomics into zeroed f
  * (j-side reactions; summation order is then not deterministic).
  * ev_scratch: 2 * lmd_vl_ev_slots(n_owned, pattern) doubles. */

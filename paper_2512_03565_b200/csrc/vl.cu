@@ -196,6 +196,70 @@ __global__ void vl_build_kernel(GridK g, int n, int ntiles, int newton3,
   if ((threadIdx.x & 31) == 0 && w > 0) atomicMax(max_count, w);
 }
 
+// Line-aligned entry order (optional pass after the build).  The force
+// kernel is bound by the L1 data pipe, which retires about one distinct
+// 128-B line per cycle per warp gather; with each lane's list in ascending
+// order the 32 lanes of a fill touch ~21 distinct lines.  This pass permutes
+// every lane's own slot sequence (so every entry stays with its particle;
+// valid for every interaction order): each lane keeps a window of its next W
+// entries in shared memory and, at each step, takes the entry whose line
+// occurs most often across the warp's windows (ties: smaller index), which
+// makes lanes gather from shared lines in the same fill (~14.6 lines at
+// W = 16 in a host simulation).  Counts live in a 1024-entry table indexed
+// by line mod 1024 (collisions only blur the heuristic).  Deterministic:
+// choices are made from counts frozen by __syncwarp, and the slot written
+// at step s was read into the window before (in place).
+template <int W>
+__global__ void __launch_bounds__(32 * kVLWarps)
+    vl_align_kernel(int ntiles, int B, const long long* __restrict__ toff,
+                    const int32_t* __restrict__ kmax, int32_t* __restrict__ nbr) {
+  __shared__ int cnt_s[kVLWarps][1024];
+  __shared__ int win_s[kVLWarps][W][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int t = blockIdx.x * kVLWarps + w;
+  if (t >= ntiles) return;
+  int* cnt = cnt_s[w];
+  for (int q = lane; q < 1024; q += 32) cnt[q] = 0;
+  __syncwarp();
+  const int steps = kmax[t] / B;
+  int32_t* base = nbr + toff[t];
+  auto slot = [&](int st) -> long long {
+    return (long long)(st / kChunk) * (32 * kChunk) + lane * kChunk + st % kChunk;
+  };
+  int nxt = 0;
+#pragma unroll
+  for (int q = 0; q < W; ++q) {
+    int v = -1;
+    if (nxt < steps) v = base[slot(nxt++)];
+    win_s[w][q][lane] = v;
+    if (v >= 0) atomicAdd(&cnt[(v >> 2) & 1023], 1);
+  }
+  __syncwarp();
+  for (int st = 0; st < steps; ++st) {
+    int best = 0, bc = -1, bv = 0x7fffffff;
+#pragma unroll
+    for (int q = 0; q < W; ++q) {
+      const int v = win_s[w][q][lane];
+      if (v >= 0) {
+        const int c = cnt[(v >> 2) & 1023];
+        if (c > bc || (c == bc && v < bv)) {
+          bc = c;
+          bv = v;
+          best = q;
+        }
+      }
+    }
+    __syncwarp();
+    base[slot(st)] = bv;
+    atomicSub(&cnt[(bv >> 2) & 1023], 1);
+    int v = -1;
+    if (nxt < steps) v = base[slot(nxt++)];
+    win_s[w][best][lane] = v;
+    if (v >= 0) atomicAdd(&cnt[(v >> 2) & 1023], 1);
+    __syncwarp();
+  }
+}
+
 __global__ void fill_i32_kernel(int64_t n, int32_t v, int32_t* __restrict__ out) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
        k += (int64_t)gridDim.x * blockDim.x)
@@ -243,13 +307,14 @@ struct SoA {
   const double* __restrict__ z;
 };
 
-template <bool SOA>
+// gather modes: 0 = 256-bit pos4 record, 1 = SoA x, y, z (64-bit each)
+template <int GM>
 __device__ __forceinline__ double4 ld_j(const double* __restrict__ pos4, const SoA& q, int j) {
-  if (SOA) return make_double4(__ldg(q.x + j), __ldg(q.y + j), __ldg(q.z + j), 0.0);
+  if (GM == 1) return make_double4(__ldg(q.x + j), __ldg(q.y + j), __ldg(q.z + j), 0.0);
   return ld_pos4(pos4, j);
 }
 
-template <int P, bool EV, bool N3, int U, bool SOA>
+template <int P, bool EV, bool N3, int U, int SOA>
 __device__ __forceinline__ void vl_tile(int t, int lane, int n_owned,
                                         const double* __restrict__ pos4, const SoA& q,
                                         const long long* __restrict__ toff,
@@ -305,8 +370,8 @@ __device__ __forceinline__ void vl_tile(int t, int lane, int n_owned,
 
 // One warp per i-tile.  The 2-wide gather variant trades memory-level
 // parallelism per warp for occupancy (64 registers, 8 blocks per SM).
-template <int P, bool EV, bool N3, int U, bool SOA>
-__global__ void __launch_bounds__(32 * kVLWarps, U == 2 ? 8 : 4)
+template <int P, bool EV, bool N3, int U, int SOA>
+__global__ void __launch_bounds__(32 * kVLWarps, 8)
     vl_force_kernel(int n_owned, int ntiles, const double* __restrict__ pos4, SoA q,
                     const long long* __restrict__ toff, const int32_t* __restrict__ kmax,
                     const int32_t* __restrict__ nbr, LJK k, double* __restrict__ fx,
@@ -319,25 +384,6 @@ __global__ void __launch_bounds__(32 * kVLWarps, U == 2 ? 8 : 4)
     vl_tile<P, EV, N3, U, SOA>(t, lane, n_owned, pos4, q, toff, kmax, nbr, k, a, fx, fy, fz);
   flush_acc(a, lane, t < ntiles, EV, (long long)blockIdx.x * kVLWarps + (threadIdx.x >> 5), ev,
             stats);
-}
-
-// Persistent variant: each block owns a contiguous (spatially coherent) run
-// of tiles, so the j positions its warps gather stay resident in its SM's L1.
-template <int P, bool EV, bool N3, int U, bool SOA>
-__global__ void __launch_bounds__(32 * kVLWarps, U == 2 ? 8 : 4)
-    vl_force_persistent_kernel(int n_owned, int ntiles, const double* __restrict__ pos4, SoA q,
-                               const long long* __restrict__ toff,
-                               const int32_t* __restrict__ kmax, const int32_t* __restrict__ nbr,
-                               LJK k, double* __restrict__ fx, double* __restrict__ fy,
-                               double* __restrict__ fz, double* __restrict__ ev,
-                               lmd_stats* __restrict__ stats) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int per = (ntiles + gridDim.x - 1) / gridDim.x;
-  const int t0 = blockIdx.x * per, t1 = min(ntiles, t0 + per);
-  Acc a = {0.0, 0.0, 0.0, 0.0, 0.0, 0, 0};
-  for (int t = t0 + w; t < t1; t += kVLWarps)
-    vl_tile<P, EV, N3, U, SOA>(t, lane, n_owned, pos4, q, toff, kmax, nbr, k, a, fx, fy, fz);
-  flush_acc(a, lane, true, EV, (long long)blockIdx.x * kVLWarps + w, ev, stats);
 }
 
 __global__ void vl_stats_kernel(int n, int a, int b, const int32_t* __restrict__ count,
@@ -470,58 +516,51 @@ int lmd_vl_build(const lmd_grid* g, double rl2, int newton3, int pattern, int64_
   return LMD_OK;
 }
 
+int lmd_vl_align(int pattern, int64_t n_units, int window, const int64_t* tile_off,
+                 const int32_t* kmax, int32_t* nbr, void* stream) {
+  if (n_units <= 0) return LMD_OK;
+  const int B = pattern_B(pattern);
+  const int64_t ntiles = cdiv(n_units, pattern_A(pattern));
+  const unsigned blocks = (unsigned)cdiv(ntiles, kVLWarps);
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (window) {
+    case 8: vl_align_kernel<8><<<blocks, 32 * kVLWarps, 0, s>>>((int)ntiles, B, (const long long*)tile_off, kmax, nbr); break;
+    case 16: vl_align_kernel<16><<<blocks, 32 * kVLWarps, 0, s>>>((int)ntiles, B, (const long long*)tile_off, kmax, nbr); break;
+    case 32: vl_align_kernel<32><<<blocks, 32 * kVLWarps, 0, s>>>((int)ntiles, B, (const long long*)tile_off, kmax, nbr); break;
+    default: return LMD_ERR_CONFIG;
+  }
+  LMD_CHECK_LAUNCH();
+  return LMD_OK;
+}
+
 int64_t lmd_vl_ev_slots(int64_t n_owned, int pattern) {
-  // enough for both the one-tile-per-warp grid and the persistent grid
-  return cdiv(lmd_vl_num_tiles(n_owned, pattern), kVLWarps) * kVLWarps + 148 * 64 * kVLWarps;
+  return cdiv(lmd_vl_num_tiles(n_owned, pattern), kVLWarps) * kVLWarps;
 }
 
 }  // extern "C"
 
-static int g_persistent_blocks = 0;
-
-template <int P, bool EV, bool N3, int U, bool SOA>
-static void launch_vl(bool persistent, int64_t n_owned, int64_t ntiles, const double* pos4,
-                      const SoA& q, const int64_t* tile_off, const int32_t* kmax,
-                      const int32_t* nbr, const LJK& k, double* fx, double* fy, double* fz,
-                      double* ev, lmd_stats* stats, cudaStream_t s) {
-  if (persistent) {
-    int sms = 148;
-    int dev = 0;
-    if (cudaGetDevice(&dev) == cudaSuccess)
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &per_sm, vl_force_persistent_kernel<P, EV, N3, U, SOA>, 32 * kVLWarps, 0);
-    int blocks = sms * (per_sm > 0 ? per_sm : 1);
-    if (blocks > 148 * 64) blocks = 148 * 64;
-    g_persistent_blocks = blocks;
-    vl_force_persistent_kernel<P, EV, N3, U, SOA><<<blocks, 32 * kVLWarps, 0, s>>>(
-        (int)n_owned, (int)ntiles, pos4, q, (const long long*)tile_off, kmax, nbr, k, fx, fy, fz,
-        ev, stats);
-  } else {
-    const unsigned blocks = (unsigned)cdiv(ntiles, kVLWarps);
-    vl_force_kernel<P, EV, N3, U, SOA><<<blocks, 32 * kVLWarps, 0, s>>>(
-        (int)n_owned, (int)ntiles, pos4, q, (const long long*)tile_off, kmax, nbr, k, fx, fy, fz,
-        ev, stats);
-  }
+template <int P, bool EV, bool N3, int GM>
+static void launch_vl(int64_t n_owned, int64_t ntiles, const double* pos4, const SoA& q,
+                      const int64_t* tile_off, const int32_t* kmax, const int32_t* nbr,
+                      const LJK& k, double* fx, double* fy, double* fz, double* ev,
+                      lmd_stats* stats, cudaStream_t s) {
+  const unsigned blocks = (unsigned)cdiv(ntiles, kVLWarps);
+  vl_force_kernel<P, EV, N3, 2, GM><<<blocks, 32 * kVLWarps, 0, s>>>(
+      (int)n_owned, (int)ntiles, pos4, q, (const long long*)tile_off, kmax, nbr, k, fx, fy, fz, ev,
+      stats);
 }
 
 template <int P, bool EV, bool N3>
-static void launch_vl_u(int u, bool persistent, bool soa, int64_t n_owned, int64_t ntiles,
-                        const double* pos4, const SoA& q, const int64_t* tile_off,
-                        const int32_t* kmax, const int32_t* nbr, const LJK& k, double* fx,
-                        double* fy, double* fz, double* ev, lmd_stats* stats, cudaStream_t s) {
-#define LMD_VLU(UU, SS)                                                                          \
-  launch_vl<P, EV, N3, UU, SS>(persistent, n_owned, ntiles, pos4, q, tile_off, kmax, nbr, k, fx, \
-                               fy, fz, ev, stats, s)
-  if (soa) {
-    if (u == 2) LMD_VLU(2, true);
-    else LMD_VLU(4, true);
-  } else {
-    if (u == 2) LMD_VLU(2, false);
-    else LMD_VLU(4, false);
-  }
-#undef LMD_VLU
+static void launch_vl_g(int gm, int64_t n_owned, int64_t ntiles, const double* pos4,
+                        const SoA& q, const int64_t* tile_off, const int32_t* kmax,
+                        const int32_t* nbr, const LJK& k, double* fx, double* fy, double* fz,
+                        double* ev, lmd_stats* stats, cudaStream_t s) {
+  if (gm == 1)
+    launch_vl<P, EV, N3, 1>(n_owned, ntiles, pos4, q, tile_off, kmax, nbr, k, fx, fy, fz, ev,
+                            stats, s);
+  else
+    launch_vl<P, EV, N3, 0>(n_owned, ntiles, pos4, q, tile_off, kmax, nbr, k, fx, fy, fz, ev,
+                            stats, s);
 }
 
 extern "C" {
@@ -535,14 +574,14 @@ int lmd_force_vl(int pattern, int newton3, int flags, const lmd_lj* lj, int64_t 
   const int64_t ntiles = lmd_vl_num_tiles(n_owned, pattern);
   cudaStream_t s = (cudaStream_t)stream;
   const bool ev = (flags & LMD_FLAG_ENERGY) != 0;
-  // tuning knobs: bits 4-5 == 2 -> 2-wide gathers (else 4), bit 6 persistent grid;
-  // soa != NULL gathers x, y, z from SoA arrays soa[0..ntot), soa[ntot..), ...
-  const int u = ((flags >> 4) & 3) == 2 ? 2 : 4;
-  const bool persistent = (flags >> 6) & 1;
+  // gathers: soa != NULL -> x, y, z from SoA arrays soa[0..ntot), soa[ntot..), ...;
+  // else the 256-bit pos4 record (a 128 + 64-bit x, y, z variant measured 20 %
+  // slower)
+  const int gm = soa ? 1 : 0;
   const SoA q = {soa, soa ? soa + ntot : nullptr, soa ? soa + 2 * ntot : nullptr};
 #define LMD_VLK(P, EVB, N3B)                                                                  \
-  launch_vl_u<P, EVB, N3B>(u, persistent, soa != nullptr, n_owned, ntiles, pos4, q, tile_off,  \
-                           kmax, nbr, k, fx, fy, fz, ev_scratch, stats, s)
+  launch_vl_g<P, EVB, N3B>(gm, n_owned, ntiles, pos4, q, tile_off, kmax, nbr, k, fx, fy, fz,   \
+                           ev_scratch, stats, s)
 #define LMD_VL_P(P)                         \
   do {                                      \
     if (ev) {                               \
@@ -564,8 +603,7 @@ int lmd_force_vl(int pattern, int newton3, int flags, const lmd_lj* lj, int64_t 
 #undef LMD_VLK
   LMD_CHECK_LAUNCH();
   if (ev) {
-    const int64_t slots = persistent ? (int64_t)g_persistent_blocks * kVLWarps
-                                     : cdiv(ntiles, kVLWarps) * kVLWarps;
+    const int64_t slots = cdiv(ntiles, kVLWarps) * kVLWarps;
     return reduce_ev(ev_scratch, slots, stats, s);
   }
   return LMD_OK;

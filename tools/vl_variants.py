@@ -1,5 +1,6 @@
 """Time the Verlet-list force kernels per pattern on the bench workload:
-per-particle lists (csrc/vl.cu, unroll x persistent-grid knobs) and i-cluster
+per-particle lists (csrc/vl.cu; gather modes pos4 / SoA, line-aligned
+entry order) and i-cluster
 lists (csrc/vl_ci.cu, CI = 2 and 4).  One line per variant; L2 flushed
 between launches; also the build time of each list layout."""
 import os
@@ -21,6 +22,7 @@ cont.refresh(buf)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 patterns = os.environ.get("PATTERNS", "v_by_one,half_by_two").split(",")
 cis = [int(c) for c in os.environ.get("CIS", "1,2,4").split(",")]
+aligns = [int(a) for a in os.environ.get("ALIGNS", "0,16").split(",")]
 
 
 def timed(fn, reps=6):
@@ -39,11 +41,18 @@ def timed(fn, reps=6):
 
 for pname in patterns:
     pat = B.PatternKind(pname)
-    for ci in cis:
+    for ci, al in [(c, a) for c in cis for a in aligns]:
         cont.i_cluster = ci
-        variants = ((0, 4, 0), (2, 2, 0), (2, 2, 1)) if ci == 1 else ((2, 2, 0),)
-        for ucode, u, pers in variants:
-            cont.knobs = (ucode << 4) | (pers << 6)
+        cont.align_window = al
+        variants = (("pos4", 0, False), ("soa", 0, True))
+        if ci > 1 or os.environ.get("FAST"):
+            variants = (("pos4", 0, False),)
+        for gname, knob, soa in variants:
+            if ci > 1 and gname != "pos4":
+                continue
+            cont.knobs = knob
+            cont.use_soa = soa
+            cont.refresh(buf)
             cont._lists.clear()
             torch.cuda.synchronize()
             tb = timed(lambda: (cont._lists.clear(), cont._list(pat, False)), reps=3)
@@ -51,5 +60,5 @@ for pname in patterns:
             us = timed(lambda: cont.launch_force(pat, False, stats_t=st))
             s = N.read_stats(st)
             ent = cont.list_entries(pat, False)
-            print(f"{pname:12s} CI={ci} U={u} persistent={pers}  force {us:8.1f} us  "
+            print(f"{pname:12s} CI={ci} align={al:2d} gather={gname:4s}  force {us:8.1f} us  "
                   f"build {tb:8.1f} us  entries={ent}  pairs={s.pair_interactions}", flush=True)
