@@ -204,8 +204,14 @@ def check(status: int, what: str = "") -> None:
     raise NativeLibraryError(where + msg)
 
 
+_FUNCS: dict = {}
+
+
 def call(name: str, *args) -> None:
-    check(getattr(load(), name)(*args), name)
+    f = _FUNCS.get(name)
+    if f is None:
+        f = _FUNCS[name] = getattr(load(), name)
+    check(f(*args), name)
 
 
 def ptr(t: torch.Tensor | None) -> int | None:
@@ -217,7 +223,9 @@ def ptr(t: torch.Tensor | None) -> int | None:
 
 
 def stream() -> int:
-    return torch.cuda.current_stream().cuda_stream
+    """The current CUDA stream of the current device (raw handle): kernels go
+    wherever torch's work goes, including a graph-capture stream."""
+    return torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice())
 
 
 def make_box(box) -> Box:

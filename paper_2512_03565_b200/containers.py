@@ -157,7 +157,12 @@ class LinkedCellsContainer:
         self._stats_cache: dict = {}
         self._tables_ready = False
         # Newton3 on lc_c08/lc_c18: "colored" dual-write passes, or "full_shell"
-        self.n3_mode = "colored"
+        # Newton3 on lc_c08/lc_c18: "full_shell" evaluates every pair from both
+        # sides with the reference's Newton3 pair bookkeeping; "colored" runs
+        # the dual-write color passes.  Both are deterministic; the full shell
+        # measured 2-3.5x faster at 1M particles and 6-20x at 8,000
+        # (tools/n3_modes.py).
+        self.n3_mode = "full_shell"
         self._max_cell = 1
 
     # ------------------------------------------------------------ geometry
@@ -382,9 +387,9 @@ class LinkedCellsContainer:
         """Launch the force phase on the current stream without synchronising;
         returns the device stats tensor (pair counts, overlap flag, energy).
 
-        Newton3 on lc_c08 / lc_c18 runs the colored dual-write traversal
-        (lmd_force_lc_n3: one launch per color, deterministic); otherwise the
-        27-cell full shell (lmd_force_lc).  Both weight cells that hold owned
+        Newton3 on lc_c08 / lc_c18 runs, with n3_mode="colored", the colored
+        dual-write traversal (lmd_force_lc_n3: one launch per color,
+        deterministic); otherwise the 27-cell full shell (lmd_force_lc).  Both weight cells that hold owned
         particles and images the way the reference's duplicated anchor units
         do (traversals.py:133)."""
         if not self._tables_ready:
