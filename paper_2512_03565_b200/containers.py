@@ -163,6 +163,8 @@ class LinkedCellsContainer:
         # measured 2-3.5x faster at 1M particles and 6-20x at 8,000
         # (tools/n3_modes.py).
         self.n3_mode = "full_shell"
+        # V_BY_ONE as thread-per-i over consecutive particles (lmd_force_lc_particles)
+        self.thread_per_particle = True
         self._max_cell = 1
 
     # ------------------------------------------------------------ geometry
@@ -217,6 +219,7 @@ class LinkedCellsContainer:
         self.n_owned = n
         self._perm = self._sorter.bin(self.grid, 0, d.pos_x, d.pos_y, d.pos_z, 0,
                                       self._o_start, self._o_count)
+        self._cell_of = self._sorter.cell_sorted[:n].clone()   # rebuild-time cell per slot
         if n:
             # one host read for the ownership check and the peak occupancy
             bad, peak = torch.stack([(d.ownership != OWNED).any().to(torch.int32),
@@ -410,14 +413,24 @@ class LinkedCellsContainer:
                    N.ptr(self._h_count), N.ptr(self._dup), self._max_cell, N.ptr(self._fx),
                    N.ptr(self._fy), N.ptr(self._fz), N.ptr(ev_t), N.ptr(stats_t), N.stream())
             return stats_t
+        dup = None if traversal == N.LC_C01 else N.ptr(self._dup)
+        if self.thread_per_particle and pattern is PatternKind.V_BY_ONE:
+            slots = int(N.load().lmd_lc_tpi_ev_slots(self.n_owned))
+            if ev_t is None or ev_t.numel() < 2 * slots:
+                ev_t = torch.empty(2 * max(slots, 1), dtype=torch.float64, device=dev)
+            N.call("lmd_force_lc_particles", self.grid, N.make_lj(self.params),
+                   N.FLAG_ENERGY if energy else 0, N.ptr(self._pos4), self.n_owned,
+                   N.ptr(self._cell_of), N.ptr(self._start), N.ptr(self._count), dup,
+                   N.ptr(self._fx), N.ptr(self._fy), N.ptr(self._fz), N.ptr(ev_t),
+                   N.ptr(stats_t), N.stream())
+            return stats_t
         if ev_t is None:
             slots = int(N.load().lmd_lc_ev_slots(self.grid))
             ev_t = torch.empty(2 * slots, dtype=torch.float64, device=dev)
         N.call("lmd_force_lc", self.grid, N.make_lj(self.params), pattern.code,
                N.FLAG_ENERGY if energy else 0, N.ptr(self._pos4), N.ptr(self._start),
-               N.ptr(self._count), None if traversal == N.LC_C01 else N.ptr(self._dup),
-               N.ptr(self._fx), N.ptr(self._fy), N.ptr(self._fz), N.ptr(ev_t),
-               N.ptr(stats_t), N.stream())
+               N.ptr(self._count), dup, N.ptr(self._fx), N.ptr(self._fy), N.ptr(self._fz),
+               N.ptr(ev_t), N.ptr(stats_t), N.stream())
         return stats_t
 
     def compute_forces(self, traversal, newton3: bool, pattern, vector_width: int,

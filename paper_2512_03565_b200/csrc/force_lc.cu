@@ -115,6 +115,81 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
   }
 }
 
+// Thread per owned particle (the V_BY_ONE order as "thread-per-i"): lane i
+// of a warp is the i-th particle of the cell-sorted backing, so a warp's 32
+// i are consecutive particles spanning ~2-3 cells instead of one cell's ~12
+// (warp-per-cell leaves most of 32 i lanes empty at cell size rc).  Each
+// lane sweeps its rebuild-time cell's 27-cell shell in the same unit order,
+// with the same per-pair arithmetic and unit multiplicity as lc_force_kernel;
+// lanes of one cell read the same j (broadcast loads).
+template <bool EV>
+__global__ void __launch_bounds__(128)
+    lc_tpi_kernel(int n_owned, long long t0, long long t1, LJK k, const double* __restrict__ pos4,
+                  const int32_t* __restrict__ cell_of, const int32_t* __restrict__ cstart,
+                  const int32_t* __restrict__ ccount, const uint8_t* __restrict__ dup,
+                  double* __restrict__ fx, double* __restrict__ fy, double* __restrict__ fz,
+                  double* __restrict__ ev, lmd_stats* __restrict__ stats) {
+  const int lane = threadIdx.x & 31;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const long long warp = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  double e_acc = 0.0, v_acc = 0.0;
+  int pairs = 0, pairs_halo = 0, overlap = 0;
+  if (i < n_owned) {
+    const long long lin = cell_of[i];
+    const double4 pi = ld_pos4(pos4, i);
+    double ax = 0.0, ay = 0.0, az = 0.0;
+    for (int d = 0; d < 27; ++d) {
+      const int dx = d / 9 - 1, dy = (d / 3) % 3 - 1, dz = d % 3 - 1;
+      const long long nl = lin + dx + t0 * (dy + t1 * dz);
+      const int js = cstart[nl], jn = ccount[nl];
+      const double fm = (dup && nl != lin) ? 1.0 + (double)dup[nl < lin ? nl : lin] : 1.0;
+      for (int j = js; j < js + jn; ++j) {
+        if (j == i) continue;
+        const double4 pj = ld_pos4(pos4, j);
+        if (pj.w == (double)LMD_DUMMY) continue;
+        const double ddx = pi.x - pj.x, ddy = pi.y - pj.y, ddz = pi.z - pj.z;
+        const double r2 = r2_exact(ddx, ddy, ddz);
+        if (r2 >= k.rc2) continue;
+        if (r2 == 0.0) {
+          overlap = 1;
+          continue;
+        }
+        double s6;
+        const double f = lj_scalar(r2, k, s6) * fm;
+        ax = fma(f, ddx, ax);
+        ay = fma(f, ddy, ay);
+        az = fma(f, ddz, az);
+        const int m = fm > 1.5 ? 2 : 1;
+        pairs += m;
+        if (pj.w != (double)LMD_OWNED) pairs_halo += m;
+        if (EV) {
+          e_acc = fma((0.5 * fm) * s6, fma(k.eps4, s6, -k.eps4), e_acc);
+          v_acc = fma(0.5 * f, r2, v_acc);
+        }
+      }
+    }
+    fx[i] = ax;
+    fy[i] = ay;
+    fz[i] = az;
+  }
+  const long long pr = warp_sum_ll((long long)pairs);
+  const long long ph = warp_sum_ll((long long)pairs_halo);
+  overlap = __any_sync(0xffffffffu, overlap);
+  if (lane == 0) {
+    if (pr) atomicAdd((unsigned long long*)&stats->pair_interactions, (unsigned long long)pr);
+    if (ph) atomicAdd((unsigned long long*)&stats->pairs_owned_halo, (unsigned long long)ph);
+    if (overlap) atomicOr(&stats->overlap, 1);
+  }
+  if (EV) {
+    e_acc = warp_sum(e_acc);
+    v_acc = warp_sum(v_acc);
+    if (lane == 0) {
+      ev[2 * warp] = e_acc;
+      ev[2 * warp + 1] = v_acc;
+    }
+  }
+}
+
 // --------------------------------------------------------- geometric stats
 struct CellView {
   int n;      // entries of buffer_at(lin)
@@ -261,6 +336,31 @@ int lmd_force_lc(const lmd_grid* g, const lmd_lj* lj, int pattern, int flags,
 #undef LMD_LC_ARGS
   LMD_CHECK_LAUNCH();
   if (ev) return reduce_ev(ev_scratch, lmd_lc_ev_slots(g), stats, s);
+  return LMD_OK;
+}
+
+int64_t lmd_lc_tpi_ev_slots(int64_t n_owned) { return cdiv(n_owned, 128) * 4; }
+
+int lmd_force_lc_particles(const lmd_grid* g, const lmd_lj* lj, int flags, const double* pos4,
+                           int64_t n_owned, const int32_t* cell_of, const int32_t* cell_start,
+                           const int32_t* cell_count, const uint8_t* dup, double* fx, double* fy,
+                           double* fz, double* ev_scratch, lmd_stats* stats, void* stream) {
+  if (n_owned <= 0) return LMD_OK;
+  if (n_owned > 0x7fffffffLL) return LMD_ERR_CONFIG;
+  const LJK k = make_ljk(lj);
+  const bool ev = (flags & LMD_FLAG_ENERGY) != 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  const unsigned blocks = (unsigned)cdiv(n_owned, 128);
+  if (ev)
+    lc_tpi_kernel<true><<<blocks, 128, 0, s>>>((int)n_owned, g->tdims[0], g->tdims[1], k, pos4,
+                                               cell_of, cell_start, cell_count, dup, fx, fy, fz,
+                                               ev_scratch, stats);
+  else
+    lc_tpi_kernel<false><<<blocks, 128, 0, s>>>((int)n_owned, g->tdims[0], g->tdims[1], k, pos4,
+                                                cell_of, cell_start, cell_count, dup, fx, fy, fz,
+                                                ev_scratch, stats);
+  LMD_CHECK_LAUNCH();
+  if (ev) return reduce_ev(ev_scratch, lmd_lc_tpi_ev_slots(n_owned), stats, s);
   return LMD_OK;
 }
 

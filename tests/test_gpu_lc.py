@@ -252,10 +252,11 @@ def test_colored_newton3_matches_full_shell_and_is_deterministic(rng, trav):
         assert abs(sc.epot - sf.epot) <= 1e-12 * abs(sf.epot)
 
 
-def test_full_shell_dup_cells_energy_and_determinism(rng):
-    """Full-shell kernel against the oracle with dup-weighted cells (images
-    mid-step in owned cells), energy/virial, and run-to-run bitwise
-    determinism, for every pattern."""
+@pytest.mark.parametrize("tpi", [True, False])
+def test_full_shell_dup_cells_energy_and_determinism(rng, tpi):
+    """Full-shell kernels (warp per cell; V_BY_ONE also thread per particle)
+    against the oracle with dup-weighted cells (images mid-step in owned
+    cells), energy/virial, and run-to-run bitwise determinism."""
     n = 6000
     span = (n / 0.7) ** (1 / 3)
     pos = jittered_lattice(rng, (19, 19, 19), span / 19, 0.3)[:n]
@@ -269,6 +270,7 @@ def test_full_shell_dup_cells_energy_and_determinism(rng):
         prev = None
         for _ in range(2):
             cont = B.LinkedCellsContainer(_box(span, True), params)
+            cont.thread_per_particle = tpi
             buf = _buf(pos)
             cont.rebuild(buf)
             cont.refresh(buf)
@@ -282,3 +284,28 @@ def test_full_shell_dup_cells_energy_and_determinism(rng):
             if prev is not None:
                 assert np.array_equal(prev, f)
             prev = f
+
+
+def test_thread_per_particle_between_rebuilds_uses_rebuild_cells(rng):
+    """With a skin, particles move between rebuilds while staying in their
+    rebuild-time cells: the thread-per-particle kernel must sweep those cells
+    (as the warp-per-cell kernel does), not cells recomputed from positions."""
+    pos = jittered_lattice(rng, (16, 16, 16), 1.1, 0.2)
+    span = 16 * 1.1
+    params = LJParams(cutoff=2.5, skin=0.4)
+    box = _box(span, True)
+    moved = np.mod(pos + rng.uniform(-0.15, 0.15, pos.shape), span)
+    res = {}
+    for tpi in (True, False):
+        cont = B.LinkedCellsContainer(box, params)
+        cont.thread_per_particle = tpi
+        buf = _buf(pos)
+        cont.rebuild(buf)
+        cont.refresh(buf)
+        buf2 = _buf(moved)
+        cont.refresh_positions(buf2)
+        st = cont.compute_forces("lc_c01", False, PatternKind.V_BY_ONE, 8)
+        cont.collect_forces(buf2)
+        res[tpi] = (st.pair_interactions, buf2.forces().cpu().numpy())
+    assert res[True][0] == res[False][0]
+    assert forces_close(res[True][1], res[False][1])
