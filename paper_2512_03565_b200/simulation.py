@@ -158,8 +158,11 @@ def run_md(owned, box, params, iterations: int, vector_width: int = 8, *,
     retunes = 0
     force_time = 0.0
     start = time.perf_counter()
+    whole = metric == "iteration"
     try:
         for it in range(iterations):
+            if whole:
+                provider.begin_region()
             velocity_verlet_step(owned, params, PRE_FORCE, check=False)
             if tuner is not None:
                 if retune_drift and it > 0 and tuner.selected is not None and it % 10 == 0:
@@ -189,21 +192,32 @@ def run_md(owned, box, params, iterations: int, vector_width: int = 8, *,
             else:
                 cont.refresh(owned)
             cont.steps_since_rebuild += 1
-            provider.begin_region()
+            # lazily built structures (Verlet lists per interaction order) are
+            # built here, outside the force-phase bracket: the reference's
+            # bracket holds the force computation only (driver.py:203-207)
+            built = cfg.container is ContainerKind.VERLET_LISTS and \
+                cont.ensure_lists(cfg.pattern, cfg.newton3)
+            if whole:
+                # the iteration bracket sees every build: such samples are displaced
+                rebuilt = rebuilt or fresh or built
+            if not whole:
+                provider.begin_region()
             t0 = time.perf_counter()
             stats_t = _launch(cont, cfg, vector_width, energy)
-            sample = provider.end_region() if metric != "laneops" else None
+            sample = provider.end_region() if metric not in ("laneops", "iteration") else None
             stats = _finish(cont, cfg, vector_width, stats_t)
             force_time += time.perf_counter() - t0
             lane_total[0] += stats.lane_slots
-            if sample is None:
+            if sample is None and not whole:
                 sample = provider.end_region()
             cont.collect_forces(owned)
-            if tuner is not None:
-                tuner.record_sample(sample, displaced=rebuilt)
             velocity_verlet_step(owned, params, POST_FORCE, check=False)
             if wrap == "always":
                 apply_boundaries(owned, box)
+            if whole:
+                sample = provider.end_region()
+            if tuner is not None:
+                tuner.record_sample(sample, displaced=rebuilt)
             if record:
                 records.append(IterationRecord(it, phase, cfg, sample, stats.lane_slots,
                                                stats.useful_interactions, stats.blank_lanes,

@@ -285,6 +285,17 @@ class VerletListContainer:
         self._lists[key] = hit
         return hit
 
+    def ensure_lists(self, pattern, newton3: bool) -> bool:
+        """Build the lists for this interaction order now (outside any timed
+        region); True if they had to be built."""
+        pattern = as_pattern(pattern)
+        ci = self._ci_for(newton3)
+        key = (pattern.code, bool(newton3), ci, self.align_window)
+        if key in self._lists:
+            return False
+        self._list(pattern, newton3)
+        return True
+
     def list_entries(self, pattern, newton3: bool) -> int:
         """List entries the force kernel reads for `pattern` (padded to whole
         fill steps and 4-step chunks; 4 B each)."""

@@ -68,7 +68,8 @@ def test_tuner_samples_every_config_and_selects_by_replay(tmp_path):
         assert seen == {c.label: 2 for c in configs}
 
 
-def test_time_metric_tuner_runs_all_containers():
+@pytest.mark.parametrize("metric", ["time", "iteration"])
+def test_time_metric_tuner_runs_all_containers(metric):
     rng = np.random.default_rng(5)
     n = 4000
     span = (n / 0.7) ** (1 / 3)
@@ -81,8 +82,11 @@ def test_time_metric_tuner_runs_all_containers():
                                      [B.PatternKind.V_BY_ONE, B.PatternKind.HALF_BY_TWO])
     buf = ParticleBuffer.from_positions(pos, device="cuda")
     records, summary = run_md(buf, box, params, len(configs) + 5, 8, configurations=configs,
-                              policy=TuningPolicy(1, len(configs) + 5, "mean", "time"),
-                              metric="time")
+                              policy=TuningPolicy(1, len(configs) + 5, "mean", metric),
+                              metric=metric)
     assert len(summary.phase_selections) == 1
     pairs = {r.pair_interactions for r in records[:2]}
     assert min(r.metric_value for r in records) > 0
+    if metric == "iteration":   # the whole step contains the force phase
+        force = {r.configuration.label: r.metric_value for r in records}
+        assert all(v > 0 for v in force.values())

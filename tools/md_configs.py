@@ -34,7 +34,8 @@ def main():
     ap.add_argument("--config", type=int, default=1)
     ap.add_argument("--steps", type=int, default=None)
     ap.add_argument("--n", type=int, default=None)
-    ap.add_argument("--metric", default="time")
+    ap.add_argument("--metric", default="iteration",
+                    help="tuner metric: iteration (whole MD step), time (force phase), laneops")
     ap.add_argument("--rho", default="0.2,0.5,0.8")
     args = ap.parse_args()
     torch.cuda.set_device(0)
@@ -103,7 +104,13 @@ def main():
         "generation_s": t_gen, "note": w.note,
         "tuning_iterations": sum(r.phase == "tuning" for r in records),
         "configs_seen": sorted({r.configuration.label for r in records}),
+        "metric": args.metric,
     }
+    per = {}
+    for r in records:
+        per.setdefault((r.phase, r.configuration.label), []).append(r.metric_value)
+    out["mean_metric_ms"] = {f"{ph}:{lab}": round(sum(v) / len(v) * 1e-6, 4)
+                             for (ph, lab), v in sorted(per.items())}
     if args.config == 1:
         out["pairs_per_step"] = [r.pair_interactions for r in records]
     print(json.dumps(out))
