@@ -36,3 +36,19 @@ def test_two_ranks_on_one_gpu_gloo():
     s = json.loads([ln for ln in single.stdout.splitlines() if ln.startswith("{")][-1])
     one = s["config"]["pairs_per_step"]
     assert abs(d["config"]["pairs_per_step"] - 2 * one) < 1e-3 * one
+
+
+def test_brick_md_two_ranks_matches_single_domain():
+    """run_md_bricks on 2 ranks (one GPU, gloo): migration at every rebuild,
+    ghost exchange every step; per-step global pair counts equal to the
+    single-domain loop's and final positions equal to rounding."""
+    env = dict(os.environ, LMD_DIST_BACKEND="gloo", LMD_DEVICE="0")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29562", "tools/md_bricks_check.py",
+           "--particles", "60000", "--steps", "22"]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert d["rebuilds"] >= 3 and d["ids_complete"]
+    assert d["single_pairs_equal"]
+    assert d["max_position_diff"] < 1e-10
