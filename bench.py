@@ -515,8 +515,23 @@ def sweep(args, w, torch, N, flush):
         _, t = time_steps(phase, 5, flush, torch)
         st = N.read_stats(phase.stats_t)
         pairs = finish(cfg, st, (0, 0, 0)).pair_interactions
-        rows.append({"config": label, "ms": min(t) * 1e3, "pairs": pairs,
-                     "pairs_per_s": pairs / min(t)})
+        row = {"config": label, "ms": min(t) * 1e3, "pairs": pairs,
+               "pairs_per_s": pairs / min(t)}
+        if hasattr(cont, "gpu_lane_stats") and not (cfg.container.value == "lc" and
+                                                     cont.uses_colored_n3(phase.trav,
+                                                                          cfg.newton3)):
+            try:
+                steps, active = (cont.gpu_lane_stats(cfg.pattern, phase.trav, cfg.newton3)
+                                 if cfg.container.value == "lc"
+                                 else cont.gpu_lane_stats(cfg.pattern, cfg.newton3))
+                row.update({"gpu_lane_steps": steps, "gpu_active_lanes": active,
+                            "gpu_lane_utilisation": active / max(steps, 1),
+                            # N3 runs evaluate ordered pairs; the reported count is Newton3's
+                            "gpu_pair_lanes_fraction": (None if cfg.newton3
+                                                        else pairs / max(steps, 1))})
+            except Exception as exc:  # noqa: BLE001 -- reported, not fatal
+                row["gpu_lane_stats_error"] = str(exc)[:200]
+        rows.append(row)
         print(f"sweep {label:36s} {min(t) * 1e3:8.3f} ms  {pairs / min(t):.3e} pairs/s",
               file=sys.stderr)
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)

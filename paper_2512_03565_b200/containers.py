@@ -382,6 +382,35 @@ class LinkedCellsContainer:
         self._stats_cache[key] = hit
         return hit
 
+    def gpu_lane_stats(self, pattern, traversal=N.LC_C01, newton3: bool = False):
+        """Physical lane use of the kernel that executes this configuration
+        (the GPU analogue of the reference's lane statistics):
+        (lane_steps, active_lanes) = 32 x warp fill steps executed, and the
+        lanes of those steps holding a real (i, j) candidate.  Exact by
+        construction: warp per cell sweeps ceil(nC/A) x ceil(nD/B) fills per
+        occupied (C, D) at width 32 -- the reference's c01 formula at V = 32;
+        thread per particle runs, per warp of 32 consecutive particles and
+        per neighbour offset, as many steps as the lane with the largest
+        neighbour cell.  Colored Newton3 passes are not covered."""
+        pattern = as_pattern(pattern)
+        if self.uses_colored_n3(traversal, newton3):
+            raise ConfigurationError("lane statistics cover the full-shell kernels")
+        _, _, useful = self._lc_stats(N.LC_C01, False, pattern, 32)
+        if self.thread_per_particle and pattern is PatternKind.V_BY_ONE:
+            n = self.n_owned
+            t0, t1 = int(self.total_dims[0]), int(self.total_dims[1])
+            offs = torch.tensor([(d // 9 - 1) + t0 * ((d // 3) % 3 - 1 + t1 * (d % 3 - 1))
+                                 for d in range(27)], dtype=torch.int64, device=self._pos4.device)
+            cells = self._cell_of.long()
+            pad = (-n) % 32
+            per = self._count.long()[cells[:, None] + offs[None, :]]          # (n, 27)
+            if pad:
+                per = torch.cat([per, torch.zeros((pad, 27), dtype=per.dtype, device=per.device)])
+            steps = int(per.view(-1, 32, 27).amax(dim=1).sum().item())
+            return 32 * steps, useful
+        _, slots, _ = self._lc_stats(N.LC_C01, False, pattern, 32)
+        return slots, useful
+
     def uses_colored_n3(self, traversal, newton3: bool) -> bool:
         return bool(newton3) and traversal in (N.LC_C08, N.LC_C18) and self.n3_mode == "colored"
 

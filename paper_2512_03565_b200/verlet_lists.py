@@ -285,6 +285,21 @@ class VerletListContainer:
         self._lists[key] = hit
         return hit
 
+    def gpu_lane_stats(self, pattern, newton3: bool = False):
+        """(lane_steps, active_lanes) of the force kernel over the current
+        lists: every tile runs kmax/B fill steps on 32 lanes; a lane is
+        active when its entry is a real neighbour, not the sentinel pad
+        (SURVEY §8f-4).  Exact by construction of the list layout."""
+        pattern = as_pattern(pattern)
+        _, kmax, _, _ = self._list(pattern, newton3)
+        b = pattern.shape(32)[1]
+        ntiles = int(N.load().lmd_vl_num_tiles(self.n_owned, pattern.code))
+        steps = int((kmax[:ntiles].long() // b).sum().item())
+        active = int(self._count(newton3, pattern)[: self.n_owned].long().sum().item())
+        if self._ci_for(newton3) > 1:   # union lists: one entry serves a cluster
+            raise ConfigurationError("lane statistics cover per-particle lists")
+        return 32 * steps, active
+
     def ensure_lists(self, pattern, newton3: bool) -> bool:
         """Build the lists for this interaction order now (outside any timed
         region); True if they had to be built."""

@@ -309,3 +309,48 @@ def test_thread_per_particle_between_rebuilds_uses_rebuild_cells(rng):
         res[tpi] = (st.pair_interactions, buf2.forces().cpu().numpy())
     assert res[True][0] == res[False][0]
     assert forces_close(res[True][1], res[False][1])
+
+
+def test_gpu_lane_stats_lc_and_vl(rng):
+    """Physical lane use of the executing kernels: recomputed
+    here from the cell tables / list layout independently."""
+    pos = jittered_lattice(rng, (14, 14, 14), 1.05, 0.3)
+    span = 14 * 1.05
+    box = _box(span, True)
+    cont = B.LinkedCellsContainer(box, LJParams(cutoff=2.5, skin=0.0))
+    buf = _buf(pos)
+    cont.rebuild(buf)
+    cont.refresh(buf)
+    # warp per cell: the reference's c01 formula at V = 32
+    for pat in (PatternKind.ONE_BY_V, PatternKind.HALF_BY_TWO):
+        steps, active = cont.gpu_lane_stats(pat)
+        inv, slots, useful = cont._lc_stats(B.traversals.traversal_code(TraversalKind.LC_C01),
+                                            False, pat, 32)
+        assert (steps, active) == (slots, useful)
+    # thread per particle: per warp of 32 consecutive particles and per
+    # neighbour offset, the largest neighbour cell
+    steps, active = cont.gpu_lane_stats(PatternKind.V_BY_ONE)
+    cells = cont._cell_of.cpu().numpy().astype(np.int64)
+    count = cont._count.cpu().numpy().astype(np.int64)
+    t0, t1 = int(cont.total_dims[0]), int(cont.total_dims[1])
+    want = 0
+    for w0 in range(0, len(cells), 32):
+        c = cells[w0:w0 + 32]
+        for d in range(27):
+            off = (d // 9 - 1) + t0 * ((d // 3) % 3 - 1 + t1 * (d % 3 - 1))
+            want += int(count[c + off].max())
+    assert steps == 32 * want and 0 < active <= steps
+    # Verlet lists: tiles x kmax / B steps; active = list entries
+    vl = B.VerletListContainer(box, LJParams(cutoff=2.5, skin=0.3))
+    vl.rebuild(buf)
+    vl.refresh(buf)
+    for pat in PATTERNS:
+        steps, active = vl.gpu_lane_stats(pat, False)
+        inv, slots, useful = vl.vl_stats(False, pat, 32)
+        a, b = pat.shape(32)
+        cnt = vl._count(False, pat)[: vl.n_owned].cpu().numpy().astype(np.int64)
+        pad = (-len(cnt)) % a
+        m = np.concatenate([cnt, np.zeros(pad, np.int64)]).reshape(-1, a).max(axis=1)
+        fills = -(-m // b)
+        want = int((-(-fills // 4) * 4).sum())          # whole 4-step index chunks
+        assert active == useful and steps == 32 * want and steps >= slots
