@@ -90,3 +90,25 @@ def test_time_metric_tuner_runs_all_containers(metric):
     if metric == "iteration":   # the whole step contains the force phase
         force = {r.configuration.label: r.metric_value for r in records}
         assert all(v > 0 for v in force.values())
+
+
+def test_energy_metric_reads_board_energy():
+    """NVML energy over a ~0.3 s DFMA burn is positive; run_md accepts the
+    metric (samples are coarse, >= 0)."""
+    m = B.make_metric_provider("energy", lambda: 0)
+    out = torch.empty(148 * 8 * 256, dtype=torch.float64, device="cuda")
+    m.begin_region()
+    import time as _t
+    t0 = _t.perf_counter()
+    while _t.perf_counter() - t0 < 0.3:
+        B._native.call("lmd_dfma_burn", 148 * 8, 256, 20000, B._native.ptr(out), None)
+        torch.cuda.synchronize()
+    assert m.end_region() > 0
+    rng = np.random.default_rng(2)
+    grid = np.stack(np.meshgrid(*[np.arange(10)] * 3, indexing="ij"), -1).reshape(-1, 3)
+    pos = (grid + 0.5) * 1.1 + rng.uniform(-0.05, 0.05, grid.shape)
+    buf = ParticleBuffer.from_positions(pos, device="cuda")
+    cfg = B.Configuration.parse("vl,vl,false,v_by_one")
+    records, _ = run_md(buf, SimulationBox.cube(11.0, periodic=True), LJParams(cutoff=2.5,
+                        skin=0.3, dt=0.001), 4, 8, fixed_config=cfg, metric="energy")
+    assert all(r.metric_value >= 0 for r in records)

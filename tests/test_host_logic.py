@@ -174,3 +174,15 @@ def test_cluster_size_is_a_tuning_dimension():
     assert Configuration.parse("vcl,vcl,true,half_by_two,m8").cluster_size == 8
     with pytest.raises(ConfigurationError):
         Configuration.parse("lc,lc_c08,true,half_by_two,m8")
+
+
+def test_energy_metric_needs_a_device():
+    """The NVML energy metric (the paper's PMT analogue) refuses to run
+    without a CUDA device instead of falling back to a host clock."""
+    import torch
+
+    import paper_2512_03565_b200 as B
+    if torch.cuda.is_available():
+        pytest.skip("host-only check")
+    with pytest.raises(B.ConfigurationError):
+        B.make_metric_provider("energy", lambda: 0)
