@@ -255,15 +255,18 @@ def algorithmic_bytes(cfg, cont, stats, n):
     return int(b)
 
 
-def finish(cfg, st, geo):
+def finish(cfg, st, geo, cont):
+    """KernelStats in the reference's pair convention for the kernel that ran
+    (the container knows whether Newton3 pairs were seen from both sides)."""
     from paper_2512_03565_b200 import KernelStats
     from paper_2512_03565_b200.containers import LinkedCellsContainer
+    from paper_2512_03565_b200.traversals import traversal_code
     if cfg.container.value == "lc":
-        once = cfg.newton3 and cfg.traversal.value in ("lc_c08", "lc_c18")
+        once = cont.uses_colored_n3(traversal_code(cfg.traversal), cfg.newton3)
         return LinkedCellsContainer.finish_stats(st, cfg.newton3 and not once, *geo)
     if cfg.container.value == "vcl":
         return LinkedCellsContainer.finish_stats(st, cfg.newton3, *geo)
-    return KernelStats(geo[0], geo[1], geo[2], int(st.pair_interactions))
+    return KernelStats(geo[0], geo[1], geo[2], cont.pair_count(st, cfg.newton3))
 
 
 def time_steps(phase, steps, flush, torch):
@@ -361,7 +364,7 @@ def run_b200(args):
         phase.launch()
     torch.cuda.synchronize()
     st = N.read_stats(phase.stats_t)
-    stats = finish(cfg, st, geo)
+    stats = finish(cfg, st, geo, cont)
     pairs = stats.pair_interactions
     n_local = int(buf.pos_x.shape[0])
 
@@ -514,7 +517,7 @@ def sweep(args, w, torch, N, flush):
             phase.launch()
         _, t = time_steps(phase, 5, flush, torch)
         st = N.read_stats(phase.stats_t)
-        pairs = finish(cfg, st, (0, 0, 0)).pair_interactions
+        pairs = finish(cfg, st, (0, 0, 0), cont).pair_interactions
         row = {"config": label, "ms": min(t) * 1e3, "pairs": pairs,
                "pairs_per_s": pairs / min(t)}
         if hasattr(cont, "gpu_lane_stats") and not (cfg.container.value == "lc" and

@@ -252,12 +252,13 @@ int lmd_vl_fill(const lmd_grid* g, double rl2, int newton3, int pattern, int64_t
  * nbr holds ceil(n_owned / A) * cap_steps * 32 entries.  Writes count[i],
  * tile_off, kmax and *max_count = the longest list; if *max_count >
  * cap_steps * B the lists were truncated and the caller must rebuild with a
- * larger capacity. */
+ * larger capacity.  count_half (nullable) receives each particle's half-list
+ * length (images, and owned j > i), the Newton3 statistics of full lists. */
 int lmd_vl_build(const lmd_grid* g, double rl2, int newton3, int pattern, int64_t n_owned,
                  int32_t sentinel, const double* pos4, const int32_t* o_start,
                  const int32_t* o_count, const int32_t* h_start, const int32_t* h_count,
-                 int32_t cap_steps, int32_t* count, int64_t* tile_off, int32_t* kmax,
-                 int32_t* max_count, int32_t* nbr, void* stream);
+                 int32_t cap_steps, int32_t* count, int32_t* count_half, int64_t* tile_off,
+                 int32_t* kmax, int32_t* max_count, int32_t* nbr, void* stream);
 /* Optional pass after lmd_vl_build / lmd_vl_ci_build: permutes every lane's
  * own slot sequence of every tile so that the lanes of a fill gather from
  * shared 128-B lines (window of `window` = 8, 16 or 32 entries per lane,
@@ -291,8 +292,11 @@ int lmd_force_vl_ci(int pattern, int ci, int flags, const lmd_lj* lj, int64_t n_
  * gathers), or, if soa != NULL, SoA copies x = soa[0..ntot), y, z of the
  * same ntot records (three 64-bit gathers that share sectors between
  * neighbouring lanes).  newton3 = 0
- * writes f[i]; newton3 = 1 accumulates with FP64 atomics into zeroed f
- * (j-side reactions; summation order is then not deterministic).
+ * writes f[i]; newton3 = 1 (half lists) accumulates with FP64 atomics into
+ * zeroed f (j-side reactions; summation order is then not deterministic);
+ * newton3 = 2 runs full lists like 0 and also counts the pairs with an image
+ * j into pairs_owned_halo, for the reference's Newton3 pair bookkeeping
+ * (owned-owned pairs once = (pairs - halo) / 2 + halo).
  * ev_scratch: 2 * lmd_vl_ev_slots(n_owned, pattern) doubles. */
 int64_t lmd_vl_ev_slots(int64_t n_owned, int pattern);
 int lmd_force_vl(int pattern, int newton3, int flags, const lmd_lj* lj, int64_t n_owned,

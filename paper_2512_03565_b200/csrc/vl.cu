@@ -120,6 +120,7 @@ __global__ void vl_build_kernel(GridK g, int n, int ntiles, int newton3,
                                 const int32_t* __restrict__ os, const int32_t* __restrict__ oc,
                                 const int32_t* __restrict__ hs, const int32_t* __restrict__ hc,
                                 int cap_steps, int32_t* __restrict__ count,
+                                int32_t* __restrict__ count_half,
                                 long long* __restrict__ toff, int32_t* __restrict__ kmax,
                                 int32_t* __restrict__ max_count, int32_t* __restrict__ nbr) {
   constexpr int A = Pattern<P>::A, B = Pattern<P>::B, pattern = P;
@@ -128,7 +129,7 @@ __global__ void vl_build_kernel(GridK g, int n, int ntiles, int newton3,
   const long long stride = (long long)cap_steps * 32;
   int32_t* out = nbr + (long long)t * stride;
   const int cap = cap_steps * B;
-  int k = 0;
+  int k = 0, kh = 0;
   if (i < n) {
     const double4 pi = ld_pos4(pos4, i);
     if (pi.w == (double)LMD_OWNED) {
@@ -163,6 +164,7 @@ __global__ void vl_build_kernel(GridK g, int n, int ntiles, int newton3,
                 while (mask) {
                   const int jj = j0 + __ffs(mask) - 1;
                   mask &= mask - 1u;
+                  kh += view || jj > i;
                   if (k < cap) {
                     const int st = k / B, l = lane_of(pattern, il, k % B);
                     out[(long long)(st / kChunk) * (32 * kChunk) + l * kChunk + st % kChunk] = jj;
@@ -174,6 +176,7 @@ __global__ void vl_build_kernel(GridK g, int n, int ntiles, int newton3,
       }
     }
     count[i] = k;
+    if (count_half) count_half[i] = kh;
   }
   // the tile's longest list (aligned groups of A lanes)
   int m = k;
@@ -267,7 +270,11 @@ __global__ void fill_i32_kernel(int64_t n, int32_t v, int32_t* __restrict__ out)
 }
 
 // ------------------------------------------------------------------ force
-template <bool EV, bool N3>
+// N3: 0 = full lists; 1 = half lists, the j side by FP64 atomics; 2 = full
+// lists with the reference's Newton3 pair bookkeeping (pairs with an image j
+// counted apart, the host halves the owned-owned ones): no atomics,
+// deterministic.
+template <bool EV, int N3>
 __device__ __forceinline__ void vl_pair(const double4& pi, const double4& pj, int j, int n_owned,
                                         const LJK& k, Acc& a, double* __restrict__ fx,
                                         double* __restrict__ fy, double* __restrict__ fz) {
@@ -285,13 +292,14 @@ __device__ __forceinline__ void vl_pair(const double4& pi, const double4& pj, in
   a.az = fma(f, dz, a.az);
   ++a.pairs;
   const bool jhalo = j >= n_owned;
-  if (N3 && !jhalo) {
+  if (N3 == 2) a.halo += jhalo;
+  if (N3 == 1 && !jhalo) {
     atomicAdd(fx + j, -f * dx);
     atomicAdd(fy + j, -f * dy);
     atomicAdd(fz + j, -f * dz);
   }
   if (EV) {
-    const double w = (N3 && !jhalo) ? 1.0 : 0.5;
+    const double w = (N3 == 1 && !jhalo) ? 1.0 : 0.5;
     a.e = fma(w * s6, fma(k.eps4, s6, -k.eps4), a.e);
     a.v = fma(w * f, r2, a.v);
   }
@@ -314,7 +322,7 @@ __device__ __forceinline__ double4 ld_j(const double* __restrict__ pos4, const S
   return ld_pos4(pos4, j);
 }
 
-template <int P, bool EV, bool N3, int U, int SOA>
+template <int P, bool EV, int N3, int U, int SOA>
 __device__ __forceinline__ void vl_tile(int t, int lane, int n_owned,
                                         const double* __restrict__ pos4, const SoA& q,
                                         const long long* __restrict__ toff,
@@ -353,7 +361,7 @@ __device__ __forceinline__ void vl_tile(int t, int lane, int n_owned,
   if (!iact) a.ax = a.ay = a.az = 0.0;
   const double rx = reduce_j<P>(a.ax), ry = reduce_j<P>(a.ay), rz = reduce_j<P>(a.az);
   if (iact && jo == 0) {
-    if (N3) {
+    if (N3 == 1) {
       atomicAdd(fx + i, rx);
       atomicAdd(fy + i, ry);
       atomicAdd(fz + i, rz);
@@ -370,7 +378,7 @@ __device__ __forceinline__ void vl_tile(int t, int lane, int n_owned,
 
 // One warp per i-tile.  The 2-wide gather variant trades memory-level
 // parallelism per warp for occupancy (64 registers, 8 blocks per SM).
-template <int P, bool EV, bool N3, int U, int SOA>
+template <int P, bool EV, int N3, int U, int SOA>
 __global__ void __launch_bounds__(32 * kVLWarps, 8)
     vl_force_kernel(int n_owned, int ntiles, const double* __restrict__ pos4, SoA q,
                     const long long* __restrict__ toff, const int32_t* __restrict__ kmax,
@@ -379,7 +387,7 @@ __global__ void __launch_bounds__(32 * kVLWarps, 8)
                     lmd_stats* __restrict__ stats) {
   const int lane = threadIdx.x & 31;
   const int t = blockIdx.x * kVLWarps + (threadIdx.x >> 5);
-  Acc a = {0.0, 0.0, 0.0, 0.0, 0.0, 0, 0};
+  Acc a = {0.0, 0.0, 0.0, 0.0, 0.0, 0, 0, 0};
   if (t < ntiles)
     vl_tile<P, EV, N3, U, SOA>(t, lane, n_owned, pos4, q, toff, kmax, nbr, k, a, fx, fy, fz);
   flush_acc(a, lane, t < ntiles, EV, (long long)blockIdx.x * kVLWarps + (threadIdx.x >> 5), ev,
@@ -489,8 +497,8 @@ int lmd_vl_fill(const lmd_grid* g, double rl2, int newton3, int pattern, int64_t
 int lmd_vl_build(const lmd_grid* g, double rl2, int newton3, int pattern, int64_t n_owned,
                  int32_t sentinel, const double* pos4, const int32_t* o_start,
                  const int32_t* o_count, const int32_t* h_start, const int32_t* h_count,
-                 int32_t cap_steps, int32_t* count, int64_t* tile_off, int32_t* kmax,
-                 int32_t* max_count, int32_t* nbr, void* stream) {
+                 int32_t cap_steps, int32_t* count, int32_t* count_half, int64_t* tile_off,
+                 int32_t* kmax, int32_t* max_count, int32_t* nbr, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e = cudaMemsetAsync(max_count, 0, sizeof(int32_t), s);
   if (e != cudaSuccess) return set_cuda_error(e);
@@ -502,8 +510,8 @@ int lmd_vl_build(const lmd_grid* g, double rl2, int newton3, int pattern, int64_
 #define LMD_VLB(P)                                                                             \
   vl_build_kernel<P><<<blocks, 128, 0, s>>>(make_gridk(g), (int)n_owned, (int)ntiles, newton3, \
                                             rl2, sentinel, pos4, o_start, o_count, h_start,    \
-                                            h_count, cap_steps, count, (long long*)tile_off,   \
-                                            kmax, max_count, nbr)
+                                            h_count, cap_steps, count, count_half,             \
+                                            (long long*)tile_off, kmax, max_count, nbr)
   switch (pattern) {
     case LMD_ONE_BY_V: LMD_VLB(LMD_ONE_BY_V); break;
     case LMD_V_BY_ONE: LMD_VLB(LMD_V_BY_ONE); break;
@@ -539,7 +547,7 @@ int64_t lmd_vl_ev_slots(int64_t n_owned, int pattern) {
 
 }  // extern "C"
 
-template <int P, bool EV, bool N3, int GM>
+template <int P, bool EV, int N3, int GM>
 static void launch_vl(int64_t n_owned, int64_t ntiles, const double* pos4, const SoA& q,
                       const int64_t* tile_off, const int32_t* kmax, const int32_t* nbr,
                       const LJK& k, double* fx, double* fy, double* fz, double* ev,
@@ -550,7 +558,7 @@ static void launch_vl(int64_t n_owned, int64_t ntiles, const double* pos4, const
       stats);
 }
 
-template <int P, bool EV, bool N3>
+template <int P, bool EV, int N3>
 static void launch_vl_g(int gm, int64_t n_owned, int64_t ntiles, const double* pos4,
                         const SoA& q, const int64_t* tile_off, const int32_t* kmax,
                         const int32_t* nbr, const LJK& k, double* fx, double* fy, double* fz,
@@ -570,6 +578,7 @@ int lmd_force_vl(int pattern, int newton3, int flags, const lmd_lj* lj, int64_t 
                  const int32_t* kmax, const int32_t* nbr, double* fx, double* fy, double* fz,
                  double* ev_scratch, lmd_stats* stats, void* stream) {
   if (n_owned <= 0) return LMD_OK;
+  if (newton3 < 0 || newton3 > 2) return LMD_ERR_CONFIG;
   const LJK k = make_ljk(lj);
   const int64_t ntiles = lmd_vl_num_tiles(n_owned, pattern);
   cudaStream_t s = (cudaStream_t)stream;
@@ -582,15 +591,17 @@ int lmd_force_vl(int pattern, int newton3, int flags, const lmd_lj* lj, int64_t 
 #define LMD_VLK(P, EVB, N3B)                                                                  \
   launch_vl_g<P, EVB, N3B>(gm, n_owned, ntiles, pos4, q, tile_off, kmax, nbr, k, fx, fy, fz,   \
                            ev_scratch, stats, s)
-#define LMD_VL_P(P)                         \
-  do {                                      \
-    if (ev) {                               \
-      if (newton3) LMD_VLK(P, true, true);   \
-      else LMD_VLK(P, true, false);          \
-    } else {                                \
-      if (newton3) LMD_VLK(P, false, true);  \
-      else LMD_VLK(P, false, false);         \
-    }                                       \
+#define LMD_VL_P(P)                                   \
+  do {                                                \
+    if (ev) {                                         \
+      if (newton3 == 1) LMD_VLK(P, true, 1);          \
+      else if (newton3 == 2) LMD_VLK(P, true, 2);     \
+      else LMD_VLK(P, true, 0);                       \
+    } else {                                          \
+      if (newton3 == 1) LMD_VLK(P, false, 1);         \
+      else if (newton3 == 2) LMD_VLK(P, false, 2);    \
+      else LMD_VLK(P, false, 0);                      \
+    }                                                 \
   } while (0)
   switch (pattern) {
     case LMD_ONE_BY_V: LMD_VL_P(LMD_ONE_BY_V); break;

@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(32 * kVLWarps, CiBounds<CI>::kMinBlocks)
   constexpr int U = 2;
   const int lane = threadIdx.x & 31;
   const int t = blockIdx.x * kVLWarps + (threadIdx.x >> 5);
-  Acc a = {0.0, 0.0, 0.0, 0.0, 0.0, 0, 0};
+  Acc a = {0.0, 0.0, 0.0, 0.0, 0.0, 0, 0, 0};
   if (t < ntiles) {
     const int io = Pat::ioff(lane), jo = Pat::joff(lane);
     const int c = t * Pat::A + io;

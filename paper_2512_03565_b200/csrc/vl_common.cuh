@@ -42,21 +42,22 @@ struct GridK {
 
 // ------------------------------------------------------------------ force
 // per-lane accumulators; counts are 32-bit (a lane sees at most a few
-// thousand pairs per launch) and widened once in flush_acc.  The Verlet-list
-// kernels leave pairs_owned_halo at 0 (only the cell kernels' Newton3
-// bookkeeping needs it).
+// thousand pairs per launch) and widened once in flush_acc.  `halo` (pairs
+// with an image j) is counted only where Newton3 bookkeeping needs it.
 struct Acc {
   double ax, ay, az, e, v;
-  int pairs, overlap;
+  int pairs, overlap, halo;
 };
 
 __device__ __forceinline__ void flush_acc(const Acc& a, int lane, bool live, bool ev_on,
                                           long long warp_slot, double* __restrict__ ev,
                                           lmd_stats* __restrict__ stats) {
   const long long pairs = warp_sum_ll((long long)a.pairs);
+  const long long halo = warp_sum_ll((long long)a.halo);
   const int overlap = __any_sync(0xffffffffu, a.overlap);
   if (lane == 0 && live) {
     if (pairs) atomicAdd((unsigned long long*)&stats->pair_interactions, (unsigned long long)pairs);
+    if (halo) atomicAdd((unsigned long long*)&stats->pairs_owned_halo, (unsigned long long)halo);
     if (overlap) atomicOr(&stats->overlap, 1);
   }
   if (ev_on) {

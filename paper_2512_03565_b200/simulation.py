@@ -107,7 +107,8 @@ def _finish(cont, cfg: Configuration, V: int, stats_t) -> KernelStats:
         geo = cont.vl_stats(cfg.newton3, cfg.pattern, V)
         if st.overlap:
             raise ParticleOverlapError("zero distance between interacting particles")
-        return KernelStats(geo[0], geo[1], geo[2], int(st.pair_interactions), st.epot, st.virial)
+        return KernelStats(geo[0], geo[1], geo[2], cont.pair_count(st, cfg.newton3), st.epot,
+                           st.virial)
     geo = cont.vcl_stats(cfg.newton3, cfg.pattern, V)
     return LinkedCellsContainer.finish_stats(st, cfg.newton3, *geo)
 

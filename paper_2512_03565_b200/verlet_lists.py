@@ -57,6 +57,10 @@ class VerletListContainer:
         # line-aligned entry order after each list build (0 = ascending lists);
         # measured <= 2 % faster force for +0.9 ms per build
         self.align_window = 0
+        # Newton3: "full_list" runs the full lists with the reference's Newton3
+        # pair bookkeeping (no atomics, deterministic); "half_list" runs half
+        # lists with FP64 atomics on the j side
+        self.n3_mode = "full_list"
         self._clusters_cache: dict = {}
 
     # ------------------------------------------------------------ protocol
@@ -190,12 +194,25 @@ class VerletListContainer:
 
     # ----------------------------------------------------------------- lists
     def _count(self, newton3: bool, pattern=None) -> torch.Tensor:
-        """Per-particle list lengths (written by the first list build)."""
-        c = self._counts.get(bool(newton3))
+        """Per-particle list lengths (written by the first list build); with
+        Newton3 in "full_list" mode, the half-list lengths that the full-list
+        build records alongside."""
+        key = bool(newton3)
+        c = self._counts.get(key)
         if c is None:
-            self._list(pattern or as_pattern("v_by_one"), newton3)
-            c = self._counts[bool(newton3)]
+            self._list(pattern or as_pattern("v_by_one"), self._list_n3(newton3))
+            c = self._counts[key]
         return c
+
+    def _list_n3(self, newton3: bool) -> bool:
+        """Whether the lists used for this Newton3 setting are half lists."""
+        return bool(newton3) and self.n3_mode == "half_list"
+
+    def _kernel_n3(self, newton3: bool) -> int:
+        """lmd_force_vl's newton3 mode: 0 full, 1 half + atomics, 2 full + bookkeeping."""
+        if not newton3:
+            return 0
+        return 1 if self.n3_mode == "half_list" else 2
 
     def _clusters(self, ci: int):
         """(first, len) of the i-clusters: each cell's owned particles (one
@@ -218,6 +235,7 @@ class VerletListContainer:
 
     def _ci_for(self, newton3: bool) -> int:
         return 1 if newton3 else int(self.i_cluster)
+
 
     def _capacity_guess(self, newton3: bool, ci: int = 1) -> int:
         """Entries per particle to reserve: the last build's longest list
@@ -252,6 +270,9 @@ class VerletListContainer:
         tile_off = torch.empty(max(ntiles, 1), dtype=torch.int64, device=dev)
         kmax = torch.zeros(max(ntiles, 1), dtype=torch.int32, device=dev)
         count = torch.zeros(max(n, 1), dtype=torch.int32, device=dev)
+        # a full per-particle build also records the half-list lengths
+        half = (torch.zeros(max(n, 1), dtype=torch.int32, device=dev)
+                if ci == 1 and not newton3 else None)
         mx = torch.zeros(1, dtype=torch.int32, device=dev)
         rl2 = self.params.interaction_length * self.params.interaction_length
         cap = self._capacity_guess(newton3, ci)
@@ -269,7 +290,8 @@ class VerletListContainer:
                        N.ptr(count), N.ptr(tile_off), N.ptr(kmax), N.ptr(mx), N.ptr(nbr), s)
             else:
                 N.call("lmd_vl_build", self.grid, float(rl2), int(newton3), pattern.code, n,
-                       sentinel, *tables, cap_steps, N.ptr(count), N.ptr(tile_off),
+                       sentinel, *tables, cap_steps, N.ptr(count),
+                       N.ptr(half) if half is not None else None, N.ptr(tile_off),
                        N.ptr(kmax), N.ptr(mx), N.ptr(nbr), s)
             longest = int(mx.item()) if n else 0
             if longest <= cap_steps * b_:
@@ -278,6 +300,8 @@ class VerletListContainer:
             cap = longest
         self._max_seen[(bool(newton3), ci)] = longest
         self._counts.setdefault(bool(newton3), count)
+        if half is not None and self.n3_mode == "full_list":
+            self._counts.setdefault(True, half)
         if align and units:
             N.call("lmd_vl_align", pattern.code, units, int(align), N.ptr(tile_off), N.ptr(kmax),
                    N.ptr(nbr), s)
@@ -291,11 +315,12 @@ class VerletListContainer:
         active when its entry is a real neighbour, not the sentinel pad
         (SURVEY §8f-4).  Exact by construction of the list layout."""
         pattern = as_pattern(pattern)
-        _, kmax, _, _ = self._list(pattern, newton3)
+        _, kmax, _, _ = self._list(pattern, self._list_n3(newton3), ci=self._ci_for(newton3))
         b = pattern.shape(32)[1]
         ntiles = int(N.load().lmd_vl_num_tiles(self.n_owned, pattern.code))
         steps = int((kmax[:ntiles].long() // b).sum().item())
-        active = int(self._count(newton3, pattern)[: self.n_owned].long().sum().item())
+        active = int(self._count(self._list_n3(newton3), pattern)[: self.n_owned].long()
+                     .sum().item())
         if self._ci_for(newton3) > 1:   # union lists: one entry serves a cluster
             raise ConfigurationError("lane statistics cover per-particle lists")
         return 32 * steps, active
@@ -305,10 +330,11 @@ class VerletListContainer:
         region); True if they had to be built."""
         pattern = as_pattern(pattern)
         ci = self._ci_for(newton3)
-        key = (pattern.code, bool(newton3), ci, self.align_window)
+        key = (pattern.code, self._list_n3(newton3), ci, self.align_window)
         if key in self._lists:
             return False
-        self._list(pattern, newton3)
+        self._list(pattern, self._list_n3(newton3), ci=ci)
+        self._count(newton3, pattern)
         return True
 
     def list_entries(self, pattern, newton3: bool) -> int:
@@ -347,7 +373,8 @@ class VerletListContainer:
                      ev_t=None):
         pattern = as_pattern(pattern)
         ci = self._ci_for(newton3)
-        tile_off, kmax, nbr, _ = self._list(pattern, newton3)
+        mode = self._kernel_n3(newton3)
+        tile_off, kmax, nbr, _ = self._list(pattern, self._list_n3(newton3), ci=ci)
         dev = self._pos4.device
         if stats_t is None:
             stats_t = N.new_stats(dev)
@@ -366,16 +393,26 @@ class VerletListContainer:
         if ev_t is None:
             slots = int(N.load().lmd_vl_ev_slots(self.n_owned, pattern.code))
             ev_t = torch.empty(2 * max(slots, 1), dtype=torch.float64, device=dev)
-        if newton3:
+        if mode == 1:
             self._fx.zero_()
             self._fy.zero_()
             self._fz.zero_()
-        N.call("lmd_force_vl", pattern.code, int(newton3), (N.FLAG_ENERGY if energy else 0) | self.knobs,
+        N.call("lmd_force_vl", pattern.code, mode, (N.FLAG_ENERGY if energy else 0) | self.knobs,
                N.make_lj(self.params), self.n_owned, N.ptr(self._pos4),
                N.ptr(self._soa) if self.use_soa else None, self._soa.shape[1],
                N.ptr(tile_off), N.ptr(kmax), N.ptr(nbr), N.ptr(self._fx),
                N.ptr(self._fy), N.ptr(self._fz), N.ptr(ev_t), N.ptr(stats_t), N.stream())
         return stats_t
+
+    def pair_count(self, st, newton3: bool) -> int:
+        """pair_interactions in the reference's convention from a device
+        stats record of launch_force (Newton3 on full lists: owned-owned
+        pairs were seen from both sides)."""
+        p = int(st.pair_interactions)
+        if self._kernel_n3(newton3) == 2:
+            h = int(st.pairs_owned_halo)
+            p = (p - h) // 2 + h
+        return p
 
     def vl_stats(self, newton3: bool, pattern, V: int):
         key = (self.structure_version, bool(newton3), pattern, V)
@@ -402,7 +439,7 @@ class VerletListContainer:
         if st.overlap:
             raise ParticleOverlapError("zero distance between interacting particles")
         return KernelStats(kernel_invocations=inv, lane_slots=slots, useful_interactions=useful,
-                           pair_interactions=int(st.pair_interactions), epot=st.epot,
+                           pair_interactions=self.pair_count(st, newton3), epot=st.epot,
                            virial=st.virial)
 
     def collect_forces(self, owned) -> None:

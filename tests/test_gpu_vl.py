@@ -45,8 +45,9 @@ def test_pair_sets_exact(rng, periodic):
         assert got == want
 
 
+@pytest.mark.parametrize("n3_mode", ["full_list", "half_list"])
 @pytest.mark.parametrize("pattern", list(PatternKind))
-def test_forces_stats_energy_vs_oracle(rng, pattern):
+def test_forces_stats_energy_vs_oracle(rng, pattern, n3_mode):
     pos, span = _state(rng, 4000, 0.8)
     params = LJParams(cutoff=2.5, skin=0.3)
     box = SimulationBox.cube(span, periodic=True)
@@ -55,8 +56,12 @@ def test_forces_stats_energy_vs_oracle(rng, pattern):
         for V in (8, 16):
             of, ost = O.force_phase_vl(pos, lo, hi, [True] * 3, params, n3, pattern.value, V)
             buf = ParticleBuffer.from_positions(pos, device="cuda")
-            cfg = Configuration(B.ContainerKind.VERLET_LISTS, B.TraversalKind.VL, n3, pattern)
-            st = B.force_phase(buf, box, params, cfg, V, energy=True)
+            cont = B.VerletListContainer(box, params)
+            cont.n3_mode = n3_mode
+            cont.rebuild(buf)
+            cont.refresh(buf)
+            st = cont.compute_forces("vl", n3, pattern, V, energy=True)
+            cont.collect_forces(buf)
             assert st == B.KernelStats(*ost.as_tuple()), (n3, V)
             assert forces_close(buf.forces().cpu().numpy(), of), (n3, V)
             assert abs(st.epot - ost.epot) <= 1e-12 * abs(ost.epot)
