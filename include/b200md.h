@@ -394,6 +394,10 @@ int lmd_apply_boundaries(const lmd_box* box, int64_t n, double* x, double* y, do
 
 /* integrator.py:21-48: phase 0 = pre-force (drift, stash old force, zero
  * force), 1 = post-force (kick).  *nonfinite |= 1 on non-finite state. */
+/* *out = max_k |r_k - ref_k|^2 with the reference's unfused (dx^2 + dy^2) +
+ * dz^2 (containers.py:23-38, needs_rebuild); ref_xyz rows are (x, y, z). */
+int lmd_max_displacement2(int64_t n, const double* x, const double* y, const double* z,
+                          const double* ref_xyz, double* out, void* stream);
 int lmd_verlet_step(int64_t n, int phase, double dt, double mass, double* x, double* y,
                     double* z, double* vx, double* vy, double* vz, double* fx, double* fy,
                     double* fz, double* ox, double* oy, double* oz, int32_t* nonfinite,

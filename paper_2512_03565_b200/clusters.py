@@ -17,7 +17,7 @@ import numpy as np
 import torch
 
 from . import _native as N
-from .containers import _check_all_owned, device_soa, needs_rebuild
+from .containers import _check_all_owned, device_soa, needs_rebuild_buffer
 from .domain import as_box, build_halo
 from .errors import ConfigurationError, ParticleOverlapError
 from .kernels import KernelStats, as_pattern, validate_vector_width
@@ -108,7 +108,7 @@ class VerletClusterContainer:
     # ------------------------------------------------------------ protocol
     def needs_rebuild(self, owned) -> bool:
         d = device_soa(owned)
-        return needs_rebuild(d.positions(), self.reference_positions, self.params.skin,
+        return needs_rebuild_buffer(d, self.reference_positions, self.params.skin,
                              self.steps_since_rebuild, self.rebuild_period)
 
     def _table(self, cl: _Clustered, dev):

@@ -50,6 +50,23 @@ def needs_rebuild(positions, reference_positions, skin: float, steps_since_rebui
     return bool(disp2.max() >= (0.5 * skin) ** 2)
 
 
+def needs_rebuild_buffer(buf: ParticleBuffer, reference_positions, skin: float,
+                         steps_since_rebuild: int, period: int) -> bool:
+    """needs_rebuild for a device buffer: one fused max-displacement kernel
+    and one 8-byte read instead of stacking the positions."""
+    if steps_since_rebuild >= period:
+        return True
+    n = len(buf)
+    if reference_positions is None or tuple(reference_positions.shape) != (n, 3):
+        return True
+    if n == 0:
+        return False
+    out = torch.empty(1, dtype=torch.float64, device=buf.device)
+    N.call("lmd_max_displacement2", n, N.ptr(buf.pos_x), N.ptr(buf.pos_y), N.ptr(buf.pos_z),
+           N.ptr(reference_positions), N.ptr(out), N.stream())
+    return bool(out.item() >= (0.5 * skin) ** 2)
+
+
 def max_particles_per_cell(buf: ParticleBuffer, box, cell_size: float) -> int:
     """Peak owned-particle occupancy on a reference grid (containers.py:41-53)."""
     box = as_box(box)
@@ -195,7 +212,7 @@ class LinkedCellsContainer:
     # ------------------------------------------------------------ protocol
     def needs_rebuild(self, owned) -> bool:
         d = device_soa(owned)
-        return needs_rebuild(d.positions(), self.reference_positions, self.params.skin,
+        return needs_rebuild_buffer(d, self.reference_positions, self.params.skin,
                              self.steps_since_rebuild, self.rebuild_period)
 
     def _alloc_tables(self, dev):

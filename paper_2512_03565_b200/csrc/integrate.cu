@@ -92,7 +92,42 @@ __global__ void verlet_kernel(int64_t n, int phase, double dt, double half_over_
 
 using namespace lmd;
 
+// max over particles of |r - r_ref|^2 with the reference's unfused
+// (dx^2 + dy^2) + dz^2 (containers.py:23-38); r_ref rows are (x, y, z).
+// Non-negative doubles order like their bit patterns: one 64-bit atomicMax
+// per warp on the bits.
+__global__ void max_disp2_kernel(int64_t n, const double* __restrict__ x,
+                                 const double* __restrict__ y, const double* __restrict__ z,
+                                 const double* __restrict__ ref,
+                                 unsigned long long* __restrict__ out) {
+  double m = 0.0;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const double dx = __dadd_rn(x[k], -ref[3 * k]);
+    const double dy = __dadd_rn(y[k], -ref[3 * k + 1]);
+    const double dz = __dadd_rn(z[k], -ref[3 * k + 2]);
+    const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+    m = fmax(m, d2);
+  }
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m > 0.0)
+    atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+
 extern "C" {
+
+int lmd_max_displacement2(int64_t n, const double* x, const double* y, const double* z,
+                          const double* ref_xyz, double* out, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(out, 0, sizeof(double), s);
+  if (e != cudaSuccess) return set_cuda_error(e);
+  if (n <= 0) return LMD_OK;
+  const int64_t blocks = cdiv(n, 256) < 148 * 8 ? cdiv(n, 256) : 148 * 8;
+  max_disp2_kernel<<<(unsigned)blocks, 256, 0, s>>>(n, x, y, z, ref_xyz,
+                                                    (unsigned long long*)out);
+  LMD_CHECK_LAUNCH();
+  return LMD_OK;
+}
 
 int lmd_apply_boundaries(const lmd_box* box, int64_t n, double* x, double* y, double* z,
                          double* vx, double* vy, double* vz, int32_t* diverged, void* stream) {

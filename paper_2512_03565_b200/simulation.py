@@ -149,7 +149,12 @@ def run_md(owned, box, params, iterations: int, vector_width: int = 8, *,
             raise ConfigurationError(f"invalid configuration {fixed_config.label!r}")
         tuner = None
     lane_total = [0]
-    provider = make_metric_provider(metric, lambda: lane_total[0])
+    deferred = tuner is None and metric in ("time", "iteration")
+    if deferred:   # nobody waits for the samples: resolve the events after the run
+        from .tuning import DeferredTimeMetric
+        provider = DeferredTimeMetric()
+    else:
+        provider = make_metric_provider(metric, lambda: lane_total[0])
     containers: dict = {}
     records: list = []
     per_config: dict = {}
@@ -223,7 +228,13 @@ def run_md(owned, box, params, iterations: int, vector_width: int = 8, *,
                 records.append(IterationRecord(it, phase, cfg, sample, stats.lane_slots,
                                                stats.useful_interactions, stats.blank_lanes,
                                                stats.pair_interactions, len(owned)))
-            per_config[cfg.label] = per_config.get(cfg.label, 0.0) + sample
+            if not deferred:
+                per_config[cfg.label] = per_config.get(cfg.label, 0.0) + sample
+        if deferred:
+            values = provider.resolve()
+            for rec in records:
+                rec.metric_value = values[int(rec.metric_value)]
+            per_config[fixed_config.label] = float(sum(values))
         flag = owned.extra.get("nonfinite")
         if flag is not None and int(flag.item()):
             raise SimulationDivergedError("non-finite particle state")
