@@ -151,15 +151,22 @@ __global__ void vl_build_kernel(GridK g, int n, int ntiles, int newton3,
               // bit mask and emitted afterwards in ascending order, so the
               // (warp-divergent) emit path runs once per hit, not once per
               // candidate that some lane of the warp accepted
+              // branch-free candidate loop: the backing holds no DUMMY
+              // records (owned checked at rebuild, images / ghosts tagged
+              // HALO, the sentinel is in no cell) and the self pair is
+              // cleared from the mask afterwards
               for (int j0 = j; j0 < e; j0 += 32) {
-                const int j1 = min(e, j0 + 32);
+                const int cnt = min(e - j0, 32);
                 unsigned mask = 0u;
-                for (int jj = j0; jj < j1; ++jj) {
-                  if (!view && jj == i) continue;
-                  const double4 pj = ld_pos4(pos4, jj);
-                  if (pj.w == (double)LMD_DUMMY) continue;
+#pragma unroll 2
+                for (int q = 0; q < cnt; ++q) {
+                  const double4 pj = ld_pos4(pos4, j0 + q);
                   const double r2 = r2_exact(pi.x - pj.x, pi.y - pj.y, pi.z - pj.z);
-                  if (r2 < rl2) mask |= 1u << (jj - j0);
+                  mask |= (r2 < rl2 ? 1u : 0u) << q;
+                }
+                if (!view) {
+                  const unsigned self = (unsigned)(i - j0);
+                  if (self < 32u) mask &= ~(1u << self);
                 }
                 while (mask) {
                   const int jj = j0 + __ffs(mask) - 1;
