@@ -21,7 +21,7 @@ from .containers import _check_all_owned, device_soa, needs_rebuild_buffer
 from .domain import as_box, build_halo
 from .errors import ConfigurationError, ParticleOverlapError
 from .kernels import KernelStats, as_pattern, validate_vector_width
-from .particles import DUMMY, HALO, OWNED, ParticleBuffer
+from .particles import HALO, OWNED, ParticleBuffer
 
 REBUILD_PERIOD_DEFAULT = 20
 

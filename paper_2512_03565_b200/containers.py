@@ -20,7 +20,7 @@ from . import _native as N
 from .domain import SimulationBox, as_box, build_halo
 from .errors import ConfigurationError, DegenerateDomainError
 from .kernels import KernelStats, PatternKind, as_pattern, validate_vector_width
-from .particles import DUMMY, HALO, OWNED, ParticleBuffer
+from .particles import HALO, OWNED, ParticleBuffer
 
 REBUILD_PERIOD_DEFAULT = 20
 
@@ -483,7 +483,7 @@ class LinkedCellsContainer:
                        energy: bool = False) -> KernelStats:
         """Execute one force phase over the current structure; forces are
         written into the sorted backing (collect_forces scatters them)."""
-        from .traversals import TraversalKind, traversal_code
+        from .traversals import traversal_code
         validate_vector_width(vector_width)
         pattern = as_pattern(pattern)
         code = traversal_code(traversal)

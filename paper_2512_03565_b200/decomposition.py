@@ -21,7 +21,6 @@ Migration (``migrate``) moves particles that left the brick at a rebuild.
 
 from __future__ import annotations
 
-import math
 from dataclasses import dataclass, field
 
 import numpy as np

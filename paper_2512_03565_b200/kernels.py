@@ -20,7 +20,7 @@ import torch
 
 from . import _native as N
 from .errors import ConfigurationError, ParticleOverlapError
-from .particles import DUMMY, OWNED, ParticleBuffer
+from .particles import ParticleBuffer
 
 
 class PatternKind(Enum):

@@ -18,7 +18,6 @@ from __future__ import annotations
 import time
 from dataclasses import dataclass, field
 
-import numpy as np
 import torch
 
 from . import _native as N

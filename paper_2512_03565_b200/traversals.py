@@ -215,7 +215,6 @@ def greedy_base_colors(n: int, lists) -> tuple[list, int]:
 
 def _schedule_vcl(cont, newton3: bool) -> Schedule:
     """traversals.py:244-266 on the device cluster container."""
-    from .clusters import Cluster
     lists = cont.neighbor_lists[newton3]
     links = cont.halo_links
     n = cont.n_clusters

@@ -11,7 +11,7 @@ import numpy as np
 import pytest
 import torch
 
-from conftest import P, brute_energy_virial, forces_close, golden, jittered_lattice
+from conftest import brute_energy_virial, forces_close, golden, jittered_lattice
 from oracle import oracle as O
 
 import paper_2512_03565_b200 as B

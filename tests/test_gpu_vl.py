@@ -10,7 +10,6 @@ from __future__ import annotations
 
 import numpy as np
 import pytest
-import torch
 
 from conftest import forces_close, jittered_lattice
 from oracle import oracle as O

@@ -4,7 +4,6 @@ test_kernels.py / test_tuning.py / test_acceptance.py criteria 3, 4, 6)."""
 
 from __future__ import annotations
 
-import itertools
 import math
 
 import numpy as np

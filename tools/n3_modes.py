@@ -9,7 +9,6 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 import paper_2512_03565_b200 as B  # noqa: E402
-from paper_2512_03565_b200 import _native as N  # noqa: E402
 from paper_2512_03565_b200 import workloads  # noqa: E402
 
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
