@@ -24,13 +24,14 @@ from dataclasses import dataclass
 import torch
 import torch.distributed as dist
 
+from .containers import needs_rebuild_buffer
 from .domain import SimulationBox, apply_boundaries
 from .driver import make_container
 from .errors import ConfigurationError, SimulationDivergedError
 from .integrator import POST_FORCE, PRE_FORCE, velocity_verlet_step
 from .kernels import validate_vector_width
 from .particles import HALO, ParticleBuffer
-from .tuning import Configuration, ContainerKind
+from .tuning import Configuration, ContainerKind, TimeMetric, Tuner, TuningPolicy
 
 # migrated state: x y z | vx vy vz | fx fy fz | ofx ofy ofz | id
 _STATE = ("pos_x", "pos_y", "pos_z", "vel_x", "vel_y", "vel_z", "force_x", "force_y", "force_z",
@@ -47,6 +48,7 @@ class BrickRunSummary:
     particles_local: int
     ghosts_local: int
     pairs_per_step: list
+    phase_selections: list = None
 
     @property
     def particle_steps_per_s(self) -> float:
@@ -91,57 +93,104 @@ def _allreduce(t: torch.Tensor, dec, op=dist.ReduceOp.SUM) -> torch.Tensor:
 
 
 def run_md_bricks(owned: ParticleBuffer, dec, params, iterations: int, vector_width: int = 8,
-                  *, config: Configuration, rebuild_period: int | None = None,
+                  *, config: Configuration | None = None, configurations=None,
+                  policy: TuningPolicy | None = None, rebuild_period: int | None = None,
                   record: bool = True):
     """Run ``iterations`` MD steps of this rank's particles (global
     coordinates, inside its brick or anywhere: the first rebuild migrates
-    them).  Returns (final local ParticleBuffer, BrickRunSummary)."""
+    them).  Returns (final local ParticleBuffer, BrickRunSummary).
+
+    ``config`` fixes the configuration; otherwise ``configurations`` is the
+    search space of a per-rank tuner (tuning.py:182-271) whose samples --
+    the force phase's device time, CUDA events -- are MAX-reduced over the
+    ranks before they are recorded, so every rank selects the same
+    configuration.  One container per container kind; a
+    container last rebuilt before the latest migration is rebuilt when next
+    used, and that iteration's sample is displaced."""
     validate_vector_width(vector_width)
-    if config.container not in (ContainerKind.LINKED_CELLS, ContainerKind.VERLET_LISTS):
-        raise ConfigurationError("brick MD runs the linked-cell or Verlet-list containers")
-    if not config.is_valid():
-        raise ConfigurationError(f"invalid configuration {config.label!r}")
+    if config is None:
+        if not configurations:
+            raise ConfigurationError("give a configuration or a search space")
+        space = list(configurations)
+        tuner = Tuner(space, policy or TuningPolicy(1, max(100, 2 * len(space)), "mean", "time"))
+    else:
+        space = [config]
+        tuner = None
+    for c in space:
+        if c.container not in (ContainerKind.LINKED_CELLS, ContainerKind.VERLET_LISTS):
+            raise ConfigurationError("brick MD runs the linked-cell or Verlet-list containers")
+        if not c.is_valid():
+            raise ConfigurationError(f"invalid configuration {c.label!r}")
     dev = owned.device
     gbox = SimulationBox(dec.lo, dec.hi, ("periodic",) * 3)
     kw = {} if rebuild_period is None else {"rebuild_period": rebuild_period}
-    cont = make_container(config.container, dec.local_box(), params, **kw)
-    is_vl = config.container is ContainerKind.VERLET_LISTS
-    trav = config.traversal
+    containers: dict = {}      # kind -> [container, epoch of its last rebuild]
+    epoch = 0                  # bumped by every migration
     ghosts = None
+    ref_pos = None             # owned positions at the last migration
+    since_migration = 0
     rebuilds = 0
     pairs_per_step = []
+    selections: list = []
     force_time = 0.0
     flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    metric = TimeMetric() if tuner is not None else None
     torch.cuda.synchronize(dev)
     if dec.nranks > 1:
         dist.barrier(group=dec.group)
     start = time.perf_counter()
     for it in range(iterations):
         velocity_verlet_step(owned, params, PRE_FORCE, check=False)
-        need = cont.reference_positions is None or cont.needs_rebuild(owned)
+        cfg, _phase = tuner.next_configuration(it) if tuner is not None else (config, None)
+        slot = containers.get(cfg.container)
+        if slot is None:
+            slot = containers[cfg.container] = [make_container(cfg.container, dec.local_box(),
+                                                               params, **kw), -1]
+        cont = slot[0]
+        # the ghost layer was planned at the last migration: its validity
+        # (displacement < skin/2, the period) is measured from there, not from
+        # a container's own later rebuild
+        period = rebuild_period or cont.rebuild_period
+        need = ghosts is None or needs_rebuild_buffer(owned, ref_pos, params.skin,
+                                                      since_migration, period)
         flag.fill_(1 if need else 0)
         need = bool(_allreduce(flag, dec, dist.ReduceOp.MAX).item())
+        displaced = False
         if need:
             apply_boundaries(owned, gbox)
             bad = owned.extra.get("nonfinite")
             if bad is not None and int(bad.item()):
                 raise SimulationDivergedError("non-finite particle state in the brick run")
             owned = _unpack(dec.migrate(_pack(owned)), dev)
-            ghosts = _ghost_buffer(dec.plan(_positions(owned)), dev)
-            cont.rebuild(owned, ghosts)
-            cont.refresh(owned, ghosts)
+            ref_pos = _positions(owned)
+            ghosts = _ghost_buffer(dec.plan(ref_pos), dev)
+            since_migration = 0
+            epoch += 1
             rebuilds += 1
         else:
             g = dec.exchange(_positions(owned))
             ghosts.pos_x.copy_(g[:, 0])
             ghosts.pos_y.copy_(g[:, 1])
             ghosts.pos_z.copy_(g[:, 2])
-            cont.refresh(owned, ghosts)
+        if slot[1] != epoch:
+            cont.rebuild(owned, ghosts)
+            slot[1] = epoch
+            displaced = True
+        cont.refresh(owned, ghosts)
         cont.steps_since_rebuild += 1
-        if is_vl:
-            cont.ensure_lists(config.pattern, config.newton3)
+        since_migration += 1
+        if cfg.container is ContainerKind.VERLET_LISTS:
+            displaced |= cont.ensure_lists(cfg.pattern, cfg.newton3)
         t0 = time.perf_counter()
-        st = cont.compute_forces(trav, config.newton3, config.pattern, vector_width)
+        if metric is not None:
+            metric.begin_region()
+        st = cont.compute_forces(cfg.traversal, cfg.newton3, cfg.pattern, vector_width)
+        if metric is not None:
+            sample = torch.tensor([metric.end_region()], dtype=torch.float64, device=dev)
+            sample = float(_allreduce(sample, dec, dist.ReduceOp.MAX).item())
+            d = torch.tensor([1 if displaced else 0], dtype=torch.int32, device=dev)
+            displaced = bool(_allreduce(d, dec, dist.ReduceOp.MAX).item())
+            tuner.record_sample(sample, displaced=displaced)
         force_time += time.perf_counter() - t0
         cont.collect_forces(owned)
         velocity_verlet_step(owned, params, POST_FORCE, check=False)
@@ -158,6 +207,9 @@ def run_md_bricks(owned: ParticleBuffer, dec, params, iterations: int, vector_wi
     nonfinite = owned.extra.get("nonfinite")
     if nonfinite is not None and int(nonfinite.item()):
         raise SimulationDivergedError("non-finite particle state in the brick run")
+    if tuner is not None:
+        selections = [c.label for c in tuner.phase_selection]
     summary = BrickRunSummary(iterations, wall, force_time, rebuilds, n_global, n_local,
-                              len(ghosts) if ghosts is not None else 0, pairs_per_step)
+                              len(ghosts) if ghosts is not None else 0, pairs_per_step,
+                              selections)
     return owned, summary

@@ -52,3 +52,16 @@ def test_brick_md_two_ranks_matches_single_domain():
     assert d["rebuilds"] >= 3 and d["ids_complete"]
     assert d["single_pairs_equal"]
     assert d["max_position_diff"] < 1e-10
+
+
+def test_brick_md_tuner_ranks_agree():
+    """Per-rank tuners with MAX-reduced samples select the same
+    configurations on every rank."""
+    env = dict(os.environ, LMD_DIST_BACKEND="gloo", LMD_DEVICE="0")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29563", "tools/md_bricks_check.py",
+           "--particles", "60000", "--steps", "50", "--tune", "1"]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert d["selections_agree"] and len(d["phase_selections"]) >= 1

@@ -29,6 +29,8 @@ def main():
     ap.add_argument("--rho", type=float, default=0.8)
     ap.add_argument("--steps", type=int, default=25)
     ap.add_argument("--single", type=int, default=1, help="also run the single-domain check")
+    ap.add_argument("--tune", type=int, default=0,
+                    help="tune over VL / LC x two orders instead of --config (no single check)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -61,19 +63,33 @@ def main():
               "force_z", "old_force_x", "old_force_y", "old_force_z"):
         getattr(local_buf, f).copy_(getattr(full, f)[idx])
     local_buf.id.copy_(full.id[idx])
-    owned, summ = B.run_md_bricks(local_buf, dec, params, args.steps, 8, config=cfg,
-                                  rebuild_period=10 if skin else None)
+    if args.tune:
+        space = [B.Configuration.parse(x) for x in ("vl,vl,false,v_by_one", "vl,vl,false,half_by_two",
+                                                    "lc,lc_c01,false,v_by_one",
+                                                    "lc,lc_c18,true,half_by_two")]
+        owned, summ = B.run_md_bricks(local_buf, dec, B.LJParams(cutoff=2.5, skin=0.3, dt=0.001),
+                                      args.steps, 8, configurations=space,
+                                      policy=B.TuningPolicy(2, 40, "mean", "time"))
+        args.single = 0
+    else:
+        owned, summ = B.run_md_bricks(local_buf, dec, params, args.steps, 8, config=cfg,
+                                      rebuild_period=10 if skin else None)
     mine_rows = torch.cat([owned.id.to(torch.float64)[:, None], owned.positions()], 1).cpu()
     gathered = [None] * world
+    sels = [None] * world
     if world > 1:
         dist.all_gather_object(gathered, mine_rows)
+        dist.all_gather_object(sels, summ.phase_selections)
     else:
         gathered = [mine_rows]
+        sels = [summ.phase_selections]
     if rank == 0:
         out = {"config": args.config, "ranks": world, "grid": list(dec.grid),
                "particles": summ.particles_global, "steps": args.steps,
                "rebuilds": summ.rebuilds, "particle_steps_per_s": summ.particle_steps_per_s,
-               "pairs_per_step": summ.pairs_per_step[:5] + ["..."] + summ.pairs_per_step[-2:]}
+               "pairs_per_step": summ.pairs_per_step[:5] + ["..."] + summ.pairs_per_step[-2:],
+               "phase_selections": summ.phase_selections,
+               "selections_agree": all(x == sels[0] for x in sels)}
         if args.single:
             t0 = time.perf_counter()
             recs, _ = B.run_md(full, box, params, args.steps, 8, fixed_config=cfg,
