@@ -61,6 +61,8 @@ def needs_rebuild_buffer(buf: ParticleBuffer, reference_positions, skin: float,
         return True
     if n == 0:
         return False
+    if skin <= 0.0:            # any displacement >= 0: no need to look
+        return True
     out = torch.empty(1, dtype=torch.float64, device=buf.device)
     N.call("lmd_max_displacement2", n, N.ptr(buf.pos_x), N.ptr(buf.pos_y), N.ptr(buf.pos_z),
            N.ptr(reference_positions), N.ptr(out), N.stream())
