@@ -143,28 +143,43 @@ __global__ void __launch_bounds__(128)
       const long long nl = lin + dx + t0 * (dy + t1 * dz);
       const int js = cstart[nl], jn = ccount[nl];
       const double fm = (dup && nl != lin) ? 1.0 + (double)dup[nl < lin ? nl : lin] : 1.0;
-      for (int j = js; j < js + jn; ++j) {
-        if (j == i) continue;
-        const double4 pj = ld_pos4(pos4, j);
-        if (pj.w == (double)LMD_DUMMY) continue;
-        const double ddx = pi.x - pj.x, ddy = pi.y - pj.y, ddz = pi.z - pj.z;
-        const double r2 = r2_exact(ddx, ddy, ddz);
-        if (r2 >= k.rc2) continue;
-        if (r2 == 0.0) {
-          overlap = 1;
-          continue;
+      const int m = fm > 1.5 ? 2 : 1;
+      // (1) branch-free cutoff tests of up to 32 candidates into a hit mask
+      //     (the backing holds no DUMMY records: owned checked at rebuild,
+      //     images tagged HALO); (2) LJ for the set bits only, in ascending
+      //     j -- the same pairs in the same order as the one-pass loop
+      for (int j0 = js; j0 < js + jn; j0 += 32) {
+        const int cnt = min(js + jn - j0, 32);
+        unsigned mask = 0u;
+#pragma unroll 2
+        for (int q = 0; q < cnt; ++q) {
+          const double4 pj = ld_pos4(pos4, j0 + q);
+          const double r2 = r2_exact(pi.x - pj.x, pi.y - pj.y, pi.z - pj.z);
+          mask |= (r2 < k.rc2 ? 1u : 0u) << q;
         }
-        double s6;
-        const double f = lj_scalar(r2, k, s6) * fm;
-        ax = fma(f, ddx, ax);
-        ay = fma(f, ddy, ay);
-        az = fma(f, ddz, az);
-        const int m = fm > 1.5 ? 2 : 1;
-        pairs += m;
-        if (pj.w != (double)LMD_OWNED) pairs_halo += m;
-        if (EV) {
-          e_acc = fma((0.5 * fm) * s6, fma(k.eps4, s6, -k.eps4), e_acc);
-          v_acc = fma(0.5 * f, r2, v_acc);
+        const unsigned self = (unsigned)(i - j0);
+        if (self < 32u) mask &= ~(1u << self);
+        while (mask) {
+          const int j = j0 + __ffs(mask) - 1;
+          mask &= mask - 1u;
+          const double4 pj = ld_pos4(pos4, j);
+          const double ddx = pi.x - pj.x, ddy = pi.y - pj.y, ddz = pi.z - pj.z;
+          const double r2 = r2_exact(ddx, ddy, ddz);
+          if (r2 == 0.0) {
+            overlap = 1;
+            continue;
+          }
+          double s6;
+          const double f = lj_scalar(r2, k, s6) * fm;
+          ax = fma(f, ddx, ax);
+          ay = fma(f, ddy, ay);
+          az = fma(f, ddz, az);
+          pairs += m;
+          if (pj.w != (double)LMD_OWNED) pairs_halo += m;
+          if (EV) {
+            e_acc = fma((0.5 * fm) * s6, fma(k.eps4, s6, -k.eps4), e_acc);
+            v_acc = fma(0.5 * f, r2, v_acc);
+          }
         }
       }
     }
