@@ -239,24 +239,29 @@ __global__ void vcl_pairs_kernel(int ncl, const int32_t* __restrict__ ckey,
 }
 
 // ------------------------------------------------------------------ force
-// warp per owned cluster; MP = M rounded to a power of two <= 32; lanes =
-// (i slot il = lane % MP) x (j lane jl = lane / MP), JL = 32 / MP j slots per fill
+// Warp per owned cluster, stream mapping: lane (il, g) = (lane % MP, lane / MP)
+// (MP = M rounded up to a power of two <= 32) holds i slot il of the
+// cluster; the G = 32 / MP lane groups take the cluster's units (self, list
+// entries, halo links) round-robin, and each lane tests its i against all
+// M slots of its unit branch-free into a hit mask, then evaluates LJ for the
+// set bits only.  With ~10 % of cluster-pair tests inside rc, the LJ path runs
+// a few times per unit instead of on nearly every fill.  Same pairs; each
+// lane's summation order is fixed by the list, so results are deterministic.
 template <int MP, bool EV>
 __global__ void __launch_bounds__(128)
-    vcl_force_kernel(int ncl, int M, const double* __restrict__ pos4,
-                     const long long* __restrict__ off, const int32_t* __restrict__ nlist,
-                     const int32_t* __restrict__ list, const long long* __restrict__ hoff,
-                     const int32_t* __restrict__ hnlist, const int32_t* __restrict__ hlist,
-                     LJK k, double* __restrict__ fx,
-                     double* __restrict__ fy, double* __restrict__ fz, double* __restrict__ ev,
-                     lmd_stats* __restrict__ stats) {
-  constexpr int JL = 32 / MP;
+    vcl_stream_kernel(int ncl, int M, const double* __restrict__ pos4,
+                      const long long* __restrict__ off, const int32_t* __restrict__ nlist,
+                      const int32_t* __restrict__ list, const long long* __restrict__ hoff,
+                      const int32_t* __restrict__ hnlist, const int32_t* __restrict__ hlist,
+                      LJK k, double* __restrict__ fx, double* __restrict__ fy,
+                      double* __restrict__ fz, double* __restrict__ ev,
+                      lmd_stats* __restrict__ stats) {
+  constexpr int G = 32 / MP;
   const int lane = threadIdx.x & 31;
   const long long warp = (long long)blockIdx.x * 4 + (threadIdx.x >> 5);
-  long long pairs = 0, pairs_halo = 0;
-  int overlap = 0;
+  int pairs = 0, pairs_halo = 0, overlap = 0;
   double e_acc = 0.0, v_acc = 0.0;
-  const int il = lane % MP, jl = lane / MP;
+  const int il = lane % MP, g = lane / MP;
   if (warp < ncl) {
     const int a = (int)warp;
     const long long n_owned_slots = (long long)ncl * M;
@@ -264,6 +269,7 @@ __global__ void __launch_bounds__(128)
     const int nhl = hnlist ? hnlist[a] : 0;
     const int32_t* lst = list + off[a];
     const int32_t* hlst = hlist ? hlist + hoff[a] : nullptr;
+    const int units = 1 + nl + nhl;
     for (int ci = 0; ci < M; ci += MP) {
       const int islot = ci + il;
       const bool ilive = islot < M;
@@ -271,58 +277,69 @@ __global__ void __launch_bounds__(128)
       const double4 pi = ld_pos4(pos4, gi);
       const bool iown = ilive && pi.w == (double)LMD_OWNED;
       double ax = 0.0, ay = 0.0, az = 0.0;
-      for (int u = -1; u < nl + nhl; ++u) {
-        // self unit first, then the owned list, then the halo links
-        const int b = u < 0 ? a : (u < nl ? lst[u] : ncl + hlst[u - nl]);
+      for (int u0 = 0; u0 < units; u0 += G) {
+        const int u = u0 + g;
+        const bool live = iown && u < units;
+        const int b = !live ? a : (u == 0 ? a : (u <= nl ? lst[u - 1] : ncl + hlst[u - 1 - nl]));
         const long long base = (long long)b * M;
-        for (int cj = 0; cj < M; cj += JL) {
-          const int jslot = cj + jl;
-          if (!iown || jslot >= M) continue;
-          const long long gj = base + jslot;
-          if (gj == gi) continue;
-          const double4 pj = ld_pos4(pos4, gj);
-          if (pj.w == (double)LMD_DUMMY) continue;
-          const double dx = pi.x - pj.x, dy = pi.y - pj.y, dz = pi.z - pj.z;
-          double r2;
-          if (!within_cutoff(dx, dy, dz, k, r2)) continue;
-          if (r2 == 0.0) {
-            overlap = 1;
-            continue;
+        for (int c0 = 0; c0 < M; c0 += 32) {
+          const int cnt = min(M - c0, 32);
+          unsigned mask = 0u;
+#pragma unroll 4
+          for (int q = 0; q < cnt; ++q) {
+            const double4 pj = ld_pos4(pos4, base + c0 + q);
+            const double r2 = r2_exact(pi.x - pj.x, pi.y - pj.y, pi.z - pj.z);
+            const bool hit = pj.w != (double)LMD_DUMMY && r2 < k.rc2;
+            mask |= (hit ? 1u : 0u) << q;
           }
-          double s6;
-          const double f = lj_scalar(r2, k, s6);
-          ax = fma(f, dx, ax);
-          ay = fma(f, dy, ay);
-          az = fma(f, dz, az);
-          ++pairs;
-          pairs_halo += gj >= n_owned_slots;
-          if (EV) {
-            e_acc = fma(0.5 * s6, fma(k.eps4, s6, -k.eps4), e_acc);
-            v_acc = fma(0.5 * f, r2, v_acc);
+          if (!live) mask = 0u;
+          if (b == a) {   // self unit: not with itself
+            const unsigned self = (unsigned)(gi - base - c0);
+            if (self < 32u) mask &= ~(1u << self);
+          }
+          while (mask) {
+            const long long gj = base + c0 + __ffs(mask) - 1;
+            mask &= mask - 1u;
+            const double4 pj = ld_pos4(pos4, gj);
+            const double dx = pi.x - pj.x, dy = pi.y - pj.y, dz = pi.z - pj.z;
+            const double r2 = r2_exact(dx, dy, dz);
+            if (r2 == 0.0) {
+              overlap = 1;
+              continue;
+            }
+            double s6;
+            const double f = lj_scalar(r2, k, s6);
+            ax = fma(f, dx, ax);
+            ay = fma(f, dy, ay);
+            az = fma(f, dz, az);
+            ++pairs;
+            pairs_halo += gj >= n_owned_slots;
+            if (EV) {
+              e_acc = fma(0.5 * s6, fma(k.eps4, s6, -k.eps4), e_acc);
+              v_acc = fma(0.5 * f, r2, v_acc);
+            }
           }
         }
       }
-      // reduce over the j lanes (lanes with the same il)
 #pragma unroll
       for (int o = MP; o < 32; o <<= 1) {
         ax += __shfl_xor_sync(0xffffffffu, ax, o);
         ay += __shfl_xor_sync(0xffffffffu, ay, o);
         az += __shfl_xor_sync(0xffffffffu, az, o);
       }
-      if (jl == 0 && ilive) {
+      if (g == 0 && ilive) {
         fx[gi] = ax;
         fy[gi] = ay;
         fz[gi] = az;
       }
     }
   }
-  pairs = warp_sum_ll(pairs);
-  pairs_halo = warp_sum_ll(pairs_halo);
+  const long long pr = warp_sum_ll((long long)pairs);
+  const long long ph = warp_sum_ll((long long)pairs_halo);
   overlap = __any_sync(0xffffffffu, overlap);
   if (lane == 0 && warp < ncl) {
-    if (pairs) atomicAdd((unsigned long long*)&stats->pair_interactions, (unsigned long long)pairs);
-    if (pairs_halo)
-      atomicAdd((unsigned long long*)&stats->pairs_owned_halo, (unsigned long long)pairs_halo);
+    if (pr) atomicAdd((unsigned long long*)&stats->pair_interactions, (unsigned long long)pr);
+    if (ph) atomicAdd((unsigned long long*)&stats->pairs_owned_halo, (unsigned long long)ph);
     if (overlap) atomicOr(&stats->overlap, 1);
   }
   if (EV) {
@@ -581,11 +598,11 @@ int lmd_force_vcl(int64_t ncl, int M, int flags, const lmd_lj* lj, const double*
 #define LMD_VCLK(MPV)                                                                         \
   do {                                                                                        \
     if (ev)                                                                                   \
-      vcl_force_kernel<MPV, true><<<blocks, 128, 0, s>>>(                                     \
+      vcl_stream_kernel<MPV, true><<<blocks, 128, 0, s>>>(                                    \
           (int)ncl, M, pos4, (const long long*)off, nlist, list, (const long long*)hoff,      \
           hnlist, hlist, k, fx, fy, fz, ev_scratch, stats);                                   \
     else                                                                                      \
-      vcl_force_kernel<MPV, false><<<blocks, 128, 0, s>>>(                                    \
+      vcl_stream_kernel<MPV, false><<<blocks, 128, 0, s>>>(                                   \
           (int)ncl, M, pos4, (const long long*)off, nlist, list, (const long long*)hoff,      \
           hnlist, hlist, k, fx, fy, fz, ev_scratch, stats);                                   \
   } while (0)
