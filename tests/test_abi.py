@@ -77,3 +77,37 @@ def test_no_cpu_fallback_for_device_entry_points():
     from paper_2512_03565_b200.errors import NativeLibraryError
     with pytest.raises(NativeLibraryError):
         N.ptr(torch.zeros(3))
+
+
+def test_force_phase_refuses_to_run_without_a_device():
+    """The public entry point has no CPU fallback: without a CUDA device it
+    raises instead of computing anything on the host."""
+    import torch
+
+    import paper_2512_03565_b200 as B
+    from paper_2512_03565_b200.errors import NativeLibraryError
+    if torch.cuda.is_available():
+        pytest.skip("host-only check")
+
+    class Host:
+        pass
+
+    h = Host()
+    pos = np.random.default_rng(0).uniform(0, 10, (50, 3))
+    for k, v in zip(("pos_x", "pos_y", "pos_z"), pos.T):
+        setattr(h, k, np.ascontiguousarray(v))
+    for k in ("force_x", "force_y", "force_z"):
+        setattr(h, k, np.zeros(50))
+    h.ownership = np.zeros(50, dtype=np.int8)
+    with pytest.raises(NativeLibraryError):
+        B.force_phase(h, B.SimulationBox.cube(10.0), B.LJParams(cutoff=2.5, skin=0.3),
+                      B.Configuration.parse("vl,vl,false,v_by_one"), 8)
+
+
+def test_missing_library_is_an_error(monkeypatch, tmp_path):
+    """A missing libb200md.so raises NativeLibraryError (no silent fallback)."""
+    from paper_2512_03565_b200.errors import NativeLibraryError
+    monkeypatch.setattr(N, "_lib", None)
+    monkeypatch.setattr(N, "lib_path", lambda: str(tmp_path / "absent.so"))
+    with pytest.raises(NativeLibraryError):
+        N.load()
