@@ -156,7 +156,7 @@ class Phase:
         elif self.kind == "lc":
             slots = max(int(N.load().lmd_lc_ev_slots(cont.grid)),
                         int(N.load().lmd_lc_n3_ev_slots(cont.grid)),
-                        int(N.load().lmd_lc_tpi_ev_slots(cont.n_owned)))
+                        int(N.load().lmd_lc_tpi_ev_slots(cont.n_owned, cfg.pattern.code)))
         else:
             slots = int(N.load().lmd_vcl_ev_slots(cont.n_clusters))
         self.ev_t = torch.empty(2 * max(slots, 1), dtype=torch.float64, device=dev)

@@ -205,15 +205,17 @@ int lmd_force_lc_n3(const lmd_grid* g, const lmd_lj* lj, int traversal, int patt
  * executor.py:38-69, 165-171) for lc_c01 / lc_c08 / lc_c18: kernel
  * invocations, lane slots and useful interactions for shape (a, b) and
  * width V, from per-cell owned/halo counts.  Adds into *stats. */
-/* Same sweep as lmd_force_lc, thread per owned particle (the V_BY_ONE order
- * as thread-per-i over consecutive cell-sorted particles; csrc/force_lc.cu
- * lc_tpi_kernel).  cell_of[i] = the rebuild-time cell of backing particle i.
- * ev_scratch: 2 * lmd_lc_tpi_ev_slots(n_owned) doubles. */
-int64_t lmd_lc_tpi_ev_slots(int64_t n_owned);
-int lmd_force_lc_particles(const lmd_grid* g, const lmd_lj* lj, int flags, const double* pos4,
-                           int64_t n_owned, const int32_t* cell_of, const int32_t* cell_start,
-                           const int32_t* cell_count, const uint8_t* dup, double* fx, double* fy,
-                           double* fz, double* ev_scratch, lmd_stats* stats, void* stream);
+/* Same sweep as lmd_force_lc, thread per particle for every interaction
+ * order (a, b): a warp holds a consecutive cell-sorted particles, b lanes per
+ * particle split its candidate stream (csrc/force_lc.cu lc_tpi_kernel).
+ * cell_of[i] = the rebuild-time cell of backing particle i.  ev_scratch:
+ * 2 * lmd_lc_tpi_ev_slots(n_owned, pattern) doubles. */
+int64_t lmd_lc_tpi_ev_slots(int64_t n_owned, int pattern);
+int lmd_force_lc_particles(const lmd_grid* g, const lmd_lj* lj, int pattern, int flags,
+                           const double* pos4, int64_t n_owned, const int32_t* cell_of,
+                           const int32_t* cell_start, const int32_t* cell_count,
+                           const uint8_t* dup, double* fx, double* fy, double* fz,
+                           double* ev_scratch, lmd_stats* stats, void* stream);
 int lmd_lc_stats(const lmd_grid* g, int traversal, int newton3, int a, int b, int vector_width,
                  const int32_t* o_count, const int32_t* h_count, lmd_stats* stats,
                  void* stream);

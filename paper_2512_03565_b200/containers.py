@@ -182,7 +182,11 @@ class LinkedCellsContainer:
         # measured 2-3.5x faster at 1M particles and 6-20x at 8,000
         # (tools/n3_modes.py).
         self.n3_mode = "full_shell"
-        # V_BY_ONE as thread-per-i over consecutive particles (lmd_force_lc_particles)
+        # thread per particle over consecutive cell-sorted particles
+        # (lmd_force_lc_particles) for the orders with a >= 16 distinct i per
+        # fill -- N x 1: 1.83 -> 0.78 ms, N/2 x 2: 1.08 -> 0.89 ms at 1M; the
+        # 1 x N and 2 x N/2 orders stay warp per cell (lmd_force_lc), where a
+        # warp per one or two particles is 2x slower.  False: warp per cell
         self.thread_per_particle = True
         self._max_cell = 1
 
@@ -401,6 +405,9 @@ class LinkedCellsContainer:
         self._stats_cache[key] = hit
         return hit
 
+    def _uses_tpi(self, pattern) -> bool:
+        return bool(self.thread_per_particle) and pattern.shape(32)[0] >= 16
+
     def gpu_lane_stats(self, pattern, traversal=N.LC_C01, newton3: bool = False):
         """Physical lane use of the kernel that executes this configuration
         (the GPU analogue of the reference's lane statistics):
@@ -408,24 +415,25 @@ class LinkedCellsContainer:
         lanes of those steps holding a real (i, j) candidate.  Exact by
         construction: warp per cell sweeps ceil(nC/A) x ceil(nD/B) fills per
         occupied (C, D) at width 32 -- the reference's c01 formula at V = 32;
-        thread per particle runs, per warp of 32 consecutive particles and
-        per neighbour offset, as many steps as the lane with the largest
-        neighbour cell.  Colored Newton3 passes are not covered."""
+        thread per particle runs, per warp of a consecutive particles and per
+        neighbour offset, ceil(n/b) steps for the largest neighbour cell n of
+        those particles.  Colored Newton3 passes are not covered."""
         pattern = as_pattern(pattern)
         if self.uses_colored_n3(traversal, newton3):
             raise ConfigurationError("lane statistics cover the full-shell kernels")
         _, _, useful = self._lc_stats(N.LC_C01, False, pattern, 32)
-        if self.thread_per_particle and pattern is PatternKind.V_BY_ONE:
+        if self._uses_tpi(pattern):
             n = self.n_owned
+            a, b = pattern.shape(32)
             t0, t1 = int(self.total_dims[0]), int(self.total_dims[1])
             offs = torch.tensor([(d // 9 - 1) + t0 * ((d // 3) % 3 - 1 + t1 * (d % 3 - 1))
                                  for d in range(27)], dtype=torch.int64, device=self._pos4.device)
             cells = self._cell_of.long()
-            pad = (-n) % 32
-            per = self._count.long()[cells[:, None] + offs[None, :]]          # (n, 27)
+            pad = (-n) % a
+            per = (self._count.long()[cells[:, None] + offs[None, :]] + b - 1) // b  # (n, 27)
             if pad:
                 per = torch.cat([per, torch.zeros((pad, 27), dtype=per.dtype, device=per.device)])
-            steps = int(per.view(-1, 32, 27).amax(dim=1).sum().item())
+            steps = int(per.view(-1, a, 27).amax(dim=1).sum().item())
             return 32 * steps, useful
         _, slots, _ = self._lc_stats(N.LC_C01, False, pattern, 32)
         return slots, useful
@@ -462,11 +470,11 @@ class LinkedCellsContainer:
                    N.ptr(self._fy), N.ptr(self._fz), N.ptr(ev_t), N.ptr(stats_t), N.stream())
             return stats_t
         dup = None if traversal == N.LC_C01 else N.ptr(self._dup)
-        if self.thread_per_particle and pattern is PatternKind.V_BY_ONE:
-            slots = int(N.load().lmd_lc_tpi_ev_slots(self.n_owned))
+        if self._uses_tpi(pattern):
+            slots = int(N.load().lmd_lc_tpi_ev_slots(self.n_owned, pattern.code))
             if ev_t is None or ev_t.numel() < 2 * slots:
                 ev_t = torch.empty(2 * max(slots, 1), dtype=torch.float64, device=dev)
-            N.call("lmd_force_lc_particles", self.grid, N.make_lj(self.params),
+            N.call("lmd_force_lc_particles", self.grid, N.make_lj(self.params), pattern.code,
                    N.FLAG_ENERGY if energy else 0, N.ptr(self._pos4), self.n_owned,
                    N.ptr(self._cell_of), N.ptr(self._start), N.ptr(self._count), dup,
                    N.ptr(self._fx), N.ptr(self._fy), N.ptr(self._fz), N.ptr(ev_t),

@@ -115,52 +115,61 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
   }
 }
 
-// Thread per owned particle (the V_BY_ONE order as "thread-per-i"): lane i
-// of a warp is the i-th particle of the cell-sorted backing, so a warp's 32
-// i are consecutive particles spanning ~2-3 cells instead of one cell's ~12
-// (warp-per-cell leaves most of 32 i lanes empty at cell size rc).  Each
-// lane sweeps its rebuild-time cell's 27-cell shell in the same unit order,
-// with the same per-pair arithmetic and unit multiplicity as lc_force_kernel;
-// lanes of one cell read the same j (broadcast loads).
-template <bool EV>
+// Thread per particle for every interaction order (a, b) = (A, B): a warp
+// holds A consecutive particles of the cell-sorted backing (spanning cells,
+// instead of one cell's ~12 particles in 32 i lanes) and B lanes per
+// particle split its candidate stream -- lane (io, jo) takes, in each of the
+// 27 neighbour cells, the candidates jo, jo + B, ... (N x 1 = one lane per
+// particle, 1 x N = one warp per particle).  Each lane tests its candidates
+// branch-free into a hit mask (the backing holds no DUMMY records: owned
+// checked at rebuild, images tagged HALO) and evaluates LJ for the set bits
+// only; the B partial forces are reduced with shuffles.  Same unit order,
+// per-pair arithmetic and unit multiplicity as lc_force_kernel.
+template <int P, bool EV>
 __global__ void __launch_bounds__(128)
     lc_tpi_kernel(int n_owned, long long t0, long long t1, LJK k, const double* __restrict__ pos4,
                   const int32_t* __restrict__ cell_of, const int32_t* __restrict__ cstart,
                   const int32_t* __restrict__ ccount, const uint8_t* __restrict__ dup,
                   double* __restrict__ fx, double* __restrict__ fy, double* __restrict__ fz,
                   double* __restrict__ ev, lmd_stats* __restrict__ stats) {
+  using Pat = Pattern<P>;
+  constexpr int A = Pat::A, B = Pat::B;
   const int lane = threadIdx.x & 31;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const long long warp = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int io = Pat::ioff(lane), jo = Pat::joff(lane);
+  const long long il = warp * A + io;
+  const bool iact = il < n_owned;
+  const int i = iact ? (int)il : 0;
   double e_acc = 0.0, v_acc = 0.0;
   int pairs = 0, pairs_halo = 0, overlap = 0;
-  if (i < n_owned) {
+  double ax = 0.0, ay = 0.0, az = 0.0;
+  if (warp * A < n_owned) {
     const long long lin = cell_of[i];
     const double4 pi = ld_pos4(pos4, i);
-    double ax = 0.0, ay = 0.0, az = 0.0;
     for (int d = 0; d < 27; ++d) {
       const int dx = d / 9 - 1, dy = (d / 3) % 3 - 1, dz = d % 3 - 1;
       const long long nl = lin + dx + t0 * (dy + t1 * dz);
       const int js = cstart[nl], jn = ccount[nl];
       const double fm = (dup && nl != lin) ? 1.0 + (double)dup[nl < lin ? nl : lin] : 1.0;
       const int m = fm > 1.5 ? 2 : 1;
-      // (1) branch-free cutoff tests of up to 32 candidates into a hit mask
-      //     (the backing holds no DUMMY records: owned checked at rebuild,
-      //     images tagged HALO); (2) LJ for the set bits only, in ascending
-      //     j -- the same pairs in the same order as the one-pass loop
-      for (int j0 = js; j0 < js + jn; j0 += 32) {
-        const int cnt = min(js + jn - j0, 32);
+      const int nq = (iact && jn > jo) ? (jn - jo + B - 1) / B : 0;
+      const int jb = js + jo;
+      for (int q0 = 0; q0 < nq; q0 += 32) {
+        const int cnt = min(nq - q0, 32);
         unsigned mask = 0u;
 #pragma unroll 2
         for (int q = 0; q < cnt; ++q) {
-          const double4 pj = ld_pos4(pos4, j0 + q);
+          const double4 pj = ld_pos4(pos4, jb + B * (q0 + q));
           const double r2 = r2_exact(pi.x - pj.x, pi.y - pj.y, pi.z - pj.z);
           mask |= (r2 < k.rc2 ? 1u : 0u) << q;
         }
-        const unsigned self = (unsigned)(i - j0);
-        if (self < 32u) mask &= ~(1u << self);
+        const int rel = i - jb;                       // the self pair, if on this stream
+        if (rel >= 0 && rel % B == 0) {
+          const unsigned self = (unsigned)(rel / B - q0);
+          if (self < 32u) mask &= ~(1u << self);
+        }
         while (mask) {
-          const int j = j0 + __ffs(mask) - 1;
+          const int j = jb + B * (q0 + __ffs(mask) - 1);
           mask &= mask - 1u;
           const double4 pj = ld_pos4(pos4, j);
           const double ddx = pi.x - pj.x, ddy = pi.y - pj.y, ddz = pi.z - pj.z;
@@ -183,6 +192,11 @@ __global__ void __launch_bounds__(128)
         }
       }
     }
+  }
+  ax = reduce_j<P>(ax);
+  ay = reduce_j<P>(ay);
+  az = reduce_j<P>(az);
+  if (iact && jo == 0) {
     fx[i] = ax;
     fy[i] = ay;
     fz[i] = az;
@@ -354,28 +368,48 @@ int lmd_force_lc(const lmd_grid* g, const lmd_lj* lj, int pattern, int flags,
   return LMD_OK;
 }
 
-int64_t lmd_lc_tpi_ev_slots(int64_t n_owned) { return cdiv(n_owned, 128) * 4; }
+static inline int order_A(int p) {
+  return p == LMD_ONE_BY_V ? 1 : p == LMD_V_BY_ONE ? 32 : p == LMD_TWO_BY_HALF ? 2 : 16;
+}
 
-int lmd_force_lc_particles(const lmd_grid* g, const lmd_lj* lj, int flags, const double* pos4,
-                           int64_t n_owned, const int32_t* cell_of, const int32_t* cell_start,
-                           const int32_t* cell_count, const uint8_t* dup, double* fx, double* fy,
-                           double* fz, double* ev_scratch, lmd_stats* stats, void* stream) {
+int64_t lmd_lc_tpi_ev_slots(int64_t n_owned, int pattern) {
+  return cdiv(cdiv(n_owned, order_A(pattern)), 4) * 4;
+}
+
+int lmd_force_lc_particles(const lmd_grid* g, const lmd_lj* lj, int pattern, int flags,
+                           const double* pos4, int64_t n_owned, const int32_t* cell_of,
+                           const int32_t* cell_start, const int32_t* cell_count,
+                           const uint8_t* dup, double* fx, double* fy, double* fz,
+                           double* ev_scratch, lmd_stats* stats, void* stream) {
   if (n_owned <= 0) return LMD_OK;
   if (n_owned > 0x7fffffffLL) return LMD_ERR_CONFIG;
   const LJK k = make_ljk(lj);
   const bool ev = (flags & LMD_FLAG_ENERGY) != 0;
   cudaStream_t s = (cudaStream_t)stream;
-  const unsigned blocks = (unsigned)cdiv(n_owned, 128);
-  if (ev)
-    lc_tpi_kernel<true><<<blocks, 128, 0, s>>>((int)n_owned, g->tdims[0], g->tdims[1], k, pos4,
-                                               cell_of, cell_start, cell_count, dup, fx, fy, fz,
-                                               ev_scratch, stats);
-  else
-    lc_tpi_kernel<false><<<blocks, 128, 0, s>>>((int)n_owned, g->tdims[0], g->tdims[1], k, pos4,
-                                                cell_of, cell_start, cell_count, dup, fx, fy, fz,
-                                                ev_scratch, stats);
+  const unsigned blocks = (unsigned)cdiv(cdiv(n_owned, order_A(pattern)), 4);
+#define LMD_TPI(P)                                                                          \
+  do {                                                                                      \
+    if (ev)                                                                                 \
+      lc_tpi_kernel<P, true><<<blocks, 128, 0, s>>>((int)n_owned, g->tdims[0], g->tdims[1], \
+                                                    k, pos4, cell_of, cell_start,           \
+                                                    cell_count, dup, fx, fy, fz,            \
+                                                    ev_scratch, stats);                     \
+    else                                                                                    \
+      lc_tpi_kernel<P, false><<<blocks, 128, 0, s>>>((int)n_owned, g->tdims[0],             \
+                                                     g->tdims[1], k, pos4, cell_of,         \
+                                                     cell_start, cell_count, dup, fx, fy,   \
+                                                     fz, ev_scratch, stats);                \
+  } while (0)
+  switch (pattern) {
+    case LMD_ONE_BY_V: LMD_TPI(LMD_ONE_BY_V); break;
+    case LMD_V_BY_ONE: LMD_TPI(LMD_V_BY_ONE); break;
+    case LMD_TWO_BY_HALF: LMD_TPI(LMD_TWO_BY_HALF); break;
+    case LMD_HALF_BY_TWO: LMD_TPI(LMD_HALF_BY_TWO); break;
+    default: return LMD_ERR_CONFIG;
+  }
+#undef LMD_TPI
   LMD_CHECK_LAUNCH();
-  if (ev) return reduce_ev(ev_scratch, lmd_lc_tpi_ev_slots(n_owned), stats, s);
+  if (ev) return reduce_ev(ev_scratch, lmd_lc_tpi_ev_slots(n_owned, pattern), stats, s);
   return LMD_OK;
 }
 

@@ -322,24 +322,28 @@ def test_gpu_lane_stats_lc_and_vl(rng):
     cont.rebuild(buf)
     cont.refresh(buf)
     # warp per cell: the reference's c01 formula at V = 32
-    for pat in (PatternKind.ONE_BY_V, PatternKind.HALF_BY_TWO):
+    cont.thread_per_particle = False
+    for pat in PATTERNS:
         steps, active = cont.gpu_lane_stats(pat)
         inv, slots, useful = cont._lc_stats(B.traversals.traversal_code(TraversalKind.LC_C01),
                                             False, pat, 32)
         assert (steps, active) == (slots, useful)
-    # thread per particle: per warp of 32 consecutive particles and per
-    # neighbour offset, the largest neighbour cell
-    steps, active = cont.gpu_lane_stats(PatternKind.V_BY_ONE)
+    # thread per particle: per warp of a consecutive particles and per
+    # neighbour offset, ceil(n / b) for the largest neighbour cell n
+    cont.thread_per_particle = True
     cells = cont._cell_of.cpu().numpy().astype(np.int64)
     count = cont._count.cpu().numpy().astype(np.int64)
     t0, t1 = int(cont.total_dims[0]), int(cont.total_dims[1])
-    want = 0
-    for w0 in range(0, len(cells), 32):
-        c = cells[w0:w0 + 32]
-        for d in range(27):
-            off = (d // 9 - 1) + t0 * ((d // 3) % 3 - 1 + t1 * (d % 3 - 1))
-            want += int(count[c + off].max())
-    assert steps == 32 * want and 0 < active <= steps
+    for pat in (PatternKind.V_BY_ONE, PatternKind.HALF_BY_TWO):   # the orders it serves
+        a, b = pat.shape(32)
+        steps, active = cont.gpu_lane_stats(pat)
+        want = 0
+        for w0 in range(0, len(cells), a):
+            c = cells[w0:w0 + a]
+            for d in range(27):
+                off = (d // 9 - 1) + t0 * ((d // 3) % 3 - 1 + t1 * (d % 3 - 1))
+                want += int((-(-count[c + off] // b)).max())
+        assert steps == 32 * want and 0 < active <= steps
     # Verlet lists: tiles x kmax / B steps; active = list entries
     vl = B.VerletListContainer(box, LJParams(cutoff=2.5, skin=0.3))
     vl.rebuild(buf)
