@@ -298,13 +298,15 @@ int lmd_force_vl_ci(int pattern, int ci, int flags, const lmd_lj* lj, int64_t n_
  * zeroed f (j-side reactions; summation order is then not deterministic);
  * newton3 = 2 runs full lists like 0 and also counts the pairs with an image
  * j into pairs_owned_halo, for the reference's Newton3 pair bookkeeping
- * (owned-owned pairs once = (pairs - halo) / 2 + halo).
+ * (owned-owned pairs once = (pairs - halo) / 2 + halo).  out_perm (nullable,
+ * newton3 0 / 2): the force of backing particle i goes to f[out_perm[i]] --
+ * the caller's order, collect_forces fused into the kernel.
  * ev_scratch: 2 * lmd_vl_ev_slots(n_owned, pattern) doubles. */
 int64_t lmd_vl_ev_slots(int64_t n_owned, int pattern);
 int lmd_force_vl(int pattern, int newton3, int flags, const lmd_lj* lj, int64_t n_owned,
                  const double* pos4, const double* soa, int64_t ntot, const int64_t* tile_off,
-                 const int32_t* kmax, const int32_t* nbr, double* fx, double* fy, double* fz,
-                 double* ev_scratch, lmd_stats* stats, void* stream);
+                 const int32_t* kmax, const int32_t* nbr, const int32_t* out_perm, double* fx,
+                 double* fy, double* fz, double* ev_scratch, lmd_stats* stats, void* stream);
 /* KernelStats of a Verlet-list force phase: i-tiles of `a` consecutive owned
  * particles, each tile's j-stream its longest list chunked by b. */
 int lmd_vl_stats(int64_t n_owned, int a, int b, int vector_width, const int32_t* count,

@@ -171,7 +171,7 @@ _sig("lmd_vl_ci_ev_slots", _I64, _I64, _INT)
 _sig("lmd_force_vl_ci", _INT, _INT, _INT, _INT, C.POINTER(LJ), _I64, _I64, _VP, _VP, _VP, _VP,
      _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP)
 _sig("lmd_force_vl", _INT, _INT, _INT, _INT, C.POINTER(LJ), _I64, _VP, _VP, _I64, _VP, _VP,
-     _VP, _VP, _VP, _VP, _VP, _VP, _VP)
+     _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP)
 _sig("lmd_vl_stats", _INT, _I64, _INT, _INT, _INT, _VP, _VP, _VP)
 _sig("lmd_vcl_temp_bytes", _SZ, _I64)
 _sig("lmd_vcl_order", _INT, _I64, _VP, _VP, _VP, _D, _D, _D, _I64, *([_VP] * 8), _SZ, _VP)

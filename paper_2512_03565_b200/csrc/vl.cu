@@ -331,6 +331,7 @@ __device__ __forceinline__ double4 ld_j(const double* __restrict__ pos4, const S
 
 template <int P, bool EV, int N3, int U, int SOA>
 __device__ __forceinline__ void vl_tile(int t, int lane, int n_owned,
+                                        const int32_t* __restrict__ out_perm,
                                         const double* __restrict__ pos4, const SoA& q,
                                         const long long* __restrict__ toff,
                                         const int32_t* __restrict__ kmax,
@@ -373,9 +374,11 @@ __device__ __forceinline__ void vl_tile(int t, int lane, int n_owned,
       atomicAdd(fy + i, ry);
       atomicAdd(fz + i, rz);
     } else {
-      fx[i] = rx;
-      fy[i] = ry;
-      fz[i] = rz;
+      // out_perm: write straight into the caller's order (collect_forces fused)
+      const int o = out_perm ? out_perm[i] : i;
+      fx[o] = rx;
+      fy[o] = ry;
+      fz[o] = rz;
     }
   }
   a.ax = ax0;
@@ -387,7 +390,8 @@ __device__ __forceinline__ void vl_tile(int t, int lane, int n_owned,
 // parallelism per warp for occupancy (64 registers, 8 blocks per SM).
 template <int P, bool EV, int N3, int U, int SOA>
 __global__ void __launch_bounds__(32 * kVLWarps, 8)
-    vl_force_kernel(int n_owned, int ntiles, const double* __restrict__ pos4, SoA q,
+    vl_force_kernel(int n_owned, int ntiles, const int32_t* __restrict__ out_perm,
+                    const double* __restrict__ pos4, SoA q,
                     const long long* __restrict__ toff, const int32_t* __restrict__ kmax,
                     const int32_t* __restrict__ nbr, LJK k, double* __restrict__ fx,
                     double* __restrict__ fy, double* __restrict__ fz, double* __restrict__ ev,
@@ -396,7 +400,8 @@ __global__ void __launch_bounds__(32 * kVLWarps, 8)
   const int t = blockIdx.x * kVLWarps + (threadIdx.x >> 5);
   Acc a = {0.0, 0.0, 0.0, 0.0, 0.0, 0, 0, 0};
   if (t < ntiles)
-    vl_tile<P, EV, N3, U, SOA>(t, lane, n_owned, pos4, q, toff, kmax, nbr, k, a, fx, fy, fz);
+    vl_tile<P, EV, N3, U, SOA>(t, lane, n_owned, out_perm, pos4, q, toff, kmax, nbr, k, a, fx, fy,
+                               fz);
   flush_acc(a, lane, t < ntiles, EV, (long long)blockIdx.x * kVLWarps + (threadIdx.x >> 5), ev,
             stats);
 }
@@ -555,26 +560,28 @@ int64_t lmd_vl_ev_slots(int64_t n_owned, int pattern) {
 }  // extern "C"
 
 template <int P, bool EV, int N3, int GM>
-static void launch_vl(int64_t n_owned, int64_t ntiles, const double* pos4, const SoA& q,
+static void launch_vl(int64_t n_owned, int64_t ntiles, const int32_t* out_perm,
+                      const double* pos4, const SoA& q,
                       const int64_t* tile_off, const int32_t* kmax, const int32_t* nbr,
                       const LJK& k, double* fx, double* fy, double* fz, double* ev,
                       lmd_stats* stats, cudaStream_t s) {
   const unsigned blocks = (unsigned)cdiv(ntiles, kVLWarps);
   vl_force_kernel<P, EV, N3, 2, GM><<<blocks, 32 * kVLWarps, 0, s>>>(
-      (int)n_owned, (int)ntiles, pos4, q, (const long long*)tile_off, kmax, nbr, k, fx, fy, fz, ev,
+      (int)n_owned, (int)ntiles, out_perm, pos4, q, (const long long*)tile_off, kmax, nbr, k, fx, fy, fz, ev,
       stats);
 }
 
 template <int P, bool EV, int N3>
-static void launch_vl_g(int gm, int64_t n_owned, int64_t ntiles, const double* pos4,
+static void launch_vl_g(int gm, int64_t n_owned, int64_t ntiles, const int32_t* out_perm,
+                        const double* pos4,
                         const SoA& q, const int64_t* tile_off, const int32_t* kmax,
                         const int32_t* nbr, const LJK& k, double* fx, double* fy, double* fz,
                         double* ev, lmd_stats* stats, cudaStream_t s) {
   if (gm == 1)
-    launch_vl<P, EV, N3, 1>(n_owned, ntiles, pos4, q, tile_off, kmax, nbr, k, fx, fy, fz, ev,
+    launch_vl<P, EV, N3, 1>(n_owned, ntiles, out_perm, pos4, q, tile_off, kmax, nbr, k, fx, fy, fz, ev,
                             stats, s);
   else
-    launch_vl<P, EV, N3, 0>(n_owned, ntiles, pos4, q, tile_off, kmax, nbr, k, fx, fy, fz, ev,
+    launch_vl<P, EV, N3, 0>(n_owned, ntiles, out_perm, pos4, q, tile_off, kmax, nbr, k, fx, fy, fz, ev,
                             stats, s);
 }
 
@@ -582,10 +589,11 @@ extern "C" {
 
 int lmd_force_vl(int pattern, int newton3, int flags, const lmd_lj* lj, int64_t n_owned,
                  const double* pos4, const double* soa, int64_t ntot, const int64_t* tile_off,
-                 const int32_t* kmax, const int32_t* nbr, double* fx, double* fy, double* fz,
-                 double* ev_scratch, lmd_stats* stats, void* stream) {
+                 const int32_t* kmax, const int32_t* nbr, const int32_t* out_perm, double* fx,
+                 double* fy, double* fz, double* ev_scratch, lmd_stats* stats, void* stream) {
   if (n_owned <= 0) return LMD_OK;
   if (newton3 < 0 || newton3 > 2) return LMD_ERR_CONFIG;
+  if (out_perm && newton3 == 1) return LMD_ERR_CONFIG;
   const LJK k = make_ljk(lj);
   const int64_t ntiles = lmd_vl_num_tiles(n_owned, pattern);
   cudaStream_t s = (cudaStream_t)stream;
@@ -596,7 +604,8 @@ int lmd_force_vl(int pattern, int newton3, int flags, const lmd_lj* lj, int64_t 
   const int gm = soa ? 1 : 0;
   const SoA q = {soa, soa ? soa + ntot : nullptr, soa ? soa + 2 * ntot : nullptr};
 #define LMD_VLK(P, EVB, N3B)                                                                  \
-  launch_vl_g<P, EVB, N3B>(gm, n_owned, ntiles, pos4, q, tile_off, kmax, nbr, k, fx, fy, fz,   \
+  launch_vl_g<P, EVB, N3B>(gm, n_owned, ntiles, out_perm, pos4, q, tile_off, kmax, nbr, k, fx, \
+                           fy, fz,                                                            \
                            ev_scratch, stats, s)
 #define LMD_VL_P(P)                                   \
   do {                                                \

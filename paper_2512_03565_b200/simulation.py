@@ -84,13 +84,13 @@ class RunSummary:
         return self.particle_count * self.steps / self.wall_time_s if self.wall_time_s else 0.0
 
 
-def _launch(cont, cfg: Configuration, V: int, energy: bool):
+def _launch(cont, cfg: Configuration, V: int, energy: bool, owned=None):
     kind = cfg.container
     if kind is ContainerKind.LINKED_CELLS:
         code = traversal_code(cfg.traversal)
         return cont.launch_force(cfg.pattern, energy, traversal=code, newton3=cfg.newton3)
-    if kind is ContainerKind.VERLET_LISTS:
-        return cont.launch_force(cfg.pattern, cfg.newton3, energy)
+    if kind is ContainerKind.VERLET_LISTS:   # forces written in the caller's order
+        return cont.launch_force(cfg.pattern, cfg.newton3, energy, out=owned)
     return cont.launch_force(energy)
 
 
@@ -208,7 +208,7 @@ def run_md(owned, box, params, iterations: int, vector_width: int = 8, *,
             if not whole:
                 provider.begin_region()
             t0 = time.perf_counter()
-            stats_t = _launch(cont, cfg, vector_width, energy)
+            stats_t = _launch(cont, cfg, vector_width, energy, owned)
             sample = provider.end_region() if metric not in ("laneops", "iteration") else None
             stats = _finish(cont, cfg, vector_width, stats_t)
             force_time += time.perf_counter() - t0

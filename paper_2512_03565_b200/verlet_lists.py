@@ -61,6 +61,7 @@ class VerletListContainer:
         # pair bookkeeping (no atomics, deterministic); "half_list" runs half
         # lists with FP64 atomics on the j side
         self.n3_mode = "full_list"
+        self._collected_into = None
         self._clusters_cache: dict = {}
 
     # ------------------------------------------------------------ protocol
@@ -370,7 +371,12 @@ class VerletListContainer:
 
     # ----------------------------------------------------------------- force
     def launch_force(self, pattern, newton3: bool, energy: bool = False, stats_t=None,
-                     ev_t=None):
+                     ev_t=None, out=None):
+        """Launch the force kernel without synchronising; returns the device
+        stats tensor.  ``out`` (a device ParticleBuffer of the rebuild's
+        particles): write the forces straight into out.force_* in its order
+        -- collect_forces fused into the kernel (full lists only); the next
+        collect_forces(out) is then a no-op."""
         pattern = as_pattern(pattern)
         ci = self._ci_for(newton3)
         mode = self._kernel_n3(newton3)
@@ -397,11 +403,16 @@ class VerletListContainer:
             self._fx.zero_()
             self._fy.zero_()
             self._fz.zero_()
+        direct = out is not None and mode != 1 and len(out) == self.n_owned
+        fx, fy, fz = ((out.force_x, out.force_y, out.force_z) if direct
+                      else (self._fx, self._fy, self._fz))
         N.call("lmd_force_vl", pattern.code, mode, (N.FLAG_ENERGY if energy else 0) | self.knobs,
                N.make_lj(self.params), self.n_owned, N.ptr(self._pos4),
                N.ptr(self._soa) if self.use_soa else None, self._soa.shape[1],
-               N.ptr(tile_off), N.ptr(kmax), N.ptr(nbr), N.ptr(self._fx),
-               N.ptr(self._fy), N.ptr(self._fz), N.ptr(ev_t), N.ptr(stats_t), N.stream())
+               N.ptr(tile_off), N.ptr(kmax), N.ptr(nbr),
+               N.ptr(self._perm) if direct else None, N.ptr(fx), N.ptr(fy), N.ptr(fz),
+               N.ptr(ev_t), N.ptr(stats_t), N.stream())
+        self._collected_into = out if direct else None
         return stats_t
 
     def pair_count(self, st, newton3: bool) -> int:
@@ -443,6 +454,10 @@ class VerletListContainer:
                            virial=st.virial)
 
     def collect_forces(self, owned) -> None:
+        if self._collected_into is not None and owned is self._collected_into:
+            self._collected_into = None        # the kernel already wrote them
+            return
+        self._collected_into = None
         d = device_soa(owned)
         n = self.n_owned
         if n:

@@ -200,3 +200,22 @@ def test_line_aligned_lists_same_pairs_and_forces(rng, window):
         if prev is not None:
             assert np.array_equal(prev, f)
         prev = f
+
+
+@pytest.mark.parametrize("n3", [False, True])
+def test_fused_collect_matches_scatter(rng, n3):
+    """launch_force(out=buf) writes the forces straight into the caller's
+    order (collect_forces fused); bitwise equal to launch + scatter."""
+    pos, span = _state(rng, 3000, 0.8)
+    params = LJParams(cutoff=2.5, skin=0.3)
+    box = SimulationBox.cube(span, periodic=True)
+    res = []
+    for fused in (False, True):
+        cont = B.VerletListContainer(box, params)
+        buf = ParticleBuffer.from_positions(pos, device="cuda")
+        cont.rebuild(buf)
+        cont.refresh(buf)
+        st = cont.launch_force(PatternKind.V_BY_ONE, n3, out=buf if fused else None)
+        cont.collect_forces(buf)
+        res.append((buf.forces().cpu().numpy(), cont.pair_count(B._native.read_stats(st), n3)))
+    assert np.array_equal(res[0][0], res[1][0]) and res[0][1] == res[1][1]
