@@ -345,10 +345,13 @@ int lmd_force_vcl(int64_t ncl, int M, int flags, const lmd_lj* lj, const double*
                   const int64_t* off, const int32_t* nlist, const int32_t* list,
                   const int64_t* hoff, const int32_t* hnlist, const int32_t* hlist, double* fx,
                   double* fy, double* fz, double* ev_scratch, lmd_stats* stats, void* stream);
+/* ncl_total = owned + halo clusters of pos4; nd_scratch: ncl_total int32
+ * (per-cluster non-dummy counts, computed here). */
 int lmd_vcl_stats(int64_t ncl, int M, int newton3, int a, int b, int vector_width,
                   const double* pos4, const int64_t* off, const int32_t* nlist,
                   const int32_t* n3count, const int32_t* list, const int64_t* hoff,
-                  const int32_t* hcount, const int32_t* hlist, lmd_stats* stats, void* stream);
+                  const int32_t* hcount, const int32_t* hlist, int64_t ncl_total,
+                  int32_t* nd_scratch, lmd_stats* stats, void* stream);
 int lmd_vcl_collect(int64_t n, const int32_t* order, const int32_t* slot, const double* fx,
                     const double* fy, const double* fz, double* ox, double* oy, double* oz,
                     void* stream);

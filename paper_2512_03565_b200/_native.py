@@ -182,7 +182,8 @@ _sig("lmd_vcl_pairs", _INT, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _I64, _I64,
      _VP, _VP, _VP, _VP, _VP)
 _sig("lmd_vcl_ev_slots", _I64, _I64)
 _sig("lmd_force_vcl", _INT, _I64, _INT, _INT, C.POINTER(LJ), *([_VP] * 12), _VP)
-_sig("lmd_vcl_stats", _INT, _I64, _INT, _INT, _INT, _INT, _INT, *([_VP] * 8), _VP, _VP)
+_sig("lmd_vcl_stats", _INT, _I64, _INT, _INT, _INT, _INT, _INT, *([_VP] * 8), _I64, _VP, _VP,
+     _VP)
 _sig("lmd_vcl_collect", _INT, _I64, *([_VP] * 8), _VP)
 _sig("lmd_lc_n3_ev_slots", _I64, C.POINTER(Grid))
 _sig("lmd_force_lc_n3", _INT, C.POINTER(Grid), C.POINTER(LJ), _INT, _INT, _INT, _VP, _I64,

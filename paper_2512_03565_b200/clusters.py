@@ -292,10 +292,12 @@ class VerletClusterContainer:
         if hit is None:
             a, b = pattern.shape(V)
             t = N.new_stats(self._pos4.device)
+            nclt = int(self._pos4.shape[0]) // self.cluster_size
+            nd = torch.empty(max(nclt, 1), dtype=torch.int32, device=self._pos4.device)
             N.call("lmd_vcl_stats", self._own.ncl, self.cluster_size, int(newton3), a, b, V,
                    N.ptr(self._pos4), N.ptr(self._off), N.ptr(self._count), N.ptr(self._n3count),
                    N.ptr(self._list), N.ptr(self._hoff), N.ptr(self._hcount), N.ptr(self._hlist),
-                   N.ptr(t), N.stream())
+                   nclt, N.ptr(nd), N.ptr(t), N.stream())
             st = N.read_stats(t)
             hit = (int(st.kernel_invocations), int(st.lane_slots), int(st.useful_interactions))
             self._stats_cache[key] = hit

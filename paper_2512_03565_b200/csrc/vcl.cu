@@ -363,7 +363,9 @@ __global__ void vcl_stats_kernel(int ncl, int M, int newton3, int a, int b,
                                  const int32_t* __restrict__ list,
                                  const long long* __restrict__ hoff,
                                  const int32_t* __restrict__ hcount,
-                                 const int32_t* __restrict__ hlist, lmd_stats* __restrict__ stats) {
+                                 const int32_t* __restrict__ hlist,
+                                 const int32_t* __restrict__ nd_of,
+                                 lmd_stats* __restrict__ stats) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   long long inv = 0, useful = 0;
   if (c < ncl) {
@@ -391,10 +393,7 @@ __global__ void vcl_stats_kernel(int ncl, int M, int newton3, int a, int b,
       const bool halo = u >= nlist[c];
       const int z = halo ? ncl + hlist[hoff[c] + (u - nlist[c])] : lst[u];
       if (!halo && newton3 && z < c) continue;
-      int ndz = 0;
-      for (int t = 0; t < M; ++t)
-        ndz += pos4[4 * ((long long)z * M + t) + 3] != (double)LMD_DUMMY;
-      useful += (long long)owned * ndz;
+      useful += (long long)owned * nd_of[z];
     }
   }
   inv = warp_sum_ll(inv);
@@ -403,6 +402,17 @@ __global__ void vcl_stats_kernel(int ncl, int M, int newton3, int a, int b,
     atomicAdd((unsigned long long*)&stats->kernel_invocations, (unsigned long long)inv);
     atomicAdd((unsigned long long*)&stats->useful_interactions, (unsigned long long)useful);
   }
+}
+
+// non-dummy slots per cluster (owned and halo clusters), read once instead of
+// once per list entry by vcl_stats_kernel
+__global__ void cluster_nd_kernel(int64_t nclt, int M, const double* __restrict__ pos4,
+                                  int32_t* __restrict__ nd) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= nclt) return;
+  int k = 0;
+  for (int t = 0; t < M; ++t) k += pos4[4 * (c * M + t) + 3] != (double)LMD_DUMMY;
+  nd[c] = k;
 }
 
 __global__ void vcl_lane_slots_kernel(lmd_stats* stats, int V) {
@@ -622,14 +632,18 @@ int lmd_force_vcl(int64_t ncl, int M, int flags, const lmd_lj* lj, const double*
 int lmd_vcl_stats(int64_t ncl, int M, int newton3, int a, int b, int vector_width,
                   const double* pos4, const int64_t* off, const int32_t* nlist,
                   const int32_t* n3count, const int32_t* list, const int64_t* hoff,
-                  const int32_t* hcount, const int32_t* hlist, lmd_stats* stats, void* stream) {
+                  const int32_t* hcount, const int32_t* hlist, int64_t ncl_total,
+                  int32_t* nd_scratch, lmd_stats* stats, void* stream) {
   if (vector_width < 4 || (vector_width & (vector_width - 1)) != 0) return LMD_ERR_CONFIG;
   if (a < 1 || b < 1 || a * b != vector_width) return LMD_ERR_CONFIG;
+  if (ncl_total < ncl) return LMD_ERR_CONFIG;
   cudaStream_t s = (cudaStream_t)stream;
   if (ncl > 0) {
+    cluster_nd_kernel<<<g1(ncl_total, 256), 256, 0, s>>>(ncl_total, M, pos4, nd_scratch);
+    LMD_CHECK_LAUNCH();
     vcl_stats_kernel<<<g1(ncl, 128), 128, 0, s>>>(
         (int)ncl, M, newton3, a, b, pos4, (const long long*)off, nlist, n3count, list,
-        (const long long*)hoff, hcount, hlist, stats);
+        (const long long*)hoff, hcount, hlist, nd_scratch, stats);
     LMD_CHECK_LAUNCH();
   }
   vcl_lane_slots_kernel<<<1, 1, 0, s>>>(stats, vector_width);
