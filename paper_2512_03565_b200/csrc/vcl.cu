@@ -277,29 +277,43 @@ __global__ void __launch_bounds__(128)
       const double4 pi = ld_pos4(pos4, gi);
       const bool iown = ilive && pi.w == (double)LMD_OWNED;
       double ax = 0.0, ay = 0.0, az = 0.0;
-      for (int u0 = 0; u0 < units; u0 += G) {
-        const int u = u0 + g;
-        const bool live = iown && u < units;
-        const int b = !live ? a : (u == 0 ? a : (u <= nl ? lst[u - 1] : ncl + hlst[u - 1 - nl]));
-        const long long base = (long long)b * M;
+      // R = 32 / MP units per lane fill one 32-bit hit mask (unit r at bits
+      // [r * MP, r * MP + M)), so the LJ loop runs once per set bit over R
+      // units' worth of tests; M > 16 keeps one unit per mask, in 32-slot chunks
+      constexpr int R = MP >= 32 ? 1 : 32 / MP;
+      auto unit_cluster = [&](int u) {
+        return u == 0 ? a : (u <= nl ? lst[u - 1] : ncl + hlst[u - 1 - nl]);
+      };
+      for (int u0 = 0; u0 < units; u0 += G * R) {
+        const int bc0 = (u0 + g < units) ? unit_cluster(u0 + g) : a;   // unit r = 0
         for (int c0 = 0; c0 < M; c0 += 32) {
           const int cnt = min(M - c0, 32);
           unsigned mask = 0u;
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            const int u = u0 + g + r * G;
+            if (!iown || u >= units) continue;
+            const int bc = r == 0 ? bc0 : unit_cluster(u);
+            const long long base = (long long)bc * M + c0;
+            unsigned m = 0u;
 #pragma unroll 4
-          for (int q = 0; q < cnt; ++q) {
-            const double4 pj = ld_pos4(pos4, base + c0 + q);
-            const double r2 = r2_exact(pi.x - pj.x, pi.y - pj.y, pi.z - pj.z);
-            const bool hit = pj.w != (double)LMD_DUMMY && r2 < k.rc2;
-            mask |= (hit ? 1u : 0u) << q;
-          }
-          if (!live) mask = 0u;
-          if (b == a) {   // self unit: not with itself
-            const unsigned self = (unsigned)(gi - base - c0);
-            if (self < 32u) mask &= ~(1u << self);
+            for (int q = 0; q < cnt; ++q) {
+              const double4 pj = ld_pos4(pos4, base + q);
+              const double r2 = r2_exact(pi.x - pj.x, pi.y - pj.y, pi.z - pj.z);
+              m |= (pj.w != (double)LMD_DUMMY && r2 < k.rc2 ? 1u : 0u) << q;
+            }
+            if (bc == a) {   // self unit: not with itself
+              const unsigned self = (unsigned)(gi - base);
+              if (self < 32u) m &= ~(1u << self);
+            }
+            mask |= m << (r * MP);
           }
           while (mask) {
-            const long long gj = base + c0 + __ffs(mask) - 1;
+            const int bit = __ffs(mask) - 1;
             mask &= mask - 1u;
+            const int r = bit / MP, q = bit - r * MP;
+            const long long gj =
+                (long long)(r == 0 ? bc0 : unit_cluster(u0 + g + r * G)) * M + c0 + q;
             const double4 pj = ld_pos4(pos4, gj);
             const double dx = pi.x - pj.x, dy = pi.y - pj.y, dz = pi.z - pj.z;
             const double r2 = r2_exact(dx, dy, dz);
