@@ -18,6 +18,7 @@ from __future__ import annotations
 import time
 from dataclasses import dataclass, field
 
+import numpy as np
 import torch
 
 from . import _native as N
@@ -282,3 +283,123 @@ def read_records_csv(path) -> list:
         out.append(IterationRecord(int(p[0]), p[1], cfg, float(p[6]), int(p[7]), int(p[8]),
                                    int(p[9]), int(p[10]), int(p[11])))
     return out
+
+
+def run_md_graph(owned, box, params, iterations: int, vector_width: int = 8, *,
+                 config: Configuration, rebuild_period: int | None = None,
+                 energy: bool = False):
+    """``run_md`` for a fixed Verlet-list configuration with the steady-state
+    step as a CUDA graph (the north star's "CUDA streams and graphs instead
+    of a tracing compiler").
+
+    After every rebuild two graphs are captured: (refresh -> force, written
+    in the caller's order -> post-force half step) and (the next step's
+    pre-force half step -> max-displacement kernel), each ending with an
+    async copy of (stats, displacement) into pinned host memory.  Each later
+    step is two replays and one host read, which decides the next rebuild
+    (displacement >= skin/2 or the period); a rebuild step runs the same
+    work eagerly and re-captures.  Positions
+    are wrapped at rebuilds (``wrap="at_rebuild"``).  Same kernels in the
+    same order as ``run_md``: identical trajectory.  Returns (records,
+    summary)."""
+    from .verlet_lists import VerletListContainer
+    if config.container is not ContainerKind.VERLET_LISTS:
+        raise ConfigurationError("run_md_graph runs the Verlet-list container")
+    if not config.is_valid():
+        raise ConfigurationError(f"invalid configuration {config.label!r}")
+    validate_vector_width(vector_width)
+    box = as_box(box)
+    dev = owned.device
+    kw = {} if rebuild_period is None else {"rebuild_period": rebuild_period}
+    cont = VerletListContainer(box, params, device=dev, **kw)
+    pattern, n3 = config.pattern, config.newton3
+    stats_t = N.new_stats(dev)
+    disp = torch.zeros(1, dtype=torch.float64, device=dev)
+    host = torch.zeros(N.STATS_BYTES + 8, dtype=torch.uint8).pin_memory()
+    dev_out = torch.zeros(N.STATS_BYTES + 8, dtype=torch.uint8, device=dev)
+    slots = int(N.load().lmd_vl_ev_slots(len(owned), pattern.code))
+    ev_t = torch.empty(2 * max(slots, 1), dtype=torch.float64, device=dev)
+    half = (0.5 * params.skin) ** 2
+    records: list = []
+    pairs_total = 0
+    rebuilds = 0
+
+    def step():
+        """One step from the refresh to the post-force half step."""
+        cont.refresh(owned)
+        cont.launch_force(pattern, n3, energy, stats_t, ev_t, out=owned)
+        cont.collect_forces(owned)
+        velocity_verlet_step(owned, params, POST_FORCE, check=False)
+        dev_out[:N.STATS_BYTES].copy_(stats_t)
+
+    def advance():
+        """The next step's pre-force half step and displacement test."""
+        velocity_verlet_step(owned, params, PRE_FORCE, check=False)
+        N.call("lmd_max_displacement2", len(owned), N.ptr(owned.pos_x), N.ptr(owned.pos_y),
+               N.ptr(owned.pos_z), N.ptr(cont.reference_positions), N.ptr(disp), N.stream())
+        dev_out[N.STATS_BYTES:].copy_(disp.view(torch.uint8))
+
+    def fetch():
+        host.copy_(dev_out, non_blocking=True)
+
+    def read():
+        raw = host.numpy().tobytes()
+        st = N.Stats.from_buffer_copy(raw[:N.STATS_BYTES])
+        d2 = float(np.frombuffer(raw[N.STATS_BYTES:], dtype=np.float64)[0])
+        return st, d2
+
+    graphs = None
+    side = torch.cuda.Stream(device=dev)
+    start = time.perf_counter()
+    velocity_verlet_step(owned, params, PRE_FORCE, check=False)
+    need = True
+    for it in range(iterations):
+        last = it == iterations - 1
+        if need:
+            apply_boundaries(owned, box)
+            cont.rebuild(owned)
+            cont.ensure_lists(pattern, n3)
+            step()
+            if not last:
+                advance()
+            fetch()
+            rebuilds += 1
+            torch.cuda.current_stream().synchronize()
+            # capture on a side stream with capture_begin / capture_end (the
+            # torch.cuda.graph context also runs gc and empties the cache)
+            graphs = (torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph())
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                for g_, fn in zip(graphs, (step, advance)):
+                    g_.capture_begin()             # captured, not run
+                    fn()
+                    fetch()
+                    g_.capture_end()
+            torch.cuda.current_stream().wait_stream(side)
+        else:
+            graphs[0].replay()
+            if not last:
+                graphs[1].replay()
+        torch.cuda.current_stream().synchronize()
+        st, d2 = read()
+        if st.overlap:
+            raise ParticleOverlapError("zero distance between interacting particles")
+        cont.steps_since_rebuild += 1
+        geo = cont.vl_stats(n3, pattern, vector_width)
+        pairs = cont.pair_count(st, n3)
+        pairs_total += pairs
+        records.append(IterationRecord(it, PRODUCTION, config, 0.0, geo[1], geo[2],
+                                       geo[1] - geo[2], pairs, len(owned)))
+        need = (cont.steps_since_rebuild >= cont.rebuild_period) or d2 >= half
+    apply_boundaries(owned, box)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - start
+    flag = owned.extra.get("nonfinite")
+    if flag is not None and int(flag.item()):
+        raise SimulationDivergedError("non-finite particle state")
+    summary = RunSummary(per_config_metric={config.label: 0.0}, phase_selections=[],
+                         failed_configs=[], wall_time_s=wall, particle_count=len(owned),
+                         initial_max_per_cell=0, final_max_per_cell=0, final_max_speed=0.0,
+                         force_time_s=0.0, steps=iterations, retunes=0,
+                         extra={"rebuilds": rebuilds, "pairs_total": pairs_total})
+    return records, summary
