@@ -166,11 +166,15 @@ class Phase:
 
     def refresh(self):
         if self.dec is not None:
-            g = self.dec.exchange(self.owned_rows)
-            self.ghosts.pos_x.copy_(g[:, 0])
-            self.ghosts.pos_y.copy_(g[:, 1])
-            self.ghosts.pos_z.copy_(g[:, 2])
-            self.cont.refresh(self.buf, self.ghosts)
+            b = self.buf
+            rows = self.dec.exchange_positions(b.pos_x, b.pos_y, b.pos_z)
+            if self.kind == "vl":
+                self.cont.refresh(b, rows)
+            else:
+                self.ghosts.pos_x.copy_(rows[:, 0])
+                self.ghosts.pos_y.copy_(rows[:, 1])
+                self.ghosts.pos_z.copy_(rows[:, 2])
+                self.cont.refresh(b, self.ghosts)
         elif self.kind == "lc":
             self.cont.refresh_positions(self.buf)
         elif self.kind == "vl":

@@ -401,6 +401,18 @@ int lmd_apply_boundaries(const lmd_box* box, int64_t n, double* x, double* y, do
 
 /* integrator.py:21-48: phase 0 = pre-force (drift, stash old force, zero
  * force), 1 = post-force (kick).  *nonfinite |= 1 on non-finite state. */
+/* ----------------------------------------- brick decomposition (§8e) */
+/* One exchange stage's pack (decomposition.py): out_rows[k] (row-major
+ * x, y, z) = source(idx[k]) with coordinate `axis` shifted by `shift` (the
+ * exact image offset, or 0), where source indexes [owned SoA ox/oy/oz |
+ * ghost rows received in earlier stages]. */
+int lmd_ghost_pack(int64_t count, const int32_t* idx, int64_t n_owned, const double* ox,
+                   const double* oy, const double* oz, const double* ghost_rows, int axis,
+                   double shift, double* out_rows, void* stream);
+/* pos4[k] = (rows[perm[k]], own_value): gather row-major positions. */
+int lmd_gather_pos4_rows(int64_t n, const int32_t* perm, const double* rows, double own_value,
+                         double* pos4, void* stream);
+
 /* *out = max_k |r_k - ref_k|^2 with the reference's unfused (dx^2 + dy^2) +
  * dz^2 (containers.py:23-38, needs_rebuild); ref_xyz rows are (x, y, z). */
 int lmd_max_displacement2(int64_t n, const double* x, const double* y, const double* z,

@@ -160,6 +160,8 @@ _sig("lmd_vl_fill", _INT, C.POINTER(Grid), _D, _INT, _INT, _I64, _I32, _VP, _VP,
 _sig("lmd_vl_build", _INT, C.POINTER(Grid), _D, _INT, _INT, _I64, _I32, _VP, _VP, _VP, _VP, _VP,
      _I32, _VP, _VP, _VP, _VP, _VP, _VP, _VP)
 _sig("lmd_vl_ev_slots", _I64, _I64, _INT)
+_sig("lmd_ghost_pack", _INT, _I64, _VP, _I64, _VP, _VP, _VP, _VP, _INT, _D, _VP, _VP)
+_sig("lmd_gather_pos4_rows", _INT, _I64, _VP, _VP, _D, _VP, _VP)
 _sig("lmd_max_displacement2", _INT, _I64, _VP, _VP, _VP, _VP, _VP, _VP)
 _sig("lmd_lc_tpi_ev_slots", _I64, _I64, _INT)
 _sig("lmd_force_lc_particles", _INT, C.POINTER(Grid), C.POINTER(LJ), _INT, _INT, _VP, _I64, _VP,

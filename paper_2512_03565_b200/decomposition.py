@@ -209,7 +209,58 @@ class BrickDecomposition:
             ghosts = self._stage_move(st, pos)
             pos = torch.cat([pos, ghosts])
         self.n_ghost = pos.shape[0] - owned_pos.shape[0]
+        self._prepare_fast(owned_pos.shape[0], dev)
         return pos[owned_pos.shape[0]:]
+
+    def _prepare_fast(self, n_owned: int, dev) -> None:
+        """Persistent buffers for exchange_positions: int32 send lists, send
+        buffers, and the row-major ghost block [stage 0 | stage 1 | stage 2]."""
+        self._n_owned = n_owned
+        self._ghost_rows = None
+        if dev.type != "cuda":
+            return
+        self._ghost_rows = torch.empty((max(self.n_ghost, 1), 3), dtype=torch.float64,
+                                       device=dev)
+        off = 0
+        for st in self.stages:
+            st.idx32 = [st.send_idx[d].to(torch.int32).contiguous() for d in (0, 1)]
+            local = self.nranks == 1 or self.grid[st.axis] == 1
+            st.local = local
+            if local:     # arrival order: my down-send, then my up-send
+                c0, c1 = st.idx32[0].numel(), st.idx32[1].numel()
+                st.dst = [self._ghost_rows[off:off + c0], self._ghost_rows[off + c0:off + c0 + c1]]
+                off += c0 + c1
+            else:         # arrival order: from the upper neighbour (slot 1), then the lower
+                r1, r0 = st.recv_count[1], st.recv_count[0]
+                st.recv = [self._ghost_rows[off + r1:off + r1 + r0], self._ghost_rows[off:off + r1]]
+                st.sendbuf = [torch.empty((max(st.idx32[d].numel(), 1), 3), dtype=torch.float64,
+                                          device=dev) for d in (0, 1)]
+                off += r0 + r1
+
+    def exchange_positions(self, x: torch.Tensor, y: torch.Tensor,
+                           z: torch.Tensor) -> torch.Tensor:
+        """``exchange`` for owned SoA positions on the device, without
+        concatenations: one fused pack kernel per stage and direction
+        (lmd_ghost_pack: gather + exact image shift), received blocks land in
+        their slot of a persistent row-major ghost buffer (same order and
+        values as ``exchange``).  Returns the (n_ghost, 3) ghost rows."""
+        from . import _native as N
+        g = self._ghost_rows
+        s = N.stream()
+        for st in self.stages:
+            outs = st.dst if st.local else st.sendbuf
+            for d in (0, 1):
+                cnt = st.idx32[d].numel()
+                if cnt:
+                    N.call("lmd_ghost_pack", cnt, N.ptr(st.idx32[d]), self._n_owned, N.ptr(x),
+                           N.ptr(y), N.ptr(z), N.ptr(g), st.axis, float(st.shift[d]),
+                           N.ptr(outs[d]), s)
+            if not st.local:
+                sends = [(st.peer[0], st.sendbuf[0][:st.idx32[0].numel()]),
+                         (st.peer[1], st.sendbuf[1][:st.idx32[1].numel()])]
+                recvs = [(st.peer[0], st.recv[0]), (st.peer[1], st.recv[1])]
+                self._pair_exchange(st, sends, recvs)
+        return g[:self.n_ghost]
 
     def _exchange_counts(self, st: _Stage, sendcounts: list, dev) -> list:
         if self.nranks == 1 or self.grid[st.axis] == 1:

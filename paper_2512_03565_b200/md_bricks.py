@@ -168,10 +168,10 @@ def run_md_bricks(owned: ParticleBuffer, dec, params, iterations: int, vector_wi
             epoch += 1
             rebuilds += 1
         else:
-            g = dec.exchange(_positions(owned))
-            ghosts.pos_x.copy_(g[:, 0])
-            ghosts.pos_y.copy_(g[:, 1])
-            ghosts.pos_z.copy_(g[:, 2])
+            rows = dec.exchange_positions(owned.pos_x, owned.pos_y, owned.pos_z)
+            ghosts.pos_x.copy_(rows[:, 0])
+            ghosts.pos_y.copy_(rows[:, 1])
+            ghosts.pos_z.copy_(rows[:, 2])
         if slot[1] != epoch:
             cont.rebuild(owned, ghosts)
             slot[1] = epoch

@@ -139,7 +139,7 @@ class VerletListContainer:
         self.steps_since_rebuild = 0
         self.structure_version += 1
 
-    def _load_positions(self, d, ghosts=None) -> None:
+    def _load_positions(self, d, ghosts=None, ghost_rows=None) -> None:
         """Current positions into pos4 and the SoA copies, in rebuild-time order:
         owned via the cell permutation; images either moved with their owners
         (shift codes) or, for an external ghost layer, gathered from it."""
@@ -159,6 +159,12 @@ class VerletListContainer:
             N.call("lmd_gather_pos4", n, N.ptr(self._perm), N.ptr(d.pos_x), N.ptr(d.pos_y),
                    N.ptr(d.pos_z), None, float(OWNED), N.ptr(self._pos4), s)
         if not nh:
+            return
+        if ghost_rows is not None:
+            if soa:
+                raise ConfigurationError("row-major ghosts with SoA gathers are not supported")
+            N.call("lmd_gather_pos4_rows", nh, N.ptr(self._hperm), N.ptr(ghost_rows), float(HALO),
+                   N.ptr(self._pos4[n:]), s)
             return
         if ghosts is not None:
             if soa:
@@ -187,6 +193,9 @@ class VerletListContainer:
         if self._external_halo:
             if halo is None or len(halo) != self.n_halo:
                 raise ConfigurationError("refresh needs the same ghost layer as the rebuild")
+            if isinstance(halo, torch.Tensor):    # row-major (n_halo, 3) ghost positions
+                self._load_positions(device_soa(owned), None, ghost_rows=halo)
+                return
             self._load_positions(device_soa(owned), device_soa(halo, self._pos4.device))
             return
         self._load_positions(device_soa(owned))
