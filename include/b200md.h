@@ -269,6 +269,52 @@ int lmd_vl_build(const lmd_grid* g, double rl2, int newton3, int pattern, int64_
  * particles (or clusters for the i-cluster lists). */
 int lmd_vl_align(int pattern, int64_t n_units, int window, const int64_t* tile_off,
                  const int32_t* kmax, int32_t* nbr, void* stream);
+/* Optional pass after lmd_vl_build for the SoA gathers (lmd_force_vl with
+ * soa != NULL, row stride a multiple of 16 doubles so x[j], y[j], z[j] share
+ * bank pair j & 15): permutes every lane's own slot sequence so that the
+ * lanes of each half-warp gather from distinct 8-byte bank pairs step by
+ * step (csrc/vl.cu vl_bank_kernel); slots a lane leaves idle become -1.
+ * Same entries per lane and the same step count, so forces, pair counts and
+ * statistics are unchanged up to summation order.  cap_steps = the build's
+ * per-tile capacity (bounds the shared-memory workspace,
+ * lmd_vl_bank_smem_per_warp bytes per tile, at most 200 KB). */
+size_t lmd_vl_bank_smem_per_warp(int32_t cap_steps);
+int lmd_vl_bank_schedule(int pattern, int64_t n_units, int32_t sentinel, int rounds,
+                         int32_t cap_steps, const int64_t* tile_off, const int32_t* kmax,
+                         int32_t* nbr, void* stream);
+/* Staged Verlet lists (v_by_one, full lists; csrc/vl.cu).  Owned particles
+ * form groups of group_size (128 / 256 / 512) consecutive backing slots, one
+ * block each; a group's candidates lie in 18 contiguous index runs (owned and
+ * image backing x 3 x 3 (dy, dz) cell rows), which the force kernel copies
+ * into shared memory with TMA bulk copies.  lmd_vl_groups writes one record
+ * of 64 int32 per group (csrc/vl_common.cuh: run starts, lengths, local
+ * offsets, S = staged rows, first image row, overflow flag) from the build
+ * positions and cell tables; smax[0] = largest S among groups with
+ * S <= capacity, smax[1] = groups over capacity (those gather their global
+ * indices from the SoA arrays).  lmd_vl_build_staged = lmd_vl_build for
+ * V_BY_ONE writing each entry as the local row of its group's copy; pads
+ * are -1.  lmd_vl_staged_capacity(group_size) = the largest S a group
+ * stages (pass it as `capacity`).  lmd_force_vl_staged: newton3 0 or 2 as
+ * lmd_force_vl; soa = (3, stride) rows (stride % 16 == 0, 128-B aligned)
+ * whose row `sentinel` is a far-away position (idle slots of global-gather
+ * groups); ev_scratch holds 2 * ceil(n_owned / 32) doubles. */
+int32_t lmd_vl_staged_capacity(int32_t group_size);
+int lmd_vl_groups(const lmd_grid* g, int64_t n_owned, int32_t group_size, int32_t capacity,
+                  const double* pos4, const int32_t* o_start, const int32_t* o_count,
+                  const int32_t* h_start, const int32_t* h_count, int32_t* groups,
+                  int32_t* smax, void* stream);
+int lmd_vl_build_staged(const lmd_grid* g, double rl2, int newton3, int64_t n_owned,
+                        const double* pos4, const int32_t* o_start, const int32_t* o_count,
+                        const int32_t* h_start, const int32_t* h_count, int32_t group_size,
+                        const int32_t* groups, int32_t cap_steps, int32_t* count,
+                        int32_t* count_half, int64_t* tile_off, int32_t* kmax,
+                        int32_t* max_count, int32_t* nbr, void* stream);
+int lmd_force_vl_staged(int newton3, int flags, const lmd_lj* lj, int64_t n_owned,
+                        const double* pos4, const double* soa, int64_t stride, int32_t sentinel,
+                        int32_t group_size, const int32_t* groups,
+                        const int64_t* tile_off, const int32_t* kmax, const int32_t* nbr,
+                        const int32_t* out_perm, double* fx, double* fy, double* fz,
+                        double* ev_scratch, lmd_stats* stats, void* stream);
 /* i-cluster lists (csrc/vl_ci.cu), full lists only: each cell's owned
  * particles are cut into clusters of up to ci (2 or 4) consecutive backing
  * slots, cluster c = [cl_first[c], cl_first[c] + cl_len[c]); its list is the
@@ -412,6 +458,9 @@ int lmd_ghost_pack(int64_t count, const int32_t* idx, int64_t n_owned, const dou
 /* pos4[k] = (rows[perm[k]], own_value): gather row-major positions. */
 int lmd_gather_pos4_rows(int64_t n, const int32_t* perm, const double* rows, double own_value,
                          double* pos4, void* stream);
+/* The same rows gathered into SoA x, y, z (the VL container's SoA copies). */
+int lmd_gather_rows_soa(int64_t n, const int32_t* perm, const double* rows, double* x, double* y,
+                        double* z, void* stream);
 
 /* *out = max_k |r_k - ref_k|^2 with the reference's unfused (dx^2 + dy^2) +
  * dz^2 (containers.py:23-38, needs_rebuild); ref_xyz rows are (x, y, z). */

@@ -162,11 +162,21 @@ _sig("lmd_vl_build", _INT, C.POINTER(Grid), _D, _INT, _INT, _I64, _I32, _VP, _VP
 _sig("lmd_vl_ev_slots", _I64, _I64, _INT)
 _sig("lmd_ghost_pack", _INT, _I64, _VP, _I64, _VP, _VP, _VP, _VP, _INT, _D, _VP, _VP)
 _sig("lmd_gather_pos4_rows", _INT, _I64, _VP, _VP, _D, _VP, _VP)
+_sig("lmd_gather_rows_soa", _INT, _I64, _VP, _VP, _VP, _VP, _VP, _VP)
 _sig("lmd_max_displacement2", _INT, _I64, _VP, _VP, _VP, _VP, _VP, _VP)
 _sig("lmd_lc_tpi_ev_slots", _I64, _I64, _INT)
 _sig("lmd_force_lc_particles", _INT, C.POINTER(Grid), C.POINTER(LJ), _INT, _INT, _VP, _I64, _VP,
      _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP)
 _sig("lmd_vl_align", _INT, _INT, _I64, _INT, _VP, _VP, _VP, _VP)
+_sig("lmd_vl_bank_smem_per_warp", C.c_size_t, _I32)
+_sig("lmd_vl_groups", _INT, C.POINTER(Grid), _I64, _I32, _I32, _VP, _VP, _VP, _VP, _VP, _VP, _VP,
+     _VP)
+_sig("lmd_vl_build_staged", _INT, C.POINTER(Grid), _D, _INT, _I64, _VP, _VP, _VP, _VP, _VP, _I32,
+     _VP, _I32, _VP, _VP, _VP, _VP, _VP, _VP, _VP)
+_sig("lmd_vl_staged_capacity", _I32, _I32)
+_sig("lmd_force_vl_staged", _INT, _INT, _INT, C.POINTER(LJ), _I64, _VP, _VP, _I64, _I32, _I32, _VP,
+     _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP)
+_sig("lmd_vl_bank_schedule", _INT, _INT, _I64, _I32, _INT, _I32, _VP, _VP, _VP, _VP)
 _sig("lmd_vl_ci_build", _INT, C.POINTER(Grid), _D, _INT, _INT, _I64, _VP, _VP, _I32, _VP, _VP,
      _VP, _VP, _VP, _I32, _VP, _VP, _VP, _VP, _VP, _VP)
 _sig("lmd_vl_ci_ev_slots", _I64, _I64, _INT)

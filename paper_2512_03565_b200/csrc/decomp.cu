@@ -40,6 +40,17 @@ __global__ void gather_pos4_rows_kernel(int64_t n, const int32_t* __restrict__ p
   pos4[k] = make_double4(rows[3 * s], rows[3 * s + 1], rows[3 * s + 2], own_value);
 }
 
+__global__ void gather_rows_soa_kernel(int64_t n, const int32_t* __restrict__ perm,
+                                       const double* __restrict__ rows, double* __restrict__ x,
+                                       double* __restrict__ y, double* __restrict__ z) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int64_t s = perm ? perm[k] : k;
+  x[k] = rows[3 * s];
+  y[k] = rows[3 * s + 1];
+  z[k] = rows[3 * s + 2];
+}
+
 }  // namespace lmd
 
 using namespace lmd;
@@ -62,6 +73,15 @@ int lmd_gather_pos4_rows(int64_t n, const int32_t* perm, const double* rows, dou
   if (n <= 0) return LMD_OK;
   gather_pos4_rows_kernel<<<(unsigned)cdiv(n, 256), 256, 0, (cudaStream_t)stream>>>(
       n, perm, rows, own_value, reinterpret_cast<double4*>(pos4));
+  LMD_CHECK_LAUNCH();
+  return LMD_OK;
+}
+
+int lmd_gather_rows_soa(int64_t n, const int32_t* perm, const double* rows, double* x, double* y,
+                        double* z, void* stream) {
+  if (n <= 0) return LMD_OK;
+  gather_rows_soa_kernel<<<(unsigned)cdiv(n, 256), 256, 0, (cudaStream_t)stream>>>(n, perm, rows,
+                                                                                  x, y, z);
   LMD_CHECK_LAUNCH();
   return LMD_OK;
 }

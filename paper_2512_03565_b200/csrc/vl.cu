@@ -122,7 +122,8 @@ __global__ void vl_build_kernel(GridK g, int n, int ntiles, int newton3,
                                 int cap_steps, int32_t* __restrict__ count,
                                 int32_t* __restrict__ count_half,
                                 long long* __restrict__ toff, int32_t* __restrict__ kmax,
-                                int32_t* __restrict__ max_count, int32_t* __restrict__ nbr) {
+                                int32_t* __restrict__ max_count, int32_t* __restrict__ nbr,
+                                const int32_t* __restrict__ groups, int G) {
   constexpr int A = Pattern<P>::A, B = Pattern<P>::B, pattern = P;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int t = i / A, il = i - t * A;
@@ -146,6 +147,12 @@ __global__ void vl_build_kernel(GridK g, int n, int ntiles, int newton3,
               if (c == 0) continue;
               int j = vs[nl];
               const int e = j + c;
+              // staged lists: index into the group's shared-memory copy of
+              // this (view, dy, dz) run (vl_group_kernel); 0 for global
+              const int roff =
+                  groups ? __ldg(groups + (long long)(i / G) * kGroupRec + kGrpOff + view * 9 +
+                                 (dz + 1) * 3 + (dy + 1))
+                         : 0;
               if (!view && newton3) j = max(j, i + 1);
               // hits of up to 32 consecutive candidates are collected as a
               // bit mask and emitted afterwards in ascending order, so the
@@ -174,7 +181,8 @@ __global__ void vl_build_kernel(GridK g, int n, int ntiles, int newton3,
                   kh += view || jj > i;
                   if (k < cap) {
                     const int st = k / B, l = lane_of(pattern, il, k % B);
-                    out[(long long)(st / kChunk) * (32 * kChunk) + l * kChunk + st % kChunk] = jj;
+                    out[(long long)(st / kChunk) * (32 * kChunk) + l * kChunk + st % kChunk] =
+                        jj + roff;
                   }
                   ++k;
                 }
@@ -204,6 +212,66 @@ __global__ void vl_build_kernel(GridK g, int n, int ntiles, int newton3,
   int w = m;
   for (int off = 16; off > 0; off >>= 1) w = max(w, __shfl_xor_sync(0xffffffffu, w, off));
   if ((threadIdx.x & 31) == 0 && w > 0) atomicMax(max_count, w);
+}
+
+// Group run table for the staged lists (one warp per group, lane r < 18
+// scans run r's cells for its first and last particle).
+__global__ void vl_group_kernel(GridK g, int n, int G, int scap, const double* __restrict__ pos4,
+                                const int32_t* __restrict__ os, const int32_t* __restrict__ oc,
+                                const int32_t* __restrict__ hs, const int32_t* __restrict__ hc,
+                                int32_t* __restrict__ groups, int32_t* __restrict__ smax) {
+  const int lane = threadIdx.x & 31;
+  const long long grp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long ngroups = ((long long)n + G - 1) / G;
+  if (grp >= ngroups) return;
+  const long long i0 = grp * G, i1 = min((long long)n, i0 + G) - 1;
+  const long long lo = cell_of_owned(ld_pos4(pos4, i0), g.lo0, g.lo1, g.lo2, g.cl0, g.cl1, g.cl2,
+                                     g.d0, g.d1, g.d2, g.t0, g.t1);
+  const long long hi = cell_of_owned(ld_pos4(pos4, i1), g.lo0, g.lo1, g.lo2, g.cl0, g.cl1, g.cl2,
+                                     g.d0, g.d1, g.d2, g.t0, g.t1);
+  int start = 0, len = 0;
+  if (lane < kGroupRuns) {
+    const int view = lane / 9, q = lane % 9, dz = q / 3 - 1, dy = q % 3 - 1;
+    const int32_t* vs = view ? hs : os;
+    const int32_t* vc = view ? hc : oc;
+    const long long off = g.t0 * (dy + g.t1 * dz);
+    int first = -1, last = -1;
+    for (long long c = lo - 1 + off; c <= hi + 1 + off; ++c) {
+      const int k = vc[c];
+      if (k) {
+        if (first < 0) first = vs[c];
+        last = vs[c] + k;
+      }
+    }
+    if (first >= 0) {
+      start = first & ~1;                 // 16-B aligned bulk copies
+      len = (last - start + 1) & ~1;
+    }
+  }
+  // exclusive scan of the run lengths -> shared-memory bases
+  int incl = len;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += v;
+  }
+  const int base = incl - len;
+  const int S = __shfl_sync(0xffffffffu, incl, 31);
+  const int halo_base = __shfl_sync(0xffffffffu, base, 9);
+  const bool glob = S > scap;
+  int32_t* rec = groups + grp * kGroupRec;
+  if (lane < kGroupRuns) {
+    rec[kGrpStart + lane] = start;
+    rec[kGrpLen + lane] = len;
+    rec[kGrpOff + lane] = glob ? 0 : base - start;
+  }
+  if (lane == 0) {
+    rec[kGrpS] = S;
+    rec[kGrpHalo] = glob ? n : halo_base;
+    rec[kGrpGlobal] = glob ? 1 : 0;
+    atomicMax(smax, glob ? 0 : S);
+    if (glob) atomicAdd(smax + 1, 1);
+  }
 }
 
 // Line-aligned entry order (optional pass after the build).  The force
@@ -270,6 +338,129 @@ __global__ void __launch_bounds__(32 * kVLWarps)
   }
 }
 
+// Bank-conflict-aware entry order (optional pass after the build, for the
+// SoA gathers).  Measured (tools/bank_probe.cu, profiles/r01_bank_probe.jsonl):
+// a warp's 64-bit gather -- shared memory or L1-resident global alike -- is
+// served per half-warp, costing the largest number of lanes of that half
+// that hit one 8-byte bank pair (16 pairs per 128 B), i.e. 2 cycles when
+// conflict-free and ~6-8.5 for random indices.  With SoA arrays whose rows
+// start on 128 B, x[j], y[j], z[j] sit in bank pair j & 15.  This pass
+// permutes every lane's own slot sequence so that, step by step, the lanes
+// of each half-warp gather from distinct bank pairs:
+//   * each lane buckets its entries by bank pair (shared memory);
+//   * at step s, lane l of a half first takes its Latin-square pair
+//     (l + s) & 15 if it still holds one (conflict-free by construction);
+//     then `rounds` proposal rounds: a lane proposes the first pair, rotated
+//     to start at (l + s) & 15, that it holds and no winner of its half has
+//     taken; the lowest proposing lane wins (prefix OR over the half);
+//   * a lane that lost every round idles (slot -1) if it can still finish
+//     within the tile's T steps, otherwise it takes a conflicting entry.
+// Entries never leave their lane, the step count T is unchanged, every
+// choice is a function of warp-uniform state: the list is a deterministic
+// permutation of the build's.  Idle slots are -1 (ld_j<1> skips the load).
+__device__ __forceinline__ int first_rot16(unsigned m, int k) {
+  const unsigned r = ((m >> k) | (m << (16 - k))) & 0xffffu;
+  return r ? ((__ffs(r) - 1 + k) & 15) : -1;
+}
+
+__global__ void vl_bank_kernel(int ntiles, int B, int32_t sentinel, int rounds, int tcap,
+                               const long long* __restrict__ toff,
+                               const int32_t* __restrict__ kmax, int32_t* __restrict__ nbr) {
+  extern __shared__ int32_t bank_sm[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int t = blockIdx.x * nw + w;
+  if (t >= ntiles) return;  // warp-uniform
+  const int T = kmax[t] / B;
+  int32_t* cur = bank_sm + (size_t)w * (64 * 16 + (size_t)tcap * 32);
+  int32_t* cnt = cur + 16 * 32;
+  int32_t* ent = cnt + 16 * 32;
+  int4* base4 = reinterpret_cast<int4*>(nbr + toff[t]);
+#pragma unroll
+  for (int b = 0; b < 16; ++b) cnt[b * 32 + lane] = 0;
+  int n = 0;
+  for (int c = 0; c < T / kChunk; ++c) {
+    const int4 v = base4[c * 32 + lane];
+    const int j[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (j[u] != sentinel && j[u] >= 0) {
+        ++cnt[(j[u] & 15) * 32 + lane];
+        ++n;
+      }
+  }
+  unsigned avail = 0u;
+  int acc = 0;
+#pragma unroll
+  for (int b = 0; b < 16; ++b) {
+    const int c = cnt[b * 32 + lane];
+    cur[b * 32 + lane] = acc;
+    acc += c;
+    avail |= (c ? 1u : 0u) << b;
+  }
+  for (int c = 0; c < T / kChunk; ++c) {
+    const int4 v = base4[c * 32 + lane];
+    const int j[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (j[u] != sentinel && j[u] >= 0) {
+        const int p = cur[(j[u] & 15) * 32 + lane]++;
+        ent[p * 32 + lane] = j[u];
+      }
+  }
+  // cursors back to the bucket starts
+#pragma unroll
+  for (int b = 0; b < 16; ++b) cur[b * 32 + lane] -= cnt[b * 32 + lane];
+  const int half = lane >> 4, hl = lane & 15;
+  int lrem = n;
+  for (int s0 = 0; s0 < T; s0 += kChunk) {
+  int out[kChunk];
+#pragma unroll
+  for (int u = 0; u < kChunk; ++u) {
+    const int s = s0 + u;
+    const int rot = (hl + s) & 15;
+    int pick = -1;
+    bool pending = lrem > 0;
+    // the lane's own bank pair of this step (a Latin square: conflict-free)
+    if (pending && ((avail >> rot) & 1u)) {
+      pick = rot;
+      pending = false;
+    }
+    unsigned usedw = __reduce_or_sync(0xffffffffu, pick >= 0 ? 1u << (pick + 16 * half) : 0u);
+    for (int r = 0; r < rounds; ++r) {
+      const unsigned used = (usedw >> (16 * half)) & 0xffffu;
+      const int b = pending ? first_rot16(avail & ~used, rot) : -1;
+      if (!__any_sync(0xffffffffu, b >= 0)) break;
+      // lowest lane of the half proposing a pair wins it: prefix OR
+      const unsigned p = b >= 0 ? 1u << (b + 16 * half) : 0u;
+      unsigned incl = p;
+#pragma unroll
+      for (int d = 1; d < 16; d <<= 1) {
+        const unsigned v = __shfl_up_sync(0xffffffffu, incl, d);
+        if (hl >= d) incl |= v;
+      }
+      unsigned lower = __shfl_up_sync(0xffffffffu, incl, 1);
+      if (hl == 0) lower = 0u;
+      const bool win = p != 0u && !(lower & p);
+      usedw |= __reduce_or_sync(0xffffffffu, win ? p : 0u);
+      if (win) {
+        pick = b;
+        pending = false;
+      }
+    }
+    if (pending && T - s <= lrem) pick = first_rot16(avail, rot);  // no slack left
+    int j = -1;
+    if (pick >= 0) {
+      const int p = cur[pick * 32 + lane]++;
+      j = ent[p * 32 + lane];
+      if (--cnt[pick * 32 + lane] == 0) avail &= ~(1u << pick);
+      --lrem;
+    }
+    out[u] = j;
+  }
+  base4[(s0 / kChunk) * 32 + lane] = make_int4(out[0], out[1], out[2], out[3]);
+  }
+}
+
 __global__ void fill_i32_kernel(int64_t n, int32_t v, int32_t* __restrict__ out) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
        k += (int64_t)gridDim.x * blockDim.x)
@@ -323,9 +514,15 @@ struct SoA {
 };
 
 // gather modes: 0 = 256-bit pos4 record, 1 = SoA x, y, z (64-bit each)
+// GM = 1: j < 0 is an idle slot of a bank-scheduled list (vl_bank_kernel):
+// no load (the lane drops out of the gather, so it adds no bank conflict),
+// a position far outside every cutoff.
 template <int GM>
 __device__ __forceinline__ double4 ld_j(const double* __restrict__ pos4, const SoA& q, int j) {
-  if (GM == 1) return make_double4(__ldg(q.x + j), __ldg(q.y + j), __ldg(q.z + j), 0.0);
+  if (GM == 1) {
+    if (j < 0) return make_double4(1.0e300, 1.0e300, 1.0e300, 0.0);
+    return make_double4(__ldg(q.x + j), __ldg(q.y + j), __ldg(q.z + j), 0.0);
+  }
   return ld_pos4(pos4, j);
 }
 
@@ -404,6 +601,255 @@ __global__ void __launch_bounds__(32 * kVLWarps, 8)
                                fz);
   flush_acc(a, lane, t < ntiles, EV, (long long)blockIdx.x * kVLWarps + (threadIdx.x >> 5), ev,
             stats);
+}
+
+// ------------------------------------------------------------ staged force
+// One block per group of G = 32 * W owned particles (W tiles, thread per i):
+// thread 0 arms an mbarrier and issues one TMA bulk copy per (run, axis) of
+// the SoA positions into shared memory (no register staging, no LSU
+// writeback), every warp then walks its tile's bank-scheduled local
+// indices with conflict-free 64-bit shared-memory loads.  Groups whose runs
+// exceed the capacity gather their global indices from the SoA arrays.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// rows per axis of the shared-memory copy, by group size; the last row is a
+// dummy far away (idle slots), so a group stages at most rows - 16 rows
+template <int W>
+struct StageRows {
+  static constexpr int value = W == 4 ? 2304 : (W == 8 ? 4096 : 7168);
+};
+static inline int stage_rows(int group_size) {
+  return group_size == 128 ? StageRows<4>::value
+                           : (group_size == 256 ? StageRows<8>::value : StageRows<16>::value);
+}
+
+// One list slot of the staged kernel, branch-free apart from the rare exact
+// re-evaluation near the cutoff: the LJ expression runs for every lane (the
+// warp would run it anyway whenever one lane hits) and is masked.
+// Four list slots of the staged kernel, branch-free: r2 is always the
+// reference's unfused expression (two FP64 instructions more than the FMA
+// form, but no near-cutoff re-evaluation branch), the cutoff test compares
+// bit patterns on the integer pipe, the LJ expression runs for every lane
+// (the warp would run it anyway whenever one lane hits) and the
+// accumulation is predicated.
+template <bool EV, int N3>
+__device__ __forceinline__ void staged_pairs4(const double4& pi, const double* xj,
+                                              const double* yj, const double* zj,
+                                              const unsigned* j, int hb, const LJK& k, Acc& a) {
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const double dx = pi.x - xj[u], dy = pi.y - yj[u], dz = pi.z - zj[u];
+    const double r2 = r2_exact(dx, dy, dz);
+    const long long b = __double_as_longlong(r2);
+    const bool in = b < k.rc2_bits;
+    const bool zero = b == 0;
+    a.overlap |= (in && zero);
+    const bool hit = in && !zero;
+    const double inv = rcp_fast(r2);
+    const double s2 = k.sigma2 * inv;
+    const double s6 = s2 * s2 * s2;
+    double f = (s6 * inv) * fma(k.eps48, s6, -k.eps24);
+    f = hit ? f : 0.0;  // one select; the accumulation then runs unpredicated
+    a.ax = fma(f, dx, a.ax);
+    a.ay = fma(f, dy, a.ay);
+    a.az = fma(f, dz, a.az);
+    if (EV) {
+      const double hs = hit ? 0.5 * s6 : 0.0;
+      a.e = fma(hs, fma(k.eps4, s6, -k.eps4), a.e);
+      a.v = fma(0.5 * f, r2, a.v);
+    }
+    a.pairs += in;
+    if (N3 == 2) a.halo += (in && (int)j[u] >= hb);
+  }
+}
+
+#ifndef LMD_STAGED_PREFETCH
+#define LMD_STAGED_PREFETCH 4
+#endif
+#ifndef LMD_STAGED_BATCH
+#define LMD_STAGED_BATCH 2
+#endif
+constexpr int kStagedPrefetch = LMD_STAGED_PREFETCH;  // index chunks in flight
+constexpr int kStagedBatch = LMD_STAGED_BATCH;        // chunks evaluated together
+
+template <bool EV, int N3, int ROWS, bool STAGED>
+__device__ __forceinline__ void vl_staged_tile(int t, int lane, int n_owned, int hb,
+                                               unsigned dummy, unsigned long long* bar,
+                                               const int32_t* __restrict__ out_perm,
+                                               const double* __restrict__ pos4,
+                                               const double* __restrict__ xs,
+                                               const double* __restrict__ ys,
+                                               const double* __restrict__ zs,
+                                               const long long* __restrict__ toff,
+                                               const int32_t* __restrict__ kmax,
+                                               const int32_t* __restrict__ nbr, const LJK& k,
+                                               Acc& a, double* __restrict__ fx,
+                                               double* __restrict__ fy, double* __restrict__ fz) {
+  const int i = t * 32 + lane;
+  const bool iact = i < n_owned;
+  const int4* chunks = reinterpret_cast<const int4*>(nbr + toff[t]) + lane;
+  const int nchunks = kmax[t] / kChunk;
+  // the tile's whole index list towards L2 first (one bulk prefetch), so the
+  // streamed chunk loads below see L2, not HBM, latency
+  if (lane == 0 && nchunks > 0)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(chunks),
+                 "r"((unsigned)nchunks * 512u)
+                 : "memory");
+  const double4 pi = ld_pos4(pos4, iact ? i : 0);
+  // Index chunks stream kStagedPrefetch chunks ahead in a register ring
+  // addressed statically (the loop is unrolled by the ring size, so no
+  // register move waits on an outstanding load).  Slots are evaluated in
+  // batches of kStagedBatch chunks; the positions of batch b + 1 are loaded
+  // while batch b is evaluated.
+  constexpr int R = kStagedPrefetch, NB = kStagedBatch, NS = 4 * NB;
+  static_assert(R % NB == 0, "ring must hold whole batches");
+  int4 ring[R];
+#pragma unroll
+  for (int d = 0; d < R; ++d)
+    ring[d] = d < nchunks ? __ldg(chunks + (long long)d * 32) : make_int4(-1, -1, -1, -1);
+  if (bar) mbar_wait(bar, 0);  // the staged rows have landed
+  auto load_batch = [&](int d0, unsigned* j, double* x, double* y, double* z) {
+#pragma unroll
+    for (int q = 0; q < NB; ++q) {
+      const int4 v = ring[(d0 + q) % R];
+      // idle slots (-1) read the dummy row
+      j[4 * q + 0] = min((unsigned)v.x, dummy);
+      j[4 * q + 1] = min((unsigned)v.y, dummy);
+      j[4 * q + 2] = min((unsigned)v.z, dummy);
+      j[4 * q + 3] = min((unsigned)v.w, dummy);
+    }
+#pragma unroll
+    for (int u = 0; u < NS; ++u) {
+      if (STAGED) {
+        x[u] = xs[j[u]];
+        y[u] = xs[j[u] + ROWS];
+        z[u] = xs[j[u] + 2 * ROWS];
+      } else {
+        x[u] = __ldg(xs + j[u]);
+        y[u] = __ldg(ys + j[u]);
+        z[u] = __ldg(zs + j[u]);
+      }
+    }
+  };
+  unsigned j[NS];
+  double x[NS], y[NS], z[NS];
+  load_batch(0, j, x, y, z);
+  for (int c0 = 0; c0 < nchunks; c0 += R) {
+#pragma unroll
+    for (int d = 0; d < R; d += NB) {
+      const int c = c0 + d;
+      if (c < nchunks) {
+        // the batch's ring slots are consumed (positions in x, y, z): refill
+#pragma unroll
+        for (int q = 0; q < NB; ++q)
+          ring[d + q] = c + q + R < nchunks
+                            ? __ldg(chunks + (long long)(c + q + R) * 32)
+                            : make_int4(-1, -1, -1, -1);
+        unsigned jn[NS];
+        double xn[NS], yn[NS], zn[NS];
+        load_batch((d + NB) % R, jn, xn, yn, zn);
+#pragma unroll
+        for (int q = 0; q < NB; ++q)
+          staged_pairs4<EV, N3>(pi, x + 4 * q, y + 4 * q, z + 4 * q, j + 4 * q, hb, k, a);
+#pragma unroll
+        for (int u = 0; u < NS; ++u) {
+          j[u] = jn[u];
+          x[u] = xn[u];
+          y[u] = yn[u];
+          z[u] = zn[u];
+        }
+      }
+    }
+  }
+  if (iact) {
+    const int o = out_perm ? out_perm[i] : i;
+    fx[o] = a.ax;
+    fy[o] = a.ay;
+    fz[o] = a.az;
+  }
+}
+
+// 16 warps per SM (shared memory bounds it): up to 128 registers per thread
+template <bool EV, int N3, int W>
+__global__ void __launch_bounds__(32 * W, 16 / W)
+    vl_staged_kernel(int n_owned, int ntiles, int sentinel, const int32_t* __restrict__ out_perm,
+                     const double* __restrict__ pos4, SoA q, const int32_t* __restrict__ groups,
+                     const long long* __restrict__ toff, const int32_t* __restrict__ kmax,
+                     const int32_t* __restrict__ nbr, LJK k, double* __restrict__ fx,
+                     double* __restrict__ fy, double* __restrict__ fz, double* __restrict__ ev,
+                     lmd_stats* __restrict__ stats, int dbg) {
+  constexpr int ROWS = StageRows<W>::value;
+  extern __shared__ __align__(128) double st_sm[];
+  double* xs = st_sm;  // y at + ROWS, z at + 2 ROWS
+  __shared__ unsigned long long bar;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int32_t* rec = groups + (long long)blockIdx.x * kGroupRec;
+  const bool glob = rec[kGrpGlobal] != 0;
+  const int hb = rec[kGrpHalo];
+  if (!glob && !(dbg & 2)) {
+    if (threadIdx.x == 0) mbar_init(&bar, 1);
+    if (threadIdx.x == 32 % (32 * W)) {
+      xs[ROWS - 1] = 1.0e30;
+      xs[2 * ROWS - 1] = 1.0e30;
+      xs[3 * ROWS - 1] = 1.0e30;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      mbar_expect_tx(&bar, (unsigned)rec[kGrpS] * 3u * 8u);
+      for (int r = 0; r < kGroupRuns; ++r) {
+        const int len = rec[kGrpLen + r];
+        if (!len) continue;
+        const int st = rec[kGrpStart + r];
+        const int base = st + rec[kGrpOff + r];
+        bulk_g2s(xs + base, q.x + st, (unsigned)len * 8u, &bar);
+        bulk_g2s(xs + ROWS + base, q.y + st, (unsigned)len * 8u, &bar);
+        bulk_g2s(xs + 2 * ROWS + base, q.z + st, (unsigned)len * 8u, &bar);
+      }
+    }
+  }
+  const int t = blockIdx.x * W + w;
+  if (t >= ntiles) return;  // warp-uniform; no block barrier follows
+  if (dbg & 1) {            // timing probe: staging only
+    if (!glob && !(dbg & 2)) mbar_wait(&bar, 0);
+    return;
+  }
+  Acc a = {0.0, 0.0, 0.0, 0.0, 0.0, 0, 0, 0};
+  if (glob)
+    vl_staged_tile<EV, N3, ROWS, false>(t, lane, n_owned, hb, (unsigned)sentinel, nullptr,
+                                        out_perm, pos4,
+                                        q.x, q.y, q.z, toff, kmax, nbr, k, a, fx, fy, fz);
+  else
+    vl_staged_tile<EV, N3, ROWS, true>(t, lane, n_owned, hb, (unsigned)(ROWS - 1),
+                                       (dbg & 2) ? nullptr : &bar, out_perm,
+                                       pos4, xs, xs, xs, toff, kmax, nbr, k, a, fx, fy, fz);
+  flush_acc(a, lane, true, EV, t, ev, stats);
 }
 
 __global__ void vl_stats_kernel(int n, int a, int b, const int32_t* __restrict__ count,
@@ -506,11 +952,12 @@ int lmd_vl_fill(const lmd_grid* g, double rl2, int newton3, int pattern, int64_t
   return LMD_OK;
 }
 
-int lmd_vl_build(const lmd_grid* g, double rl2, int newton3, int pattern, int64_t n_owned,
-                 int32_t sentinel, const double* pos4, const int32_t* o_start,
-                 const int32_t* o_count, const int32_t* h_start, const int32_t* h_count,
-                 int32_t cap_steps, int32_t* count, int32_t* count_half, int64_t* tile_off,
-                 int32_t* kmax, int32_t* max_count, int32_t* nbr, void* stream) {
+static int vl_build_impl(const lmd_grid* g, double rl2, int newton3, int pattern, int64_t n_owned,
+                         int32_t sentinel, const double* pos4, const int32_t* o_start,
+                         const int32_t* o_count, const int32_t* h_start, const int32_t* h_count,
+                         int32_t cap_steps, int32_t* count, int32_t* count_half,
+                         int64_t* tile_off, int32_t* kmax, int32_t* max_count, int32_t* nbr,
+                         const int32_t* staged_groups, int staged_G, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e = cudaMemsetAsync(max_count, 0, sizeof(int32_t), s);
   if (e != cudaSuccess) return set_cuda_error(e);
@@ -519,11 +966,14 @@ int lmd_vl_build(const lmd_grid* g, double rl2, int newton3, int pattern, int64_
   const int A = pattern_A(pattern), B = pattern_B(pattern);
   const int64_t ntiles = cdiv(n_owned, A);
   const unsigned blocks = (unsigned)cdiv(ntiles * A, 128);
+  const int32_t* groups = staged_groups;
+  const int G = staged_G;
 #define LMD_VLB(P)                                                                             \
   vl_build_kernel<P><<<blocks, 128, 0, s>>>(make_gridk(g), (int)n_owned, (int)ntiles, newton3, \
                                             rl2, sentinel, pos4, o_start, o_count, h_start,    \
                                             h_count, cap_steps, count, count_half,             \
-                                            (long long*)tile_off, kmax, max_count, nbr)
+                                            (long long*)tile_off, kmax, max_count, nbr,        \
+                                            groups, G)
   switch (pattern) {
     case LMD_ONE_BY_V: LMD_VLB(LMD_ONE_BY_V); break;
     case LMD_V_BY_ONE: LMD_VLB(LMD_V_BY_ONE); break;
@@ -534,6 +984,28 @@ int lmd_vl_build(const lmd_grid* g, double rl2, int newton3, int pattern, int64_
 #undef LMD_VLB
   LMD_CHECK_LAUNCH();
   return LMD_OK;
+}
+
+int lmd_vl_build(const lmd_grid* g, double rl2, int newton3, int pattern, int64_t n_owned,
+                 int32_t sentinel, const double* pos4, const int32_t* o_start,
+                 const int32_t* o_count, const int32_t* h_start, const int32_t* h_count,
+                 int32_t cap_steps, int32_t* count, int32_t* count_half, int64_t* tile_off,
+                 int32_t* kmax, int32_t* max_count, int32_t* nbr, void* stream) {
+  return vl_build_impl(g, rl2, newton3, pattern, n_owned, sentinel, pos4, o_start, o_count,
+                       h_start, h_count, cap_steps, count, count_half, tile_off, kmax, max_count,
+                       nbr, nullptr, 0, stream);
+}
+
+int lmd_vl_build_staged(const lmd_grid* g, double rl2, int newton3, int64_t n_owned,
+                        const double* pos4, const int32_t* o_start, const int32_t* o_count,
+                        const int32_t* h_start, const int32_t* h_count, int32_t group_size,
+                        const int32_t* groups, int32_t cap_steps, int32_t* count,
+                        int32_t* count_half, int64_t* tile_off, int32_t* kmax,
+                        int32_t* max_count, int32_t* nbr, void* stream) {
+  if (group_size <= 0 || group_size % 32) return LMD_ERR_CONFIG;
+  return vl_build_impl(g, rl2, newton3, LMD_V_BY_ONE, n_owned, -1, pos4, o_start, o_count,
+                       h_start, h_count, cap_steps, count, count_half, tile_off, kmax, max_count,
+                       nbr, groups, group_size, stream);
 }
 
 int lmd_vl_align(int pattern, int64_t n_units, int window, const int64_t* tile_off,
@@ -549,6 +1021,32 @@ int lmd_vl_align(int pattern, int64_t n_units, int window, const int64_t* tile_o
     case 32: vl_align_kernel<32><<<blocks, 32 * kVLWarps, 0, s>>>((int)ntiles, B, (const long long*)tile_off, kmax, nbr); break;
     default: return LMD_ERR_CONFIG;
   }
+  LMD_CHECK_LAUNCH();
+  return LMD_OK;
+}
+
+size_t lmd_vl_bank_smem_per_warp(int32_t cap_steps) {
+  return (size_t)(64 * 16 + (size_t)cap_steps * 32) * sizeof(int32_t);
+}
+
+int lmd_vl_bank_schedule(int pattern, int64_t n_units, int32_t sentinel, int rounds,
+                         int32_t cap_steps, const int64_t* tile_off, const int32_t* kmax,
+                         int32_t* nbr, void* stream) {
+  if (n_units <= 0) return LMD_OK;
+  if (rounds < 1 || rounds > 16 || cap_steps <= 0 || cap_steps % kChunk) return LMD_ERR_CONFIG;
+  const int B = pattern_B(pattern);
+  const int64_t ntiles = cdiv(n_units, pattern_A(pattern));
+  const size_t per_warp = lmd_vl_bank_smem_per_warp(cap_steps);
+  const size_t budget = 200 * 1024;
+  if (per_warp > budget) return LMD_ERR_CONFIG;
+  int nw = (int)(96 * 1024 / per_warp);
+  nw = nw < 1 ? 1 : (nw > 8 ? 8 : nw);
+  const size_t smem = per_warp * nw;
+  cudaError_t e = cudaFuncSetAttribute(vl_bank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return set_cuda_error(e);
+  vl_bank_kernel<<<(unsigned)cdiv(ntiles, nw), 32 * nw, smem, (cudaStream_t)stream>>>(
+      (int)ntiles, B, sentinel, rounds, cap_steps, (const long long*)tile_off, kmax, nbr);
   LMD_CHECK_LAUNCH();
   return LMD_OK;
 }
@@ -633,6 +1131,80 @@ int lmd_force_vl(int pattern, int newton3, int flags, const lmd_lj* lj, int64_t 
     const int64_t slots = cdiv(ntiles, kVLWarps) * kVLWarps;
     return reduce_ev(ev_scratch, slots, stats, s);
   }
+  return LMD_OK;
+}
+
+int lmd_vl_groups(const lmd_grid* g, int64_t n_owned, int32_t group_size, int32_t capacity,
+                  const double* pos4, const int32_t* o_start, const int32_t* o_count,
+                  const int32_t* h_start, const int32_t* h_count, int32_t* groups,
+                  int32_t* smax, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (cudaMemsetAsync(smax, 0, 2 * sizeof(int32_t), s) != cudaSuccess)
+    return set_cuda_error(cudaGetLastError());
+  if (n_owned <= 0) return LMD_OK;
+  if (n_owned > 0x7fffffffLL || group_size <= 0 || group_size % 32 || capacity <= 0)
+    return LMD_ERR_CONFIG;
+  const int64_t ngroups = cdiv(n_owned, group_size);
+  vl_group_kernel<<<(unsigned)cdiv(ngroups * 32, 256), 256, 0, s>>>(
+      make_gridk(g), (int)n_owned, group_size, capacity, pos4, o_start, o_count, h_start, h_count,
+      groups, smax);
+  LMD_CHECK_LAUNCH();
+  return LMD_OK;
+}
+
+int32_t lmd_vl_staged_capacity(int32_t group_size) {
+  if (group_size != 128 && group_size != 256 && group_size != 512) return 0;
+  return stage_rows(group_size) - 16;
+}
+
+int lmd_force_vl_staged(int newton3, int flags, const lmd_lj* lj, int64_t n_owned,
+                        const double* pos4, const double* soa, int64_t stride, int32_t sentinel,
+                        int32_t group_size, const int32_t* groups,
+                        const int64_t* tile_off, const int32_t* kmax, const int32_t* nbr,
+                        const int32_t* out_perm, double* fx, double* fy, double* fz,
+                        double* ev_scratch, lmd_stats* stats, void* stream) {
+  if (n_owned <= 0) return LMD_OK;
+  if (newton3 != 0 && newton3 != 2) return LMD_ERR_CONFIG;
+  if (!soa || stride % 16 || sentinel < 0 || sentinel >= stride) return LMD_ERR_CONFIG;
+  if (group_size != 128 && group_size != 256 && group_size != 512) return LMD_ERR_CONFIG;
+  const LJK k = make_ljk(lj);
+  const int64_t ntiles = cdiv(n_owned, 32);
+  const int64_t ngroups = cdiv(n_owned, group_size);
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool ev = (flags & LMD_FLAG_ENERGY) != 0;
+  const SoA q = {soa, soa + stride, soa + 2 * stride};
+  const size_t smem = (size_t)stage_rows(group_size) * 3 * sizeof(double);
+#define LMD_VLS(EVB, N3B, W)                                                                   \
+  do {                                                                                         \
+    auto kern = vl_staged_kernel<EVB, N3B, W>;                                                 \
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+                                         (int)smem);                                          \
+    if (e != cudaSuccess) return set_cuda_error(e);                                            \
+    kern<<<(unsigned)ngroups, 32 * W, smem, s>>>((int)n_owned, (int)ntiles, (int)sentinel,     \
+                                                 out_perm, pos4, q, groups,                    \
+                                                 (const long long*)tile_off, kmax, nbr, k, fx, \
+                                                 fy, fz, ev_scratch, stats, (flags >> 8) & 3); \
+  } while (0)
+#define LMD_VLS_W(EVB, N3B)                                 \
+  do {                                                      \
+    switch (group_size) {                                   \
+      case 128: LMD_VLS(EVB, N3B, 4); break;                \
+      case 256: LMD_VLS(EVB, N3B, 8); break;                \
+      case 512: LMD_VLS(EVB, N3B, 16); break;               \
+      default: return LMD_ERR_CONFIG;                       \
+    }                                                       \
+  } while (0)
+  if (ev) {
+    if (newton3) LMD_VLS_W(true, 2);
+    else LMD_VLS_W(true, 0);
+  } else {
+    if (newton3) LMD_VLS_W(false, 2);
+    else LMD_VLS_W(false, 0);
+  }
+#undef LMD_VLS_W
+#undef LMD_VLS
+  LMD_CHECK_LAUNCH();
+  if (ev) return reduce_ev(ev_scratch, ntiles, stats, s);
   return LMD_OK;
 }
 

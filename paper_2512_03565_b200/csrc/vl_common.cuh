@@ -8,6 +8,20 @@ namespace lmd {
 constexpr int kVLWarps = 4;
 constexpr int kChunk = 4;  // fill steps per lane per 128-bit index load
 
+// Staged Verlet lists (v_by_one): a group of G consecutive owned particles
+// (G/32 tiles, one block) copies the SoA positions of its candidate runs
+// into shared memory.  Run r = view * 9 + (dz + 1) * 3 + (dy + 1) covers the
+// cells lin_lo - 1 + off .. lin_hi + 1 + off (off = t0 * (dy + t1 * dz)) of
+// the owned (view 0) or image (view 1) backing: one contiguous index range.
+// Per-group record of kGroupRec int32: run starts (even), lengths (even),
+// local-index offsets (base - start), then S, the first image-run local
+// index, and a flag (1: S > capacity, the group gathers from global memory
+// with global indices).
+constexpr int kGroupRec = 64;
+constexpr int kGrpStart = 0, kGrpLen = 18, kGrpOff = 36, kGrpS = 54, kGrpHalo = 55,
+              kGrpGlobal = 56;
+constexpr int kGroupRuns = 18;
+
 // lane holding (i_off = il, j_off = jo) of a pattern (inverse of Pattern<P>)
 __device__ __forceinline__ int lane_of(int pattern, int il, int jo) {
   switch (pattern) {

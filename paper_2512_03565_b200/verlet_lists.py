@@ -50,7 +50,18 @@ class VerletListContainer:
         self._stats_cache: dict = {}
         self._max_seen: dict = {}
         self.knobs = 0        # extra lmd_force_vl flags
-        self.use_soa = False  # True: gather SoA x, y, z instead of 256-bit pos4
+        # gathers: SoA x, y, z (three 64-bit loads, rows 128-B aligned) in a
+        # bank-conflict-aware entry order (bank_rounds proposal rounds per
+        # step, csrc/vl.cu vl_bank_kernel); use_soa=False: 256-bit pos4
+        # records in ascending order
+        self.use_soa = True
+        self.bank_rounds = 2
+        # staged lists (v_by_one, full lists): groups of staged_group owned
+        # particles copy their candidate runs into shared memory (TMA) and
+        # gather there; groups needing more than staged_capacity rows gather
+        # from global memory.  0 = off.
+        self.staged_group = 128
+        self._staging: dict = {}
         # particles per lane sharing one union list (csrc/vl_ci.cu) for full
         # lists; 1 = one list per particle (csrc/vl.cu)
         self.i_cluster = 1   # CI = 2 or 4 measured 2-3x slower
@@ -119,8 +130,7 @@ class VerletListContainer:
             self._halo_owner = torch.zeros(0, dtype=torch.int32, device=dev)
             self._halo_shift = torch.zeros(0, dtype=torch.int8, device=dev)
         if self.use_soa:
-            self._soa = torch.empty((3, n + nh + 1), dtype=torch.float64, device=dev)
-            self._soa[:, -1] = SENTINEL_POSITION
+            self._soa = self._new_soa(n + nh + 1, dev)
         else:
             self._soa = torch.empty((3, 1), dtype=torch.float64, device=dev)
         # every owned slot is written by the force kernel (Newton3 zeroes first)
@@ -132,6 +142,7 @@ class VerletListContainer:
         # rebuild-time positions, whatever the particles did since
         self._build_pos4 = self._pos4.clone()
         self._lists.clear()
+        self._staging.clear()
         self._counts.clear()
         self._clusters_cache.clear()
         self._stats_cache.clear()
@@ -147,10 +158,8 @@ class VerletListContainer:
         s = N.stream()
         soa = self.use_soa
         if soa:
-            if self._soa.shape[1] != n + nh + 1:   # SoA switched on after the rebuild
-                self._soa = torch.empty((3, n + nh + 1), dtype=torch.float64,
-                                        device=self._pos4.device)
-                self._soa[:, -1] = SENTINEL_POSITION
+            if self._soa.shape[1] < n + nh + 1:   # SoA switched on after the rebuild
+                self._soa = self._new_soa(n + nh + 1, self._pos4.device)
             sx, sy, sz = self._soa[0], self._soa[1], self._soa[2]
         if n:
             if soa:
@@ -162,7 +171,8 @@ class VerletListContainer:
             return
         if ghost_rows is not None:
             if soa:
-                raise ConfigurationError("row-major ghosts with SoA gathers are not supported")
+                N.call("lmd_gather_rows_soa", nh, N.ptr(self._hperm), N.ptr(ghost_rows),
+                       N.ptr(sx[n:]), N.ptr(sy[n:]), N.ptr(sz[n:]), s)
             N.call("lmd_gather_pos4_rows", nh, N.ptr(self._hperm), N.ptr(ghost_rows), float(HALO),
                    N.ptr(self._pos4[n:]), s)
             return
@@ -182,6 +192,18 @@ class VerletListContainer:
                    N.ptr(sx[n:]), N.ptr(sy[n:]), N.ptr(sz[n:]), s)
         N.call("lmd_halo_refresh_pos4", box, nh, N.ptr(self._halo_owner), N.ptr(self._halo_shift),
                N.ptr(d.pos_x), N.ptr(d.pos_y), N.ptr(d.pos_z), N.ptr(self._pos4[n:]), s)
+
+    @staticmethod
+    def _new_soa(rows: int, dev) -> torch.Tensor:
+        """(3, stride) x, y, z rows over the combined backing + sentinel; the
+        stride is a multiple of 16 doubles so every row starts on 128 B and
+        x[j], y[j], z[j] fall in the same bank pair j & 15 (the bank-aware
+        list order relies on it)."""
+        stride = (rows + 15) // 16 * 16
+        t = torch.empty((3, stride), dtype=torch.float64, device=dev)
+        t[:, rows - 1:] = SENTINEL_POSITION
+        assert t.data_ptr() % 128 == 0
+        return t
 
     def refresh(self, owned, halo=None) -> None:
         """Reload current positions (rebuild-time order) and move the images
@@ -262,10 +284,23 @@ class VerletListContainer:
             est *= 1.0 + 0.45 * (ci - 1)
         return int(2.0 * est) + 32
 
-    def _list(self, pattern, newton3: bool, ci: int | None = None, align: int | None = None):
+    def _bank_for(self, ci: int) -> int:
+        return int(self.bank_rounds) if (self.use_soa and ci == 1) else 0
+
+    def _staged_for(self, pattern, newton3_list: bool, ci: int) -> int:
+        """Group size of the staged layout for these lists (0: not staged)."""
+        if (self.staged_group and self.use_soa and ci == 1 and not newton3_list
+                and pattern.code == as_pattern("v_by_one").code):
+            return int(self.staged_group)
+        return 0
+
+    def _list(self, pattern, newton3: bool, ci: int | None = None, align: int | None = None,
+              bank: int | None = None):
         ci = self._ci_for(newton3) if ci is None else ci
         align = self.align_window if align is None else align
-        key = (pattern.code, bool(newton3), ci, align)
+        bank = self._bank_for(ci) if bank is None else bank
+        staged = self._staged_for(pattern, bool(newton3), ci) if align == 0 else 0
+        key = (pattern.code, bool(newton3), ci, align, bank, staged)
         hit = self._lists.get(key)
         if hit is not None:
             return hit
@@ -290,11 +325,24 @@ class VerletListContainer:
         tables = (N.ptr(self._build_pos4), N.ptr(self._o_start), N.ptr(self._o_count),
                   N.ptr(self._h_start), N.ptr(self._h_count))
         sentinel = self.n_owned + self.n_halo
+        if staged and n:
+            ngroups = (n + staged - 1) // staged
+            groups = torch.empty(ngroups * 64, dtype=torch.int32, device=dev)
+            smax = torch.zeros(2, dtype=torch.int32, device=dev)
+            capacity = int(N.load().lmd_vl_staged_capacity(staged))
+            N.call("lmd_vl_groups", self.grid, n, staged, capacity, *tables,
+                   N.ptr(groups), N.ptr(smax), s)
+            sentinel = -1
         while True:
             steps = (cap + b_ - 1) // b_
             cap_steps = max(4, (steps + 3) // 4 * 4)
             nbr = torch.empty(max(ntiles * cap_steps * 32, 1), dtype=torch.int32, device=dev)
-            if ci > 1:
+            if staged and n:
+                N.call("lmd_vl_build_staged", self.grid, float(rl2), int(newton3), n, *tables,
+                       staged, N.ptr(groups), cap_steps, N.ptr(count),
+                       N.ptr(half) if half is not None else None, N.ptr(tile_off),
+                       N.ptr(kmax), N.ptr(mx), N.ptr(nbr), s)
+            elif ci > 1:
                 N.call("lmd_vl_ci_build", self.grid, float(rl2), pattern.code, ci, units,
                        N.ptr(cl_first), N.ptr(cl_len), sentinel, *tables, cap_steps,
                        N.ptr(count), N.ptr(tile_off), N.ptr(kmax), N.ptr(mx), N.ptr(nbr), s)
@@ -315,6 +363,13 @@ class VerletListContainer:
         if align and units:
             N.call("lmd_vl_align", pattern.code, units, int(align), N.ptr(tile_off), N.ptr(kmax),
                    N.ptr(nbr), s)
+        if bank and units:
+            N.call("lmd_vl_bank_schedule", pattern.code, units, sentinel, int(bank), cap_steps,
+                   N.ptr(tile_off), N.ptr(kmax), N.ptr(nbr), s)
+        if staged and n:
+            sm = smax.tolist()
+            rows = max(16, (int(sm[0]) + 15) // 16 * 16)
+            self._staging[key] = (groups, rows, staged, int(sm[1]))
         hit = (tile_off, kmax, nbr, ntiles * cap_steps * 32)
         self._lists[key] = hit
         return hit
@@ -340,7 +395,9 @@ class VerletListContainer:
         region); True if they had to be built."""
         pattern = as_pattern(pattern)
         ci = self._ci_for(newton3)
-        key = (pattern.code, self._list_n3(newton3), ci, self.align_window)
+        n3l = self._list_n3(newton3)
+        key = (pattern.code, n3l, ci, self.align_window, self._bank_for(ci),
+               self._staged_for(pattern, n3l, ci) if self.align_window == 0 else 0)
         if key in self._lists:
             return False
         self._list(pattern, self._list_n3(newton3), ci=ci)
@@ -358,7 +415,7 @@ class VerletListContainer:
     def pairs(self, newton3: bool = False):
         """(id_i, id_j, j_is_image) of every list entry, for exact set checks."""
         pattern = as_pattern("one_by_v")
-        tile_off, kmax, nbr, total = self._list(pattern, newton3, ci=1, align=0)
+        tile_off, kmax, nbr, total = self._list(pattern, newton3, ci=1, align=0, bank=0)
         count = self._count(newton3)[: self.n_owned].long()
         n = self.n_owned
         perm = self._perm.long()
@@ -408,6 +465,23 @@ class VerletListContainer:
         if ev_t is None:
             slots = int(N.load().lmd_vl_ev_slots(self.n_owned, pattern.code))
             ev_t = torch.empty(2 * max(slots, 1), dtype=torch.float64, device=dev)
+        n3l = self._list_n3(newton3)
+        stg = self._staging.get((pattern.code, n3l, ci, self.align_window, self._bank_for(ci),
+                                 self._staged_for(pattern, n3l, ci)
+                                 if self.align_window == 0 else 0))
+        if stg is not None and mode != 1:
+            groups, _, gsize, _ = stg
+            direct = out is not None and len(out) == self.n_owned
+            fx, fy, fz = ((out.force_x, out.force_y, out.force_z) if direct
+                          else (self._fx, self._fy, self._fz))
+            N.call("lmd_force_vl_staged", mode, (N.FLAG_ENERGY if energy else 0) | self.knobs,
+                   N.make_lj(self.params), self.n_owned, N.ptr(self._pos4), N.ptr(self._soa),
+                   self._soa.shape[1], self.n_owned + self.n_halo, gsize, N.ptr(groups),
+                   N.ptr(tile_off), N.ptr(kmax),
+                   N.ptr(nbr), N.ptr(self._perm) if direct else None, N.ptr(fx), N.ptr(fy),
+                   N.ptr(fz), N.ptr(ev_t), N.ptr(stats_t), N.stream())
+            self._collected_into = out if direct else None
+            return stats_t
         if mode == 1:
             self._fx.zero_()
             self._fy.zero_()

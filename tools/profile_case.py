@@ -29,6 +29,10 @@ for label in args.config.split("+"):
         cont = B.make_container(cfg.container, box, params, cluster_size=8)
         if hasattr(cont, "i_cluster"):
             cont.i_cluster = ci
+        # container knobs from the environment, e.g. VL_KNOBS=staged_group=128,bank_rounds=2
+        for kv in filter(None, os.environ.get("VL_KNOBS", "").split(",")):
+            name, val = kv.split("=")
+            setattr(cont, name, type(getattr(cont, name))(val))
         cont.rebuild(buf)
         cont.refresh(buf)
         for _ in range(args.launches):
