@@ -164,6 +164,15 @@ int lmd_halo_refresh_pos4(const lmd_box* box, int64_t nh, const int32_t* owner,
                           const double* z, double* pos4_halo, void* stream);
 
 /* The same into SoA arrays (Verlet-list gathers read x, y, z separately). */
+/* lmd_gather_pos4 (own = NULL) and lmd_halo_refresh_pos4 that also write
+ * the SoA copies sx, sy, sz in the same pass (one read, both layouts). */
+int lmd_gather_pos4_soa(int64_t n, const int32_t* perm, const double* x, const double* y,
+                        const double* z, double own_value, double* pos4, double* sx, double* sy,
+                        double* sz, void* stream);
+int lmd_halo_refresh_pos4_soa(const lmd_box* box, int64_t nh, const int32_t* owner,
+                              const int8_t* shift, const double* x, const double* y,
+                              const double* z, double* pos4_halo, double* sx, double* sy,
+                              double* sz, void* stream);
 int lmd_halo_refresh_soa(const lmd_box* box, int64_t nh, const int32_t* owner,
                          const int8_t* shift, const double* x, const double* y, const double* z,
                          double* ox, double* oy, double* oz, void* stream);
@@ -269,19 +278,21 @@ int lmd_vl_build(const lmd_grid* g, double rl2, int newton3, int pattern, int64_
  * particles (or clusters for the i-cluster lists). */
 int lmd_vl_align(int pattern, int64_t n_units, int window, const int64_t* tile_off,
                  const int32_t* kmax, int32_t* nbr, void* stream);
-/* Optional pass after lmd_vl_build for the SoA gathers (lmd_force_vl with
- * soa != NULL, row stride a multiple of 16 doubles so x[j], y[j], z[j] share
- * bank pair j & 15): permutes every lane's own slot sequence so that the
- * lanes of each half-warp gather from distinct 8-byte bank pairs step by
- * step (csrc/vl.cu vl_bank_kernel); slots a lane leaves idle become -1.
- * Same entries per lane and the same step count, so forces, pair counts and
- * statistics are unchanged up to summation order.  cap_steps = the build's
- * per-tile capacity (bounds the shared-memory workspace,
- * lmd_vl_bank_smem_per_warp bytes per tile, at most 200 KB). */
+/* Optional pass after lmd_vl_build / lmd_vl_build_staged: permutes every
+ * lane's own slot sequence so that the lanes of each half-warp gather from
+ * distinct 8-byte bank pairs (index & 15) step by step -- the cost unit of a
+ * 64-bit shared-memory or L1 gather (csrc/vl.cu vl_bank_local_kernel,
+ * vl_bank_kernel); slots a lane leaves idle become -1.  Same entries per
+ * lane and the same step count, so forces, pair counts and statistics are
+ * unchanged up to summation order.  rounds = 0: lane-local Latin-square
+ * order (16-bit workspace: staged lists only, max_steps = the longest
+ * tile's step count, <= 255); rounds >= 1: warp-cooperative with that many
+ * proposal rounds per step (workspace lmd_vl_bank_smem_per_warp(cap_steps)
+ * bytes per tile, at most 200 KB). */
 size_t lmd_vl_bank_smem_per_warp(int32_t cap_steps);
 int lmd_vl_bank_schedule(int pattern, int64_t n_units, int32_t sentinel, int rounds,
-                         int32_t cap_steps, const int64_t* tile_off, const int32_t* kmax,
-                         int32_t* nbr, void* stream);
+                         int32_t cap_steps, int32_t max_steps, const int64_t* tile_off,
+                         const int32_t* kmax, int32_t* nbr, void* stream);
 /* Staged Verlet lists (v_by_one, full lists; csrc/vl.cu).  Owned particles
  * form groups of group_size (128 / 256 / 512) consecutive backing slots, one
  * block each; a group's candidates lie in 18 contiguous index runs (owned and

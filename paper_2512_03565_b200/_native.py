@@ -148,6 +148,9 @@ _sig("lmd_pair_sweep", _INT, _I64, _VP, _I64, _VP, _INT, _INT, _INT, _INT, C.POI
      *([_VP] * 6), _VP, _VP, _VP)
 _sig("lmd_buffer_counts", _INT, _I64, _VP, _VP, _VP)
 _sig("lmd_dfma_burn", _INT, _INT, _INT, _INT, _VP, _VP)
+_sig("lmd_gather_pos4_soa", _INT, _I64, _VP, _VP, _VP, _VP, _D, _VP, _VP, _VP, _VP, _VP)
+_sig("lmd_halo_refresh_pos4_soa", _INT, C.POINTER(Box), _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP,
+     _VP, _VP, _VP)
 _sig("lmd_halo_refresh_soa", _INT, C.POINTER(Box), _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP,
      _VP, _VP)
 _sig("lmd_gather_soa", _INT, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP)
@@ -176,7 +179,7 @@ _sig("lmd_vl_build_staged", _INT, C.POINTER(Grid), _D, _INT, _I64, _VP, _VP, _VP
 _sig("lmd_vl_staged_capacity", _I32, _I32)
 _sig("lmd_force_vl_staged", _INT, _INT, _INT, C.POINTER(LJ), _I64, _VP, _VP, _I64, _I32, _I32, _VP,
      _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP)
-_sig("lmd_vl_bank_schedule", _INT, _INT, _I64, _I32, _INT, _I32, _VP, _VP, _VP, _VP)
+_sig("lmd_vl_bank_schedule", _INT, _INT, _I64, _I32, _INT, _I32, _I32, _VP, _VP, _VP, _VP)
 _sig("lmd_vl_ci_build", _INT, C.POINTER(Grid), _D, _INT, _INT, _I64, _VP, _VP, _I32, _VP, _VP,
      _VP, _VP, _VP, _I32, _VP, _VP, _VP, _VP, _VP, _VP)
 _sig("lmd_vl_ci_ev_slots", _I64, _I64, _INT)

@@ -95,15 +95,25 @@ __global__ void merge_tables_kernel(int64_t ncell, const int32_t* __restrict__ o
   }
 }
 
+// sx != nullptr: also the SoA copies (one read, both layouts)
 __global__ void gather_pos4_kernel(int64_t n, const int32_t* __restrict__ perm,
                                    const double* __restrict__ x, const double* __restrict__ y,
                                    const double* __restrict__ z, const int8_t* __restrict__ own,
-                                   double own_value, double4* __restrict__ pos4) {
+                                   double own_value, double4* __restrict__ pos4,
+                                   double* __restrict__ sx = nullptr,
+                                   double* __restrict__ sy = nullptr,
+                                   double* __restrict__ sz = nullptr) {
   int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k >= n) return;
   int32_t s = perm ? perm[k] : (int32_t)k;
   double w = own ? (double)own[s] : own_value;
-  pos4[k] = make_double4(x[s], y[s], z[s], w);
+  const double px = x[s], py = y[s], pz = z[s];
+  pos4[k] = make_double4(px, py, pz, w);
+  if (sx) {
+    sx[k] = px;
+    sy[k] = py;
+    sz[k] = pz;
+  }
 }
 
 __global__ void scatter_forces_kernel(int64_t n, const int32_t* __restrict__ perm,
@@ -192,7 +202,9 @@ __global__ void halo_emit_kernel(BoxK b, double margin, int64_t n, const double*
 __global__ void halo_refresh_kernel(BoxK b, int64_t nh, const int32_t* __restrict__ owner,
                                     const int8_t* __restrict__ shift, const double* __restrict__ x,
                                     const double* __restrict__ y, const double* __restrict__ z,
-                                    double4* __restrict__ pos4) {
+                                    double4* __restrict__ pos4, double* __restrict__ sx = nullptr,
+                                    double* __restrict__ sy = nullptr,
+                                    double* __restrict__ sz = nullptr) {
   int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k >= nh) return;
   int32_t o = owner[k];
@@ -208,6 +220,11 @@ __global__ void halo_refresh_kernel(BoxK b, int64_t nh, const int32_t* __restric
     q[ax] = __dadd_rn(p[ax], sh);
   }
   pos4[k] = make_double4(q[0], q[1], q[2], (double)LMD_HALO);
+  if (sx) {
+    sx[k] = q[0];
+    sy[k] = q[1];
+    sz[k] = q[2];
+  }
 }
 
 __global__ void halo_refresh_soa_kernel(BoxK b, int64_t nh, const int32_t* __restrict__ owner,
@@ -440,6 +457,28 @@ int lmd_halo_refresh_pos4(const lmd_box* box, int64_t nh, const int32_t* owner,
   if (nh <= 0) return LMD_OK;
   halo_refresh_kernel<<<grid1d(nh, 256), 256, 0, (cudaStream_t)stream>>>(
       make_boxk(box), nh, owner, shift, x, y, z, reinterpret_cast<double4*>(pos4_halo));
+  LMD_CHECK_LAUNCH();
+  return LMD_OK;
+}
+
+int lmd_gather_pos4_soa(int64_t n, const int32_t* perm, const double* x, const double* y,
+                        const double* z, double own_value, double* pos4, double* sx, double* sy,
+                        double* sz, void* stream) {
+  if (n <= 0) return LMD_OK;
+  gather_pos4_kernel<<<grid1d(n, 256), 256, 0, (cudaStream_t)stream>>>(
+      n, perm, x, y, z, nullptr, own_value, reinterpret_cast<double4*>(pos4), sx, sy, sz);
+  LMD_CHECK_LAUNCH();
+  return LMD_OK;
+}
+
+int lmd_halo_refresh_pos4_soa(const lmd_box* box, int64_t nh, const int32_t* owner,
+                              const int8_t* shift, const double* x, const double* y,
+                              const double* z, double* pos4_halo, double* sx, double* sy,
+                              double* sz, void* stream) {
+  if (nh <= 0) return LMD_OK;
+  halo_refresh_kernel<<<grid1d(nh, 256), 256, 0, (cudaStream_t)stream>>>(
+      make_boxk(box), nh, owner, shift, x, y, z, reinterpret_cast<double4*>(pos4_halo), sx, sy,
+      sz);
   LMD_CHECK_LAUNCH();
   return LMD_OK;
 }

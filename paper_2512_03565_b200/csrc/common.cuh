@@ -19,6 +19,8 @@ int set_cuda_error(cudaError_t e);
 // (executor.py:160-161): eps24 = 24*eps, sigma2 = sigma*sigma, rc2 = cutoff*cutoff.
 struct LJK {
   double rc2, sigma2, eps24, eps48, eps4;
+  // folded powers of sigma: f = u^4 (c12 u^3 - c6), e = u^3 (e12 u^3 - e6), u = 1/r2
+  double c12, c6, e12, e6;
   long long rc2_bits;  // bit pattern of rc2 (positive doubles order like int64)
 };
 
@@ -37,6 +39,11 @@ inline LJK make_ljk(const lmd_lj* p) {
   k.eps24 = 24.0 * p->epsilon;
   k.eps48 = 48.0 * p->epsilon;
   k.eps4 = 4.0 * p->epsilon;
+  const double s6 = k.sigma2 * k.sigma2 * k.sigma2;
+  k.c12 = k.eps48 * s6 * s6;
+  k.c6 = k.eps24 * s6;
+  k.e12 = k.eps4 * s6 * s6;
+  k.e6 = k.eps4 * s6;
   return k;
 }
 

@@ -461,6 +461,121 @@ __global__ void vl_bank_kernel(int ntiles, int B, int32_t sentinel, int rounds, 
   }
 }
 
+// Lane-local variant (rounds == 0): lane l of a half takes its Latin-square
+// pair (l + s) & 15 at step s when it still holds one, idles while it has
+// slack, and otherwise takes the first pair it holds in rotated order.  No
+// cross-lane communication, so every lane schedules independently; per-lane
+// bank counts and bucket cursors live in registers as packed bytes (tiles of
+// more than 255 steps are left in build order), only the bucketed entries
+// are in shared memory.
+__device__ __forceinline__ unsigned get_byte4(const unsigned (&v)[4], int b) {
+  const unsigned w = (b & 8) ? ((b & 4) ? v[3] : v[2]) : ((b & 4) ? v[1] : v[0]);
+  return (w >> ((b & 3) * 8)) & 0xffu;
+}
+__device__ __forceinline__ void add_byte4(unsigned (&v)[4], int b, unsigned x) {
+  const unsigned inc = x << ((b & 3) * 8);
+  if (b < 4) v[0] += inc;
+  else if (b < 8) v[1] += inc;
+  else if (b < 12) v[2] += inc;
+  else v[3] += inc;
+}
+
+__global__ void __launch_bounds__(256)
+    vl_bank_local_kernel(int ntiles, int B, int32_t sentinel, int tcap,
+                         const long long* __restrict__ toff, const int32_t* __restrict__ kmax,
+                         int32_t* __restrict__ nbr) {
+  extern __shared__ __align__(128) uint16_t bank_ent[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int t = blockIdx.x * nw + w;
+  if (t >= ntiles) return;  // warp-uniform
+  const int T = kmax[t] / B;
+  if (T > tcap || T == 0) return;  // byte counters / workspace; keep the build order
+  // entries bucketed by bank pair, 16-bit (staged lists: local rows < 2^16)
+  uint16_t* ent = bank_ent + (size_t)w * tcap * 32;
+  int4* base4 = reinterpret_cast<int4*>(nbr + toff[t]);
+  const int nch = T / kChunk;
+  unsigned cnt[4] = {0u, 0u, 0u, 0u};
+  int n = 0;
+  bool wide = false;
+  // pass 1: bank counts (4 chunk loads in flight)
+  for (int c0 = 0; c0 < nch; c0 += 4) {
+    int4 v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      v[q] = c0 + q < nch ? base4[(c0 + q) * 32 + lane] : make_int4(-1, -1, -1, -1);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int j[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (j[u] != sentinel && j[u] >= 0) {
+          add_byte4(cnt, j[u] & 15, 1u);
+          wide |= j[u] > 0xffff;
+          ++n;
+        }
+    }
+  }
+  // tiles of groups that gather global indices keep the build order
+  if (__any_sync(0xffffffffu, wide)) return;
+  // bucket starts (exclusive prefix over the 16 pairs) and the avail mask
+  unsigned cur[4] = {0u, 0u, 0u, 0u}, end[4] = {0u, 0u, 0u, 0u};
+  unsigned avail = 0u, acc = 0u;
+#pragma unroll
+  for (int b = 0; b < 16; ++b) {
+    const unsigned c = get_byte4(cnt, b);
+    add_byte4(cur, b, acc);
+    acc += c;
+    add_byte4(end, b, acc);
+    avail |= (c ? 1u : 0u) << b;
+  }
+  // pass 2: scatter into the buckets
+  for (int c0 = 0; c0 < nch; c0 += 4) {
+    int4 v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      v[q] = c0 + q < nch ? base4[(c0 + q) * 32 + lane] : make_int4(-1, -1, -1, -1);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int j[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (j[u] != sentinel && j[u] >= 0) {
+          const int b = j[u] & 15;
+          ent[get_byte4(cur, b) * 32 + lane] = (uint16_t)j[u];
+          add_byte4(cur, b, 1u);
+        }
+    }
+  }
+  // cursors back to the bucket starts: start = end - count
+#pragma unroll
+  for (int q = 0; q < 4; ++q) cur[q] = end[q] - cnt[q];
+  const int hl = lane & 15;
+  int lrem = n;
+  for (int s0 = 0; s0 < T; s0 += kChunk) {
+    int out[kChunk];
+#pragma unroll
+    for (int u = 0; u < kChunk; ++u) {
+      const int s = s0 + u;
+      const int rot = (hl + s) & 15;
+      int pick = -1;
+      if (lrem > 0) {
+        if ((avail >> rot) & 1u) pick = rot;
+        else if (T - s <= lrem) pick = first_rot16(avail, rot);  // no slack left
+      }
+      int j = -1;
+      if (pick >= 0) {
+        const unsigned p = get_byte4(cur, pick);
+        j = ent[p * 32 + lane];
+        add_byte4(cur, pick, 1u);
+        if (p + 1u == get_byte4(end, pick)) avail &= ~(1u << pick);
+        --lrem;
+      }
+      out[u] = j;
+    }
+    base4[(s0 / kChunk) * 32 + lane] = make_int4(out[0], out[1], out[2], out[3]);
+  }
+}
+
 __global__ void fill_i32_kernel(int64_t n, int32_t v, int32_t* __restrict__ out) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
        k += (int64_t)gridDim.x * blockDim.x)
@@ -610,35 +725,6 @@ __global__ void __launch_bounds__(32 * kVLWarps, 8)
 // writeback), every warp then walks its tile's bank-scheduled local
 // indices with conflict-free 64-bit shared-memory loads.  Groups whose runs
 // exceed the capacity gather their global indices from the SoA arrays.
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return (unsigned)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
-                                         unsigned long long* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-          "r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
 // rows per axis of the shared-memory copy, by group size; the last row is a
 // dummy far away (idle slots), so a group stages at most rows - 16 rows
 template <int W>
@@ -672,17 +758,20 @@ __device__ __forceinline__ void staged_pairs4(const double4& pi, const double* x
     const bool zero = b == 0;
     a.overlap |= (in && zero);
     const bool hit = in && !zero;
-    const double inv = rcp_fast(r2);
-    const double s2 = k.sigma2 * inv;
-    const double s6 = s2 * s2 * s2;
-    double f = (s6 * inv) * fma(k.eps48, s6, -k.eps24);
+    // u = 1/r2; f = 24 eps (2 s6^2 - s6) / r2 = u^4 (c12 u^3 - c6) with the
+    // powers of sigma folded into c12, c6: 5 FP64 instructions after the
+    // reciprocal (kernels.py:112-126 evaluates the same expression)
+    const double ur = rcp_fast(r2);
+    const double u2 = ur * ur;
+    const double u3 = u2 * ur;
+    double f = (u2 * u2) * fma(k.c12, u3, -k.c6);
     f = hit ? f : 0.0;  // one select; the accumulation then runs unpredicated
     a.ax = fma(f, dx, a.ax);
     a.ay = fma(f, dy, a.ay);
     a.az = fma(f, dz, a.az);
     if (EV) {
-      const double hs = hit ? 0.5 * s6 : 0.0;
-      a.e = fma(hs, fma(k.eps4, s6, -k.eps4), a.e);
+      const double hu = hit ? 0.5 * u3 : 0.0;
+      a.e = fma(hu, fma(k.e12, u3, -k.e6), a.e);
       a.v = fma(0.5 * f, r2, a.v);
     }
     a.pairs += in;
@@ -821,16 +910,20 @@ __global__ void __launch_bounds__(32 * W, 16 / W)
       xs[3 * ROWS - 1] = 1.0e30;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      mbar_expect_tx(&bar, (unsigned)rec[kGrpS] * 3u * 8u);
-      for (int r = 0; r < kGroupRuns; ++r) {
-        const int len = rec[kGrpLen + r];
-        if (!len) continue;
-        const int st = rec[kGrpStart + r];
-        const int base = st + rec[kGrpOff + r];
-        bulk_g2s(xs + base, q.x + st, (unsigned)len * 8u, &bar);
-        bulk_g2s(xs + ROWS + base, q.y + st, (unsigned)len * 8u, &bar);
-        bulk_g2s(xs + 2 * ROWS + base, q.z + st, (unsigned)len * 8u, &bar);
+    // warp 0: lane 0 arms the barrier, then lane r < 18 issues run r's
+    // three bulk copies (issuing 54 copies from one thread serialises them)
+    if (threadIdx.x < 32) {
+      if (lane == 0) mbar_expect_tx(&bar, (unsigned)rec[kGrpS] * 3u * 8u);
+      __syncwarp();
+      if (lane < kGroupRuns) {
+        const int len = rec[kGrpLen + lane];
+        if (len) {
+          const int st = rec[kGrpStart + lane];
+          const int base = st + rec[kGrpOff + lane];
+          bulk_g2s(xs + base, q.x + st, (unsigned)len * 8u, &bar);
+          bulk_g2s(xs + ROWS + base, q.y + st, (unsigned)len * 8u, &bar);
+          bulk_g2s(xs + 2 * ROWS + base, q.z + st, (unsigned)len * 8u, &bar);
+        }
       }
     }
   }
@@ -1030,12 +1123,28 @@ size_t lmd_vl_bank_smem_per_warp(int32_t cap_steps) {
 }
 
 int lmd_vl_bank_schedule(int pattern, int64_t n_units, int32_t sentinel, int rounds,
-                         int32_t cap_steps, const int64_t* tile_off, const int32_t* kmax,
-                         int32_t* nbr, void* stream) {
+                         int32_t cap_steps, int32_t max_steps, const int64_t* tile_off,
+                         const int32_t* kmax, int32_t* nbr, void* stream) {
   if (n_units <= 0) return LMD_OK;
-  if (rounds < 1 || rounds > 16 || cap_steps <= 0 || cap_steps % kChunk) return LMD_ERR_CONFIG;
+  if (rounds < 0 || rounds > 16 || cap_steps <= 0 || cap_steps % kChunk) return LMD_ERR_CONFIG;
   const int B = pattern_B(pattern);
   const int64_t ntiles = cdiv(n_units, pattern_A(pattern));
+  cudaStream_t st = (cudaStream_t)stream;
+  if (rounds == 0) {
+    // workspace sized by the longest tile of this list (tcap steps, <= 255)
+    const int tcap = max_steps;
+    if (tcap <= 0 || tcap > 255) return LMD_ERR_CONFIG;
+    const size_t per = (size_t)tcap * 32 * sizeof(uint16_t);
+    int nwl = (int)(72 * 1024 / per);
+    nwl = nwl < 1 ? 1 : (nwl > 8 ? 8 : nwl);
+    cudaError_t e0 = cudaFuncSetAttribute(
+        vl_bank_local_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(per * nwl));
+    if (e0 != cudaSuccess) return set_cuda_error(e0);
+    vl_bank_local_kernel<<<(unsigned)cdiv(ntiles, nwl), 32 * nwl, per * nwl, st>>>(
+        (int)ntiles, B, sentinel, tcap, (const long long*)tile_off, kmax, nbr);
+    LMD_CHECK_LAUNCH();
+    return LMD_OK;
+  }
   const size_t per_warp = lmd_vl_bank_smem_per_warp(cap_steps);
   const size_t budget = 200 * 1024;
   if (per_warp > budget) return LMD_ERR_CONFIG;

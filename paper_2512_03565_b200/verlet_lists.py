@@ -51,11 +51,12 @@ class VerletListContainer:
         self._max_seen: dict = {}
         self.knobs = 0        # extra lmd_force_vl flags
         # gathers: SoA x, y, z (three 64-bit loads, rows 128-B aligned) in a
-        # bank-conflict-aware entry order (bank_rounds proposal rounds per
-        # step, csrc/vl.cu vl_bank_kernel); use_soa=False: 256-bit pos4
-        # records in ascending order
+        # bank-conflict-aware entry order (bank_rounds: -1 off, 0 lane-local
+        # Latin-square order, >= 1 warp-cooperative with that many proposal
+        # rounds per step; csrc/vl.cu vl_bank_local_kernel / vl_bank_kernel)
+        # use_soa=False: 256-bit pos4 records in ascending order
         self.use_soa = True
-        self.bank_rounds = 2
+        self.bank_rounds = -1   # off: ~8 % faster force, ~1 ms per list build
         # staged lists (v_by_one, full lists): groups of staged_group owned
         # particles copy their candidate runs into shared memory (TMA) and
         # gather there; groups needing more than staged_capacity rows gather
@@ -163,10 +164,12 @@ class VerletListContainer:
             sx, sy, sz = self._soa[0], self._soa[1], self._soa[2]
         if n:
             if soa:
-                N.call("lmd_gather_soa", n, N.ptr(self._perm), N.ptr(d.pos_x), N.ptr(d.pos_y),
-                       N.ptr(d.pos_z), N.ptr(sx), N.ptr(sy), N.ptr(sz), s)
-            N.call("lmd_gather_pos4", n, N.ptr(self._perm), N.ptr(d.pos_x), N.ptr(d.pos_y),
-                   N.ptr(d.pos_z), None, float(OWNED), N.ptr(self._pos4), s)
+                N.call("lmd_gather_pos4_soa", n, N.ptr(self._perm), N.ptr(d.pos_x),
+                       N.ptr(d.pos_y), N.ptr(d.pos_z), float(OWNED), N.ptr(self._pos4),
+                       N.ptr(sx), N.ptr(sy), N.ptr(sz), s)
+            else:
+                N.call("lmd_gather_pos4", n, N.ptr(self._perm), N.ptr(d.pos_x), N.ptr(d.pos_y),
+                       N.ptr(d.pos_z), None, float(OWNED), N.ptr(self._pos4), s)
         if not nh:
             return
         if ghost_rows is not None:
@@ -187,9 +190,10 @@ class VerletListContainer:
             return
         box = N.make_box(self.box)
         if soa:
-            N.call("lmd_halo_refresh_soa", box, nh, N.ptr(self._halo_owner),
+            N.call("lmd_halo_refresh_pos4_soa", box, nh, N.ptr(self._halo_owner),
                    N.ptr(self._halo_shift), N.ptr(d.pos_x), N.ptr(d.pos_y), N.ptr(d.pos_z),
-                   N.ptr(sx[n:]), N.ptr(sy[n:]), N.ptr(sz[n:]), s)
+                   N.ptr(self._pos4[n:]), N.ptr(sx[n:]), N.ptr(sy[n:]), N.ptr(sz[n:]), s)
+            return
         N.call("lmd_halo_refresh_pos4", box, nh, N.ptr(self._halo_owner), N.ptr(self._halo_shift),
                N.ptr(d.pos_x), N.ptr(d.pos_y), N.ptr(d.pos_z), N.ptr(self._pos4[n:]), s)
 
@@ -285,7 +289,7 @@ class VerletListContainer:
         return int(2.0 * est) + 32
 
     def _bank_for(self, ci: int) -> int:
-        return int(self.bank_rounds) if (self.use_soa and ci == 1) else 0
+        return int(self.bank_rounds) if (self.use_soa and ci == 1) else -1
 
     def _staged_for(self, pattern, newton3_list: bool, ci: int) -> int:
         """Group size of the staged layout for these lists (0: not staged)."""
@@ -363,9 +367,14 @@ class VerletListContainer:
         if align and units:
             N.call("lmd_vl_align", pattern.code, units, int(align), N.ptr(tile_off), N.ptr(kmax),
                    N.ptr(nbr), s)
-        if bank and units:
-            N.call("lmd_vl_bank_schedule", pattern.code, units, sentinel, int(bank), cap_steps,
-                   N.ptr(tile_off), N.ptr(kmax), N.ptr(nbr), s)
+        # lane-local order: 16-bit workspace, staged lists only
+        if bank == 0 and not staged:
+            bank = -1
+        if bank >= 0 and units:
+            max_steps = min(cap_steps, ((longest + b_ - 1) // b_ + 3) // 4 * 4)
+            if bank > 0 or max_steps <= 255:
+                N.call("lmd_vl_bank_schedule", pattern.code, units, sentinel, int(bank), cap_steps,
+                       max_steps, N.ptr(tile_off), N.ptr(kmax), N.ptr(nbr), s)
         if staged and n:
             sm = smax.tolist()
             rows = max(16, (int(sm[0]) + 15) // 16 * 16)
@@ -415,7 +424,7 @@ class VerletListContainer:
     def pairs(self, newton3: bool = False):
         """(id_i, id_j, j_is_image) of every list entry, for exact set checks."""
         pattern = as_pattern("one_by_v")
-        tile_off, kmax, nbr, total = self._list(pattern, newton3, ci=1, align=0, bank=0)
+        tile_off, kmax, nbr, total = self._list(pattern, newton3, ci=1, align=0, bank=-1)
         count = self._count(newton3)[: self.n_owned].long()
         n = self.n_owned
         perm = self._perm.long()

@@ -28,7 +28,7 @@ cont.rebuild(buf)
 cont.refresh(buf)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 patterns = os.environ.get("PATTERNS", "v_by_one").split(",")
-rounds = [int(r) for r in os.environ.get("ROUNDS", "1,2,4").split(",")]
+rounds = [int(r) for r in os.environ.get("ROUNDS", "0,2").split(",")]
 
 
 def timed(fn, reps=6):
@@ -83,10 +83,10 @@ def lane_sorted(v, steps, sentinel):
 
 
 groups_env = [int(g) for g in os.environ.get("STAGE_GROUPS", "128,256,512").split(",")]
-variants = ([("pos4", False, 0, 0), ("soa", True, 0, 0)]
+variants = ([("pos4", False, -1, 0), ("soa", True, -1, 0)]
             + [(f"soa_bank{r}", True, r, 0) for r in rounds]
-            + [(f"staged{g}", True, 0, g) for g in groups_env]
-            + [(f"staged{g}_bank{rounds[-1]}", True, rounds[-1], g) for g in groups_env])
+            + [(f"staged{g}", True, -1, g) for g in groups_env]
+            + [(f"staged{g}_bank{r}", True, r, g) for g in groups_env for r in rounds])
 for pname in patterns:
     pat = B.PatternKind(pname)
     ref_sorted = None
