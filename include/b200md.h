@@ -317,9 +317,18 @@ int lmd_vl_groups(const lmd_grid* g, int64_t n_owned, int32_t group_size, int32_
 int lmd_vl_build_staged(const lmd_grid* g, double rl2, int newton3, int64_t n_owned,
                         const double* pos4, const int32_t* o_start, const int32_t* o_count,
                         const int32_t* h_start, const int32_t* h_count, int32_t group_size,
-                        const int32_t* groups, int32_t cap_steps, int32_t* count,
-                        int32_t* count_half, int64_t* tile_off, int32_t* kmax,
-                        int32_t* max_count, int32_t* nbr, void* stream);
+                        const int32_t* groups, const float* pf, float rl2f_lo, float rl2f_hi,
+                        int32_t cap_steps, int32_t* count, int32_t* count_half,
+                        int64_t* tile_off, int32_t* kmax, int32_t* max_count, int32_t* nbr,
+                        void* stream);
+/* FP32 rows for lmd_vl_build_staged (pf != NULL): float4 (x - cx, y - cy,
+ * z - cz, 0) of every pos4 row.  The build decides a candidate in FP32 when
+ * its FP32 r2 is below rl2f_lo (inside) or at least rl2f_hi (outside) and
+ * re-tests the rest exactly (FP64, the reference's r2); the caller sets
+ * rl2f_lo / rl2f_hi to rl^2 minus / plus a margin above the FP32 error bound
+ * of r2 for the coordinate range, so the pair set is the exact one. */
+int lmd_vl_prefilter_rows(int64_t rows, const double* pos4, const double* center, float* pf,
+                          void* stream);
 int lmd_force_vl_staged(int newton3, int flags, const lmd_lj* lj, int64_t n_owned,
                         const double* pos4, const double* soa, int64_t stride, int32_t sentinel,
                         int32_t group_size, const int32_t* groups,

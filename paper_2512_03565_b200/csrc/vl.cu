@@ -114,7 +114,7 @@ __global__ void vl_fill_kernel(GridK g, int n, int A, int B, int pattern, int ne
 // a shuffle reduction, and each thread pads its own slots with the sentinel
 // up to that count.  Entries past the capacity are dropped and reported
 // through *max_count (the caller rebuilds with a larger capacity).
-template <int P>
+template <int P, bool PF>
 __global__ void vl_build_kernel(GridK g, int n, int ntiles, int newton3,
                                 double rl2, int32_t sentinel, const double* __restrict__ pos4,
                                 const int32_t* __restrict__ os, const int32_t* __restrict__ oc,
@@ -123,7 +123,8 @@ __global__ void vl_build_kernel(GridK g, int n, int ntiles, int newton3,
                                 int32_t* __restrict__ count_half,
                                 long long* __restrict__ toff, int32_t* __restrict__ kmax,
                                 int32_t* __restrict__ max_count, int32_t* __restrict__ nbr,
-                                const int32_t* __restrict__ groups, int G) {
+                                const int32_t* __restrict__ groups, int G,
+                                const float4* __restrict__ pf, float rl2f_lo, float rl2f) {
   constexpr int A = Pattern<P>::A, B = Pattern<P>::B, pattern = P;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int t = i / A, il = i - t * A;
@@ -133,6 +134,7 @@ __global__ void vl_build_kernel(GridK g, int n, int ntiles, int newton3,
   int k = 0, kh = 0;
   if (i < n) {
     const double4 pi = ld_pos4(pos4, i);
+    const float4 pif = PF ? __ldg(pf + i) : make_float4(0.f, 0.f, 0.f, 0.f);
     if (pi.w == (double)LMD_OWNED) {
       const long long lin = cell_of_owned(pi, g.lo0, g.lo1, g.lo2, g.cl0, g.cl1, g.cl2, g.d0,
                                           g.d1, g.d2, g.t0, g.t1);
@@ -165,11 +167,35 @@ __global__ void vl_build_kernel(GridK g, int n, int ntiles, int newton3,
               for (int j0 = j; j0 < e; j0 += 32) {
                 const int cnt = min(e - j0, 32);
                 unsigned mask = 0u;
+                if (PF) {
+                  // FP32 decision with an exact fallback: r2f < rl2f_lo is
+                  // inside and r2f >= rl2f_hi outside for the reference's
+                  // exact r2 too (the margin bounds the FP32 error for this
+                  // coordinate range); only candidates in between -- a band
+                  // of ~1e-4 relative width -- are re-tested in FP64
+                  unsigned band = 0u;
+#pragma unroll 4
+                  for (int q = 0; q < cnt; ++q) {
+                    const float4 f = __ldg(pf + j0 + q);
+                    const float fx = pif.x - f.x, fy = pif.y - f.y, fz = pif.z - f.z;
+                    const float r2f = fmaf(fz, fz, fmaf(fy, fy, fx * fx));
+                    mask |= (r2f < rl2f_lo ? 1u : 0u) << q;
+                    band |= (r2f >= rl2f_lo && r2f < rl2f ? 1u : 0u) << q;
+                  }
+                  while (band) {
+                    const int q = __ffs(band) - 1;
+                    band &= band - 1u;
+                    const double4 pj = ld_pos4(pos4, j0 + q);
+                    const double r2 = r2_exact(pi.x - pj.x, pi.y - pj.y, pi.z - pj.z);
+                    mask |= (r2 < rl2 ? 1u : 0u) << q;
+                  }
+                } else {
 #pragma unroll 2
-                for (int q = 0; q < cnt; ++q) {
-                  const double4 pj = ld_pos4(pos4, j0 + q);
-                  const double r2 = r2_exact(pi.x - pj.x, pi.y - pj.y, pi.z - pj.z);
-                  mask |= (r2 < rl2 ? 1u : 0u) << q;
+                  for (int q = 0; q < cnt; ++q) {
+                    const double4 pj = ld_pos4(pos4, j0 + q);
+                    const double r2 = r2_exact(pi.x - pj.x, pi.y - pj.y, pi.z - pj.z);
+                    mask |= (r2 < rl2 ? 1u : 0u) << q;
+                  }
                 }
                 if (!view) {
                   const unsigned self = (unsigned)(i - j0);
@@ -212,6 +238,181 @@ __global__ void vl_build_kernel(GridK g, int n, int ntiles, int newton3,
   int w = m;
   for (int off = 16; off > 0; off >>= 1) w = max(w, __shfl_xor_sync(0xffffffffu, w, off));
   if ((threadIdx.x & 31) == 0 && w > 0) atomicMax(max_count, w);
+}
+
+// ---------------------------------------------------- cell-cooperative build
+// Staged full lists (v_by_one) built one owned cell per warp: the warp copies
+// the cell's 18 candidate runs (3 x 3 cell rows x owned / image backing, 3
+// consecutive cells each) into shared memory as FP32 centred rows, then for
+// each particle i of the cell tests 32 candidates per step, one per lane:
+// FP32 r2 below rl2f_lo is inside, at or above rl2f_hi outside -- for the
+// reference's exact r2 as well (the margin bounds the FP32
+// error) -- and the rare candidates in between are re-tested exactly in
+// FP64.  Hits are compacted with a ballot and written at the i's next list
+// slots (entry k of owned particle i at tile i / 32, lane i % 32, step k).
+// Lanes share the i and stream the candidates, so there is no divergence
+// over cell sizes; the per-candidate work is 7 FP32 instructions.  Lists
+// are padded per tile afterwards (vl_pad_kernel).
+constexpr int kCellWarps = 2;
+constexpr int kCellCand = 768;  // candidates staged per pass and warp
+
+__global__ void __launch_bounds__(32 * kCellWarps)
+    vl_build_cells_kernel(GridK g, long long ncell, int n, double rl2, float rl2f_lo,
+                          float rl2f_hi, const double* __restrict__ pos4,
+                          const float4* __restrict__ pf, const int32_t* __restrict__ os,
+                          const int32_t* __restrict__ oc, const int32_t* __restrict__ hs,
+                          const int32_t* __restrict__ hc, const int32_t* __restrict__ groups,
+                          int G, int cap_steps, int32_t* __restrict__ count,
+                          int32_t* __restrict__ count_half, int32_t* __restrict__ nbr) {
+  __shared__ float4 cf_s[kCellWarps][kCellCand];
+  __shared__ int32_t cj_s[kCellWarps][kCellCand];
+  __shared__ uint8_t cr_s[kCellWarps][kCellCand];
+  __shared__ int32_t roff_s[kCellWarps][2][kGroupRuns];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const long long stride = (long long)cap_steps * 32;
+  float4* cf = cf_s[w];
+  int32_t* cj = cj_s[w];
+  uint8_t* cr = cr_s[w];
+  for (long long c = blockIdx.x * (long long)kCellWarps + w; c < ncell;
+       c += (long long)gridDim.x * kCellWarps) {
+    const int ni = oc[c];
+    if (ni == 0) continue;  // warp-uniform
+    const int i0 = os[c];
+    // the 18 runs: lane r < 18 -> [rs, rs + rl) of its backing
+    int rs = 0, rl = 0;
+    if (lane < kGroupRuns) {
+      const int view = lane / 9, q = lane % 9, dz = q / 3 - 1, dy = q % 3 - 1;
+      const int32_t* vs = view ? hs : os;
+      const int32_t* vc = view ? hc : oc;
+      const long long nl = c - 1 + g.t0 * (dy + g.t1 * dz);
+      int first = -1, last = -1;
+#pragma unroll
+      for (int dx = 0; dx < 3; ++dx) {
+        const int k = vc[nl + dx];
+        if (k) {
+          if (first < 0) first = vs[nl + dx];
+          last = vs[nl + dx] + k;
+        }
+      }
+      if (first >= 0) {
+        rs = first;
+        rl = last - first;
+      }
+    }
+    int incl = rl;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += v;
+    }
+    const int roff_base = incl - rl;  // exclusive prefix
+    const int M = __shfl_sync(0xffffffffu, incl, 31);
+    // local-row offsets of the (at most two) groups the cell's particles fall in
+    const int gA = groups ? i0 / G : 0, gB = groups ? (i0 + ni - 1) / G : 0;
+    if (lane < kGroupRuns) {
+      roff_s[w][0][lane] = groups ? groups[(long long)gA * kGroupRec + kGrpOff + lane] : 0;
+      roff_s[w][1][lane] = groups ? groups[(long long)gB * kGroupRec + kGrpOff + lane] : 0;
+    }
+    // running list lengths of a batch of up to 64 of the cell's particles:
+    // lane l holds particles ib + l and ib + 32 + l
+    for (int ib = 0; ib < ni; ib += 64) {
+    const int nb = min(ni - ib, 64);
+    int kq[2] = {0, 0}, hq[2] = {0, 0};
+    for (int m0 = 0; m0 < M; m0 += kCellCand) {
+      const int mend = min(M, m0 + kCellCand);
+      __syncwarp();
+      // stage candidates [m0, mend): run r covers [base_r, base_r + len_r)
+      for (int r = 0; r < kGroupRuns; ++r) {
+        const int rb = __shfl_sync(0xffffffffu, roff_base, r);
+        const int rn = __shfl_sync(0xffffffffu, rl, r);
+        const int r0 = __shfl_sync(0xffffffffu, rs, r);
+        const int lo = max(rb, m0), hi = min(rb + rn, mend);
+        for (int m = lo + lane; m < hi; m += 32) {
+          const int j = r0 + (m - rb);
+          cf[m - m0] = __ldg(pf + j);
+          cj[m - m0] = j;
+          cr[m - m0] = (uint8_t)r;
+        }
+      }
+      __syncwarp();
+      const int mc = mend - m0;
+      for (int ii = 0; ii < nb; ++ii) {
+        const int i = i0 + ib + ii;
+        const float4 pif = __ldg(pf + i);
+        const int gsel = (groups && i / G != gA) ? 1 : 0;
+        const int t = i >> 5, il = i & 31;
+        int32_t* out = nbr + (long long)t * stride;
+        int k = __shfl_sync(0xffffffffu, kq[ii >> 5], ii & 31);
+        int kh = __shfl_sync(0xffffffffu, hq[ii >> 5], ii & 31);
+        for (int q0 = 0; q0 < mc; q0 += 32) {
+          const int m = q0 + lane;
+          bool hit = false, band = false;
+          int j = -1;
+          if (m < mc) {
+            const float4 f = cf[m];
+            j = cj[m];
+            const float fx = pif.x - f.x, fy = pif.y - f.y, fz = pif.z - f.z;
+            const float r2f = fmaf(fz, fz, fmaf(fy, fy, fx * fx));
+            hit = r2f < rl2f_lo;
+            band = r2f >= rl2f_lo && r2f < rl2f_hi;
+            if (j == i) hit = band = false;  // self (owned run)
+          }
+          if (__any_sync(0xffffffffu, band) && band) {
+            const double4 pi = ld_pos4(pos4, i), pj = ld_pos4(pos4, j);
+            hit = r2_exact(pi.x - pj.x, pi.y - pj.y, pi.z - pj.z) < rl2;
+          }
+          const unsigned mask = __ballot_sync(0xffffffffu, hit);
+          if (hit) {
+            const int kk = k + __popc(mask & ((1u << lane) - 1u));
+            if (kk < cap_steps) {
+              const int r = cr[m];
+              out[(long long)(kk >> 2) * 128 + il * 4 + (kk & 3)] = j + roff_s[w][gsel][r];
+            }
+          }
+          k += __popc(mask);
+          kh += __popc(__ballot_sync(0xffffffffu, hit && (j >= n || j > i)));
+        }
+        if (lane == (ii & 31)) {
+          kq[ii >> 5] = k;
+          hq[ii >> 5] = kh;
+        }
+      }
+    }
+    // counts of the batch's particles
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int ii = h * 32 + lane;
+      if (ii < nb) {
+        count[i0 + ib + ii] = kq[h];
+        if (count_half) count_half[i0 + ib + ii] = hq[h];
+      }
+    }
+    }
+  }
+}
+
+// Per tile: step count = the longest list (4-step chunks, capped), idle
+// slots up to it = -1, tile offsets; the longest list overall -> max_count.
+__global__ void vl_pad_kernel(int n, int ntiles, int cap_steps, const int32_t* __restrict__ count,
+                              long long* __restrict__ toff, int32_t* __restrict__ kmax,
+                              int32_t* __restrict__ max_count, int32_t* __restrict__ nbr) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int t = i >> 5, il = i & 31;
+  const int k = i < n ? count[i] : 0;
+  int m = k;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, off));
+  if (t >= ntiles) return;
+  int steps = (m + kChunk - 1) / kChunk * kChunk;
+  if (steps > cap_steps) steps = cap_steps;
+  const long long stride = (long long)cap_steps * 32;
+  int32_t* out = nbr + (long long)t * stride;
+  for (int q = min(k, cap_steps); q < steps; ++q) out[(long long)(q >> 2) * 128 + il * 4 + (q & 3)] = -1;
+  if (il == 0) {
+    kmax[t] = steps;
+    toff[t] = (long long)t * stride;
+    if (m > 0) atomicMax(max_count, m);
+  }
 }
 
 // Group run table for the staged lists (one warp per group, lane r < 18
@@ -574,6 +775,15 @@ __global__ void __launch_bounds__(256)
     }
     base4[(s0 / kChunk) * 32 + lane] = make_int4(out[0], out[1], out[2], out[3]);
   }
+}
+
+__global__ void vl_prefilter_kernel(int64_t rows, const double* __restrict__ pos4, double cx,
+                                    double cy, double cz, float4* __restrict__ pf) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= rows) return;
+  const double4 p = ld_pos4(pos4, k);
+  pf[k] = make_float4(__double2float_rn(p.x - cx), __double2float_rn(p.y - cy),
+                      __double2float_rn(p.z - cz), 0.f);
 }
 
 __global__ void fill_i32_kernel(int64_t n, int32_t v, int32_t* __restrict__ out) {
@@ -1050,7 +1260,8 @@ static int vl_build_impl(const lmd_grid* g, double rl2, int newton3, int pattern
                          const int32_t* o_count, const int32_t* h_start, const int32_t* h_count,
                          int32_t cap_steps, int32_t* count, int32_t* count_half,
                          int64_t* tile_off, int32_t* kmax, int32_t* max_count, int32_t* nbr,
-                         const int32_t* staged_groups, int staged_G, void* stream) {
+                         const int32_t* staged_groups, int staged_G, const float4* pf,
+                         float rl2f_lo, float rl2f, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e = cudaMemsetAsync(max_count, 0, sizeof(int32_t), s);
   if (e != cudaSuccess) return set_cuda_error(e);
@@ -1061,12 +1272,19 @@ static int vl_build_impl(const lmd_grid* g, double rl2, int newton3, int pattern
   const unsigned blocks = (unsigned)cdiv(ntiles * A, 128);
   const int32_t* groups = staged_groups;
   const int G = staged_G;
-#define LMD_VLB(P)                                                                             \
-  vl_build_kernel<P><<<blocks, 128, 0, s>>>(make_gridk(g), (int)n_owned, (int)ntiles, newton3, \
+#define LMD_VLB_(P, PFB)                                                                             \
+  vl_build_kernel<P, PFB><<<blocks, 128, 0, s>>>(make_gridk(g), (int)n_owned, (int)ntiles, newton3, \
                                             rl2, sentinel, pos4, o_start, o_count, h_start,    \
                                             h_count, cap_steps, count, count_half,             \
                                             (long long*)tile_off, kmax, max_count, nbr,        \
-                                            groups, G)
+                                            groups, G, pf, rl2f_lo, rl2f)
+#define LMD_VLB(P)          \
+  do {                      \
+    if (pf)                 \
+      LMD_VLB_(P, true);    \
+    else                    \
+      LMD_VLB_(P, false);   \
+  } while (0)
   switch (pattern) {
     case LMD_ONE_BY_V: LMD_VLB(LMD_ONE_BY_V); break;
     case LMD_V_BY_ONE: LMD_VLB(LMD_V_BY_ONE); break;
@@ -1075,6 +1293,7 @@ static int vl_build_impl(const lmd_grid* g, double rl2, int newton3, int pattern
     default: return LMD_ERR_CONFIG;
   }
 #undef LMD_VLB
+#undef LMD_VLB_
   LMD_CHECK_LAUNCH();
   return LMD_OK;
 }
@@ -1086,19 +1305,49 @@ int lmd_vl_build(const lmd_grid* g, double rl2, int newton3, int pattern, int64_
                  int32_t* kmax, int32_t* max_count, int32_t* nbr, void* stream) {
   return vl_build_impl(g, rl2, newton3, pattern, n_owned, sentinel, pos4, o_start, o_count,
                        h_start, h_count, cap_steps, count, count_half, tile_off, kmax, max_count,
-                       nbr, nullptr, 0, stream);
+                       nbr, nullptr, 0, nullptr, 0.f, 0.f, stream);
 }
 
 int lmd_vl_build_staged(const lmd_grid* g, double rl2, int newton3, int64_t n_owned,
                         const double* pos4, const int32_t* o_start, const int32_t* o_count,
                         const int32_t* h_start, const int32_t* h_count, int32_t group_size,
-                        const int32_t* groups, int32_t cap_steps, int32_t* count,
-                        int32_t* count_half, int64_t* tile_off, int32_t* kmax,
-                        int32_t* max_count, int32_t* nbr, void* stream) {
+                        const int32_t* groups, const float* pf, float rl2f_lo, float rl2f_hi,
+                        int32_t cap_steps, int32_t* count, int32_t* count_half,
+                        int64_t* tile_off, int32_t* kmax, int32_t* max_count, int32_t* nbr,
+                        void* stream) {
   if (group_size <= 0 || group_size % 32) return LMD_ERR_CONFIG;
-  return vl_build_impl(g, rl2, newton3, LMD_V_BY_ONE, n_owned, -1, pos4, o_start, o_count,
-                       h_start, h_count, cap_steps, count, count_half, tile_off, kmax, max_count,
-                       nbr, groups, group_size, stream);
+  if (pf && !(rl2f_lo < rl2f_hi)) return LMD_ERR_CONFIG;
+  if (!pf || newton3)
+    return vl_build_impl(g, rl2, newton3, LMD_V_BY_ONE, n_owned, -1, pos4, o_start, o_count,
+                         h_start, h_count, cap_steps, count, count_half, tile_off, kmax,
+                         max_count, nbr, groups, group_size, reinterpret_cast<const float4*>(pf),
+                         rl2f_lo, rl2f_hi, stream);
+  // cell-cooperative build (cells of at most 64 owned particles)
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(max_count, 0, sizeof(int32_t), s);
+  if (e != cudaSuccess) return set_cuda_error(e);
+  if (n_owned <= 0) return LMD_OK;
+  if (n_owned > 0x7fffffffLL || cap_steps <= 0 || cap_steps % kChunk) return LMD_ERR_CONFIG;
+  const long long ncell = g->ncell;
+  vl_build_cells_kernel<<<1184, 32 * kCellWarps, 0, s>>>(
+      make_gridk(g), ncell, (int)n_owned, rl2, rl2f_lo, rl2f_hi, pos4,
+      reinterpret_cast<const float4*>(pf), o_start, o_count, h_start, h_count, groups,
+      group_size, cap_steps, count, count_half, nbr);
+  LMD_CHECK_LAUNCH();
+  const int64_t ntiles = cdiv(n_owned, 32);
+  vl_pad_kernel<<<(unsigned)cdiv(ntiles * 32, 256), 256, 0, s>>>(
+      (int)n_owned, (int)ntiles, cap_steps, count, (long long*)tile_off, kmax, max_count, nbr);
+  LMD_CHECK_LAUNCH();
+  return LMD_OK;
+}
+
+int lmd_vl_prefilter_rows(int64_t rows, const double* pos4, const double* center, float* pf,
+                          void* stream) {
+  if (rows <= 0) return LMD_OK;
+  vl_prefilter_kernel<<<(unsigned)cdiv(rows, 256), 256, 0, (cudaStream_t)stream>>>(
+      rows, pos4, center[0], center[1], center[2], reinterpret_cast<float4*>(pf));
+  LMD_CHECK_LAUNCH();
+  return LMD_OK;
 }
 
 int lmd_vl_align(int pattern, int64_t n_units, int window, const int64_t* tile_off,

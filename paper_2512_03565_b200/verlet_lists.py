@@ -12,6 +12,8 @@ built by K3 on the rc+skin cell grid and laid out per interaction order
 
 from __future__ import annotations
 
+import ctypes
+
 import numpy as np
 import torch
 
@@ -63,6 +65,10 @@ class VerletListContainer:
         # from global memory.  0 = off.
         self.staged_group = 128
         self._staging: dict = {}
+        # staged lists: True = cell-cooperative FP32 build (exact decisions,
+        # csrc/vl.cu vl_build_cells_kernel; measured 3.8 ms vs 1.0 ms at 1M,
+        # latency-bound at 14 warps/SM); False = thread per particle, FP64 tests
+        self.build_fp32 = False
         # particles per lane sharing one union list (csrc/vl_ci.cu) for full
         # lists; 1 = one list per particle (csrc/vl.cu)
         self.i_cluster = 1   # CI = 2 or 4 measured 2-3x slower
@@ -298,6 +304,32 @@ class VerletListContainer:
             return int(self.staged_group)
         return 0
 
+    def _prefilter_rows(self):
+        """FP32 centred copies of the build positions and the FP32 decision
+        bounds rl^2 -/+ four times the worst-case FP32 error of r2 near the
+        cutoff for this coordinate range (conversion and arithmetic
+        roundings): below / above them the FP32 and the reference's exact
+        decisions agree; in between the build re-tests in FP64."""
+        hit = self._clusters_cache.get("prefilter")
+        if hit is not None:
+            return hit
+        rows = self._build_pos4.shape[0]
+        lo, hi = np.asarray(self.box.min, float), np.asarray(self.box.max, float)
+        center = (ctypes.c_double * 3)(*((lo + hi) / 2.0))
+        pf = torch.empty((rows, 4), dtype=torch.float32, device=self._build_pos4.device)
+        N.call("lmd_vl_prefilter_rows", rows, N.ptr(self._build_pos4), ctypes.addressof(center),
+               N.ptr(pf), N.stream())
+        rl = float(self.params.interaction_length)
+        max_abs = float(np.max(hi - lo)) / 2.0 + 2.0 * rl
+        e = max_abs * 2.0 ** -23                    # coordinate conversion
+        d = 2.0 * e + rl * 2.0 ** -23               # per-axis difference
+        err = 3.0 * (2.0 * rl * d + d * d) + 3.0 * rl * rl * 2.0 ** -22
+        hi = float(np.nextafter(np.float32(rl * rl + 4.0 * err), np.float32(np.inf)))
+        lo = float(np.nextafter(np.float32(rl * rl - 4.0 * err), np.float32(-np.inf)))
+        hit = (pf, lo, hi)
+        self._clusters_cache["prefilter"] = hit
+        return hit
+
     def _list(self, pattern, newton3: bool, ci: int | None = None, align: int | None = None,
               bank: int | None = None):
         ci = self._ci_for(newton3) if ci is None else ci
@@ -330,6 +362,7 @@ class VerletListContainer:
                   N.ptr(self._h_start), N.ptr(self._h_count))
         sentinel = self.n_owned + self.n_halo
         if staged and n:
+            pf, rl2f_lo, rl2f_hi = self._prefilter_rows()
             ngroups = (n + staged - 1) // staged
             groups = torch.empty(ngroups * 64, dtype=torch.int32, device=dev)
             smax = torch.zeros(2, dtype=torch.int32, device=dev)
@@ -343,7 +376,9 @@ class VerletListContainer:
             nbr = torch.empty(max(ntiles * cap_steps * 32, 1), dtype=torch.int32, device=dev)
             if staged and n:
                 N.call("lmd_vl_build_staged", self.grid, float(rl2), int(newton3), n, *tables,
-                       staged, N.ptr(groups), cap_steps, N.ptr(count),
+                       staged, N.ptr(groups), N.ptr(pf) if self.build_fp32 else None,
+                       rl2f_lo, rl2f_hi, cap_steps,
+                       N.ptr(count),
                        N.ptr(half) if half is not None else None, N.ptr(tile_off),
                        N.ptr(kmax), N.ptr(mx), N.ptr(nbr), s)
             elif ci > 1:
