@@ -963,11 +963,13 @@ __device__ __forceinline__ void staged_pairs4(const double4& pi, const double* x
   for (int u = 0; u < 4; ++u) {
     const double dx = pi.x - xj[u], dy = pi.y - yj[u], dz = pi.z - zj[u];
     const double r2 = r2_exact(dx, dy, dz);
-    const long long b = __double_as_longlong(r2);
-    const bool in = b < k.rc2_bits;
-    const bool zero = b == 0;
-    a.overlap |= (in && zero);
-    const bool hit = in && !zero;
+    const unsigned long long b = (unsigned long long)__double_as_longlong(r2);
+    // 0 < r2 < rc2 in one unsigned compare of the bit patterns (r2 >= +0)
+    const bool hit = b - 1ull < (unsigned long long)k.rc2_bits - 1ull;
+    // overlap: r2 == 0 (the numba -1 sentinel); the high word is 0 only for
+    // r2 < 2^-1022, i.e. coincident particles -- tracked as a running min
+    a.hi_min = min(a.hi_min, (unsigned)(b >> 32));
+    const bool in = hit;
     // u = 1/r2; f = 24 eps (2 s6^2 - s6) / r2 = u^4 (c12 u^3 - c6) with the
     // powers of sigma folded into c12, c6: 5 FP64 instructions after the
     // reciprocal (kernels.py:112-126 evaluates the same expression)
@@ -1057,35 +1059,31 @@ __device__ __forceinline__ void vl_staged_tile(int t, int lane, int n_owned, int
       }
     }
   };
-  unsigned j[NS];
-  double x[NS], y[NS], z[NS];
-  load_batch(0, j, x, y, z);
+  // two batch buffers used in turn (ping-pong: no register moves)
+  static_assert(R == 2 * NB, "the ring holds exactly two batches");
+  unsigned jA[NS], jB[NS];
+  double xA[NS], yA[NS], zA[NS], xB[NS], yB[NS], zB[NS];
+  auto refill = [&](int d, int c) {
+#pragma unroll
+    for (int q = 0; q < NB; ++q)
+      ring[d + q] = c + q + R < nchunks ? __ldg(chunks + (long long)(c + q + R) * 32)
+                                        : make_int4(-1, -1, -1, -1);
+  };
+  load_batch(0, jA, xA, yA, zA);
   for (int c0 = 0; c0 < nchunks; c0 += R) {
+    // batch A = chunks c0 .. c0 + NB - 1 (ring slots 0 .. NB - 1)
+    refill(0, c0);
+    load_batch(NB, jB, xB, yB, zB);
 #pragma unroll
-    for (int d = 0; d < R; d += NB) {
-      const int c = c0 + d;
-      if (c < nchunks) {
-        // the batch's ring slots are consumed (positions in x, y, z): refill
+    for (int q = 0; q < NB; ++q)
+      staged_pairs4<EV, N3>(pi, xA + 4 * q, yA + 4 * q, zA + 4 * q, jA + 4 * q, hb, k, a);
+    if (c0 + NB >= nchunks) break;
+    // batch B = chunks c0 + NB .. c0 + R - 1 (ring slots NB .. R - 1)
+    refill(NB, c0 + NB);
+    load_batch(0, jA, xA, yA, zA);
 #pragma unroll
-        for (int q = 0; q < NB; ++q)
-          ring[d + q] = c + q + R < nchunks
-                            ? __ldg(chunks + (long long)(c + q + R) * 32)
-                            : make_int4(-1, -1, -1, -1);
-        unsigned jn[NS];
-        double xn[NS], yn[NS], zn[NS];
-        load_batch((d + NB) % R, jn, xn, yn, zn);
-#pragma unroll
-        for (int q = 0; q < NB; ++q)
-          staged_pairs4<EV, N3>(pi, x + 4 * q, y + 4 * q, z + 4 * q, j + 4 * q, hb, k, a);
-#pragma unroll
-        for (int u = 0; u < NS; ++u) {
-          j[u] = jn[u];
-          x[u] = xn[u];
-          y[u] = yn[u];
-          z[u] = zn[u];
-        }
-      }
-    }
+    for (int q = 0; q < NB; ++q)
+      staged_pairs4<EV, N3>(pi, xB + 4 * q, yB + 4 * q, zB + 4 * q, jB + 4 * q, hb, k, a);
   }
   if (iact) {
     const int o = out_perm ? out_perm[i] : i;
@@ -1152,6 +1150,7 @@ __global__ void __launch_bounds__(32 * W, 16 / W)
     vl_staged_tile<EV, N3, ROWS, true>(t, lane, n_owned, hb, (unsigned)(ROWS - 1),
                                        (dbg & 2) ? nullptr : &bar, out_perm,
                                        pos4, xs, xs, xs, toff, kmax, nbr, k, a, fx, fy, fz);
+  a.overlap |= a.hi_min == 0u;
   flush_acc(a, lane, true, EV, t, ev, stats);
 }
 

@@ -61,6 +61,7 @@ struct GridK {
 struct Acc {
   double ax, ay, az, e, v;
   int pairs, overlap, halo;
+  unsigned hi_min = 0xffffffffu;  // staged kernel: smallest r2 high word seen
 };
 
 __device__ __forceinline__ void flush_acc(const Acc& a, int lane, bool live, bool ev_on,
