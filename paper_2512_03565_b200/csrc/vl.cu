@@ -690,12 +690,17 @@ __global__ void __launch_bounds__(256)
   const int t = blockIdx.x * nw + w;
   if (t >= ntiles) return;  // warp-uniform
   const int T = kmax[t] / B;
-  if (T > tcap || T == 0) return;  // byte counters / workspace; keep the build order
-  // entries bucketed by bank pair, 16-bit (staged lists: local rows < 2^16)
-  uint16_t* ent = bank_ent + (size_t)w * tcap * 32;
+  if (T > tcap || T == 0) return;  // workspace bound; keep the build order
+  // per warp: counts and cursors per (bank pair, lane) as 16-bit words,
+  // then the entries bucketed by bank pair (16-bit local rows)
+  uint16_t* cnt = bank_ent + (size_t)w * (48 * 32 + (size_t)tcap * 32);
+  uint16_t* cur = cnt + 16 * 32;
+  uint16_t* end = cur + 16 * 32;
+  uint16_t* ent = end + 16 * 32;
   int4* base4 = reinterpret_cast<int4*>(nbr + toff[t]);
   const int nch = T / kChunk;
-  unsigned cnt[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+  for (int b = 0; b < 16; ++b) cnt[b * 32 + lane] = 0;
   int n = 0;
   bool wide = false;
   // pass 1: bank counts (4 chunk loads in flight)
@@ -710,7 +715,7 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
       for (int u = 0; u < 4; ++u)
         if (j[u] != sentinel && j[u] >= 0) {
-          add_byte4(cnt, j[u] & 15, 1u);
+          ++cnt[(j[u] & 15) * 32 + lane];
           wide |= j[u] > 0xffff;
           ++n;
         }
@@ -718,15 +723,15 @@ __global__ void __launch_bounds__(256)
   }
   // tiles of groups that gather global indices keep the build order
   if (__any_sync(0xffffffffu, wide)) return;
-  // bucket starts (exclusive prefix over the 16 pairs) and the avail mask
-  unsigned cur[4] = {0u, 0u, 0u, 0u}, end[4] = {0u, 0u, 0u, 0u};
-  unsigned avail = 0u, acc = 0u;
+  // bucket starts / ends and the avail mask
+  unsigned avail = 0u;
+  int acc = 0;
 #pragma unroll
   for (int b = 0; b < 16; ++b) {
-    const unsigned c = get_byte4(cnt, b);
-    add_byte4(cur, b, acc);
+    const int c = cnt[b * 32 + lane];
+    cur[b * 32 + lane] = (uint16_t)acc;
     acc += c;
-    add_byte4(end, b, acc);
+    end[b * 32 + lane] = (uint16_t)acc;
     avail |= (c ? 1u : 0u) << b;
   }
   // pass 2: scatter into the buckets
@@ -742,14 +747,15 @@ __global__ void __launch_bounds__(256)
       for (int u = 0; u < 4; ++u)
         if (j[u] != sentinel && j[u] >= 0) {
           const int b = j[u] & 15;
-          ent[get_byte4(cur, b) * 32 + lane] = (uint16_t)j[u];
-          add_byte4(cur, b, 1u);
+          const int p = cur[b * 32 + lane];
+          cur[b * 32 + lane] = (uint16_t)(p + 1);
+          ent[p * 32 + lane] = (uint16_t)j[u];
         }
     }
   }
-  // cursors back to the bucket starts: start = end - count
+  // cursors back to the bucket starts
 #pragma unroll
-  for (int q = 0; q < 4; ++q) cur[q] = end[q] - cnt[q];
+  for (int b = 0; b < 16; ++b) cur[b * 32 + lane] = (uint16_t)(end[b * 32 + lane] - cnt[b * 32 + lane]);
   const int hl = lane & 15;
   int lrem = n;
   for (int s0 = 0; s0 < T; s0 += kChunk) {
@@ -765,10 +771,10 @@ __global__ void __launch_bounds__(256)
       }
       int j = -1;
       if (pick >= 0) {
-        const unsigned p = get_byte4(cur, pick);
+        const int p = cur[pick * 32 + lane];
         j = ent[p * 32 + lane];
-        add_byte4(cur, pick, 1u);
-        if (p + 1u == get_byte4(end, pick)) avail &= ~(1u << pick);
+        cur[pick * 32 + lane] = (uint16_t)(p + 1);
+        if (p + 1 == end[pick * 32 + lane]) avail &= ~(1u << pick);
         --lrem;
       }
       out[u] = j;
@@ -1382,7 +1388,7 @@ int lmd_vl_bank_schedule(int pattern, int64_t n_units, int32_t sentinel, int rou
     // workspace sized by the longest tile of this list (tcap steps, <= 255)
     const int tcap = max_steps;
     if (tcap <= 0 || tcap > 255) return LMD_ERR_CONFIG;
-    const size_t per = (size_t)tcap * 32 * sizeof(uint16_t);
+    const size_t per = (48 * 32 + (size_t)tcap * 32) * sizeof(uint16_t);
     int nwl = (int)(72 * 1024 / per);
     nwl = nwl < 1 ? 1 : (nwl > 8 ? 8 : nwl);
     cudaError_t e0 = cudaFuncSetAttribute(
