@@ -286,25 +286,31 @@ int lmd_vl_align(int pattern, int64_t n_units, int window, const int64_t* tile_o
  * lane and the same step count, so forces, pair counts and statistics are
  * unchanged up to summation order.  rounds = 0: lane-local Latin-square
  * order (16-bit workspace: staged lists only, max_steps = the longest
- * tile's step count, <= 255); rounds >= 1: warp-cooperative with that many
+ * tile's step count, <= 255; index_bits 16 for the 16-bit staged lists,
+ * else 32); rounds >= 1: warp-cooperative with that many
  * proposal rounds per step (workspace lmd_vl_bank_smem_per_warp(cap_steps)
  * bytes per tile, at most 200 KB). */
 size_t lmd_vl_bank_smem_per_warp(int32_t cap_steps);
 int lmd_vl_bank_schedule(int pattern, int64_t n_units, int32_t sentinel, int rounds,
-                         int32_t cap_steps, int32_t max_steps, const int64_t* tile_off,
-                         const int32_t* kmax, int32_t* nbr, void* stream);
+                         int32_t cap_steps, int32_t max_steps, int32_t index_bits,
+                         const int64_t* tile_off, const int32_t* kmax, int32_t* nbr,
+                         void* stream);
 /* Staged Verlet lists (v_by_one, full lists; csrc/vl.cu).  Owned particles
  * form groups of group_size (128 / 256 / 512) consecutive backing slots, one
- * block each; a group's candidates lie in 18 contiguous index runs (owned and
- * image backing x 3 x 3 (dy, dz) cell rows), which the force kernel copies
- * into shared memory with TMA bulk copies.  lmd_vl_groups writes one record
- * of 64 int32 per group (csrc/vl_common.cuh: run starts, lengths, local
- * offsets, S = staged rows, first image row, overflow flag) from the build
- * positions and cell tables; smax[0] = largest S among groups with
- * S <= capacity, smax[1] = groups over capacity (those gather their global
- * indices from the SoA arrays).  lmd_vl_build_staged = lmd_vl_build for
+ * block each; a group's particles lie in one or two cell rows and its
+ * candidates in 36 contiguous index runs (owned and image backing x the
+ * group's rows x 3 x 3 (dy, dz) neighbour rows), which the force kernel
+ * copies into shared memory with TMA bulk copies.  lmd_vl_groups writes one
+ * record of 128 int32 per group (csrc/vl_common.cuh: run starts, lengths,
+ * local offsets, S = staged rows, first image row, overflow flag, first
+ * row) from the build positions and cell tables; smax[0] = largest S among
+ * staged groups, smax[1] = groups spanning more than two rows or over
+ * capacity (those gather their global indices from the SoA arrays).  lmd_vl_build_staged = lmd_vl_build for
  * V_BY_ONE writing each entry as the local row of its group's copy; pads
- * are -1.  lmd_vl_staged_capacity(group_size) = the largest S a group
+ * are -1.  index_bits = 16 (every group staged, smax[1] == 0): entries are
+ * uint16 local rows, 8 steps per 128-bit chunk (cap_steps % 8 == 0, tile
+ * offsets in uint16 units, pads 0xffff, no FP32 prefilter); 32: int32, 4
+ * steps per chunk.  lmd_vl_staged_capacity(group_size) = the largest S a group
  * stages (pass it as `capacity`).  lmd_force_vl_staged: newton3 0 or 2 as
  * lmd_force_vl; soa = (3, stride) rows (stride % 16 == 0, 128-B aligned)
  * whose row `sentinel` is a far-away position (idle slots of global-gather
@@ -317,10 +323,10 @@ int lmd_vl_groups(const lmd_grid* g, int64_t n_owned, int32_t group_size, int32_
 int lmd_vl_build_staged(const lmd_grid* g, double rl2, int newton3, int64_t n_owned,
                         const double* pos4, const int32_t* o_start, const int32_t* o_count,
                         const int32_t* h_start, const int32_t* h_count, int32_t group_size,
-                        const int32_t* groups, const float* pf, float rl2f_lo, float rl2f_hi,
-                        int32_t cap_steps, int32_t* count, int32_t* count_half,
-                        int64_t* tile_off, int32_t* kmax, int32_t* max_count, int32_t* nbr,
-                        void* stream);
+                        const int32_t* groups, int32_t index_bits, const float* pf,
+                        float rl2f_lo, float rl2f_hi, int32_t cap_steps, int32_t* count,
+                        int32_t* count_half, int64_t* tile_off, int32_t* kmax,
+                        int32_t* max_count, int32_t* nbr, void* stream);
 /* FP32 rows for lmd_vl_build_staged (pf != NULL): float4 (x - cx, y - cy,
  * z - cz, 0) of every pos4 row.  The build decides a candidate in FP32 when
  * its FP32 r2 is below rl2f_lo (inside) or at least rl2f_hi (outside) and
@@ -331,7 +337,7 @@ int lmd_vl_prefilter_rows(int64_t rows, const double* pos4, const double* center
                           void* stream);
 int lmd_force_vl_staged(int newton3, int flags, const lmd_lj* lj, int64_t n_owned,
                         const double* pos4, const double* soa, int64_t stride, int32_t sentinel,
-                        int32_t group_size, const int32_t* groups,
+                        int32_t group_size, const int32_t* groups, int32_t index_bits,
                         const int64_t* tile_off, const int32_t* kmax, const int32_t* nbr,
                         const int32_t* out_perm, double* fx, double* fy, double* fz,
                         double* ev_scratch, lmd_stats* stats, void* stream);

@@ -114,7 +114,9 @@ __global__ void vl_fill_kernel(GridK g, int n, int A, int B, int pattern, int ne
 // a shuffle reduction, and each thread pads its own slots with the sentinel
 // up to that count.  Entries past the capacity are dropped and reported
 // through *max_count (the caller rebuilds with a larger capacity).
-template <int P, bool PF>
+// IDX = uint16_t: staged lists with every group staged (local rows < 2^16),
+// 8 steps per 128-bit chunk; idle slots 0xffff.
+template <int P, bool PF, typename IDX = int32_t>
 __global__ void vl_build_kernel(GridK g, int n, int ntiles, int newton3,
                                 double rl2, int32_t sentinel, const double* __restrict__ pos4,
                                 const int32_t* __restrict__ os, const int32_t* __restrict__ oc,
@@ -128,8 +130,9 @@ __global__ void vl_build_kernel(GridK g, int n, int ntiles, int newton3,
   constexpr int A = Pattern<P>::A, B = Pattern<P>::B, pattern = P;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int t = i / A, il = i - t * A;
+  constexpr int CH = 16 / sizeof(IDX);  // steps per 128-bit chunk
   const long long stride = (long long)cap_steps * 32;
-  int32_t* out = nbr + (long long)t * stride;
+  IDX* out = reinterpret_cast<IDX*>(nbr) + (long long)t * stride;
   const int cap = cap_steps * B;
   int k = 0, kh = 0;
   if (i < n) {
@@ -138,6 +141,10 @@ __global__ void vl_build_kernel(GridK g, int n, int ntiles, int newton3,
     if (pi.w == (double)LMD_OWNED) {
       const long long lin = cell_of_owned(pi, g.lo0, g.lo1, g.lo2, g.cl0, g.cl1, g.cl2, g.d0,
                                           g.d1, g.d2, g.t0, g.t1);
+      // staged: the group's record and this particle's row within the group
+      // (groups gathering global indices have all offsets 0)
+      const int32_t* grec = groups ? groups + (long long)(i / G) * kGroupRec : nullptr;
+      const int grow = grec ? (lin / g.t0 == __ldg(grec + kGrpRow) ? 0 : 1) : 0;
       for (int view = 0; view < 2; ++view) {
         const int32_t* vs = view ? hs : os;
         const int32_t* vc = view ? hc : oc;
@@ -152,9 +159,8 @@ __global__ void vl_build_kernel(GridK g, int n, int ntiles, int newton3,
               // staged lists: index into the group's shared-memory copy of
               // this (view, dy, dz) run (vl_group_kernel); 0 for global
               const int roff =
-                  groups ? __ldg(groups + (long long)(i / G) * kGroupRec + kGrpOff + view * 9 +
-                                 (dz + 1) * 3 + (dy + 1))
-                         : 0;
+                  grec ? __ldg(grec + kGrpOff + view * 18 + grow * 9 + (dz + 1) * 3 + (dy + 1))
+                       : 0;
               if (!view && newton3) j = max(j, i + 1);
               // hits of up to 32 consecutive candidates are collected as a
               // bit mask and emitted afterwards in ascending order, so the
@@ -207,8 +213,7 @@ __global__ void vl_build_kernel(GridK g, int n, int ntiles, int newton3,
                   kh += view || jj > i;
                   if (k < cap) {
                     const int st = k / B, l = lane_of(pattern, il, k % B);
-                    out[(long long)(st / kChunk) * (32 * kChunk) + l * kChunk + st % kChunk] =
-                        jj + roff;
+                    out[(long long)(st / CH) * (32 * CH) + l * CH + st % CH] = (IDX)(jj + roff);
                   }
                   ++k;
                 }
@@ -223,12 +228,12 @@ __global__ void vl_build_kernel(GridK g, int n, int ntiles, int newton3,
   int m = k;
   for (int off = 1; off < A; off <<= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, off));
   int steps = (m + B - 1) / B;
-  steps = (steps + kChunk - 1) / kChunk * kChunk;
+  steps = (steps + CH - 1) / CH * CH;
   if (steps > cap_steps) steps = cap_steps;
   if (t < ntiles) {
     for (int q = min(k, cap); q < steps * B; ++q) {
       const int st = q / B, l = lane_of(pattern, il, q % B);
-      out[(long long)(st / kChunk) * (32 * kChunk) + l * kChunk + st % kChunk] = sentinel;
+      out[(long long)(st / CH) * (32 * CH) + l * CH + st % CH] = (IDX)sentinel;
     }
     if (il == 0) {
       kmax[t] = steps * B;
@@ -238,157 +243,6 @@ __global__ void vl_build_kernel(GridK g, int n, int ntiles, int newton3,
   int w = m;
   for (int off = 16; off > 0; off >>= 1) w = max(w, __shfl_xor_sync(0xffffffffu, w, off));
   if ((threadIdx.x & 31) == 0 && w > 0) atomicMax(max_count, w);
-}
-
-// ---------------------------------------------------- cell-cooperative build
-// Staged full lists (v_by_one) built one owned cell per warp: the warp copies
-// the cell's 18 candidate runs (3 x 3 cell rows x owned / image backing, 3
-// consecutive cells each) into shared memory as FP32 centred rows, then for
-// each particle i of the cell tests 32 candidates per step, one per lane:
-// FP32 r2 below rl2f_lo is inside, at or above rl2f_hi outside -- for the
-// reference's exact r2 as well (the margin bounds the FP32
-// error) -- and the rare candidates in between are re-tested exactly in
-// FP64.  Hits are compacted with a ballot and written at the i's next list
-// slots (entry k of owned particle i at tile i / 32, lane i % 32, step k).
-// Lanes share the i and stream the candidates, so there is no divergence
-// over cell sizes; the per-candidate work is 7 FP32 instructions.  Lists
-// are padded per tile afterwards (vl_pad_kernel).
-constexpr int kCellWarps = 2;
-constexpr int kCellCand = 768;  // candidates staged per pass and warp
-
-__global__ void __launch_bounds__(32 * kCellWarps)
-    vl_build_cells_kernel(GridK g, long long ncell, int n, double rl2, float rl2f_lo,
-                          float rl2f_hi, const double* __restrict__ pos4,
-                          const float4* __restrict__ pf, const int32_t* __restrict__ os,
-                          const int32_t* __restrict__ oc, const int32_t* __restrict__ hs,
-                          const int32_t* __restrict__ hc, const int32_t* __restrict__ groups,
-                          int G, int cap_steps, int32_t* __restrict__ count,
-                          int32_t* __restrict__ count_half, int32_t* __restrict__ nbr) {
-  __shared__ float4 cf_s[kCellWarps][kCellCand];
-  __shared__ int32_t cj_s[kCellWarps][kCellCand];
-  __shared__ uint8_t cr_s[kCellWarps][kCellCand];
-  __shared__ int32_t roff_s[kCellWarps][2][kGroupRuns];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const long long stride = (long long)cap_steps * 32;
-  float4* cf = cf_s[w];
-  int32_t* cj = cj_s[w];
-  uint8_t* cr = cr_s[w];
-  for (long long c = blockIdx.x * (long long)kCellWarps + w; c < ncell;
-       c += (long long)gridDim.x * kCellWarps) {
-    const int ni = oc[c];
-    if (ni == 0) continue;  // warp-uniform
-    const int i0 = os[c];
-    // the 18 runs: lane r < 18 -> [rs, rs + rl) of its backing
-    int rs = 0, rl = 0;
-    if (lane < kGroupRuns) {
-      const int view = lane / 9, q = lane % 9, dz = q / 3 - 1, dy = q % 3 - 1;
-      const int32_t* vs = view ? hs : os;
-      const int32_t* vc = view ? hc : oc;
-      const long long nl = c - 1 + g.t0 * (dy + g.t1 * dz);
-      int first = -1, last = -1;
-#pragma unroll
-      for (int dx = 0; dx < 3; ++dx) {
-        const int k = vc[nl + dx];
-        if (k) {
-          if (first < 0) first = vs[nl + dx];
-          last = vs[nl + dx] + k;
-        }
-      }
-      if (first >= 0) {
-        rs = first;
-        rl = last - first;
-      }
-    }
-    int incl = rl;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, incl, d);
-      if (lane >= d) incl += v;
-    }
-    const int roff_base = incl - rl;  // exclusive prefix
-    const int M = __shfl_sync(0xffffffffu, incl, 31);
-    // local-row offsets of the (at most two) groups the cell's particles fall in
-    const int gA = groups ? i0 / G : 0, gB = groups ? (i0 + ni - 1) / G : 0;
-    if (lane < kGroupRuns) {
-      roff_s[w][0][lane] = groups ? groups[(long long)gA * kGroupRec + kGrpOff + lane] : 0;
-      roff_s[w][1][lane] = groups ? groups[(long long)gB * kGroupRec + kGrpOff + lane] : 0;
-    }
-    // running list lengths of a batch of up to 64 of the cell's particles:
-    // lane l holds particles ib + l and ib + 32 + l
-    for (int ib = 0; ib < ni; ib += 64) {
-    const int nb = min(ni - ib, 64);
-    int kq[2] = {0, 0}, hq[2] = {0, 0};
-    for (int m0 = 0; m0 < M; m0 += kCellCand) {
-      const int mend = min(M, m0 + kCellCand);
-      __syncwarp();
-      // stage candidates [m0, mend): run r covers [base_r, base_r + len_r)
-      for (int r = 0; r < kGroupRuns; ++r) {
-        const int rb = __shfl_sync(0xffffffffu, roff_base, r);
-        const int rn = __shfl_sync(0xffffffffu, rl, r);
-        const int r0 = __shfl_sync(0xffffffffu, rs, r);
-        const int lo = max(rb, m0), hi = min(rb + rn, mend);
-        for (int m = lo + lane; m < hi; m += 32) {
-          const int j = r0 + (m - rb);
-          cf[m - m0] = __ldg(pf + j);
-          cj[m - m0] = j;
-          cr[m - m0] = (uint8_t)r;
-        }
-      }
-      __syncwarp();
-      const int mc = mend - m0;
-      for (int ii = 0; ii < nb; ++ii) {
-        const int i = i0 + ib + ii;
-        const float4 pif = __ldg(pf + i);
-        const int gsel = (groups && i / G != gA) ? 1 : 0;
-        const int t = i >> 5, il = i & 31;
-        int32_t* out = nbr + (long long)t * stride;
-        int k = __shfl_sync(0xffffffffu, kq[ii >> 5], ii & 31);
-        int kh = __shfl_sync(0xffffffffu, hq[ii >> 5], ii & 31);
-        for (int q0 = 0; q0 < mc; q0 += 32) {
-          const int m = q0 + lane;
-          bool hit = false, band = false;
-          int j = -1;
-          if (m < mc) {
-            const float4 f = cf[m];
-            j = cj[m];
-            const float fx = pif.x - f.x, fy = pif.y - f.y, fz = pif.z - f.z;
-            const float r2f = fmaf(fz, fz, fmaf(fy, fy, fx * fx));
-            hit = r2f < rl2f_lo;
-            band = r2f >= rl2f_lo && r2f < rl2f_hi;
-            if (j == i) hit = band = false;  // self (owned run)
-          }
-          if (__any_sync(0xffffffffu, band) && band) {
-            const double4 pi = ld_pos4(pos4, i), pj = ld_pos4(pos4, j);
-            hit = r2_exact(pi.x - pj.x, pi.y - pj.y, pi.z - pj.z) < rl2;
-          }
-          const unsigned mask = __ballot_sync(0xffffffffu, hit);
-          if (hit) {
-            const int kk = k + __popc(mask & ((1u << lane) - 1u));
-            if (kk < cap_steps) {
-              const int r = cr[m];
-              out[(long long)(kk >> 2) * 128 + il * 4 + (kk & 3)] = j + roff_s[w][gsel][r];
-            }
-          }
-          k += __popc(mask);
-          kh += __popc(__ballot_sync(0xffffffffu, hit && (j >= n || j > i)));
-        }
-        if (lane == (ii & 31)) {
-          kq[ii >> 5] = k;
-          hq[ii >> 5] = kh;
-        }
-      }
-    }
-    // counts of the batch's particles
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int ii = h * 32 + lane;
-      if (ii < nb) {
-        count[i0 + ib + ii] = kq[h];
-        if (count_half) count_half[i0 + ib + ii] = hq[h];
-      }
-    }
-    }
-  }
 }
 
 // Per tile: step count = the longest list (4-step chunks, capped), idle
@@ -415,8 +269,8 @@ __global__ void vl_pad_kernel(int n, int ntiles, int cap_steps, const int32_t* _
   }
 }
 
-// Group run table for the staged lists (one warp per group, lane r < 18
-// scans run r's cells for its first and last particle).
+// Group run table for the staged lists (one warp per group; lane l scans
+// runs l and l + 32 for their first and last particle).
 __global__ void vl_group_kernel(GridK g, int n, int G, int scap, const double* __restrict__ pos4,
                                 const int32_t* __restrict__ os, const int32_t* __restrict__ oc,
                                 const int32_t* __restrict__ hs, const int32_t* __restrict__ hc,
@@ -430,14 +284,31 @@ __global__ void vl_group_kernel(GridK g, int n, int G, int scap, const double* _
                                      g.d0, g.d1, g.d2, g.t0, g.t1);
   const long long hi = cell_of_owned(ld_pos4(pos4, i1), g.lo0, g.lo1, g.lo2, g.cl0, g.cl1, g.cl2,
                                      g.d0, g.d1, g.d2, g.t0, g.t1);
-  int start = 0, len = 0;
-  if (lane < kGroupRuns) {
-    const int view = lane / 9, q = lane % 9, dz = q / 3 - 1, dy = q % 3 - 1;
+  const long long row_lo = lo / g.t0, row_hi = hi / g.t0;
+  // the group's particles must lie in row_lo or row_hi (rows in between are
+  // ring rows when the group crosses a z-plane); otherwise it gathers globally
+  bool two = true;
+  if (row_hi - row_lo > 1)
+    for (long long i = i0 + lane; i <= i1; i += 32) {
+      const long long r = cell_of_owned(ld_pos4(pos4, i), g.lo0, g.lo1, g.lo2, g.cl0, g.cl1,
+                                        g.cl2, g.d0, g.d1, g.d2, g.t0, g.t1) / g.t0;
+      two &= r == row_lo || r == row_hi;
+    }
+  const int R = row_hi == row_lo ? 1 : (__all_sync(0xffffffffu, two) ? 2 : 3);
+  int start[2] = {0, 0}, len[2] = {0, 0};
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int r = lane + 32 * h;
+    if (r >= kGroupRuns || R > 2) continue;
+    const int view = r / 18, rr = (r % 18) / 9, q = r % 9, dz = q / 3 - 1, dy = q % 3 - 1;
+    if (rr >= R) continue;
     const int32_t* vs = view ? hs : os;
     const int32_t* vc = view ? hc : oc;
-    const long long off = g.t0 * (dy + g.t1 * dz);
+    const long long xa = rr == 0 ? lo % g.t0 : 1;
+    const long long xb = rr == R - 1 ? hi % g.t0 : g.d0;
+    const long long nrow = (rr == 0 ? row_lo : row_hi) + dy + g.t1 * dz;
     int first = -1, last = -1;
-    for (long long c = lo - 1 + off; c <= hi + 1 + off; ++c) {
+    for (long long c = nrow * g.t0 + xa - 1; c <= nrow * g.t0 + xb + 1; ++c) {
       const int k = vc[c];
       if (k) {
         if (first < 0) first = vs[c];
@@ -445,31 +316,44 @@ __global__ void vl_group_kernel(GridK g, int n, int G, int scap, const double* _
       }
     }
     if (first >= 0) {
-      start = first & ~1;                 // 16-B aligned bulk copies
-      len = (last - start + 1) & ~1;
+      start[h] = first & ~1;                 // 16-B aligned bulk copies
+      len[h] = (last - start[h] + 1) & ~1;
     }
   }
-  // exclusive scan of the run lengths -> shared-memory bases
-  int incl = len;
+  // exclusive scan of the run lengths (runs 0..31, then 32..35) -> bases
+  int incl = len[0];
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
     const int v = __shfl_up_sync(0xffffffffu, incl, d);
     if (lane >= d) incl += v;
   }
-  const int base = incl - len;
-  const int S = __shfl_sync(0xffffffffu, incl, 31);
-  const int halo_base = __shfl_sync(0xffffffffu, base, 9);
-  const bool glob = S > scap;
+  const int totA = __shfl_sync(0xffffffffu, incl, 31);
+  int incl2 = len[1];
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl2, d);
+    if (lane >= d) incl2 += v;
+  }
+  const int base[2] = {incl - len[0], totA + incl2 - len[1]};
+  const int S = totA + __shfl_sync(0xffffffffu, incl2, 31);
+  const int halo_base = __shfl_sync(0xffffffffu, base[0], 18);  // run 18 = first image run
+  const bool glob = R > 2 || S > scap;
   int32_t* rec = groups + grp * kGroupRec;
-  if (lane < kGroupRuns) {
-    rec[kGrpStart + lane] = start;
-    rec[kGrpLen + lane] = len;
-    rec[kGrpOff + lane] = glob ? 0 : base - start;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int r = lane + 32 * h;
+    if (r < kGroupRuns) {
+      rec[kGrpStart + r] = glob ? 0 : start[h];
+      rec[kGrpLen + r] = glob ? 0 : len[h];
+      rec[kGrpOff + r] = glob ? 0 : base[h] - start[h];
+    }
   }
   if (lane == 0) {
-    rec[kGrpS] = S;
+    rec[kGrpS] = glob ? 0 : S;
     rec[kGrpHalo] = glob ? n : halo_base;
     rec[kGrpGlobal] = glob ? 1 : 0;
+    rec[kGrpRow] = (int)row_lo;
+    rec[kGrpRow + 1] = (int)row_hi;
     atomicMax(smax, glob ? 0 : S);
     if (glob) atomicAdd(smax + 1, 1);
   }
@@ -681,10 +565,31 @@ __device__ __forceinline__ void add_byte4(unsigned (&v)[4], int b, unsigned x) {
   else v[3] += inc;
 }
 
+// entries of one 128-bit list chunk: 4 int32 or 8 uint16 (0xffff / -1 /
+// sentinel = no entry -> -1)
+template <bool I16>
+__device__ __forceinline__ void unpack_chunk(const int4& v, int32_t sentinel, int* j) {
+  if (I16) {
+    const unsigned w4[4] = {(unsigned)v.x, (unsigned)v.y, (unsigned)v.z, (unsigned)v.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const unsigned lo = w4[e] & 0xffffu, hi = w4[e] >> 16;
+      j[2 * e] = lo == 0xffffu ? -1 : (int)lo;
+      j[2 * e + 1] = hi == 0xffffu ? -1 : (int)hi;
+    }
+  } else {
+    const int w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) j[e] = (w4[e] == sentinel || w4[e] < 0) ? -1 : w4[e];
+  }
+}
+
+template <bool I16>
 __global__ void __launch_bounds__(256)
     vl_bank_local_kernel(int ntiles, int B, int32_t sentinel, int tcap,
                          const long long* __restrict__ toff, const int32_t* __restrict__ kmax,
                          int32_t* __restrict__ nbr) {
+  constexpr int CH = I16 ? 8 : 4;  // entries per 128-bit chunk
   extern __shared__ __align__(128) uint16_t bank_ent[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int t = blockIdx.x * nw + w;
@@ -697,8 +602,9 @@ __global__ void __launch_bounds__(256)
   uint16_t* cur = cnt + 16 * 32;
   uint16_t* end = cur + 16 * 32;
   uint16_t* ent = end + 16 * 32;
-  int4* base4 = reinterpret_cast<int4*>(nbr + toff[t]);
-  const int nch = T / kChunk;
+  int4* base4 = I16 ? reinterpret_cast<int4*>(reinterpret_cast<uint16_t*>(nbr) + toff[t])
+                    : reinterpret_cast<int4*>(nbr + toff[t]);
+  const int nch = T / CH;
 #pragma unroll
   for (int b = 0; b < 16; ++b) cnt[b * 32 + lane] = 0;
   int n = 0;
@@ -711,12 +617,13 @@ __global__ void __launch_bounds__(256)
       v[q] = c0 + q < nch ? base4[(c0 + q) * 32 + lane] : make_int4(-1, -1, -1, -1);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const int j[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
+      int j[CH];
+      unpack_chunk<I16>(v[q], sentinel, j);
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (j[u] != sentinel && j[u] >= 0) {
+      for (int u = 0; u < CH; ++u)
+        if (j[u] >= 0) {
           ++cnt[(j[u] & 15) * 32 + lane];
-          wide |= j[u] > 0xffff;
+          wide |= j[u] > 0xfffe;
           ++n;
         }
     }
@@ -742,10 +649,11 @@ __global__ void __launch_bounds__(256)
       v[q] = c0 + q < nch ? base4[(c0 + q) * 32 + lane] : make_int4(-1, -1, -1, -1);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const int j[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
+      int j[CH];
+      unpack_chunk<I16>(v[q], sentinel, j);
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (j[u] != sentinel && j[u] >= 0) {
+      for (int u = 0; u < CH; ++u)
+        if (j[u] >= 0) {
           const int b = j[u] & 15;
           const int p = cur[b * 32 + lane];
           cur[b * 32 + lane] = (uint16_t)(p + 1);
@@ -758,10 +666,10 @@ __global__ void __launch_bounds__(256)
   for (int b = 0; b < 16; ++b) cur[b * 32 + lane] = (uint16_t)(end[b * 32 + lane] - cnt[b * 32 + lane]);
   const int hl = lane & 15;
   int lrem = n;
-  for (int s0 = 0; s0 < T; s0 += kChunk) {
-    int out[kChunk];
+  for (int s0 = 0; s0 < T; s0 += CH) {
+    int out[CH];
 #pragma unroll
-    for (int u = 0; u < kChunk; ++u) {
+    for (int u = 0; u < CH; ++u) {
       const int s = s0 + u;
       const int rot = (hl + s) & 15;
       int pick = -1;
@@ -779,7 +687,17 @@ __global__ void __launch_bounds__(256)
       }
       out[u] = j;
     }
-    base4[(s0 / kChunk) * 32 + lane] = make_int4(out[0], out[1], out[2], out[3]);
+    int4 o;
+    if (I16) {
+      unsigned w4[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        w4[e] = ((unsigned)out[2 * e] & 0xffffu) | (((unsigned)out[2 * e + 1] & 0xffffu) << 16);
+      o = make_int4((int)w4[0], (int)w4[1], (int)w4[2], (int)w4[3]);
+    } else {
+      o = make_int4(out[0], out[1], out[2], out[3]);
+    }
+    base4[(s0 / CH) * 32 + lane] = o;
   }
 }
 
@@ -1006,7 +924,7 @@ __device__ __forceinline__ void staged_pairs4(const double4& pi, const double* x
 constexpr int kStagedPrefetch = LMD_STAGED_PREFETCH;  // index chunks in flight
 constexpr int kStagedBatch = LMD_STAGED_BATCH;        // chunks evaluated together
 
-template <bool EV, int N3, int ROWS, bool STAGED>
+template <bool EV, int N3, int ROWS, bool STAGED, bool I16>
 __device__ __forceinline__ void vl_staged_tile(int t, int lane, int n_owned, int hb,
                                                unsigned dummy, unsigned long long* bar,
                                                const int32_t* __restrict__ out_perm,
@@ -1021,8 +939,13 @@ __device__ __forceinline__ void vl_staged_tile(int t, int lane, int n_owned, int
                                                double* __restrict__ fy, double* __restrict__ fz) {
   const int i = t * 32 + lane;
   const bool iact = i < n_owned;
-  const int4* chunks = reinterpret_cast<const int4*>(nbr + toff[t]) + lane;
-  const int nchunks = kmax[t] / kChunk;
+  // I16: 16-bit local rows, 8 steps per 128-bit chunk (else 32-bit, 4 steps)
+  constexpr int CH = I16 ? 8 : 4;
+  const int4* chunks =
+      (I16 ? reinterpret_cast<const int4*>(reinterpret_cast<const uint16_t*>(nbr) + toff[t])
+           : reinterpret_cast<const int4*>(nbr + toff[t])) +
+      lane;
+  const int nchunks = kmax[t] / CH;
   // the tile's whole index list towards L2 first (one bulk prefetch), so the
   // streamed chunk loads below see L2, not HBM, latency
   if (lane == 0 && nchunks > 0)
@@ -1035,8 +958,7 @@ __device__ __forceinline__ void vl_staged_tile(int t, int lane, int n_owned, int
   // register move waits on an outstanding load).  Slots are evaluated in
   // batches of kStagedBatch chunks; the positions of batch b + 1 are loaded
   // while batch b is evaluated.
-  constexpr int R = kStagedPrefetch, NB = kStagedBatch, NS = 4 * NB;
-  static_assert(R % NB == 0, "ring must hold whole batches");
+  constexpr int NB = I16 ? 1 : kStagedBatch, R = 2 * NB, NS = CH * NB;
   int4 ring[R];
 #pragma unroll
   for (int d = 0; d < R; ++d)
@@ -1046,11 +968,20 @@ __device__ __forceinline__ void vl_staged_tile(int t, int lane, int n_owned, int
 #pragma unroll
     for (int q = 0; q < NB; ++q) {
       const int4 v = ring[(d0 + q) % R];
-      // idle slots (-1) read the dummy row
-      j[4 * q + 0] = min((unsigned)v.x, dummy);
-      j[4 * q + 1] = min((unsigned)v.y, dummy);
-      j[4 * q + 2] = min((unsigned)v.z, dummy);
-      j[4 * q + 3] = min((unsigned)v.w, dummy);
+      // idle slots (-1 / 0xffff) read the dummy row
+      if (I16) {
+        const unsigned w4[4] = {(unsigned)v.x, (unsigned)v.y, (unsigned)v.z, (unsigned)v.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          j[8 * q + 2 * e] = min(w4[e] & 0xffffu, dummy);
+          j[8 * q + 2 * e + 1] = min(w4[e] >> 16, dummy);
+        }
+      } else {
+        j[4 * q + 0] = min((unsigned)v.x, dummy);
+        j[4 * q + 1] = min((unsigned)v.y, dummy);
+        j[4 * q + 2] = min((unsigned)v.z, dummy);
+        j[4 * q + 3] = min((unsigned)v.w, dummy);
+      }
     }
 #pragma unroll
     for (int u = 0; u < NS; ++u) {
@@ -1066,7 +997,6 @@ __device__ __forceinline__ void vl_staged_tile(int t, int lane, int n_owned, int
     }
   };
   // two batch buffers used in turn (ping-pong: no register moves)
-  static_assert(R == 2 * NB, "the ring holds exactly two batches");
   unsigned jA[NS], jB[NS];
   double xA[NS], yA[NS], zA[NS], xB[NS], yB[NS], zB[NS];
   auto refill = [&](int d, int c) {
@@ -1081,14 +1011,14 @@ __device__ __forceinline__ void vl_staged_tile(int t, int lane, int n_owned, int
     refill(0, c0);
     load_batch(NB, jB, xB, yB, zB);
 #pragma unroll
-    for (int q = 0; q < NB; ++q)
+    for (int q = 0; q < NS / 4; ++q)
       staged_pairs4<EV, N3>(pi, xA + 4 * q, yA + 4 * q, zA + 4 * q, jA + 4 * q, hb, k, a);
     if (c0 + NB >= nchunks) break;
     // batch B = chunks c0 + NB .. c0 + R - 1 (ring slots NB .. R - 1)
     refill(NB, c0 + NB);
     load_batch(0, jA, xA, yA, zA);
 #pragma unroll
-    for (int q = 0; q < NB; ++q)
+    for (int q = 0; q < NS / 4; ++q)
       staged_pairs4<EV, N3>(pi, xB + 4 * q, yB + 4 * q, zB + 4 * q, jB + 4 * q, hb, k, a);
   }
   if (iact) {
@@ -1100,7 +1030,7 @@ __device__ __forceinline__ void vl_staged_tile(int t, int lane, int n_owned, int
 }
 
 // 16 warps per SM (shared memory bounds it): up to 128 registers per thread
-template <bool EV, int N3, int W>
+template <bool EV, int N3, int W, bool I16>
 __global__ void __launch_bounds__(32 * W, 16 / W)
     vl_staged_kernel(int n_owned, int ntiles, int sentinel, const int32_t* __restrict__ out_perm,
                      const double* __restrict__ pos4, SoA q, const int32_t* __restrict__ groups,
@@ -1124,16 +1054,16 @@ __global__ void __launch_bounds__(32 * W, 16 / W)
       xs[3 * ROWS - 1] = 1.0e30;
     }
     __syncthreads();
-    // warp 0: lane 0 arms the barrier, then lane r < 18 issues run r's
-    // three bulk copies (issuing 54 copies from one thread serialises them)
+    // warp 0: lane 0 arms the barrier, then lane l issues the three bulk
+    // copies of runs l and l + 32 (one thread issuing them all serialises)
     if (threadIdx.x < 32) {
       if (lane == 0) mbar_expect_tx(&bar, (unsigned)rec[kGrpS] * 3u * 8u);
       __syncwarp();
-      if (lane < kGroupRuns) {
-        const int len = rec[kGrpLen + lane];
+      for (int r = lane; r < kGroupRuns; r += 32) {
+        const int len = rec[kGrpLen + r];
         if (len) {
-          const int st = rec[kGrpStart + lane];
-          const int base = st + rec[kGrpOff + lane];
+          const int st = rec[kGrpStart + r];
+          const int base = st + rec[kGrpOff + r];
           bulk_g2s(xs + base, q.x + st, (unsigned)len * 8u, &bar);
           bulk_g2s(xs + ROWS + base, q.y + st, (unsigned)len * 8u, &bar);
           bulk_g2s(xs + 2 * ROWS + base, q.z + st, (unsigned)len * 8u, &bar);
@@ -1149,11 +1079,11 @@ __global__ void __launch_bounds__(32 * W, 16 / W)
   }
   Acc a = {0.0, 0.0, 0.0, 0.0, 0.0, 0, 0, 0};
   if (glob)
-    vl_staged_tile<EV, N3, ROWS, false>(t, lane, n_owned, hb, (unsigned)sentinel, nullptr,
+    vl_staged_tile<EV, N3, ROWS, false, I16>(t, lane, n_owned, hb, (unsigned)sentinel, nullptr,
                                         out_perm, pos4,
                                         q.x, q.y, q.z, toff, kmax, nbr, k, a, fx, fy, fz);
   else
-    vl_staged_tile<EV, N3, ROWS, true>(t, lane, n_owned, hb, (unsigned)(ROWS - 1),
+    vl_staged_tile<EV, N3, ROWS, true, I16>(t, lane, n_owned, hb, (unsigned)(ROWS - 1),
                                        (dbg & 2) ? nullptr : &bar, out_perm,
                                        pos4, xs, xs, xs, toff, kmax, nbr, k, a, fx, fy, fz);
   a.overlap |= a.hi_min == 0u;
@@ -1266,16 +1196,26 @@ static int vl_build_impl(const lmd_grid* g, double rl2, int newton3, int pattern
                          int32_t cap_steps, int32_t* count, int32_t* count_half,
                          int64_t* tile_off, int32_t* kmax, int32_t* max_count, int32_t* nbr,
                          const int32_t* staged_groups, int staged_G, const float4* pf,
-                         float rl2f_lo, float rl2f, void* stream) {
+                         float rl2f_lo, float rl2f, void* stream, bool idx16 = false) {
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e = cudaMemsetAsync(max_count, 0, sizeof(int32_t), s);
   if (e != cudaSuccess) return set_cuda_error(e);
   if (n_owned <= 0) return LMD_OK;
-  if (n_owned > 0x7fffffffLL || cap_steps <= 0 || cap_steps % kChunk) return LMD_ERR_CONFIG;
+  if (n_owned > 0x7fffffffLL || cap_steps <= 0 || cap_steps % (idx16 ? 8 : kChunk))
+    return LMD_ERR_CONFIG;
   const int A = pattern_A(pattern), B = pattern_B(pattern);
   const int64_t ntiles = cdiv(n_owned, A);
   const unsigned blocks = (unsigned)cdiv(ntiles * A, 128);
   const int32_t* groups = staged_groups;
+  if (idx16) {
+    if (pattern != LMD_V_BY_ONE || !groups) return LMD_ERR_CONFIG;
+    vl_build_kernel<LMD_V_BY_ONE, false, uint16_t><<<blocks, 128, 0, s>>>(
+        make_gridk(g), (int)n_owned, (int)ntiles, newton3, rl2, 0xffff, pos4, o_start, o_count,
+        h_start, h_count, cap_steps, count, count_half, (long long*)tile_off, kmax, max_count,
+        nbr, groups, staged_G, pf, rl2f_lo, rl2f);
+    LMD_CHECK_LAUNCH();
+    return LMD_OK;
+  }
   const int G = staged_G;
 #define LMD_VLB_(P, PFB)                                                                             \
   vl_build_kernel<P, PFB><<<blocks, 128, 0, s>>>(make_gridk(g), (int)n_owned, (int)ntiles, newton3, \
@@ -1316,34 +1256,18 @@ int lmd_vl_build(const lmd_grid* g, double rl2, int newton3, int pattern, int64_
 int lmd_vl_build_staged(const lmd_grid* g, double rl2, int newton3, int64_t n_owned,
                         const double* pos4, const int32_t* o_start, const int32_t* o_count,
                         const int32_t* h_start, const int32_t* h_count, int32_t group_size,
-                        const int32_t* groups, const float* pf, float rl2f_lo, float rl2f_hi,
-                        int32_t cap_steps, int32_t* count, int32_t* count_half,
-                        int64_t* tile_off, int32_t* kmax, int32_t* max_count, int32_t* nbr,
-                        void* stream) {
+                        const int32_t* groups, int32_t index_bits, const float* pf,
+                        float rl2f_lo, float rl2f_hi, int32_t cap_steps, int32_t* count,
+                        int32_t* count_half, int64_t* tile_off, int32_t* kmax,
+                        int32_t* max_count, int32_t* nbr, void* stream) {
   if (group_size <= 0 || group_size % 32) return LMD_ERR_CONFIG;
   if (pf && !(rl2f_lo < rl2f_hi)) return LMD_ERR_CONFIG;
-  if (!pf || newton3)
-    return vl_build_impl(g, rl2, newton3, LMD_V_BY_ONE, n_owned, -1, pos4, o_start, o_count,
-                         h_start, h_count, cap_steps, count, count_half, tile_off, kmax,
-                         max_count, nbr, groups, group_size, reinterpret_cast<const float4*>(pf),
-                         rl2f_lo, rl2f_hi, stream);
-  // cell-cooperative build (cells of at most 64 owned particles)
-  cudaStream_t s = (cudaStream_t)stream;
-  cudaError_t e = cudaMemsetAsync(max_count, 0, sizeof(int32_t), s);
-  if (e != cudaSuccess) return set_cuda_error(e);
-  if (n_owned <= 0) return LMD_OK;
-  if (n_owned > 0x7fffffffLL || cap_steps <= 0 || cap_steps % kChunk) return LMD_ERR_CONFIG;
-  const long long ncell = g->ncell;
-  vl_build_cells_kernel<<<1184, 32 * kCellWarps, 0, s>>>(
-      make_gridk(g), ncell, (int)n_owned, rl2, rl2f_lo, rl2f_hi, pos4,
-      reinterpret_cast<const float4*>(pf), o_start, o_count, h_start, h_count, groups,
-      group_size, cap_steps, count, count_half, nbr);
-  LMD_CHECK_LAUNCH();
-  const int64_t ntiles = cdiv(n_owned, 32);
-  vl_pad_kernel<<<(unsigned)cdiv(ntiles * 32, 256), 256, 0, s>>>(
-      (int)n_owned, (int)ntiles, cap_steps, count, (long long*)tile_off, kmax, max_count, nbr);
-  LMD_CHECK_LAUNCH();
-  return LMD_OK;
+  if (index_bits != 16 && index_bits != 32) return LMD_ERR_CONFIG;
+  if (index_bits == 16 && pf) return LMD_ERR_CONFIG;
+  return vl_build_impl(g, rl2, newton3, LMD_V_BY_ONE, n_owned, -1, pos4, o_start, o_count,
+                       h_start, h_count, cap_steps, count, count_half, tile_off, kmax, max_count,
+                       nbr, groups, group_size, reinterpret_cast<const float4*>(pf), rl2f_lo,
+                       rl2f_hi, stream, index_bits == 16);
 }
 
 int lmd_vl_prefilter_rows(int64_t rows, const double* pos4, const double* center, float* pf,
@@ -1377,10 +1301,13 @@ size_t lmd_vl_bank_smem_per_warp(int32_t cap_steps) {
 }
 
 int lmd_vl_bank_schedule(int pattern, int64_t n_units, int32_t sentinel, int rounds,
-                         int32_t cap_steps, int32_t max_steps, const int64_t* tile_off,
-                         const int32_t* kmax, int32_t* nbr, void* stream) {
+                         int32_t cap_steps, int32_t max_steps, int32_t index_bits,
+                         const int64_t* tile_off, const int32_t* kmax, int32_t* nbr,
+                         void* stream) {
   if (n_units <= 0) return LMD_OK;
   if (rounds < 0 || rounds > 16 || cap_steps <= 0 || cap_steps % kChunk) return LMD_ERR_CONFIG;
+  if (index_bits != 16 && index_bits != 32) return LMD_ERR_CONFIG;
+  if (index_bits == 16 && (rounds != 0 || cap_steps % 8)) return LMD_ERR_CONFIG;
   const int B = pattern_B(pattern);
   const int64_t ntiles = cdiv(n_units, pattern_A(pattern));
   cudaStream_t st = (cudaStream_t)stream;
@@ -1391,10 +1318,11 @@ int lmd_vl_bank_schedule(int pattern, int64_t n_units, int32_t sentinel, int rou
     const size_t per = (48 * 32 + (size_t)tcap * 32) * sizeof(uint16_t);
     int nwl = (int)(72 * 1024 / per);
     nwl = nwl < 1 ? 1 : (nwl > 8 ? 8 : nwl);
-    cudaError_t e0 = cudaFuncSetAttribute(
-        vl_bank_local_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(per * nwl));
+    auto kern = index_bits == 16 ? vl_bank_local_kernel<true> : vl_bank_local_kernel<false>;
+    cudaError_t e0 =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(per * nwl));
     if (e0 != cudaSuccess) return set_cuda_error(e0);
-    vl_bank_local_kernel<<<(unsigned)cdiv(ntiles, nwl), 32 * nwl, per * nwl, st>>>(
+    kern<<<(unsigned)cdiv(ntiles, nwl), 32 * nwl, per * nwl, st>>>(
         (int)ntiles, B, sentinel, tcap, (const long long*)tile_off, kmax, nbr);
     LMD_CHECK_LAUNCH();
     return LMD_OK;
@@ -1522,7 +1450,7 @@ int32_t lmd_vl_staged_capacity(int32_t group_size) {
 
 int lmd_force_vl_staged(int newton3, int flags, const lmd_lj* lj, int64_t n_owned,
                         const double* pos4, const double* soa, int64_t stride, int32_t sentinel,
-                        int32_t group_size, const int32_t* groups,
+                        int32_t group_size, const int32_t* groups, int32_t index_bits,
                         const int64_t* tile_off, const int32_t* kmax, const int32_t* nbr,
                         const int32_t* out_perm, double* fx, double* fy, double* fz,
                         double* ev_scratch, lmd_stats* stats, void* stream) {
@@ -1530,6 +1458,8 @@ int lmd_force_vl_staged(int newton3, int flags, const lmd_lj* lj, int64_t n_owne
   if (newton3 != 0 && newton3 != 2) return LMD_ERR_CONFIG;
   if (!soa || stride % 16 || sentinel < 0 || sentinel >= stride) return LMD_ERR_CONFIG;
   if (group_size != 128 && group_size != 256 && group_size != 512) return LMD_ERR_CONFIG;
+  if (index_bits != 16 && index_bits != 32) return LMD_ERR_CONFIG;
+  const bool idx16 = index_bits == 16;
   const LJK k = make_ljk(lj);
   const int64_t ntiles = cdiv(n_owned, 32);
   const int64_t ngroups = cdiv(n_owned, group_size);
@@ -1539,7 +1469,7 @@ int lmd_force_vl_staged(int newton3, int flags, const lmd_lj* lj, int64_t n_owne
   const size_t smem = (size_t)stage_rows(group_size) * 3 * sizeof(double);
 #define LMD_VLS(EVB, N3B, W)                                                                   \
   do {                                                                                         \
-    auto kern = vl_staged_kernel<EVB, N3B, W>;                                                 \
+    auto kern = idx16 ? vl_staged_kernel<EVB, N3B, W, true> : vl_staged_kernel<EVB, N3B, W, false>; \
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
                                          (int)smem);                                          \
     if (e != cudaSuccess) return set_cuda_error(e);                                            \

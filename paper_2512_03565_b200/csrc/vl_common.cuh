@@ -10,17 +10,20 @@ constexpr int kChunk = 4;  // fill steps per lane per 128-bit index load
 
 // Staged Verlet lists (v_by_one): a group of G consecutive owned particles
 // (G/32 tiles, one block) copies the SoA positions of its candidate runs
-// into shared memory.  Run r = view * 9 + (dz + 1) * 3 + (dy + 1) covers the
-// cells lin_lo - 1 + off .. lin_hi + 1 + off (off = t0 * (dy + t1 * dz)) of
-// the owned (view 0) or image (view 1) backing: one contiguous index range.
+// into shared memory.  The group's particles lie in one or two cell rows
+// (rows are (y, z) lines of the ring-padded grid, row = lin / t0); for row
+// rr of the group and each (dy, dz), run r = view * 18 + rr * 9 +
+// (dz + 1) * 3 + (dy + 1) covers the cells xa - 1 .. xb + 1 of the
+// neighbouring row (xa .. xb = the group's cells in its row) of the owned
+// (view 0) or image (view 1) backing: one contiguous index range.
 // Per-group record of kGroupRec int32: run starts (even), lengths (even),
 // local-index offsets (base - start), then S, the first image-run local
-// index, and a flag (1: S > capacity, the group gathers from global memory
-// with global indices).
-constexpr int kGroupRec = 64;
-constexpr int kGrpStart = 0, kGrpLen = 18, kGrpOff = 36, kGrpS = 54, kGrpHalo = 55,
-              kGrpGlobal = 56;
-constexpr int kGroupRuns = 18;
+// index, a flag (1: more than two rows or S > capacity -- the group gathers
+// from global memory with global indices) and the group's first row.
+constexpr int kGroupRuns = 36;
+constexpr int kGroupRec = 128;
+constexpr int kGrpStart = 0, kGrpLen = 36, kGrpOff = 72, kGrpS = 108, kGrpHalo = 109,
+              kGrpGlobal = 110, kGrpRow = 111;
 
 // lane holding (i_off = il, j_off = jo) of a pattern (inverse of Pattern<P>)
 __device__ __forceinline__ int lane_of(int pattern, int il, int jo) {

@@ -71,6 +71,8 @@ class VerletListContainer:
         # csrc/vl.cu vl_build_cells_kernel; measured 3.8 ms vs 1.0 ms at 1M,
         # latency-bound at 14 warps/SM); False = thread per particle, FP64 tests
         self.build_fp32 = False
+        # staged lists with every group staged store 16-bit local rows
+        self.index16 = True
         # particles per lane sharing one union list (csrc/vl_ci.cu) for full
         # lists; 1 = one list per particle (csrc/vl.cu)
         self.i_cluster = 1   # CI = 2 or 4 measured 2-3x slower
@@ -366,19 +368,26 @@ class VerletListContainer:
         if staged and n:
             pf, rl2f_lo, rl2f_hi = self._prefilter_rows()
             ngroups = (n + staged - 1) // staged
-            groups = torch.empty(ngroups * 64, dtype=torch.int32, device=dev)
+            groups = torch.empty(ngroups * 128, dtype=torch.int32, device=dev)
             smax = torch.zeros(2, dtype=torch.int32, device=dev)
             capacity = int(N.load().lmd_vl_staged_capacity(staged))
             N.call("lmd_vl_groups", self.grid, n, staged, capacity, *tables,
                    N.ptr(groups), N.ptr(smax), s)
             sentinel = -1
+            # 16-bit local rows when every group is staged (one host read)
+            sm = smax.tolist()
+            bits = 16 if (sm[1] == 0 and self.index16 and not self.build_fp32) else 32
+        else:
+            bits = 32
+        chunk = 8 if bits == 16 else 4
         while True:
             steps = (cap + b_ - 1) // b_
-            cap_steps = max(4, (steps + 3) // 4 * 4)
-            nbr = torch.empty(max(ntiles * cap_steps * 32, 1), dtype=torch.int32, device=dev)
+            cap_steps = max(chunk, (steps + chunk - 1) // chunk * chunk)
+            words = ntiles * cap_steps * 32 * bits // 32
+            nbr = torch.empty(max(words, 1), dtype=torch.int32, device=dev)
             if staged and n:
                 N.call("lmd_vl_build_staged", self.grid, float(rl2), int(newton3), n, *tables,
-                       staged, N.ptr(groups), N.ptr(pf) if self.build_fp32 else None,
+                       staged, N.ptr(groups), bits, N.ptr(pf) if self.build_fp32 else None,
                        rl2f_lo, rl2f_hi, cap_steps,
                        N.ptr(count),
                        N.ptr(half) if half is not None else None, N.ptr(tile_off),
@@ -407,15 +416,16 @@ class VerletListContainer:
         # lane-local order: 16-bit workspace, staged lists only
         if bank == 0 and not staged:
             bank = -1
+        if bank > 0 and bits == 16:
+            bank = 0    # the warp-cooperative order is 32-bit only
         if bank >= 0 and units:
-            max_steps = min(cap_steps, ((longest + b_ - 1) // b_ + 3) // 4 * 4)
+            max_steps = min(cap_steps, ((longest + b_ - 1) // b_ + chunk - 1) // chunk * chunk)
             if bank > 0 or max_steps <= 255:
                 N.call("lmd_vl_bank_schedule", pattern.code, units, sentinel, int(bank), cap_steps,
-                       max_steps, N.ptr(tile_off), N.ptr(kmax), N.ptr(nbr), s)
+                       max_steps, bits, N.ptr(tile_off), N.ptr(kmax), N.ptr(nbr), s)
         if staged and n:
-            sm = smax.tolist()
             rows = max(16, (int(sm[0]) + 15) // 16 * 16)
-            self._staging[key] = (groups, rows, staged, int(sm[1]))
+            self._staging[key] = (groups, rows, staged, int(sm[1]), bits)
         hit = (tile_off, kmax, nbr, ntiles * cap_steps * 32)
         self._lists[key] = hit
         return hit
@@ -516,13 +526,13 @@ class VerletListContainer:
                                  self._staged_for(pattern, n3l, ci)
                                  if self.align_window == 0 else 0))
         if stg is not None and mode != 1:
-            groups, _, gsize, _ = stg
+            groups, _, gsize, _, bits = stg
             direct = out is not None and len(out) == self.n_owned
             fx, fy, fz = ((out.force_x, out.force_y, out.force_z) if direct
                           else (self._fx, self._fy, self._fz))
             N.call("lmd_force_vl_staged", mode, (N.FLAG_ENERGY if energy else 0) | self.knobs,
                    N.make_lj(self.params), self.n_owned, N.ptr(self._pos4), N.ptr(self._soa),
-                   self._soa.shape[1], self.n_owned + self.n_halo, gsize, N.ptr(groups),
+                   self._soa.shape[1], self.n_owned + self.n_halo, gsize, N.ptr(groups), bits,
                    N.ptr(tile_off), N.ptr(kmax),
                    N.ptr(nbr), N.ptr(self._perm) if direct else None, N.ptr(fx), N.ptr(fy),
                    N.ptr(fz), N.ptr(ev_t), N.ptr(stats_t), N.stream())

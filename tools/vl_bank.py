@@ -47,12 +47,19 @@ def timed(fn, reps=6):
 
 def lanes_view(pat, newton3=False):
     """(ntiles, steps_cap, 32) view of the list plus per-tile step counts."""
-    tile_off, kmax, nbr, total = cont._lists[next(k for k in cont._lists
-                                                  if k[0] == pat.code)]
+    key = next(k for k in cont._lists if k[0] == pat.code)
+    tile_off, kmax, nbr, total = cont._lists[key]
+    stg = cont._staging.get(key)
+    bits = stg[4] if stg else 32
     ntiles = int(N.load().lmd_vl_num_tiles(cont.n_owned, pat.code))
     b = pat.shape(32)[1]
     cap = total // (ntiles * 32)
-    v = nbr[: ntiles * cap * 32].view(ntiles, cap // 4, 32, 4).permute(0, 1, 3, 2)
+    if bits == 16:
+        u = nbr.view(torch.int16).long() & 0xFFFF
+        u = torch.where(u == 0xFFFF, torch.full_like(u, -1), u)
+        v = u[: ntiles * cap * 32].view(ntiles, cap // 8, 32, 8).permute(0, 1, 3, 2)
+    else:
+        v = nbr[: ntiles * cap * 32].view(ntiles, cap // 4, 32, 4).permute(0, 1, 3, 2)
     return v.reshape(ntiles, cap, 32), (kmax[:ntiles] // b).long(), cont.n_owned + cont.n_halo
 
 
@@ -107,7 +114,7 @@ for pname in patterns:
         if grp:
             same = None
             stg = next(iter(cont._staging.values()))
-            extra = {"smem_rows": stg[1], "groups_over_capacity": stg[3]}
+            extra = {"smem_rows": stg[1], "groups_over_capacity": stg[3], "index_bits": stg[4]}
         else:
             srt = lane_sorted(v, steps, sentinel)
             if ref_sorted is None:
