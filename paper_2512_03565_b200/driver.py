@@ -45,6 +45,10 @@ def force_phase(owned, box, params, config: Configuration, vector_width: int,
     dev_owned = device_soa(owned)
     cont = make_container(config.container, box, params,
                           cluster_size=config.cluster_size or cluster_size or vector_width)
+    if hasattr(cont, "bank_rounds"):
+        # one force phase on a temporary container: the bank-aware list order
+        # pays for its pass only when lists are reused
+        cont.bank_rounds = -1
     cont.rebuild(dev_owned)
     cont.refresh(dev_owned)
     stats = cont.compute_forces(config.traversal, config.newton3, as_pattern(config.pattern),
