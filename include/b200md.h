@@ -335,9 +335,21 @@ int lmd_vl_build_staged(const lmd_grid* g, double rl2, int newton3, int64_t n_ow
  * of r2 for the coordinate range, so the pair set is the exact one. */
 int lmd_vl_prefilter_rows(int64_t rows, const double* pos4, const double* center, float* pf,
                           void* stream);
+/* Staged lists, per group of group_size particles (<= 256): deal the
+ * group's particles to lanes by descending list length (count[]), copy each
+ * particle's entries from its build slot to the new slot (same capacity,
+ * fresh tile offsets / step counts) and, with bank != 0, in the lane-local
+ * bank order (max_steps as for lmd_vl_bank_schedule).  slot_particle[t*32+l]
+ * = particle at tile t, lane l (-1: none); pass it to lmd_force_vl_staged. */
+int lmd_vl_reorder(int64_t n_owned, int32_t group_size, int32_t index_bits, int32_t cap_steps,
+                   int32_t max_steps, int bank, int32_t sentinel, const int32_t* count,
+                   const int64_t* tile_off, const int32_t* kmax, const int32_t* nbr,
+                   int32_t* slot_particle, int64_t* tile_off_out, int32_t* kmax_out,
+                   int32_t* nbr_out, void* stream);
 int lmd_force_vl_staged(int newton3, int flags, const lmd_lj* lj, int64_t n_owned,
                         const double* pos4, const double* soa, int64_t stride, int32_t sentinel,
                         int32_t group_size, const int32_t* groups, int32_t index_bits,
+                        const int32_t* slot_particle,
                         const int64_t* tile_off, const int32_t* kmax, const int32_t* nbr,
                         const int32_t* out_perm, double* fx, double* fy, double* fz,
                         double* ev_scratch, lmd_stats* stats, void* stream);

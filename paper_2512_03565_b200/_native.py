@@ -179,7 +179,9 @@ _sig("lmd_vl_build_staged", _INT, C.POINTER(Grid), _D, _INT, _I64, _VP, _VP, _VP
 _sig("lmd_vl_prefilter_rows", _INT, _I64, _VP, _VP, _VP, _VP)
 _sig("lmd_vl_staged_capacity", _I32, _I32)
 _sig("lmd_force_vl_staged", _INT, _INT, _INT, C.POINTER(LJ), _I64, _VP, _VP, _I64, _I32, _I32, _VP,
-     _I32, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP)
+     _I32, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP)
+_sig("lmd_vl_reorder", _INT, _I64, _I32, _I32, _I32, _I32, _INT, _I32, _VP, _VP, _VP, _VP, _VP, _VP,
+     _VP, _VP, _VP)
 _sig("lmd_vl_bank_schedule", _INT, _INT, _I64, _I32, _INT, _I32, _I32, _I32, _VP, _VP, _VP, _VP)
 _sig("lmd_vl_ci_build", _INT, C.POINTER(Grid), _D, _INT, _INT, _I64, _VP, _VP, _I32, _VP, _VP,
      _VP, _VP, _VP, _I32, _VP, _VP, _VP, _VP, _VP, _VP)

@@ -16,6 +16,7 @@
 // contiguous bytes per chunk.  Tiles are padded to a whole number of chunks
 // with a sentinel particle far away.  Lists are ascending in j.
 #include <cub/cub.cuh>
+#include <type_traits>
 
 #include "vl_common.cuh"
 
@@ -701,6 +702,116 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Staged lists, per group (one block of W warps = the group's W tiles):
+// re-deal the group's particles to lanes by descending list length (a tile
+// then holds lanes of similar length, so less padding up to its longest
+// list), copy every particle's entries from its build slot to its new slot
+// and, with `bank`, in the lane-local bank order of vl_bank_local_kernel.
+// slot_particle[t * 32 + l] = the particle at tile t, lane l (-1: none).
+template <bool I16>
+__global__ void __launch_bounds__(256)
+    vl_reorder_kernel(int n, int ntiles, int tcap, int cap_steps, int bank, int32_t sentinel,
+                      const int32_t* __restrict__ count, const long long* __restrict__ toff_in,
+                      const int32_t* __restrict__ kmax_in, const int32_t* __restrict__ nbr_in,
+                      int32_t* __restrict__ slot_particle, long long* __restrict__ toff_out,
+                      int32_t* __restrict__ kmax_out, int32_t* __restrict__ nbr_out) {
+  constexpr int CH = I16 ? 8 : 4;
+  extern __shared__ __align__(128) uint16_t bank_ent[];
+  __shared__ int cnt_s[256];
+  __shared__ int src_s[256];
+  const int G = blockDim.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int i0 = blockIdx.x * G;
+  // ranks by (count desc, index asc)
+  const int p = threadIdx.x;
+  const int cp = i0 + p < n ? count[i0 + p] : -1;
+  cnt_s[p] = cp;
+  __syncthreads();
+  int rank = 0;
+  for (int q = 0; q < G; ++q) {
+    const int cq = cnt_s[q];
+    rank += (cq > cp) || (cq == cp && q < p);
+  }
+  src_s[rank] = p;
+  __syncthreads();
+  const int t = blockIdx.x * (G / 32) + w;
+  if (t >= ntiles) return;  // warp-uniform; no block barrier follows
+  const int ps = src_s[w * 32 + lane];
+  const int i = i0 + ps < n ? i0 + ps : -1;
+  const int c = i >= 0 ? min(cnt_s[ps], cap_steps) : 0;
+  int m = c;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  const int T = (m + CH - 1) / CH * CH;
+  const long long stride = (long long)cap_steps * 32;
+  slot_particle[t * 32 + lane] = i;
+  if (lane == 0) {
+    kmax_out[t] = T;
+    toff_out[t] = (long long)t * stride;
+  }
+  // the particle's column in the build layout
+  const int ot = i >= 0 ? i >> 5 : 0, ol = i >= 0 ? i & 31 : 0;
+  typedef typename std::conditional<I16, uint16_t, int32_t>::type IDX;
+  const IDX* src = reinterpret_cast<const IDX*>(nbr_in) + toff_in[ot];
+  IDX* dst = reinterpret_cast<IDX*>(nbr_out) + (long long)t * stride;
+  auto src_at = [&](int s) -> int {
+    const IDX v = src[(long long)(s / CH) * (32 * CH) + ol * CH + s % CH];
+    return I16 ? (int)(uint16_t)v : (int)v;
+  };
+  auto put = [&](int s, int j) {
+    dst[(long long)(s / CH) * (32 * CH) + lane * CH + s % CH] =
+        I16 ? (IDX)(j < 0 ? 0xffff : j) : (IDX)(j < 0 ? sentinel : j);
+  };
+  if (!bank || T > tcap) {
+    for (int s = 0; s < T; ++s) put(s, s < c ? src_at(s) : -1);
+    return;
+  }
+  // bank order (vl_bank_local_kernel): bucket by bank pair, Latin-square walk
+  uint16_t* bc = bank_ent + (size_t)w * (48 * 32 + (size_t)tcap * 32);
+  uint16_t* cur = bc + 16 * 32;
+  uint16_t* end = cur + 16 * 32;
+  uint16_t* ent = end + 16 * 32;
+#pragma unroll
+  for (int b = 0; b < 16; ++b) bc[b * 32 + lane] = 0;
+  for (int s = 0; s < c; ++s) ++bc[(src_at(s) & 15) * 32 + lane];
+  unsigned avail = 0u;
+  int acc = 0;
+#pragma unroll
+  for (int b = 0; b < 16; ++b) {
+    const int k = bc[b * 32 + lane];
+    cur[b * 32 + lane] = (uint16_t)acc;
+    acc += k;
+    end[b * 32 + lane] = (uint16_t)acc;
+    avail |= (k ? 1u : 0u) << b;
+  }
+  for (int s = 0; s < c; ++s) {
+    const int j = src_at(s), b = j & 15;
+    const int q = cur[b * 32 + lane];
+    cur[b * 32 + lane] = (uint16_t)(q + 1);
+    ent[q * 32 + lane] = (uint16_t)j;
+  }
+#pragma unroll
+  for (int b = 0; b < 16; ++b) cur[b * 32 + lane] = (uint16_t)(end[b * 32 + lane] - bc[b * 32 + lane]);
+  const int hl = lane & 15;
+  int lrem = c;
+  for (int s = 0; s < T; ++s) {
+    const int rot = (hl + s) & 15;
+    int pick = -1;
+    if (lrem > 0) {
+      if ((avail >> rot) & 1u) pick = rot;
+      else if (T - s <= lrem) pick = first_rot16(avail, rot);
+    }
+    int j = -1;
+    if (pick >= 0) {
+      const int q = cur[pick * 32 + lane];
+      j = ent[q * 32 + lane];
+      cur[pick * 32 + lane] = (uint16_t)(q + 1);
+      if (q + 1 == end[pick * 32 + lane]) avail &= ~(1u << pick);
+      --lrem;
+    }
+    put(s, j);
+  }
+}
+
 __global__ void vl_prefilter_kernel(int64_t rows, const double* __restrict__ pos4, double cx,
                                     double cy, double cz, float4* __restrict__ pf) {
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -927,6 +1038,7 @@ constexpr int kStagedBatch = LMD_STAGED_BATCH;        // chunks evaluated togeth
 template <bool EV, int N3, int ROWS, bool STAGED, bool I16>
 __device__ __forceinline__ void vl_staged_tile(int t, int lane, int n_owned, int hb,
                                                unsigned dummy, unsigned long long* bar,
+                                               const int32_t* __restrict__ slot_particle,
                                                const int32_t* __restrict__ out_perm,
                                                const double* __restrict__ pos4,
                                                const double* __restrict__ xs,
@@ -937,8 +1049,9 @@ __device__ __forceinline__ void vl_staged_tile(int t, int lane, int n_owned, int
                                                const int32_t* __restrict__ nbr, const LJK& k,
                                                Acc& a, double* __restrict__ fx,
                                                double* __restrict__ fy, double* __restrict__ fz) {
-  const int i = t * 32 + lane;
-  const bool iact = i < n_owned;
+  // the particle this lane holds (re-dealt lists: slot_particle)
+  const int i = slot_particle ? slot_particle[t * 32 + lane] : t * 32 + lane;
+  const bool iact = i >= 0 && i < n_owned;
   // I16: 16-bit local rows, 8 steps per 128-bit chunk (else 32-bit, 4 steps)
   constexpr int CH = I16 ? 8 : 4;
   const int4* chunks =
@@ -1035,7 +1148,8 @@ __global__ void __launch_bounds__(32 * W, 16 / W)
     vl_staged_kernel(int n_owned, int ntiles, int sentinel, const int32_t* __restrict__ out_perm,
                      const double* __restrict__ pos4, SoA q, const int32_t* __restrict__ groups,
                      const long long* __restrict__ toff, const int32_t* __restrict__ kmax,
-                     const int32_t* __restrict__ nbr, LJK k, double* __restrict__ fx,
+                     const int32_t* __restrict__ nbr, const int32_t* __restrict__ slot_particle,
+                     LJK k, double* __restrict__ fx,
                      double* __restrict__ fy, double* __restrict__ fz, double* __restrict__ ev,
                      lmd_stats* __restrict__ stats, int dbg) {
   constexpr int ROWS = StageRows<W>::value;
@@ -1080,11 +1194,12 @@ __global__ void __launch_bounds__(32 * W, 16 / W)
   Acc a = {0.0, 0.0, 0.0, 0.0, 0.0, 0, 0, 0};
   if (glob)
     vl_staged_tile<EV, N3, ROWS, false, I16>(t, lane, n_owned, hb, (unsigned)sentinel, nullptr,
+                                             slot_particle,
                                         out_perm, pos4,
                                         q.x, q.y, q.z, toff, kmax, nbr, k, a, fx, fy, fz);
   else
     vl_staged_tile<EV, N3, ROWS, true, I16>(t, lane, n_owned, hb, (unsigned)(ROWS - 1),
-                                       (dbg & 2) ? nullptr : &bar, out_perm,
+                                       (dbg & 2) ? nullptr : &bar, slot_particle, out_perm,
                                        pos4, xs, xs, xs, toff, kmax, nbr, k, a, fx, fy, fz);
   a.overlap |= a.hi_min == 0u;
   flush_acc(a, lane, true, EV, t, ev, stats);
@@ -1342,6 +1457,34 @@ int lmd_vl_bank_schedule(int pattern, int64_t n_units, int32_t sentinel, int rou
   return LMD_OK;
 }
 
+int lmd_vl_reorder(int64_t n_owned, int32_t group_size, int32_t index_bits, int32_t cap_steps,
+                   int32_t max_steps, int bank, int32_t sentinel, const int32_t* count,
+                   const int64_t* tile_off, const int32_t* kmax, const int32_t* nbr,
+                   int32_t* slot_particle, int64_t* tile_off_out, int32_t* kmax_out,
+                   int32_t* nbr_out, void* stream) {
+  if (n_owned <= 0) return LMD_OK;
+  if (group_size % 32 || group_size < 32 || group_size > 256) return LMD_ERR_CONFIG;
+  if (index_bits != 16 && index_bits != 32) return LMD_ERR_CONFIG;
+  const int CH = index_bits == 16 ? 8 : 4;
+  if (cap_steps <= 0 || cap_steps % CH) return LMD_ERR_CONFIG;
+  const int tcap = max_steps < 255 ? max_steps : 255;
+  const int nw = group_size / 32;
+  const size_t smem = bank ? (size_t)nw * (48 * 32 + (size_t)tcap * 32) * sizeof(uint16_t) : 0;
+  const int64_t ngroups = cdiv(n_owned, group_size);
+  const int64_t ntiles = cdiv(n_owned, 32);
+  auto kern = index_bits == 16 ? vl_reorder_kernel<true> : vl_reorder_kernel<false>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return set_cuda_error(e);
+  }
+  kern<<<(unsigned)ngroups, group_size, smem, (cudaStream_t)stream>>>(
+      (int)n_owned, (int)ntiles, tcap, cap_steps, bank, sentinel, count,
+      (const long long*)tile_off, kmax, nbr, slot_particle, (long long*)tile_off_out, kmax_out,
+      nbr_out);
+  LMD_CHECK_LAUNCH();
+  return LMD_OK;
+}
+
 int64_t lmd_vl_ev_slots(int64_t n_owned, int pattern) {
   return cdiv(lmd_vl_num_tiles(n_owned, pattern), kVLWarps) * kVLWarps;
 }
@@ -1451,6 +1594,7 @@ int32_t lmd_vl_staged_capacity(int32_t group_size) {
 int lmd_force_vl_staged(int newton3, int flags, const lmd_lj* lj, int64_t n_owned,
                         const double* pos4, const double* soa, int64_t stride, int32_t sentinel,
                         int32_t group_size, const int32_t* groups, int32_t index_bits,
+                        const int32_t* slot_particle,
                         const int64_t* tile_off, const int32_t* kmax, const int32_t* nbr,
                         const int32_t* out_perm, double* fx, double* fy, double* fz,
                         double* ev_scratch, lmd_stats* stats, void* stream) {
@@ -1475,7 +1619,8 @@ int lmd_force_vl_staged(int newton3, int flags, const lmd_lj* lj, int64_t n_owne
     if (e != cudaSuccess) return set_cuda_error(e);                                            \
     kern<<<(unsigned)ngroups, 32 * W, smem, s>>>((int)n_owned, (int)ntiles, (int)sentinel,     \
                                                  out_perm, pos4, q, groups,                    \
-                                                 (const long long*)tile_off, kmax, nbr, k, fx, \
+                                                 (const long long*)tile_off, kmax, nbr,        \
+                                                 slot_particle, k, fx,                         \
                                                  fy, fz, ev_scratch, stats, (flags >> 8) & 3); \
   } while (0)
 #define LMD_VLS_W(EVB, N3B)                                 \

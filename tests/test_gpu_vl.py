@@ -221,11 +221,12 @@ def test_fused_collect_matches_scatter(rng, n3):
     assert np.array_equal(res[0][0], res[1][0]) and res[0][1] == res[1][1]
 
 
-@pytest.mark.parametrize("staged,bank,index16", [(0, -1, True), (128, -1, True), (128, 0, True),
-                                                 (128, 0, False), (128, 2, False), (256, 0, True),
-                                                 (512, 0, True), (0, 2, True)])
+@pytest.mark.parametrize("staged,bank,index16,redeal", [
+    (0, -1, True, False), (128, -1, True, False), (128, 0, True, False), (128, 0, False, False),
+    (128, 2, False, False), (256, 0, True, False), (512, 0, True, False), (0, 2, True, False),
+    (128, 0, True, True), (128, -1, True, True), (256, 0, False, True)])
 @pytest.mark.parametrize("n3", [False, True])
-def test_staged_and_bank_ordered_lists_match_oracle(rng, staged, bank, index16, n3):
+def test_staged_and_bank_ordered_lists_match_oracle(rng, staged, bank, index16, redeal, n3):
     """Staged lists (TMA copies of each group's candidate runs into shared
     memory, local rows) and the bank-pair-aware entry orders: pair counts,
     statistics and energy exact / 1e-12 vs the oracle, forces within
@@ -244,6 +245,7 @@ def test_staged_and_bank_ordered_lists_match_oracle(rng, staged, bank, index16, 
             cont.staged_group = staged
             cont.bank_rounds = bank
             cont.index16 = index16
+            cont.redeal = redeal
             buf = ParticleBuffer.from_positions(pos, device="cuda")
             cont.rebuild(buf)
             cont.refresh(buf)
@@ -258,6 +260,6 @@ def test_staged_and_bank_ordered_lists_match_oracle(rng, staged, bank, index16, 
                 assert np.array_equal(prev, f)
             prev = f
         if staged:
-            groups, rows, g, over, bits = next(iter(cont._staging.values()))
+            groups, rows, g, over, bits, slots = next(iter(cont._staging.values()))
             assert rows >= 16 and g == staged
             assert bits == (16 if (over == 0 and index16) else 32)
