@@ -370,7 +370,8 @@ class VerletListContainer:
                   N.ptr(self._h_start), N.ptr(self._h_count))
         sentinel = self.n_owned + self.n_halo
         if staged and n:
-            pf, rl2f_lo, rl2f_hi = self._prefilter_rows()
+            pf, rl2f_lo, rl2f_hi = (self._prefilter_rows() if self.build_fp32
+                                    else (None, 0.0, 0.0))
             ngroups = (n + staged - 1) // staged
             groups = torch.empty(ngroups * 128, dtype=torch.int32, device=dev)
             smax = torch.zeros(2, dtype=torch.int32, device=dev)
@@ -391,7 +392,7 @@ class VerletListContainer:
             nbr = torch.empty(max(words, 1), dtype=torch.int32, device=dev)
             if staged and n:
                 N.call("lmd_vl_build_staged", self.grid, float(rl2), int(newton3), n, *tables,
-                       staged, N.ptr(groups), bits, N.ptr(pf) if self.build_fp32 else None,
+                       staged, N.ptr(groups), bits, N.ptr(pf) if pf is not None else None,
                        rl2f_lo, rl2f_hi, cap_steps,
                        N.ptr(count),
                        N.ptr(half) if half is not None else None, N.ptr(tile_off),
