@@ -95,22 +95,68 @@ def _launch(cont, cfg: Configuration, V: int, energy: bool, owned=None):
     return cont.launch_force(energy)
 
 
-def _finish(cont, cfg: Configuration, V: int, stats_t) -> KernelStats:
-    st = N.read_stats(stats_t)
+def _geometry(cont, cfg: Configuration, V: int):
+    """The geometric statistics of the structure the force phase ran on
+    (cached per rebuild; read before the structure can change)."""
     kind = cfg.container
     if kind is ContainerKind.LINKED_CELLS:
         code = traversal_code(cfg.traversal)
-        geo = cont._lc_stats(code, cfg.newton3, cfg.pattern, V)
-        once = cont.uses_colored_n3(code, cfg.newton3)
+        return cont._lc_stats(code, cfg.newton3, cfg.pattern, V)
+    if kind is ContainerKind.VERLET_LISTS:
+        return cont.vl_stats(cfg.newton3, cfg.pattern, V)
+    return cont.vcl_stats(cfg.newton3, cfg.pattern, V)
+
+
+def _stats_from(st, cont, cfg: Configuration, geo) -> KernelStats:
+    kind = cfg.container
+    if kind is ContainerKind.LINKED_CELLS:
+        once = cont.uses_colored_n3(traversal_code(cfg.traversal), cfg.newton3)
         return LinkedCellsContainer.finish_stats(st, cfg.newton3 and not once, *geo)
     if kind is ContainerKind.VERLET_LISTS:
-        geo = cont.vl_stats(cfg.newton3, cfg.pattern, V)
         if st.overlap:
             raise ParticleOverlapError("zero distance between interacting particles")
         return KernelStats(geo[0], geo[1], geo[2], cont.pair_count(st, cfg.newton3), st.epot,
                            st.virial)
-    geo = cont.vcl_stats(cfg.newton3, cfg.pattern, V)
     return LinkedCellsContainer.finish_stats(st, cfg.newton3, *geo)
+
+
+def _finish(cont, cfg: Configuration, V: int, stats_t) -> KernelStats:
+    return _stats_from(N.read_stats(stats_t), cont, cfg, _geometry(cont, cfg, V))
+
+
+class _DeferredStats:
+    """Force-phase statistics read one step late: the device record is copied
+    to pinned memory right after the launch and parsed at the next step's
+    host synchronisation (the rebuild decision), so a step needs one host
+    read instead of two.  An overlap (ParticleOverlapError) is then raised at
+    the start of the following step, before its force phase."""
+
+    def __init__(self):
+        import torch
+        self.buf = [torch.empty(N.STATS_BYTES, dtype=torch.uint8).pin_memory()
+                    for _ in range(2)]
+        self.pending = None
+        self.k = 0
+
+    def push(self, stats_t, cont, cfg, geo, record):
+        import torch
+        b = self.buf[self.k % 2]
+        self.k += 1
+        b.copy_(stats_t.view(torch.uint8), non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self.pending = (ev, b, cont, cfg, geo, record)
+
+    def resolve(self):
+        if self.pending is None:
+            return
+        ev, b, cont, cfg, geo, record = self.pending
+        self.pending = None
+        ev.synchronize()
+        st = N.Stats.from_buffer_copy(b.numpy().tobytes())
+        stats = _stats_from(st, cont, cfg, geo)
+        if record is not None:
+            record.pair_interactions = stats.pair_interactions
 
 
 def run_md(owned, box, params, iterations: int, vector_width: int = 8, *,
@@ -156,6 +202,7 @@ def run_md(owned, box, params, iterations: int, vector_width: int = 8, *,
     else:
         provider = make_metric_provider(metric, lambda: lane_total[0])
     containers: dict = {}
+    late = _DeferredStats()
     records: list = []
     per_config: dict = {}
     margin = params.interaction_length
@@ -190,12 +237,14 @@ def run_md(owned, box, params, iterations: int, vector_width: int = 8, *,
             rebuilt = False
             fresh = cont.reference_positions is None
             if fresh or cont.needs_rebuild(owned):
+                late.resolve()   # (the decision above synchronised)
                 if wrap == "at_rebuild":
                     apply_boundaries(owned, box)
                 cont.rebuild(owned)
                 cont.refresh(owned)
                 rebuilt = not fresh
             else:
+                late.resolve()
                 cont.refresh(owned)
             cont.steps_since_rebuild += 1
             # lazily built structures (Verlet lists per interaction order) are
@@ -211,7 +260,11 @@ def run_md(owned, box, params, iterations: int, vector_width: int = 8, *,
             t0 = time.perf_counter()
             stats_t = _launch(cont, cfg, vector_width, energy, owned)
             sample = provider.end_region() if metric not in ("laneops", "iteration") else None
-            stats = _finish(cont, cfg, vector_width, stats_t)
+            if deferred and not energy:
+                geo = _geometry(cont, cfg, vector_width)
+                stats = KernelStats(geo[0], geo[1], geo[2], -1)   # pairs filled in late
+            else:
+                stats = _finish(cont, cfg, vector_width, stats_t)
             force_time += time.perf_counter() - t0
             lane_total[0] += stats.lane_slots
             if sample is None and not whole:
@@ -224,12 +277,17 @@ def run_md(owned, box, params, iterations: int, vector_width: int = 8, *,
                 sample = provider.end_region()
             if tuner is not None:
                 tuner.record_sample(sample, displaced=rebuilt)
+            rec = None
             if record:
-                records.append(IterationRecord(it, phase, cfg, sample, stats.lane_slots,
-                                               stats.useful_interactions, stats.blank_lanes,
-                                               stats.pair_interactions, len(owned)))
+                rec = IterationRecord(it, phase, cfg, sample, stats.lane_slots,
+                                      stats.useful_interactions, stats.blank_lanes,
+                                      stats.pair_interactions, len(owned))
+                records.append(rec)
+            if deferred and not energy:
+                late.push(stats_t, cont, cfg, geo, rec)
             if not deferred:
                 per_config[cfg.label] = per_config.get(cfg.label, 0.0) + sample
+        late.resolve()
         if deferred:
             values = provider.resolve()
             for rec in records:
