@@ -246,30 +246,6 @@ __global__ void vl_build_kernel(GridK g, int n, int ntiles, int newton3,
   if ((threadIdx.x & 31) == 0 && w > 0) atomicMax(max_count, w);
 }
 
-// Per tile: step count = the longest list (4-step chunks, capped), idle
-// slots up to it = -1, tile offsets; the longest list overall -> max_count.
-__global__ void vl_pad_kernel(int n, int ntiles, int cap_steps, const int32_t* __restrict__ count,
-                              long long* __restrict__ toff, int32_t* __restrict__ kmax,
-                              int32_t* __restrict__ max_count, int32_t* __restrict__ nbr) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const int t = i >> 5, il = i & 31;
-  const int k = i < n ? count[i] : 0;
-  int m = k;
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, off));
-  if (t >= ntiles) return;
-  int steps = (m + kChunk - 1) / kChunk * kChunk;
-  if (steps > cap_steps) steps = cap_steps;
-  const long long stride = (long long)cap_steps * 32;
-  int32_t* out = nbr + (long long)t * stride;
-  for (int q = min(k, cap_steps); q < steps; ++q) out[(long long)(q >> 2) * 128 + il * 4 + (q & 3)] = -1;
-  if (il == 0) {
-    kmax[t] = steps;
-    toff[t] = (long long)t * stride;
-    if (m > 0) atomicMax(max_count, m);
-  }
-}
-
 // Group run table for the staged lists (one warp per group; lane l scans
 // runs l and l + 32 for their first and last particle).
 __global__ void vl_group_kernel(GridK g, int n, int G, int scap, const double* __restrict__ pos4,
