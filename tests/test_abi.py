@@ -111,3 +111,17 @@ def test_missing_library_is_an_error(monkeypatch, tmp_path):
     monkeypatch.setattr(N, "lib_path", lambda: str(tmp_path / "absent.so"))
     with pytest.raises(NativeLibraryError):
         N.load()
+
+
+def test_staged_list_host_entry_points():
+    """Host-side sizing entry points of the staged Verlet lists (no GPU):
+    the staged-row capacity per group size (the dummy row and a 16-row
+    margin below the shared-memory rows), invalid sizes rejected, and the
+    bank-order workspace per warp."""
+    lib = N.load()
+    assert lib.lmd_vl_staged_capacity(128) == 2304 - 16
+    assert lib.lmd_vl_staged_capacity(256) == 4096 - 16
+    assert lib.lmd_vl_staged_capacity(512) == 7168 - 16
+    for bad in (0, 64, 100, 1024):
+        assert lib.lmd_vl_staged_capacity(bad) == 0
+    assert lib.lmd_vl_bank_smem_per_warp(100) == (64 * 16 + 100 * 32) * 4
