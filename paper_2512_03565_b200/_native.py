@@ -251,18 +251,34 @@ def stream() -> int:
     return torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice())
 
 
+# per-object caches of the ctypes structs (boxes and LJ parameters are frozen
+# dataclasses; the cache holds the object, so its id is not reused)
+_STRUCT_CACHE: dict = {}
+
+
 def make_box(box) -> Box:
+    hit = _STRUCT_CACHE.get(("box", id(box)))
+    if hit is not None and hit[0] is box:
+        return hit[1]
     b = Box()
     for ax in range(3):
         b.lo[ax] = float(box.min[ax])
         b.hi[ax] = float(box.max[ax])
         b.periodic[ax] = 1 if ax in box.periodic_axes else 0
+    if len(_STRUCT_CACHE) < 4096:
+        _STRUCT_CACHE[("box", id(box))] = (box, b)
     return b
 
 
 def make_lj(params) -> LJ:
-    return LJ(float(params.epsilon), float(params.sigma), float(params.cutoff),
-              float(params.skin))
+    hit = _STRUCT_CACHE.get(("lj", id(params)))
+    if hit is not None and hit[0] is params:
+        return hit[1]
+    lj = LJ(float(params.epsilon), float(params.sigma), float(params.cutoff),
+            float(params.skin))
+    if len(_STRUCT_CACHE) < 4096:
+        _STRUCT_CACHE[("lj", id(params))] = (params, lj)
+    return lj
 
 
 def new_stats(device) -> torch.Tensor:
