@@ -137,6 +137,7 @@ class _DeferredStats:
                     for _ in range(2)]
         self.pending = None
         self.k = 0
+        self.stream = torch.cuda.current_stream()   # fixed for the run
 
     def push(self, stats_t, cont, cfg, geo, record):
         import torch
@@ -144,7 +145,7 @@ class _DeferredStats:
         self.k += 1
         b.copy_(stats_t.view(torch.uint8), non_blocking=True)
         ev = torch.cuda.Event()
-        ev.record()
+        ev.record(self.stream)
         self.pending = (ev, b, cont, cfg, geo, record)
 
     def resolve(self):
