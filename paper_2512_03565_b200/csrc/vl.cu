@@ -117,8 +117,11 @@ __global__ void vl_fill_kernel(GridK g, int n, int A, int B, int pattern, int ne
 // through *max_count (the caller rebuilds with a larger capacity).
 // IDX = uint16_t: staged lists with every group staged (local rows < 2^16),
 // 8 steps per 128-bit chunk; idle slots 0xffff.
+#ifndef LMD_BUILD_MIN_BLOCKS
+#define LMD_BUILD_MIN_BLOCKS 12
+#endif
 template <int P, bool PF, typename IDX = int32_t>
-__global__ void vl_build_kernel(GridK g, int n, int ntiles, int newton3,
+__global__ void __launch_bounds__(128, LMD_BUILD_MIN_BLOCKS) vl_build_kernel(GridK g, int n, int ntiles, int newton3,
                                 double rl2, int32_t sentinel, const double* __restrict__ pos4,
                                 const int32_t* __restrict__ os, const int32_t* __restrict__ oc,
                                 const int32_t* __restrict__ hs, const int32_t* __restrict__ hc,
