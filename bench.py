@@ -249,13 +249,18 @@ def committed_traffic(label):
 
 
 def algorithmic_bytes(cfg, cont, stats, n):
-    """Bytes one force launch must move: positions (32 B pos4 per particle and
-    image), forces (24 B per owned particle) and, for Verlet lists, 4 B per
-    list entry (useful interactions)."""
+    """Bytes one force launch must move: positions (x, y, z: 24 B per particle
+    and image; 32 B pos4 records where the kernel gathers those), forces
+    (24 B per owned particle) and, for Verlet lists, one index per list entry
+    (useful interactions) at the width the kernel reads (2 B for the staged
+    16-bit lists, else 4 B)."""
     images = getattr(cont, "n_halo", 0) or 0
-    b = 32 * (n + images) + 24 * n
+    staged = getattr(cont, "_staging", None)
+    stg = next(iter(staged.values())) if staged else None
+    pos_b = 24 if (stg is not None or getattr(cont, "use_soa", False)) else 32
+    b = pos_b * (n + images) + 24 * n
     if cfg.container.value == "vl":
-        b += 4 * stats.useful_interactions
+        b += (stg[4] // 8 if stg is not None else 4) * stats.useful_interactions
     return int(b)
 
 
