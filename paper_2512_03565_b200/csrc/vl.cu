@@ -153,76 +153,84 @@ __global__ void __launch_bounds__(128, LMD_BUILD_MIN_BLOCKS) vl_build_kernel(Gri
         const int32_t* vs = view ? hs : os;
         const int32_t* vc = view ? hc : oc;
         for (int dz = -1; dz <= 1; ++dz)
-          for (int dy = -1; dy <= 1; ++dy)
-            for (int dx = -1; dx <= 1; ++dx) {
-              const long long nl = lin + dx + g.t0 * (dy + g.t1 * dz);
-              const int c = vc[nl];
-              if (c == 0) continue;
-              int j = vs[nl];
-              const int e = j + c;
-              // staged lists: index into the group's shared-memory copy of
-              // this (view, dy, dz) run (vl_group_kernel); 0 for global
-              const int roff =
-                  grec ? __ldg(grec + kGrpOff + view * 18 + grow * 9 + (dz + 1) * 3 + (dy + 1))
-                       : 0;
-              if (!view && newton3) j = max(j, i + 1);
-              // hits of up to 32 consecutive candidates are collected as a
-              // bit mask and emitted afterwards in ascending order, so the
-              // (warp-divergent) emit path runs once per hit, not once per
-              // candidate that some lane of the warp accepted
-              // branch-free candidate loop: the backing holds no DUMMY
-              // records (owned checked at rebuild, images / ghosts tagged
-              // HALO, the sentinel is in no cell) and the self pair is
-              // cleared from the mask afterwards
-              for (int j0 = j; j0 < e; j0 += 32) {
-                const int cnt = min(e - j0, 32);
-                unsigned mask = 0u;
-                if (PF) {
-                  // FP32 decision with an exact fallback: r2f < rl2f_lo is
-                  // inside and r2f >= rl2f_hi outside for the reference's
-                  // exact r2 too (the margin bounds the FP32 error for this
-                  // coordinate range); only candidates in between -- a band
-                  // of ~1e-4 relative width -- are re-tested in FP64
-                  unsigned band = 0u;
-#pragma unroll 4
-                  for (int q = 0; q < cnt; ++q) {
-                    const float4 f = __ldg(pf + j0 + q);
-                    const float fx = pif.x - f.x, fy = pif.y - f.y, fz = pif.z - f.z;
-                    const float r2f = fmaf(fz, fz, fmaf(fy, fy, fx * fx));
-                    mask |= (r2f < rl2f_lo ? 1u : 0u) << q;
-                    band |= (r2f >= rl2f_lo && r2f < rl2f ? 1u : 0u) << q;
-                  }
-                  while (band) {
-                    const int q = __ffs(band) - 1;
-                    band &= band - 1u;
-                    const double4 pj = ld_pos4(pos4, j0 + q);
-                    const double r2 = r2_exact(pi.x - pj.x, pi.y - pj.y, pi.z - pj.z);
-                    mask |= (r2 < rl2 ? 1u : 0u) << q;
-                  }
-                } else {
-#pragma unroll 2
-                  for (int q = 0; q < cnt; ++q) {
-                    const double4 pj = ld_pos4(pos4, j0 + q);
-                    const double r2 = r2_exact(pi.x - pj.x, pi.y - pj.y, pi.z - pj.z);
-                    mask |= (r2 < rl2 ? 1u : 0u) << q;
-                  }
-                }
-                if (!view) {
-                  const unsigned self = (unsigned)(i - j0);
-                  if (self < 32u) mask &= ~(1u << self);
-                }
-                while (mask) {
-                  const int jj = j0 + __ffs(mask) - 1;
-                  mask &= mask - 1u;
-                  kh += view || jj > i;
-                  if (k < cap) {
-                    const int st = k / B, l = lane_of(pattern, il, k % B);
-                    out[(long long)(st / CH) * (32 * CH) + l * CH + st % CH] = (IDX)(jj + roff);
-                  }
-                  ++k;
-                }
+          for (int dy = -1; dy <= 1; ++dy) {
+            // the 3 cells dx = -1..1 of this row are consecutive linear
+            // cells: their particles form one contiguous index range
+            const long long nl0 = lin - 1 + g.t0 * (dy + g.t1 * dz);
+            int j = 0x7fffffff, e = -1;
+#pragma unroll
+            for (int dx = 0; dx < 3; ++dx) {
+              const int c = vc[nl0 + dx];
+              if (c) {
+                const int s0 = vs[nl0 + dx];
+                j = min(j, s0);
+                e = max(e, s0 + c);
               }
             }
+            if (e < 0) continue;
+            // staged lists: index into the group's shared-memory copy of
+            // this (view, dy, dz) run (vl_group_kernel); 0 for global
+            const int roff =
+                grec ? __ldg(grec + kGrpOff + view * 18 + grow * 9 + (dz + 1) * 3 + (dy + 1))
+                     : 0;
+            if (!view && newton3) j = max(j, i + 1);
+            // hits of up to 64 consecutive candidates are collected as a
+            // bit mask and emitted afterwards in ascending order, so the
+            // (warp-divergent) emit path runs once per hit, not once per
+            // candidate that some lane of the warp accepted; one range per
+            // row (not per cell) keeps the lanes' emission loops balanced.
+            // Branch-free candidate loop: the backing holds no DUMMY records
+            // (owned checked at rebuild, images / ghosts tagged HALO, the
+            // sentinel is in no cell) and the self pair is cleared afterwards
+            for (int j0 = j; j0 < e; j0 += 64) {
+              const int cnt = min(e - j0, 64);
+              unsigned long long mask = 0ull;
+              if (PF) {
+                // FP32 decision with an exact fallback: r2f < rl2f_lo is
+                // inside and r2f >= rl2f_hi outside for the reference's exact
+                // r2 too (the margin bounds the FP32 error for this
+                // coordinate range); only candidates in between -- a band of
+                // ~1e-4 relative width -- are re-tested in FP64
+                unsigned long long band = 0ull;
+#pragma unroll 4
+                for (int q = 0; q < cnt; ++q) {
+                  const float4 f = __ldg(pf + j0 + q);
+                  const float fx = pif.x - f.x, fy = pif.y - f.y, fz = pif.z - f.z;
+                  const float r2f = fmaf(fz, fz, fmaf(fy, fy, fx * fx));
+                  mask |= (unsigned long long)(r2f < rl2f_lo ? 1u : 0u) << q;
+                  band |= (unsigned long long)(r2f >= rl2f_lo && r2f < rl2f ? 1u : 0u) << q;
+                }
+                while (band) {
+                  const int q = __ffsll((long long)band) - 1;
+                  band &= band - 1ull;
+                  const double4 pj = ld_pos4(pos4, j0 + q);
+                  const double r2 = r2_exact(pi.x - pj.x, pi.y - pj.y, pi.z - pj.z);
+                  mask |= (unsigned long long)(r2 < rl2 ? 1u : 0u) << q;
+                }
+              } else {
+#pragma unroll 2
+                for (int q = 0; q < cnt; ++q) {
+                  const double4 pj = ld_pos4(pos4, j0 + q);
+                  const double r2 = r2_exact(pi.x - pj.x, pi.y - pj.y, pi.z - pj.z);
+                  mask |= (unsigned long long)(r2 < rl2 ? 1u : 0u) << q;
+                }
+              }
+              if (!view) {
+                const unsigned self = (unsigned)(i - j0);
+                if (self < 64u) mask &= ~(1ull << self);
+              }
+              while (mask) {
+                const int jj = j0 + __ffsll((long long)mask) - 1;
+                mask &= mask - 1ull;
+                kh += view || jj > i;
+                if (k < cap) {
+                  const int st = k / B, l = lane_of(pattern, il, k % B);
+                  out[(long long)(st / CH) * (32 * CH) + l * CH + st % CH] = (IDX)(jj + roff);
+                }
+                ++k;
+              }
+            }
+          }
       }
     }
     count[i] = k;
