@@ -219,10 +219,14 @@ __global__ void __launch_bounds__(128, LMD_BUILD_MIN_BLOCKS) vl_build_kernel(Gri
                 const unsigned self = (unsigned)(i - j0);
                 if (self < 64u) mask &= ~(1ull << self);
               }
+              // half-list length: every image hit, owned hits with j > i
+              {
+                const int d = i + 1 - j0;
+                kh += __popcll(view || d <= 0 ? mask : (d >= 64 ? 0ull : mask & (~0ull << d)));
+              }
               while (mask) {
                 const int jj = j0 + __ffsll((long long)mask) - 1;
                 mask &= mask - 1ull;
-                kh += view || jj > i;
                 if (k < cap) {
                   const int st = k / B, l = lane_of(pattern, il, k % B);
                   out[(long long)(st / CH) * (32 * CH) + l * CH + st % CH] = (IDX)(jj + roff);
