@@ -208,12 +208,16 @@ __global__ void __launch_bounds__(128, LMD_BUILD_MIN_BLOCKS) vl_build_kernel(Gri
                   mask |= (unsigned long long)(r2 < rl2 ? 1u : 0u) << q;
                 }
               } else {
+                // shift-and-add accumulation (2 integer instructions per
+                // candidate); bit-reversed below to candidate order
+                unsigned long long racc = 0ull;
 #pragma unroll 2
                 for (int q = 0; q < cnt; ++q) {
                   const double4 pj = ld_pos4(pos4, j0 + q);
                   const double r2 = r2_exact(pi.x - pj.x, pi.y - pj.y, pi.z - pj.z);
-                  mask |= (unsigned long long)(r2 < rl2 ? 1u : 0u) << q;
+                  racc = racc + racc + (r2 < rl2 ? 1ull : 0ull);
                 }
+                mask = __brevll(racc << (64 - cnt));
               }
               if (!view) {
                 const unsigned self = (unsigned)(i - j0);
