@@ -1,17 +1,25 @@
 #!/usr/bin/env python
 """Benchmark: LJ FP64 pair-interactions/s on B200 (BASELINE.json metric).
 
-Workload (N=1): BASELINE config 2 at rho = 0.8 -- 1,000,000 particles,
-uniform random (RSA, min distance 0.9, seed 42) in a periodic cube, LJ
-cutoff 2.5, FP64.  A step is one force phase over the resident particles
-(the reference's metric region, driver.py:203-207: traversal + kernel);
-the neighbor structure is built before the timed region.  The L2 is
-flushed (256 MiB write) before every timed step; only the force phase is
-inside the CUDA-event bracket.  With --gpus N > 1 the periodic box is N bricks
-(2x1x1, 2x2x1, 2x2x2) of the N=1 box (weak scaling); every step includes the
-NCCL point-to-point ghost exchange.
+Workload (N=1, the default ``--workload c4``): BASELINE config 4 --
+16,777,216 particles on a 256^3 simple-cubic lattice at rho = 0.8 perturbed by
+N(0, 0.05^2) per component (seed 42), periodic cube L = 275.77, LJ cutoff
+2.5, FP64, Verlet lists with skin 0.3.  This is the configuration the
+metric's 1/2/4/8-GPU series is quoted on and the largest BASELINE config
+that fits one GPU.  A step is one force phase over the resident particles
+(the reference's metric region, driver.py:203-207: refresh + kernel); the
+neighbour structure is built before the timed region and its cost is
+reported separately (``list_maintenance``: measured rebuild + list build,
+amortised over the rebuild period).  The inputs (1.8 GB of particle state,
+≈ 3 GB of lists) are far larger than the 126 MB L2, and the L2 is also
+flushed (256 MiB write) before every timed step.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config LABEL]
+With --gpus N > 1: ``c4`` is strong scaling (the 16.8M-particle box split
+into 2x1x1 / 2x2x1 / 2x2x2 bricks), ``c5`` weak scaling (8,388,608 particles
+per GPU at rho 0.3, one brick per GPU), ``c2`` weak scaling (1M per GPU);
+every step includes the NCCL point-to-point ghost exchange.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c4|c5|c2]
     python bench.py --impl reference ...   # the reference algorithm on host cores
 """
 
@@ -44,9 +52,12 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default=DEFAULT_CONFIG)
-    ap.add_argument("--rho", type=float, default=0.8)
-    ap.add_argument("--n", "--particles", dest="n", type=int, default=1_000_000,
-                    help="particles per GPU (--particles under torchrun: --n is ambiguous there)")
+    ap.add_argument("--workload", default="c4", choices=["c4", "c5", "c2"],
+                    help="BASELINE config: c4 (16.8M lattice, strong scaling; default), "
+                         "c5 (8.4M gas per GPU, weak), c2 (1M gas per GPU, weak)")
+    ap.add_argument("--rho", type=float, default=0.8, help="c2 density")
+    ap.add_argument("--n", "--particles", dest="n", type=int, default=None,
+                    help="c2/c5: particles per GPU; c4: lattice side^3 (default 256^3)")
     ap.add_argument("--vector-width", type=int, default=8)
     ap.add_argument("--energy", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -109,8 +120,18 @@ class ClockSampler:
 
 # --------------------------------------------------------------- workload
 def make_workload(args, device, seed):
+    """The per-GPU (c2, c5) or global (c4) workload, seeded."""
     from paper_2512_03565_b200 import workloads
-    return workloads.config2(args.rho, n=args.n, seed=seed, device=device)
+    if args.workload == "c4":
+        side = round(args.n ** (1.0 / 3.0)) if args.n else 256
+        return workloads.config4(side, seed=seed, device=device)
+    if args.workload == "c5":
+        return workloads.config5(n=args.n or 8_388_608, seed=seed, device=device)
+    return workloads.config2(args.rho, n=args.n or 1_000_000, seed=seed, device=device)
+
+
+def scaling_of(args) -> str:
+    return "strong" if args.workload == "c4" else "weak"
 
 
 def params_for(cfg, w):
@@ -295,6 +316,35 @@ def time_steps(phase, steps, flush, torch):
     return step, kern
 
 
+def time_rebuild(phase, torch, reps: int = 2):
+    """Neighbour-structure maintenance of a Verlet-list phase, measured: the
+    container rebuild (binning, images) + list build, wall clock between two
+    synchronisations (host work and reads included), best of ``reps``; and
+    the list build alone in CUDA events.  None for containers rebuilt inside
+    every step (LC re-bins its images in refresh)."""
+    if phase.kind != "vl":
+        return None
+    cont = phase.cont
+    wall, gpu = [], []
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        if phase.dec is None:
+            cont.rebuild(phase.buf)
+        else:
+            cont.rebuild(phase.buf, phase.ghosts)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        cont.ensure_lists(phase.cfg.pattern, phase.cfg.newton3)
+        e1.record()
+        torch.cuda.synchronize()
+        wall.append(time.perf_counter() - t0)
+        gpu.append(e0.elapsed_time(e1) * 1e-3)
+    phase.refresh()
+    return min(wall), min(gpu)
+
+
 def cpu_baseline_lc(w, cfg, params, threads):
     from oracle import oracle as O
     span = w.box_length
@@ -343,14 +393,27 @@ def run_b200(args):
         # global periodic box stacks the bricks; one NCCL ghost exchange per step
         from paper_2512_03565_b200.decomposition import BrickDecomposition, brick_grid
         grid = brick_grid(world)
-        w = make_workload(args, "cuda", 42 + rank)
-        Lb = w.box_length
-        c = (rank % grid[0], (rank // grid[0]) % grid[1], rank // (grid[0] * grid[1]))
-        w.positions = w.positions + torch.tensor([c[0] * Lb, c[1] * Lb, c[2] * Lb],
-                                                 dtype=torch.float64, device="cuda")
-        params0 = params_for(cfg, w)
-        dec = BrickDecomposition(np.zeros(3), np.array(grid, dtype=np.float64) * Lb,
-                                 params0.interaction_length, rank, world, grid=grid)
+        if scaling_of(args) == "strong":
+            # strong scaling: every rank generates the same global system
+            # (seeded) and keeps the particles of its brick
+            w = make_workload(args, "cuda", 42)
+            params0 = params_for(cfg, w)
+            dec = BrickDecomposition(np.zeros(3), np.full(3, w.box_length),
+                                     params0.interaction_length, rank, world, grid=grid)
+            pos = torch.as_tensor(w.positions).to("cuda", torch.float64)
+            w.positions = pos[dec.owner_of(pos) == rank].contiguous()
+        else:
+            # weak scaling: every rank's brick is the N=1 box (same density), the
+            # global periodic box stacks the bricks
+            w = make_workload(args, "cuda", 42 + rank)
+            Lb = w.box_length
+            c = (rank % grid[0], (rank // grid[0]) % grid[1], rank // (grid[0] * grid[1]))
+            w.positions = (torch.as_tensor(w.positions).to("cuda", torch.float64)
+                           + torch.tensor([c[0] * Lb, c[1] * Lb, c[2] * Lb],
+                                          dtype=torch.float64, device="cuda"))
+            params0 = params_for(cfg, w)
+            dec = BrickDecomposition(np.zeros(3), np.array(grid, dtype=np.float64) * Lb,
+                                     params0.interaction_length, rank, world, grid=grid)
     else:
         w = make_workload(args, "cuda", 42)
     dec_error = None
@@ -403,6 +466,19 @@ def run_b200(args):
 
     value = total_pairs * args.steps / t_max
     avg_launch = t_kern / args.steps
+    maint = None
+    rb = time_rebuild(phase, torch)
+    if rb is not None:
+        period = cont.rebuild_period
+        step_s = t_max / args.steps
+        maint = {"rebuild_and_lists_ms": rb[0] * 1e3, "list_build_gpu_ms": rb[1] * 1e3,
+                 "rebuild_period": period,
+                 "amortized_ms_per_step": (step_s + rb[0] / period) * 1e3,
+                 "amortized_pairs_per_s": total_pairs / (step_s + rb[0] / period),
+                 "note": "rank 0; outside the timed region: container rebuild (binning, "
+                         "images) + list build, wall clock between synchronisations, "
+                         "amortised over the rebuild period" +
+                         ("; ghost migration/planning not included" if dec else "")}
     flops = pairs * FLOPS_PER_PAIR[cfg.newton3]
     achieved = flops / avg_launch / 1e12
 
@@ -472,9 +548,9 @@ def run_b200(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": t_max / args.steps * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": scaling_of(args), "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": w.name, "particles_per_gpu": n_local, "rho": args.rho,
+            "config": {"workload": w.name, "particles_rank0": n_local,
                        "box_length_per_gpu": w.box_length, "cutoff": w.cutoff,
                        "skin": params.skin, "configuration": cfg.label,
                        "vector_width": args.vector_width,
@@ -484,7 +560,8 @@ def run_b200(args):
                        "step": "refresh (positions -> cell order, images/ghosts) + force "
                                "kernel" + (f" + {backend} ghost exchange" if world > 1 else ""),
                        "kernel_ms_rank0": avg_launch * 1e3,
-                       "l2": "flushed (256 MiB write) before every timed step",
+                       "l2": "inputs larger than L2 (1.8 GB state at c4) and L2 flushed "
+                             "(256 MiB write) before every timed step",
                        "parallelism": (f"bricks {dec.grid}, {backend} P2P ghost exchange"
                                        if dec else ("replicas (decomposition failed: "
                                                     f"{dec_error})" if dec_error
@@ -500,6 +577,7 @@ def run_b200(args):
                          "algorithmic_bytes": algorithmic_bytes(cfg, cont, stats, n_local),
                          "hbm_gbs_achieved": algorithmic_bytes(cfg, cont, stats, n_local)
                          / avg_launch / 1e9},
+            "list_maintenance": maint,
             "e2e": e2e,
             "cpu_baseline": cpu,
             "gpu_launches": args.steps * phase.launches_per_step,
@@ -567,7 +645,7 @@ def run_reference(args):
     params = params_for(cfg, w)
     threads = O.max_threads()
     h, prep, trav, n3 = cpu_baseline_lc(w, cfg, params, threads)
-    for _ in range(max(args.warmup, 1)):
+    for _ in range(min(max(args.warmup, 1), 2)):   # a CPU sweep needs no long warm-up
         h.execute(threads)
     times = []
     pairs = None
@@ -584,7 +662,8 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": sum(times) / args.steps * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": scaling_of(args), "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
             "config": {"workload": w.name, "configuration": cfg.label,
                        "executed": f"lc,{trav},{str(n3).lower()}", "pairs_per_step": pairs},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
