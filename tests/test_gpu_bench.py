@@ -25,7 +25,7 @@ KEYS = ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
 
 def _bench(cfg, extra=()):
     cmd = [sys.executable, "bench.py", "--config", cfg, "--steps", "3", "--warmup", "3",
-           "--particles", str(N), *extra]
+           "--workload", "c2", "--particles", str(N), *extra]
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stderr[-2000:]
     return json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
