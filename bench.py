@@ -273,9 +273,16 @@ def algorithmic_bytes(cfg, cont, stats, n):
     """Bytes one force launch must move: positions (x, y, z: 24 B per particle
     and image; 32 B pos4 records where the kernel gathers those), forces
     (24 B per owned particle) and, for Verlet lists, one index per list entry
-    (useful interactions) at the width the kernel reads (2 B for the staged
-    16-bit lists, else 4 B)."""
+    at the width the kernel reads (segmented lists: 2 B per slot of the
+    segments the launch runs; round-1 staged lists: 2 B per useful
+    interaction; else 4 B)."""
     images = getattr(cont, "n_halo", 0) or 0
+    vls = cont._vls_for(cfg.pattern, cfg.newton3) if hasattr(cont, "_vls_for") else None
+    if vls is not None:
+        ng = vls["plan"]["ngroups"]
+        segc = vls["segc"][: 8 * ng].view(-1, 2).long()
+        chunks = int(segc[:, 0].sum()) + (int(segc[:, 1].sum()) if cont._vls_outer() else 0)
+        return int(24 * (n + images) + 24 * n + 2 * chunks * 8 * 32)
     staged = getattr(cont, "_staging", None)
     stg = next(iter(staged.values())) if staged else None
     pos_b = 24 if (stg is not None or getattr(cont, "use_soa", False)) else 32

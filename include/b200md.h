@@ -173,6 +173,11 @@ int lmd_halo_refresh_pos4_soa(const lmd_box* box, int64_t nh, const int32_t* own
                               const int8_t* shift, const double* x, const double* y,
                               const double* z, double* pos4_halo, double* sx, double* sy,
                               double* sz, void* stream);
+/* The same image positions as (nh, 3) row-major rows (the segmented Verlet
+ * lists' staged layout). */
+int lmd_halo_refresh_rows(const lmd_box* box, int64_t nh, const int32_t* owner,
+                          const int8_t* shift, const double* x, const double* y, const double* z,
+                          double* rows, void* stream);
 int lmd_halo_refresh_soa(const lmd_box* box, int64_t nh, const int32_t* owner,
                          const int8_t* shift, const double* x, const double* y, const double* z,
                          double* ox, double* oy, double* oz, void* stream);
@@ -353,6 +358,67 @@ int lmd_force_vl_staged(int newton3, int flags, const lmd_lj* lj, int64_t n_owne
                         const int64_t* tile_off, const int32_t* kmax, const int32_t* nbr,
                         const int32_t* out_perm, double* fx, double* fy, double* fz,
                         double* ev_scratch, lmd_stats* stats, void* stream);
+/* Segmented staged Verlet lists (csrc/vls.cu) -- the default force path for
+ * V_BY_ONE full lists; replaces the reference's execute_packed sweep over
+ * the schedule's units (executor.py:72-171) for the Verlet-list container.
+ * Positions are (x, y, z) rows (24 B, 16-B aligned base) in rebuild order:
+ * owned cell-sorted, then images cell-sorted.  Groups: each interior cell
+ * line's owned particles cut into ceil(n_line / 128) balanced groups; a
+ * group stages its 18 candidate runs ((owned | image) x (dz, dy) neighbour
+ * lines, cells xa-1 .. xb+1) into shared memory with one TMA copy each.
+ * lmd_vls_plan writes the filled cell starts fs_own / fs_img (ncell each),
+ * per-line group counts / inclusive offsets (tdims[1] * tdims[2] each), the
+ * group records (64 int32 each, at most lmd_vls_max_groups) and info[8] =
+ * {largest staged rows, groups over capacity, number of groups, -, -}.
+ * lmd_vls_rows_for(info[0]) = the row capacity to pass as `rows` (0: too
+ * many rows for 16-bit byte offsets, use the other staged path).
+ * lmd_vls_build: lists with rl2 = (rc+skin)^2 from the build-time rows (the
+ * reference's exact r2), entries with r2 < rin2 in the inner segment, the
+ * rest in the outer; per tile t: seg_chunks[2t], [2t+1] = chunks of 8
+ * entries; list chunk c of lane l at int4 index (t * cap_chunks + c) * 32 +
+ * l (uint16 byte offsets 24 * local row, lane-local bank order);
+ * slotmap[g * 128 + lane slot] = the group-local particle the slot holds
+ * (0xff: none); count[i] / count_half[i] = full / half list lengths (sorted
+ * order); info[3] / info[4] = most chunks per tile / entries per lane seen
+ * (rebuild with larger caps when above cap_chunks / cap_entries <= 255).
+ * lmd_vls_force: one block per group (n_groups = info[2] of the plan);
+ * newton3 0 or 2 (as lmd_force_vl); the outer segment runs iff disp == NULL
+ * or *disp >= half_delta2 (bit patterns), i.e. once some particle moved at
+ * least delta / 2 since the build; ev_scratch holds
+ * 2 * lmd_vls_ev_slots(n_groups) doubles.  lmd_vls_refresh: rows[k] =
+ * (x, y, z)[perm[k]] (perm NULL: identity) and with disp != NULL the
+ * largest squared displacement from build_rows max-reduced into disp[slot]
+ * (disp[slot ^ 1] cleared).  lmd_vls_gather_rows: rows_out[k] =
+ * rows_in[perm[k]].  lmd_vls_rows_to_legacy: rows -> pos4 (OWNED below
+ * n_owned, HALO above) and SoA copies (either may be NULL). */
+int64_t lmd_vls_max_groups(const lmd_grid* g, int64_t n_owned);
+int32_t lmd_vls_rows_for(int32_t staged_rows);
+size_t lmd_vls_plan_temp_bytes(const lmd_grid* g);
+int lmd_vls_plan(const lmd_grid* g, int64_t n_owned, const int32_t* o_start,
+                 const int32_t* o_count, const int32_t* h_start, const int32_t* h_count,
+                 int32_t* fs_own, int32_t* fs_img, int32_t* row_groups, int32_t* row_gend,
+                 void* temp, size_t temp_bytes, int32_t* groups, int32_t* info, void* stream);
+size_t lmd_vls_build_smem(int32_t rows, int32_t cap_entries);
+int lmd_vls_build(const lmd_grid* g, double rin2, double rl2, int64_t n_owned, int32_t rows,
+                  const double* pos_rows, const int32_t* fs_own, const int32_t* o_count,
+                  const int32_t* fs_img, const int32_t* h_count, const int32_t* groups,
+                  int64_t max_groups, int32_t cap_chunks, int32_t cap_entries, void* nbr,
+                  int32_t* seg_chunks, uint8_t* slotmap, int32_t* count, int32_t* count_half,
+                  int32_t* info, void* stream);
+int64_t lmd_vls_ev_slots(int64_t max_groups);
+int lmd_vls_force(int newton3, int flags, const lmd_lj* lj, int64_t n_owned, int32_t rows,
+                  const double* pos_rows, const int32_t* groups, int64_t n_groups,
+                  const int32_t* info, const void* nbr, const int32_t* seg_chunks,
+                  const uint8_t* slotmap, int32_t cap_chunks, const uint64_t* disp,
+                  double half_delta2, const int32_t* out_perm, double* fx, double* fy,
+                  double* fz, double* ev_scratch, lmd_stats* stats, void* stream);
+int lmd_vls_refresh(int64_t n, const int32_t* perm, const double* x, const double* y,
+                    const double* z, double* rows, const double* build_rows, uint64_t* disp,
+                    int32_t slot, void* stream);
+int lmd_vls_gather_rows(int64_t n, const int32_t* perm, const double* rows_in, double* rows_out,
+                        void* stream);
+int lmd_vls_rows_to_legacy(int64_t n, int64_t n_owned, const double* rows, double* pos4,
+                           double* sx, double* sy, double* sz, void* stream);
 /* i-cluster lists (csrc/vl_ci.cu), full lists only: each cell's owned
  * particles are cut into clusters of up to ci (2 or 4) consecutive backing
  * slots, cluster c = [cl_first[c], cl_first[c] + cl_len[c]); its list is the

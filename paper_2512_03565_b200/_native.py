@@ -153,6 +153,7 @@ _sig("lmd_halo_refresh_pos4_soa", _INT, C.POINTER(Box), _I64, _VP, _VP, _VP, _VP
      _VP, _VP, _VP)
 _sig("lmd_halo_refresh_soa", _INT, C.POINTER(Box), _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP,
      _VP, _VP)
+_sig("lmd_halo_refresh_rows", _INT, C.POINTER(Box), _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP)
 _sig("lmd_gather_soa", _INT, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP)
 _sig("lmd_vl_count", _INT, C.POINTER(Grid), _D, _INT, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP)
 _sig("lmd_vl_num_tiles", _I64, _I64, _INT)
@@ -183,6 +184,19 @@ _sig("lmd_force_vl_staged", _INT, _INT, _INT, C.POINTER(LJ), _I64, _VP, _VP, _I6
 _sig("lmd_vl_reorder", _INT, _I64, _I32, _I32, _I32, _I32, _INT, _I32, _VP, _VP, _VP, _VP, _VP, _VP,
      _VP, _VP, _VP)
 _sig("lmd_vl_bank_schedule", _INT, _INT, _I64, _I32, _INT, _I32, _I32, _I32, _VP, _VP, _VP, _VP)
+_sig("lmd_vls_max_groups", _I64, C.POINTER(Grid), _I64)
+_sig("lmd_vls_rows_for", _I32, _I32)
+_sig("lmd_vls_plan_temp_bytes", _SZ, C.POINTER(Grid))
+_sig("lmd_vls_plan", _INT, C.POINTER(Grid), _I64, *([_VP] * 9), _SZ, _VP, _VP, _VP)
+_sig("lmd_vls_build_smem", _SZ, _I32, _I32)
+_sig("lmd_vls_build", _INT, C.POINTER(Grid), _D, _D, _I64, _I32, _VP, _VP, _VP, _VP, _VP, _VP,
+     _I64, _I32, _I32, _VP, _VP, _VP, _VP, _VP, _VP, _VP)
+_sig("lmd_vls_ev_slots", _I64, _I64)
+_sig("lmd_vls_force", _INT, _INT, _INT, C.POINTER(LJ), _I64, _I32, _VP, _VP, _I64, _VP, _VP, _VP,
+     _VP, _I32, _VP, _D, _VP, _VP, _VP, _VP, _VP, _VP, _VP)
+_sig("lmd_vls_refresh", _INT, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _I32, _VP)
+_sig("lmd_vls_gather_rows", _INT, _I64, _VP, _VP, _VP, _VP)
+_sig("lmd_vls_rows_to_legacy", _INT, _I64, _I64, _VP, _VP, _VP, _VP, _VP, _VP)
 _sig("lmd_vl_ci_build", _INT, C.POINTER(Grid), _D, _INT, _INT, _I64, _VP, _VP, _I32, _VP, _VP,
      _VP, _VP, _VP, _I32, _VP, _VP, _VP, _VP, _VP, _VP)
 _sig("lmd_vl_ci_ev_slots", _I64, _I64, _INT)

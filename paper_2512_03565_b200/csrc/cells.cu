@@ -231,7 +231,8 @@ __global__ void halo_refresh_soa_kernel(BoxK b, int64_t nh, const int32_t* __res
                                         const int8_t* __restrict__ shift,
                                         const double* __restrict__ x, const double* __restrict__ y,
                                         const double* __restrict__ z, double* __restrict__ ox,
-                                        double* __restrict__ oy, double* __restrict__ oz) {
+                                        double* __restrict__ oy, double* __restrict__ oz,
+                                        int stride) {
   int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k >= nh) return;
   int32_t o = owner[k];
@@ -246,9 +247,9 @@ __global__ void halo_refresh_soa_kernel(BoxK b, int64_t nh, const int32_t* __res
                        : (d == 2 ? __dadd_rn(b.lo[ax], -b.hi[ax]) : 0.0);
     q[ax] = __dadd_rn(p[ax], sh);
   }
-  ox[k] = q[0];
-  oy[k] = q[1];
-  oz[k] = q[2];
+  ox[k * stride] = q[0];
+  oy[k * stride] = q[1];
+  oz[k * stride] = q[2];
 }
 
 // ------------------------------------------------ deterministic reductions
@@ -488,7 +489,17 @@ int lmd_halo_refresh_soa(const lmd_box* box, int64_t nh, const int32_t* owner,
                          double* ox, double* oy, double* oz, void* stream) {
   if (nh <= 0) return LMD_OK;
   halo_refresh_soa_kernel<<<grid1d(nh, 256), 256, 0, (cudaStream_t)stream>>>(
-      make_boxk(box), nh, owner, shift, x, y, z, ox, oy, oz);
+      make_boxk(box), nh, owner, shift, x, y, z, ox, oy, oz, 1);
+  LMD_CHECK_LAUNCH();
+  return LMD_OK;
+}
+
+int lmd_halo_refresh_rows(const lmd_box* box, int64_t nh, const int32_t* owner,
+                          const int8_t* shift, const double* x, const double* y, const double* z,
+                          double* rows, void* stream) {
+  if (nh <= 0) return LMD_OK;
+  halo_refresh_soa_kernel<<<grid1d(nh, 256), 256, 0, (cudaStream_t)stream>>>(
+      make_boxk(box), nh, owner, shift, x, y, z, rows, rows + 1, rows + 2, 3);
   LMD_CHECK_LAUNCH();
   return LMD_OK;
 }

@@ -89,6 +89,20 @@ class VerletListContainer:
         self.n3_mode = "full_list"
         self._collected_into = None
         self._clusters_cache: dict = {}
+        # segmented staged lists (csrc/vls.cu): the default for v_by_one full
+        # lists (N3 off, or Newton3 by bookkeeping).  Entries whose build-time
+        # distance is below rc + inner_skin form the inner segment, which
+        # alone covers every pair while no particle moved inner_skin / 2 since
+        # the build (decided on the device from the refresh's displacement)
+        self.segmented = True
+        self.inner_skin = 0.1
+        self._vls: dict = {}
+        self._vls_plan = None
+        self._vls_cap = None
+        self._vls_ev = None
+        self._disp = None          # (2,) int64: bit patterns of max |dr|^2, per slot
+        self._disp_slot = -1       # slot of the last fused refresh (-1: unknown)
+        self._pos4_stale = False
 
     # ------------------------------------------------------------ protocol
     def needs_rebuild(self, owned) -> bool:
@@ -148,6 +162,10 @@ class VerletListContainer:
             self._soa = self._new_soa(n + nh + 1, dev)
         else:
             self._soa = torch.empty((3, 1), dtype=torch.float64, device=dev)
+        # (x, y, z) rows for the segmented lists (+2 rows: staged runs are
+        # rounded to even lengths)
+        self._rows = (torch.zeros((n + nh + 2, 3), dtype=torch.float64, device=dev)
+                      if self.segmented else None)
         # every owned slot is written by the force kernel (Newton3 zeroes first)
         self._fx = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
         self._fy = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
@@ -156,6 +174,15 @@ class VerletListContainer:
         # lists are built lazily per interaction order: always from the
         # rebuild-time positions, whatever the particles did since
         self._build_pos4 = self._pos4.clone()
+        self._build_rows = self._rows.clone() if self.segmented else None
+        self._vls.clear()
+        self._vls_plan = None
+        if self._disp is None or self._disp.device != dev:
+            self._disp = torch.zeros(2, dtype=torch.int64, device=dev)
+        else:
+            self._disp.zero_()
+        self._disp_slot = -1 if self._external_halo else 0
+        self._pos4_stale = False
         self._lists.clear()
         self._staging.clear()
         self._counts.clear()
@@ -165,10 +192,59 @@ class VerletListContainer:
         self.steps_since_rebuild = 0
         self.structure_version += 1
 
-    def _load_positions(self, d, ghosts=None, ghost_rows=None) -> None:
+    def _need_pos4(self) -> bool:
+        """Whether a kernel reading the pos4 records may run on these lists
+        (the segmented kernels read the SoA rows only)."""
+        return not self.segmented or any(k not in self._vls for k in self._lists)
+
+    def _regen_pos4(self) -> None:
+        """pos4 and the SoA copies from the current rows (after refreshes
+        that only wrote the rows)."""
+        n, nh = self.n_owned, self.n_halo
+        soa = self.use_soa and self._soa.shape[1] >= n + nh + 1
+        N.call("lmd_vls_rows_to_legacy", n + nh, n, N.ptr(self._rows), N.ptr(self._pos4),
+               N.ptr(self._soa[0]) if soa else None, N.ptr(self._soa[1]) if soa else None,
+               N.ptr(self._soa[2]) if soa else None, N.stream())
+        self._pos4_stale = False
+
+    def _load_rows(self, d, ghosts=None, ghost_rows=None, disp: bool = False) -> None:
+        """Current positions into the (x, y, z) rows of the segmented lists;
+        with ``disp`` the owned gather also reduces the largest displacement
+        since the build into the next displacement slot (on the device)."""
+        n, nh = self.n_owned, self.n_halo
+        s = N.stream()
+        rows = self._rows
+        if n:
+            dp = None
+            slot = 0
+            if disp and not self._external_halo and self._build_rows is not None:
+                slot = 0 if self._disp_slot < 0 else self._disp_slot ^ 1
+                dp = self._disp
+            N.call("lmd_vls_refresh", n, N.ptr(self._perm), N.ptr(d.pos_x), N.ptr(d.pos_y),
+                   N.ptr(d.pos_z), N.ptr(rows), N.ptr(self._build_rows) if dp is not None else None,
+                   N.ptr(dp), slot, s)
+            if disp:
+                self._disp_slot = slot if dp is not None else -1
+        if not nh:
+            return
+        if ghost_rows is not None:
+            N.call("lmd_vls_gather_rows", nh, N.ptr(self._hperm), N.ptr(ghost_rows),
+                   N.ptr(rows[n:]), s)
+        elif ghosts is not None:
+            N.call("lmd_vls_refresh", nh, N.ptr(self._hperm), N.ptr(ghosts.pos_x),
+                   N.ptr(ghosts.pos_y), N.ptr(ghosts.pos_z), N.ptr(rows[n:]), None, None, 0, s)
+        else:
+            N.call("lmd_halo_refresh_rows", N.make_box(self.box), nh, N.ptr(self._halo_owner),
+                   N.ptr(self._halo_shift), N.ptr(d.pos_x), N.ptr(d.pos_y), N.ptr(d.pos_z),
+                   N.ptr(rows[n:]), s)
+
+    def _load_positions(self, d, ghosts=None, ghost_rows=None, fused: bool = False) -> None:
         """Current positions into pos4 and the SoA copies, in rebuild-time order:
         owned via the cell permutation; images either moved with their owners
-        (shift codes) or, for an external ghost layer, gathered from it."""
+        (shift codes) or, for an external ghost layer, gathered from it.
+        ``fused`` (per-step refresh of segmented lists): the owned gather also
+        reduces the largest displacement since the build on the device, and
+        pos4 is written only when a kernel reading it may run."""
         n, nh = self.n_owned, self.n_halo
         s = N.stream()
         soa = self.use_soa
@@ -176,6 +252,13 @@ class VerletListContainer:
             if self._soa.shape[1] < n + nh + 1:   # SoA switched on after the rebuild
                 self._soa = self._new_soa(n + nh + 1, self._pos4.device)
             sx, sy, sz = self._soa[0], self._soa[1], self._soa[2]
+        if self.segmented and self._rows is not None:
+            self._load_rows(d, ghosts, ghost_rows, disp=fused)
+        write4 = not (fused and self.segmented) or self._need_pos4()
+        if not write4:
+            self._pos4_stale = True
+            return
+        self._pos4_stale = False
         if n:
             if soa:
                 N.call("lmd_gather_pos4_soa", n, N.ptr(self._perm), N.ptr(d.pos_x),
@@ -234,11 +317,12 @@ class VerletListContainer:
             if halo is None or len(halo) != self.n_halo:
                 raise ConfigurationError("refresh needs the same ghost layer as the rebuild")
             if isinstance(halo, torch.Tensor):    # row-major (n_halo, 3) ghost positions
-                self._load_positions(device_soa(owned), None, ghost_rows=halo)
+                self._load_positions(device_soa(owned), None, ghost_rows=halo, fused=True)
                 return
-            self._load_positions(device_soa(owned), device_soa(halo, self._pos4.device))
+            self._load_positions(device_soa(owned), device_soa(halo, self._pos4.device),
+                                 fused=True)
             return
-        self._load_positions(device_soa(owned))
+        self._load_positions(device_soa(owned), fused=True)
 
     refresh_positions = refresh
 
@@ -350,6 +434,11 @@ class VerletListContainer:
             return hit
         n = self.n_owned
         dev = self._pos4.device
+        if staged and n and self.segmented and align == 0:
+            hit = self._vls_lists(key)
+            if hit is not None:
+                self._lists[key] = hit
+                return hit
         if ci > 1:
             cl_first, cl_len, units = self._clusters(ci)
         else:
@@ -450,13 +539,121 @@ class VerletListContainer:
         self._lists[key] = hit
         return hit
 
+    def _vls_plan_groups(self):
+        """Row-aligned groups and their staged runs (one host read: the
+        number of groups and the largest staging footprint)."""
+        plan = self._vls_plan
+        if plan is not None:
+            return plan
+        dev = self._pos4.device
+        lib = N.load()
+        g = self.grid
+        ncell = int(g.ncell)
+        nrows = int(g.tdims[1] * g.tdims[2])
+        maxg = int(lib.lmd_vls_max_groups(g, self.n_owned))
+        tb = int(lib.lmd_vls_plan_temp_bytes(g))
+        plan = {
+            "fs_own": torch.empty(ncell, dtype=torch.int32, device=dev),
+            "fs_img": torch.empty(ncell, dtype=torch.int32, device=dev),
+            "groups": torch.empty(maxg * 64, dtype=torch.int32, device=dev),
+            "info": torch.zeros(8, dtype=torch.int32, device=dev),
+            "maxg": maxg,
+        }
+        rg = torch.empty(nrows, dtype=torch.int32, device=dev)
+        re = torch.empty(nrows, dtype=torch.int32, device=dev)
+        temp = torch.empty(max(tb, 1), dtype=torch.uint8, device=dev)
+        N.call("lmd_vls_plan", g, self.n_owned, N.ptr(self._o_start), N.ptr(self._o_count),
+               N.ptr(self._h_start), N.ptr(self._h_count), N.ptr(plan["fs_own"]),
+               N.ptr(plan["fs_img"]), N.ptr(rg), N.ptr(re), N.ptr(temp), tb, N.ptr(plan["groups"]),
+               N.ptr(plan["info"]), N.stream())
+        info = plan["info"].tolist()
+        plan["rows"] = int(lib.lmd_vls_rows_for(info[0]))
+        plan["ngroups"] = info[2]
+        self._vls_plan = plan
+        return plan
+
+    def _vls_lists(self, key):
+        """Segmented staged lists (csrc/vls.cu) for the v_by_one full lists;
+        None when a group's staging footprint or a lane's list is too large
+        for them (the other staged path then serves)."""
+        if self._build_rows is None:
+            return None
+        plan = self._vls_plan_groups()
+        if plan["rows"] == 0:
+            return None
+        dev = self._pos4.device
+        lib = N.load()
+        n = self.n_owned
+        maxg = plan["maxg"]
+        rl = float(self.params.interaction_length)
+        rin = min(float(self.params.cutoff) + float(self.inner_skin), rl)
+        cap = self._vls_cap
+        if cap is None:
+            vol = float(np.prod(self.box.lengths))
+            est = (self.n_owned + self.n_halo) / vol * (4.0 / 3.0) * np.pi * rl ** 3
+            cap = int(min(255, est * 1.5 + 16))
+        info = plan["info"]
+        s = N.stream()
+        ng = plan["ngroups"]
+        while True:
+            cap_chunks = cap // 8 + 2
+            nbr = torch.empty(ng * 4 * cap_chunks * 32 * 4, dtype=torch.int32, device=dev)
+            segc = torch.empty(ng * 4 * 2, dtype=torch.int32, device=dev)
+            slotmap = torch.empty(ng * 128, dtype=torch.uint8, device=dev)
+            count = torch.zeros(max(n, 1), dtype=torch.int32, device=dev)
+            half = torch.zeros(max(n, 1), dtype=torch.int32, device=dev)
+            info[3:5].zero_()
+            N.call("lmd_vls_build", self.grid, rin * rin, rl * rl, n, plan["rows"],
+                   N.ptr(self._build_rows), N.ptr(plan["fs_own"]), N.ptr(self._o_count),
+                   N.ptr(plan["fs_img"]), N.ptr(self._h_count), N.ptr(plan["groups"]), ng,
+                   cap_chunks, cap, N.ptr(nbr), N.ptr(segc), N.ptr(slotmap), N.ptr(count),
+                   N.ptr(half), N.ptr(info), s)
+            chunks_seen, ent_seen = info[3:5].tolist()
+            if ent_seen <= cap and chunks_seen <= cap_chunks:
+                break
+            if ent_seen > 255:
+                return None
+            cap = min(255, ent_seen + 8)
+        self._vls_cap = min(255, int(ent_seen * 1.2) + 8)
+        self._counts.setdefault(False, count)
+        if self.n3_mode == "full_list":
+            self._counts.setdefault(True, half)
+        hit = {"nbr": nbr, "segc": segc, "slotmap": slotmap, "cap_chunks": cap_chunks,
+               "plan": plan,
+               "total": ng * 4 * cap_chunks * 32 * 8}
+        self._vls[key] = hit
+        return (None, None, nbr, hit["total"])
+
+    def _vls_outer(self) -> bool:
+        """Whether the next segmented launch runs the outer segment too (the
+        device decides; this mirrors it for statistics)."""
+        if self._disp_slot < 0:
+            return True
+        d = float(torch.tensor(self._disp[self._disp_slot].item(), dtype=torch.int64)
+                  .view(torch.float64).item())
+        return d >= self._vls_half_delta2()
+
+    def _vls_half_delta2(self) -> float:
+        # (delta / 2)^2 with a relative margin against rounding in the
+        # displacement and distance evaluations
+        return (0.5 * float(self.inner_skin) * (1.0 - 1e-9)) ** 2
+
     def gpu_lane_stats(self, pattern, newton3: bool = False):
         """(lane_steps, active_lanes) of the force kernel over the current
         lists: every tile runs kmax/B fill steps on 32 lanes; a lane is
         active when its entry is a real neighbour, not the sentinel pad
         (SURVEY §8f-4).  Exact by construction of the list layout."""
         pattern = as_pattern(pattern)
-        _, kmax, _, _ = self._list(pattern, self._list_n3(newton3), ci=self._ci_for(newton3))
+        tile_off, kmax, _, _ = self._list(pattern, self._list_n3(newton3),
+                                          ci=self._ci_for(newton3))
+        if tile_off is None:   # segmented lists: chunks of 8 steps per tile segment
+            vls = self._vls_for(pattern, newton3)
+            ng = vls["plan"]["ngroups"]
+            segc = vls["segc"][: 8 * ng].view(-1, 2).long()
+            steps = int(segc.sum().item()) * 8
+            active = int(self._count(self._list_n3(newton3), pattern)[: self.n_owned].long()
+                         .sum().item())
+            return 32 * steps, active
         b = pattern.shape(32)[1]
         ntiles = int(N.load().lmd_vl_num_tiles(self.n_owned, pattern.code))
         steps = int((kmax[:ntiles].long() // b).sum().item())
@@ -465,6 +662,15 @@ class VerletListContainer:
         if self._ci_for(newton3) > 1:   # union lists: one entry serves a cluster
             raise ConfigurationError("lane statistics cover per-particle lists")
         return 32 * steps, active
+
+    def _key(self, pattern, newton3: bool):
+        ci = self._ci_for(newton3)
+        n3l = self._list_n3(newton3)
+        return (pattern.code, n3l, ci, self.align_window, self._bank_for(ci),
+                self._staged_for(pattern, n3l, ci) if self.align_window == 0 else 0)
+
+    def _vls_for(self, pattern, newton3: bool):
+        return self._vls.get(self._key(as_pattern(pattern), newton3))
 
     def ensure_lists(self, pattern, newton3: bool) -> bool:
         """Build the lists for this interaction order now (outside any timed
@@ -484,7 +690,10 @@ class VerletListContainer:
         """List entries the force kernel reads for `pattern` (padded to whole
         fill steps and 4-step chunks; 4 B each)."""
         pattern = as_pattern(pattern)
-        _, kmax, _, _ = self._list(pattern, newton3)
+        n3l = self._list_n3(newton3)
+        tile_off, kmax, _, _ = self._list(pattern, n3l, ci=self._ci_for(newton3))
+        if tile_off is None:
+            return self.gpu_lane_stats(pattern, newton3)[0]
         b = pattern.shape(32)[1]
         return int((kmax.long() // b).sum().item()) * 32
 
@@ -529,6 +738,8 @@ class VerletListContainer:
         else:
             stats_t.zero_()
         if ci > 1:
+            if self._pos4_stale:
+                self._regen_pos4()
             cl_first, cl_len, units = self._clusters(ci)
             if ev_t is None:
                 slots = int(N.load().lmd_vl_ci_ev_slots(units, pattern.code))
@@ -538,6 +749,30 @@ class VerletListContainer:
                    N.ptr(self._pos4), N.ptr(tile_off), N.ptr(kmax), N.ptr(nbr), N.ptr(self._fx),
                    N.ptr(self._fy), N.ptr(self._fz), N.ptr(ev_t), N.ptr(stats_t), N.stream())
             return stats_t
+        vls = self._vls.get(self._key(pattern, newton3))
+        if vls is not None and mode != 1:
+            plan = vls["plan"]
+            if energy:
+                slots = int(N.load().lmd_vls_ev_slots(plan["ngroups"]))
+                if ev_t is None or ev_t.numel() < 2 * slots:
+                    if self._vls_ev is None or self._vls_ev.numel() < 2 * slots:
+                        self._vls_ev = torch.empty(2 * slots, dtype=torch.float64, device=dev)
+                    ev_t = self._vls_ev
+            direct = out is not None and len(out) == self.n_owned
+            fx, fy, fz = ((out.force_x, out.force_y, out.force_z) if direct
+                          else (self._fx, self._fy, self._fz))
+            disp = None if self._disp_slot < 0 else self._disp[self._disp_slot:]
+            N.call("lmd_vls_force", mode, N.FLAG_ENERGY if energy else 0,
+                   N.make_lj(self.params), self.n_owned, plan["rows"], N.ptr(self._rows),
+                   N.ptr(plan["groups"]), plan["ngroups"], N.ptr(plan["info"]), N.ptr(vls["nbr"]),
+                   N.ptr(vls["segc"]), N.ptr(vls["slotmap"]), vls["cap_chunks"], N.ptr(disp),
+                   self._vls_half_delta2(), N.ptr(self._perm) if direct else None, N.ptr(fx),
+                   N.ptr(fy), N.ptr(fz), N.ptr(ev_t) if energy else None, N.ptr(stats_t),
+                   N.stream())
+            self._collected_into = out if direct else None
+            return stats_t
+        if self._pos4_stale:
+            self._regen_pos4()
         if ev_t is None:
             slots = int(N.load().lmd_vl_ev_slots(self.n_owned, pattern.code))
             ev_t = torch.empty(2 * max(slots, 1), dtype=torch.float64, device=dev)

@@ -23,19 +23,41 @@ def test_two_ranks_on_one_gpu_gloo():
     env = dict(os.environ, LMD_DIST_BACKEND="gloo", LMD_DEVICE="0")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", "29561", "bench.py", "--gpus", "2",
-           "--steps", "2", "--warmup", "3", "--particles", "200000"]
+           "--steps", "2", "--warmup", "3", "--workload", "c2", "--particles", "200000"]
     r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     line = [ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1]
     d = json.loads(line)
     assert d["n_gpus"] == 2 and d["config"]["parallelism"].startswith("bricks (2, 1, 1)")
     single = subprocess.run([sys.executable, "bench.py", "--steps", "2", "--warmup", "3",
-                             "--n=200000", "--e2e-steps", "0", "--no-cpu-baseline"], cwd=ROOT,
+                             "--workload", "c2", "--n=200000", "--e2e-steps", "0",
+                             "--no-cpu-baseline"], cwd=ROOT,
                             capture_output=True, text=True, timeout=600)
     assert single.returncode == 0, single.stderr[-2000:]
     s = json.loads([ln for ln in single.stdout.splitlines() if ln.startswith("{")][-1])
     one = s["config"]["pairs_per_step"]
     assert abs(d["config"]["pairs_per_step"] - 2 * one) < 1e-3 * one
+
+
+def test_strong_scaling_c4_bricks_match_single_domain():
+    """The headline workload (BASELINE config 4, here a 48^3 lattice) split
+    into 2x1x1 bricks: the global pair count equals the single-domain count
+    exactly (ghost pairs are one-sided, counted once on the owning rank)."""
+    env = dict(os.environ, LMD_DIST_BACKEND="gloo", LMD_DEVICE="0")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29564", "bench.py", "--gpus", "2",
+           "--steps", "2", "--warmup", "3", "--workload", "c4", "--particles", str(48 ** 3)]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert d["scaling"] == "strong" and d["config"]["parallelism"].startswith("bricks (2, 1, 1)")
+    single = subprocess.run([sys.executable, "bench.py", "--steps", "2", "--warmup", "3",
+                             "--workload", "c4", f"--n={48 ** 3}", "--e2e-steps", "0",
+                             "--no-cpu-baseline"], cwd=ROOT, capture_output=True, text=True,
+                            timeout=600)
+    assert single.returncode == 0, single.stderr[-2000:]
+    s = json.loads([ln for ln in single.stdout.splitlines() if ln.startswith("{")][-1])
+    assert d["config"]["pairs_per_step"] == s["config"]["pairs_per_step"]
 
 
 def test_brick_md_two_ranks_matches_single_domain():

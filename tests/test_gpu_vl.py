@@ -242,6 +242,7 @@ def test_staged_and_bank_ordered_lists_match_oracle(rng, staged, bank, index16, 
         prev = None
         for _ in range(2):
             cont = B.VerletListContainer(box, params)
+            cont.segmented = False     # the round-1 staged path (fallback)
             cont.staged_group = staged
             cont.bank_rounds = bank
             cont.index16 = index16

@@ -1,0 +1,129 @@
+"""Segmented staged Verlet lists (csrc/vls.cu), the default v_by_one path.
+
+The lists hold every candidate within rc + skin of the build positions, the
+inner segment those within rc + inner_skin; the force kernel runs the inner
+segment alone while no particle moved inner_skin / 2 since the build, and
+both segments afterwards (decided on the device).  Checked against the
+oracle (the reference's force phase restated, oracle/lj_oracle.c) at the
+CURRENT positions: pair counts exact, forces within the reference's
+forces_close, energy / virial 1e-12 -- before any move, after moves that keep
+the inner segment valid, and after moves that need the outer segment."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import forces_close, jittered_lattice
+from oracle import oracle as O
+
+import paper_2512_03565_b200 as B
+from paper_2512_03565_b200 import LJParams, ParticleBuffer, PatternKind, SimulationBox
+
+pytestmark = pytest.mark.gpu
+
+
+def _state(rng, n, rho):
+    span = (n / rho) ** (1 / 3)
+    k = int(np.ceil(n ** (1 / 3)))
+    pos = jittered_lattice(rng, (k, k, k), span / k, 0.3 * span / k)[:n]
+    return pos, span
+
+
+def _check(cont, buf, pos, span, periodic, params, n3):
+    of, ost = O.force_phase_vl(pos, np.zeros(3), np.full(3, span), [periodic] * 3, params, n3,
+                               "v_by_one", 8)
+    st = cont.compute_forces("vl", n3, PatternKind.V_BY_ONE, 8, energy=True)
+    cont.collect_forces(buf)
+    f = buf.forces().cpu().numpy()
+    assert st.pair_interactions == ost.pair_interactions
+    assert forces_close(f, of)
+    assert abs(st.epot - ost.epot) <= 1e-12 * abs(ost.epot)
+    assert abs(st.virial - ost.virial) <= 1e-12 * abs(ost.virial)
+    return st, f
+
+
+@pytest.mark.parametrize("n3", [False, True])
+@pytest.mark.parametrize("periodic", [True, False])
+def test_segmented_lists_match_oracle_and_are_used(rng, periodic, n3):
+    pos, span = _state(rng, 6000, 0.8)
+    params = LJParams(cutoff=2.5, skin=0.3)
+    box = SimulationBox.cube(span, periodic=periodic)
+    prev = None
+    for _ in range(2):
+        cont = B.VerletListContainer(box, params)
+        buf = ParticleBuffer.from_positions(pos, device="cuda")
+        cont.rebuild(buf)
+        cont.refresh(buf)
+        st, f = _check(cont, buf, pos, span, periodic, params, n3)
+        assert cont._vls_for("v_by_one", n3) is not None      # the segmented path ran
+        _, ost = O.force_phase_vl(pos, np.zeros(3), np.full(3, span), [periodic] * 3, params,
+                                  n3, "v_by_one", 8)
+        assert (st.kernel_invocations, st.lane_slots, st.useful_interactions) == \
+            ost.as_tuple()[:3]
+        if prev is not None:
+            assert np.array_equal(prev, f)                     # deterministic
+        prev = f
+
+
+@pytest.mark.parametrize("move", [0.02, 0.07, 0.14])
+def test_segments_cover_moved_particles(rng, move):
+    """Moves below inner_skin / 2 (0.05) run the inner segment, larger ones
+    (up to skin / 2 = 0.15) need the outer segment -- exact either way."""
+    pos, span = _state(rng, 8000, 0.8)
+    params = LJParams(cutoff=2.5, skin=0.3)
+    box = SimulationBox.cube(span, periodic=True)
+    cont = B.VerletListContainer(box, params)
+    buf = ParticleBuffer.from_positions(pos, device="cuda")
+    cont.rebuild(buf)
+    cont.refresh(buf)
+    cont.ensure_lists("v_by_one", False)
+    d = rng.normal(size=pos.shape)
+    d *= (move * 0.999) / np.linalg.norm(d, axis=1, keepdims=True)
+    moved = pos + d
+    for ax, t in enumerate((buf.pos_x, buf.pos_y, buf.pos_z)):
+        t.copy_(torch.from_numpy(np.ascontiguousarray(moved[:, ax])))
+    cont.refresh(buf)
+    assert cont._vls_outer() == (move >= 0.05)
+    _check(cont, buf, moved, span, True, params, False)
+
+
+def test_inner_skin_equal_to_skin_and_zero(rng):
+    """Degenerate segmentations: everything inner (inner_skin >= skin) or
+    everything outer (inner_skin = 0: the inner segment holds r < rc)."""
+    pos, span = _state(rng, 5000, 0.7)
+    params = LJParams(cutoff=2.5, skin=0.3)
+    box = SimulationBox.cube(span, periodic=True)
+    for inner in (0.3, 0.0):
+        cont = B.VerletListContainer(box, params)
+        cont.inner_skin = inner
+        buf = ParticleBuffer.from_positions(pos, device="cuda")
+        cont.rebuild(buf)
+        cont.refresh(buf)
+        _check(cont, buf, pos, span, True, params, False)
+
+
+def test_collect_fused_and_overlap(rng):
+    """Forces written straight into the caller's order (launch_force(out=)),
+    and a coincident pair raises ParticleOverlapError as the reference does."""
+    pos, span = _state(rng, 4000, 0.6)
+    params = LJParams(cutoff=2.5, skin=0.3)
+    box = SimulationBox.cube(span, periodic=True)
+    of, _ = O.force_phase_vl(pos, np.zeros(3), np.full(3, span), [True] * 3, params, False,
+                             "v_by_one", 8)
+    cont = B.VerletListContainer(box, params)
+    buf = ParticleBuffer.from_positions(pos, device="cuda")
+    cont.rebuild(buf)
+    cont.refresh(buf)
+    cont.launch_force("v_by_one", False, out=buf)
+    cont.collect_forces(buf)
+    assert forces_close(buf.forces().cpu().numpy(), of)
+    bad = pos.copy()
+    bad[1] = bad[0]
+    buf2 = ParticleBuffer.from_positions(bad, device="cuda")
+    cont2 = B.VerletListContainer(box, params)
+    cont2.rebuild(buf2)
+    cont2.refresh(buf2)
+    with pytest.raises(B.ParticleOverlapError):
+        cont2.compute_forces("vl", False, PatternKind.V_BY_ONE, 8)
