@@ -286,6 +286,45 @@ __global__ void __launch_bounds__(kVsG, 4)
     py = xs[3 * irow + 1];
     pz = xs[3 * irow + 2];
   }
+  // FP32 copies of the staged rows relative to the group's first particle,
+  // written over the FP64 rows (row j: float4 at byte 16 j) in rounds of
+  // 128 rows -- a round's writes never reach a later round's rows
+  const int S = rec[kVsS];
+  const int self0 = rec[kVsSelf];
+  const double ox = xs[3 * self0], oy = xs[3 * self0 + 1], oz = xs[3 * self0 + 2];
+  float4* xf = reinterpret_cast<float4*>(sm_b);
+  float rmax = 0.f;
+#pragma unroll 1
+  for (int r0 = 0; r0 < S; r0 += kVsG) {
+    const int j = r0 + tid;
+    double a = 0.0, b = 0.0, c = 0.0;
+    if (j < S) {
+      a = xs[3 * j] - ox;
+      b = xs[3 * j + 1] - oy;
+      c = xs[3 * j + 2] - oz;
+    }
+    __syncthreads();
+    if (j < S) {
+      xf[j] = make_float4((float)a, (float)b, (float)c, 0.f);
+      rmax = fmaxf(rmax, fmaxf(fabsf((float)a), fmaxf(fabsf((float)b), fabsf((float)c))));
+    }
+  }
+  // decision bounds: |FP32 r2 - exact r2| <= err for coordinates up to
+  // rmax from the origin (conversion: 2^-24 rmax per coordinate, twice per
+  // difference; arithmetic: a few ulp of rl^2); outside [rl2 - err, rl2 +
+  // err) the FP32 decision is the exact one, inside the candidate is
+  // re-tested exactly from the FP64 rows in global memory
+  __shared__ float rmax_sm;
+  if (tid == 0) rmax_sm = 0.f;
+  __syncthreads();
+  atomicMax(reinterpret_cast<int*>(&rmax_sm), __float_as_int(rmax));  // rmax >= 0
+  __syncthreads();
+  const double rl = sqrt(rl2);
+  const double err = 8.0 * 5.9604644775390625e-8 * ((double)rmax_sm + 4.0) * 2.0 * rl +
+                     8.0 * 5.9604644775390625e-8 * rl2;
+  const float rl2_lo = (float)(rl2 - err), rl2_hi = (float)(rl2 + err);
+  const float rin2_hi = (float)(rin2 + err);
+  const float pxf = (float)(px - ox), pyf = (float)(py - oy), pzf = (float)(pz - oz);
   int n_in = 0, n_half = 0, n_ent = 0;
 #pragma unroll 1
   for (int q = 0; q < kVsRuns; ++q) {
@@ -303,17 +342,65 @@ __global__ void __launch_bounds__(kVsG, 4)
     const int u1 = __reduce_max_sync(0xffffffffu, l1 > l0 ? l1 : 0);
     const unsigned span = (unsigned)(l1 - l0);
     const int gshift = st - rb;  // global row of local row j: j + gshift
+    // lean, branch-free walk: hits are appended (predicated store), the
+    // rare candidates whose FP32 r2 falls in the band around rl^2 are noted
+    // and decided exactly after the run
+    int pend = -1, npend = 0;
+    auto append = [&](int j, bool inner) {
+      if (n_ent < cap_ent) hits[n_ent] = (uint16_t)(j | (inner ? 0 : 0x8000));
+      ++n_ent;
+      n_in += inner ? 1 : 0;
+      n_half += (v || j + gshift > p) ? 1 : 0;
+    };
+    {
+      uint16_t* const hp = hits + n_ent;
+      const int left = cap_ent - n_ent;  // appends beyond it are counted only
+      int nh = 0, ni = 0, nhalf = 0;
+      // owned runs: j counts towards the half list when its global row
+      // exceeds p (image runs: always)
+      const int half_from = v ? -0x7fffffff : p - gshift;
 #pragma unroll 2
-    for (int j = u0; j < u1; ++j) {
-      const double r2 = r2_exact(px - xs[3 * j], py - xs[3 * j + 1], pz - xs[3 * j + 2]);
-      if ((unsigned)(j - l0) < span && j != irow && r2 < rl2) {
-        const int outer = r2 < rin2 ? 0 : 1;
-        if (n_ent < cap_ent) hits[n_ent] = (uint16_t)(j | (outer << 15));
-        const int bk = (outer << 4) + ((3 * j) & 15);
-        cnt[bk * kVsG + tid] = (uint8_t)(cnt[bk * kVsG + tid] + 1);
-        ++n_ent;
-        n_in += 1 - outer;
-        n_half += (v || j + gshift > p) ? 1 : 0;
+      for (int j = u0; j < u1; ++j) {
+        const float4 f = xf[j];
+        const float dx = pxf - f.x, dy = pyf - f.y, dz = pzf - f.z;
+        const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+        const bool mine = (unsigned)(j - l0) < span && j != irow;
+        const bool hit = mine && r2 < rl2_lo;
+        const bool band = mine && r2 >= rl2_lo && r2 < rl2_hi;
+        pend = band ? j : pend;
+        npend += band ? 1 : 0;
+        const bool inner = r2 < rin2_hi;
+        // predicated store and increments, no branch
+        asm volatile(
+            "{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p st.global.u16 [%0], %1;\n}" ::"l"(hp + nh),
+            "h"((unsigned short)(j | (inner ? 0 : 0x8000))), "r"((unsigned)(hit && nh < left))
+            : "memory");
+        nh += hit ? 1 : 0;
+        ni += (hit && inner) ? 1 : 0;
+        nhalf += (hit && j > half_from) ? 1 : 0;
+      }
+      n_ent += nh;
+      n_in += ni;
+      n_half += nhalf;
+    }
+    if (__any_sync(0xffffffffu, npend > 0)) {
+      // exact decisions (the reference's unfused r2 from the FP64 rows) of
+      // the band candidates: the noted one, or the run again for the rare
+      // lane with several
+      auto exact = [&](int j) {
+        const long long gj = 3LL * (j + gshift);
+        const double r2 = r2_exact(px - rows[gj], py - rows[gj + 1], pz - rows[gj + 2]);
+        if (r2 < rl2) append(j, r2 < rin2);
+      };
+      if (npend == 1) {
+        exact(pend);
+      } else if (npend > 1) {
+        for (int j = l0; j < l1; ++j) {
+          const float4 f = xf[j];
+          const float dx = pxf - f.x, dy = pyf - f.y, dz = pzf - f.z;
+          const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+          if (j != irow && r2 >= rl2_lo && r2 < rl2_hi) exact(j);
+        }
       }
     }
   }
@@ -328,21 +415,44 @@ __global__ void __launch_bounds__(kVsG, 4)
   // 2. counting sort into shared memory (bucket starts -> pos; a lane's
   //    counts stay below 256: cap_ent <= 255)
   uint16_t* mine = sorted + tid * cap_ent;
+  // hits are read back 8 at a time (a lane's stretch is 16-B aligned:
+  // cap_ent % 8 == 0)
+  const uint4* hits8 = reinterpret_cast<const uint4*>(hits);
+  auto hit_at = [](const uint4& v, int e) {
+    const unsigned w = e < 2 ? v.x : e < 4 ? v.y : e < 6 ? v.z : v.w;
+    return (e & 1) ? w >> 16 : w & 0xffffu;
+  };
   if (ok) {
+    for (int e0 = 0; e0 < n_ent; e0 += 8) {
+      const uint4 v = hits8[e0 >> 3];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        if (e0 + e < n_ent) {
+          const unsigned h = hit_at(v, e);
+          const int bk = ((h >> 15) << 4) + ((3 * (h & 0x7fffu)) & 15);
+          cnt[bk * kVsG + tid] = (uint8_t)(cnt[bk * kVsG + tid] + 1);
+        }
+      }
+    }
     int acc = 0;
 #pragma unroll
     for (int b = 0; b < 32; ++b) {
       pos[b * kVsG + tid] = (uint8_t)acc;
       acc += cnt[b * kVsG + tid];
     }
-    __threadfence_block();
-    for (int e = 0; e < n_ent; ++e) {
-      const unsigned h = hits[e];
-      const unsigned j = h & 0x7fffu;
-      const int bk = ((h >> 15) << 4) + ((3 * j) & 15);
-      const int at = pos[bk * kVsG + tid];
-      mine[at] = (uint16_t)j;
-      pos[bk * kVsG + tid] = (uint8_t)(at + 1);
+    for (int e0 = 0; e0 < n_ent; e0 += 8) {
+      const uint4 v = hits8[e0 >> 3];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        if (e0 + e < n_ent) {
+          const unsigned h = hit_at(v, e);
+          const unsigned j = h & 0x7fffu;
+          const int bk = ((h >> 15) << 4) + ((3 * j) & 15);
+          const int at = pos[bk * kVsG + tid];
+          mine[at] = (uint16_t)j;
+          pos[bk * kVsG + tid] = (uint8_t)(at + 1);
+        }
+      }
     }
     // pos[b] = end of bucket b; the emission takes from start = end - cnt
   }
@@ -776,7 +886,8 @@ int lmd_vls_build(const lmd_grid* g, double rin2, double rl2, int64_t n_owned, i
                   int32_t* seg_chunks, uint8_t* slotmap, int32_t* count, int32_t* count_half,
                   int32_t* info, void* stream) {
   if (n_owned <= 0 || max_groups <= 0) return LMD_OK;
-  if (cap_entries < 8 || cap_entries > 255 || !(rin2 <= rl2)) return LMD_ERR_CONFIG;
+  if (cap_entries < 8 || cap_entries > 255 || cap_entries % 8 || !(rin2 <= rl2))
+    return LMD_ERR_CONFIG;
   // each lane's hits fit its tile's list area before the lists are written
   if (cap_chunks < 2 || cap_chunks * 8 < cap_entries) return LMD_ERR_CONFIG;
   if (rows <= 0 || rows > kVsMaxRows + 64 || (uintptr_t)pos_rows % 16) return LMD_ERR_CONFIG;

@@ -591,11 +591,12 @@ class VerletListContainer:
         if cap is None:
             vol = float(np.prod(self.box.lengths))
             est = (self.n_owned + self.n_halo) / vol * (4.0 / 3.0) * np.pi * rl ** 3
-            cap = int(min(255, est * 1.5 + 16))
+            cap = int(min(248, est * 1.5 + 16))
         info = plan["info"]
         s = N.stream()
         ng = plan["ngroups"]
         while True:
+            cap = min(248, (cap + 7) // 8 * 8)   # 16-B aligned lane stretches
             cap_chunks = cap // 8 + 2
             nbr = torch.empty(ng * 4 * cap_chunks * 32 * 4, dtype=torch.int32, device=dev)
             segc = torch.empty(ng * 4 * 2, dtype=torch.int32, device=dev)
@@ -611,10 +612,10 @@ class VerletListContainer:
             chunks_seen, ent_seen = info[3:5].tolist()
             if ent_seen <= cap and chunks_seen <= cap_chunks:
                 break
-            if ent_seen > 255:
+            if ent_seen > 248:
                 return None
-            cap = min(255, ent_seen + 8)
-        self._vls_cap = min(255, int(ent_seen * 1.2) + 8)
+            cap = ent_seen + 8
+        self._vls_cap = min(248, int(ent_seen * 1.2) + 8)
         self._counts.setdefault(False, count)
         if self.n3_mode == "full_list":
             self._counts.setdefault(True, half)
