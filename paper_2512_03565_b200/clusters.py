@@ -336,3 +336,97 @@ class VerletClusterContainer:
                     dst.copy_(val)   # direct device -> (pinned) host DMA
                 else:
                     torch.from_numpy(dst).copy_(val)
+
+
+# ------------------------------------------------------- standalone cluster API
+def build_clusters(buf, size: int, column_length: float | None = None) -> list:
+    """Group particles into clusters of exactly ``size`` entries
+    (containers.py:216-247), on the device: x-y columns of ``column_length``
+    (default: the particles' x/y span over floor(sqrt(n / size)) columns,
+    slightly widened), each column ordered by z (a stable lexsort as two
+    stable device sorts), chunked into ``size``; a column's last chunk is
+    padded with DUMMY entries parked at its bounding-box minimum.  Returns
+    :class:`Cluster` objects whose buffers are device ParticleBuffers."""
+    import math
+    if size < 2:
+        raise ConfigurationError(f"cluster size must be >= 2, got {size}")
+    d = device_soa(buf)
+    n = len(d)
+    if n == 0:
+        return []
+    x, y, z = d.pos_x, d.pos_y, d.pos_z
+    xmin, ymin = x.min(), y.min()
+    if column_length is None:
+        span = max(float((x.max() - xmin).item()), float((y.max() - ymin).item()), 1e-12)
+        column_length = span * (1.0 + 1e-9) / max(1, int(math.sqrt(n / size)))
+    col_x = torch.floor((x - xmin) / column_length).to(torch.int64)
+    col_y = torch.floor((y - ymin) / column_length).to(torch.int64)
+    col = col_x + col_y * (col_x.max() + 1)
+    # np.lexsort((z, col)): stable by z, then stable by col
+    o1 = torch.sort(z, stable=True).indices
+    order = o1[torch.sort(col[o1], stable=True).indices]
+    scol = col[order]
+    starts = torch.nonzero(torch.diff(scol)).flatten() + 1
+    bounds = [0] + starts.tolist() + [n]
+    clusters = []
+    cid = 0
+    for b in range(len(bounds) - 1):
+        lo, hi = bounds[b], bounds[b + 1]
+        for s0 in range(lo, hi, size):
+            clusters.append(_make_cluster(cid, d, order[s0:min(s0 + size, hi)], size))
+            cid += 1
+    return clusters
+
+
+def _make_cluster(cid: int, src, members, size: int) -> Cluster:
+    """containers.py:250-268 on device buffers."""
+    n_real = int(members.shape[0])
+    cb = ParticleBuffer.empty(size, device=src.device)
+    for name in tuple(ParticleBuffer._FLOAT_FIELDS) + ("id", "ownership"):
+        getattr(cb, name)[:n_real] = getattr(src, name)[members]
+    pos = torch.stack([cb.pos_x[:n_real], cb.pos_y[:n_real], cb.pos_z[:n_real]], dim=1)
+    amin = pos.min(dim=0).values
+    amax = pos.max(dim=0).values
+    if n_real < size:
+        cb.pos_x[n_real:] = amin[0]
+        cb.pos_y[n_real:] = amin[1]
+        cb.pos_z[n_real:] = amin[2]
+        cb.id[n_real:] = -1
+        cb.ownership[n_real:] = 2   # DUMMY
+    return Cluster(cid, cb, amin.cpu().numpy(), amax.cpu().numpy(), n_real)
+
+
+def build_cluster_neighbor_lists(clusters: list, interaction_length: float,
+                                 newton3: bool) -> list:
+    """Neighbour cluster ids per cluster by bounding-box distance
+    (containers.py:271-299): d2 = sum of squared per-axis gaps, listed iff
+    d2 <= interaction_length^2; with ``newton3`` each unordered pair once
+    (the lower id keeps it), else in both lists; never self.  The gap
+    expression is evaluated on the device in the reference's order, in
+    blocks of rows (the reference's dense C x C matrix, without the
+    memory)."""
+    n = len(clusters)
+    if n == 0:
+        return []
+    dev = torch.device("cuda") if torch.cuda.is_available() else None
+    if dev is None:
+        raise ConfigurationError("build_cluster_neighbor_lists needs a CUDA device")
+    mins = torch.as_tensor(np.stack([c.aabb_min for c in clusters]), dtype=torch.float64,
+                           device=dev)
+    maxs = torch.as_tensor(np.stack([c.aabb_max for c in clusters]), dtype=torch.float64,
+                           device=dev)
+    limit = interaction_length * interaction_length
+    ids = torch.arange(n, device=dev)
+    lists = []
+    block = 2048
+    for r0 in range(0, n, block):
+        a0, a1 = mins[r0:r0 + block, None, :], maxs[r0:r0 + block, None, :]
+        gap = torch.clamp(torch.maximum(a0 - maxs[None, :, :], mins[None, :, :] - a1), min=0.0)
+        g2 = gap * gap
+        d2 = (g2[..., 0] + g2[..., 1]) + g2[..., 2]
+        close = d2 <= limit
+        rows = ids[r0:r0 + block, None]
+        keep = close & ((ids[None, :] > rows) if newton3 else (ids[None, :] != rows))
+        for row in keep.cpu().numpy():
+            lists.append([int(z) for z in np.nonzero(row)[0]])
+    return lists

@@ -71,7 +71,7 @@ class RunSummary:
     initial_max_per_cell: int
     final_max_per_cell: int
     final_max_speed: float
-    force_time_s: float = 0.0
+    force_time_s: float = 0.0    # device time of the force launches (CUDA events)
     steps: int = 0
     retunes: int = 0
     extra: dict = field(default_factory=dict)
@@ -210,7 +210,7 @@ def run_md(owned, box, params, iterations: int, vector_width: int = 8, *,
     initial_max = max_particles_per_cell(owned, box, margin)
     phase_max = initial_max
     retunes = 0
-    force_time = 0.0
+    force_events: list = []   # CUDA events around each force launch (device time)
     start = time.perf_counter()
     whole = metric == "iteration"
     try:
@@ -258,15 +258,18 @@ def run_md(owned, box, params, iterations: int, vector_width: int = 8, *,
                 rebuilt = rebuilt or fresh or built
             if not whole:
                 provider.begin_region()
-            t0 = time.perf_counter()
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev0.record()
             stats_t = _launch(cont, cfg, vector_width, energy, owned)
+            ev1 = torch.cuda.Event(enable_timing=True)
+            ev1.record()
+            force_events.append((ev0, ev1))
             sample = provider.end_region() if metric not in ("laneops", "iteration") else None
             if deferred and not energy:
                 geo = _geometry(cont, cfg, vector_width)
                 stats = KernelStats(geo[0], geo[1], geo[2], -1)   # pairs filled in late
             else:
                 stats = _finish(cont, cfg, vector_width, stats_t)
-            force_time += time.perf_counter() - t0
             lane_total[0] += stats.lane_slots
             if sample is None and not whole:
                 sample = provider.end_region()
@@ -304,6 +307,7 @@ def run_md(owned, box, params, iterations: int, vector_width: int = 8, *,
         apply_boundaries(owned, box)
     torch.cuda.synchronize()
     wall = time.perf_counter() - start
+    force_time = sum(a.elapsed_time(b) for a, b in force_events) * 1e-3
     speed = torch.sqrt(owned.vel_x ** 2 + owned.vel_y ** 2 + owned.vel_z ** 2)
     failed, selections = [], []
     if tuner is not None:
@@ -462,3 +466,86 @@ def run_md_graph(owned, box, params, iterations: int, vector_width: int = 8, *,
                          force_time_s=0.0, steps=iterations, retunes=0,
                          extra={"rebuilds": rebuilds, "pairs_total": pairs_total})
     return records, summary
+
+
+# ---------------------------------------------------------------- scenarios
+# The reference's scenario-level entry points (driver.py:75-313) over the
+# device MD loop: a ScenarioSpec (scenario.py:47-65; any object with its
+# attributes) is materialised on the device and run with the spec's search
+# space, tuning policy and metric.
+
+def build_initial_state(spec, device="cuda"):
+    """All lattice sources of ``spec`` in one owned buffer (driver.py:75-93):
+    positions in x-fastest lattice order, ids sequential, source velocity plus
+    uniform jitter drawn from ``default_rng(spec.seed)`` in the reference's
+    call order."""
+    from .particles import ParticleBuffer, lattice_positions
+    rng = np.random.default_rng(spec.seed)
+    pos, vel = [], []
+    for src in spec.sources:
+        p = lattice_positions(src.origin, src.counts, src.spacing)
+        v = np.tile(np.asarray(src.velocity, dtype=np.float64).reshape(1, 3), (len(p), 1))
+        pos.append(p)
+        vel.append(v)
+    pos = np.concatenate(pos) if pos else np.zeros((0, 3))
+    vel = np.concatenate(vel) if vel else np.zeros((0, 3))
+    offset = 0
+    for src in spec.sources:
+        n = int(np.prod(src.counts))
+        if src.jitter > 0:
+            for ax in range(3):
+                vel[offset:offset + n, ax] += rng.uniform(-src.jitter, src.jitter, n)
+        offset += n
+    buf = ParticleBuffer.from_positions(pos, device=device)
+    for ax, name in enumerate(("vel_x", "vel_y", "vel_z")):
+        getattr(buf, name).copy_(torch.from_numpy(np.ascontiguousarray(vel[:, ax])))
+    return buf
+
+
+def resolve_search_space(spec) -> list:
+    """enumerate_search_space over the spec's axes (driver.py:103-105)."""
+    from .tuning import enumerate_search_space
+    return enumerate_search_space(spec.containers, spec.traversals, spec.newton3_options,
+                                  spec.patterns)
+
+
+def run_simulation(spec, fixed_config: Configuration | None = None, **kw):
+    """The reference's ``run_simulation`` (driver.py:132-224) on the device:
+    returns (records, summary).  Without ``fixed_config`` the tuner searches
+    ``resolve_search_space(spec)`` with the reference's default tuning
+    interval ``max(1000, samples * |space|)``; the metric is ``spec.metric``
+    ("laneops" is deterministic and reproduces the reference's records)."""
+    owned = build_initial_state(spec)
+    policy = None
+    configs = None
+    if fixed_config is None:
+        configs = resolve_search_space(spec)
+        if not configs:
+            raise ConfigurationError("search space has no valid configuration")
+        interval = spec.tuning_interval
+        if interval is None:
+            interval = max(1000, spec.samples_per_config * len(configs))
+        policy = TuningPolicy(spec.samples_per_config, interval, spec.reduction, spec.metric)
+    return run_md(owned, spec.box, spec.params, spec.iterations, spec.vector_width,
+                  configurations=configs, fixed_config=fixed_config, policy=policy,
+                  metric=spec.metric, cluster_size=spec.cluster_size,
+                  rebuild_period=spec.rebuild_period, **kw)
+
+
+def emit_summary(summary, path) -> None:
+    """The reference's summary text (driver.py:296-313)."""
+    lines = [
+        f"particle_count: {summary.particle_count}",
+        f"wall_time_s: {summary.wall_time_s:.3f}",
+        f"total_force_phase_metric: {repr(summary.total_metric)}",
+        f"initial_max_per_cell: {summary.initial_max_per_cell}",
+        f"final_max_per_cell: {summary.final_max_per_cell}",
+        f"final_max_speed: {repr(summary.final_max_speed)}",
+        f"phase_selections: {' '.join(summary.phase_selections) or '-'}",
+        f"failed_configs: {' '.join(summary.failed_configs) or '-'}",
+        "per_config_metric:",
+    ]
+    for label, total in summary.per_config_metric.items():
+        lines.append(f"  {label}: {repr(total)}")
+    with open(path, "w", encoding="utf-8", newline="\n") as fh:
+        fh.write("\n".join(lines) + "\n")

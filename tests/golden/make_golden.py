@@ -229,12 +229,79 @@ def clusters(L):
     np.savez_compressed(os.path.join(HERE, "clusters.npz"), **out)
 
 
+def api_spec(L):
+    """The scenario run by api(): a jittered lattice block, periodic box, a
+    small mixed search space tuned with the deterministic laneops metric."""
+    from lanemd.kernels import PatternKind
+    from lanemd.scenario import CubeSource, ScenarioSpec
+    from lanemd.traversals import TraversalKind
+    from lanemd.tuning import ContainerKind
+    box = L.SimulationBox(np.zeros(3), np.full(3, 9.6), (L.BoundaryKind.PERIODIC,) * 3)
+    params = L.LJParams(cutoff=2.5, skin=0.3, dt=0.002)
+    src = CubeSource(origin=np.full(3, 0.6), counts=(8, 8, 8), spacing=1.2,
+                     velocity=np.array([0.1, -0.05, 0.0]), jitter=0.8)
+    return ScenarioSpec(box=box, params=params, sources=[src], iterations=60, seed=7,
+                        vector_width=8, cluster_size=4, rebuild_period=5,
+                        samples_per_config=2, tuning_interval=30, reduction="mean",
+                        metric="laneops",
+                        containers=[ContainerKind.LINKED_CELLS,
+                                    ContainerKind.VERLET_CLUSTER_LISTS],
+                        traversals=[TraversalKind.LC_C01, TraversalKind.LC_C08,
+                                    TraversalKind.VCL],
+                        newton3_options=[False, True],
+                        patterns=[PatternKind.ONE_BY_V, PatternKind.V_BY_ONE])
+
+
+def api(L):
+    """Standalone cluster API (containers.py:216-299) and the scenario
+    driver (driver.py:75-313: build_initial_state, resolve_search_space,
+    run_simulation) on small seeded inputs."""
+    from lanemd.containers import build_cluster_neighbor_lists, build_clusters
+    from lanemd.driver import build_initial_state, resolve_search_space, run_simulation
+    out = {}
+    rng = np.random.default_rng(21)
+    pos = rng.uniform(0, 12.0, (300, 3))
+    out["cl_pos"] = pos
+    for M in (4, 8):
+        buf = make_buffer(L, pos)
+        cl = build_clusters(buf, M)
+        out[f"cl{M}_ids"] = np.stack([c.buffer.id for c in cl])
+        out[f"cl{M}_nreal"] = np.array([c.n_real for c in cl])
+        out[f"cl{M}_amin"] = np.stack([c.aabb_min for c in cl])
+        out[f"cl{M}_amax"] = np.stack([c.aabb_max for c in cl])
+        out[f"cl{M}_pos"] = np.stack([c.buffer.positions() for c in cl])
+        for n3 in (False, True):
+            lists = build_cluster_neighbor_lists(cl, 2.7, n3)
+            flat = [(k, z) for k, zs in enumerate(lists) for z in zs]
+            out[f"cl{M}_pairs_n3{int(n3)}"] = np.array(flat, dtype=np.int64).reshape(-1, 2)
+    spec = api_spec(L)
+    b0 = build_initial_state(spec)
+    out["init_pos"] = b0.positions()
+    out["init_vel"] = np.stack([b0.vel_x, b0.vel_y, b0.vel_z], axis=1)
+    out["space"] = np.array([c.label for c in resolve_search_space(spec)])
+    records, summary = run_simulation(spec)
+    out["rec_label"] = np.array([r.configuration.label for r in records])
+    out["rec_phase"] = np.array([r.phase for r in records])
+    out["rec_num"] = np.array([[r.metric_value, r.lane_slots, r.useful_interactions,
+                                r.blank_lanes, r.pair_interactions] for r in records])
+    out["sum_selections"] = np.array(summary.phase_selections)
+    out["sum_metric_labels"] = np.array(list(summary.per_config_metric.keys()))
+    out["sum_metric_values"] = np.array(list(summary.per_config_metric.values()))
+    out["sum_cells"] = np.array([summary.initial_max_per_cell, summary.final_max_per_cell])
+    out["sum_speed"] = np.array([summary.final_max_speed])
+    np.savez_compressed(os.path.join(HERE, "api.npz"), **out)
+
+
 def main():
     L = _ref()
+    if len(sys.argv) > 1 and sys.argv[1] == "api":
+        api(L)
+        return
     instances(L)
     config1(L)
     functor(L)
     clusters(L)
+    api(L)
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))
