@@ -166,6 +166,7 @@ class Phase:
 
     def __init__(self, cfg, cont, buf, args, torch, N, dec=None, owned_rows=None):
         import paper_2512_03565_b200 as B
+        self.torch = torch
         self.cfg, self.cont, self.buf, self.dec = cfg, cont, buf, dec
         self.owned_rows = owned_rows
         self.energy = args.energy
@@ -185,7 +186,16 @@ class Phase:
         self.ghosts = None
         self.launch()   # builds lazily-built lists outside the timed region
 
+    @property
+    def overlapped(self) -> bool:
+        """Brick runs on segmented Verlet lists hide the ghost exchange
+        behind the interior groups (launch_force_overlapped)."""
+        return (self.dec is not None and self.kind == "vl" and
+                self.cont._vls_for(self.cfg.pattern, self.cfg.newton3) is not None)
+
     def refresh(self):
+        if self.overlapped:
+            return     # part of launch(): refresh, exchange and kernels interleave
         if self.dec is not None:
             b = self.buf
             rows = self.dec.exchange_positions(b.pos_x, b.pos_y, b.pos_z)
@@ -203,6 +213,14 @@ class Phase:
         # vcl: refresh re-derives halo clusters (host-synchronising); not per step
 
     def launch(self):
+        if self.overlapped:
+            b = self.buf
+            if not hasattr(self, "_side"):
+                self._side = self.torch.cuda.Stream()
+            return self.cont.launch_force_overlapped(
+                b, lambda: self.dec.exchange_positions(b.pos_x, b.pos_y, b.pos_z),
+                self.cfg.pattern, self.cfg.newton3, self.energy, self.stats_t, self.ev_t,
+                side_stream=self._side)
         if self.kind == "vl":
             return self.cont.launch_force(self.cfg.pattern, self.cfg.newton3, self.energy,
                                           self.stats_t, self.ev_t)
@@ -213,7 +231,11 @@ class Phase:
 
     @property
     def launches_per_step(self) -> int:
-        # force kernel + refresh gathers (owned pos4; images / ghosts pos4)
+        # force kernel + refresh gathers (owned rows; images / ghost rows);
+        # overlapped bricks: two force launches (interior, boundary), the
+        # ghost pack kernels are counted apart
+        if self.overlapped:
+            return 2 + 2
         if self.kind == "vl":
             return 1 + 2
         if self.kind == "lc":

@@ -58,6 +58,8 @@ extern "C" {
 
 /* kernel flags */
 #define LMD_FLAG_ENERGY 1 /* accumulate potential energy and virial */
+#define LMD_FLAG_DEFER_EV 2 /* lmd_vls_force: leave the energy/virial reduction to
+                               lmd_vls_reduce_ev (launches over group subsets) */
 
 /* KernelStats (kernels.py:67-89) + extensions.  Device resident; kernels
  * accumulate into it, the caller zeroes it (cudaMemsetAsync) beforehand. */
@@ -385,7 +387,10 @@ int lmd_force_vl_staged(int newton3, int flags, const lmd_lj* lj, int64_t n_owne
  * newton3 0 or 2 (as lmd_force_vl); the outer segment runs iff disp == NULL
  * or *disp >= half_delta2 (bit patterns), i.e. once some particle moved at
  * least delta / 2 since the build; ev_scratch holds
- * 2 * lmd_vls_ev_slots(n_groups) doubles.  lmd_vls_refresh: rows[k] =
+ * 2 * lmd_vls_ev_slots(n_groups) doubles.  group_index != NULL launches the
+ * n_index groups it lists (e.g. the interior groups, which stage no image or
+ * ghost rows, while a ghost exchange is in flight); LMD_FLAG_DEFER_EV leaves
+ * the energy/virial reduction over all groups to lmd_vls_reduce_ev.  lmd_vls_refresh: rows[k] =
  * (x, y, z)[perm[k]] (perm NULL: identity) and with disp != NULL the
  * largest squared displacement from build_rows max-reduced into disp[slot]
  * (disp[slot ^ 1] cleared).  lmd_vls_gather_rows: rows_out[k] =
@@ -408,10 +413,11 @@ int lmd_vls_build(const lmd_grid* g, double rin2, double rl2, int64_t n_owned, i
 int64_t lmd_vls_ev_slots(int64_t max_groups);
 int lmd_vls_force(int newton3, int flags, const lmd_lj* lj, int64_t n_owned, int32_t rows,
                   const double* pos_rows, const int32_t* groups, int64_t n_groups,
-                  const int32_t* info, const void* nbr, const int32_t* seg_chunks,
+                  const int32_t* group_index, int64_t n_index, const void* nbr, const int32_t* seg_chunks,
                   const uint8_t* slotmap, int32_t cap_chunks, const uint64_t* disp,
                   double half_delta2, const int32_t* out_perm, double* fx, double* fy,
                   double* fz, double* ev_scratch, lmd_stats* stats, void* stream);
+int lmd_vls_reduce_ev(int64_t n_groups, const double* ev_scratch, lmd_stats* stats, void* stream);
 int lmd_vls_refresh(int64_t n, const int32_t* perm, const double* x, const double* y,
                     const double* z, double* rows, const double* build_rows, uint64_t* disp,
                     int32_t slot, void* stream);

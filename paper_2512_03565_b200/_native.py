@@ -24,6 +24,7 @@ OWNED, HALO, DUMMY = 0, 1, 2
 ONE_BY_V, V_BY_ONE, TWO_BY_HALF, HALF_BY_TWO = 0, 1, 2, 3
 LC_C01, LC_C08, LC_C18, VCL, VL = 0, 1, 2, 3, 4
 FLAG_ENERGY = 1
+FLAG_DEFER_EV = 2
 
 
 class Stats(C.Structure):
@@ -192,8 +193,9 @@ _sig("lmd_vls_build_smem", _SZ, _I32, _I32)
 _sig("lmd_vls_build", _INT, C.POINTER(Grid), _D, _D, _I64, _I32, _VP, _VP, _VP, _VP, _VP, _VP,
      _I64, _I32, _I32, _VP, _VP, _VP, _VP, _VP, _VP, _VP)
 _sig("lmd_vls_ev_slots", _I64, _I64)
-_sig("lmd_vls_force", _INT, _INT, _INT, C.POINTER(LJ), _I64, _I32, _VP, _VP, _I64, _VP, _VP, _VP,
-     _VP, _I32, _VP, _D, _VP, _VP, _VP, _VP, _VP, _VP, _VP)
+_sig("lmd_vls_force", _INT, _INT, _INT, C.POINTER(LJ), _I64, _I32, _VP, _VP, _I64, _VP, _I64,
+     _VP, _VP, _VP, _I32, _VP, _D, _VP, _VP, _VP, _VP, _VP, _VP, _VP)
+_sig("lmd_vls_reduce_ev", _INT, _I64, _VP, _VP, _VP)
 _sig("lmd_vls_refresh", _INT, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _I32, _VP)
 _sig("lmd_vls_gather_rows", _INT, _I64, _VP, _VP, _VP, _VP)
 _sig("lmd_vls_rows_to_legacy", _INT, _I64, _I64, _VP, _VP, _VP, _VP, _VP, _VP)

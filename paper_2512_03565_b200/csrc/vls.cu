@@ -612,7 +612,7 @@ __device__ __forceinline__ double lds_at(const double* sm, unsigned off, int axi
 
 template <int OCC, bool EV, int N3>
 __global__ void __launch_bounds__(kVsG, OCC)
-    vls_force_kernel(const int32_t* __restrict__ groups, const int32_t* __restrict__ info_in,
+    vls_force_kernel(const int32_t* __restrict__ groups, const int32_t* __restrict__ gindex,
                      const double* __restrict__ rows, const int4* __restrict__ nbr,
                      const int32_t* __restrict__ segc, const uint8_t* __restrict__ slotmap,
                      int cap_chunks, const unsigned long long* __restrict__ disp,
@@ -626,7 +626,7 @@ __global__ void __launch_bounds__(kVsG, OCC)
   // one block per group (grid = number of groups); every global load the
   // block needs is independent of the others and issued up front, so the
   // start costs one round trip plus the staging copy
-  const int g = blockIdx.x;
+  const int g = gindex ? __ldg(gindex + blockIdx.x) : (int)blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int t = g * (kVsG / 32) + w;
   const int32_t* rec = groups + (long long)g * kVsRec;
@@ -798,7 +798,7 @@ __global__ void vls_rows_to_legacy_kernel(long long n, long long n_owned,
 
 template <int OCC, bool EV, int N3>
 static int launch_force(dim3 grid, size_t smem, cudaStream_t s, const int32_t* groups,
-                        const int32_t* info, const double* rows, const void* nbr,
+                        const int32_t* gindex, const double* rows, const void* nbr,
                         const int32_t* segc, const uint8_t* slotmap, int cap_chunks,
                         const unsigned long long* disp, unsigned long long hd2, const LJK& k,
                         const int32_t* out_perm, double* fx, double* fy, double* fz, double* ev,
@@ -806,7 +806,7 @@ static int launch_force(dim3 grid, size_t smem, cudaStream_t s, const int32_t* g
   auto kern = vls_force_kernel<OCC, EV, N3>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return set_cuda_error(e);
-  kern<<<grid, kVsG, smem, s>>>(groups, info, rows, (const int4*)nbr, segc, slotmap, cap_chunks,
+  kern<<<grid, kVsG, smem, s>>>(groups, gindex, rows, (const int4*)nbr, segc, slotmap, cap_chunks,
                                disp, hd2, k, out_perm, fx, fy, fz, ev, stats);
   LMD_CHECK_LAUNCH();
   return LMD_OK;
@@ -909,7 +909,7 @@ int64_t lmd_vls_ev_slots(int64_t max_groups) { return max_groups * (kVsG / 32); 
 
 int lmd_vls_force(int newton3, int flags, const lmd_lj* lj, int64_t n_owned, int32_t rows,
                   const double* pos_rows, const int32_t* groups, int64_t n_groups,
-                  const int32_t* info, const void* nbr, const int32_t* seg_chunks,
+                  const int32_t* group_index, int64_t n_index, const void* nbr, const int32_t* seg_chunks,
                   const uint8_t* slotmap, int32_t cap_chunks, const uint64_t* disp,
                   double half_delta2, const int32_t* out_perm, double* fx, double* fy,
                   double* fz, double* ev_scratch, lmd_stats* stats, void* stream) {
@@ -927,14 +927,19 @@ int lmd_vls_force(int newton3, int flags, const lmd_lj* lj, int64_t n_owned, int
     unsigned long long u;
   } hd;
   hd.d = half_delta2;
-  const dim3 grid((unsigned)n_groups);
+  if (group_index && n_index <= 0) {  // an empty subset: nothing to launch
+    if (ev && !(flags & LMD_FLAG_DEFER_EV))
+      return reduce_ev(ev_scratch, lmd_vls_ev_slots(n_groups), stats, (cudaStream_t)stream);
+    return LMD_OK;
+  }
+  const dim3 grid((unsigned)(group_index ? n_index : n_groups));
   const size_t smem = stage_bytes(rows);
   const unsigned long long* dp = (const unsigned long long*)disp;
   // blocks per SM by the staging footprint (228 KB per SM, 1 KB reserved
   // per block): 5 up to ~44 KB, else 4
   const bool five = smem + 1024 + 128 <= 45 * 1024;
 #define LMD_VSF(OCC, EVB, N3B)                                                                  \
-  rc = launch_force<OCC, EVB, N3B>(grid, smem, s, groups, info, pos_rows, nbr, seg_chunks,      \
+  rc = launch_force<OCC, EVB, N3B>(grid, smem, s, groups, group_index, pos_rows, nbr, seg_chunks, \
                                    slotmap, cap_chunks, dp, hd.u, k, out_perm, fx, fy, fz,      \
                                    ev_scratch, stats)
 #define LMD_VSF_O(EVB, N3B)       \
@@ -949,8 +954,14 @@ int lmd_vls_force(int newton3, int flags, const lmd_lj* lj, int64_t n_owned, int
 #undef LMD_VSF_O
 #undef LMD_VSF
   if (rc != LMD_OK) return rc;
-  if (ev) return reduce_ev(ev_scratch, lmd_vls_ev_slots(n_groups), stats, s);
+  if (ev && !(flags & LMD_FLAG_DEFER_EV))
+    return reduce_ev(ev_scratch, lmd_vls_ev_slots(n_groups), stats, s);
   return LMD_OK;
+}
+
+int lmd_vls_reduce_ev(int64_t n_groups, const double* ev_scratch, lmd_stats* stats, void* stream) {
+  if (n_groups <= 0) return LMD_OK;
+  return reduce_ev(ev_scratch, lmd_vls_ev_slots(n_groups), stats, (cudaStream_t)stream);
 }
 
 int lmd_vls_refresh(int64_t n, const int32_t* perm, const double* x, const double* y,

@@ -207,14 +207,15 @@ class VerletListContainer:
                N.ptr(self._soa[2]) if soa else None, N.stream())
         self._pos4_stale = False
 
-    def _load_rows(self, d, ghosts=None, ghost_rows=None, disp: bool = False) -> None:
+    def _load_rows(self, d, ghosts=None, ghost_rows=None, disp: bool = False,
+                   which: str = "all") -> None:
         """Current positions into the (x, y, z) rows of the segmented lists;
         with ``disp`` the owned gather also reduces the largest displacement
         since the build into the next displacement slot (on the device)."""
         n, nh = self.n_owned, self.n_halo
         s = N.stream()
         rows = self._rows
-        if n:
+        if n and which != "ghosts":
             dp = None
             slot = 0
             if disp and not self._external_halo and self._build_rows is not None:
@@ -225,7 +226,7 @@ class VerletListContainer:
                    N.ptr(dp), slot, s)
             if disp:
                 self._disp_slot = slot if dp is not None else -1
-        if not nh:
+        if not nh or which == "owned":
             return
         if ghost_rows is not None:
             N.call("lmd_vls_gather_rows", nh, N.ptr(self._hperm), N.ptr(ghost_rows),
@@ -238,7 +239,8 @@ class VerletListContainer:
                    N.ptr(self._halo_shift), N.ptr(d.pos_x), N.ptr(d.pos_y), N.ptr(d.pos_z),
                    N.ptr(rows[n:]), s)
 
-    def _load_positions(self, d, ghosts=None, ghost_rows=None, fused: bool = False) -> None:
+    def _load_positions(self, d, ghosts=None, ghost_rows=None, fused: bool = False,
+                        which: str = "all") -> None:
         """Current positions into pos4 and the SoA copies, in rebuild-time order:
         owned via the cell permutation; images either moved with their owners
         (shift codes) or, for an external ghost layer, gathered from it.
@@ -253,8 +255,10 @@ class VerletListContainer:
                 self._soa = self._new_soa(n + nh + 1, self._pos4.device)
             sx, sy, sz = self._soa[0], self._soa[1], self._soa[2]
         if self.segmented and self._rows is not None:
-            self._load_rows(d, ghosts, ghost_rows, disp=fused)
+            self._load_rows(d, ghosts, ghost_rows, disp=fused, which=which)
         write4 = not (fused and self.segmented) or self._need_pos4()
+        if which != "all" and write4:
+            raise ConfigurationError("split refreshes serve the segmented lists only")
         if not write4:
             self._pos4_stale = True
             return
@@ -325,6 +329,17 @@ class VerletListContainer:
         self._load_positions(device_soa(owned), fused=True)
 
     refresh_positions = refresh
+
+    def refresh_owned(self, owned) -> None:
+        """First half of an overlapped refresh with an external ghost layer:
+        the owned rows only (the interior groups can run on them)."""
+        self._load_positions(device_soa(owned), None, None, fused=True, which="owned")
+
+    def refresh_ghosts(self, owned, ghost_rows) -> None:
+        """Second half: the exchanged ghost rows (n_halo, 3)."""
+        if ghost_rows is None or len(ghost_rows) != self.n_halo:
+            raise ConfigurationError("refresh needs the same ghost layer as the rebuild")
+        self._load_positions(device_soa(owned), None, ghost_rows, fused=True, which="ghosts")
 
     # ----------------------------------------------------------------- lists
     def _count(self, newton3: bool, pattern=None) -> torch.Tensor:
@@ -722,8 +737,29 @@ class VerletListContainer:
         return perm[i_idx], jid, is_img
 
     # ----------------------------------------------------------------- force
+    def _vls_parts(self, plan):
+        """Device index lists of the interior groups (no image / ghost rows
+        staged: computable before a ghost exchange lands) and the others."""
+        parts = plan.get("parts")
+        if parts is None:
+            ng = plan["ngroups"]
+            rec = plan["groups"][: ng * 64].view(ng, 64)
+            img_rows = rec[:, 26 + 9:26 + 18].sum(dim=1)   # lengths of the 9 image runs
+            ids = torch.arange(ng, dtype=torch.int32, device=rec.device)
+            parts = {"interior": ids[img_rows == 0].contiguous(),
+                     "boundary": ids[img_rows != 0].contiguous()}
+            plan["parts"] = parts
+        return parts
+
+    def reduce_ev(self, pattern, newton3: bool, stats_t, ev_t=None) -> None:
+        """Energy / virial reduction after launches with ``defer_ev``."""
+        vls = self._vls.get(self._key(as_pattern(pattern), newton3))
+        N.call("lmd_vls_reduce_ev", vls["plan"]["ngroups"],
+               N.ptr(ev_t if ev_t is not None else self._vls_ev), N.ptr(stats_t), N.stream())
+
     def launch_force(self, pattern, newton3: bool, energy: bool = False, stats_t=None,
-                     ev_t=None, out=None):
+                     ev_t=None, out=None, part: str | None = None, zero_stats: bool = True,
+                     defer_ev: bool = False):
         """Launch the force kernel without synchronising; returns the device
         stats tensor.  ``out`` (a device ParticleBuffer of the rebuild's
         particles): write the forces straight into out.force_* in its order
@@ -736,8 +772,10 @@ class VerletListContainer:
         dev = self._pos4.device
         if stats_t is None:
             stats_t = N.new_stats(dev)
-        else:
+        elif zero_stats:
             stats_t.zero_()
+        if part is not None and self._vls.get(self._key(pattern, newton3)) is None:
+            raise ConfigurationError("group subsets need the segmented lists")
         if ci > 1:
             if self._pos4_stale:
                 self._regen_pos4()
@@ -763,9 +801,14 @@ class VerletListContainer:
             fx, fy, fz = ((out.force_x, out.force_y, out.force_z) if direct
                           else (self._fx, self._fy, self._fz))
             disp = None if self._disp_slot < 0 else self._disp[self._disp_slot:]
-            N.call("lmd_vls_force", mode, N.FLAG_ENERGY if energy else 0,
+            gidx, nidx = None, 0
+            if part is not None:
+                gidx = self._vls_parts(plan)[part]
+                nidx = int(gidx.numel())
+            flags = (N.FLAG_ENERGY if energy else 0) | (N.FLAG_DEFER_EV if defer_ev else 0)
+            N.call("lmd_vls_force", mode, flags,
                    N.make_lj(self.params), self.n_owned, plan["rows"], N.ptr(self._rows),
-                   N.ptr(plan["groups"]), plan["ngroups"], N.ptr(plan["info"]), N.ptr(vls["nbr"]),
+                   N.ptr(plan["groups"]), plan["ngroups"], N.ptr(gidx), nidx, N.ptr(vls["nbr"]),
                    N.ptr(vls["segc"]), N.ptr(vls["slotmap"]), vls["cap_chunks"], N.ptr(disp),
                    self._vls_half_delta2(), N.ptr(self._perm) if direct else None, N.ptr(fx),
                    N.ptr(fy), N.ptr(fz), N.ptr(ev_t) if energy else None, N.ptr(stats_t),
@@ -808,6 +851,42 @@ class VerletListContainer:
                N.ptr(self._perm) if direct else None, N.ptr(fx), N.ptr(fy), N.ptr(fz),
                N.ptr(ev_t), N.ptr(stats_t), N.stream())
         self._collected_into = out if direct else None
+        return stats_t
+
+    def launch_force_overlapped(self, owned, exchange, pattern, newton3: bool,
+                                energy: bool = False, stats_t=None, ev_t=None, out=None,
+                                side_stream=None):
+        """One force phase with an external ghost layer, the exchange hidden
+        behind the interior groups: owned rows -> interior groups on a side
+        stream, meanwhile ``exchange()`` (the ghost exchange, returning the
+        (n_halo, 3) ghost rows) -> ghost rows -> boundary groups on the
+        current stream -> join.  Same pairs and forces as refresh + launch."""
+        pattern = as_pattern(pattern)
+        self.ensure_lists(pattern, newton3)
+        if self._vls.get(self._key(pattern, newton3)) is None or not self._external_halo:
+            rows = exchange()
+            self.refresh(owned, rows)
+            return self.launch_force(pattern, newton3, energy, stats_t, ev_t, out)
+        dev = self._rows.device
+        if stats_t is None:
+            stats_t = N.new_stats(dev)
+        stats_t.zero_()
+        main = torch.cuda.current_stream(dev)
+        side = side_stream or torch.cuda.Stream(dev)
+        self.refresh_owned(owned)
+        forked = torch.cuda.Event()
+        forked.record(main)
+        side.wait_event(forked)
+        with torch.cuda.stream(side):
+            self.launch_force(pattern, newton3, energy, stats_t, ev_t, out, part="interior",
+                              zero_stats=False, defer_ev=True)
+        rows = exchange()
+        self.refresh_ghosts(owned, rows)
+        self.launch_force(pattern, newton3, energy, stats_t, ev_t, out, part="boundary",
+                          zero_stats=False, defer_ev=True)
+        main.wait_stream(side)
+        if energy:
+            self.reduce_ev(pattern, newton3, stats_t, ev_t)
         return stats_t
 
     def pair_count(self, st, newton3: bool) -> int:

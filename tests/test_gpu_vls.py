@@ -127,3 +127,38 @@ def test_collect_fused_and_overlap(rng):
     cont2.refresh(buf2)
     with pytest.raises(B.ParticleOverlapError):
         cont2.compute_forces("vl", False, PatternKind.V_BY_ONE, 8)
+
+
+def test_overlapped_ghost_exchange_matches_plain_refresh(rng):
+    """launch_force_overlapped (interior groups on a side stream while the
+    ghost rows are produced, boundary groups after) gives bitwise the forces
+    and exactly the statistics of refresh + launch with an external ghost
+    layer (here: the periodic images as the ghost layer)."""
+    pos, span = _state(rng, 12000, 0.8)
+    params = LJParams(cutoff=2.5, skin=0.3)
+    box = SimulationBox.cube(span, periodic=True)
+    buf = ParticleBuffer.from_positions(pos, device="cuda")
+    halo = B.build_halo(buf, box, params.interaction_length)
+    rows = torch.stack([halo.pos_x, halo.pos_y, halo.pos_z], 1).contiguous()
+    inner = SimulationBox.cube(span, periodic=False)   # ghosts supply the images
+    res = []
+    for overlapped in (False, True):
+        cont = B.VerletListContainer(inner, params)
+        cont.rebuild(buf, halo)
+        cont.refresh(buf, rows)
+        cont.ensure_lists("v_by_one", False)
+        parts = cont._vls_parts(cont._vls_for("v_by_one", False)["plan"])
+        assert parts["interior"].numel() > 0 and parts["boundary"].numel() > 0
+        if overlapped:
+            st_t = cont.launch_force_overlapped(buf, lambda: rows, "v_by_one", False, energy=True)
+        else:
+            cont.refresh(buf, rows)
+            st_t = cont.launch_force("v_by_one", False, energy=True)
+        st = B._native.read_stats(st_t)
+        cont.collect_forces(buf)
+        res.append((buf.forces().cpu().numpy(), st.pair_interactions, st.epot, st.virial))
+    assert np.array_equal(res[0][0], res[1][0])
+    assert res[0][1:] == res[1][1:]
+    of, ost = O.force_phase_vl(pos, np.zeros(3), np.full(3, span), [True] * 3, params, False,
+                               "v_by_one", 8)
+    assert res[1][1] == ost.pair_interactions and forces_close(res[1][0], of)
