@@ -227,7 +227,7 @@ class Phase:
         if self.kind == "lc":
             return self.cont.launch_force(self.cfg.pattern, self.energy, self.stats_t, self.ev_t,
                                           self.trav, self.cfg.newton3)
-        return self.cont.launch_force(self.energy, self.stats_t, self.ev_t)
+        return self.cont.launch_force(self.energy, self.stats_t, self.ev_t, pattern=self.cfg.pattern)
 
     @property
     def launches_per_step(self) -> int:

@@ -497,6 +497,19 @@ int lmd_vcl_pairs(int64_t ncl, const int32_t* cluster_key, const double* amin, c
                   double limit, int32_t* count, int32_t* n3count, const int64_t* off,
                   int32_t* list, void* stream);
 int64_t lmd_vcl_ev_slots(int64_t ncl);
+/* K7o: the same force phase with the interaction order as the warp's lane
+ * template (pattern (A, B) at V = 32, kernels.py:250-265): A i-slots x B
+ * j-slots per fill, B >= M packing B / M neighbour clusters per fill, lanes
+ * past the cluster size blank.  M <= 32.  amin / amax (ncl x 3) and hmin /
+ * hmax (halo clusters x 3): the cluster boxes of the last rebuild / refresh;
+ * a lane skips a cluster whose box is farther than cutoff + skin/2 from its
+ * i (members moved less than skin/2 since the boxes were taken). */
+int lmd_force_vcl_order(int64_t ncl, int M, int pattern, int flags, const lmd_lj* lj,
+                        const double* pos4, const int64_t* off, const int32_t* nlist,
+                        const int32_t* list, const int64_t* hoff, const int32_t* hnlist,
+                        const int32_t* hlist, const double* amin, const double* amax,
+                        const double* hmin, const double* hmax, double* fx, double* fy,
+                        double* fz, double* ev_scratch, lmd_stats* stats, void* stream);
 int lmd_force_vcl(int64_t ncl, int M, int flags, const lmd_lj* lj, const double* pos4,
                   const int64_t* off, const int32_t* nlist, const int32_t* list,
                   const int64_t* hoff, const int32_t* hnlist, const int32_t* hlist, double* fx,

@@ -102,6 +102,9 @@ class VerletClusterContainer:
         self.reference_positions = None
         self.steps_since_rebuild = 0
         self.structure_version = 0
+        # interaction orders as warp lane templates (lmd_force_vcl_order);
+        # False: the packed stream kernel for every order
+        self.order_kernels = True
         self._own = None
         self._stats_cache: dict = {}
 
@@ -267,7 +270,10 @@ class VerletClusterContainer:
                     padded=self._owned_pos4[: ncl * M, :3].cpu().numpy())
 
     # ---------------------------------------------------------------- force
-    def launch_force(self, energy: bool = False, stats_t=None, ev_t=None):
+    def launch_force(self, energy: bool = False, stats_t=None, ev_t=None, pattern=None):
+        """Force kernel over the cluster lists.  With ``pattern`` (and
+        ``order_kernels``) the interaction order is the warp's lane template
+        (lmd_force_vcl_order); without, the packed stream kernel."""
         if not self._halo_ready:
             raise ConfigurationError("cluster container has not been refreshed")
         dev = self._pos4.device
@@ -279,6 +285,14 @@ class VerletClusterContainer:
         if ev_t is None:
             ev_t = torch.empty(2 * max(int(N.load().lmd_vcl_ev_slots(ncl)), 1),
                                dtype=torch.float64, device=dev)
+        if pattern is not None and self.order_kernels and self.cluster_size <= 32:
+            N.call("lmd_force_vcl_order", ncl, self.cluster_size, as_pattern(pattern).code,
+                   N.FLAG_ENERGY if energy else 0, N.make_lj(self.params), N.ptr(self._pos4),
+                   N.ptr(self._off), N.ptr(self._count), N.ptr(self._list), N.ptr(self._hoff),
+                   N.ptr(self._hcount), N.ptr(self._hlist), N.ptr(self._amin),
+                   N.ptr(self._amax), N.ptr(self._hmin), N.ptr(self._hmax), N.ptr(self._fx),
+                   N.ptr(self._fy), N.ptr(self._fz), N.ptr(ev_t), N.ptr(stats_t), N.stream())
+            return stats_t
         N.call("lmd_force_vcl", ncl, self.cluster_size, N.FLAG_ENERGY if energy else 0,
                N.make_lj(self.params), N.ptr(self._pos4), N.ptr(self._off), N.ptr(self._count),
                N.ptr(self._list), N.ptr(self._hoff), N.ptr(self._hcount), N.ptr(self._hlist),
@@ -311,7 +325,7 @@ class VerletClusterContainer:
             raise ConfigurationError(f"{traversal} traversal requires linked cells")
         pattern = as_pattern(pattern)
         inv, slots, useful = self.vcl_stats(newton3, pattern, vector_width)
-        st = N.read_stats(self.launch_force(energy))
+        st = N.read_stats(self.launch_force(energy, pattern=pattern))
         if st.overlap:
             raise ParticleOverlapError("zero distance between interacting particles")
         pairs = int(st.pair_interactions)

@@ -366,6 +366,143 @@ __global__ void __launch_bounds__(128)
   }
 }
 
+// Interaction orders as warp mappings.  One warp per owned cluster a; the
+// 32 lanes form the order's A x B template (Pattern<P>: lane -> (i_off,
+// j_off), kernels.py:250-265): a fill evaluates A i-slots of the base
+// cluster against B j-slots.  With B >= M the B j-lanes cover B / M whole
+// units (neighbour clusters) per fill, else a unit takes ceil(M / B) fills;
+// the base cluster takes ceil(M / A) i-blocks and lanes whose i-slot is >= M
+// stay blank -- so, as in the paper, how well the
+// order's A matches the cluster size M decides how many lanes do work.  Each
+// lane first tests its pair of up to 32 fills into a hit mask (exact r2
+// cutoff decision), then evaluates LJ for the set bits; the i force is
+// reduced over the lanes sharing the i-slot (reduce_j<P>).
+template <int P, bool EV>
+__global__ void __launch_bounds__(128)
+    vcl_order_kernel(int ncl, int M, int mshift, const double* __restrict__ pos4,
+                     const long long* __restrict__ off, const int32_t* __restrict__ nlist,
+                     const int32_t* __restrict__ list, const long long* __restrict__ hoff,
+                     const int32_t* __restrict__ hnlist, const int32_t* __restrict__ hlist,
+                     const double* __restrict__ amin, const double* __restrict__ amax,
+                     const double* __restrict__ hmin, const double* __restrict__ hmax,
+                     double skip2, LJK k, double* __restrict__ fx, double* __restrict__ fy,
+                     double* __restrict__ fz, double* __restrict__ ev,
+                     lmd_stats* __restrict__ stats) {
+  constexpr int A = Pattern<P>::A, B = Pattern<P>::B;
+  const int lane = threadIdx.x & 31;
+  const long long warp = (long long)blockIdx.x * 4 + (threadIdx.x >> 5);
+  int pairs = 0, pairs_halo = 0, overlap = 0;
+  double e_acc = 0.0, v_acc = 0.0;
+  const int io = Pattern<P>::ioff(lane), jo = Pattern<P>::joff(lane);
+  // M a power of two (mshift >= 0): shifts; else divisions
+  const bool pack = B >= M;
+  const int upf = pack ? (mshift >= 0 ? B >> mshift : B / M) : 1;   // units per fill
+  const int jf_n = pack ? 1 : (M + B - 1) / B;                       // fills per unit
+  const int ju = pack ? (mshift >= 0 ? jo >> mshift : jo / M) : 0;
+  const int js0 = pack ? (mshift >= 0 ? jo & (M - 1) : jo % M) : jo;
+  if (warp < ncl) {
+    const int a = (int)warp;
+    const long long n_owned_slots = (long long)ncl * M;
+    const int nl = nlist[a];
+    const int nhl = hnlist ? hnlist[a] : 0;
+    const int32_t* lst = list + off[a];
+    const int32_t* hlst = hlist ? hlist + hoff[a] : nullptr;
+    const int units = 1 + nl + nhl;
+    const int groups = (units + upf - 1) / upf;  // unit groups (one fill row each)
+    auto unit_cluster = [&](int u) {
+      return u == 0 ? a : (u <= nl ? __ldg(lst + u - 1) : ncl + __ldg(hlst + u - 1 - nl));
+    };
+    for (int ib = 0; ib < M; ib += A) {
+      const int islot = ib + io;
+      const bool ilive = islot < M;
+      const long long gi = (long long)a * M + (ilive ? islot : 0);
+      const double4 pi = ld_pos4(pos4, gi);
+      const bool iown = ilive && pi.w == (double)LMD_OWNED;
+      double ax = 0.0, ay = 0.0, az = 0.0;
+      // fills in (unit group, j-fill) order; 32 fills per hit mask
+      for (int g0 = 0; g0 < groups; g0 += 32 / jf_n > 0 ? (32 / jf_n) : 1) {
+        const int gstep = 32 / jf_n > 0 ? 32 / jf_n : 1;
+        const int gn = min(gstep, groups - g0);
+        unsigned mask = 0u;
+        for (int gq = 0; gq < gn; ++gq) {
+          const int u = (g0 + gq) * upf + ju;
+          if (!iown || u >= units) continue;
+          const int bc = unit_cluster(u);
+          // with several fills per unit: skip the unit when this lane's i is
+          // farther than rc + skin / 2 from the cluster's box (rebuild-time
+          // AABB; members moved < skin / 2 since) -- no hit possible
+          if (jf_n >= 4) {
+            const double* lo = bc < ncl ? amin + 3LL * bc : hmin + 3LL * (bc - ncl);
+            const double* hi = bc < ncl ? amax + 3LL * bc : hmax + 3LL * (bc - ncl);
+            const double gx = fmax(0.0, fmax(__ldg(lo) - pi.x, pi.x - __ldg(hi)));
+            const double gy = fmax(0.0, fmax(__ldg(lo + 1) - pi.y, pi.y - __ldg(hi + 1)));
+            const double gz = fmax(0.0, fmax(__ldg(lo + 2) - pi.z, pi.z - __ldg(hi + 2)));
+            if (gx * gx + gy * gy + gz * gz > skip2) continue;
+          }
+          for (int jf = 0; jf < jf_n; ++jf) {
+            const int jslot = jf * B + js0;
+            if (jslot >= M) break;
+            const long long gj = (long long)bc * M + jslot;
+            const double4 pj = ld_pos4(pos4, gj);
+            const double r2 = r2_exact(pi.x - pj.x, pi.y - pj.y, pi.z - pj.z);
+            const bool hit = pj.w != (double)LMD_DUMMY && r2 < k.rc2 && gj != gi;
+            mask |= (hit ? 1u : 0u) << (gq * jf_n + jf);
+          }
+        }
+        while (mask) {
+          const int q = __ffs(mask) - 1;
+          mask &= mask - 1u;
+          const int gq = q / jf_n, jf = q - gq * jf_n;
+          const int u = (g0 + gq) * upf + ju, jslot = jf * B + js0;
+          const long long gj = (long long)unit_cluster(u) * M + jslot;
+          const double4 pj = ld_pos4(pos4, gj);
+          const double dx = pi.x - pj.x, dy = pi.y - pj.y, dz = pi.z - pj.z;
+          const double r2 = r2_exact(dx, dy, dz);
+          if (r2 == 0.0) {
+            overlap = 1;
+            continue;
+          }
+          double s6;
+          const double fs = lj_scalar(r2, k, s6);
+          ax = fma(fs, dx, ax);
+          ay = fma(fs, dy, ay);
+          az = fma(fs, dz, az);
+          ++pairs;
+          pairs_halo += gj >= n_owned_slots;
+          if (EV) {
+            e_acc = fma(0.5 * s6, fma(k.eps4, s6, -k.eps4), e_acc);
+            v_acc = fma(0.5 * fs, r2, v_acc);
+          }
+        }
+      }
+      ax = reduce_j<P>(ax);
+      ay = reduce_j<P>(ay);
+      az = reduce_j<P>(az);
+      if (jo == 0 && ilive) {
+        fx[gi] = ax;
+        fy[gi] = ay;
+        fz[gi] = az;
+      }
+    }
+  }
+  const long long pr = warp_sum_ll((long long)pairs);
+  const long long ph = warp_sum_ll((long long)pairs_halo);
+  overlap = __any_sync(0xffffffffu, overlap);
+  if (lane == 0 && warp < ncl) {
+    if (pr) atomicAdd((unsigned long long*)&stats->pair_interactions, (unsigned long long)pr);
+    if (ph) atomicAdd((unsigned long long*)&stats->pairs_owned_halo, (unsigned long long)ph);
+    if (overlap) atomicOr(&stats->overlap, 1);
+  }
+  if (EV) {
+    e_acc = warp_sum(e_acc);
+    v_acc = warp_sum(v_acc);
+    if (lane == 0) {
+      ev[2 * warp] = e_acc;
+      ev[2 * warp + 1] = v_acc;
+    }
+  }
+}
+
 // KernelStats of the vcl schedule (traversals.py:244-266 + executor.py:38-69):
 // per owned cluster a self unit, one unit per list entry (N3: z > k only)
 // and one per halo link; invocations ceil(M/a)*ceil(M/b) each; useful from
@@ -608,6 +745,49 @@ int64_t lmd_vcl_ev_slots(int64_t ncl) { return cdiv(ncl, 4) * 4; }
 /* K7: force over the cluster lists (Newton3 off: every owned cluster against
  * itself, its full list and its halo links).  pos4 = [owned padded | halo
  * padded]; forces written per owned slot. */
+int lmd_force_vcl_order(int64_t ncl, int M, int pattern, int flags, const lmd_lj* lj,
+                        const double* pos4, const int64_t* off, const int32_t* nlist,
+                        const int32_t* list, const int64_t* hoff, const int32_t* hnlist,
+                        const int32_t* hlist, const double* amin, const double* amax,
+                        const double* hmin, const double* hmax, double* fx, double* fy,
+                        double* fz, double* ev_scratch, lmd_stats* stats, void* stream) {
+  if (ncl <= 0) return LMD_OK;
+  if (M < 2 || M > 32 || pattern < 0 || pattern > 3 || !amin || !amax) return LMD_ERR_CONFIG;
+  const LJK k = make_ljk(lj);
+  int mshift = -1;
+  for (int b = 0; b < 6; ++b)
+    if ((1 << b) == M) mshift = b;
+  // skip a unit when the i particle is farther than rc + skin/2 from its box
+  const double skip_r = lj->cutoff + 0.5 * lj->skin;
+  const double skip2 = skip_r * skip_r * (1.0 + 1e-12);
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool ev = (flags & LMD_FLAG_ENERGY) != 0;
+  const unsigned blocks = (unsigned)cdiv(ncl, 4);
+#define LMD_VCLO(PV)                                                                          \
+  do {                                                                                        \
+    if (ev)                                                                                   \
+      vcl_order_kernel<PV, true><<<blocks, 128, 0, s>>>(                                      \
+          (int)ncl, M, mshift, pos4, (const long long*)off, nlist, list,                      \
+          (const long long*)hoff, hnlist, hlist, amin, amax, hmin, hmax, skip2, k, fx, fy, fz, \
+          ev_scratch, stats);                                                                 \
+    else                                                                                      \
+      vcl_order_kernel<PV, false><<<blocks, 128, 0, s>>>(                                     \
+          (int)ncl, M, mshift, pos4, (const long long*)off, nlist, list,                      \
+          (const long long*)hoff, hnlist, hlist, amin, amax, hmin, hmax, skip2, k, fx, fy, fz, \
+          ev_scratch, stats);                                                                 \
+  } while (0)
+  switch (pattern) {
+    case LMD_ONE_BY_V: LMD_VCLO(LMD_ONE_BY_V); break;
+    case LMD_V_BY_ONE: LMD_VCLO(LMD_V_BY_ONE); break;
+    case LMD_TWO_BY_HALF: LMD_VCLO(LMD_TWO_BY_HALF); break;
+    default: LMD_VCLO(LMD_HALF_BY_TWO); break;
+  }
+#undef LMD_VCLO
+  LMD_CHECK_LAUNCH();
+  if (ev) return reduce_ev(ev_scratch, lmd_vcl_ev_slots(ncl), stats, s);
+  return LMD_OK;
+}
+
 int lmd_force_vcl(int64_t ncl, int M, int flags, const lmd_lj* lj, const double* pos4,
                   const int64_t* off, const int32_t* nlist, const int32_t* list,
                   const int64_t* hoff, const int32_t* hnlist, const int32_t* hlist, double* fx,

@@ -92,7 +92,7 @@ def _launch(cont, cfg: Configuration, V: int, energy: bool, owned=None):
         return cont.launch_force(cfg.pattern, energy, traversal=code, newton3=cfg.newton3)
     if kind is ContainerKind.VERLET_LISTS:   # forces written in the caller's order
         return cont.launch_force(cfg.pattern, cfg.newton3, energy, out=owned)
-    return cont.launch_force(energy)
+    return cont.launch_force(energy, pattern=cfg.pattern)
 
 
 def _geometry(cont, cfg: Configuration, V: int):

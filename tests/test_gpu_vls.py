@@ -134,7 +134,7 @@ def test_overlapped_ghost_exchange_matches_plain_refresh(rng):
     ghost rows are produced, boundary groups after) gives bitwise the forces
     and exactly the statistics of refresh + launch with an external ghost
     layer (here: the periodic images as the ghost layer)."""
-    pos, span = _state(rng, 12000, 0.8)
+    pos, span = _state(rng, 60000, 0.8)    # 15 cells per line: interior groups exist
     params = LJParams(cutoff=2.5, skin=0.3)
     box = SimulationBox.cube(span, periodic=True)
     buf = ParticleBuffer.from_positions(pos, device="cuda")
