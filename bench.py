@@ -281,13 +281,14 @@ def build_phase(cfg, w, args, torch, N, dec=None):
     return phase, cont, buf, box, params, geo
 
 
-def committed_traffic(label):
-    """DRAM bytes per launch of this configuration's force kernel, from the
-    committed ncu capture (profiles/traffic.json), else None."""
+def committed_traffic(label, workload):
+    """DRAM bytes per launch of this configuration's force kernel on this
+    workload, from the committed ncu capture (profiles/traffic.json), else
+    None."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
-            return json.load(fh).get(label, {}).get("bytes")
-    except (OSError, ValueError):
+            return json.load(fh).get(workload, {}).get(label, {}).get("bytes")
+    except (OSError, ValueError, AttributeError):
         return None
 
 
@@ -602,7 +603,7 @@ def run_b200(args):
                          "flops_per_pair": FLOPS_PER_PAIR[cfg.newton3],
                          "kernel": "force kernel alone (CUDA events on its stream)",
                          "peak_source": "measured in this run: lmd_dfma_burn (DFMA, 2 flop)",
-                         "traffic": committed_traffic(cfg.label),
+                         "traffic": committed_traffic(cfg.label, w.name),
                          "algorithmic_bytes": algorithmic_bytes(cfg, cont, stats, n_local),
                          "hbm_gbs_achieved": algorithmic_bytes(cfg, cont, stats, n_local)
                          / avg_launch / 1e9},

@@ -61,7 +61,7 @@ constexpr int kVsG = 128;      // particles per group (4 warps)
 constexpr int kVsRec = 64;     // int32 per group record
 constexpr int kVsRuns = 18;    // (view, dz, dy)
 constexpr int kVsSelfRun = 4;  // view 0, dz = 0, dy = 0
-constexpr int kVsMaxRows = 2720;  // 24 * row + 16 < 65536: byte offsets fit 16 bits
+constexpr int kVsMaxRows = 2704;  // 24 * (row + 15) < 65536: byte offsets (dummies incl.) fit 16 bits
 // staged-row budget of a group: groups shrink (in steps of 32 particles)
 // until they stage at most this many rows, so 5 blocks (44 KB each) fit an SM
 constexpr int kVsBudget = 1840;
@@ -202,8 +202,7 @@ __global__ void vls_groups_kernel(long long nrows, int t0, int t1, int d0, int d
 }
 
 // warp 0 copies the group's runs into shared memory (one bulk copy per run;
-// lane 0 arms the barrier with the byte count first); the dummy row after
-// the last run is written by thread 32
+// lane 0 arms the barrier with the byte count first)
 __device__ __forceinline__ void vls_stage(const int32_t* __restrict__ rec,
                                           const double* __restrict__ rows, double* sm,
                                           unsigned long long* bar) {
@@ -217,11 +216,19 @@ __device__ __forceinline__ void vls_stage(const int32_t* __restrict__ rec,
         bulk_g2s(sm + 3 * rec[kVsBase + lane], rows + 3LL * rec[kVsStart + lane],
                  (unsigned)len * 24u, bar);
     }
-  } else if (threadIdx.x == 32) {
-    const int S = rec[kVsS];
-    sm[3 * S] = 1.0e30;
-    sm[3 * S + 1] = 1.0e30;
-    sm[3 * S + 2] = 1.0e30;
+  }
+}
+
+// 16 dummy rows far away, one per shared-memory bank pair, from row D = S
+// rounded up to 16 (row D + t sits in bank pair 3 t & 15); written before the
+// block barrier that precedes the staging
+__device__ __forceinline__ void vls_dummies(const int32_t* __restrict__ rec, double* sm) {
+  if (threadIdx.x >= 32 && threadIdx.x < 48) {
+    const int D = (rec[kVsS] + 15) & ~15;
+    const int r = D + (int)threadIdx.x - 32;
+    sm[3 * r] = 1.0e30;
+    sm[3 * r + 1] = 1.0e30;
+    sm[3 * r + 2] = 1.0e30;
   }
 }
 
@@ -253,19 +260,15 @@ __global__ void __launch_bounds__(kVsG, 4)
   uint8_t* cnt = reinterpret_cast<uint8_t*>(sm_b) + area_bytes;  // [32 buckets][128]
   uint8_t* pos = cnt + 32 * kVsG;                                 // [32 buckets][128]
   __shared__ unsigned long long bar;
-  __shared__ int n_in_sm[kVsG];
-  __shared__ int tile_len[2][kVsG / 32];
+  __shared__ int n_in_sm[kVsG], n_out_sm[kVsG], slot_sm[kVsG];
   const int g = blockIdx.x;
   if (g >= info_in[2]) return;
   const int32_t* rec = groups + (long long)g * kVsRec;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   if (tid == 0) mbar_init(&bar, 1);
-  if (tid < kVsG / 32) {
-    tile_len[0][tid] = 0;
-    tile_len[1][tid] = 0;
-  }
 #pragma unroll
   for (int b = 0; b < 32; ++b) cnt[b * kVsG + tid] = 0;
+  vls_dummies(rec, xs);
   __syncthreads();
   vls_stage(rec, rows, xs, &bar);
   const int cnt_p = rec[kVsCnt], p0 = rec[kVsP0];
@@ -460,6 +463,7 @@ __global__ void __launch_bounds__(kVsG, 4)
   //    thread order); inactive threads rank last
   const int key = active ? n_in : -1;
   n_in_sm[tid] = key;
+  n_out_sm[tid] = n_out;
   __syncthreads();
   int rank = 0;
 #pragma unroll 8
@@ -467,23 +471,33 @@ __global__ void __launch_bounds__(kVsG, 4)
     const int ko = n_in_sm[o];
     rank += (ko > key || (ko == key && o < tid)) ? 1 : 0;
   }
-  const int w2 = rank >> 5, l2 = rank & 31;
+  slot_sm[rank] = active ? tid : 0xff;
   slotmap[(long long)g * kVsG + rank] = active ? (uint8_t)tid : (uint8_t)0xff;
-  atomicMax(&tile_len[0][w2], n_in);
-  atomicMax(&tile_len[1][w2], n_out);
   __syncthreads();  // every lane has read its hits: the list area is free
-  const int t = g * (kVsG / 32) + w2;
-  const unsigned dummy = (unsigned)rec[kVsS] * 24u;
+  // 4. emission, one warp per tile (its lanes = the particles dealt to it):
+  //    lane-local Latin-square bank order -- at step k the lane takes an
+  //    entry from bucket (bank pair) (lane + k) & 15 if it has one, else the
+  //    next non-empty bucket in rotation; past its list it takes the dummy
+  //    row of bank (lane + k) & 15 (16 dummies, one per bank pair, from row
+  //    D = S rounded up to 16), so padding never conflicts within a
+  //    half-warp.  (A warp-cooperative matching of lanes to free banks per
+  //    step cut the conflicts by a quarter but not the force time: measured,
+  //    DESIGN.md.)
+  const int src = slot_sm[tid];
+  const bool live = src != 0xff;
+  const int t = g * (kVsG / 32) + w;
+  const unsigned dbase = (unsigned)((S + 15) & ~15);
+  const uint16_t* hits_of = sorted + (live ? src : 0) * cap_ent;
   int chunk = 0;
 #pragma unroll 1
   for (int seg = 0; seg < 2; ++seg) {
-    const int ns = seg ? n_out : n_in;
-    const int C = (tile_len[seg][w2] + 7) >> 3;
+    const int ns = live ? (seg ? n_out_sm[src] : n_in_sm[src]) : 0;
+    const int C = (__reduce_max_sync(0xffffffffu, ns) + 7) >> 3;
     unsigned m = 0;
-    if (ok) {
+    if (ok && live) {
 #pragma unroll
       for (int b = 0; b < 16; ++b)
-        m |= (cnt[(seg * 16 + b) * kVsG + tid] != 0 ? 1u : 0u) << b;
+        m |= (cnt[(seg * 16 + b) * kVsG + src] != 0 ? 1u : 0u) << b;
     }
 #pragma unroll 1
     for (int c = 0; c < C; ++c) {
@@ -491,27 +505,27 @@ __global__ void __launch_bounds__(kVsG, 4)
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         const int k = c * 8 + e;
-        unsigned val = dummy;
+        const int d = (lane + k) & 15;
+        unsigned val = (dbase + (unsigned)((11 * d) & 15)) * 24u;   // dummy of bank d
         if (k < ns && m) {
-          const int d = (l2 + k) & 15;
           const unsigned rot = ((m >> d) | (m << (16 - d))) & 0xffffu;
           const int b = (d + __ffs(rot) - 1) & 15;
-          const int bi = (seg * 16 + b) * kVsG + tid;
+          const int bi = (seg * 16 + b) * kVsG + src;
           const int left = cnt[bi];
-          val = (unsigned)mine[pos[bi] - left] * 24u;
+          val = (unsigned)hits_of[pos[bi] - left] * 24u;
           cnt[bi] = (uint8_t)(left - 1);
           if (left == 1) m &= ~(1u << b);
         }
         wv[e >> 1] |= val << (16 * (e & 1));
       }
       if (chunk + c < cap_chunks)
-        nbr[((long long)t * cap_chunks + chunk + c) * 32 + l2] =
+        nbr[((long long)t * cap_chunks + chunk + c) * 32 + lane] =
             make_int4((int)wv[0], (int)wv[1], (int)wv[2], (int)wv[3]);
     }
-    if (l2 == 0) segc[2 * t + seg] = C;
+    if (lane == 0) segc[2 * t + seg] = C;
     chunk += C;
   }
-  if (l2 == 0 && chunk > 0) atomicMax(info + 3, chunk);
+  if (lane == 0 && chunk > 0) atomicMax(info + 3, chunk);
 }
 
 // ------------------------------------------------------------------ force
@@ -639,6 +653,7 @@ __global__ void __launch_bounds__(kVsG, OCC)
   // inner segment alone while every particle moved less than delta / 2
   const bool outer = disp == nullptr || *disp >= half_delta2_bits;
   if (tid == 0) mbar_init(&bar, 1);
+  vls_dummies(rec, xs);
   __syncthreads();
   vls_stage(rec, rows, xs, &bar);
   const int nch = c_in + (outer ? c_out : 0);
@@ -813,7 +828,7 @@ static int launch_force(dim3 grid, size_t smem, cudaStream_t s, const int32_t* g
 }
 
 static inline size_t stage_bytes(int32_t rows) {
-  return ((size_t)(rows + 2) * 24 + 127) / 128 * 128;
+  return ((size_t)(rows + 16) * 24 + 127) / 128 * 128;   // + the 16 dummy rows
 }
 
 }  // namespace lmd
@@ -871,7 +886,7 @@ int lmd_vls_plan(const lmd_grid* g, int64_t n_owned, const int32_t* o_start,
 
 static inline int build_area(int32_t rows, int32_t cap_entries) {
   // staged rows (step 1), then the lanes' sorted hits (steps 2-3)
-  const size_t a = std::max((size_t)(rows + 2) * 24, (size_t)cap_entries * kVsG * 2);
+  const size_t a = std::max((size_t)(rows + 16) * 24, (size_t)cap_entries * kVsG * 2);
   return (int)((a + 127) / 128 * 128);
 }
 
