@@ -633,7 +633,7 @@ __global__ void __launch_bounds__(kVsG, OCC)
                      unsigned long long half_delta2_bits, LJK k,
                      const int32_t* __restrict__ out_perm, double* __restrict__ fx,
                      double* __restrict__ fy, double* __restrict__ fz, double* __restrict__ ev,
-                     lmd_stats* __restrict__ stats) {
+                     lmd_stats* __restrict__ stats, int n_groups, int pf_dist) {
   extern __shared__ __align__(128) double sm_f[];
   double* xs = sm_f;
   __shared__ unsigned long long bar;
@@ -656,6 +656,18 @@ __global__ void __launch_bounds__(kVsG, OCC)
   vls_dummies(rec, xs);
   __syncthreads();
   vls_stage(rec, rows, xs, &bar);
+  // warm the L2 with the rows of the group that starts about one wave of
+  // blocks later, so its staging copies hit the L2 rather than HBM
+  if (!gindex && pf_dist > 0 && tid >= 32 && tid < 32 + kVsRuns &&
+      (int)blockIdx.x + pf_dist < n_groups) {
+    const int32_t* nrec = groups + (long long)(blockIdx.x + pf_dist) * kVsRec;
+    const int q = tid - 32, len = __ldg(nrec + kVsLen + q);
+    if (len)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                       rows + 3LL * __ldg(nrec + kVsStart + q)),
+                   "r"((unsigned)len * 24u)
+                   : "memory");
+  }
   const int nch = c_in + (outer ? c_out : 0);
   if (lane == 0 && nch > 2)
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(chunks + 64),
@@ -821,8 +833,12 @@ static int launch_force(dim3 grid, size_t smem, cudaStream_t s, const int32_t* g
   auto kern = vls_force_kernel<OCC, EV, N3>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return set_cuda_error(e);
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   kern<<<grid, kVsG, smem, s>>>(groups, gindex, rows, (const int4*)nbr, segc, slotmap, cap_chunks,
-                               disp, hd2, k, out_perm, fx, fy, fz, ev, stats);
+                               disp, hd2, k, out_perm, fx, fy, fz, ev, stats, (int)grid.x,
+                               OCC * sms);
   LMD_CHECK_LAUNCH();
   return LMD_OK;
 }
