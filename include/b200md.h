@@ -246,27 +246,12 @@ int lmd_scatter_forces(int64_t n, const int32_t* perm, const double* fx, const d
  * by cell | images sorted by cell], with SEPARATE owned and image cell tables
  * (o_*, h_*; image starts include the n_owned base).  Candidates: owned
  * particles and images of the 27 cells; listed iff r2 < rl2 with the
- * reference's exact r2.  newton3 = 1 builds half lists (owned j > i).
- * 1) lmd_vl_count -> count[i];  2) lmd_vl_layout -> per-tile kmax / offsets
- * for `pattern` (tiles of A = distinct i per fill; kmax = fill steps x B,
- * steps padded to whole 4-step chunks); 3) lmd_vl_fill -> nbr (`total` =
- * tile_off[last] + tile_len[last] entries, lane-chunked as documented in
- * csrc/vl.cu, padded with `sentinel`, the index of a far-away record). */
-int lmd_vl_count(const lmd_grid* g, double rl2, int newton3, int64_t n_owned, const double* pos4,
-                 const int32_t* o_start, const int32_t* o_count, const int32_t* h_start,
-                 const int32_t* h_count, int32_t* count, void* stream);
+ * reference's exact r2.  newton3 = 1 builds half lists (owned j > i). */
 int64_t lmd_vl_num_tiles(int64_t n_owned, int pattern);
-size_t lmd_vl_scan_temp_bytes(int64_t ntiles);
-int lmd_vl_layout(int64_t n_owned, int pattern, const int32_t* count, int64_t* tile_len,
-                  int64_t* tile_off, int32_t* kmax, void* temp, size_t temp_bytes,
-                  void* stream);
-int lmd_vl_fill(const lmd_grid* g, double rl2, int newton3, int pattern, int64_t n_owned,
-                int32_t sentinel, const double* pos4, const int32_t* o_start,
-                const int32_t* o_count, const int32_t* h_start, const int32_t* h_count,
-                const int64_t* tile_off, int64_t total, int32_t* nbr, void* stream);
-/* Single-pass build (what the containers use): same lists and lane layout
- * as count/layout/fill, but tile t starts at tile_off[t] = t * cap_steps * 32
- * (cap_steps a multiple of 4), so no count pass, scan or prefill is needed;
+/* Single-pass build: lists laid out per interaction order (tiles of A =
+ * distinct i per fill, lane-chunked as documented in csrc/vl.cu, padded
+ * with `sentinel`, the index of a far-away record); tile t starts at
+ * tile_off[t] = t * cap_steps * 32 (cap_steps a multiple of 4);
  * nbr holds ceil(n_owned / A) * cap_steps * 32 entries.  Writes count[i],
  * tile_off, kmax and *max_count = the longest list; if *max_count >
  * cap_steps * B the lists were truncated and the caller must rebuild with a
@@ -277,14 +262,6 @@ int lmd_vl_build(const lmd_grid* g, double rl2, int newton3, int pattern, int64_
                  const int32_t* o_count, const int32_t* h_start, const int32_t* h_count,
                  int32_t cap_steps, int32_t* count, int32_t* count_half, int64_t* tile_off,
                  int32_t* kmax, int32_t* max_count, int32_t* nbr, void* stream);
-/* Optional pass after lmd_vl_build / lmd_vl_ci_build: permutes every lane's
- * own slot sequence of every tile so that the lanes of a fill gather from
- * shared 128-B lines (window of `window` = 8, 16 or 32 entries per lane,
- * see csrc/vl.cu vl_align_kernel).  Same entries per lane, so forces, pair
- * counts and statistics are unchanged up to summation order.  n_units = owned
- * particles (or clusters for the i-cluster lists). */
-int lmd_vl_align(int pattern, int64_t n_units, int window, const int64_t* tile_off,
-                 const int32_t* kmax, int32_t* nbr, void* stream);
 /* Optional pass after lmd_vl_build / lmd_vl_build_staged: permutes every
  * lane's own slot sequence so that the lanes of each half-warp gather from
  * distinct 8-byte bank pairs (index & 15) step by step -- the cost unit of a
@@ -316,7 +293,7 @@ int lmd_vl_bank_schedule(int pattern, int64_t n_units, int32_t sentinel, int rou
  * V_BY_ONE writing each entry as the local row of its group's copy; pads
  * are -1.  index_bits = 16 (every group staged, smax[1] == 0): entries are
  * uint16 local rows, 8 steps per 128-bit chunk (cap_steps % 8 == 0, tile
- * offsets in uint16 units, pads 0xffff, no FP32 prefilter); 32: int32, 4
+ * offsets in uint16 units, pads 0xffff); 32: int32, 4
  * steps per chunk.  lmd_vl_staged_capacity(group_size) = the largest S a group
  * stages (pass it as `capacity`).  lmd_force_vl_staged: newton3 0 or 2 as
  * lmd_force_vl; soa = (3, stride) rows (stride % 16 == 0, 128-B aligned)
@@ -330,33 +307,12 @@ int lmd_vl_groups(const lmd_grid* g, int64_t n_owned, int32_t group_size, int32_
 int lmd_vl_build_staged(const lmd_grid* g, double rl2, int newton3, int64_t n_owned,
                         const double* pos4, const int32_t* o_start, const int32_t* o_count,
                         const int32_t* h_start, const int32_t* h_count, int32_t group_size,
-                        const int32_t* groups, int32_t index_bits, const float* pf,
-                        float rl2f_lo, float rl2f_hi, int32_t cap_steps, int32_t* count,
-                        int32_t* count_half, int64_t* tile_off, int32_t* kmax,
+                        const int32_t* groups, int32_t index_bits, int32_t cap_steps,
+                        int32_t* count, int32_t* count_half, int64_t* tile_off, int32_t* kmax,
                         int32_t* max_count, int32_t* nbr, void* stream);
-/* FP32 rows for lmd_vl_build_staged (pf != NULL): float4 (x - cx, y - cy,
- * z - cz, 0) of every pos4 row.  The build decides a candidate in FP32 when
- * its FP32 r2 is below rl2f_lo (inside) or at least rl2f_hi (outside) and
- * re-tests the rest exactly (FP64, the reference's r2); the caller sets
- * rl2f_lo / rl2f_hi to rl^2 minus / plus a margin above the FP32 error bound
- * of r2 for the coordinate range, so the pair set is the exact one. */
-int lmd_vl_prefilter_rows(int64_t rows, const double* pos4, const double* center, float* pf,
-                          void* stream);
-/* Staged lists, per group of group_size particles (<= 256): deal the
- * group's particles to lanes by descending list length (count[]), copy each
- * particle's entries from its build slot to the new slot (same capacity,
- * fresh tile offsets / step counts) and, with bank != 0, in the lane-local
- * bank order (max_steps as for lmd_vl_bank_schedule).  slot_particle[t*32+l]
- * = particle at tile t, lane l (-1: none); pass it to lmd_force_vl_staged. */
-int lmd_vl_reorder(int64_t n_owned, int32_t group_size, int32_t index_bits, int32_t cap_steps,
-                   int32_t max_steps, int bank, int32_t sentinel, const int32_t* count,
-                   const int64_t* tile_off, const int32_t* kmax, const int32_t* nbr,
-                   int32_t* slot_particle, int64_t* tile_off_out, int32_t* kmax_out,
-                   int32_t* nbr_out, void* stream);
 int lmd_force_vl_staged(int newton3, int flags, const lmd_lj* lj, int64_t n_owned,
                         const double* pos4, const double* soa, int64_t stride, int32_t sentinel,
                         int32_t group_size, const int32_t* groups, int32_t index_bits,
-                        const int32_t* slot_particle,
                         const int64_t* tile_off, const int32_t* kmax, const int32_t* nbr,
                         const int32_t* out_perm, double* fx, double* fy, double* fz,
                         double* ev_scratch, lmd_stats* stats, void* stream);
@@ -425,26 +381,6 @@ int lmd_vls_gather_rows(int64_t n, const int32_t* perm, const double* rows_in, d
                         void* stream);
 int lmd_vls_rows_to_legacy(int64_t n, int64_t n_owned, const double* rows, double* pos4,
                            double* sx, double* sy, double* sz, void* stream);
-/* i-cluster lists (csrc/vl_ci.cu), full lists only: each cell's owned
- * particles are cut into clusters of up to ci (2 or 4) consecutive backing
- * slots, cluster c = [cl_first[c], cl_first[c] + cl_len[c]); its list is the
- * union of its members' lists.  Layout and capacity as lmd_vl_build with
- * clusters in place of particles; count[i] = each member's own list length.
- * The force entry tests every entry against all members: same pairs, forces
- * and counts as lmd_force_vl with newton3 = 0; ev_scratch holds
- * 2 * lmd_vl_ci_ev_slots(n_clusters, pattern) doubles. */
-int lmd_vl_ci_build(const lmd_grid* g, double rl2, int pattern, int ci, int64_t n_clusters,
-                    const int32_t* cl_first, const int32_t* cl_len, int32_t sentinel,
-                    const double* pos4, const int32_t* o_start, const int32_t* o_count,
-                    const int32_t* h_start, const int32_t* h_count, int32_t cap_steps,
-                    int32_t* count, int64_t* tile_off, int32_t* kmax, int32_t* max_count,
-                    int32_t* nbr, void* stream);
-int64_t lmd_vl_ci_ev_slots(int64_t n_clusters, int pattern);
-int lmd_force_vl_ci(int pattern, int ci, int flags, const lmd_lj* lj, int64_t n_owned,
-                    int64_t n_clusters, const int32_t* cl_first, const int32_t* cl_len,
-                    const double* pos4, const int64_t* tile_off, const int32_t* kmax,
-                    const int32_t* nbr, double* fx, double* fy, double* fz, double* ev_scratch,
-                    lmd_stats* stats, void* stream);
 /* Force over the lists: one warp per i-tile, lanes by `pattern`; positions
  * are pos4 over the combined backing plus one sentinel record (256-bit
  * gathers), or, if soa != NULL, SoA copies x = soa[0..ntot), y, z of the

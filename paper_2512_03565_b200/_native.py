@@ -156,12 +156,7 @@ _sig("lmd_halo_refresh_soa", _INT, C.POINTER(Box), _I64, _VP, _VP, _VP, _VP, _VP
      _VP, _VP)
 _sig("lmd_halo_refresh_rows", _INT, C.POINTER(Box), _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP)
 _sig("lmd_gather_soa", _INT, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP)
-_sig("lmd_vl_count", _INT, C.POINTER(Grid), _D, _INT, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP)
 _sig("lmd_vl_num_tiles", _I64, _I64, _INT)
-_sig("lmd_vl_scan_temp_bytes", _SZ, _I64)
-_sig("lmd_vl_layout", _INT, _I64, _INT, _VP, _VP, _VP, _VP, _VP, _SZ, _VP)
-_sig("lmd_vl_fill", _INT, C.POINTER(Grid), _D, _INT, _INT, _I64, _I32, _VP, _VP, _VP, _VP, _VP,
-     _VP, _I64, _VP, _VP)
 _sig("lmd_vl_build", _INT, C.POINTER(Grid), _D, _INT, _INT, _I64, _I32, _VP, _VP, _VP, _VP, _VP,
      _I32, _VP, _VP, _VP, _VP, _VP, _VP, _VP)
 _sig("lmd_vl_ev_slots", _I64, _I64, _INT)
@@ -172,18 +167,14 @@ _sig("lmd_max_displacement2", _INT, _I64, _VP, _VP, _VP, _VP, _VP, _VP)
 _sig("lmd_lc_tpi_ev_slots", _I64, _I64, _INT)
 _sig("lmd_force_lc_particles", _INT, C.POINTER(Grid), C.POINTER(LJ), _INT, _INT, _VP, _I64, _VP,
      _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP)
-_sig("lmd_vl_align", _INT, _INT, _I64, _INT, _VP, _VP, _VP, _VP)
 _sig("lmd_vl_bank_smem_per_warp", C.c_size_t, _I32)
 _sig("lmd_vl_groups", _INT, C.POINTER(Grid), _I64, _I32, _I32, _VP, _VP, _VP, _VP, _VP, _VP, _VP,
      _VP)
 _sig("lmd_vl_build_staged", _INT, C.POINTER(Grid), _D, _INT, _I64, _VP, _VP, _VP, _VP, _VP, _I32,
-     _VP, _I32, _VP, C.c_float, C.c_float, _I32, _VP, _VP, _VP, _VP, _VP, _VP, _VP)
-_sig("lmd_vl_prefilter_rows", _INT, _I64, _VP, _VP, _VP, _VP)
+     _VP, _I32, _I32, _VP, _VP, _VP, _VP, _VP, _VP, _VP)
 _sig("lmd_vl_staged_capacity", _I32, _I32)
 _sig("lmd_force_vl_staged", _INT, _INT, _INT, C.POINTER(LJ), _I64, _VP, _VP, _I64, _I32, _I32, _VP,
-     _I32, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP)
-_sig("lmd_vl_reorder", _INT, _I64, _I32, _I32, _I32, _I32, _INT, _I32, _VP, _VP, _VP, _VP, _VP, _VP,
-     _VP, _VP, _VP)
+     _I32, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP)
 _sig("lmd_vl_bank_schedule", _INT, _INT, _I64, _I32, _INT, _I32, _I32, _I32, _VP, _VP, _VP, _VP)
 _sig("lmd_vls_max_groups", _I64, C.POINTER(Grid), _I64)
 _sig("lmd_vls_rows_for", _I32, _I32)
@@ -199,11 +190,6 @@ _sig("lmd_vls_reduce_ev", _INT, _I64, _VP, _VP, _VP)
 _sig("lmd_vls_refresh", _INT, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _I32, _VP)
 _sig("lmd_vls_gather_rows", _INT, _I64, _VP, _VP, _VP, _VP)
 _sig("lmd_vls_rows_to_legacy", _INT, _I64, _I64, _VP, _VP, _VP, _VP, _VP, _VP)
-_sig("lmd_vl_ci_build", _INT, C.POINTER(Grid), _D, _INT, _INT, _I64, _VP, _VP, _I32, _VP, _VP,
-     _VP, _VP, _VP, _I32, _VP, _VP, _VP, _VP, _VP, _VP)
-_sig("lmd_vl_ci_ev_slots", _I64, _I64, _INT)
-_sig("lmd_force_vl_ci", _INT, _INT, _INT, _INT, C.POINTER(LJ), _I64, _I64, _VP, _VP, _VP, _VP,
-     _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP)
 _sig("lmd_force_vl", _INT, _INT, _INT, _INT, C.POINTER(LJ), _I64, _VP, _VP, _I64, _VP, _VP,
      _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP)
 _sig("lmd_vl_stats", _INT, _I64, _INT, _INT, _INT, _VP, _VP, _VP)

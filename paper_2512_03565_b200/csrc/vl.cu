@@ -27,87 +27,6 @@ struct Tile {
   static constexpr int A = Pattern<P>::A, B = Pattern<P>::B;
 };
 
-// visits every candidate j (index into the combined backing) of owned i
-template <typename F>
-__device__ __forceinline__ void for_candidates(int i, const double4& pi, int newton3, long long t0,
-                                               long long t1, long long lin,
-                                               const int32_t* __restrict__ os,
-                                               const int32_t* __restrict__ oc,
-                                               const int32_t* __restrict__ hs,
-                                               const int32_t* __restrict__ hc,
-                                               const double* __restrict__ pos4, double rl2,
-                                               F&& visit) {
-  for (int view = 0; view < 2; ++view) {
-    const int32_t* vs = view ? hs : os;
-    const int32_t* vc = view ? hc : oc;
-    for (int dz = -1; dz <= 1; ++dz)
-      for (int dy = -1; dy <= 1; ++dy)
-        for (int dx = -1; dx <= 1; ++dx) {
-          const long long nl = lin + dx + t0 * (dy + t1 * dz);
-          const int s = vs[nl], c = vc[nl];
-          for (int j = s; j < s + c; ++j) {
-            if (!view && (j == i || (newton3 && j < i))) continue;
-            const double4 pj = ld_pos4(pos4, j);
-            if (pj.w == (double)LMD_DUMMY) continue;
-            const double r2 = r2_exact(pi.x - pj.x, pi.y - pj.y, pi.z - pj.z);
-            if (r2 < rl2) visit(j);
-          }
-        }
-  }
-}
-
-__global__ void vl_count_kernel(GridK g, int n, int newton3, double rl2,
-                                const double* __restrict__ pos4, const int32_t* __restrict__ os,
-                                const int32_t* __restrict__ oc, const int32_t* __restrict__ hs,
-                                const int32_t* __restrict__ hc, int32_t* __restrict__ count) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const double4 pi = ld_pos4(pos4, i);
-  int c = 0;
-  if (pi.w == (double)LMD_OWNED) {
-    const long long lin = cell_of_owned(pi, g.lo0, g.lo1, g.lo2, g.cl0, g.cl1, g.cl2, g.d0, g.d1,
-                                        g.d2, g.t0, g.t1);
-    for_candidates(i, pi, newton3, g.t0, g.t1, lin, os, oc, hs, hc, pos4, rl2,
-                   [&](int) { ++c; });
-  }
-  count[i] = c;
-}
-
-__global__ void vl_tile_kernel(int n, int A, int B, const int32_t* __restrict__ count,
-                               long long* __restrict__ tile_len, int32_t* __restrict__ kmax) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  const int ntiles = (n + A - 1) / A;
-  if (t >= ntiles) return;
-  int m = 0;
-  for (int k = t * A; k < t * A + A && k < n; ++k) m = max(m, count[k]);
-  int steps = (m + B - 1) / B;
-  steps = (steps + kChunk - 1) / kChunk * kChunk;
-  kmax[t] = steps * B;
-  tile_len[t] = (long long)steps * 32;
-}
-
-__global__ void vl_fill_kernel(GridK g, int n, int A, int B, int pattern, int newton3, double rl2,
-                               const double* __restrict__ pos4, const int32_t* __restrict__ os,
-                               const int32_t* __restrict__ oc, const int32_t* __restrict__ hs,
-                               const int32_t* __restrict__ hc, const long long* __restrict__ toff,
-                               int32_t* __restrict__ nbr) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int t = i / A, il = i - t * A;
-  int32_t* out = nbr + toff[t];
-  int k = 0;
-  const double4 pi = ld_pos4(pos4, i);
-  if (pi.w == (double)LMD_OWNED) {
-    const long long lin = cell_of_owned(pi, g.lo0, g.lo1, g.lo2, g.cl0, g.cl1, g.cl2, g.d0, g.d1,
-                                        g.d2, g.t0, g.t1);
-    for_candidates(i, pi, newton3, g.t0, g.t1, lin, os, oc, hs, hc, pos4, rl2, [&](int j) {
-      const int st = k / B, l = lane_of(pattern, il, k % B);
-      out[(long long)(st / kChunk) * (32 * kChunk) + l * kChunk + st % kChunk] = j;
-      ++k;
-    });
-  }
-}
-
 // Single-pass build into a fixed per-tile capacity: tile t owns the slots
 // [t * cap_steps * 32, (t + 1) * cap_steps * 32), so no count pass and no
 // prefix scan are needed.  Thread per owned particle; a tile's A particles
@@ -120,7 +39,7 @@ __global__ void vl_fill_kernel(GridK g, int n, int A, int B, int pattern, int ne
 #ifndef LMD_BUILD_MIN_BLOCKS
 #define LMD_BUILD_MIN_BLOCKS 12
 #endif
-template <int P, bool PF, typename IDX = int32_t>
+template <int P, typename IDX = int32_t>
 __global__ void __launch_bounds__(128, LMD_BUILD_MIN_BLOCKS) vl_build_kernel(GridK g, int n, int ntiles, int newton3,
                                 double rl2, int32_t sentinel, const double* __restrict__ pos4,
                                 const int32_t* __restrict__ os, const int32_t* __restrict__ oc,
@@ -129,8 +48,7 @@ __global__ void __launch_bounds__(128, LMD_BUILD_MIN_BLOCKS) vl_build_kernel(Gri
                                 int32_t* __restrict__ count_half,
                                 long long* __restrict__ toff, int32_t* __restrict__ kmax,
                                 int32_t* __restrict__ max_count, int32_t* __restrict__ nbr,
-                                const int32_t* __restrict__ groups, int G,
-                                const float4* __restrict__ pf, float rl2f_lo, float rl2f) {
+                                const int32_t* __restrict__ groups, int G) {
   constexpr int A = Pattern<P>::A, B = Pattern<P>::B, pattern = P;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int t = i / A, il = i - t * A;
@@ -141,7 +59,6 @@ __global__ void __launch_bounds__(128, LMD_BUILD_MIN_BLOCKS) vl_build_kernel(Gri
   int k = 0, kh = 0;
   if (i < n) {
     const double4 pi = ld_pos4(pos4, i);
-    const float4 pif = PF ? __ldg(pf + i) : make_float4(0.f, 0.f, 0.f, 0.f);
     if (pi.w == (double)LMD_OWNED) {
       const long long lin = cell_of_owned(pi, g.lo0, g.lo1, g.lo2, g.cl0, g.cl1, g.cl2, g.d0,
                                           g.d1, g.d2, g.t0, g.t1);
@@ -185,40 +102,16 @@ __global__ void __launch_bounds__(128, LMD_BUILD_MIN_BLOCKS) vl_build_kernel(Gri
             for (int j0 = j; j0 < e; j0 += 64) {
               const int cnt = min(e - j0, 64);
               unsigned long long mask = 0ull;
-              if (PF) {
-                // FP32 decision with an exact fallback: r2f < rl2f_lo is
-                // inside and r2f >= rl2f_hi outside for the reference's exact
-                // r2 too (the margin bounds the FP32 error for this
-                // coordinate range); only candidates in between -- a band of
-                // ~1e-4 relative width -- are re-tested in FP64
-                unsigned long long band = 0ull;
-#pragma unroll 4
-                for (int q = 0; q < cnt; ++q) {
-                  const float4 f = __ldg(pf + j0 + q);
-                  const float fx = pif.x - f.x, fy = pif.y - f.y, fz = pif.z - f.z;
-                  const float r2f = fmaf(fz, fz, fmaf(fy, fy, fx * fx));
-                  mask |= (unsigned long long)(r2f < rl2f_lo ? 1u : 0u) << q;
-                  band |= (unsigned long long)(r2f >= rl2f_lo && r2f < rl2f ? 1u : 0u) << q;
-                }
-                while (band) {
-                  const int q = __ffsll((long long)band) - 1;
-                  band &= band - 1ull;
-                  const double4 pj = ld_pos4(pos4, j0 + q);
-                  const double r2 = r2_exact(pi.x - pj.x, pi.y - pj.y, pi.z - pj.z);
-                  mask |= (unsigned long long)(r2 < rl2 ? 1u : 0u) << q;
-                }
-              } else {
-                // shift-and-add accumulation (2 integer instructions per
-                // candidate); bit-reversed below to candidate order
-                unsigned long long racc = 0ull;
+              // shift-and-add accumulation (2 integer instructions per
+              // candidate); bit-reversed below to candidate order
+              unsigned long long racc = 0ull;
 #pragma unroll 2
-                for (int q = 0; q < cnt; ++q) {
-                  const double4 pj = ld_pos4(pos4, j0 + q);
-                  const double r2 = r2_exact(pi.x - pj.x, pi.y - pj.y, pi.z - pj.z);
-                  racc = racc + racc + (r2 < rl2 ? 1ull : 0ull);
-                }
-                mask = __brevll(racc << (64 - cnt));
+              for (int q = 0; q < cnt; ++q) {
+                const double4 pj = ld_pos4(pos4, j0 + q);
+                const double r2 = r2_exact(pi.x - pj.x, pi.y - pj.y, pi.z - pj.z);
+                racc = racc + racc + (r2 < rl2 ? 1ull : 0ull);
               }
+              mask = __brevll(racc << (64 - cnt));
               if (!view) {
                 const unsigned self = (unsigned)(i - j0);
                 if (self < 64u) mask &= ~(1ull << self);
@@ -352,70 +245,6 @@ __global__ void vl_group_kernel(GridK g, int n, int G, int scap, const double* _
     rec[kGrpRow + 1] = (int)row_hi;
     atomicMax(smax, glob ? 0 : S);
     if (glob) atomicAdd(smax + 1, 1);
-  }
-}
-
-// Line-aligned entry order (optional pass after the build).  The force
-// kernel is bound by the L1 data pipe, which retires about one distinct
-// 128-B line per cycle per warp gather; with each lane's list in ascending
-// order the 32 lanes of a fill touch ~21 distinct lines.  This pass permutes
-// every lane's own slot sequence (so every entry stays with its particle;
-// valid for every interaction order): each lane keeps a window of its next W
-// entries in shared memory and, at each step, takes the entry whose line
-// occurs most often across the warp's windows (ties: smaller index), which
-// makes lanes gather from shared lines in the same fill (~14.6 lines at
-// W = 16 in a host simulation).  Counts live in a 1024-entry table indexed
-// by line mod 1024 (collisions only blur the heuristic).  Deterministic:
-// choices are made from counts frozen by __syncwarp, and the slot written
-// at step s was read into the window before (in place).
-template <int W>
-__global__ void __launch_bounds__(32 * kVLWarps)
-    vl_align_kernel(int ntiles, int B, const long long* __restrict__ toff,
-                    const int32_t* __restrict__ kmax, int32_t* __restrict__ nbr) {
-  __shared__ int cnt_s[kVLWarps][1024];
-  __shared__ int win_s[kVLWarps][W][32];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int t = blockIdx.x * kVLWarps + w;
-  if (t >= ntiles) return;
-  int* cnt = cnt_s[w];
-  for (int q = lane; q < 1024; q += 32) cnt[q] = 0;
-  __syncwarp();
-  const int steps = kmax[t] / B;
-  int32_t* base = nbr + toff[t];
-  auto slot = [&](int st) -> long long {
-    return (long long)(st / kChunk) * (32 * kChunk) + lane * kChunk + st % kChunk;
-  };
-  int nxt = 0;
-#pragma unroll
-  for (int q = 0; q < W; ++q) {
-    int v = -1;
-    if (nxt < steps) v = base[slot(nxt++)];
-    win_s[w][q][lane] = v;
-    if (v >= 0) atomicAdd(&cnt[(v >> 2) & 1023], 1);
-  }
-  __syncwarp();
-  for (int st = 0; st < steps; ++st) {
-    int best = 0, bc = -1, bv = 0x7fffffff;
-#pragma unroll
-    for (int q = 0; q < W; ++q) {
-      const int v = win_s[w][q][lane];
-      if (v >= 0) {
-        const int c = cnt[(v >> 2) & 1023];
-        if (c > bc || (c == bc && v < bv)) {
-          bc = c;
-          bv = v;
-          best = q;
-        }
-      }
-    }
-    __syncwarp();
-    base[slot(st)] = bv;
-    atomicSub(&cnt[(bv >> 2) & 1023], 1);
-    int v = -1;
-    if (nxt < steps) v = base[slot(nxt++)];
-    win_s[w][best][lane] = v;
-    if (v >= 0) atomicAdd(&cnt[(v >> 2) & 1023], 1);
-    __syncwarp();
   }
 }
 
@@ -697,131 +526,6 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// Staged lists, per group (one block of W warps = the group's W tiles):
-// re-deal the group's particles to lanes by descending list length (a tile
-// then holds lanes of similar length, so less padding up to its longest
-// list), copy every particle's entries from its build slot to its new slot
-// and, with `bank`, in the lane-local bank order of vl_bank_local_kernel.
-// slot_particle[t * 32 + l] = the particle at tile t, lane l (-1: none).
-template <bool I16>
-__global__ void __launch_bounds__(256)
-    vl_reorder_kernel(int n, int ntiles, int tcap, int cap_steps, int bank, int32_t sentinel,
-                      const int32_t* __restrict__ count, const long long* __restrict__ toff_in,
-                      const int32_t* __restrict__ kmax_in, const int32_t* __restrict__ nbr_in,
-                      int32_t* __restrict__ slot_particle, long long* __restrict__ toff_out,
-                      int32_t* __restrict__ kmax_out, int32_t* __restrict__ nbr_out) {
-  constexpr int CH = I16 ? 8 : 4;
-  extern __shared__ __align__(128) uint16_t bank_ent[];
-  __shared__ int cnt_s[256];
-  __shared__ int src_s[256];
-  const int G = blockDim.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int i0 = blockIdx.x * G;
-  // ranks by (count desc, index asc)
-  const int p = threadIdx.x;
-  const int cp = i0 + p < n ? count[i0 + p] : -1;
-  cnt_s[p] = cp;
-  __syncthreads();
-  int rank = 0;
-  for (int q = 0; q < G; ++q) {
-    const int cq = cnt_s[q];
-    rank += (cq > cp) || (cq == cp && q < p);
-  }
-  src_s[rank] = p;
-  __syncthreads();
-  const int t = blockIdx.x * (G / 32) + w;
-  if (t >= ntiles) return;  // warp-uniform; no block barrier follows
-  const int ps = src_s[w * 32 + lane];
-  const int i = i0 + ps < n ? i0 + ps : -1;
-  const int c = i >= 0 ? min(cnt_s[ps], cap_steps) : 0;
-  int m = c;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-  const int T = (m + CH - 1) / CH * CH;
-  const long long stride = (long long)cap_steps * 32;
-  slot_particle[t * 32 + lane] = i;
-  if (lane == 0) {
-    kmax_out[t] = T;
-    toff_out[t] = (long long)t * stride;
-  }
-  // the particle's column in the build layout
-  const int ot = i >= 0 ? i >> 5 : 0, ol = i >= 0 ? i & 31 : 0;
-  typedef typename std::conditional<I16, uint16_t, int32_t>::type IDX;
-  const IDX* src = reinterpret_cast<const IDX*>(nbr_in) + toff_in[ot];
-  IDX* dst = reinterpret_cast<IDX*>(nbr_out) + (long long)t * stride;
-  auto src_at = [&](int s) -> int {
-    const IDX v = src[(long long)(s / CH) * (32 * CH) + ol * CH + s % CH];
-    return I16 ? (int)(uint16_t)v : (int)v;
-  };
-  auto put = [&](int s, int j) {
-    dst[(long long)(s / CH) * (32 * CH) + lane * CH + s % CH] =
-        I16 ? (IDX)(j < 0 ? 0xffff : j) : (IDX)(j < 0 ? sentinel : j);
-  };
-  if (!bank || T > tcap) {
-    for (int s = 0; s < T; ++s) put(s, s < c ? src_at(s) : -1);
-    return;
-  }
-  // bank order (vl_bank_local_kernel): bucket by bank pair, Latin-square walk
-  uint16_t* bc = bank_ent + (size_t)w * (48 * 32 + (size_t)tcap * 32);
-  uint16_t* cur = bc + 16 * 32;
-  uint16_t* end = cur + 16 * 32;
-  uint16_t* ent = end + 16 * 32;
-#pragma unroll
-  for (int b = 0; b < 16; ++b) bc[b * 32 + lane] = 0;
-  for (int s = 0; s < c; ++s) ++bc[(src_at(s) & 15) * 32 + lane];
-  unsigned avail = 0u;
-  int acc = 0;
-#pragma unroll
-  for (int b = 0; b < 16; ++b) {
-    const int k = bc[b * 32 + lane];
-    cur[b * 32 + lane] = (uint16_t)acc;
-    acc += k;
-    end[b * 32 + lane] = (uint16_t)acc;
-    avail |= (k ? 1u : 0u) << b;
-  }
-  for (int s = 0; s < c; ++s) {
-    const int j = src_at(s), b = j & 15;
-    const int q = cur[b * 32 + lane];
-    cur[b * 32 + lane] = (uint16_t)(q + 1);
-    ent[q * 32 + lane] = (uint16_t)j;
-  }
-#pragma unroll
-  for (int b = 0; b < 16; ++b) cur[b * 32 + lane] = (uint16_t)(end[b * 32 + lane] - bc[b * 32 + lane]);
-  const int hl = lane & 15;
-  int lrem = c;
-  for (int s = 0; s < T; ++s) {
-    const int rot = (hl + s) & 15;
-    int pick = -1;
-    if (lrem > 0) {
-      if ((avail >> rot) & 1u) pick = rot;
-      else if (T - s <= lrem) pick = first_rot16(avail, rot);
-    }
-    int j = -1;
-    if (pick >= 0) {
-      const int q = cur[pick * 32 + lane];
-      j = ent[q * 32 + lane];
-      cur[pick * 32 + lane] = (uint16_t)(q + 1);
-      if (q + 1 == end[pick * 32 + lane]) avail &= ~(1u << pick);
-      --lrem;
-    }
-    put(s, j);
-  }
-}
-
-__global__ void vl_prefilter_kernel(int64_t rows, const double* __restrict__ pos4, double cx,
-                                    double cy, double cz, float4* __restrict__ pf) {
-  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (k >= rows) return;
-  const double4 p = ld_pos4(pos4, k);
-  pf[k] = make_float4(__double2float_rn(p.x - cx), __double2float_rn(p.y - cy),
-                      __double2float_rn(p.z - cz), 0.f);
-}
-
-__global__ void fill_i32_kernel(int64_t n, int32_t v, int32_t* __restrict__ out) {
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
-       k += (int64_t)gridDim.x * blockDim.x)
-    out[k] = v;
-}
-
 // ------------------------------------------------------------------ force
 // N3: 0 = full lists; 1 = half lists, the j side by FP64 atomics; 2 = full
 // lists with the reference's Newton3 pair bookkeeping (pairs with an image j
@@ -1033,7 +737,6 @@ constexpr int kStagedBatch = LMD_STAGED_BATCH;        // chunks evaluated togeth
 template <bool EV, int N3, int ROWS, bool STAGED, bool I16>
 __device__ __forceinline__ void vl_staged_tile(int t, int lane, int n_owned, int hb,
                                                unsigned dummy, unsigned long long* bar,
-                                               const int32_t* __restrict__ slot_particle,
                                                const int32_t* __restrict__ out_perm,
                                                const double* __restrict__ pos4,
                                                const double* __restrict__ xs,
@@ -1044,8 +747,7 @@ __device__ __forceinline__ void vl_staged_tile(int t, int lane, int n_owned, int
                                                const int32_t* __restrict__ nbr, const LJK& k,
                                                Acc& a, double* __restrict__ fx,
                                                double* __restrict__ fy, double* __restrict__ fz) {
-  // the particle this lane holds (re-dealt lists: slot_particle)
-  const int i = slot_particle ? slot_particle[t * 32 + lane] : t * 32 + lane;
+  const int i = t * 32 + lane;
   const bool iact = i >= 0 && i < n_owned;
   // I16: 16-bit local rows, 8 steps per 128-bit chunk (else 32-bit, 4 steps)
   constexpr int CH = I16 ? 8 : 4;
@@ -1143,7 +845,7 @@ __global__ void __launch_bounds__(32 * W, 16 / W)
     vl_staged_kernel(int n_owned, int ntiles, int sentinel, const int32_t* __restrict__ out_perm,
                      const double* __restrict__ pos4, SoA q, const int32_t* __restrict__ groups,
                      const long long* __restrict__ toff, const int32_t* __restrict__ kmax,
-                     const int32_t* __restrict__ nbr, const int32_t* __restrict__ slot_particle,
+                     const int32_t* __restrict__ nbr,
                      LJK k, double* __restrict__ fx,
                      double* __restrict__ fy, double* __restrict__ fz, double* __restrict__ ev,
                      lmd_stats* __restrict__ stats, int dbg) {
@@ -1189,12 +891,11 @@ __global__ void __launch_bounds__(32 * W, 16 / W)
   Acc a = {0.0, 0.0, 0.0, 0.0, 0.0, 0, 0, 0};
   if (glob)
     vl_staged_tile<EV, N3, ROWS, false, I16>(t, lane, n_owned, hb, (unsigned)sentinel, nullptr,
-                                             slot_particle,
-                                        out_perm, pos4,
+                                             out_perm, pos4,
                                         q.x, q.y, q.z, toff, kmax, nbr, k, a, fx, fy, fz);
   else
     vl_staged_tile<EV, N3, ROWS, true, I16>(t, lane, n_owned, hb, (unsigned)(ROWS - 1),
-                                       (dbg & 2) ? nullptr : &bar, slot_particle, out_perm,
+                                       (dbg & 2) ? nullptr : &bar, out_perm,
                                        pos4, xs, xs, xs, toff, kmax, nbr, k, a, fx, fy, fz);
   a.overlap |= a.hi_min == 0u;
   flush_acc(a, lane, true, EV, t, ev, stats);
@@ -1245,59 +946,8 @@ using namespace lmd;
 
 extern "C" {
 
-int lmd_vl_count(const lmd_grid* g, double rl2, int newton3, int64_t n_owned, const double* pos4,
-                 const int32_t* o_start, const int32_t* o_count, const int32_t* h_start,
-                 const int32_t* h_count, int32_t* count, void* stream) {
-  if (n_owned <= 0) return LMD_OK;
-  if (n_owned > 0x7fffffffLL) return LMD_ERR_CONFIG;
-  vl_count_kernel<<<(unsigned)cdiv(n_owned, 128), 128, 0, (cudaStream_t)stream>>>(
-      make_gridk(g), (int)n_owned, newton3, rl2, pos4, o_start, o_count, h_start, h_count, count);
-  LMD_CHECK_LAUNCH();
-  return LMD_OK;
-}
-
 int64_t lmd_vl_num_tiles(int64_t n_owned, int pattern) {
   return cdiv(n_owned, pattern_A(pattern));
-}
-
-size_t lmd_vl_scan_temp_bytes(int64_t ntiles) {
-  size_t bytes = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, bytes, (const long long*)nullptr, (long long*)nullptr,
-                                (int)(ntiles > 0 ? ntiles : 1));
-  return bytes;
-}
-
-int lmd_vl_layout(int64_t n_owned, int pattern, const int32_t* count, int64_t* tile_len,
-                  int64_t* tile_off, int32_t* kmax, void* temp, size_t temp_bytes,
-                  void* stream) {
-  if (n_owned <= 0) return LMD_OK;
-  const int A = pattern_A(pattern), B = pattern_B(pattern);
-  const int64_t ntiles = cdiv(n_owned, A);
-  cudaStream_t s = (cudaStream_t)stream;
-  vl_tile_kernel<<<(unsigned)cdiv(ntiles, 256), 256, 0, s>>>((int)n_owned, A, B, count,
-                                                             (long long*)tile_len, kmax);
-  LMD_CHECK_LAUNCH();
-  size_t bytes = temp_bytes;
-  cudaError_t e = cub::DeviceScan::ExclusiveSum(temp, bytes, (const long long*)tile_len,
-                                                (long long*)tile_off, (int)ntiles, s);
-  if (e != cudaSuccess) return set_cuda_error(e);
-  return LMD_OK;
-}
-
-int lmd_vl_fill(const lmd_grid* g, double rl2, int newton3, int pattern, int64_t n_owned,
-                int32_t sentinel, const double* pos4, const int32_t* o_start,
-                const int32_t* o_count, const int32_t* h_start, const int32_t* h_count,
-                const int64_t* tile_off, int64_t total, int32_t* nbr, void* stream) {
-  if (n_owned <= 0) return LMD_OK;
-  const int A = pattern_A(pattern), B = pattern_B(pattern);
-  cudaStream_t s = (cudaStream_t)stream;
-  fill_i32_kernel<<<1184, 256, 0, s>>>(total, sentinel, nbr);
-  LMD_CHECK_LAUNCH();
-  vl_fill_kernel<<<(unsigned)cdiv(n_owned, 128), 128, 0, s>>>(
-      make_gridk(g), (int)n_owned, A, B, pattern, newton3, rl2, pos4, o_start, o_count, h_start,
-      h_count, (const long long*)tile_off, nbr);
-  LMD_CHECK_LAUNCH();
-  return LMD_OK;
 }
 
 static int vl_build_impl(const lmd_grid* g, double rl2, int newton3, int pattern, int64_t n_owned,
@@ -1305,8 +955,8 @@ static int vl_build_impl(const lmd_grid* g, double rl2, int newton3, int pattern
                          const int32_t* o_count, const int32_t* h_start, const int32_t* h_count,
                          int32_t cap_steps, int32_t* count, int32_t* count_half,
                          int64_t* tile_off, int32_t* kmax, int32_t* max_count, int32_t* nbr,
-                         const int32_t* staged_groups, int staged_G, const float4* pf,
-                         float rl2f_lo, float rl2f, void* stream, bool idx16 = false) {
+                         const int32_t* staged_groups, int staged_G, void* stream,
+                         bool idx16 = false) {
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e = cudaMemsetAsync(max_count, 0, sizeof(int32_t), s);
   if (e != cudaSuccess) return set_cuda_error(e);
@@ -1319,27 +969,20 @@ static int vl_build_impl(const lmd_grid* g, double rl2, int newton3, int pattern
   const int32_t* groups = staged_groups;
   if (idx16) {
     if (pattern != LMD_V_BY_ONE || !groups) return LMD_ERR_CONFIG;
-    vl_build_kernel<LMD_V_BY_ONE, false, uint16_t><<<blocks, 128, 0, s>>>(
+    vl_build_kernel<LMD_V_BY_ONE, uint16_t><<<blocks, 128, 0, s>>>(
         make_gridk(g), (int)n_owned, (int)ntiles, newton3, rl2, 0xffff, pos4, o_start, o_count,
         h_start, h_count, cap_steps, count, count_half, (long long*)tile_off, kmax, max_count,
-        nbr, groups, staged_G, pf, rl2f_lo, rl2f);
+        nbr, groups, staged_G);
     LMD_CHECK_LAUNCH();
     return LMD_OK;
   }
   const int G = staged_G;
-#define LMD_VLB_(P, PFB)                                                                             \
-  vl_build_kernel<P, PFB><<<blocks, 128, 0, s>>>(make_gridk(g), (int)n_owned, (int)ntiles, newton3, \
+#define LMD_VLB(P)                                                                          \
+  vl_build_kernel<P><<<blocks, 128, 0, s>>>(make_gridk(g), (int)n_owned, (int)ntiles, newton3, \
                                             rl2, sentinel, pos4, o_start, o_count, h_start,    \
                                             h_count, cap_steps, count, count_half,             \
                                             (long long*)tile_off, kmax, max_count, nbr,        \
-                                            groups, G, pf, rl2f_lo, rl2f)
-#define LMD_VLB(P)          \
-  do {                      \
-    if (pf)                 \
-      LMD_VLB_(P, true);    \
-    else                    \
-      LMD_VLB_(P, false);   \
-  } while (0)
+                                            groups, G)
   switch (pattern) {
     case LMD_ONE_BY_V: LMD_VLB(LMD_ONE_BY_V); break;
     case LMD_V_BY_ONE: LMD_VLB(LMD_V_BY_ONE); break;
@@ -1348,7 +991,6 @@ static int vl_build_impl(const lmd_grid* g, double rl2, int newton3, int pattern
     default: return LMD_ERR_CONFIG;
   }
 #undef LMD_VLB
-#undef LMD_VLB_
   LMD_CHECK_LAUNCH();
   return LMD_OK;
 }
@@ -1360,50 +1002,20 @@ int lmd_vl_build(const lmd_grid* g, double rl2, int newton3, int pattern, int64_
                  int32_t* kmax, int32_t* max_count, int32_t* nbr, void* stream) {
   return vl_build_impl(g, rl2, newton3, pattern, n_owned, sentinel, pos4, o_start, o_count,
                        h_start, h_count, cap_steps, count, count_half, tile_off, kmax, max_count,
-                       nbr, nullptr, 0, nullptr, 0.f, 0.f, stream);
+                       nbr, nullptr, 0, stream);
 }
 
 int lmd_vl_build_staged(const lmd_grid* g, double rl2, int newton3, int64_t n_owned,
                         const double* pos4, const int32_t* o_start, const int32_t* o_count,
                         const int32_t* h_start, const int32_t* h_count, int32_t group_size,
-                        const int32_t* groups, int32_t index_bits, const float* pf,
-                        float rl2f_lo, float rl2f_hi, int32_t cap_steps, int32_t* count,
-                        int32_t* count_half, int64_t* tile_off, int32_t* kmax,
+                        const int32_t* groups, int32_t index_bits, int32_t cap_steps,
+                        int32_t* count, int32_t* count_half, int64_t* tile_off, int32_t* kmax,
                         int32_t* max_count, int32_t* nbr, void* stream) {
   if (group_size <= 0 || group_size % 32) return LMD_ERR_CONFIG;
-  if (pf && !(rl2f_lo < rl2f_hi)) return LMD_ERR_CONFIG;
   if (index_bits != 16 && index_bits != 32) return LMD_ERR_CONFIG;
-  if (index_bits == 16 && pf) return LMD_ERR_CONFIG;
   return vl_build_impl(g, rl2, newton3, LMD_V_BY_ONE, n_owned, -1, pos4, o_start, o_count,
                        h_start, h_count, cap_steps, count, count_half, tile_off, kmax, max_count,
-                       nbr, groups, group_size, reinterpret_cast<const float4*>(pf), rl2f_lo,
-                       rl2f_hi, stream, index_bits == 16);
-}
-
-int lmd_vl_prefilter_rows(int64_t rows, const double* pos4, const double* center, float* pf,
-                          void* stream) {
-  if (rows <= 0) return LMD_OK;
-  vl_prefilter_kernel<<<(unsigned)cdiv(rows, 256), 256, 0, (cudaStream_t)stream>>>(
-      rows, pos4, center[0], center[1], center[2], reinterpret_cast<float4*>(pf));
-  LMD_CHECK_LAUNCH();
-  return LMD_OK;
-}
-
-int lmd_vl_align(int pattern, int64_t n_units, int window, const int64_t* tile_off,
-                 const int32_t* kmax, int32_t* nbr, void* stream) {
-  if (n_units <= 0) return LMD_OK;
-  const int B = pattern_B(pattern);
-  const int64_t ntiles = cdiv(n_units, pattern_A(pattern));
-  const unsigned blocks = (unsigned)cdiv(ntiles, kVLWarps);
-  cudaStream_t s = (cudaStream_t)stream;
-  switch (window) {
-    case 8: vl_align_kernel<8><<<blocks, 32 * kVLWarps, 0, s>>>((int)ntiles, B, (const long long*)tile_off, kmax, nbr); break;
-    case 16: vl_align_kernel<16><<<blocks, 32 * kVLWarps, 0, s>>>((int)ntiles, B, (const long long*)tile_off, kmax, nbr); break;
-    case 32: vl_align_kernel<32><<<blocks, 32 * kVLWarps, 0, s>>>((int)ntiles, B, (const long long*)tile_off, kmax, nbr); break;
-    default: return LMD_ERR_CONFIG;
-  }
-  LMD_CHECK_LAUNCH();
-  return LMD_OK;
+                       nbr, groups, group_size, stream, index_bits == 16);
 }
 
 size_t lmd_vl_bank_smem_per_warp(int32_t cap_steps) {
@@ -1448,34 +1060,6 @@ int lmd_vl_bank_schedule(int pattern, int64_t n_units, int32_t sentinel, int rou
   if (e != cudaSuccess) return set_cuda_error(e);
   vl_bank_kernel<<<(unsigned)cdiv(ntiles, nw), 32 * nw, smem, (cudaStream_t)stream>>>(
       (int)ntiles, B, sentinel, rounds, cap_steps, (const long long*)tile_off, kmax, nbr);
-  LMD_CHECK_LAUNCH();
-  return LMD_OK;
-}
-
-int lmd_vl_reorder(int64_t n_owned, int32_t group_size, int32_t index_bits, int32_t cap_steps,
-                   int32_t max_steps, int bank, int32_t sentinel, const int32_t* count,
-                   const int64_t* tile_off, const int32_t* kmax, const int32_t* nbr,
-                   int32_t* slot_particle, int64_t* tile_off_out, int32_t* kmax_out,
-                   int32_t* nbr_out, void* stream) {
-  if (n_owned <= 0) return LMD_OK;
-  if (group_size % 32 || group_size < 32 || group_size > 256) return LMD_ERR_CONFIG;
-  if (index_bits != 16 && index_bits != 32) return LMD_ERR_CONFIG;
-  const int CH = index_bits == 16 ? 8 : 4;
-  if (cap_steps <= 0 || cap_steps % CH) return LMD_ERR_CONFIG;
-  const int tcap = max_steps < 255 ? max_steps : 255;
-  const int nw = group_size / 32;
-  const size_t smem = bank ? (size_t)nw * (48 * 32 + (size_t)tcap * 32) * sizeof(uint16_t) : 0;
-  const int64_t ngroups = cdiv(n_owned, group_size);
-  const int64_t ntiles = cdiv(n_owned, 32);
-  auto kern = index_bits == 16 ? vl_reorder_kernel<true> : vl_reorder_kernel<false>;
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return set_cuda_error(e);
-  }
-  kern<<<(unsigned)ngroups, group_size, smem, (cudaStream_t)stream>>>(
-      (int)n_owned, (int)ntiles, tcap, cap_steps, bank, sentinel, count,
-      (const long long*)tile_off, kmax, nbr, slot_particle, (long long*)tile_off_out, kmax_out,
-      nbr_out);
   LMD_CHECK_LAUNCH();
   return LMD_OK;
 }
@@ -1589,7 +1173,6 @@ int32_t lmd_vl_staged_capacity(int32_t group_size) {
 int lmd_force_vl_staged(int newton3, int flags, const lmd_lj* lj, int64_t n_owned,
                         const double* pos4, const double* soa, int64_t stride, int32_t sentinel,
                         int32_t group_size, const int32_t* groups, int32_t index_bits,
-                        const int32_t* slot_particle,
                         const int64_t* tile_off, const int32_t* kmax, const int32_t* nbr,
                         const int32_t* out_perm, double* fx, double* fy, double* fz,
                         double* ev_scratch, lmd_stats* stats, void* stream) {
@@ -1614,8 +1197,7 @@ int lmd_force_vl_staged(int newton3, int flags, const lmd_lj* lj, int64_t n_owne
     if (e != cudaSuccess) return set_cuda_error(e);                                            \
     kern<<<(unsigned)ngroups, 32 * W, smem, s>>>((int)n_owned, (int)ntiles, (int)sentinel,     \
                                                  out_perm, pos4, q, groups,                    \
-                                                 (const long long*)tile_off, kmax, nbr,        \
-                                                 slot_particle, k, fx,                         \
+                                                 (const long long*)tile_off, kmax, nbr, k, fx, \
                                                  fy, fz, ev_scratch, stats, (flags >> 8) & 3); \
   } while (0)
 #define LMD_VLS_W(EVB, N3B)                                 \

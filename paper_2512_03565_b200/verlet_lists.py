@@ -67,28 +67,13 @@ class VerletListContainer:
         # from global memory.  0 = off.
         self.staged_group = 128
         self._staging: dict = {}
-        # staged lists: True = cell-cooperative FP32 build (exact decisions,
-        # csrc/vl.cu vl_build_cells_kernel; measured 3.8 ms vs 1.0 ms at 1M,
-        # latency-bound at 14 warps/SM); False = thread per particle, FP64 tests
-        self.build_fp32 = False
         # staged lists with every group staged store 16-bit local rows
         self.index16 = True
-        # staged lists: deal each group's particles to lanes by list length
-        # (tile padding 11 -> 7 % of slots, but 167 vs 171 us for +0.18 ms per
-        # list build at 1M: off)
-        self.redeal = False
-        # particles per lane sharing one union list (csrc/vl_ci.cu) for full
-        # lists; 1 = one list per particle (csrc/vl.cu)
-        self.i_cluster = 1   # CI = 2 or 4 measured 2-3x slower
-        # line-aligned entry order after each list build (0 = ascending lists);
-        # measured <= 2 % faster force for +0.9 ms per build
-        self.align_window = 0
         # Newton3: "full_list" runs the full lists with the reference's Newton3
         # pair bookkeeping (no atomics, deterministic); "half_list" runs half
         # lists with FP64 atomics on the j side
         self.n3_mode = "full_list"
         self._collected_into = None
-        self._clusters_cache: dict = {}
         # segmented staged lists (csrc/vls.cu): the default for v_by_one full
         # lists (N3 off, or Newton3 by bookkeeping).  Entries whose build-time
         # distance is below rc + inner_skin form the inner segment, which
@@ -186,7 +171,6 @@ class VerletListContainer:
         self._lists.clear()
         self._staging.clear()
         self._counts.clear()
-        self._clusters_cache.clear()
         self._stats_cache.clear()
         self.reference_positions = d.positions().clone()
         self.steps_since_rebuild = 0
@@ -363,33 +347,10 @@ class VerletListContainer:
             return 0
         return 1 if self.n3_mode == "half_list" else 2
 
-    def _clusters(self, ci: int):
-        """(first, len) of the i-clusters: each cell's owned particles (one
-        contiguous run of the cell-sorted backing) cut into runs of ci."""
-        hit = self._clusters_cache.get(ci)
-        if hit is not None:
-            return hit
-        dev = self._pos4.device
-        oc = self._o_count.long()
-        per_cell = (oc + ci - 1) // ci
-        k = int(per_cell.sum().item())
-        cell = torch.repeat_interleave(torch.arange(len(oc), device=dev), per_cell, output_size=k)
-        first_of_cell = torch.cumsum(per_cell, 0) - per_cell
-        idx = torch.arange(k, device=dev) - first_of_cell[cell]
-        first = (self._o_start.long()[cell] + idx * ci).to(torch.int32)
-        ln = torch.clamp(oc[cell] - idx * ci, max=ci).to(torch.int32)
-        hit = (first.contiguous(), ln.contiguous(), k)
-        self._clusters_cache[ci] = hit
-        return hit
-
-    def _ci_for(self, newton3: bool) -> int:
-        return 1 if newton3 else int(self.i_cluster)
-
-
-    def _capacity_guess(self, newton3: bool, ci: int = 1) -> int:
+    def _capacity_guess(self, newton3: bool) -> int:
         """Entries per particle to reserve: the last build's longest list
         (+25 %), else twice the mean-density estimate."""
-        seen = self._max_seen.get((bool(newton3), ci))
+        seen = self._max_seen.get(bool(newton3))
         if seen is not None:
             return int(seen * 1.25) + 8
         rl = self.params.interaction_length
@@ -397,85 +358,47 @@ class VerletListContainer:
         est = (self.n_owned + self.n_halo) / vol * (4.0 / 3.0) * np.pi * rl ** 3
         if newton3:
             est *= 0.5
-        if ci > 1:   # union of ci nearby spheres
-            est *= 1.0 + 0.45 * (ci - 1)
         return int(2.0 * est) + 32
 
-    def _bank_for(self, ci: int) -> int:
-        return int(self.bank_rounds) if (self.use_soa and ci == 1) else -1
+    def _bank_for(self) -> int:
+        return int(self.bank_rounds) if self.use_soa else -1
 
-    def _staged_for(self, pattern, newton3_list: bool, ci: int) -> int:
+    def _staged_for(self, pattern, newton3_list: bool) -> int:
         """Group size of the staged layout for these lists (0: not staged)."""
-        if (self.staged_group and self.use_soa and ci == 1 and not newton3_list
+        if (self.staged_group and self.use_soa and not newton3_list
                 and pattern.code == as_pattern("v_by_one").code):
             return int(self.staged_group)
         return 0
 
-    def _prefilter_rows(self):
-        """FP32 centred copies of the build positions and the FP32 decision
-        bounds rl^2 -/+ four times the worst-case FP32 error of r2 near the
-        cutoff for this coordinate range (conversion and arithmetic
-        roundings): below / above them the FP32 and the reference's exact
-        decisions agree; in between the build re-tests in FP64."""
-        hit = self._clusters_cache.get("prefilter")
-        if hit is not None:
-            return hit
-        rows = self._build_pos4.shape[0]
-        lo, hi = np.asarray(self.box.min, float), np.asarray(self.box.max, float)
-        center = (ctypes.c_double * 3)(*((lo + hi) / 2.0))
-        pf = torch.empty((rows, 4), dtype=torch.float32, device=self._build_pos4.device)
-        N.call("lmd_vl_prefilter_rows", rows, N.ptr(self._build_pos4), ctypes.addressof(center),
-               N.ptr(pf), N.stream())
-        rl = float(self.params.interaction_length)
-        max_abs = float(np.max(hi - lo)) / 2.0 + 2.0 * rl
-        e = max_abs * 2.0 ** -23                    # coordinate conversion
-        d = 2.0 * e + rl * 2.0 ** -23               # per-axis difference
-        err = 3.0 * (2.0 * rl * d + d * d) + 3.0 * rl * rl * 2.0 ** -22
-        hi = float(np.nextafter(np.float32(rl * rl + 4.0 * err), np.float32(np.inf)))
-        lo = float(np.nextafter(np.float32(rl * rl - 4.0 * err), np.float32(-np.inf)))
-        hit = (pf, lo, hi)
-        self._clusters_cache["prefilter"] = hit
-        return hit
-
-    def _list(self, pattern, newton3: bool, ci: int | None = None, align: int | None = None,
-              bank: int | None = None):
-        ci = self._ci_for(newton3) if ci is None else ci
-        align = self.align_window if align is None else align
-        bank = self._bank_for(ci) if bank is None else bank
-        staged = self._staged_for(pattern, bool(newton3), ci) if align == 0 else 0
-        key = (pattern.code, bool(newton3), ci, align, bank, staged)
+    def _list(self, pattern, newton3: bool, bank: int | None = None):
+        bank = self._bank_for() if bank is None else bank
+        staged = self._staged_for(pattern, bool(newton3))
+        key = (pattern.code, bool(newton3), bank, staged)
         hit = self._lists.get(key)
         if hit is not None:
             return hit
         n = self.n_owned
         dev = self._pos4.device
-        if staged and n and self.segmented and align == 0:
+        if staged and n and self.segmented:
             hit = self._vls_lists(key)
             if hit is not None:
                 self._lists[key] = hit
                 return hit
-        if ci > 1:
-            cl_first, cl_len, units = self._clusters(ci)
-        else:
-            units = n
-        ntiles = int(N.load().lmd_vl_num_tiles(units, pattern.code))
+        ntiles = int(N.load().lmd_vl_num_tiles(n, pattern.code))
         b_ = pattern.shape(32)[1]
         tile_off = torch.empty(max(ntiles, 1), dtype=torch.int64, device=dev)
         kmax = torch.zeros(max(ntiles, 1), dtype=torch.int32, device=dev)
         count = torch.zeros(max(n, 1), dtype=torch.int32, device=dev)
         # a full per-particle build also records the half-list lengths
-        half = (torch.zeros(max(n, 1), dtype=torch.int32, device=dev)
-                if ci == 1 and not newton3 else None)
+        half = torch.zeros(max(n, 1), dtype=torch.int32, device=dev) if not newton3 else None
         mx = torch.zeros(1, dtype=torch.int32, device=dev)
         rl2 = self.params.interaction_length * self.params.interaction_length
-        cap = self._capacity_guess(newton3, ci)
+        cap = self._capacity_guess(newton3)
         s = N.stream()
         tables = (N.ptr(self._build_pos4), N.ptr(self._o_start), N.ptr(self._o_count),
                   N.ptr(self._h_start), N.ptr(self._h_count))
         sentinel = self.n_owned + self.n_halo
         if staged and n:
-            pf, rl2f_lo, rl2f_hi = (self._prefilter_rows() if self.build_fp32
-                                    else (None, 0.0, 0.0))
             ngroups = (n + staged - 1) // staged
             groups = torch.empty(ngroups * 128, dtype=torch.int32, device=dev)
             smax = torch.zeros(2, dtype=torch.int32, device=dev)
@@ -485,7 +408,7 @@ class VerletListContainer:
             sentinel = -1
             # 16-bit local rows when every group is staged (one host read)
             sm = smax.tolist()
-            bits = 16 if (sm[1] == 0 and self.index16 and not self.build_fp32) else 32
+            bits = 16 if (sm[1] == 0 and self.index16) else 32
         else:
             bits = 32
         chunk = 8 if bits == 16 else 4
@@ -496,15 +419,9 @@ class VerletListContainer:
             nbr = torch.empty(max(words, 1), dtype=torch.int32, device=dev)
             if staged and n:
                 N.call("lmd_vl_build_staged", self.grid, float(rl2), int(newton3), n, *tables,
-                       staged, N.ptr(groups), bits, N.ptr(pf) if pf is not None else None,
-                       rl2f_lo, rl2f_hi, cap_steps,
-                       N.ptr(count),
+                       staged, N.ptr(groups), bits, cap_steps, N.ptr(count),
                        N.ptr(half) if half is not None else None, N.ptr(tile_off),
                        N.ptr(kmax), N.ptr(mx), N.ptr(nbr), s)
-            elif ci > 1:
-                N.call("lmd_vl_ci_build", self.grid, float(rl2), pattern.code, ci, units,
-                       N.ptr(cl_first), N.ptr(cl_len), sentinel, *tables, cap_steps,
-                       N.ptr(count), N.ptr(tile_off), N.ptr(kmax), N.ptr(mx), N.ptr(nbr), s)
             else:
                 N.call("lmd_vl_build", self.grid, float(rl2), int(newton3), pattern.code, n,
                        sentinel, *tables, cap_steps, N.ptr(count),
@@ -515,41 +432,23 @@ class VerletListContainer:
                 break
             del nbr
             cap = longest
-        self._max_seen[(bool(newton3), ci)] = longest
+        self._max_seen[bool(newton3)] = longest
         self._counts.setdefault(bool(newton3), count)
         if half is not None and self.n3_mode == "full_list":
             self._counts.setdefault(True, half)
-        if align and units:
-            N.call("lmd_vl_align", pattern.code, units, int(align), N.ptr(tile_off), N.ptr(kmax),
-                   N.ptr(nbr), s)
         # lane-local order: 16-bit workspace, staged lists only
         if bank == 0 and not staged:
             bank = -1
         if bank > 0 and bits == 16:
             bank = 0    # the warp-cooperative order is 32-bit only
-        slots = None
-        if staged and n and self.redeal and bank <= 0 and staged <= 256:
-            # deal each group's particles to lanes by list length (less tile
-            # padding), bank order in the same pass
-            max_steps = min(cap_steps, ((longest + b_ - 1) // b_ + chunk - 1) // chunk * chunk)
-            slots = torch.empty(ntiles * 32, dtype=torch.int32, device=dev)
-            nbr2 = torch.empty_like(nbr)
-            toff2 = torch.empty_like(tile_off)
-            kmax2 = torch.empty_like(kmax)
-            N.call("lmd_vl_reorder", n, staged, bits, cap_steps, max_steps,
-                   int(bank == 0 and bits == 16),
-                   sentinel, N.ptr(count), N.ptr(tile_off), N.ptr(kmax), N.ptr(nbr),
-                   N.ptr(slots), N.ptr(toff2), N.ptr(kmax2), N.ptr(nbr2), s)
-            nbr, tile_off, kmax = nbr2, toff2, kmax2
-            bank = -1
-        if bank >= 0 and units:
+        if bank >= 0 and n:
             max_steps = min(cap_steps, ((longest + b_ - 1) // b_ + chunk - 1) // chunk * chunk)
             if bank > 0 or max_steps <= 255:
-                N.call("lmd_vl_bank_schedule", pattern.code, units, sentinel, int(bank), cap_steps,
+                N.call("lmd_vl_bank_schedule", pattern.code, n, sentinel, int(bank), cap_steps,
                        max_steps, bits, N.ptr(tile_off), N.ptr(kmax), N.ptr(nbr), s)
         if staged and n:
             rows = max(16, (int(sm[0]) + 15) // 16 * 16)
-            self._staging[key] = (groups, rows, staged, int(sm[1]), bits, slots)
+            self._staging[key] = (groups, rows, staged, int(sm[1]), bits)
         hit = (tile_off, kmax, nbr, ntiles * cap_steps * 32)
         self._lists[key] = hit
         return hit
@@ -660,8 +559,7 @@ class VerletListContainer:
         active when its entry is a real neighbour, not the sentinel pad
         (SURVEY §8f-4).  Exact by construction of the list layout."""
         pattern = as_pattern(pattern)
-        tile_off, kmax, _, _ = self._list(pattern, self._list_n3(newton3),
-                                          ci=self._ci_for(newton3))
+        tile_off, kmax, _, _ = self._list(pattern, self._list_n3(newton3))
         if tile_off is None:   # segmented lists: chunks of 8 steps per tile segment
             vls = self._vls_for(pattern, newton3)
             ng = vls["plan"]["ngroups"]
@@ -675,15 +573,11 @@ class VerletListContainer:
         steps = int((kmax[:ntiles].long() // b).sum().item())
         active = int(self._count(self._list_n3(newton3), pattern)[: self.n_owned].long()
                      .sum().item())
-        if self._ci_for(newton3) > 1:   # union lists: one entry serves a cluster
-            raise ConfigurationError("lane statistics cover per-particle lists")
         return 32 * steps, active
 
     def _key(self, pattern, newton3: bool):
-        ci = self._ci_for(newton3)
         n3l = self._list_n3(newton3)
-        return (pattern.code, n3l, ci, self.align_window, self._bank_for(ci),
-                self._staged_for(pattern, n3l, ci) if self.align_window == 0 else 0)
+        return (pattern.code, n3l, self._bank_for(), self._staged_for(pattern, n3l))
 
     def _vls_for(self, pattern, newton3: bool):
         return self._vls.get(self._key(as_pattern(pattern), newton3))
@@ -692,13 +586,9 @@ class VerletListContainer:
         """Build the lists for this interaction order now (outside any timed
         region); True if they had to be built."""
         pattern = as_pattern(pattern)
-        ci = self._ci_for(newton3)
-        n3l = self._list_n3(newton3)
-        key = (pattern.code, n3l, ci, self.align_window, self._bank_for(ci),
-               self._staged_for(pattern, n3l, ci) if self.align_window == 0 else 0)
-        if key in self._lists:
+        if self._key(pattern, newton3) in self._lists:
             return False
-        self._list(pattern, self._list_n3(newton3), ci=ci)
+        self._list(pattern, self._list_n3(newton3))
         self._count(newton3, pattern)
         return True
 
@@ -707,7 +597,7 @@ class VerletListContainer:
         fill steps and 4-step chunks; 4 B each)."""
         pattern = as_pattern(pattern)
         n3l = self._list_n3(newton3)
-        tile_off, kmax, _, _ = self._list(pattern, n3l, ci=self._ci_for(newton3))
+        tile_off, kmax, _, _ = self._list(pattern, n3l)
         if tile_off is None:
             return self.gpu_lane_stats(pattern, newton3)[0]
         b = pattern.shape(32)[1]
@@ -716,7 +606,7 @@ class VerletListContainer:
     def pairs(self, newton3: bool = False):
         """(id_i, id_j, j_is_image) of every list entry, for exact set checks."""
         pattern = as_pattern("one_by_v")
-        tile_off, kmax, nbr, total = self._list(pattern, newton3, ci=1, align=0, bank=-1)
+        tile_off, kmax, nbr, total = self._list(pattern, newton3, bank=-1)
         count = self._count(newton3)[: self.n_owned].long()
         n = self.n_owned
         perm = self._perm.long()
@@ -766,9 +656,8 @@ class VerletListContainer:
         -- collect_forces fused into the kernel (full lists only); the next
         collect_forces(out) is then a no-op."""
         pattern = as_pattern(pattern)
-        ci = self._ci_for(newton3)
         mode = self._kernel_n3(newton3)
-        tile_off, kmax, nbr, _ = self._list(pattern, self._list_n3(newton3), ci=ci)
+        tile_off, kmax, nbr, _ = self._list(pattern, self._list_n3(newton3))
         dev = self._pos4.device
         if stats_t is None:
             stats_t = N.new_stats(dev)
@@ -776,18 +665,6 @@ class VerletListContainer:
             stats_t.zero_()
         if part is not None and self._vls.get(self._key(pattern, newton3)) is None:
             raise ConfigurationError("group subsets need the segmented lists")
-        if ci > 1:
-            if self._pos4_stale:
-                self._regen_pos4()
-            cl_first, cl_len, units = self._clusters(ci)
-            if ev_t is None:
-                slots = int(N.load().lmd_vl_ci_ev_slots(units, pattern.code))
-                ev_t = torch.empty(2 * max(slots, 1), dtype=torch.float64, device=dev)
-            N.call("lmd_force_vl_ci", pattern.code, ci, N.FLAG_ENERGY if energy else 0,
-                   N.make_lj(self.params), self.n_owned, units, N.ptr(cl_first), N.ptr(cl_len),
-                   N.ptr(self._pos4), N.ptr(tile_off), N.ptr(kmax), N.ptr(nbr), N.ptr(self._fx),
-                   N.ptr(self._fy), N.ptr(self._fz), N.ptr(ev_t), N.ptr(stats_t), N.stream())
-            return stats_t
         vls = self._vls.get(self._key(pattern, newton3))
         if vls is not None and mode != 1:
             plan = vls["plan"]
@@ -805,6 +682,9 @@ class VerletListContainer:
             if part is not None:
                 gidx = self._vls_parts(plan)[part]
                 nidx = int(gidx.numel())
+                if nidx == 0:      # an empty part (a null index means "all groups")
+                    self._collected_into = out if direct else None
+                    return stats_t
             flags = (N.FLAG_ENERGY if energy else 0) | (N.FLAG_DEFER_EV if defer_ev else 0)
             N.call("lmd_vls_force", mode, flags,
                    N.make_lj(self.params), self.n_owned, plan["rows"], N.ptr(self._rows),
@@ -820,19 +700,16 @@ class VerletListContainer:
         if ev_t is None:
             slots = int(N.load().lmd_vl_ev_slots(self.n_owned, pattern.code))
             ev_t = torch.empty(2 * max(slots, 1), dtype=torch.float64, device=dev)
-        n3l = self._list_n3(newton3)
-        stg = self._staging.get((pattern.code, n3l, ci, self.align_window, self._bank_for(ci),
-                                 self._staged_for(pattern, n3l, ci)
-                                 if self.align_window == 0 else 0))
+        stg = self._staging.get(self._key(pattern, newton3))
         if stg is not None and mode != 1:
-            groups, _, gsize, _, bits, slots = stg
+            groups, _, gsize, _, bits = stg
             direct = out is not None and len(out) == self.n_owned
             fx, fy, fz = ((out.force_x, out.force_y, out.force_z) if direct
                           else (self._fx, self._fy, self._fz))
             N.call("lmd_force_vl_staged", mode, (N.FLAG_ENERGY if energy else 0) | self.knobs,
                    N.make_lj(self.params), self.n_owned, N.ptr(self._pos4), N.ptr(self._soa),
                    self._soa.shape[1], self.n_owned + self.n_halo, gsize, N.ptr(groups), bits,
-                   N.ptr(slots) if slots is not None else None, N.ptr(tile_off), N.ptr(kmax),
+                   N.ptr(tile_off), N.ptr(kmax),
                    N.ptr(nbr), N.ptr(self._perm) if direct else None, N.ptr(fx), N.ptr(fy),
                    N.ptr(fz), N.ptr(ev_t), N.ptr(stats_t), N.stream())
             self._collected_into = out if direct else None

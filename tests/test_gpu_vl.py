@@ -119,89 +119,6 @@ def test_lists_for_a_new_pattern_use_rebuild_positions(rng):
         assert st.pair_interactions == ost.pair_interactions
 
 
-@pytest.mark.parametrize("ci", [1, 2, 4])
-@pytest.mark.parametrize("pattern", list(PatternKind))
-def test_i_cluster_lists_match_oracle(rng, ci, pattern):
-    """Union lists over i-clusters (csrc/vl_ci.cu) give the same pairs,
-    forces, per-particle counts and statistics as per-particle lists."""
-    pos, span = _state(rng, 3500, 0.8)
-    pos[::97] = pos[::97] * 0.999     # ragged cells
-    params = LJParams(cutoff=2.5, skin=0.3)
-    box = SimulationBox.cube(span, periodic=True)
-    of, ost = O.force_phase_vl(pos, np.zeros(3), np.full(3, span), [True] * 3, params, False,
-                               pattern.value, 8)
-    cont = B.VerletListContainer(box, params)
-    cont.i_cluster = ci
-    buf = ParticleBuffer.from_positions(pos, device="cuda")
-    cont.rebuild(buf)
-    cont.refresh(buf)
-    st = cont.compute_forces("vl", False, pattern, 8, energy=True)
-    cont.collect_forces(buf)
-    assert st == B.KernelStats(*ost.as_tuple())
-    assert forces_close(buf.forces().cpu().numpy(), of)
-    assert abs(st.epot - ost.epot) <= 1e-12 * abs(ost.epot)
-    assert abs(st.virial - ost.virial) <= 1e-12 * abs(ost.virial)
-
-
-def test_i_cluster_capacity_retry_and_overlap(rng):
-    """A clustered droplet overflows the density-based capacity guess (the
-    build retries with the observed longest list); zero distance raises."""
-    pos, span = _state(rng, 3000, 0.3)
-    pos[:600] = pos[:600] * 0.25 + span * 0.3     # dense blob
-    params = LJParams(cutoff=2.5, skin=0.3)
-    box = SimulationBox.cube(span, periodic=True)
-    of, ost = O.force_phase_vl(pos, np.zeros(3), np.full(3, span), [True] * 3, params, False,
-                               "v_by_one", 8)
-    for ci in (1, 2, 4):
-        buf = ParticleBuffer.from_positions(pos, device="cuda")
-        cfg = Configuration(B.ContainerKind.VERLET_LISTS, B.TraversalKind.VL, False,
-                            PatternKind.V_BY_ONE)
-        cont = B.VerletListContainer(box, params)
-        cont.i_cluster = ci
-        cont.rebuild(buf)
-        cont.refresh(buf)
-        st = cont.compute_forces("vl", False, PatternKind.V_BY_ONE, 8)
-        cont.collect_forces(buf)
-        assert st == B.KernelStats(*ost.as_tuple()), ci
-        assert forces_close(buf.forces().cpu().numpy(), of), ci
-    bad = pos.copy()
-    bad[11] = bad[10]
-    cont = B.VerletListContainer(box, params)
-    cont.i_cluster = 2
-    buf = ParticleBuffer.from_positions(bad, device="cuda")
-    cont.rebuild(buf)
-    cont.refresh(buf)
-    with pytest.raises(B.ParticleOverlapError):
-        cont.compute_forces("vl", False, PatternKind.V_BY_ONE, 8)
-
-
-@pytest.mark.parametrize("window", [8, 16, 32])
-def test_line_aligned_lists_same_pairs_and_forces(rng, window):
-    """The optional line-aligned entry order (lmd_vl_align) permutes each
-    lane's entries only: pair counts and statistics identical, forces within
-    tolerance, and deterministic."""
-    pos, span = _state(rng, 4000, 0.8)
-    params = LJParams(cutoff=2.5, skin=0.3)
-    box = SimulationBox.cube(span, periodic=True)
-    of, ost = O.force_phase_vl(pos, np.zeros(3), np.full(3, span), [True] * 3, params, False,
-                               "v_by_one", 8)
-    prev = None
-    for _ in range(2):
-        cont = B.VerletListContainer(box, params)
-        cont.align_window = window
-        buf = ParticleBuffer.from_positions(pos, device="cuda")
-        cont.rebuild(buf)
-        cont.refresh(buf)
-        st = cont.compute_forces("vl", False, PatternKind.V_BY_ONE, 8)
-        cont.collect_forces(buf)
-        f = buf.forces().cpu().numpy()
-        assert st == B.KernelStats(*ost.as_tuple())
-        assert forces_close(f, of)
-        if prev is not None:
-            assert np.array_equal(prev, f)
-        prev = f
-
-
 @pytest.mark.parametrize("n3", [False, True])
 def test_fused_collect_matches_scatter(rng, n3):
     """launch_force(out=buf) writes the forces straight into the caller's
@@ -221,12 +138,11 @@ def test_fused_collect_matches_scatter(rng, n3):
     assert np.array_equal(res[0][0], res[1][0]) and res[0][1] == res[1][1]
 
 
-@pytest.mark.parametrize("staged,bank,index16,redeal", [
-    (0, -1, True, False), (128, -1, True, False), (128, 0, True, False), (128, 0, False, False),
-    (128, 2, False, False), (256, 0, True, False), (512, 0, True, False), (0, 2, True, False),
-    (128, 0, True, True), (128, -1, True, True), (256, 0, False, True)])
+@pytest.mark.parametrize("staged,bank,index16", [
+    (0, -1, True), (128, -1, True), (128, 0, True), (128, 0, False), (128, 2, False),
+    (256, 0, True), (512, 0, True), (0, 2, True), (256, 0, False)])
 @pytest.mark.parametrize("n3", [False, True])
-def test_staged_and_bank_ordered_lists_match_oracle(rng, staged, bank, index16, redeal, n3):
+def test_staged_and_bank_ordered_lists_match_oracle(rng, staged, bank, index16, n3):
     """Staged lists (TMA copies of each group's candidate runs into shared
     memory, local rows) and the bank-pair-aware entry orders: pair counts,
     statistics and energy exact / 1e-12 vs the oracle, forces within
@@ -246,7 +162,6 @@ def test_staged_and_bank_ordered_lists_match_oracle(rng, staged, bank, index16, 
             cont.staged_group = staged
             cont.bank_rounds = bank
             cont.index16 = index16
-            cont.redeal = redeal
             buf = ParticleBuffer.from_positions(pos, device="cuda")
             cont.rebuild(buf)
             cont.refresh(buf)
@@ -261,6 +176,6 @@ def test_staged_and_bank_ordered_lists_match_oracle(rng, staged, bank, index16, 
                 assert np.array_equal(prev, f)
             prev = f
         if staged:
-            groups, rows, g, over, bits, slots = next(iter(cont._staging.values()))
+            groups, rows, g, over, bits = next(iter(cont._staging.values()))
             assert rows >= 16 and g == staged
             assert bits == (16 if (over == 0 and index16) else 32)

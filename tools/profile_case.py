@@ -16,7 +16,6 @@ ap.add_argument("--config", default="vl,vl,false,v_by_one", help="comma-separate
 ap.add_argument("--n", type=int, default=1_000_000)
 ap.add_argument("--rho", type=float, default=0.8)
 ap.add_argument("--launches", type=int, default=3)
-ap.add_argument("--ci", default="1", help="VL i-cluster sizes to run, comma-separated")
 args = ap.parse_args()
 w = workloads.config2(args.rho, n=args.n, device="cuda")
 for label in args.config.split("+"):
@@ -25,17 +24,14 @@ for label in args.config.split("+"):
     params = B.LJParams(cutoff=2.5, skin=skin)
     box = B.SimulationBox.cube(w.box_length, periodic=True)
     buf = B.ParticleBuffer.from_positions(w.positions.cpu().numpy(), device="cuda")
-    for ci in [int(c) for c in args.ci.split(",")]:
-        cont = B.make_container(cfg.container, box, params, cluster_size=8)
-        if hasattr(cont, "i_cluster"):
-            cont.i_cluster = ci
-        # container knobs from the environment, e.g. VL_KNOBS=staged_group=128,bank_rounds=2
-        for kv in filter(None, os.environ.get("VL_KNOBS", "").split(",")):
-            name, val = kv.split("=")
-            setattr(cont, name, type(getattr(cont, name))(val))
-        cont.rebuild(buf)
-        cont.refresh(buf)
-        for _ in range(args.launches):
-            st = cont.compute_forces(cfg.traversal, cfg.newton3, cfg.pattern, 8)
-        torch.cuda.synchronize()
-        print(label, "ci", ci, st)
+    cont = B.make_container(cfg.container, box, params, cluster_size=8)
+    # container knobs from the environment, e.g. VL_KNOBS=segmented=0,staged_group=128
+    for kv in filter(None, os.environ.get("VL_KNOBS", "").split(",")):
+        name, val = kv.split("=")
+        setattr(cont, name, type(getattr(cont, name))(int(val) if val.isdigit() else val))
+    cont.rebuild(buf)
+    cont.refresh(buf)
+    for _ in range(args.launches):
+        st = cont.compute_forces(cfg.traversal, cfg.newton3, cfg.pattern, 8)
+    torch.cuda.synchronize()
+    print(label, st)

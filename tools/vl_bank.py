@@ -114,8 +114,7 @@ for pname in patterns:
         if grp:
             same = None
             stg = next(iter(cont._staging.values()))
-            extra = {"smem_rows": stg[1], "groups_over_capacity": stg[3], "index_bits": stg[4],
-                     "redealt": stg[5] is not None}
+            extra = {"smem_rows": stg[1], "groups_over_capacity": stg[3], "index_bits": stg[4]}
         else:
             srt = lane_sorted(v, steps, sentinel)
             if ref_sorted is None:
