@@ -718,7 +718,9 @@ __global__ void __launch_bounds__(kVsG, OCC)
   // one chunk: cw = chunk c (its first pair already loaded into P), nw =
   // chunk c + 1, fw receives chunk c + 2
   auto chunk = [&](const int4& cw, const int4& nw, int4& fw, int c) {
-    fw = __ldg(chunks + (long long)min(c + 2, cap_chunks - 1) * 32);
+    // (clamped to the launch's last chunk: the two chunks past it belong to
+    // the outer segment or the padding and would be fetched for nothing)
+    fw = __ldg(chunks + (long long)min(c + 2, nch - 1) * 32);
     bool band = false;
     load2(cw, 2, xQ, yQ, zQ);
     eval2(cw, 0, xP, yP, zP, band);
