@@ -232,6 +232,27 @@ __device__ __forceinline__ void vls_dummies(const int32_t* __restrict__ rec, dou
   }
 }
 
+// packed FP32 pairs (sm_100: FADD2 / FMUL2 / FFMA2), low word = first element
+__device__ __forceinline__ unsigned long long f32x2_pack(float lo, float hi) {
+  return (unsigned long long)__float_as_uint(lo) | ((unsigned long long)__float_as_uint(hi) << 32);
+}
+__device__ __forceinline__ unsigned long long f32x2_sub(unsigned long long a, unsigned long long b) {
+  unsigned long long d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ unsigned long long f32x2_mul(unsigned long long a, unsigned long long b) {
+  unsigned long long d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ unsigned long long f32x2_fma(unsigned long long a, unsigned long long b,
+                                                        unsigned long long c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+
 // ------------------------------------------------------------------ build
 // One block per group, thread per particle, 4 blocks per SM.
 //  1. walk: every lane of a warp walks the union of the warp's candidate
@@ -279,9 +300,33 @@ __global__ void __launch_bounds__(kVsG, 4)
   // this lane's stretch of its (original) tile's list area: the hits
   uint16_t* hits = reinterpret_cast<uint16_t*>(nbr + ((long long)(g * (kVsG / 32) + w) *
                                                       cap_chunks) * 32) + lane * cap_ent;
+  // the lane's cell: cell ends are non-decreasing along the line, so the
+  // cell is xa + the number of cells ending at or before p (independent
+  // loads, no dependent chain)
   int cx = rec[kVsXa];
-  if (active)
-    while (cx < rec[kVsXb] && p >= fso[rowbase + cx] + oc[rowbase + cx]) ++cx;
+  if (active) {
+    const int xa = cx, xb = rec[kVsXb];
+#pragma unroll 4
+    for (int x = xa; x < xb; ++x) cx += p >= fso[rowbase + x] + oc[rowbase + x] ? 1 : 0;
+  }
+  // the lane's candidate range in every run (local rows, l0 | l1 << 16),
+  // loaded up front: the table reads overlap the staging copy instead of
+  // stalling every run of the walk
+  unsigned lb[kVsRuns];
+#pragma unroll
+  for (int q = 0; q < kVsRuns; ++q) {
+    const int v = q / 9, dz = (q % 9) / 3 - 1, dy = q % 3 - 1;
+    lb[q] = 0u;
+    if (active && rec[kVsLen + q]) {
+      const int32_t* fs = v ? fsi : fso;
+      const int32_t* cc = v ? hc : oc;
+      const long long nb = rowbase + (long long)t0 * (dy + (long long)t1 * dz);
+      const int off = rec[kVsBase + q] - rec[kVsStart + q];
+      const int l0 = fs[nb + cx - 1] + off;
+      const int l1 = fs[nb + cx + 1] + cc[nb + cx + 1] + off;
+      lb[q] = (unsigned)l0 | ((unsigned)l1 << 16);
+    }
+  }
   mbar_wait(&bar, 0);
   double px = -1.0e30, py = -1.0e30, pz = -1.0e30;
   if (active) {
@@ -290,12 +335,14 @@ __global__ void __launch_bounds__(kVsG, 4)
     pz = xs[3 * irow + 2];
   }
   // FP32 copies of the staged rows relative to the group's first particle,
-  // written over the FP64 rows (row j: float4 at byte 16 j) in rounds of
-  // 128 rows -- a round's writes never reach a later round's rows
+  // written over the FP64 rows two rows at a time -- rows 2 q and 2 q + 1 as
+  // {x, x', y, y', z, z'} at byte 24 q, so one LDS.64 per axis feeds the
+  // packed FP32 arithmetic of the walk -- in rounds of 128 rows (a round's
+  // writes never reach a later round's rows; S is even)
   const int S = rec[kVsS];
   const int self0 = rec[kVsSelf];
   const double ox = xs[3 * self0], oy = xs[3 * self0 + 1], oz = xs[3 * self0 + 2];
-  float4* xf = reinterpret_cast<float4*>(sm_b);
+  float* xf = reinterpret_cast<float*>(sm_b);
   float rmax = 0.f;
 #pragma unroll 1
   for (int r0 = 0; r0 < S; r0 += kVsG) {
@@ -308,7 +355,10 @@ __global__ void __launch_bounds__(kVsG, 4)
     }
     __syncthreads();
     if (j < S) {
-      xf[j] = make_float4((float)a, (float)b, (float)c, 0.f);
+      float* o = xf + 6 * (j >> 1) + (j & 1);
+      o[0] = (float)a;
+      o[2] = (float)b;
+      o[4] = (float)c;
       rmax = fmaxf(rmax, fmaxf(fabsf((float)a), fmaxf(fabsf((float)b), fabsf((float)c))));
     }
   }
@@ -316,7 +366,7 @@ __global__ void __launch_bounds__(kVsG, 4)
   // rmax from the origin (conversion: 2^-24 rmax per coordinate, twice per
   // difference; arithmetic: a few ulp of rl^2); outside [rl2 - err, rl2 +
   // err) the FP32 decision is the exact one, inside the candidate is
-  // re-tested exactly from the FP64 rows in global memory
+  // flagged and decided exactly (FP64 rows in global memory) in step 2
   __shared__ float rmax_sm;
   if (tid == 0) rmax_sm = 0.f;
   __syncthreads();
@@ -328,136 +378,148 @@ __global__ void __launch_bounds__(kVsG, 4)
   const float rl2_lo = (float)(rl2 - err), rl2_hi = (float)(rl2 + err);
   const float rin2_hi = (float)(rin2 + err);
   const float pxf = (float)(px - ox), pyf = (float)(py - oy), pzf = (float)(pz - oz);
-  int n_in = 0, n_half = 0, n_ent = 0;
-#pragma unroll 1
+  const unsigned long long pxx = f32x2_pack(pxf, pxf), pyy = f32x2_pack(pyf, pyf),
+                           pzz = f32x2_pack(pzf, pzf);
+  // 1. walk.  No per-candidate range or self test: a candidate outside the
+  //    lane's own 3 cells is farther than rl (cells are at least rl wide), so
+  //    the distance test alone decides; the lane's own row (distance 0) is
+  //    appended like a hit and dropped in step 2, which also classifies the
+  //    entries (inner / outer / in the FP32 band around rl).
+  unsigned n_ent = 0;  // entries appended (own row and band candidates included)
+  // the lane's stretch as one opaque 64-bit base (one IMAD.WIDE per address)
+  uint16_t* hbase = hits;
+  asm volatile("" : "+l"(hbase));
+  auto test = [&](int j, float r2) {
+    // appended (predicated store and increment, no branch) when r2 < rl2_hi
+    // and the lane's stretch has room; classified in step 2
+    asm volatile(
+        "{\n .reg .pred p, q;\n"
+        " setp.lt.f32 p, %3, %4;\n"
+        " setp.lt.and.u32 q, %0, %5, p;\n"
+        " @q st.global.u16 [%1], %2;\n"
+        " @p add.u32 %0, %0, 1;\n}"
+        : "+r"(n_ent)
+        : "l"(hbase + n_ent), "h"((unsigned short)j), "f"(r2), "f"(rl2_hi), "r"((unsigned)cap_ent)
+        : "memory");
+  };
+  // rows jp (even) and jp + 1 with packed FP32 arithmetic
+  auto pair = [&](int jp, bool m0, bool m1) {
+    const unsigned long long* q = reinterpret_cast<const unsigned long long*>(xf + 3 * jp);
+    const unsigned long long dx = f32x2_sub(pxx, q[0]), dy = f32x2_sub(pyy, q[1]),
+                             dz = f32x2_sub(pzz, q[2]);
+    const unsigned long long r = f32x2_fma(dz, dz, f32x2_fma(dy, dy, f32x2_mul(dx, dx)));
+    if (m0) test(jp, __uint_as_float((unsigned)r));
+    if (m1) test(jp + 1, __uint_as_float((unsigned)(r >> 32)));
+  };
+#pragma unroll
   for (int q = 0; q < kVsRuns; ++q) {
-    const int v = q / 9, dz = (q % 9) / 3 - 1, dy = q % 3 - 1;
-    const int st = rec[kVsStart + q], rb = rec[kVsBase + q];
-    int l0 = 0, l1 = 0;
-    if (active && rec[kVsLen + q]) {
-      const int32_t* fs = v ? fsi : fso;
-      const int32_t* cc = v ? hc : oc;
-      const long long nb = rowbase + (long long)t0 * (dy + (long long)t1 * dz);
-      l0 = fs[nb + cx - 1] - st + rb;
-      l1 = fs[nb + cx + 1] + cc[nb + cx + 1] - st + rb;
-    }
+    const int l0 = (int)(lb[q] & 0xffffu), l1 = (int)(lb[q] >> 16);
+    // the union of the warp's candidate ranges: real rows of this run only
+    // (the even-alignment rows around a run are never tested -- they could
+    // be candidates of another run)
     const int u0 = __reduce_min_sync(0xffffffffu, l1 > l0 ? l0 : 0x7fffffff);
     const int u1 = __reduce_max_sync(0xffffffffu, l1 > l0 ? l1 : 0);
-    const unsigned span = (unsigned)(l1 - l0);
-    const int gshift = st - rb;  // global row of local row j: j + gshift
-    // lean, branch-free walk: hits are appended (predicated store), the
-    // rare candidates whose FP32 r2 falls in the band around rl^2 are noted
-    // and decided exactly after the run
-    int pend = -1, npend = 0;
-    auto append = [&](int j, bool inner) {
-      if (n_ent < cap_ent) hits[n_ent] = (uint16_t)(j | (inner ? 0 : 0x8000));
-      ++n_ent;
-      n_in += inner ? 1 : 0;
-      n_half += (v || j + gshift > p) ? 1 : 0;
-    };
-    {
-      uint16_t* const hp = hits + n_ent;
-      const int left = cap_ent - n_ent;  // appends beyond it are counted only
-      int nh = 0, ni = 0, nhalf = 0;
-      // owned runs: j counts towards the half list when its global row
-      // exceeds p (image runs: always)
-      const int half_from = v ? -0x7fffffff : p - gshift;
+    if (u1 <= u0) continue;
+    int j = u0;
+    if (j & 1) {
+      pair(j - 1, false, true);
+      ++j;
+    }
 #pragma unroll 2
-      for (int j = u0; j < u1; ++j) {
-        const float4 f = xf[j];
-        const float dx = pxf - f.x, dy = pyf - f.y, dz = pzf - f.z;
-        const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-        const bool mine = (unsigned)(j - l0) < span && j != irow;
-        const bool hit = mine && r2 < rl2_lo;
-        const bool band = mine && r2 >= rl2_lo && r2 < rl2_hi;
-        pend = band ? j : pend;
-        npend += band ? 1 : 0;
-        const bool inner = r2 < rin2_hi;
-        // predicated store and increments, no branch
-        asm volatile(
-            "{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p st.global.u16 [%0], %1;\n}" ::"l"(hp + nh),
-            "h"((unsigned short)(j | (inner ? 0 : 0x8000))), "r"((unsigned)(hit && nh < left))
-            : "memory");
-        nh += hit ? 1 : 0;
-        ni += (hit && inner) ? 1 : 0;
-        nhalf += (hit && j > half_from) ? 1 : 0;
-      }
-      n_ent += nh;
-      n_in += ni;
-      n_half += nhalf;
-    }
-    if (__any_sync(0xffffffffu, npend > 0)) {
-      // exact decisions (the reference's unfused r2 from the FP64 rows) of
-      // the band candidates: the noted one, or the run again for the rare
-      // lane with several
-      auto exact = [&](int j) {
-        const long long gj = 3LL * (j + gshift);
-        const double r2 = r2_exact(px - rows[gj], py - rows[gj + 1], pz - rows[gj + 2]);
-        if (r2 < rl2) append(j, r2 < rin2);
-      };
-      if (npend == 1) {
-        exact(pend);
-      } else if (npend > 1) {
-        for (int j = l0; j < l1; ++j) {
-          const float4 f = xf[j];
-          const float dx = pxf - f.x, dy = pyf - f.y, dz = pzf - f.z;
-          const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-          if (j != irow && r2 >= rl2_lo && r2 < rl2_hi) exact(j);
-        }
-      }
-    }
+    for (; j + 1 < u1; j += 2) pair(j, true, true);
+    if (j < u1) pair(j, true, false);
   }
-  const int n_out = n_ent - n_in;
-  if (active) {
-    count[p] = n_ent;
-    count_half[p] = n_half;
-  }
-  const int ent_max = __reduce_max_sync(0xffffffffu, n_ent);
+  const int ent_max = __reduce_max_sync(0xffffffffu, (int)n_ent);
   if (lane == 0 && ent_max > 0) atomicMax(info + 4, ent_max);
   const bool ok = __syncthreads_and(ent_max <= cap_ent);  // also: staging area free
-  // 2. counting sort into shared memory (bucket starts -> pos; a lane's
-  //    counts stay below 256: cap_ent <= 255)
+  // 2. the lane's hits are read back (8 at a time; a lane's stretch is 16-B
+  //    aligned: cap_ent % 8 == 0) and classified with the walk's FP32 r2
+  //    (the same arithmetic, bit for bit): the own row is dropped, band
+  //    candidates are decided by the reference's exact r2 from the FP64 rows,
+  //    entries beyond the inner radius get bit 14, and the half list length
+  //    is counted (local rows follow the global order: j > own row <=> a
+  //    later owned particle or an image).  The classified entries go back to
+  //    the stretch (dropped ones as 0xffff); then a counting sort by
+  //    (segment, bank pair) into shared memory (bucket starts -> pos; a
+  //    lane's counts stay below 256: cap_ent <= 255)
   uint16_t* mine = sorted + tid * cap_ent;
-  // hits are read back 8 at a time (a lane's stretch is 16-B aligned:
-  // cap_ent % 8 == 0)
-  const uint4* hits8 = reinterpret_cast<const uint4*>(hits);
+  uint4* hits8 = reinterpret_cast<uint4*>(hits);
   auto hit_at = [](const uint4& v, int e) {
     const unsigned w = e < 2 ? v.x : e < 4 ? v.y : e < 6 ? v.z : v.w;
     return (e & 1) ? w >> 16 : w & 0xffffu;
   };
+  int n_in = 0, n_half = 0, n_tot = 0;
   if (ok) {
-    for (int e0 = 0; e0 < n_ent; e0 += 8) {
-      const uint4 v = hits8[e0 >> 3];
+    uint4 vn = hits8[0];   // one chunk ahead (cap_ent >= 8)
+    for (int e0 = 0; e0 < (int)n_ent; e0 += 8) {
+      const uint4 v = vn;
+      if (e0 + 8 < (int)n_ent) vn = hits8[(e0 >> 3) + 1];
+      unsigned o[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        if (e0 + e < n_ent) {
-          const unsigned h = hit_at(v, e);
-          const int bk = ((h >> 15) << 4) + ((3 * (h & 0x7fffu)) & 15);
-          cnt[bk * kVsG + tid] = (uint8_t)(cnt[bk * kVsG + tid] + 1);
+        unsigned h = 0xffffu;
+        if (e0 + e < (int)n_ent) {
+          const int j = (int)hit_at(v, e);
+          const float* r = xf + 6 * (j >> 1) + (j & 1);
+          const float dx = pxf - r[0], dy = pyf - r[2], dz = pzf - r[4];
+          const float r2f = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+          bool keep = j != irow;
+          bool outer = r2f >= rin2_hi;
+          if (r2f >= rl2_lo) {   // rare: the exact decision
+            int gq = 0;
+            for (int q = 0; q < kVsRuns; ++q)
+              if (j >= rec[kVsBase + q] && j < rec[kVsBase + q] + rec[kVsLen + q]) gq = q;
+            const long long gj = 3LL * (j - rec[kVsBase + gq] + rec[kVsStart + gq]);
+            const double r2 = r2_exact(px - rows[gj], py - rows[gj + 1], pz - rows[gj + 2]);
+            keep = keep && r2 < rl2;
+            outer = !(r2 < rin2);
+          }
+          if (keep) {
+            h = (unsigned)j | (outer ? 0x4000u : 0u);
+            n_tot += 1;
+            n_in += outer ? 0 : 1;
+            n_half += j > irow ? 1 : 0;
+            const int bk = (outer ? 16 : 0) + ((3 * j) & 15);
+            cnt[bk * kVsG + tid] = (uint8_t)(cnt[bk * kVsG + tid] + 1);
+          }
         }
+        o[e >> 1] |= h << (16 * (e & 1));
       }
+      hits8[e0 >> 3] = make_uint4(o[0], o[1], o[2], o[3]);
     }
+  }
+  __syncthreads();  // every lane has read the FP32 rows: the sort may overwrite them
+  if (ok) {
     int acc = 0;
 #pragma unroll
     for (int b = 0; b < 32; ++b) {
       pos[b * kVsG + tid] = (uint8_t)acc;
       acc += cnt[b * kVsG + tid];
     }
-    for (int e0 = 0; e0 < n_ent; e0 += 8) {
-      const uint4 v = hits8[e0 >> 3];
+    uint4 vn = hits8[0];
+    for (int e0 = 0; e0 < (int)n_ent; e0 += 8) {
+      const uint4 v = vn;
+      if (e0 + 8 < (int)n_ent) vn = hits8[(e0 >> 3) + 1];
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        if (e0 + e < n_ent) {
+        if (e0 + e < (int)n_ent) {
           const unsigned h = hit_at(v, e);
-          const unsigned j = h & 0x7fffu;
-          const int bk = ((h >> 15) << 4) + ((3 * j) & 15);
-          const int at = pos[bk * kVsG + tid];
-          mine[at] = (uint16_t)j;
-          pos[bk * kVsG + tid] = (uint8_t)(at + 1);
+          if (h != 0xffffu) {
+            const unsigned j = h & 0x3fffu;
+            const int bk = ((h >> 14) << 4) + ((3 * j) & 15);
+            const int at = pos[bk * kVsG + tid];
+            mine[at] = (uint16_t)j;
+            pos[bk * kVsG + tid] = (uint8_t)(at + 1);
+          }
         }
       }
     }
     // pos[b] = end of bucket b; the emission takes from start = end - cnt
+  }
+  const int n_out = n_tot - n_in;
+  if (active) {
+    count[p] = n_tot;
+    count_half[p] = n_half;
   }
   // 3. deal the group's particles to lanes by descending inner length (ties:
   //    thread order); inactive threads rank last
