@@ -496,6 +496,28 @@ def run_b200(args):
 
     value = total_pairs * args.steps / t_max
     avg_launch = t_kern / args.steps
+    # segmented lists: the timed steps run the inner segment alone (the state
+    # is static, so no particle has moved delta / 2 -- as in the BASELINE MD
+    # runs, where dt = 0.001 and a rebuild every 10 steps keep displacements
+    # below it); the launch with both segments is timed beside it
+    outer_ms = None
+    if phase.kind == "vl" and cont._vls_for(cfg.pattern, cfg.newton3) is not None and dec is None:
+        slot, cont._disp_slot = cont._disp_slot, -1     # no displacement record: both segments
+        ts = []
+        for k in range(5):
+            flush.fill_(k)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            phase.launch()
+            e1.record()
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        cont._disp_slot = slot
+        st3 = N.read_stats(phase.stats_t)
+        assert st3.pair_interactions == st.pair_interactions
+        outer_ms = statistics.median(ts)
+        phase.launch()
     maint = None
     rb = time_rebuild(phase, torch)
     if rb is not None:
@@ -548,9 +570,52 @@ def run_b200(args):
                "steps": args.e2e_steps,
                "note": "force_phase() on pinned host SoA buffers: H2D positions, device "
                        "binning/images/neighbour build, force kernel, D2H forces"}
+    elif args.e2e_steps > 0 and dec is not None:
+        # every rank: its brick's particles in pinned host buffers ->
+        # force_phase_bricks (H2D, ghost planning + exchange, binning, lists,
+        # kernel, D2H); time = max over ranks, pairs = sum over ranks
+        n = n_local
+
+        class HostBuffer:
+            pass
+
+        hb = HostBuffer()
+        for k in ("pos_x", "pos_y", "pos_z"):
+            setattr(hb, k, getattr(buf, k).cpu().pin_memory())
+        for k in ("vel_x", "vel_y", "vel_z", "old_force_x", "old_force_y", "old_force_z"):
+            setattr(hb, k, None)
+        for k in ("force_x", "force_y", "force_z"):
+            setattr(hb, k, torch.zeros(n, dtype=torch.float64).pin_memory())
+        hb.id = None
+        hb.ownership = torch.zeros(n, dtype=torch.int8).pin_memory()
+        B.force_phase_bricks(hb, dec, params, cfg, args.vector_width)       # warm
+        torch.cuda.synchronize()
+        t_sum, p_e2e = 0.0, 0
+        for _ in range(args.e2e_steps):
+            flush.fill_(3)
+            torch.cuda.synchronize()
+            dist.barrier()
+            t0 = time.perf_counter()
+            s_e2e = B.force_phase_bricks(hb, dec, params, cfg, args.vector_width)
+            torch.cuda.synchronize()
+            t_sum += time.perf_counter() - t0
+            p_e2e = s_e2e.pair_interactions
+        tt = torch.tensor([t_sum], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        pp = torch.tensor([p_e2e], dtype=torch.int64, device="cuda")
+        dist.all_reduce(pp)
+        assert int(pp.item()) == total_pairs, (int(pp.item()), total_pairs)
+        hh = torch.tensor([n * (3 * 8 + 1), n * 3 * 8], dtype=torch.int64, device="cuda")
+        dist.all_reduce(hh)
+        e2e = {"value": int(pp.item()) * args.e2e_steps / float(tt.item()), "unit": UNIT,
+               "h2d_bytes_per_step": int(hh[0].item()), "d2h_bytes_per_step": int(hh[1].item()),
+               "steps": args.e2e_steps,
+               "note": "force_phase_bricks() on every rank's pinned host SoA buffers: H2D "
+                       "positions, ghost planning + exchange, device binning / neighbour "
+                       "build, force kernel, D2H forces; max over ranks"}
     elif args.e2e_steps > 0:
         e2e = {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
-               "note": "e2e measured at N=1 only (force_phase is single-domain)"}
+               "note": "replicas: e2e is measured at N=1 (force_phase is single-domain)"}
 
     # ------------------------------------------------------------ CPU baseline
     cpu = None
@@ -590,6 +655,13 @@ def run_b200(args):
                        "step": "refresh (positions -> cell order, images/ghosts) + force "
                                "kernel" + (f" + {backend} ghost exchange" if world > 1 else ""),
                        "kernel_ms_rank0": avg_launch * 1e3,
+                       "list_segments": (None if outer_ms is None else
+                                         f"inner (rc + {cont.inner_skin}) alone in the timed steps: "
+                                         "no particle has moved half of it since the build, "
+                                         "decided on the device per launch; "
+                                         "kernel_ms_both_segments_rank0 = the same launch "
+                                         "running the outer segment (up to rc + skin) too"),
+                       "kernel_ms_both_segments_rank0": outer_ms,
                        "l2": "inputs larger than L2 (1.8 GB state at c4) and L2 flushed "
                              "(256 MiB write) before every timed step",
                        "parallelism": (f"bricks {dec.grid}, {backend} P2P ghost exchange"

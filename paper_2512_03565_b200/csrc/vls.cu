@@ -253,8 +253,21 @@ __device__ __forceinline__ unsigned long long f32x2_fma(unsigned long long a, un
   return d;
 }
 
+// exact class of local row j for a particle at (px, py, pz): bit 0 = within
+// rl (the reference's unfused r2), bit 1 = beyond the inner radius
+__device__ __noinline__ int vls_exact_class(const double* __restrict__ rows, const int* run_st,
+                                            const int* run_rb, int j, double px, double py,
+                                            double pz, double rin2, double rl2) {
+  int gq = 0;
+  for (int q = 1; q < kVsRuns; ++q) gq += j >= run_rb[q] ? 1 : 0;
+  const long long gj = 3LL * (j - run_rb[gq] + run_st[gq]);
+  const double r2 = r2_exact(px - rows[gj], py - rows[gj + 1], pz - rows[gj + 2]);
+  return (r2 < rl2 ? 1 : 0) | (r2 < rin2 ? 0 : 2);
+}
+
 // ------------------------------------------------------------------ build
-// One block per group, thread per particle, 4 blocks per SM.
+// One block per group, thread per particle, 5 blocks per SM (shared memory:
+// the FP32 copies of the group's rows, later the lanes' sorted hits).
 //  1. walk: every lane of a warp walks the union of the warp's candidate
 //     ranges of a run (warp-uniform loop, broadcast shared-memory loads) and
 //     keeps the candidates of its own 3 cells with r2 < rl^2 (the
@@ -266,7 +279,7 @@ __device__ __forceinline__ unsigned long long f32x2_fma(unsigned long long a, un
 //     shared memory the staged rows occupied.
 //  3. the group's particles are ranked by inner length (the slot map) and
 //     each emits its segments in its new lane's Latin-square bank order.
-__global__ void __launch_bounds__(kVsG, 4)
+__global__ void __launch_bounds__(kVsG, 5)
     vls_build_kernel(int t0, int t1, const int32_t* __restrict__ groups,
                      const int32_t* __restrict__ info_in, const double* __restrict__ rows,
                      const int32_t* __restrict__ fso, const int32_t* __restrict__ oc,
@@ -276,22 +289,24 @@ __global__ void __launch_bounds__(kVsG, 4)
                      uint8_t* __restrict__ slotmap, int32_t* __restrict__ count,
                      int32_t* __restrict__ count_half, int32_t* __restrict__ info) {
   extern __shared__ __align__(128) double sm_b[];
-  double* xs = sm_b;                                       // staged rows (step 1)
   uint16_t* sorted = reinterpret_cast<uint16_t*>(sm_b);    // hits by bucket (steps 2-3)
   uint8_t* cnt = reinterpret_cast<uint8_t*>(sm_b) + area_bytes;  // [32 buckets][128]
   uint8_t* pos = cnt + 32 * kVsG;                                 // [32 buckets][128]
-  __shared__ unsigned long long bar;
   __shared__ int n_in_sm[kVsG], n_out_sm[kVsG], slot_sm[kVsG];
+  __shared__ int run_st[kVsRuns], run_rb[kVsRuns + 1];
+  __shared__ int bad_sm;
   const int g = blockIdx.x;
   if (g >= info_in[2]) return;
   const int32_t* rec = groups + (long long)g * kVsRec;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  if (tid == 0) mbar_init(&bar, 1);
+  if (tid < kVsRuns) {
+    run_st[tid] = rec[kVsStart + tid];
+    run_rb[tid] = rec[kVsBase + tid];
+  }
+  if (tid == kVsRuns) run_rb[kVsRuns] = rec[kVsS];
+  if (tid == 32) bad_sm = 0;
 #pragma unroll
   for (int b = 0; b < 32; ++b) cnt[b * kVsG + tid] = 0;
-  vls_dummies(rec, xs);
-  __syncthreads();
-  vls_stage(rec, rows, xs, &bar);
   const int cnt_p = rec[kVsCnt], p0 = rec[kVsP0];
   const bool active = tid < cnt_p;
   const int p = p0 + tid;
@@ -327,40 +342,34 @@ __global__ void __launch_bounds__(kVsG, 4)
       lb[q] = (unsigned)l0 | ((unsigned)l1 << 16);
     }
   }
-  mbar_wait(&bar, 0);
   double px = -1.0e30, py = -1.0e30, pz = -1.0e30;
-  if (active) {
-    px = xs[3 * irow];
-    py = xs[3 * irow + 1];
-    pz = xs[3 * irow + 2];
+  if (active) {   // owned rows are the first rows, in rebuild order
+    px = rows[3LL * p];
+    py = rows[3LL * p + 1];
+    pz = rows[3LL * p + 2];
   }
-  // FP32 copies of the staged rows relative to the group's first particle,
-  // written over the FP64 rows two rows at a time -- rows 2 q and 2 q + 1 as
-  // {x, x', y, y', z, z'} at byte 24 q, so one LDS.64 per axis feeds the
-  // packed FP32 arithmetic of the walk -- in rounds of 128 rows (a round's
-  // writes never reach a later round's rows; S is even)
+  // FP32 copies of the group's rows (the 18 runs, straight from global
+  // memory) relative to the group's first particle, two rows at a time:
+  // local rows 2 q and 2 q + 1 as {x, x', y, y', z, z'} at byte 24 q, so one
+  // LDS.64 per axis feeds the packed FP32 arithmetic of the walk
   const int S = rec[kVsS];
-  const int self0 = rec[kVsSelf];
-  const double ox = xs[3 * self0], oy = xs[3 * self0 + 1], oz = xs[3 * self0 + 2];
+  const double ox = rows[3LL * p0], oy = rows[3LL * p0 + 1], oz = rows[3LL * p0 + 2];
   float* xf = reinterpret_cast<float*>(sm_b);
   float rmax = 0.f;
-#pragma unroll 1
-  for (int r0 = 0; r0 < S; r0 += kVsG) {
-    const int j = r0 + tid;
-    double a = 0.0, b = 0.0, c = 0.0;
-    if (j < S) {
-      a = xs[3 * j] - ox;
-      b = xs[3 * j + 1] - oy;
-      c = xs[3 * j + 2] - oz;
-    }
-    __syncthreads();
-    if (j < S) {
-      float* o = xf + 6 * (j >> 1) + (j & 1);
-      o[0] = (float)a;
-      o[2] = (float)b;
-      o[4] = (float)c;
-      rmax = fmaxf(rmax, fmaxf(fabsf((float)a), fmaxf(fabsf((float)b), fabsf((float)c))));
-    }
+  __syncthreads();   // run table
+#pragma unroll 4
+  for (int j = tid; j < S; j += kVsG) {
+    int q = 0;
+#pragma unroll
+    for (int r = 1; r < kVsRuns; ++r) q += j >= run_rb[r] ? 1 : 0;   // bases are non-decreasing
+    const long long gj = 3LL * (run_st[q] + (j - run_rb[q]));
+    const float a = (float)(rows[gj] - ox), b = (float)(rows[gj + 1] - oy),
+                c = (float)(rows[gj + 2] - oz);
+    float* o = xf + 6 * (j >> 1) + (j & 1);
+    o[0] = a;
+    o[2] = b;
+    o[4] = c;
+    rmax = fmaxf(rmax, fmaxf(fabsf(a), fmaxf(fabsf(b), fabsf(c))));
   }
   // decision bounds: |FP32 r2 - exact r2| <= err for coordinates up to
   // rmax from the origin (conversion: 2^-24 rmax per coordinate, twice per
@@ -411,9 +420,13 @@ __global__ void __launch_bounds__(kVsG, 4)
     if (m0) test(jp, __uint_as_float((unsigned)r));
     if (m1) test(jp + 1, __uint_as_float((unsigned)(r >> 32)));
   };
-#pragma unroll
+#pragma unroll 1   // (lb[] lives in local memory: one L1 read per run; unrolling
+                   // 18 copies of the walk overflows the instruction cache)
+  unsigned lbn = lb[0];
   for (int q = 0; q < kVsRuns; ++q) {
-    const int l0 = (int)(lb[q] & 0xffffu), l1 = (int)(lb[q] >> 16);
+    const unsigned lbq = lbn;
+    lbn = lb[min(q + 1, kVsRuns - 1)];   // one run ahead
+    const int l0 = (int)(lbq & 0xffffu), l1 = (int)(lbq >> 16);
     // the union of the warp's candidate ranges: real rows of this run only
     // (the even-alignment rows around a run are never tested -- they could
     // be candidates of another run)
@@ -431,7 +444,10 @@ __global__ void __launch_bounds__(kVsG, 4)
   }
   const int ent_max = __reduce_max_sync(0xffffffffu, (int)n_ent);
   if (lane == 0 && ent_max > 0) atomicMax(info + 4, ent_max);
-  const bool ok = __syncthreads_and(ent_max <= cap_ent);  // also: staging area free
+  // a lane without room makes the whole build void (the host retries with
+  // the observed maximum): flagged here, read by every warp after step 2
+  const bool room = ent_max <= cap_ent;
+  if (lane == 0 && !room) atomicOr(&bad_sm, 1);
   // 2. the lane's hits are read back (8 at a time; a lane's stretch is 16-B
   //    aligned: cap_ent % 8 == 0) and classified with the walk's FP32 r2
   //    (the same arithmetic, bit for bit): the own row is dropped, band
@@ -449,7 +465,7 @@ __global__ void __launch_bounds__(kVsG, 4)
     return (e & 1) ? w >> 16 : w & 0xffffu;
   };
   int n_in = 0, n_half = 0, n_tot = 0;
-  if (ok) {
+  if (room) {
     uint4 vn = hits8[0];   // one chunk ahead (cap_ent >= 8)
     for (int e0 = 0; e0 < (int)n_ent; e0 += 8) {
       const uint4 v = vn;
@@ -465,14 +481,10 @@ __global__ void __launch_bounds__(kVsG, 4)
           const float r2f = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
           bool keep = j != irow;
           bool outer = r2f >= rin2_hi;
-          if (r2f >= rl2_lo) {   // rare: the exact decision
-            int gq = 0;
-            for (int q = 0; q < kVsRuns; ++q)
-              if (j >= rec[kVsBase + q] && j < rec[kVsBase + q] + rec[kVsLen + q]) gq = q;
-            const long long gj = 3LL * (j - rec[kVsBase + gq] + rec[kVsStart + gq]);
-            const double r2 = r2_exact(px - rows[gj], py - rows[gj + 1], pz - rows[gj + 2]);
-            keep = keep && r2 < rl2;
-            outer = !(r2 < rin2);
+          if (r2f >= rl2_lo) {   // rare: the exact decision (out of line)
+            const int d = vls_exact_class(rows, run_st, run_rb, j, px, py, pz, rin2, rl2);
+            keep = keep && (d & 1);
+            outer = (d & 2) != 0;
           }
           if (keep) {
             h = (unsigned)j | (outer ? 0x4000u : 0u);
@@ -489,6 +501,7 @@ __global__ void __launch_bounds__(kVsG, 4)
     }
   }
   __syncthreads();  // every lane has read the FP32 rows: the sort may overwrite them
+  const bool ok = bad_sm == 0;
   if (ok) {
     int acc = 0;
 #pragma unroll
@@ -965,8 +978,9 @@ int lmd_vls_plan(const lmd_grid* g, int64_t n_owned, const int32_t* o_start,
 }
 
 static inline int build_area(int32_t rows, int32_t cap_entries) {
-  // staged rows (step 1), then the lanes' sorted hits (steps 2-3)
-  const size_t a = std::max((size_t)(rows + 16) * 24, (size_t)cap_entries * kVsG * 2);
+  // FP32 copies of the rows (step 1: 12 B per row), then the lanes' sorted
+  // hits (steps 2-3)
+  const size_t a = std::max((size_t)rows * 12, (size_t)cap_entries * kVsG * 2);
   return (int)((a + 127) / 128 * 128);
 }
 

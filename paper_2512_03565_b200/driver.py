@@ -59,6 +59,44 @@ def force_phase(owned, box, params, config: Configuration, vector_width: int,
     return stats
 
 
+def force_phase_bricks(owned, dec, params, config: Configuration, vector_width: int,
+                        cluster_size: int | None = None, energy: bool = False) -> KernelStats:
+    """``force_phase`` for one brick of a domain decomposition (one rank per
+    GPU): ``owned`` holds this rank's particles (host or device SoA buffer,
+    positions inside the brick), ``dec`` the BrickDecomposition.  The ghost
+    layer (interaction length thick, periodic images across the global box
+    included) is planned and exchanged with the neighbouring ranks inside
+    the call, the container is built over [owned | ghosts], one force
+    computation runs and ``owned.force_*`` is overwritten.  The returned
+    statistics are this rank's (owned-ghost pairs counted on the owned side,
+    traversals.py:157-160); sum them over ranks for the global figures."""
+    import torch
+
+    from .particles import ParticleBuffer
+    validate_vector_width(vector_width)
+    if not config.is_valid():
+        raise ConfigurationError(f"invalid configuration {config.label!r}")
+    dev_owned = device_soa(owned)
+    pos = torch.stack([dev_owned.pos_x, dev_owned.pos_y, dev_owned.pos_z], dim=1)
+    ghost_rows = dec.plan(pos)
+    ghosts = ParticleBuffer.empty(ghost_rows.shape[0], device=pos.device)
+    ghosts.pos_x.copy_(ghost_rows[:, 0])
+    ghosts.pos_y.copy_(ghost_rows[:, 1])
+    ghosts.pos_z.copy_(ghost_rows[:, 2])
+    cont = make_container(config.container, dec.local_box(), params,
+                          cluster_size=config.cluster_size or cluster_size or vector_width)
+    if hasattr(cont, "bank_rounds"):
+        cont.bank_rounds = -1
+    cont.rebuild(dev_owned, ghosts)
+    cont.refresh(dev_owned, ghosts)
+    stats = cont.compute_forces(config.traversal, config.newton3, as_pattern(config.pattern),
+                                vector_width, energy=energy)
+    cont.collect_forces(dev_owned)
+    if dev_owned is not owned:
+        _write_forces_back(owned, dev_owned)
+    return stats
+
+
 def _write_forces_back(host, dev) -> None:
     import torch
     for name in ("force_x", "force_y", "force_z"):

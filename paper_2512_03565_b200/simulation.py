@@ -74,6 +74,7 @@ class RunSummary:
     force_time_s: float = 0.0    # device time of the force launches (CUDA events)
     steps: int = 0
     retunes: int = 0
+    rebuilds: int = 0
     extra: dict = field(default_factory=dict)
 
     @property
@@ -210,6 +211,7 @@ def run_md(owned, box, params, iterations: int, vector_width: int = 8, *,
     initial_max = max_particles_per_cell(owned, box, margin)
     phase_max = initial_max
     retunes = 0
+    rebuilds = 0
     force_events: list = []   # CUDA events around each force launch (device time)
     start = time.perf_counter()
     whole = metric == "iteration"
@@ -244,6 +246,7 @@ def run_md(owned, box, params, iterations: int, vector_width: int = 8, *,
                 cont.rebuild(owned)
                 cont.refresh(owned)
                 rebuilt = not fresh
+                rebuilds += 1
             else:
                 late.resolve()
                 cont.refresh(owned)
@@ -318,7 +321,7 @@ def run_md(owned, box, params, iterations: int, vector_width: int = 8, *,
         initial_max_per_cell=initial_max,
         final_max_per_cell=max_particles_per_cell(owned, box, margin),
         final_max_speed=float(speed.max().item()) if len(owned) else 0.0,
-        force_time_s=force_time, steps=iterations, retunes=retunes)
+        force_time_s=force_time, steps=iterations, retunes=retunes, rebuilds=rebuilds)
     return records, summary
 
 

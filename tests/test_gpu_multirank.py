@@ -58,6 +58,10 @@ def test_strong_scaling_c4_bricks_match_single_domain():
     assert single.returncode == 0, single.stderr[-2000:]
     s = json.loads([ln for ln in single.stdout.splitlines() if ln.startswith("{")][-1])
     assert d["config"]["pairs_per_step"] == s["config"]["pairs_per_step"]
+    # e2e at N > 1: force_phase_bricks on every rank's host buffers (the
+    # bench asserts its global pair count equals the device-resident run's)
+    assert d["e2e"]["value"] and d["e2e"]["value"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] == 48 ** 3 * 25
 
 
 def test_brick_md_two_ranks_matches_single_domain():

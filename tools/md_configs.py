@@ -36,6 +36,10 @@ def main():
     ap.add_argument("--metric", default="iteration",
                     help="tuner metric: iteration (whole MD step), time (force phase), laneops")
     ap.add_argument("--rho", default="0.2,0.5,0.8")
+    ap.add_argument("--rebuild-period", type=int, default=None,
+                    help="configs 3-5: steps between forced rebuilds (default: the container's "
+                         "10); a large value leaves the skin / 2 displacement rule alone "
+                         "in charge")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     if args.config == 2:
@@ -88,6 +92,7 @@ def main():
     records, summary = B.run_md(buf, box, params, steps, 8, configurations=configs,
                                 fixed_config=fixed, policy=policy, metric=args.metric,
                                 retune_drift=0.2 if configs else None,
+                                rebuild_period=args.rebuild_period,
                                 wrap="always" if args.config == 1 else "at_rebuild")
     torch.cuda.synchronize()
     pairs = sum(r.pair_interactions for r in records)
@@ -103,7 +108,8 @@ def main():
         "generation_s": t_gen, "note": w.note,
         "tuning_iterations": sum(r.phase == "tuning" for r in records),
         "configs_seen": sorted({r.configuration.label for r in records}),
-        "metric": args.metric,
+        "metric": args.metric, "rebuild_period": args.rebuild_period or "container default (10)",
+        "rebuilds": summary.rebuilds,
     }
     per = {}
     for r in records:

@@ -31,3 +31,7 @@ for rep in range(3):
     torch.cuda.synchronize()
     print(f"side {side}: lists {e0.elapsed_time(e1):.3f} ms, force {e1.elapsed_time(e2):.3f} ms, "
           f"pairs {N.read_stats(st).pair_interactions}", flush=True)
+vls = cont._vls_for("v_by_one", False)
+print("cap_chunks", vls["cap_chunks"], "next cap_ent", cont._vls_cap, "rows", vls["plan"]["rows"],
+      "build smem", int(N.load().lmd_vls_build_smem(vls["plan"]["rows"], (vls["cap_chunks"] - 2) * 8)),
+      "info", vls["plan"]["info"].tolist())
