@@ -859,9 +859,11 @@ __global__ void vls_refresh_kernel(long long n, const int32_t* __restrict__ perm
     rows[3 * k + 1] = py;
     rows[3 * k + 2] = pz;
     if (disp) {
-      const double ex = px - build[3 * k], ey = py - build[3 * k + 1],
-                   ez = pz - build[3 * k + 2];
-      d2 = ex * ex + ey * ey + ez * ez;
+      // the reference's unfused expression (containers.py:23-38), so the
+      // rebuild decision taken from it is the one lmd_max_displacement2 takes
+      const double ex = __dadd_rn(px, -build[3 * k]), ey = __dadd_rn(py, -build[3 * k + 1]),
+                   ez = __dadd_rn(pz, -build[3 * k + 2]);
+      d2 = __dadd_rn(__dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey)), __dmul_rn(ez, ez));
     }
   }
   if (!disp) return;

@@ -239,7 +239,10 @@ def run_md(owned, box, params, iterations: int, vector_width: int = 8, *,
                 containers[ckey] = cont
             rebuilt = False
             fresh = cont.reference_positions is None
-            if fresh or cont.needs_rebuild(owned):
+            # containers that reduce the displacement inside their refresh
+            # (segmented Verlet lists) decide and refresh in one pass
+            fused = getattr(cont, "refresh_and_check", None)
+            if fresh or (fused(owned) if fused is not None else cont.needs_rebuild(owned)):
                 late.resolve()   # (the decision above synchronised)
                 if wrap == "at_rebuild":
                     apply_boundaries(owned, box)
@@ -249,7 +252,8 @@ def run_md(owned, box, params, iterations: int, vector_width: int = 8, *,
                 rebuilds += 1
             else:
                 late.resolve()
-                cont.refresh(owned)
+                if fused is None:
+                    cont.refresh(owned)
             cont.steps_since_rebuild += 1
             # lazily built structures (Verlet lists per interaction order) are
             # built here, outside the force-phase bracket: the reference's

@@ -314,6 +314,27 @@ class VerletListContainer:
 
     refresh_positions = refresh
 
+    def refresh_and_check(self, owned) -> bool:
+        """``needs_rebuild`` and ``refresh`` in one pass for the MD loop: True
+        when the period elapsed or a particle moved skin / 2 since the rebuild
+        (the caller rebuilds); otherwise the container has been refreshed.
+        The displacement is the one the refresh kernel reduces on the device
+        while it gathers the rows (the same unfused expression as
+        ``lmd_max_displacement2``), so no separate pass over the positions
+        runs; one 8-byte read decides."""
+        if (self.reference_positions is None or self._external_halo or self._rows is None
+                or self._build_rows is None or self.params.skin <= 0.0
+                or len(owned) != self.n_owned):
+            if self.needs_rebuild(owned):
+                return True
+            self.refresh(owned)
+            return False
+        if self.steps_since_rebuild >= self.rebuild_period:
+            return True
+        self.refresh(owned)
+        d2 = self._disp[self._disp_slot:self._disp_slot + 1].view(torch.float64).item()
+        return bool(d2 >= (0.5 * self.params.skin) ** 2)
+
     def refresh_owned(self, owned) -> None:
         """First half of an overlapped refresh with an external ghost layer:
         the owned rows only (the interior groups can run on them)."""

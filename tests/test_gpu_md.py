@@ -141,3 +141,42 @@ def test_graph_md_matches_eager_md():
         out.append((buf.positions().cpu().numpy(), [r.pair_interactions for r in recs]))
     assert out[0][1] == out[1][1]
     assert np.array_equal(out[0][0], out[1][0])
+
+
+def test_vl_refresh_and_check_decides_like_needs_rebuild():
+    """The MD loop's fused rebuild decision (displacement reduced inside the
+    Verlet-list refresh) equals needs_rebuild's (containers.py:23-38) on
+    displacements just below, at and above skin / 2, and leaves the container
+    refreshed when no rebuild is due."""
+    rng = np.random.default_rng(3)
+    n, L = 4000, 17.0
+    pos = rng.uniform(0.0, L, (n, 3))
+    box = SimulationBox.cube(L, periodic=True)
+    params = LJParams(cutoff=2.5, skin=0.3, dt=0.001)
+    cfg = Configuration.parse("vl,vl,false,v_by_one")
+    for move, expect in ((0.149999, False), (0.15, True), (0.2, True), (0.0, False)):
+        buf = ParticleBuffer.from_positions(pos, device="cuda")
+        cont = B.make_container("vl", box, params, rebuild_period=1000)
+        cont.rebuild(buf)
+        cont.refresh(buf)
+        cont.ensure_lists(cfg.pattern, False)
+        buf.pos_x[n // 2] += move * 0.6
+        buf.pos_y[n // 2] -= move * 0.8
+        want = cont.needs_rebuild(buf)
+        got = cont.refresh_and_check(buf)
+        assert got == want
+        if move in (0.2, 0.0):
+            assert got == expect
+        if not got:   # refreshed: the forces are those of the moved positions
+            st = cont.compute_forces("vl", False, cfg.pattern, 8)
+            cont.collect_forces(buf)
+            ref = ParticleBuffer.from_positions(buf.positions().cpu().numpy(), device="cuda")
+            st2 = B.force_phase(ref, box, params, cfg, 8)
+            assert st.pair_interactions == st2.pair_interactions
+            assert torch.allclose(buf.forces(), ref.forces(), rtol=0, atol=1e-9)
+    # the period rule
+    buf = ParticleBuffer.from_positions(pos, device="cuda")
+    cont = B.make_container("vl", box, params, rebuild_period=2)
+    cont.rebuild(buf)
+    cont.steps_since_rebuild = 2
+    assert cont.refresh_and_check(buf) is True
