@@ -103,10 +103,13 @@ class VerletClusterContainer:
         self.steps_since_rebuild = 0
         self.structure_version = 0
         # interaction orders as warp lane templates (lmd_force_vcl_order);
-        # False: the packed stream kernel for every order
-        self.order_kernels = True
+        # False: the packed stream kernel for every order (the cluster-aligned
+        # M x 32/M mapping with hit compaction, the fastest one on the GPU)
+        self.order_kernels = type(self).ORDER_KERNELS
         self._own = None
         self._stats_cache: dict = {}
+
+    ORDER_KERNELS = True   # default of ``order_kernels`` for new containers
 
     # ------------------------------------------------------------ protocol
     def needs_rebuild(self, owned) -> bool:

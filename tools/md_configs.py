@@ -40,8 +40,14 @@ def main():
                     help="configs 3-5: steps between forced rebuilds (default: the container's "
                          "10); a large value leaves the skin / 2 displacement rule alone "
                          "in charge")
+    ap.add_argument("--vcl-stream", action="store_true",
+                    help="config 3: the packed stream kernel (cluster-aligned M x 32/M "
+                         "mapping) for every order instead of the order's lane template")
     args = ap.parse_args()
     torch.cuda.set_device(0)
+    if args.vcl_stream:
+        from paper_2512_03565_b200.clusters import VerletClusterContainer
+        VerletClusterContainer.ORDER_KERNELS = False
     if args.config == 2:
         return sweep_config2(args)
     t_gen = time.perf_counter()
@@ -108,6 +114,7 @@ def main():
         "generation_s": t_gen, "note": w.note,
         "tuning_iterations": sum(r.phase == "tuning" for r in records),
         "configs_seen": sorted({r.configuration.label for r in records}),
+        "vcl_stream_kernel": bool(args.vcl_stream),
         "metric": args.metric, "rebuild_period": args.rebuild_period or "container default (10)",
         "rebuilds": summary.rebuilds,
     }
