@@ -162,3 +162,58 @@ def test_overlapped_ghost_exchange_matches_plain_refresh(rng):
     of, ost = O.force_phase_vl(pos, np.zeros(3), np.full(3, span), [True] * 3, params, False,
                                "v_by_one", 8)
     assert res[1][1] == ost.pair_interactions and forces_close(res[1][0], of)
+
+
+def test_capacity_retry_and_reuse(rng):
+    """A list capacity that is too small for the build (here forced to the
+    minimum) is detected on the device and the build redone at the observed
+    maximum; the next rebuild reuses the learnt capacity.  Same results."""
+    pos, span = _state(rng, 5000, 0.8)
+    params = LJParams(cutoff=2.5, skin=0.3)
+    box = SimulationBox.cube(span, periodic=True)
+    cont = B.VerletListContainer(box, params)
+    cont._vls_cap = 8
+    buf = ParticleBuffer.from_positions(pos, device="cuda")
+    cont.rebuild(buf)
+    cont.refresh(buf)
+    _check(cont, buf, pos, span, True, params, False)
+    assert cont._vls_for("v_by_one", False) is not None
+    learnt = cont._vls_cap
+    assert learnt > 8
+    cont.rebuild(buf)
+    cont.refresh(buf)
+    _check(cont, buf, pos, span, True, params, False)
+    assert cont._vls_cap == learnt
+
+
+def test_lists_too_long_for_segments_fall_back(rng):
+    """More than 248 candidates within rc + skin of a particle (a dense
+    state with a long cutoff) do not fit the segmented lists' 8-bit lane
+    counters: the container serves such a state from the round-1 staged /
+    global-gather lists instead, with the same results."""
+    pos, span = _state(rng, 4000, 1.0)
+    params = LJParams(cutoff=3.9, skin=0.3)      # ~310 neighbours within 4.2
+    box = SimulationBox.cube(span, periodic=True)
+    cont = B.VerletListContainer(box, params)
+    buf = ParticleBuffer.from_positions(pos, device="cuda")
+    cont.rebuild(buf)
+    cont.refresh(buf)
+    _check(cont, buf, pos, span, True, params, False)
+    assert cont._vls_for("v_by_one", False) is None
+
+
+@pytest.mark.parametrize("rho", [0.02, 0.1])
+def test_sparse_states_with_groups_over_many_cells(rng, rho):
+    """Dilute states: a group of 128 particles spans many cells of its line
+    (or whole lines hold a handful of particles); groups shrink to the
+    staging budget and empty runs are skipped."""
+    pos, span = _state(rng, 3000, rho)
+    params = LJParams(cutoff=2.5, skin=0.3)
+    box = SimulationBox.cube(span, periodic=True)
+    for n3 in (False, True):
+        cont = B.VerletListContainer(box, params)
+        buf = ParticleBuffer.from_positions(pos, device="cuda")
+        cont.rebuild(buf)
+        cont.refresh(buf)
+        _check(cont, buf, pos, span, True, params, n3)
+        assert cont._vls_for("v_by_one", n3) is not None
