@@ -334,7 +334,9 @@ int lmd_force_vl_staged(int newton3, int flags, const lmd_lj* lj, int64_t n_owne
  * reference's exact r2), entries with r2 < rin2 in the inner segment, the
  * rest in the outer; per tile t: seg_chunks[2t], [2t+1] = chunks of 8
  * entries; list chunk c of lane l at int4 index (t * cap_chunks + c) * 32 +
- * l (uint16 byte offsets 24 * local row, lane-local bank order);
+ * l (uint16 byte offsets 24 * local row; bank_order != 0: lane-local
+ * Latin-square bank order within each segment, else the order the walk found
+ * them in -- a cheaper build for lists that are used a few times only);
  * slotmap[g * 128 + lane slot] = the group-local particle the slot holds
  * (0xff: none); count[i] / count_half[i] = full / half list lengths (sorted
  * order); info[3] / info[4] = most chunks per tile / entries per lane seen
@@ -363,9 +365,9 @@ size_t lmd_vls_build_smem(int32_t rows, int32_t cap_entries);
 int lmd_vls_build(const lmd_grid* g, double rin2, double rl2, int64_t n_owned, int32_t rows,
                   const double* pos_rows, const int32_t* fs_own, const int32_t* o_count,
                   const int32_t* fs_img, const int32_t* h_count, const int32_t* groups,
-                  int64_t max_groups, int32_t cap_chunks, int32_t cap_entries, void* nbr,
-                  int32_t* seg_chunks, uint8_t* slotmap, int32_t* count, int32_t* count_half,
-                  int32_t* info, void* stream);
+                  int64_t max_groups, int32_t cap_chunks, int32_t cap_entries, int32_t bank_order,
+                  void* nbr, int32_t* seg_chunks, uint8_t* slotmap, int32_t* count,
+                  int32_t* count_half, int32_t* info, void* stream);
 int64_t lmd_vls_ev_slots(int64_t max_groups);
 int lmd_vls_force(int newton3, int flags, const lmd_lj* lj, int64_t n_owned, int32_t rows,
                   const double* pos_rows, const int32_t* groups, int64_t n_groups,

@@ -182,7 +182,7 @@ _sig("lmd_vls_plan_temp_bytes", _SZ, C.POINTER(Grid))
 _sig("lmd_vls_plan", _INT, C.POINTER(Grid), _I64, *([_VP] * 9), _SZ, _VP, _VP, _VP)
 _sig("lmd_vls_build_smem", _SZ, _I32, _I32)
 _sig("lmd_vls_build", _INT, C.POINTER(Grid), _D, _D, _I64, _I32, _VP, _VP, _VP, _VP, _VP, _VP,
-     _I64, _I32, _I32, _VP, _VP, _VP, _VP, _VP, _VP, _VP)
+     _I64, _I32, _I32, _I32, _VP, _VP, _VP, _VP, _VP, _VP, _VP)
 _sig("lmd_vls_ev_slots", _I64, _I64)
 _sig("lmd_vls_force", _INT, _INT, _INT, C.POINTER(LJ), _I64, _I32, _VP, _VP, _I64, _VP, _I64,
      _VP, _VP, _VP, _I32, _VP, _D, _VP, _VP, _VP, _VP, _VP, _VP, _VP)

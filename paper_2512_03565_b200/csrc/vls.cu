@@ -279,6 +279,7 @@ __device__ __noinline__ int vls_exact_class(const double* __restrict__ rows, con
 //     shared memory the staged rows occupied.
 //  3. the group's particles are ranked by inner length (the slot map) and
 //     each emits its segments in its new lane's Latin-square bank order.
+template <bool BANK>
 __global__ void __launch_bounds__(kVsG, 5)
     vls_build_kernel(int t0, int t1, const int32_t* __restrict__ groups,
                      const int32_t* __restrict__ info_in, const double* __restrict__ rows,
@@ -305,8 +306,10 @@ __global__ void __launch_bounds__(kVsG, 5)
   }
   if (tid == kVsRuns) run_rb[kVsRuns] = rec[kVsS];
   if (tid == 32) bad_sm = 0;
+  if (BANK) {
 #pragma unroll
-  for (int b = 0; b < 32; ++b) cnt[b * kVsG + tid] = 0;
+    for (int b = 0; b < 32; ++b) cnt[b * kVsG + tid] = 0;
+  }
   const int cnt_p = rec[kVsCnt], p0 = rec[kVsP0];
   const bool active = tid < cnt_p;
   const int p = p0 + tid;
@@ -491,8 +494,10 @@ __global__ void __launch_bounds__(kVsG, 5)
             n_tot += 1;
             n_in += outer ? 0 : 1;
             n_half += j > irow ? 1 : 0;
-            const int bk = (outer ? 16 : 0) + ((3 * j) & 15);
-            cnt[bk * kVsG + tid] = (uint8_t)(cnt[bk * kVsG + tid] + 1);
+            if (BANK) {
+              const int bk = (outer ? 16 : 0) + ((3 * j) & 15);
+              cnt[bk * kVsG + tid] = (uint8_t)(cnt[bk * kVsG + tid] + 1);
+            }
           }
         }
         o[e >> 1] |= h << (16 * (e & 1));
@@ -502,7 +507,7 @@ __global__ void __launch_bounds__(kVsG, 5)
   }
   __syncthreads();  // every lane has read the FP32 rows: the sort may overwrite them
   const bool ok = bad_sm == 0;
-  if (ok) {
+  if (ok && BANK) {
     int acc = 0;
 #pragma unroll
     for (int b = 0; b < 32; ++b) {
@@ -528,6 +533,28 @@ __global__ void __launch_bounds__(kVsG, 5)
       }
     }
     // pos[b] = end of bucket b; the emission takes from start = end - cnt
+  }
+  if (ok && !BANK) {
+    // plain order: a stable partition into [inner | outer], two running
+    // positions in registers
+    int at_in = 0, at_out = n_in;
+    uint4 vn = hits8[0];
+    for (int e0 = 0; e0 < (int)n_ent; e0 += 8) {
+      const uint4 v = vn;
+      if (e0 + 8 < (int)n_ent) vn = hits8[(e0 >> 3) + 1];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        if (e0 + e < (int)n_ent) {
+          const unsigned h = hit_at(v, e);
+          if (h != 0xffffu) {
+            const bool outer = (h >> 14) != 0;
+            mine[outer ? at_out : at_in] = (uint16_t)(h & 0x3fffu);
+            at_in += outer ? 0 : 1;
+            at_out += outer ? 1 : 0;
+          }
+        }
+      }
+    }
   }
   const int n_out = n_tot - n_in;
   if (active) {
@@ -569,11 +596,13 @@ __global__ void __launch_bounds__(kVsG, 5)
     const int ns = live ? (seg ? n_out_sm[src] : n_in_sm[src]) : 0;
     const int C = (__reduce_max_sync(0xffffffffu, ns) + 7) >> 3;
     unsigned m = 0;
-    if (ok && live) {
+    if (BANK && ok && live) {
 #pragma unroll
       for (int b = 0; b < 16; ++b)
         m |= (cnt[(seg * 16 + b) * kVsG + src] != 0 ? 1u : 0u) << b;
     }
+    // plain order: the segment's entries as the walk found them
+    const uint16_t* seg_of = hits_of + (seg ? (live ? n_in_sm[src] : 0) : 0);
 #pragma unroll 1
     for (int c = 0; c < C; ++c) {
       unsigned wv[4] = {0u, 0u, 0u, 0u};
@@ -582,14 +611,18 @@ __global__ void __launch_bounds__(kVsG, 5)
         const int k = c * 8 + e;
         const int d = (lane + k) & 15;
         unsigned val = (dbase + (unsigned)((11 * d) & 15)) * 24u;   // dummy of bank d
-        if (k < ns && m) {
-          const unsigned rot = ((m >> d) | (m << (16 - d))) & 0xffffu;
-          const int b = (d + __ffs(rot) - 1) & 15;
-          const int bi = (seg * 16 + b) * kVsG + src;
-          const int left = cnt[bi];
-          val = (unsigned)hits_of[pos[bi] - left] * 24u;
-          cnt[bi] = (uint8_t)(left - 1);
-          if (left == 1) m &= ~(1u << b);
+        if (BANK) {
+          if (k < ns && m) {
+            const unsigned rot = ((m >> d) | (m << (16 - d))) & 0xffffu;
+            const int b = (d + __ffs(rot) - 1) & 15;
+            const int bi = (seg * 16 + b) * kVsG + src;
+            const int left = cnt[bi];
+            val = (unsigned)hits_of[pos[bi] - left] * 24u;
+            cnt[bi] = (uint8_t)(left - 1);
+            if (left == 1) m &= ~(1u << b);
+          }
+        } else if (ok && k < ns) {
+          val = (unsigned)seg_of[k] * 24u;
         }
         wv[e >> 1] |= val << (16 * (e & 1));
       }
@@ -871,7 +904,17 @@ __global__ void vls_refresh_kernel(long long n, const int32_t* __restrict__ perm
   unsigned long long b = (unsigned long long)__double_as_longlong(d2);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) b = max(b, __shfl_xor_sync(0xffffffffu, b, o));
-  if ((threadIdx.x & 31) == 0 && b) atomicMax(disp + slot, b);
+  // one atomic per block at most, and only where it would raise the running
+  // maximum (a plain read of the hot word first): half a million same-address
+  // atomics per launch cost 0.5 ms at 16.8M particles
+  __shared__ unsigned long long wmax[8];
+  if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = b;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int w = 1; w < 8; ++w) b = max(b, wmax[w]);
+    if (b > *reinterpret_cast<volatile unsigned long long*>(disp + slot)) atomicMax(disp + slot, b);
+  }
 }
 
 // rows_out[k] = rows_in[perm[k]] (3 doubles)
@@ -993,9 +1036,9 @@ size_t lmd_vls_build_smem(int32_t rows, int32_t cap_entries) {
 int lmd_vls_build(const lmd_grid* g, double rin2, double rl2, int64_t n_owned, int32_t rows,
                   const double* pos_rows, const int32_t* fs_own, const int32_t* o_count,
                   const int32_t* fs_img, const int32_t* h_count, const int32_t* groups,
-                  int64_t max_groups, int32_t cap_chunks, int32_t cap_entries, void* nbr,
-                  int32_t* seg_chunks, uint8_t* slotmap, int32_t* count, int32_t* count_half,
-                  int32_t* info, void* stream) {
+                  int64_t max_groups, int32_t cap_chunks, int32_t cap_entries, int32_t bank_order,
+                  void* nbr, int32_t* seg_chunks, uint8_t* slotmap, int32_t* count,
+                  int32_t* count_half, int32_t* info, void* stream) {
   if (n_owned <= 0 || max_groups <= 0) return LMD_OK;
   if (cap_entries < 8 || cap_entries > 255 || cap_entries % 8 || !(rin2 <= rl2))
     return LMD_ERR_CONFIG;
@@ -1004,11 +1047,13 @@ int lmd_vls_build(const lmd_grid* g, double rin2, double rl2, int64_t n_owned, i
   if (rows <= 0 || rows > kVsMaxRows + 64 || (uintptr_t)pos_rows % 16) return LMD_ERR_CONFIG;
   cudaStream_t s = (cudaStream_t)stream;
   const GridK k = make_gridk(g);
-  const size_t smem = lmd_vls_build_smem(rows, cap_entries);
-  cudaError_t e = cudaFuncSetAttribute(vls_build_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  // the bucket counters exist only for the bank order
+  const size_t smem = (size_t)build_area(rows, cap_entries) + (bank_order ? 2 * 32 * kVsG : 0);
+  auto kern = bank_order ? vls_build_kernel<true> : vls_build_kernel<false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
   if (e != cudaSuccess) return set_cuda_error(e);
-  vls_build_kernel<<<(unsigned)max_groups, kVsG, smem, s>>>(
+  kern<<<(unsigned)max_groups, kVsG, smem, s>>>(
       (int)k.t0, (int)k.t1, groups, info, pos_rows, fs_own, o_count, fs_img, h_count, rin2, rl2,
       build_area(rows, cap_entries), cap_chunks, cap_entries, (int4*)nbr, seg_chunks, slotmap,
       count, count_half, info);

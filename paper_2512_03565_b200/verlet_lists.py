@@ -542,8 +542,8 @@ class VerletListContainer:
             N.call("lmd_vls_build", self.grid, rin * rin, rl * rl, n, plan["rows"],
                    N.ptr(self._build_rows), N.ptr(plan["fs_own"]), N.ptr(self._o_count),
                    N.ptr(plan["fs_img"]), N.ptr(self._h_count), N.ptr(plan["groups"]), ng,
-                   cap_chunks, cap, N.ptr(nbr), N.ptr(segc), N.ptr(slotmap), N.ptr(count),
-                   N.ptr(half), N.ptr(info), s)
+                   cap_chunks, cap, 1 if key[2] >= 0 else 0, N.ptr(nbr), N.ptr(segc),
+                   N.ptr(slotmap), N.ptr(count), N.ptr(half), N.ptr(info), s)
             chunks_seen, ent_seen = info[3:5].tolist()
             if ent_seen <= cap and chunks_seen <= cap_chunks:
                 break

@@ -183,3 +183,4 @@ def test_vl_refresh_and_check_decides_like_needs_rebuild():
     cont.rebuild(buf)
     cont.steps_since_rebuild = 2
     assert cont.refresh_and_check(buf) is True
+
