@@ -81,6 +81,14 @@ class VerletListContainer:
         # the build (decided on the device from the refresh's displacement)
         self.segmented = True
         self.inner_skin = 0.1
+        # adaptive: when the last epoch ended with a displacement of at least
+        # inner_skin (the outer segment ran for most of its steps), the next
+        # lists are built as one segment (cheaper to run in full than two
+        # padded segments); decided at each rebuild from the displacement
+        # refresh_and_check last read
+        self.adaptive_inner = True
+        self._last_disp2 = None
+        self._inner_eff = self.inner_skin
         self._vls: dict = {}
         self._vls_plan = None
         self._vls_cap = None
@@ -162,6 +170,10 @@ class VerletListContainer:
         self._build_rows = self._rows.clone() if self.segmented else None
         self._vls.clear()
         self._vls_plan = None
+        one_segment = (self.adaptive_inner and self._last_disp2 is not None
+                       and self._last_disp2 >= float(self.inner_skin) ** 2)
+        self._inner_eff = float(self.params.skin) if one_segment else float(self.inner_skin)
+        self._last_disp2 = None
         if self._disp is None or self._disp.device != dev:
             self._disp = torch.zeros(2, dtype=torch.int64, device=dev)
         else:
@@ -330,9 +342,13 @@ class VerletListContainer:
             self.refresh(owned)
             return False
         if self.steps_since_rebuild >= self.rebuild_period:
+            if self._disp_slot >= 0:   # the epoch's last displacement, for the next lists
+                self._last_disp2 = self._disp[self._disp_slot:self._disp_slot + 1].view(
+                    torch.float64).item()
             return True
         self.refresh(owned)
         d2 = self._disp[self._disp_slot:self._disp_slot + 1].view(torch.float64).item()
+        self._last_disp2 = d2
         return bool(d2 >= (0.5 * self.params.skin) ** 2)
 
     def refresh_owned(self, owned) -> None:
@@ -521,7 +537,7 @@ class VerletListContainer:
         n = self.n_owned
         maxg = plan["maxg"]
         rl = float(self.params.interaction_length)
-        rin = min(float(self.params.cutoff) + float(self.inner_skin), rl)
+        rin = min(float(self.params.cutoff) + float(self._inner_eff), rl)
         cap = self._vls_cap
         if cap is None:
             vol = float(np.prod(self.box.lengths))
@@ -572,7 +588,7 @@ class VerletListContainer:
     def _vls_half_delta2(self) -> float:
         # (delta / 2)^2 with a relative margin against rounding in the
         # displacement and distance evaluations
-        return (0.5 * float(self.inner_skin) * (1.0 - 1e-9)) ** 2
+        return (0.5 * float(self._inner_eff) * (1.0 - 1e-9)) ** 2
 
     def gpu_lane_stats(self, pattern, newton3: bool = False):
         """(lane_steps, active_lanes) of the force kernel over the current

@@ -217,3 +217,39 @@ def test_sparse_states_with_groups_over_many_cells(rng, rho):
         cont.refresh(buf)
         _check(cont, buf, pos, span, True, params, n3)
         assert cont._vls_for("v_by_one", n3) is not None
+
+
+def test_adaptive_single_segment_after_a_long_epoch(rng):
+    """An epoch that ended with a displacement of at least inner_skin (the
+    outer segment ran for most of its steps) is followed by one-segment lists;
+    a short epoch by two segments again.  Same results either way."""
+    pos, span = _state(rng, 5000, 0.8)
+    params = LJParams(cutoff=2.5, skin=0.3)
+    box = SimulationBox.cube(span, periodic=True)
+    cont = B.VerletListContainer(box, params, rebuild_period=1000)
+    buf = ParticleBuffer.from_positions(pos, device="cuda")
+    cont.rebuild(buf)
+    cont.refresh(buf)
+    cont.ensure_lists("v_by_one", False)
+    vls = cont._vls_for("v_by_one", False)
+    ng = vls["plan"]["ngroups"]
+    assert int(vls["segc"][: 8 * ng].view(-1, 2)[:, 1].sum()) > 0      # two segments
+    buf.pos_x[17] += 0.16                                              # >= skin / 2: rebuild due
+    assert cont.refresh_and_check(buf) is True
+    cont.rebuild(buf)
+    cont.refresh(buf)
+    now = buf.positions().cpu().numpy()
+    _check(cont, buf, now, span, True, params, False)
+    vls = cont._vls_for("v_by_one", False)
+    ng = vls["plan"]["ngroups"]
+    assert int(vls["segc"][: 8 * ng].view(-1, 2)[:, 1].sum()) == 0     # one segment
+    buf.pos_x[17] += 0.01                                              # a short epoch
+    assert cont.refresh_and_check(buf) is False
+    cont.steps_since_rebuild = 1000
+    assert cont.refresh_and_check(buf) is True                         # the period rule
+    cont.rebuild(buf)
+    cont.refresh(buf)
+    _check(cont, buf, buf.positions().cpu().numpy(), span, True, params, False)
+    vls = cont._vls_for("v_by_one", False)
+    ng = vls["plan"]["ngroups"]
+    assert int(vls["segc"][: 8 * ng].view(-1, 2)[:, 1].sum()) > 0
