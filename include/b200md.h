@@ -375,6 +375,22 @@ int lmd_vls_force(int newton3, int flags, const lmd_lj* lj, int64_t n_owned, int
                   const uint8_t* slotmap, int32_t cap_chunks, const uint64_t* disp,
                   double half_delta2, const int32_t* out_perm, double* fx, double* fy,
                   double* fz, double* ev_scratch, lmd_stats* stats, void* stream);
+/* One force phase without lists, for a neighbour structure that is used once
+ * (the reference's force_phase builds its container per call,
+ * driver.py:107-129): per group, the candidates are walked with the
+ * reference's exact r2 (executor.py:93-94), the list lengths within rc + skin
+ * are counted into count / count_half (the Verlet-list statistics), the
+ * candidates inside the cutoff are kept in `scratch` (n_groups * 128 *
+ * cap_entries uint16) and evaluated.  info[4] = most entries a lane kept
+ * (call again with a larger cap_entries when above it).  Same pairs, forces
+ * and statistics as lmd_vls_build + lmd_vls_force. */
+int lmd_vls_direct(const lmd_grid* g, int newton3, int flags, const lmd_lj* lj, int64_t n_owned,
+                   int32_t rows, const double* pos_rows, const int32_t* fs_own,
+                   const int32_t* o_count, const int32_t* fs_img, const int32_t* h_count,
+                   const int32_t* groups, int64_t n_groups, int32_t cap_entries, void* scratch,
+                   const int32_t* out_perm, double* fx, double* fy, double* fz,
+                   double* ev_scratch, lmd_stats* stats, int32_t* count, int32_t* count_half,
+                   int32_t* info, void* stream);
 int lmd_vls_reduce_ev(int64_t n_groups, const double* ev_scratch, lmd_stats* stats, void* stream);
 int lmd_vls_refresh(int64_t n, const int32_t* perm, const double* x, const double* y,
                     const double* z, double* rows, const double* build_rows, uint64_t* disp,

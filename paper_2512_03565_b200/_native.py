@@ -186,6 +186,8 @@ _sig("lmd_vls_build", _INT, C.POINTER(Grid), _D, _D, _I64, _I32, _VP, _VP, _VP, 
 _sig("lmd_vls_ev_slots", _I64, _I64)
 _sig("lmd_vls_force", _INT, _INT, _INT, C.POINTER(LJ), _I64, _I32, _VP, _VP, _I64, _VP, _I64,
      _VP, _VP, _VP, _I32, _VP, _D, _VP, _VP, _VP, _VP, _VP, _VP, _VP)
+_sig("lmd_vls_direct", _INT, C.POINTER(Grid), _INT, _INT, C.POINTER(LJ), _I64, _I32, _VP, _VP,
+     _VP, _VP, _VP, _VP, _I64, _I32, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP)
 _sig("lmd_vls_reduce_ev", _INT, _I64, _VP, _VP, _VP)
 _sig("lmd_vls_refresh", _INT, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _I32, _VP)
 _sig("lmd_vls_gather_rows", _INT, _I64, _VP, _VP, _VP, _VP)

@@ -905,6 +905,178 @@ __global__ void __launch_bounds__(kVsG, OCC)
   }
 }
 
+// ------------------------------------------------------------ direct (K4d)
+// One force phase without lists, for a structure that is used once
+// (force_phase on a temporary container, driver.py:107-129): one block per
+// group stages the group's rows as the force kernel does, every lane walks
+// the union of its warp's candidate ranges with the reference's exact r2
+// (unfused, FP64: every decision is the reference's without a band), counts
+// its list lengths (r2 < rl^2: the Verlet-list statistics) and appends the
+// candidates inside the cutoff to its stretch of a scratch area; then every
+// lane evaluates its own hits from shared memory.  Same pairs, forces (to
+// summation order) and statistics as list build + force kernel.
+template <bool EV, int N3>
+__global__ void __launch_bounds__(kVsG, 5)
+    vls_direct_kernel(int t0, int t1, const int32_t* __restrict__ groups,
+                      const double* __restrict__ rows, const int32_t* __restrict__ fso,
+                      const int32_t* __restrict__ oc, const int32_t* __restrict__ fsi,
+                      const int32_t* __restrict__ hc, double rl2, LJK k, int cap_ent,
+                      uint16_t* __restrict__ scratch, const int32_t* __restrict__ out_perm,
+                      double* __restrict__ fx, double* __restrict__ fy, double* __restrict__ fz,
+                      double* __restrict__ ev, lmd_stats* __restrict__ stats,
+                      int32_t* __restrict__ count, int32_t* __restrict__ count_half,
+                      int32_t* __restrict__ info) {
+  extern __shared__ __align__(128) double sm_d[];
+  double* xs = sm_d;
+  __shared__ unsigned long long bar;
+  __shared__ int blk_stat[4];
+  const int g = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int t = g * (kVsG / 32) + w;
+  const int32_t* rec = groups + (long long)g * kVsRec;
+  if (tid == 0) mbar_init(&bar, 1);
+  if (tid < 4) blk_stat[tid] = 0;
+  vls_dummies(rec, xs);
+  __syncthreads();
+  vls_stage(rec, rows, xs, &bar);
+  const int cnt_p = rec[kVsCnt], p0 = rec[kVsP0];
+  const bool active = tid < cnt_p;
+  const int p = p0 + tid;
+  const int irow = rec[kVsSelf] + tid;
+  const long long rowbase = (long long)rec[kVsRow] * t0;
+  const unsigned hb_off = (unsigned)rec[kVsHb];   // first image row (local)
+  uint16_t* hits = scratch + ((long long)g * kVsG + tid) * cap_ent;
+  int cx = rec[kVsXa];
+  if (active) {
+    const int xa = cx, xb = rec[kVsXb];
+#pragma unroll 4
+    for (int x = xa; x < xb; ++x) cx += p >= fso[rowbase + x] + oc[rowbase + x] ? 1 : 0;
+  }
+  unsigned lb[kVsRuns];
+#pragma unroll
+  for (int q = 0; q < kVsRuns; ++q) {
+    const int v = q / 9, dz = (q % 9) / 3 - 1, dy = q % 3 - 1;
+    lb[q] = 0u;
+    if (active && rec[kVsLen + q]) {
+      const int32_t* fs = v ? fsi : fso;
+      const int32_t* cc = v ? hc : oc;
+      const long long nb = rowbase + (long long)t0 * (dy + (long long)t1 * dz);
+      const int off = rec[kVsBase + q] - rec[kVsStart + q];
+      const int l0 = fs[nb + cx - 1] + off;
+      const int l1 = fs[nb + cx + 1] + cc[nb + cx + 1] + off;
+      lb[q] = (unsigned)l0 | ((unsigned)l1 << 16);
+    }
+  }
+  const unsigned dummy = (unsigned)((rec[kVsS] + 15) & ~15);   // a far-away row
+  mbar_wait(&bar, 0);
+  double px = -1.0e30, py = -1.0e30, pz = -1.0e30;
+  if (active) {
+    px = xs[3 * irow];
+    py = xs[3 * irow + 1];
+    pz = xs[3 * irow + 2];
+  }
+  // 1. walk (warp-uniform j, broadcast loads): exact r2; a candidate outside
+  //    the lane's own 3 cells is farther than rl, so the distance decides
+  unsigned n_hit = 0;
+  int n_list = 0, n_half = 0;
+  uint16_t* hbase = hits;
+  asm volatile("" : "+l"(hbase));
+#pragma unroll 1
+  for (int q = 0; q < kVsRuns; ++q) {
+    const int l0 = (int)(lb[q] & 0xffffu), l1 = (int)(lb[q] >> 16);
+    const int u0 = __reduce_min_sync(0xffffffffu, l1 > l0 ? l0 : 0x7fffffff);
+    const int u1 = __reduce_max_sync(0xffffffffu, l1 > l0 ? l1 : 0);
+#pragma unroll 2
+    for (int j = u0; j < u1; ++j) {
+      const double r2 = r2_exact(px - xs[3 * j], py - xs[3 * j + 1], pz - xs[3 * j + 2]);
+      const bool other = j != irow;
+      n_list += (other && r2 < rl2) ? 1 : 0;
+      n_half += (j > irow && r2 < rl2) ? 1 : 0;
+      const bool hit = other && r2 < k.rc2;
+      asm volatile(
+          "{\n .reg .pred p, q;\n"
+          " setp.ne.u32 p, %3, 0;\n"
+          " setp.lt.and.u32 q, %0, %4, p;\n"
+          " @q st.global.u16 [%1], %2;\n"
+          " @p add.u32 %0, %0, 1;\n}"
+          : "+r"(n_hit)
+          : "l"(hbase + n_hit), "h"((unsigned short)j), "r"((unsigned)hit), "r"((unsigned)cap_ent)
+          : "memory");
+    }
+  }
+  if (active) {
+    count[p] = n_list;
+    count_half[p] = n_half;
+  }
+  const int hit_max = __reduce_max_sync(0xffffffffu, (int)n_hit);
+  if (lane == 0 && hit_max > *reinterpret_cast<volatile int32_t*>(info + 4))
+    atomicMax(info + 4, hit_max);
+  // 2. the lane's hits, 8 per 128-bit read; past its own count a lane takes
+  //    the far-away dummy row (zero force by the masked reciprocal)
+  VsAcc a = {0.0, 0.0, 0.0, 0.0, 0.0, 0, 0};
+  if (hit_max <= cap_ent) {   // (else the host retries with the observed maximum)
+    const uint4* hits8 = reinterpret_cast<const uint4*>(hits);
+    uint4 vn = hits8[0];
+#pragma unroll 1
+    for (int e0 = 0; e0 < hit_max; e0 += 8) {
+      const uint4 v = vn;
+      if (e0 + 8 < hit_max) vn = hits8[min((e0 >> 3) + 1, (cap_ent >> 3) - 1)];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const bool valid = e0 + e < (int)n_hit;
+        const unsigned wv = e < 2 ? v.x : e < 4 ? v.y : e < 6 ? v.z : v.w;
+        const unsigned j = valid ? ((e & 1) ? wv >> 16 : wv & 0xffffu) : dummy;
+        const double dx = px - xs[3 * j], dy = py - xs[3 * j + 1], dz = pz - xs[3 * j + 2];
+        const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+        double u3;
+        const double f = vs_force_scalar(r2, valid, k, u3);
+        a.ax = fma(f, dx, a.ax);
+        a.ay = fma(f, dy, a.ay);
+        a.az = fma(f, dz, a.az);
+        if (EV) {
+          a.e = fma(0.5 * u3, fma(k.e12, u3, -k.e6), a.e);
+          a.v = fma(0.5 * f, r2, a.v);
+        }
+        a.pairs += valid ? 1 : 0;
+        if (N3 == 2) a.halo += (valid && j >= hb_off) ? 1 : 0;
+      }
+    }
+  }
+  // a coincident pair (r2 == 0 inside the cutoff): the numba -1 sentinel
+  const int overlap = (active && !(isfinite(a.ax) && isfinite(a.ay) && isfinite(a.az))) ? 1 : 0;
+  if (active) {
+    const int o = out_perm ? out_perm[p] : p;
+    fx[o] = a.ax;
+    fy[o] = a.ay;
+    fz[o] = a.az;
+  }
+  const int wp = __reduce_add_sync(0xffffffffu, a.pairs);
+  const int wh = __reduce_add_sync(0xffffffffu, a.halo);
+  const int wo = __any_sync(0xffffffffu, overlap);
+  if (EV) {
+    const double e = warp_sum(a.e), v = warp_sum(a.v);
+    if (lane == 0) {
+      ev[2 * (long long)t] = e;
+      ev[2 * (long long)t + 1] = v;
+    }
+  }
+  if (lane == 0) {
+    if (wp) atomicAdd(&blk_stat[0], wp);
+    if (wh) atomicAdd(&blk_stat[1], wh);
+    if (wo) atomicOr(&blk_stat[2], 1);
+    __threadfence_block();
+    if (atomicAdd(&blk_stat[3], 1) == kVsG / 32 - 1) {
+      __threadfence_block();
+      const int bp = *reinterpret_cast<volatile int*>(&blk_stat[0]);
+      const int bh = *reinterpret_cast<volatile int*>(&blk_stat[1]);
+      const int bo = *reinterpret_cast<volatile int*>(&blk_stat[2]);
+      if (bp) atomicAdd((unsigned long long*)&stats->pair_interactions, (unsigned long long)bp);
+      if (bh) atomicAdd((unsigned long long*)&stats->pairs_owned_halo, (unsigned long long)bh);
+      if (bo) atomicOr(&stats->overlap, 1);
+    }
+  }
+}
+
 // ---------------------------------------------------------------- refresh
 // rows[k] = positions of particle perm[k] (x, y, z), and with disp the
 // largest squared displacement from build[k], max-reduced into disp[slot]
@@ -1142,6 +1314,47 @@ int lmd_vls_force(int newton3, int flags, const lmd_lj* lj, int64_t n_owned, int
 #undef LMD_VSF_O
 #undef LMD_VSF
   if (rc != LMD_OK) return rc;
+  if (ev && !(flags & LMD_FLAG_DEFER_EV))
+    return reduce_ev(ev_scratch, lmd_vls_ev_slots(n_groups), stats, s);
+  return LMD_OK;
+}
+
+int lmd_vls_direct(const lmd_grid* g, int newton3, int flags, const lmd_lj* lj, int64_t n_owned,
+                   int32_t rows, const double* pos_rows, const int32_t* fs_own,
+                   const int32_t* o_count, const int32_t* fs_img, const int32_t* h_count,
+                   const int32_t* groups, int64_t n_groups, int32_t cap_entries, void* scratch,
+                   const int32_t* out_perm, double* fx, double* fy, double* fz,
+                   double* ev_scratch, lmd_stats* stats, int32_t* count, int32_t* count_half,
+                   int32_t* info, void* stream) {
+  if (n_owned <= 0 || n_groups <= 0) return LMD_OK;
+  if (newton3 != 0 && newton3 != 2) return LMD_ERR_CONFIG;
+  if (cap_entries < 8 || cap_entries % 8 || cap_entries > 4096) return LMD_ERR_CONFIG;
+  if (rows <= 0 || rows > kVsMaxRows + 64 || (uintptr_t)pos_rows % 16) return LMD_ERR_CONFIG;
+  const bool ev = (flags & LMD_FLAG_ENERGY) != 0;
+  if (ev && !ev_scratch) return LMD_ERR_CONFIG;
+  cudaStream_t s = (cudaStream_t)stream;
+  const LJK k = make_ljk(lj);
+  const GridK gk = make_gridk(g);
+  const double rl = lj->cutoff + lj->skin;
+  const size_t smem = stage_bytes(rows);
+#define LMD_VSD(EVB, N3B)                                                                       \
+  {                                                                                             \
+    auto kern = vls_direct_kernel<EVB, N3B>;                                                    \
+    cudaError_t e =                                                                             \
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
+    if (e != cudaSuccess) return set_cuda_error(e);                                             \
+    kern<<<(unsigned)n_groups, kVsG, smem, s>>>(                                                \
+        (int)gk.t0, (int)gk.t1, groups, pos_rows, fs_own, o_count, fs_img, h_count, rl * rl, k, \
+        cap_entries, (uint16_t*)scratch, out_perm, fx, fy, fz, ev_scratch, stats, count,        \
+        count_half, info);                                                                      \
+  }
+  if (ev) {
+    if (newton3) LMD_VSD(true, 2) else LMD_VSD(true, 0)
+  } else {
+    if (newton3) LMD_VSD(false, 2) else LMD_VSD(false, 0)
+  }
+#undef LMD_VSD
+  LMD_CHECK_LAUNCH();
   if (ev && !(flags & LMD_FLAG_DEFER_EV))
     return reduce_ev(ev_scratch, lmd_vls_ev_slots(n_groups), stats, s);
   return LMD_OK;

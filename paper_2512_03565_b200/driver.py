@@ -51,11 +51,25 @@ def force_phase(owned, box, params, config: Configuration, vector_width: int,
         cont.bank_rounds = -1
     cont.rebuild(dev_owned)
     cont.refresh(dev_owned)
-    stats = cont.compute_forces(config.traversal, config.newton3, as_pattern(config.pattern),
-                                vector_width, energy=energy)
+    stats = _compute_once(cont, config, vector_width, energy)
     cont.collect_forces(dev_owned)
     if dev_owned is not owned:
         _write_forces_back(owned, dev_owned)
+    return stats
+
+
+def _compute_once(cont, config, vector_width: int, energy: bool) -> KernelStats:
+    """The force computation of a container built for this one call: where
+    the container has a list-free kernel for it (Verlet lists, N x 1) that one
+    runs, else the regular ``compute_forces``."""
+    once = getattr(cont, "compute_forces_once", None)
+    stats = None
+    if once is not None:
+        stats = once(config.traversal, config.newton3, as_pattern(config.pattern),
+                     vector_width, energy=energy)
+    if stats is None:
+        stats = cont.compute_forces(config.traversal, config.newton3,
+                                    as_pattern(config.pattern), vector_width, energy=energy)
     return stats
 
 
@@ -89,8 +103,7 @@ def force_phase_bricks(owned, dec, params, config: Configuration, vector_width: 
         cont.bank_rounds = -1
     cont.rebuild(dev_owned, ghosts)
     cont.refresh(dev_owned, ghosts)
-    stats = cont.compute_forces(config.traversal, config.newton3, as_pattern(config.pattern),
-                                vector_width, energy=energy)
+    stats = _compute_once(cont, config, vector_width, energy)
     cont.collect_forces(dev_owned)
     if dev_owned is not owned:
         _write_forces_back(owned, dev_owned)

@@ -841,6 +841,72 @@ class VerletListContainer:
                            pair_interactions=self.pair_count(st, newton3), epot=st.epot,
                            virial=st.virial)
 
+    def compute_forces_once(self, traversal, newton3: bool, pattern, vector_width: int,
+                            energy: bool = False):
+        """``compute_forces`` for a container that is used once (the one-shot
+        ``force_phase``): the list-free kernel ``lmd_vls_direct`` walks the
+        candidates of the row-aligned groups, counts the list lengths for the
+        statistics and evaluates the pairs inside the cutoff -- no lists are
+        written.  Same KernelStats and forces (to summation order) as
+        ``compute_forces``.  Returns None where it does not apply (other
+        orders, half-list Newton3, groups too large to stage): the caller
+        then takes ``compute_forces``."""
+        from .traversals import TraversalKind, as_traversal
+        validate_vector_width(vector_width)
+        if as_traversal(traversal) is not TraversalKind.VL:
+            raise ConfigurationError(f"{traversal} traversal requires the verlet-list container")
+        pattern = as_pattern(pattern)
+        mode = self._kernel_n3(newton3)
+        if (not self.segmented or self._rows is None or mode == 1 or not self.n_owned
+                or self._staged_for(pattern, False) == 0 or self._lists):
+            return None
+        plan = self._vls_plan_groups()
+        if plan["rows"] == 0:
+            return None
+        dev = self._rows.device
+        n, ng = self.n_owned, plan["ngroups"]
+        rc = float(self.params.cutoff)
+        vol = float(np.prod(self.box.lengths))
+        est = (n + self.n_halo) / vol * (4.0 / 3.0) * np.pi * rc ** 3
+        cap = int(est * 1.4 + 24)
+        stats_t = N.new_stats(dev)
+        slots = int(N.load().lmd_vls_ev_slots(ng))
+        ev_t = torch.empty(2 * max(slots, 1), dtype=torch.float64, device=dev) if energy else None
+        count = torch.zeros(max(n, 1), dtype=torch.int32, device=dev)
+        half = torch.zeros(max(n, 1), dtype=torch.int32, device=dev)
+        info = plan["info"]
+        while True:
+            cap = (cap + 7) // 8 * 8
+            scratch = torch.empty(ng * 128 * cap, dtype=torch.int16, device=dev)
+            info[3:5].zero_()
+            stats_t.zero_()
+            N.call("lmd_vls_direct", self.grid, mode, N.FLAG_ENERGY if energy else 0,
+                   N.make_lj(self.params), n, plan["rows"], N.ptr(self._rows),
+                   N.ptr(plan["fs_own"]), N.ptr(self._o_count), N.ptr(plan["fs_img"]),
+                   N.ptr(self._h_count), N.ptr(plan["groups"]), ng, cap, N.ptr(scratch), None,
+                   N.ptr(self._fx), N.ptr(self._fy), N.ptr(self._fz),
+                   N.ptr(ev_t) if energy else None, N.ptr(stats_t), N.ptr(count), N.ptr(half),
+                   N.ptr(info), N.stream())
+            seen = int(info[4].item())
+            if seen <= cap:
+                break
+            if seen > 4096:
+                return None
+            cap = seen + 8
+        del scratch
+        self._collected_into = None
+        self._counts[False] = count
+        if self.n3_mode == "full_list":
+            self._counts[True] = half
+        inv, lane_slots, useful = self.vl_stats(newton3, pattern, vector_width)
+        st = N.read_stats(stats_t)
+        if st.overlap:
+            raise ParticleOverlapError("zero distance between interacting particles")
+        return KernelStats(kernel_invocations=inv, lane_slots=lane_slots,
+                           useful_interactions=useful,
+                           pair_interactions=self.pair_count(st, newton3), epot=st.epot,
+                           virial=st.virial)
+
     def collect_forces(self, owned) -> None:
         if self._collected_into is not None and owned is self._collected_into:
             self._collected_into = None        # the kernel already wrote them

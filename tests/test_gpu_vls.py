@@ -253,3 +253,52 @@ def test_adaptive_single_segment_after_a_long_epoch(rng):
     vls = cont._vls_for("v_by_one", False)
     ng = vls["plan"]["ngroups"]
     assert int(vls["segc"][: 8 * ng].view(-1, 2)[:, 1].sum()) > 0
+
+
+@pytest.mark.parametrize("n3", [False, True])
+@pytest.mark.parametrize("periodic", [True, False])
+def test_list_free_one_shot_kernel_matches_oracle(rng, periodic, n3):
+    """The one-shot path of force_phase (lmd_vls_direct: no lists written)
+    gives the oracle's pair counts, list statistics, forces, energy and
+    virial, and the same forces as the list path to summation order."""
+    pos, span = _state(rng, 6000, 0.8)
+    params = LJParams(cutoff=2.5, skin=0.3)
+    box = SimulationBox.cube(span, periodic=periodic)
+    of, ost = O.force_phase_vl(pos, np.zeros(3), np.full(3, span), [periodic] * 3, params, n3,
+                               "v_by_one", 8)
+    cont = B.VerletListContainer(box, params)
+    buf = ParticleBuffer.from_positions(pos, device="cuda")
+    cont.rebuild(buf)
+    cont.refresh(buf)
+    st = cont.compute_forces_once("vl", n3, PatternKind.V_BY_ONE, 8, energy=True)
+    assert st is not None and not cont._lists and not cont._vls        # nothing was built
+    cont.collect_forces(buf)
+    f = buf.forces().cpu().numpy()
+    assert (st.kernel_invocations, st.lane_slots, st.useful_interactions,
+            st.pair_interactions) == ost.as_tuple()
+    assert forces_close(f, of)
+    assert abs(st.epot - ost.epot) <= 1e-12 * abs(ost.epot)
+    assert abs(st.virial - ost.virial) <= 1e-12 * abs(ost.virial)
+    # and through the public entry point
+    buf2 = ParticleBuffer.from_positions(pos, device="cuda")
+    st2 = B.force_phase(buf2, box, params, B.Configuration.parse(
+        f"vl,vl,{str(n3).lower()},v_by_one"), 8)
+    assert st2.pair_interactions == ost.pair_interactions
+    assert np.array_equal(buf2.forces().cpu().numpy(), f)
+
+
+def test_list_free_kernel_capacity_retry_and_overlap(rng):
+    pos, span = _state(rng, 3000, 0.9)
+    params = LJParams(cutoff=3.2, skin=0.3)            # more hits than the first guess
+    box = SimulationBox.cube(span, periodic=True)
+    of, ost = O.force_phase_vl(pos, np.zeros(3), np.full(3, span), [True] * 3, params, False,
+                               "v_by_one", 8)
+    buf = ParticleBuffer.from_positions(pos, device="cuda")
+    st = B.force_phase(buf, box, params, B.Configuration.parse("vl,vl,false,v_by_one"), 8)
+    assert st.pair_interactions == ost.pair_interactions
+    assert forces_close(buf.forces().cpu().numpy(), of)
+    pos2 = pos.copy()
+    pos2[11] = pos2[10]                                # coincident particles
+    buf = ParticleBuffer.from_positions(pos2, device="cuda")
+    with pytest.raises(B.ParticleOverlapError):
+        B.force_phase(buf, box, params, B.Configuration.parse("vl,vl,false,v_by_one"), 8)

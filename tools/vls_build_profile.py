@@ -62,3 +62,22 @@ for bank in banks:
           "info", vls["plan"]["info"].tolist())
     del cont, buf
     torch.cuda.empty_cache()
+
+# the list-free one-shot kernel (force_phase's path) on the same state
+buf = B.ParticleBuffer.from_positions(pos, device="cuda")
+for rep in range(3):
+    cont = B.make_container("vl", box, params)
+    cont.rebuild(buf)
+    cont.refresh(buf)
+    torch.cuda.synchronize()
+    e0, e1 = (torch.cuda.Event(enable_timing=True) for _ in range(2))
+    e0.record()
+    st1 = cont.compute_forces_once("vl", False, "v_by_one", 8)
+    e1.record()
+    torch.cuda.synchronize()
+    print(f"side {side} one-shot (plan + list-free kernel + statistics): "
+          f"{e0.elapsed_time(e1):.3f} ms, pairs {st1.pair_interactions}", flush=True)
+cont.collect_forces(buf)
+if ref is not None:
+    print("max force difference one-shot vs lists / max |F|:",
+          float((buf.forces() - ref).abs().max()) / float(ref.abs().max()))
