@@ -377,13 +377,16 @@ int lmd_vls_force(int newton3, int flags, const lmd_lj* lj, int64_t n_owned, int
                   double* fz, double* ev_scratch, lmd_stats* stats, void* stream);
 /* One force phase without lists, for a neighbour structure that is used once
  * (the reference's force_phase builds its container per call,
- * driver.py:107-129): per group, the candidates are walked with the
- * reference's exact r2 (executor.py:93-94), the list lengths within rc + skin
- * are counted into count / count_half (the Verlet-list statistics), the
- * candidates inside the cutoff are kept in `scratch` (n_groups * 128 *
- * cap_entries uint16) and evaluated.  info[4] = most entries a lane kept
- * (call again with a larger cap_entries when above it).  Same pairs, forces
- * and statistics as lmd_vls_build + lmd_vls_force. */
+ * driver.py:107-129), in two kernels: the list build's walk alone (packed
+ * FP32; every candidate within rc + skin + the FP32 error bound is kept in
+ * `scratch`: n_groups * 128 * cap_entries uint16), then each lane takes its
+ * kept candidates through the reference's exact r2 (executor.py:93-94) from
+ * the staged FP64 rows: r2 < (rc + skin)^2 counts into count / count_half (the
+ * Verlet-list statistics), r2 < rc^2 is evaluated.  info[2] must hold the
+ * number of groups (as lmd_vls_plan leaves it); info[4] = most entries a lane
+ * kept (call again with a larger cap_entries when above it: nothing was
+ * evaluated).  Same pairs, forces and statistics as lmd_vls_build +
+ * lmd_vls_force. */
 int lmd_vls_direct(const lmd_grid* g, int newton3, int flags, const lmd_lj* lj, int64_t n_owned,
                    int32_t rows, const double* pos_rows, const int32_t* fs_own,
                    const int32_t* o_count, const int32_t* fs_img, const int32_t* h_count,

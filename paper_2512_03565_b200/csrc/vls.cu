@@ -65,6 +65,7 @@ constexpr int kVsMaxRows = 2704;  // 24 * (row + 15) < 65536: byte offsets (dumm
 // staged-row budget of a group: groups shrink (in steps of 32 particles)
 // until they stage at most this many rows, so 5 blocks (44 KB each) fit an SM
 constexpr int kVsBudget = 1840;
+constexpr int kVsRingBytes = 32 * kVsG;   // build: 16 hits of 2 B per lane
 enum : int {
   kVsP0 = 0, kVsCnt = 1, kVsS = 2, kVsHb = 3, kVsSelf = 4, kVsRow = 5, kVsXa = 6, kVsXb = 7,
   kVsStart = 8, kVsLen = 8 + kVsRuns, kVsBase = 8 + 2 * kVsRuns
@@ -279,7 +280,7 @@ __device__ __noinline__ int vls_exact_class(const double* __restrict__ rows, con
 //     shared memory the staged rows occupied.
 //  3. the group's particles are ranked by inner length (the slot map) and
 //     each emits its segments in its new lane's Latin-square bank order.
-template <bool BANK>
+template <int MODE>   // 0: plain entry order, 1: bank order, 2: the walk alone
 __global__ void __launch_bounds__(kVsG, 5)
     vls_build_kernel(int t0, int t1, const int32_t* __restrict__ groups,
                      const int32_t* __restrict__ info_in, const double* __restrict__ rows,
@@ -289,9 +290,13 @@ __global__ void __launch_bounds__(kVsG, 5)
                      int4* __restrict__ nbr, int32_t* __restrict__ segc,
                      uint8_t* __restrict__ slotmap, int32_t* __restrict__ count,
                      int32_t* __restrict__ count_half, int32_t* __restrict__ info) {
+  constexpr bool BANK = MODE == 1;
   extern __shared__ __align__(128) double sm_b[];
   uint16_t* sorted = reinterpret_cast<uint16_t*>(sm_b);    // hits by bucket (steps 2-3)
-  uint8_t* cnt = reinterpret_cast<uint8_t*>(sm_b) + area_bytes;  // [32 buckets][128]
+  // after the area: a 16-entry ring per lane for the walk's hits, then (bank
+  // order only) the bucket counters
+  uint8_t* ring_area = reinterpret_cast<uint8_t*>(sm_b) + area_bytes;   // [128][32 B]
+  uint8_t* cnt = ring_area + kVsRingBytes;                        // [32 buckets][128]
   uint8_t* pos = cnt + 32 * kVsG;                                 // [32 buckets][128]
   __shared__ int n_in_sm[kVsG], n_out_sm[kVsG], slot_sm[kVsG];
   __shared__ int run_st[kVsRuns], run_rb[kVsRuns + 1];
@@ -398,21 +403,38 @@ __global__ void __launch_bounds__(kVsG, 5)
   //    appended like a hit and dropped in step 2, which also classifies the
   //    entries (inner / outer / in the FP32 band around rl).
   unsigned n_ent = 0;  // entries appended (own row and band candidates included)
-  // the lane's stretch as one opaque 64-bit base (one IMAD.WIDE per address)
-  uint16_t* hbase = hits;
-  asm volatile("" : "+l"(hbase));
+  unsigned n_fl = 0;   // entries already flushed to the lane's stretch (multiple of 8)
+  // Hits go through a 16-entry ring in shared memory and reach the lane's
+  // stretch 8 at a time (one 16-B store): a 2-B global store per hit is one
+  // L2 request each -- 1.3e9 per build at 16.8M particles, and the L2 request
+  // rate, not the instruction count, then bounds the walk.
+  const unsigned ring = smem_u32(ring_area + tid * 32);
+  uint4* const stretch = reinterpret_cast<uint4*>(hits);
   auto test = [&](int j, float r2) {
-    // appended (predicated store and increment, no branch) when r2 < rl2_hi
-    // and the lane's stretch has room; classified in step 2
+    // appended (predicated store and increment, no branch) when r2 < rl2_hi;
+    // classified in step 2
+    const unsigned at = ring + ((n_ent & 15u) << 1);
     asm volatile(
-        "{\n .reg .pred p, q;\n"
+        "{\n .reg .pred p;\n"
         " setp.lt.f32 p, %3, %4;\n"
-        " setp.lt.and.u32 q, %0, %5, p;\n"
-        " @q st.global.u16 [%1], %2;\n"
+        " @p st.shared.u16 [%1], %2;\n"
         " @p add.u32 %0, %0, 1;\n}"
         : "+r"(n_ent)
-        : "l"(hbase + n_ent), "h"((unsigned short)j), "f"(r2), "f"(rl2_hi), "r"((unsigned)cap_ent)
+        : "r"(at), "h"((unsigned short)j), "f"(r2), "f"(rl2_hi)
         : "memory");
+  };
+  // called at least every 9 candidates (a lane holds at most 7 unflushed
+  // entries afterwards, so the ring never wraps onto them)
+  auto flush = [&](bool all) {
+    while (n_fl + 8u <= n_ent || (all && n_fl < n_ent)) {
+      uint4 v;
+      asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                   : "r"(ring + ((n_fl & 15u) << 1))
+                   : "memory");
+      if (n_fl + 8u <= (unsigned)cap_ent) stretch[n_fl >> 3] = v;
+      n_fl += 8u;
+    }
   };
   // rows jp (even) and jp + 1 with packed FP32 arithmetic
   auto pair = [&](int jp, bool m0, bool m1) {
@@ -423,9 +445,9 @@ __global__ void __launch_bounds__(kVsG, 5)
     if (m0) test(jp, __uint_as_float((unsigned)r));
     if (m1) test(jp + 1, __uint_as_float((unsigned)(r >> 32)));
   };
+  unsigned lbn = lb[0];
 #pragma unroll 1   // (lb[] lives in local memory: one L1 read per run; unrolling
                    // 18 copies of the walk overflows the instruction cache)
-  unsigned lbn = lb[0];
   for (int q = 0; q < kVsRuns; ++q) {
     const unsigned lbq = lbn;
     lbn = lb[min(q + 1, kVsRuns - 1)];   // one run ahead
@@ -441,15 +463,30 @@ __global__ void __launch_bounds__(kVsG, 5)
       pair(j - 1, false, true);
       ++j;
     }
-#pragma unroll 2
+#pragma unroll 1
+    for (; j + 7 < u1; j += 8) {
+      pair(j, true, true);
+      pair(j + 2, true, true);
+      pair(j + 4, true, true);
+      pair(j + 6, true, true);
+      flush(false);
+    }
     for (; j + 1 < u1; j += 2) pair(j, true, true);
     if (j < u1) pair(j, true, false);
+    flush(false);
   }
+  flush(true);
   const int ent_max = __reduce_max_sync(0xffffffffu, (int)n_ent);
   // (a plain read first: the running maximum settles after a few blocks, and
   // one same-address atomic per warp is what this avoids)
   if (lane == 0 && ent_max > *reinterpret_cast<volatile int32_t*>(info + 4))
     atomicMax(info + 4, ent_max);
+  if (MODE == 2) {
+    // the walk alone (the one-shot force phase evaluates the raw hits from
+    // the FP64 rows, lmd_vls_direct): the lane's raw count, then done
+    if (active) count[p] = (int)n_ent;
+    return;
+  }
   // a lane without room makes the whole build void (the host retries with
   // the observed maximum): flagged here, read by every warp after step 2
   const bool room = ent_max <= cap_ent;
@@ -907,29 +944,29 @@ __global__ void __launch_bounds__(kVsG, OCC)
 
 // ------------------------------------------------------------ direct (K4d)
 // One force phase without lists, for a structure that is used once
-// (force_phase on a temporary container, driver.py:107-129): one block per
-// group stages the group's rows as the force kernel does, every lane walks
-// the union of its warp's candidate ranges with the reference's exact r2
-// (unfused, FP64: every decision is the reference's without a band), counts
-// its list lengths (r2 < rl^2: the Verlet-list statistics) and appends the
-// candidates inside the cutoff to its stretch of a scratch area; then every
-// lane evaluates its own hits from shared memory.  Same pairs, forces (to
-// summation order) and statistics as list build + force kernel.
+// (force_phase on a temporary container, driver.py:107-129), in two kernels:
+// the list build's walk alone (vls_build_kernel<2>: packed FP32, every
+// candidate within rl + the FP32 error bound appended to the lane's stretch
+// of a scratch area, the own row included), then this kernel: one block per
+// group stages the group's FP64 rows as the force kernel does and every lane
+// takes its raw hits through the reference's exact r2 (unfused): r2 < rl^2
+// counts towards the list lengths (the Verlet-list statistics), r2 < rc^2 is
+// evaluated.  Same pairs, forces (to summation order) and statistics as list
+// build + force kernel.
 template <bool EV, int N3>
 __global__ void __launch_bounds__(kVsG, 5)
-    vls_direct_kernel(int t0, int t1, const int32_t* __restrict__ groups,
-                      const double* __restrict__ rows, const int32_t* __restrict__ fso,
-                      const int32_t* __restrict__ oc, const int32_t* __restrict__ fsi,
-                      const int32_t* __restrict__ hc, double rl2, LJK k, int cap_ent,
-                      uint16_t* __restrict__ scratch, const int32_t* __restrict__ out_perm,
-                      double* __restrict__ fx, double* __restrict__ fy, double* __restrict__ fz,
-                      double* __restrict__ ev, lmd_stats* __restrict__ stats,
-                      int32_t* __restrict__ count, int32_t* __restrict__ count_half,
-                      int32_t* __restrict__ info) {
+    vls_rawforce_kernel(const int32_t* __restrict__ groups, const double* __restrict__ rows,
+                        double rl2, LJK k, int cap_chunks, int cap_ent,
+                        const int4* __restrict__ scratch, const int32_t* __restrict__ out_perm,
+                        double* __restrict__ fx, double* __restrict__ fy, double* __restrict__ fz,
+                        double* __restrict__ ev, lmd_stats* __restrict__ stats,
+                        int32_t* __restrict__ count, int32_t* __restrict__ count_half,
+                        const int32_t* __restrict__ info) {
   extern __shared__ __align__(128) double sm_d[];
   double* xs = sm_d;
   __shared__ unsigned long long bar;
   __shared__ int blk_stat[4];
+  if (info[4] > cap_ent) return;   // the walk ran out of room: the host retries
   const int g = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int t = g * (kVsG / 32) + w;
@@ -939,35 +976,19 @@ __global__ void __launch_bounds__(kVsG, 5)
   vls_dummies(rec, xs);
   __syncthreads();
   vls_stage(rec, rows, xs, &bar);
-  const int cnt_p = rec[kVsCnt], p0 = rec[kVsP0];
+  const int cnt_p = rec[kVsCnt];
   const bool active = tid < cnt_p;
-  const int p = p0 + tid;
+  const int p = rec[kVsP0] + tid;
   const int irow = rec[kVsSelf] + tid;
-  const long long rowbase = (long long)rec[kVsRow] * t0;
-  const unsigned hb_off = (unsigned)rec[kVsHb];   // first image row (local)
-  uint16_t* hits = scratch + ((long long)g * kVsG + tid) * cap_ent;
-  int cx = rec[kVsXa];
-  if (active) {
-    const int xa = cx, xb = rec[kVsXb];
-#pragma unroll 4
-    for (int x = xa; x < xb; ++x) cx += p >= fso[rowbase + x] + oc[rowbase + x] ? 1 : 0;
-  }
-  unsigned lb[kVsRuns];
-#pragma unroll
-  for (int q = 0; q < kVsRuns; ++q) {
-    const int v = q / 9, dz = (q % 9) / 3 - 1, dy = q % 3 - 1;
-    lb[q] = 0u;
-    if (active && rec[kVsLen + q]) {
-      const int32_t* fs = v ? fsi : fso;
-      const int32_t* cc = v ? hc : oc;
-      const long long nb = rowbase + (long long)t0 * (dy + (long long)t1 * dz);
-      const int off = rec[kVsBase + q] - rec[kVsStart + q];
-      const int l0 = fs[nb + cx - 1] + off;
-      const int l1 = fs[nb + cx + 1] + cc[nb + cx + 1] + off;
-      lb[q] = (unsigned)l0 | ((unsigned)l1 << 16);
-    }
-  }
+  const unsigned hb_row = (unsigned)rec[kVsHb];   // first image row (local)
   const unsigned dummy = (unsigned)((rec[kVsS] + 15) & ~15);   // a far-away row
+  const int n_raw = active ? count[p] : 0;
+  // the lane's stretch, as the walk laid it out
+  const uint4* hits8 = reinterpret_cast<const uint4*>(
+      reinterpret_cast<const uint16_t*>(scratch + ((long long)t * cap_chunks) * 32) +
+      lane * cap_ent);
+  const int raw_max = __reduce_max_sync(0xffffffffu, n_raw);
+  uint4 vn = hits8[0];
   mbar_wait(&bar, 0);
   double px = -1.0e30, py = -1.0e30, pz = -1.0e30;
   if (active) {
@@ -975,72 +996,40 @@ __global__ void __launch_bounds__(kVsG, 5)
     py = xs[3 * irow + 1];
     pz = xs[3 * irow + 2];
   }
-  // 1. walk (warp-uniform j, broadcast loads): exact r2; a candidate outside
-  //    the lane's own 3 cells is farther than rl, so the distance decides
-  unsigned n_hit = 0;
+  VsAcc a = {0.0, 0.0, 0.0, 0.0, 0.0, 0, 0};
   int n_list = 0, n_half = 0;
-  uint16_t* hbase = hits;
-  asm volatile("" : "+l"(hbase));
 #pragma unroll 1
-  for (int q = 0; q < kVsRuns; ++q) {
-    const int l0 = (int)(lb[q] & 0xffffu), l1 = (int)(lb[q] >> 16);
-    const int u0 = __reduce_min_sync(0xffffffffu, l1 > l0 ? l0 : 0x7fffffff);
-    const int u1 = __reduce_max_sync(0xffffffffu, l1 > l0 ? l1 : 0);
-#pragma unroll 2
-    for (int j = u0; j < u1; ++j) {
-      const double r2 = r2_exact(px - xs[3 * j], py - xs[3 * j + 1], pz - xs[3 * j + 2]);
-      const bool other = j != irow;
-      n_list += (other && r2 < rl2) ? 1 : 0;
-      n_half += (j > irow && r2 < rl2) ? 1 : 0;
-      const bool hit = other && r2 < k.rc2;
-      asm volatile(
-          "{\n .reg .pred p, q;\n"
-          " setp.ne.u32 p, %3, 0;\n"
-          " setp.lt.and.u32 q, %0, %4, p;\n"
-          " @q st.global.u16 [%1], %2;\n"
-          " @p add.u32 %0, %0, 1;\n}"
-          : "+r"(n_hit)
-          : "l"(hbase + n_hit), "h"((unsigned short)j), "r"((unsigned)hit), "r"((unsigned)cap_ent)
-          : "memory");
+  for (int e0 = 0; e0 < raw_max; e0 += 8) {
+    const uint4 v = vn;
+    if (e0 + 8 < raw_max) vn = hits8[min((e0 >> 3) + 1, (cap_ent >> 3) - 1)];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const unsigned wv = e < 2 ? v.x : e < 4 ? v.y : e < 6 ? v.z : v.w;
+      const unsigned jr = (e & 1) ? wv >> 16 : wv & 0xffffu;
+      const bool mine = e0 + e < n_raw && (int)jr != irow;
+      const unsigned j = mine ? jr : dummy;
+      const double dx = px - xs[3 * j], dy = py - xs[3 * j + 1], dz = pz - xs[3 * j + 2];
+      const double r2 = r2_exact(dx, dy, dz);
+      const bool in_rl = r2 < rl2;            // (the dummy row is far outside)
+      const bool hit = r2 < k.rc2;
+      n_list += in_rl ? 1 : 0;
+      n_half += (in_rl && (int)j > irow) ? 1 : 0;
+      double u3;
+      const double f = vs_force_scalar(r2, hit, k, u3);
+      a.ax = fma(f, dx, a.ax);
+      a.ay = fma(f, dy, a.ay);
+      a.az = fma(f, dz, a.az);
+      if (EV) {
+        a.e = fma(0.5 * u3, fma(k.e12, u3, -k.e6), a.e);
+        a.v = fma(0.5 * f, r2, a.v);
+      }
+      a.pairs += hit ? 1 : 0;
+      if (N3 == 2) a.halo += (hit && j >= hb_row) ? 1 : 0;
     }
   }
   if (active) {
     count[p] = n_list;
     count_half[p] = n_half;
-  }
-  const int hit_max = __reduce_max_sync(0xffffffffu, (int)n_hit);
-  if (lane == 0 && hit_max > *reinterpret_cast<volatile int32_t*>(info + 4))
-    atomicMax(info + 4, hit_max);
-  // 2. the lane's hits, 8 per 128-bit read; past its own count a lane takes
-  //    the far-away dummy row (zero force by the masked reciprocal)
-  VsAcc a = {0.0, 0.0, 0.0, 0.0, 0.0, 0, 0};
-  if (hit_max <= cap_ent) {   // (else the host retries with the observed maximum)
-    const uint4* hits8 = reinterpret_cast<const uint4*>(hits);
-    uint4 vn = hits8[0];
-#pragma unroll 1
-    for (int e0 = 0; e0 < hit_max; e0 += 8) {
-      const uint4 v = vn;
-      if (e0 + 8 < hit_max) vn = hits8[min((e0 >> 3) + 1, (cap_ent >> 3) - 1)];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const bool valid = e0 + e < (int)n_hit;
-        const unsigned wv = e < 2 ? v.x : e < 4 ? v.y : e < 6 ? v.z : v.w;
-        const unsigned j = valid ? ((e & 1) ? wv >> 16 : wv & 0xffffu) : dummy;
-        const double dx = px - xs[3 * j], dy = py - xs[3 * j + 1], dz = pz - xs[3 * j + 2];
-        const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-        double u3;
-        const double f = vs_force_scalar(r2, valid, k, u3);
-        a.ax = fma(f, dx, a.ax);
-        a.ay = fma(f, dy, a.ay);
-        a.az = fma(f, dz, a.az);
-        if (EV) {
-          a.e = fma(0.5 * u3, fma(k.e12, u3, -k.e6), a.e);
-          a.v = fma(0.5 * f, r2, a.v);
-        }
-        a.pairs += valid ? 1 : 0;
-        if (N3 == 2) a.halo += (valid && j >= hb_off) ? 1 : 0;
-      }
-    }
   }
   // a coincident pair (r2 == 0 inside the cutoff): the numba -1 sentinel
   const int overlap = (active && !(isfinite(a.ax) && isfinite(a.ay) && isfinite(a.az))) ? 1 : 0;
@@ -1234,7 +1223,7 @@ static inline int build_area(int32_t rows, int32_t cap_entries) {
 }
 
 size_t lmd_vls_build_smem(int32_t rows, int32_t cap_entries) {
-  return (size_t)build_area(rows, cap_entries) + 2 * 32 * kVsG;
+  return (size_t)build_area(rows, cap_entries) + kVsRingBytes + 2 * 32 * kVsG;
 }
 
 int lmd_vls_build(const lmd_grid* g, double rin2, double rl2, int64_t n_owned, int32_t rows,
@@ -1252,8 +1241,9 @@ int lmd_vls_build(const lmd_grid* g, double rin2, double rl2, int64_t n_owned, i
   cudaStream_t s = (cudaStream_t)stream;
   const GridK k = make_gridk(g);
   // the bucket counters exist only for the bank order
-  const size_t smem = (size_t)build_area(rows, cap_entries) + (bank_order ? 2 * 32 * kVsG : 0);
-  auto kern = bank_order ? vls_build_kernel<true> : vls_build_kernel<false>;
+  const size_t smem = (size_t)build_area(rows, cap_entries) + kVsRingBytes +
+                      (bank_order ? 2 * 32 * kVsG : 0);
+  auto kern = bank_order ? vls_build_kernel<1> : vls_build_kernel<0>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return set_cuda_error(e);
@@ -1328,7 +1318,7 @@ int lmd_vls_direct(const lmd_grid* g, int newton3, int flags, const lmd_lj* lj, 
                    int32_t* info, void* stream) {
   if (n_owned <= 0 || n_groups <= 0) return LMD_OK;
   if (newton3 != 0 && newton3 != 2) return LMD_ERR_CONFIG;
-  if (cap_entries < 8 || cap_entries % 8 || cap_entries > 4096) return LMD_ERR_CONFIG;
+  if (cap_entries < 8 || cap_entries % 8 || cap_entries > 4088) return LMD_ERR_CONFIG;
   if (rows <= 0 || rows > kVsMaxRows + 64 || (uintptr_t)pos_rows % 16) return LMD_ERR_CONFIG;
   const bool ev = (flags & LMD_FLAG_ENERGY) != 0;
   if (ev && !ev_scratch) return LMD_ERR_CONFIG;
@@ -1336,17 +1326,31 @@ int lmd_vls_direct(const lmd_grid* g, int newton3, int flags, const lmd_lj* lj, 
   const LJK k = make_ljk(lj);
   const GridK gk = make_gridk(g);
   const double rl = lj->cutoff + lj->skin;
-  const size_t smem = stage_bytes(rows);
-#define LMD_VSD(EVB, N3B)                                                                       \
-  {                                                                                             \
-    auto kern = vls_direct_kernel<EVB, N3B>;                                                    \
-    cudaError_t e =                                                                             \
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
-    if (e != cudaSuccess) return set_cuda_error(e);                                             \
-    kern<<<(unsigned)n_groups, kVsG, smem, s>>>(                                                \
-        (int)gk.t0, (int)gk.t1, groups, pos_rows, fs_own, o_count, fs_img, h_count, rl * rl, k, \
-        cap_entries, (uint16_t*)scratch, out_perm, fx, fy, fz, ev_scratch, stats, count,        \
-        count_half, info);                                                                      \
+  const int cap_chunks = cap_entries / 8;   // scratch: n_groups * 4 tiles * cap_chunks * 512 B
+  {   // 1. the walk (FP32 rows only: 12 B per row)
+    const size_t area = ((size_t)rows * 12 + 127) / 128 * 128;
+    const size_t smem = area + kVsRingBytes;
+    auto kern = vls_build_kernel<2>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return set_cuda_error(e);
+    kern<<<(unsigned)n_groups, kVsG, smem, s>>>(
+        (int)gk.t0, (int)gk.t1, groups, info, pos_rows, fs_own, o_count, fs_img, h_count, rl * rl,
+        rl * rl, (int)area, cap_chunks, cap_entries, (int4*)scratch, nullptr, nullptr, count,
+        count_half, info);
+    LMD_CHECK_LAUNCH();
+  }
+  const size_t smem = stage_bytes(rows);   // 2. the raw hits from the FP64 rows
+#define LMD_VSD(EVB, N3B)                                                                   \
+  {                                                                                         \
+    auto kern = vls_rawforce_kernel<EVB, N3B>;                                              \
+    cudaError_t e =                                                                         \
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    if (e != cudaSuccess) return set_cuda_error(e);                                         \
+    kern<<<(unsigned)n_groups, kVsG, smem, s>>>(groups, pos_rows, rl * rl, k, cap_chunks,   \
+                                                cap_entries, (const int4*)scratch, out_perm, \
+                                                fx, fy, fz, ev_scratch, stats, count,       \
+                                                count_half, info);                          \
   }
   if (ev) {
     if (newton3) LMD_VSD(true, 2) else LMD_VSD(true, 0)
