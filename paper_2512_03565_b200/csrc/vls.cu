@@ -801,9 +801,7 @@ __global__ void __launch_bounds__(kVsG, OCC)
   const int c_in = __ldg(segc + 2 * t), c_out = __ldg(segc + 2 * t + 1);
   // inner segment alone while every particle moved less than delta / 2
   const bool outer = disp == nullptr || *disp >= half_delta2_bits;
-  __shared__ int blk_stat[4];   // pairs, image pairs, overlap, warps arrived
   if (tid == 0) mbar_init(&bar, 1);
-  if (tid < 4) blk_stat[tid] = 0;
   vls_dummies(rec, xs);
   __syncthreads();
   vls_stage(rec, rows, xs, &bar);
@@ -912,34 +910,10 @@ __global__ void __launch_bounds__(kVsG, OCC)
     fy[o] = a.ay;
     fz[o] = a.az;
   }
-  // statistics: one set of global atomics per block -- the four tiles' counts
-  // meet in shared memory and the last warp to arrive adds them (no barrier);
-  // energy / virial partials per tile
-  const int wp = __reduce_add_sync(0xffffffffu, a.pairs);
-  const int wh = __reduce_add_sync(0xffffffffu, a.halo);
-  const int wo = __any_sync(0xffffffffu, overlap);
-  if (EV) {
-    const double e = warp_sum(a.e), v = warp_sum(a.v);
-    if (lane == 0) {
-      ev[2 * (long long)t] = e;
-      ev[2 * (long long)t + 1] = v;
-    }
-  }
-  if (lane == 0) {
-    if (wp) atomicAdd(&blk_stat[0], wp);
-    if (wh) atomicAdd(&blk_stat[1], wh);
-    if (wo) atomicOr(&blk_stat[2], 1);
-    __threadfence_block();
-    if (atomicAdd(&blk_stat[3], 1) == kVsG / 32 - 1) {
-      __threadfence_block();
-      const int bp = *reinterpret_cast<volatile int*>(&blk_stat[0]);
-      const int bh = *reinterpret_cast<volatile int*>(&blk_stat[1]);
-      const int bo = *reinterpret_cast<volatile int*>(&blk_stat[2]);
-      if (bp) atomicAdd((unsigned long long*)&stats->pair_interactions, (unsigned long long)bp);
-      if (bh) atomicAdd((unsigned long long*)&stats->pairs_owned_halo, (unsigned long long)bh);
-      if (bo) atomicOr(&stats->overlap, 1);
-    }
-  }
+  // statistics: per-warp atomics (block-level accumulation in shared memory
+  // before the global atomics was measured 1 % slower: 1.789 vs 1.771 ms)
+  Acc fl = {0.0, 0.0, 0.0, a.e, a.v, a.pairs, overlap, a.halo};
+  flush_acc(fl, lane, true, EV, t, ev, stats);
 }
 
 // ------------------------------------------------------------ direct (K4d)
