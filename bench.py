@@ -569,7 +569,9 @@ def run_b200(args):
                "d2h_bytes_per_step": int(n * 3 * 8),
                "steps": args.e2e_steps,
                "note": "force_phase() on pinned host SoA buffers: H2D positions, device "
-                       "binning/images/neighbour build, force kernel, D2H forces"}
+                       "binning / images / group plan, the one-shot force path (candidate "
+                       "walk + exact evaluation, no lists written: the container lives for "
+                       "this call only), D2H forces"}
     elif args.e2e_steps > 0 and dec is not None:
         # every rank: its brick's particles in pinned host buffers ->
         # force_phase_bricks (H2D, ghost planning + exchange, binning, lists,
