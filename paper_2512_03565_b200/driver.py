@@ -45,17 +45,29 @@ def force_phase(owned, box, params, config: Configuration, vector_width: int,
     dev_owned = device_soa(owned)
     cont = make_container(config.container, box, params,
                           cluster_size=config.cluster_size or cluster_size or vector_width)
-    if hasattr(cont, "bank_rounds"):
-        # one force phase on a temporary container: the bank-aware list order
-        # pays for its pass only when lists are reused
-        cont.bank_rounds = -1
+    lean = _one_shot(cont)
     cont.rebuild(dev_owned)
-    cont.refresh(dev_owned)
+    if not lean:           # (a lean rebuild has loaded the current positions)
+        cont.refresh(dev_owned)
     stats = _compute_once(cont, config, vector_width, energy)
     cont.collect_forces(dev_owned)
     if dev_owned is not owned:
         _write_forces_back(owned, dev_owned)
     return stats
+
+
+def _one_shot(cont) -> bool:
+    """Mark a container as built for one force computation; True when its
+    rebuild then loads the current positions itself (Verlet lists: no pos4 /
+    SoA copies, no snapshots of the build-time state, plain list order if
+    lists are needed at all)."""
+    if hasattr(cont, "bank_rounds"):
+        # the bank-aware list order pays for its pass only when lists are reused
+        cont.bank_rounds = -1
+    if hasattr(cont, "one_shot"):
+        cont.one_shot = True
+        return bool(cont.segmented)
+    return False
 
 
 def _compute_once(cont, config, vector_width: int, energy: bool) -> KernelStats:
@@ -99,10 +111,10 @@ def force_phase_bricks(owned, dec, params, config: Configuration, vector_width: 
     ghosts.pos_z.copy_(ghost_rows[:, 2])
     cont = make_container(config.container, dec.local_box(), params,
                           cluster_size=config.cluster_size or cluster_size or vector_width)
-    if hasattr(cont, "bank_rounds"):
-        cont.bank_rounds = -1
+    lean = _one_shot(cont)
     cont.rebuild(dev_owned, ghosts)
-    cont.refresh(dev_owned, ghosts)
+    if not lean:
+        cont.refresh(dev_owned, ghosts)
     stats = _compute_once(cont, config, vector_width, energy)
     cont.collect_forces(dev_owned)
     if dev_owned is not owned:

@@ -89,6 +89,10 @@ class VerletListContainer:
         self.adaptive_inner = True
         self._last_disp2 = None
         self._inner_eff = self.inner_skin
+        # a container built for one force computation (driver.force_phase):
+        # rebuild loads the (x, y, z) rows only -- no pos4 / SoA copies and no
+        # snapshots of the build-time state (positions never change)
+        self.one_shot = False
         self._vls: dict = {}
         self._vls_plan = None
         self._vls_cap = None
@@ -163,11 +167,18 @@ class VerletListContainer:
         self._fx = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
         self._fy = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
         self._fz = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
-        self._load_positions(d, halo if self._external_halo else None)
-        # lists are built lazily per interaction order: always from the
-        # rebuild-time positions, whatever the particles did since
-        self._build_pos4 = self._pos4.clone()
-        self._build_rows = self._rows.clone() if self.segmented else None
+        lean = self.one_shot and self.segmented
+        if lean:
+            self._load_rows(d, halo if self._external_halo else None)
+            self._pos4_stale = True
+            self._build_pos4 = None            # made on demand (_list)
+            self._build_rows = self._rows
+        else:
+            self._load_positions(d, halo if self._external_halo else None)
+            # lists are built lazily per interaction order: always from the
+            # rebuild-time positions, whatever the particles did since
+            self._build_pos4 = self._pos4.clone()
+            self._build_rows = self._rows.clone() if self.segmented else None
         self._vls.clear()
         self._vls_plan = None
         one_segment = (self.adaptive_inner and self._last_disp2 is not None
@@ -179,12 +190,12 @@ class VerletListContainer:
         else:
             self._disp.zero_()
         self._disp_slot = -1 if self._external_halo else 0
-        self._pos4_stale = False
+        self._pos4_stale = lean
         self._lists.clear()
         self._staging.clear()
         self._counts.clear()
         self._stats_cache.clear()
-        self.reference_positions = d.positions().clone()
+        self.reference_positions = d.positions() if lean else d.positions().clone()
         self.steps_since_rebuild = 0
         self.structure_version += 1
 
@@ -421,6 +432,9 @@ class VerletListContainer:
             if hit is not None:
                 self._lists[key] = hit
                 return hit
+        if self._build_pos4 is None:
+            self._regen_pos4()                 # a one-shot container off its lean path
+            self._build_pos4 = self._pos4
         ntiles = int(N.load().lmd_vl_num_tiles(n, pattern.code))
         b_ = pattern.shape(32)[1]
         tile_off = torch.empty(max(ntiles, 1), dtype=torch.int64, device=dev)
