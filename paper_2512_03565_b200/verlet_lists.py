@@ -167,18 +167,21 @@ class VerletListContainer:
         self._fx = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
         self._fy = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
         self._fz = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
+        # Lists are built lazily per interaction order, always from the
+        # rebuild-time positions, whatever the particles did since.  With the
+        # segmented lists only the (x, y, z) rows are loaded and snapshot here;
+        # the pos4 / SoA copies (the other orders' kernels) follow on demand
+        # (_list).  A one-shot container (positions never change) aliases the
+        # snapshot.
         lean = self.one_shot and self.segmented
-        if lean:
+        if self.segmented:
             self._load_rows(d, halo if self._external_halo else None)
-            self._pos4_stale = True
-            self._build_pos4 = None            # made on demand (_list)
-            self._build_rows = self._rows
+            self._build_pos4 = None
+            self._build_rows = self._rows if lean else self._rows.clone()
         else:
             self._load_positions(d, halo if self._external_halo else None)
-            # lists are built lazily per interaction order: always from the
-            # rebuild-time positions, whatever the particles did since
             self._build_pos4 = self._pos4.clone()
-            self._build_rows = self._rows.clone() if self.segmented else None
+            self._build_rows = None
         self._vls.clear()
         self._vls_plan = None
         one_segment = (self.adaptive_inner and self._last_disp2 is not None
@@ -190,12 +193,12 @@ class VerletListContainer:
         else:
             self._disp.zero_()
         self._disp_slot = -1 if self._external_halo else 0
-        self._pos4_stale = lean
+        self._pos4_stale = bool(self.segmented)
         self._lists.clear()
         self._staging.clear()
         self._counts.clear()
         self._stats_cache.clear()
-        self.reference_positions = d.positions() if lean else d.positions().clone()
+        self.reference_positions = d.positions()     # (a fresh (n, 3) stack)
         self.steps_since_rebuild = 0
         self.structure_version += 1
 
@@ -433,8 +436,12 @@ class VerletListContainer:
                 self._lists[key] = hit
                 return hit
         if self._build_pos4 is None:
-            self._regen_pos4()                 # a one-shot container off its lean path
-            self._build_pos4 = self._pos4
+            # first list of another order since the rebuild: pos4 / SoA of the
+            # build-time rows
+            N.call("lmd_vls_rows_to_legacy", n + self.n_halo, n, N.ptr(self._build_rows),
+                   N.ptr(self._pos4), None, None, None, N.stream())
+            self._build_pos4 = self._pos4.clone()
+            self._pos4_stale = True
         ntiles = int(N.load().lmd_vl_num_tiles(n, pattern.code))
         b_ = pattern.shape(32)[1]
         tile_off = torch.empty(max(ntiles, 1), dtype=torch.int64, device=dev)
@@ -879,10 +886,10 @@ class VerletListContainer:
             return None
         dev = self._rows.device
         n, ng = self.n_owned, plan["ngroups"]
-        rc = float(self.params.cutoff)
+        rl = float(self.params.interaction_length)   # the walk keeps candidates within rl
         vol = float(np.prod(self.box.lengths))
-        est = (n + self.n_halo) / vol * (4.0 / 3.0) * np.pi * rc ** 3
-        cap = int(est * 1.4 + 24)
+        est = (n + self.n_halo) / vol * (4.0 / 3.0) * np.pi * rl ** 3
+        cap = int(est * 1.25 + 24)
         stats_t = N.new_stats(dev)
         slots = int(N.load().lmd_vls_ev_slots(ng))
         ev_t = torch.empty(2 * max(slots, 1), dtype=torch.float64, device=dev) if energy else None
