@@ -14,7 +14,9 @@ virial on) on the same seeded state:
 * potential energy and virial within 1e-12 relative.
 
 Workloads: C2 (1,000,000 particles, RSA, rho 0.2 / 0.5 / 0.8), C4
-(16,777,216-particle perturbed lattice; the bench's headline workload), C3
+(16,777,216-particle perturbed lattice; the bench's headline workload, also
+through the both-segment launch and the one-shot force_phase path), C5
+(8,388,608-particle gas at rho 0.3, the weak-scaling brick), C3
 (2,000,000-particle droplet, rc 3.0) for the cluster lists at M = 4 / 8 / 32.
 The oracle costs ~1.5 s per 1M particles and ~25 s at 16.8M (1 core)."""
 
@@ -121,6 +123,50 @@ def test_c4_headline_workload():
     case = Case(workloads.config4(256, device="cpu"))
     assert case.st.pair_interactions == 907_284_108   # profiles/r01_parity_full.jsonl
     _vl_all(case)
+
+
+def _one_shot_and_both_segments(case):
+    """The same state through (i) the launch that runs both list segments
+    (no displacement record: what a launch does once a particle has moved
+    inner_skin / 2) and (ii) the public one-shot force_phase (the list-free
+    path, lmd_vls_direct), which bench.py's e2e times."""
+    import paper_2512_03565_b200 as B
+    cont, buf = _bench_container(case, "vl")
+    cont.ensure_lists(B.PatternKind.V_BY_ONE, False)
+    cont._disp_slot = -1
+    _check(case, cont, buf, "vl", False, "v_by_one", case.st.pair_interactions)
+    del cont, buf
+    torch.cuda.empty_cache()
+    params = B.LJParams(cutoff=case.w.cutoff, skin=case.skin)
+    buf = B.ParticleBuffer.from_positions(case.pos, device="cuda")
+    st = B.force_phase(buf, case.box, params, B.Configuration.parse("vl,vl,false,v_by_one"), 8,
+                       energy=True)
+    f = buf.forces().cpu().numpy()
+    assert st.pair_interactions == case.st.pair_interactions
+    assert forces_close(f, case.f, RTOL)
+    assert abs(st.epot - case.st.epot) <= RTOL * abs(case.st.epot)
+    assert abs(st.virial - case.st.virial) <= RTOL * abs(case.st.virial)
+    del buf
+    torch.cuda.empty_cache()
+
+
+def test_c4_one_shot_path_and_both_segments():
+    from paper_2512_03565_b200 import workloads
+    torch.cuda.set_device(0)
+    _one_shot_and_both_segments(Case(workloads.config4(256, device="cpu")))
+
+
+def test_c5_weak_scaling_brick():
+    """BASELINE config 5's per-GPU system (8,388,608 particles, rho 0.3)."""
+    from paper_2512_03565_b200 import workloads
+    torch.cuda.set_device(0)
+    case = Case(workloads.config5(device="cuda"))
+    cont, buf = _bench_container(case, "vl")
+    _check(case, cont, buf, "vl", False, "v_by_one", case.st.pair_interactions)
+    _check(case, cont, buf, "vl", True, "v_by_one", case.n3_pairs())
+    del cont, buf
+    torch.cuda.empty_cache()
+    _one_shot_and_both_segments(case)
 
 
 @pytest.mark.parametrize("m", [4, 8, 32])
