@@ -525,8 +525,6 @@ int lmd_buffer_counts(int64_t n, const double* pos4, int64_t* out3, void* stream
 int lmd_apply_boundaries(const lmd_box* box, int64_t n, double* x, double* y, double* z,
                          double* vx, double* vy, double* vz, int32_t* diverged, void* stream);
 
-/* integrator.py:21-48: phase 0 = pre-force (drift, stash old force, zero
- * force), 1 = post-force (kick).  *nonfinite |= 1 on non-finite state. */
 /* ----------------------------------------- brick decomposition (§8e) */
 /* One exchange stage's pack (decomposition.py): out_rows[k] (row-major
  * x, y, z) = source(idx[k]) with coordinate `axis` shifted by `shift` (the
@@ -546,6 +544,11 @@ int lmd_gather_rows_soa(int64_t n, const int32_t* perm, const double* rows, doub
  * dz^2 (containers.py:23-38, needs_rebuild); ref_xyz rows are (x, y, z). */
 int lmd_max_displacement2(int64_t n, const double* x, const double* y, const double* z,
                           const double* ref_xyz, double* out, void* stream);
+/* Velocity-Verlet halves (integrator.py:21-48), numpy's expression order.
+ * phase 0: pre-force (x += v dt + f h dt^2 / m; old force = f; f = 0);
+ * phase 1: post-force (v += (f + old) h dt / m); phase 2: phase 1 followed by
+ * the next step's phase 0 in one pass (bit for bit the two launches).
+ * *nonfinite |= 1 on non-finite state. */
 int lmd_verlet_step(int64_t n, int phase, double dt, double mass, double* x, double* y,
                     double* z, double* vx, double* vy, double* vz, double* fx, double* fy,
                     double* fz, double* ox, double* oy, double* oz, int32_t* nonfinite,

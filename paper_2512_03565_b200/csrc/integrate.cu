@@ -78,11 +78,26 @@ __global__ void verlet_kernel(int64_t n, int phase, double dt, double half_over_
       O[ax][k] = f;
       F[ax][k] = 0.0;
       bad |= !isfinite(xn) || !isfinite(V[ax][k]);
-    } else {
+    } else if (phase == 1) {
       const double c = __dmul_rn(half_over_m, dt);
       const double vn = __dadd_rn(V[ax][k], __dmul_rn(__dadd_rn(F[ax][k], O[ax][k]), c));
       V[ax][k] = vn;
       bad |= !isfinite(vn) || !isfinite(X[ax][k]);
+    } else {
+      // phase 2: this step's post-force half followed by the next step's
+      // pre-force half in one pass (the same expressions in the same order,
+      // so the trajectory is bit for bit that of the two launches)
+      const double c1 = __dmul_rn(half_over_m, dt);
+      const double c2 = __dmul_rn(__dmul_rn(half_over_m, dt), dt);
+      const double f = F[ax][k];
+      const double vn = __dadd_rn(V[ax][k], __dmul_rn(__dadd_rn(f, O[ax][k]), c1));
+      const double x0 = X[ax][k];
+      const double xn = __dadd_rn(x0, __dadd_rn(__dmul_rn(vn, dt), __dmul_rn(f, c2)));
+      V[ax][k] = vn;
+      X[ax][k] = xn;
+      O[ax][k] = f;
+      F[ax][k] = 0.0;
+      bad |= !isfinite(vn) || !isfinite(x0) || !isfinite(xn);
     }
   }
   if (bad) atomicOr(nonfinite, 1);
@@ -143,7 +158,7 @@ int lmd_verlet_step(int64_t n, int phase, double dt, double mass, double* x, dou
                     double* z, double* vx, double* vy, double* vz, double* fx, double* fy,
                     double* fz, double* ox, double* oy, double* oz, int32_t* nonfinite,
                     void* stream) {
-  if (phase != 0 && phase != 1) return LMD_ERR_CONFIG;
+  if (phase < 0 || phase > 2) return LMD_ERR_CONFIG;
   if (n <= 0) return LMD_OK;
   verlet_kernel<<<(unsigned)cdiv(n, 256), 256, 0, (cudaStream_t)stream>>>(
       n, phase, dt, 0.5 / mass, x, y, z, vx, vy, vz, fx, fy, fz, ox, oy, oz, nonfinite);

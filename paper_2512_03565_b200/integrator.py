@@ -13,6 +13,7 @@ from .particles import ParticleBuffer
 
 PRE_FORCE = "pre-force"
 POST_FORCE = "post-force"
+POST_THEN_PRE = "post-then-pre"   # this step's second half + the next step's first, one pass
 
 
 def velocity_verlet_step(buf: ParticleBuffer, params, phase: str, check: bool = True) -> None:
@@ -25,6 +26,8 @@ def velocity_verlet_step(buf: ParticleBuffer, params, phase: str, check: bool = 
         code = 0
     elif phase == POST_FORCE:
         code = 1
+    elif phase == POST_THEN_PRE:
+        code = 2
     else:
         raise ValueError(f"unknown integration phase {phase!r}")
     flag = buf.extra.get("nonfinite")

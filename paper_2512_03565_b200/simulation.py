@@ -26,7 +26,7 @@ from .containers import LinkedCellsContainer, max_particles_per_cell
 from .domain import apply_boundaries, as_box
 from .driver import make_container
 from .errors import ConfigurationError, ParticleOverlapError, ScenarioError, SimulationDivergedError
-from .integrator import POST_FORCE, PRE_FORCE, velocity_verlet_step
+from .integrator import POST_FORCE, POST_THEN_PRE, PRE_FORCE, velocity_verlet_step
 from .kernels import KernelStats, validate_vector_width
 from .traversals import traversal_code
 from .tuning import (PRODUCTION, Configuration, ContainerKind, Tuner, TuningPolicy,
@@ -166,7 +166,7 @@ def run_md(owned, box, params, iterations: int, vector_width: int = 8, *,
            policy: TuningPolicy | None = None, metric: str = "time",
            cluster_size: int | None = None, rebuild_period: int | None = None,
            retune_drift: float | None = None, energy: bool = False, record: bool = True,
-           wrap: str = "always"):
+           wrap: str = "always", fuse_halves: bool | None = None):
     """Run ``iterations`` MD steps on device-resident ``owned`` (our ParticleBuffer).
 
     Returns (records, summary).  With ``fixed_config`` the tuner is off.
@@ -175,6 +175,11 @@ def run_md(owned, box, params, iterations: int, vector_width: int = 8, *,
     reference does (driver.py:214); in a large periodic system some particle
     then wraps every step, its displacement looks like a box length and
     ``needs_rebuild`` fires every step, so every tuning sample is displaced.
+    ``fuse_halves`` (default on, effective with ``wrap="at_rebuild"``): a
+    step's post-force half and the next step's pre-force half run as one pass
+    over the particles (the same expressions: bit for bit the same
+    trajectory).
+
     ``wrap="at_rebuild"`` keeps positions unwrapped between rebuilds and
     wraps them just before a rebuild (the usual MD practice): rebuilds follow
     the skin/period rule and the tuner can finish its phases.  Forces are the
@@ -216,10 +221,19 @@ def run_md(owned, box, params, iterations: int, vector_width: int = 8, *,
     start = time.perf_counter()
     whole = metric == "iteration"
     try:
+        # with positions wrapped at rebuilds only, nothing sits between a
+        # step's post-force half and the next step's pre-force half: one
+        # fused pass (the same arithmetic) serves both
+        if fuse_halves is None:
+            fuse_halves = True
+        fuse_halves = bool(fuse_halves) and wrap == "at_rebuild"
+        pre_done = False
         for it in range(iterations):
             if whole:
                 provider.begin_region()
-            velocity_verlet_step(owned, params, PRE_FORCE, check=False)
+            if not pre_done:
+                velocity_verlet_step(owned, params, PRE_FORCE, check=False)
+            pre_done = False
             if tuner is not None:
                 if retune_drift and it > 0 and tuner.selected is not None and it % 10 == 0:
                     cur = max_particles_per_cell(owned, box, margin)
@@ -281,7 +295,11 @@ def run_md(owned, box, params, iterations: int, vector_width: int = 8, *,
             if sample is None and not whole:
                 sample = provider.end_region()
             cont.collect_forces(owned)
-            velocity_verlet_step(owned, params, POST_FORCE, check=False)
+            if fuse_halves and it + 1 < iterations:
+                velocity_verlet_step(owned, params, POST_THEN_PRE, check=False)
+                pre_done = True
+            else:
+                velocity_verlet_step(owned, params, POST_FORCE, check=False)
             if wrap == "always":
                 apply_boundaries(owned, box)
             if whole:

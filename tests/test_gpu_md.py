@@ -184,3 +184,32 @@ def test_vl_refresh_and_check_decides_like_needs_rebuild():
     cont.steps_since_rebuild = 2
     assert cont.refresh_and_check(buf) is True
 
+
+
+def test_fused_integrator_halves_are_bitwise_the_two_launches():
+    """run_md with the post-force half and the next pre-force half fused into
+    one pass (the default with wrap="at_rebuild") gives bit for bit the
+    trajectory of the two separate launches."""
+    rng = np.random.default_rng(21)
+    side, a = 14, 1.12
+    n, L = side ** 3, side * a
+    grid = np.stack(np.meshgrid(*[np.arange(side)] * 3, indexing="ij"), -1).reshape(-1, 3)
+    pos = (grid + 0.5) * a + rng.uniform(-0.08, 0.08, (n, 3))
+    vel = rng.normal(0.0, 1.0, (n, 3))
+    box = SimulationBox.cube(L, periodic=True)
+    params = LJParams(cutoff=2.5, skin=0.3, dt=0.002)
+    cfg = Configuration.parse("vl,vl,false,v_by_one")
+    out = []
+    for fuse in (False, True):
+        buf = ParticleBuffer.from_positions(pos, device="cuda")
+        v = torch.as_tensor(vel, device="cuda")
+        buf.vel_x.copy_(v[:, 0]); buf.vel_y.copy_(v[:, 1]); buf.vel_z.copy_(v[:, 2])
+        B.force_phase(buf, box, params, cfg, 8)
+        records, _ = run_md(buf, box, params, 23, 8, fixed_config=cfg, rebuild_period=7,
+                            wrap="at_rebuild", fuse_halves=fuse)
+        out.append(([r.pair_interactions for r in records], buf.positions().cpu().numpy(),
+                    buf.velocities().cpu().numpy(), buf.forces().cpu().numpy()))
+    assert out[0][0] == out[1][0]
+    assert np.array_equal(out[0][1], out[1][1])
+    assert np.array_equal(out[0][2], out[1][2])
+    assert np.array_equal(out[0][3], out[1][3])
