@@ -102,7 +102,9 @@ class VerletClusterContainer:
         self.reference_positions = None
         self.steps_since_rebuild = 0
         self.structure_version = 0
-        # interaction orders as warp lane templates (lmd_force_vcl_order);
+        # interaction orders as warp lane templates (lmd_force_vcl_order; an
+        # order aligned with the cluster size runs as the stream kernel, whose
+        # mapping it is; "strict": the lane-template kernel even then);
         # False: the packed stream kernel for every order (the cluster-aligned
         # M x 32/M mapping with hit compaction, the fastest one on the GPU)
         self.order_kernels = type(self).ORDER_KERNELS
@@ -288,7 +290,13 @@ class VerletClusterContainer:
         if ev_t is None:
             ev_t = torch.empty(2 * max(int(N.load().lmd_vcl_ev_slots(ncl)), 1),
                                dtype=torch.float64, device=dev)
-        if pattern is not None and self.order_kernels and self.cluster_size <= 32:
+        # an order whose i-side is exactly one cluster (A = M: v_by_one at
+        # M = 32, half_by_two at 16, two_by_half at 2, one_by_v at 1) IS the
+        # stream kernel's M x 32/M mapping, which also compacts hits
+        aligned = (pattern is not None and
+                   as_pattern(pattern).shape(32)[0] == self.cluster_size)
+        if (pattern is not None and self.order_kernels and self.cluster_size <= 32
+                and not (aligned and self.order_kernels != "strict")):
             N.call("lmd_force_vcl_order", ncl, self.cluster_size, as_pattern(pattern).code,
                    N.FLAG_ENERGY if energy else 0, N.make_lj(self.params), N.ptr(self._pos4),
                    N.ptr(self._off), N.ptr(self._count), N.ptr(self._list), N.ptr(self._hoff),

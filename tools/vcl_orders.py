@@ -52,7 +52,7 @@ def main():
                             "pairs_per_s": p_ref / (t_ref * 1e-3)})
         print(f"M={m:2d} stream      {t_ref:8.3f} ms {p_ref / t_ref / 1e-3:.3e} pairs/s",
               flush=True)
-        cont.order_kernels = True
+        cont.order_kernels = "strict"     # the lane-template kernel for every order
         for o in ORDERS:
             t, p, f = timed(cont, o)
             scale = torch.clamp(f_ref.abs().max(dim=1).values, min=1.0)
