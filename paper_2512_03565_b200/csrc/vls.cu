@@ -939,14 +939,12 @@ __global__ void __launch_bounds__(kVsG, 5)
   extern __shared__ __align__(128) double sm_d[];
   double* xs = sm_d;
   __shared__ unsigned long long bar;
-  __shared__ int blk_stat[4];
   if (info[4] > cap_ent) return;   // the walk ran out of room: the host retries
   const int g = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int t = g * (kVsG / 32) + w;
   const int32_t* rec = groups + (long long)g * kVsRec;
   if (tid == 0) mbar_init(&bar, 1);
-  if (tid < 4) blk_stat[tid] = 0;
   vls_dummies(rec, xs);
   __syncthreads();
   vls_stage(rec, rows, xs, &bar);
@@ -1013,31 +1011,8 @@ __global__ void __launch_bounds__(kVsG, 5)
     fy[o] = a.ay;
     fz[o] = a.az;
   }
-  const int wp = __reduce_add_sync(0xffffffffu, a.pairs);
-  const int wh = __reduce_add_sync(0xffffffffu, a.halo);
-  const int wo = __any_sync(0xffffffffu, overlap);
-  if (EV) {
-    const double e = warp_sum(a.e), v = warp_sum(a.v);
-    if (lane == 0) {
-      ev[2 * (long long)t] = e;
-      ev[2 * (long long)t + 1] = v;
-    }
-  }
-  if (lane == 0) {
-    if (wp) atomicAdd(&blk_stat[0], wp);
-    if (wh) atomicAdd(&blk_stat[1], wh);
-    if (wo) atomicOr(&blk_stat[2], 1);
-    __threadfence_block();
-    if (atomicAdd(&blk_stat[3], 1) == kVsG / 32 - 1) {
-      __threadfence_block();
-      const int bp = *reinterpret_cast<volatile int*>(&blk_stat[0]);
-      const int bh = *reinterpret_cast<volatile int*>(&blk_stat[1]);
-      const int bo = *reinterpret_cast<volatile int*>(&blk_stat[2]);
-      if (bp) atomicAdd((unsigned long long*)&stats->pair_interactions, (unsigned long long)bp);
-      if (bh) atomicAdd((unsigned long long*)&stats->pairs_owned_halo, (unsigned long long)bh);
-      if (bo) atomicOr(&stats->overlap, 1);
-    }
-  }
+  Acc fl = {0.0, 0.0, 0.0, a.e, a.v, a.pairs, overlap, a.halo};
+  flush_acc(fl, lane, true, EV, t, ev, stats);
 }
 
 // ---------------------------------------------------------------- refresh
