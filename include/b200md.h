@@ -351,7 +351,9 @@ int lmd_force_vl_staged(int newton3, int flags, const lmd_lj* lj, int64_t n_owne
  * the energy/virial reduction over all groups to lmd_vls_reduce_ev.  lmd_vls_refresh: rows[k] =
  * (x, y, z)[perm[k]] (perm NULL: identity) and with disp != NULL the
  * largest squared displacement from build_rows max-reduced into disp[slot]
- * (disp[slot ^ 1] cleared).  lmd_vls_gather_rows: rows_out[k] =
+ * (disp[slot ^ 1] cleared).  lmd_vls_gather_rows (ghost rows of a
+ * decomposition; with disp != NULL their displacement from build_rows is
+ * max-reduced into disp[slot] too): rows_out[k] =
  * rows_in[perm[k]].  lmd_vls_rows_to_legacy: rows -> pos4 (OWNED below
  * n_owned, HALO above) and SoA copies (either may be NULL). */
 int64_t lmd_vls_max_groups(const lmd_grid* g, int64_t n_owned);
@@ -399,7 +401,7 @@ int lmd_vls_refresh(int64_t n, const int32_t* perm, const double* x, const doubl
                     const double* z, double* rows, const double* build_rows, uint64_t* disp,
                     int32_t slot, void* stream);
 int lmd_vls_gather_rows(int64_t n, const int32_t* perm, const double* rows_in, double* rows_out,
-                        void* stream);
+                        const double* build_rows, uint64_t* disp, int32_t slot, void* stream);
 int lmd_vls_rows_to_legacy(int64_t n, int64_t n_owned, const double* rows, double* pos4,
                            double* sx, double* sy, double* sz, void* stream);
 /* Force over the lists: one warp per i-tile, lanes by `pattern`; positions

@@ -1059,15 +1059,41 @@ __global__ void vls_refresh_kernel(long long n, const int32_t* __restrict__ perm
   }
 }
 
-// rows_out[k] = rows_in[perm[k]] (3 doubles)
+// rows_out[k] = rows_in[perm[k]] (3 doubles); with disp, the largest squared
+// displacement from build[k] is max-reduced into disp[slot] as well (ghost
+// rows of a decomposition: their displacements count for the inner segment's
+// validity like the owned particles', and are known here without asking
+// their owners)
 __global__ void vls_gather_rows_kernel(long long n, const int32_t* __restrict__ perm,
-                                       const double* __restrict__ in, double* __restrict__ out) {
+                                       const double* __restrict__ in, double* __restrict__ out,
+                                       const double* __restrict__ build,
+                                       unsigned long long* __restrict__ disp, int slot) {
   const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (k >= n) return;
-  const long long s = perm ? perm[k] : k;
-  out[3 * k] = in[3 * s];
-  out[3 * k + 1] = in[3 * s + 1];
-  out[3 * k + 2] = in[3 * s + 2];
+  double d2 = 0.0;
+  if (k < n) {
+    const long long s = perm ? perm[k] : k;
+    const double px = in[3 * s], py = in[3 * s + 1], pz = in[3 * s + 2];
+    out[3 * k] = px;
+    out[3 * k + 1] = py;
+    out[3 * k + 2] = pz;
+    if (disp) {
+      const double ex = __dadd_rn(px, -build[3 * k]), ey = __dadd_rn(py, -build[3 * k + 1]),
+                   ez = __dadd_rn(pz, -build[3 * k + 2]);
+      d2 = __dadd_rn(__dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey)), __dmul_rn(ez, ez));
+    }
+  }
+  if (!disp) return;
+  unsigned long long b = (unsigned long long)__double_as_longlong(d2);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) b = max(b, __shfl_xor_sync(0xffffffffu, b, o));
+  __shared__ unsigned long long wmax[8];
+  if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = b;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int w = 1; w < 8; ++w) b = max(b, wmax[w]);
+    if (b > *reinterpret_cast<volatile unsigned long long*>(disp + slot)) atomicMax(disp + slot, b);
+  }
 }
 
 // rows -> pos4 (ownership OWNED below n_owned, HALO above) and SoA copies
@@ -1332,10 +1358,11 @@ int lmd_vls_refresh(int64_t n, const int32_t* perm, const double* x, const doubl
 }
 
 int lmd_vls_gather_rows(int64_t n, const int32_t* perm, const double* rows_in, double* rows_out,
-                        void* stream) {
+                        const double* build_rows, uint64_t* disp, int32_t slot, void* stream) {
   if (n <= 0) return LMD_OK;
+  if (disp && (!build_rows || (slot != 0 && slot != 1))) return LMD_ERR_CONFIG;
   vls_gather_rows_kernel<<<(unsigned)cdiv(n, 256), 256, 0, (cudaStream_t)stream>>>(
-      n, perm, rows_in, rows_out);
+      n, perm, rows_in, rows_out, build_rows, (unsigned long long*)disp, slot);
   LMD_CHECK_LAUNCH();
   return LMD_OK;
 }

@@ -192,7 +192,7 @@ class VerletListContainer:
             self._disp = torch.zeros(2, dtype=torch.int64, device=dev)
         else:
             self._disp.zero_()
-        self._disp_slot = -1 if self._external_halo else 0
+        self._disp_slot = 0
         self._pos4_stale = bool(self.segmented)
         self._lists.clear()
         self._staging.clear()
@@ -225,10 +225,11 @@ class VerletListContainer:
         n, nh = self.n_owned, self.n_halo
         s = N.stream()
         rows = self._rows
+        track = disp and self._build_rows is not None
         if n and which != "ghosts":
             dp = None
             slot = 0
-            if disp and not self._external_halo and self._build_rows is not None:
+            if track:
                 slot = 0 if self._disp_slot < 0 else self._disp_slot ^ 1
                 dp = self._disp
             N.call("lmd_vls_refresh", n, N.ptr(self._perm), N.ptr(d.pos_x), N.ptr(d.pos_y),
@@ -238,12 +239,18 @@ class VerletListContainer:
                 self._disp_slot = slot if dp is not None else -1
         if not nh or which == "owned":
             return
+        # an external ghost layer: the ghosts' displacements join the same
+        # slot (they decide the inner segment's validity like the owned ones)
+        gslot = self._disp_slot if track and self._disp_slot >= 0 else -1
+        gdp = self._disp if gslot >= 0 else None
+        gbuild = self._build_rows[n:] if gslot >= 0 else None
         if ghost_rows is not None:
             N.call("lmd_vls_gather_rows", nh, N.ptr(self._hperm), N.ptr(ghost_rows),
-                   N.ptr(rows[n:]), s)
+                   N.ptr(rows[n:]), N.ptr(gbuild), N.ptr(gdp), max(gslot, 0), s)
         elif ghosts is not None:
             N.call("lmd_vls_refresh", nh, N.ptr(self._hperm), N.ptr(ghosts.pos_x),
-                   N.ptr(ghosts.pos_y), N.ptr(ghosts.pos_z), N.ptr(rows[n:]), None, None, 0, s)
+                   N.ptr(ghosts.pos_y), N.ptr(ghosts.pos_z), N.ptr(rows[n:]), N.ptr(gbuild),
+                   N.ptr(gdp), max(gslot, 0), s)
         else:
             N.call("lmd_halo_refresh_rows", N.make_box(self.box), nh, N.ptr(self._halo_owner),
                    N.ptr(self._halo_shift), N.ptr(d.pos_x), N.ptr(d.pos_y), N.ptr(d.pos_z),

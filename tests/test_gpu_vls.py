@@ -302,3 +302,37 @@ def test_list_free_kernel_capacity_retry_and_overlap(rng):
     buf = ParticleBuffer.from_positions(pos2, device="cuda")
     with pytest.raises(B.ParticleOverlapError):
         B.force_phase(buf, box, params, B.Configuration.parse("vl,vl,false,v_by_one"), 8)
+
+
+def test_external_ghost_layer_tracks_displacement_for_the_inner_segment(rng):
+    """With a decomposition's ghost layer the inner segment is used while
+    neither an owned particle nor a ghost has moved inner_skin / 2 since the
+    build (the ghost rows' displacements are reduced on the device as they
+    are refreshed), and both segments afterwards; results equal the
+    self-imaged container's either way."""
+    pos, span = _state(rng, 5000, 0.8)
+    params = LJParams(cutoff=2.5, skin=0.3)
+    box = SimulationBox.cube(span, periodic=True)
+    from paper_2512_03565_b200.domain import build_halo
+    for move_ghost in (0.0, 0.02, 0.09):
+        buf = ParticleBuffer.from_positions(pos, device="cuda")
+        halo = build_halo(buf, box, params.interaction_length)
+        ext = B.VerletListContainer(box, params)
+        ext.rebuild(buf, halo)
+        ext.refresh(buf, halo)
+        ext.ensure_lists("v_by_one", False)
+        # move one owned particle near a face together with its images
+        k = int(torch.argmin(buf.pos_x))
+        buf.pos_x[k] += move_ghost
+        halo2 = build_halo(buf, box, params.interaction_length)
+        assert len(halo2) == len(halo)
+        ext.refresh(buf, halo2)
+        assert ext._disp_slot >= 0
+        assert ext._vls_outer() == (move_ghost >= 0.05)
+        st = ext.compute_forces("vl", False, PatternKind.V_BY_ONE, 8)
+        ext.collect_forces(buf)
+        now = buf.positions().cpu().numpy()
+        of, ost = O.force_phase_vl(now, np.zeros(3), np.full(3, span), [True] * 3, params, False,
+                                   "v_by_one", 8)
+        assert st.pair_interactions == ost.pair_interactions
+        assert forces_close(buf.forces().cpu().numpy(), of)
