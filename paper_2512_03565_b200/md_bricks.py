@@ -24,12 +24,13 @@ from dataclasses import dataclass
 import torch
 import torch.distributed as dist
 
+from . import _native as N
 from .containers import needs_rebuild_buffer
 from .domain import SimulationBox, apply_boundaries
 from .driver import make_container
-from .errors import ConfigurationError, SimulationDivergedError
+from .errors import ConfigurationError, ParticleOverlapError, SimulationDivergedError
 from .integrator import POST_FORCE, PRE_FORCE, velocity_verlet_step
-from .kernels import validate_vector_width
+from .kernels import KernelStats, validate_vector_width
 from .particles import HALO, ParticleBuffer
 from .tuning import Configuration, ContainerKind, TimeMetric, Tuner, TuningPolicy
 
@@ -134,6 +135,8 @@ def run_md_bricks(owned: ParticleBuffer, dec, params, iterations: int, vector_wi
     selections: list = []
     force_time = 0.0
     flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    stats_t = N.new_stats(dev)
+    side = torch.cuda.Stream(device=dev) if dev.type == "cuda" else None
     metric = TimeMetric() if tuner is not None else None
     torch.cuda.synchronize(dev)
     if dec.nranks > 1:
@@ -167,7 +170,13 @@ def run_md_bricks(owned: ParticleBuffer, dec, params, iterations: int, vector_wi
             since_migration = 0
             epoch += 1
             rebuilds += 1
-        else:
+        # Steady state on segmented Verlet lists: the ghost exchange runs
+        # while the interior groups (no ghost rows staged) are computing
+        # (launch_force_overlapped); otherwise exchange, refresh, compute.
+        overlapped = (not need and slot[1] == epoch
+                      and cfg.container is ContainerKind.VERLET_LISTS
+                      and cont._vls_for(cfg.pattern, cfg.newton3) is not None)
+        if not need and not overlapped:
             rows = dec.exchange_positions(owned.pos_x, owned.pos_y, owned.pos_z)
             ghosts.pos_x.copy_(rows[:, 0])
             ghosts.pos_y.copy_(rows[:, 1])
@@ -176,7 +185,8 @@ def run_md_bricks(owned: ParticleBuffer, dec, params, iterations: int, vector_wi
             cont.rebuild(owned, ghosts)
             slot[1] = epoch
             displaced = True
-        cont.refresh(owned, ghosts)
+        if not overlapped:
+            cont.refresh(owned, ghosts)
         cont.steps_since_rebuild += 1
         since_migration += 1
         if cfg.container is ContainerKind.VERLET_LISTS:
@@ -184,7 +194,18 @@ def run_md_bricks(owned: ParticleBuffer, dec, params, iterations: int, vector_wi
         t0 = time.perf_counter()
         if metric is not None:
             metric.begin_region()
-        st = cont.compute_forces(cfg.traversal, cfg.newton3, cfg.pattern, vector_width)
+        if overlapped:
+            o = owned
+            stats_t = cont.launch_force_overlapped(
+                o, lambda: dec.exchange_positions(o.pos_x, o.pos_y, o.pos_z), cfg.pattern,
+                cfg.newton3, False, stats_t, side_stream=side)
+            inv, lane_slots, useful = cont.vl_stats(cfg.newton3, cfg.pattern, vector_width)
+            raw = N.read_stats(stats_t)
+            if raw.overlap:
+                raise ParticleOverlapError("zero distance between interacting particles")
+            st = KernelStats(inv, lane_slots, useful, cont.pair_count(raw, cfg.newton3))
+        else:
+            st = cont.compute_forces(cfg.traversal, cfg.newton3, cfg.pattern, vector_width)
         if metric is not None:
             sample = torch.tensor([metric.end_region()], dtype=torch.float64, device=dev)
             sample = float(_allreduce(sample, dec, dist.ReduceOp.MAX).item())
