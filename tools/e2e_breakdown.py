@@ -1,4 +1,6 @@
-"""Time the stages of a one-shot force_phase on host buffers (e2e path)."""
+"""Time the stages of a one-shot force_phase on pinned host buffers (the
+bench's e2e path), each stage between two synchronisations.
+    python tools/e2e_breakdown.py [c4|c2]"""
 import os
 import sys
 import time
@@ -10,11 +12,13 @@ import torch  # noqa: E402
 import paper_2512_03565_b200 as B  # noqa: E402
 from paper_2512_03565_b200 import workloads  # noqa: E402
 from paper_2512_03565_b200.containers import device_soa  # noqa: E402
+from paper_2512_03565_b200.driver import _compute_once, _one_shot, _write_forces_back  # noqa: E402
 
-w = workloads.config2(0.8, n=1_000_000, device="cuda")
-host = w.positions.cpu().numpy()
+which = sys.argv[1] if len(sys.argv) > 1 else "c4"
+w = workloads.config4(256) if which == "c4" else workloads.config2(0.8, n=1_000_000, device="cuda")
+host = w.positions.cpu().numpy() if hasattr(w.positions, "cpu") else np.asarray(w.positions)
 box = B.SimulationBox.cube(w.box_length, periodic=True)
-for label in os.environ.get("CONFIGS", "vl,vl,false,v_by_one+lc,lc_c01,false,half_by_two").split("+"):
+for label in os.environ.get("CONFIGS", "vl,vl,false,v_by_one").split("+"):
     cfg = B.Configuration.parse(label)
     params = B.LJParams(cutoff=2.5, skin=0.0 if cfg.container.value == "lc" else 0.3)
 
@@ -34,18 +38,19 @@ for label in os.environ.get("CONFIGS", "vl,vl,false,v_by_one+lc,lc_c01,false,hal
         d = device_soa(hb)
         torch.cuda.synchronize(); T["h2d"] = time.perf_counter() - t; t = time.perf_counter()
         cont = B.make_container(cfg.container, box, params, cluster_size=8)
+        lean = _one_shot(cont)
         cont.rebuild(d)
+        if not lean:
+            cont.refresh(d)
         torch.cuda.synchronize(); T["rebuild"] = time.perf_counter() - t; t = time.perf_counter()
-        cont.refresh(d)
-        torch.cuda.synchronize(); T["refresh"] = time.perf_counter() - t; t = time.perf_counter()
-        if cfg.container.value == "vl":
-            cont._list(cfg.pattern, cfg.newton3)
-            torch.cuda.synchronize(); T["lists"] = time.perf_counter() - t; t = time.perf_counter()
-        st = cont.compute_forces(cfg.traversal, cfg.newton3, cfg.pattern, 8)
-        torch.cuda.synchronize(); T["force+stats"] = time.perf_counter() - t; t = time.perf_counter()
+        st = _compute_once(cont, cfg, 8, False)
+        torch.cuda.synchronize(); T["force path + stats"] = time.perf_counter() - t; t = time.perf_counter()
         cont.collect_forces(d)
-        for k in ("force_x", "force_y", "force_z"):
-            getattr(hb, k).copy_(getattr(d, k))
+        torch.cuda.synchronize(); T["collect"] = time.perf_counter() - t; t = time.perf_counter()
+        _write_forces_back(hb, d)
         torch.cuda.synchronize(); T["d2h"] = time.perf_counter() - t
-        print(label, " ".join(f"{k}={v*1e3:.2f}ms" for k, v in T.items()),
-              f"total={sum(T.values())*1e3:.2f}ms", flush=True)
+        n = len(host)
+        print(label, w.name, " ".join(f"{k}={v*1e3:.2f}ms" for k, v in T.items()),
+              f"total={sum(T.values())*1e3:.2f}ms pairs={st.pair_interactions}",
+              f"h2d {n*25/T['h2d']/1e9:.1f} GB/s d2h {n*24/T['d2h']/1e9:.1f} GB/s", flush=True)
+        del cont, d
