@@ -469,10 +469,15 @@ int lmd_force_vcl_order(int64_t ncl, int M, int pattern, int flags, const lmd_lj
                         const int32_t* hlist, const double* amin, const double* amax,
                         const double* hmin, const double* hmax, double* fx, double* fy,
                         double* fz, double* ev_scratch, lmd_stats* stats, void* stream);
+/* pos4f (optional, n_records float4 = every record of pos4, owned and halo
+ * clusters): scratch for FP32 copies of the records; the cutoff tests then
+ * run in FP32 against rc^2 + the error bound for coordinates up to max_abs
+ * and the passing pairs are decided by the exact FP64 r2 -- same pairs. */
 int lmd_force_vcl(int64_t ncl, int M, int flags, const lmd_lj* lj, const double* pos4,
                   const int64_t* off, const int32_t* nlist, const int32_t* list,
                   const int64_t* hoff, const int32_t* hnlist, const int32_t* hlist, double* fx,
-                  double* fy, double* fz, double* ev_scratch, lmd_stats* stats, void* stream);
+                  double* fy, double* fz, double* ev_scratch, lmd_stats* stats,
+                  int64_t n_records, float* pos4f, double max_abs, void* stream);
 /* ncl_total = owned + halo clusters of pos4; nd_scratch: ncl_total int32
  * (per-cluster non-dummy counts, computed here). */
 int lmd_vcl_stats(int64_t ncl, int M, int newton3, int a, int b, int vector_width,

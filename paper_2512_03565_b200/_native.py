@@ -204,7 +204,7 @@ _sig("lmd_vcl_pairs", _INT, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _I64, _I64,
      _VP, _VP, _VP, _VP, _VP)
 _sig("lmd_vcl_ev_slots", _I64, _I64)
 _sig("lmd_force_vcl_order", _INT, _I64, _INT, _INT, _INT, C.POINTER(LJ), *([_VP] * 16), _VP)
-_sig("lmd_force_vcl", _INT, _I64, _INT, _INT, C.POINTER(LJ), *([_VP] * 12), _VP)
+_sig("lmd_force_vcl", _INT, _I64, _INT, _INT, C.POINTER(LJ), *([_VP] * 12), _I64, _VP, _D, _VP)
 _sig("lmd_vcl_stats", _INT, _I64, _INT, _INT, _INT, _INT, _INT, *([_VP] * 8), _I64, _VP, _VP,
      _VP)
 _sig("lmd_vcl_collect", _INT, _I64, *([_VP] * 8), _VP)

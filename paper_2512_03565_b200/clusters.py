@@ -108,6 +108,11 @@ class VerletClusterContainer:
         # False: the packed stream kernel for every order (the cluster-aligned
         # M x 32/M mapping with hit compaction, the fastest one on the GPU)
         self.order_kernels = type(self).ORDER_KERNELS
+        # stream kernel: cutoff tests in FP32 with an error band, exact FP64
+        # decision for the pairs that pass (same pairs; the FP64 pipe is the
+        # scarce one)
+        self.fp32_tests = True
+        self._pos4f = None
         self._own = None
         self._stats_cache: dict = {}
 
@@ -304,11 +309,18 @@ class VerletClusterContainer:
                    N.ptr(self._amax), N.ptr(self._hmin), N.ptr(self._hmax), N.ptr(self._fx),
                    N.ptr(self._fy), N.ptr(self._fz), N.ptr(ev_t), N.ptr(stats_t), N.stream())
             return stats_t
+        nrec = int(self._pos4.shape[0])
+        if self._pos4f is None or self._pos4f.shape[0] < nrec:
+            self._pos4f = torch.empty((nrec, 4), dtype=torch.float32, device=dev)
+        # coordinates of owned particles, images and parked dummies stay within
+        # the box grown by the interaction length (plus mid-step drift)
+        max_abs = float(max(np.abs(self.box.min).max(), np.abs(self.box.max).max())) + \
+            2.0 * float(self.params.interaction_length) + 1.0
         N.call("lmd_force_vcl", ncl, self.cluster_size, N.FLAG_ENERGY if energy else 0,
                N.make_lj(self.params), N.ptr(self._pos4), N.ptr(self._off), N.ptr(self._count),
                N.ptr(self._list), N.ptr(self._hoff), N.ptr(self._hcount), N.ptr(self._hlist),
                N.ptr(self._fx), N.ptr(self._fy), N.ptr(self._fz), N.ptr(ev_t), N.ptr(stats_t),
-               N.stream())
+               nrec, N.ptr(self._pos4f) if self.fp32_tests else None, max_abs, N.stream())
         return stats_t
 
     def vcl_stats(self, newton3: bool, pattern, V: int):

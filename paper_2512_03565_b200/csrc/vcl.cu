@@ -247,9 +247,15 @@ __global__ void vcl_pairs_kernel(int ncl, const int32_t* __restrict__ ckey,
 // set bits only.  With ~10 % of cluster-pair tests inside rc, the LJ path runs
 // a few times per unit instead of on nearly every fill.  Same pairs; each
 // lane's summation order is fixed by the list, so results are deterministic.
-template <int MP, bool EV>
+// F32: the cutoff tests run in FP32 on a float4 copy of the records
+// (pos4f) against rc^2 + the conversion / arithmetic error bound, so every
+// pair inside the cutoff passes; the pairs that pass are then decided by the
+// reference's exact FP64 r2 in the LJ loop -- same pairs, 7 FP32 instructions
+// per test instead of 8 FP64 ones on the scarce FP64 pipe.
+template <int MP, bool EV, bool F32>
 __global__ void __launch_bounds__(128)
     vcl_stream_kernel(int ncl, int M, const double* __restrict__ pos4,
+                      const float4* __restrict__ pos4f, float rc2_hi,
                       const long long* __restrict__ off, const int32_t* __restrict__ nlist,
                       const int32_t* __restrict__ list, const long long* __restrict__ hoff,
                       const int32_t* __restrict__ hnlist, const int32_t* __restrict__ hlist,
@@ -276,6 +282,7 @@ __global__ void __launch_bounds__(128)
       const long long gi = (long long)a * M + (ilive ? islot : 0);
       const double4 pi = ld_pos4(pos4, gi);
       const bool iown = ilive && pi.w == (double)LMD_OWNED;
+      const float pxf = (float)pi.x, pyf = (float)pi.y, pzf = (float)pi.z;
       double ax = 0.0, ay = 0.0, az = 0.0;
       // R = 32 / MP units per lane fill one 32-bit hit mask (unit r at bits
       // [r * MP, r * MP + M)), so the LJ loop runs once per set bit over R
@@ -298,9 +305,16 @@ __global__ void __launch_bounds__(128)
             unsigned m = 0u;
 #pragma unroll 4
             for (int q = 0; q < cnt; ++q) {
-              const double4 pj = ld_pos4(pos4, base + q);
-              const double r2 = r2_exact(pi.x - pj.x, pi.y - pj.y, pi.z - pj.z);
-              m |= (pj.w != (double)LMD_DUMMY && r2 < k.rc2 ? 1u : 0u) << q;
+              if (F32) {
+                const float4 pj = __ldg(pos4f + base + q);
+                const float dx = pxf - pj.x, dy = pyf - pj.y, dz = pzf - pj.z;
+                const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+                m |= (pj.w != (float)LMD_DUMMY && r2 < rc2_hi ? 1u : 0u) << q;
+              } else {
+                const double4 pj = ld_pos4(pos4, base + q);
+                const double r2 = r2_exact(pi.x - pj.x, pi.y - pj.y, pi.z - pj.z);
+                m |= (pj.w != (double)LMD_DUMMY && r2 < k.rc2 ? 1u : 0u) << q;
+              }
             }
             if (bc == a) {   // self unit: not with itself
               const unsigned self = (unsigned)(gi - base);
@@ -317,6 +331,7 @@ __global__ void __launch_bounds__(128)
             const double4 pj = ld_pos4(pos4, gj);
             const double dx = pi.x - pj.x, dy = pi.y - pj.y, dz = pi.z - pj.z;
             const double r2 = r2_exact(dx, dy, dz);
+            if (F32 && r2 >= k.rc2) continue;   // passed the FP32 band only
             if (r2 == 0.0) {
               overlap = 1;
               continue;
@@ -364,6 +379,18 @@ __global__ void __launch_bounds__(128)
       ev[2 * warp + 1] = v_acc;
     }
   }
+}
+
+// float4 copies of the (x, y, z, ownership) records for the FP32 tests
+// (packing two records per load for FADD2 / FFMA2 arithmetic was measured:
+// no gain at M = 8 / 32, slower at M = 4 -- the LJ loop over the set bits,
+// not the tests, bounds the kernel then)
+__global__ void vcl_to_f32_kernel(long long n, const double4* __restrict__ pos4,
+                                  float4* __restrict__ out) {
+  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const double4 p = pos4[k];
+  out[k] = make_float4((float)p.x, (float)p.y, (float)p.z, (float)p.w);
 }
 
 // Interaction orders as warp mappings.  One warp per owned cluster a; the
@@ -791,7 +818,8 @@ int lmd_force_vcl_order(int64_t ncl, int M, int pattern, int flags, const lmd_lj
 int lmd_force_vcl(int64_t ncl, int M, int flags, const lmd_lj* lj, const double* pos4,
                   const int64_t* off, const int32_t* nlist, const int32_t* list,
                   const int64_t* hoff, const int32_t* hnlist, const int32_t* hlist, double* fx,
-                  double* fy, double* fz, double* ev_scratch, lmd_stats* stats, void* stream) {
+                  double* fy, double* fz, double* ev_scratch, lmd_stats* stats,
+                  int64_t n_records, float* pos4f, double max_abs, void* stream) {
   if (ncl <= 0) return LMD_OK;
   if (M < 2) return LMD_ERR_CONFIG;
   const LJK k = make_ljk(lj);
@@ -799,16 +827,35 @@ int lmd_force_vcl(int64_t ncl, int M, int flags, const lmd_lj* lj, const double*
   const bool ev = (flags & LMD_FLAG_ENERGY) != 0;
   const unsigned blocks = (unsigned)cdiv(ncl, 4);
   const int mp = M >= 32 ? 32 : M > 8 ? 16 : M > 4 ? 8 : M > 2 ? 4 : 2;
-#define LMD_VCLK(MPV)                                                                         \
-  do {                                                                                        \
-    if (ev)                                                                                   \
-      vcl_stream_kernel<MPV, true><<<blocks, 128, 0, s>>>(                                    \
-          (int)ncl, M, pos4, (const long long*)off, nlist, list, (const long long*)hoff,      \
-          hnlist, hlist, k, fx, fy, fz, ev_scratch, stats);                                   \
-    else                                                                                      \
-      vcl_stream_kernel<MPV, false><<<blocks, 128, 0, s>>>(                                   \
-          (int)ncl, M, pos4, (const long long*)off, nlist, list, (const long long*)hoff,      \
-          hnlist, hlist, k, fx, fy, fz, ev_scratch, stats);                                   \
+  // FP32 tests (pos4f != NULL): |FP32 r2 - exact r2| <= err for coordinates
+  // up to max_abs (conversion 2^-24 |x| per coordinate, twice per difference,
+  // times 2 |d| summed over the axes; a few ulp of r2 for the arithmetic),
+  // doubled for safety
+  float rc2_hi = 0.f;
+  const bool f32 = pos4f != nullptr && n_records > 0 && max_abs > 0.0 && isfinite(max_abs);
+  if (f32) {
+    const double eps = 5.9604644775390625e-8, rc = lj->cutoff;
+    const double err = 2.0 * (4.0 * 1.7320508075688772 * (rc + 1.0) * eps * max_abs +
+                              8.0 * eps * (k.rc2 + 1.0));
+    rc2_hi = (float)(k.rc2 + err);
+    rc2_hi = nextafterf(rc2_hi, INFINITY);
+    vcl_to_f32_kernel<<<(unsigned)cdiv(n_records, 256), 256, 0, s>>>(
+        n_records, (const double4*)pos4, (float4*)pos4f);
+    LMD_CHECK_LAUNCH();
+  }
+#define LMD_VCLK2(MPV, EVB, FB)                                                             \
+  vcl_stream_kernel<MPV, EVB, FB><<<blocks, 128, 0, s>>>(                                   \
+      (int)ncl, M, pos4, (const float4*)pos4f, rc2_hi, (const long long*)off, nlist, list,  \
+      (const long long*)hoff, hnlist, hlist, k, fx, fy, fz, ev_scratch, stats)
+#define LMD_VCLK(MPV)                  \
+  do {                                 \
+    if (ev) {                          \
+      if (f32) LMD_VCLK2(MPV, true, true);   \
+      else LMD_VCLK2(MPV, true, false);      \
+    } else {                           \
+      if (f32) LMD_VCLK2(MPV, false, true);  \
+      else LMD_VCLK2(MPV, false, false);     \
+    }                                  \
   } while (0)
   switch (mp) {
     case 2: LMD_VCLK(2); break;
@@ -818,6 +865,7 @@ int lmd_force_vcl(int64_t ncl, int M, int flags, const lmd_lj* lj, const double*
     default: LMD_VCLK(32); break;
   }
 #undef LMD_VCLK
+#undef LMD_VCLK2
   LMD_CHECK_LAUNCH();
   if (ev) return reduce_ev(ev_scratch, lmd_vcl_ev_slots(ncl), stats, s);
   return LMD_OK;
