@@ -237,7 +237,9 @@ class Phase:
         if self.overlapped:
             return 2 + 2
         if self.kind == "vl":
-            return 1 + 2
+            # segmented lists: one refresh launch (owned rows + derived images
+            # + displacement) and the force kernel; a ghost layer adds its gather
+            return 2 if self.dec is None else 3
         if self.kind == "lc":
             return 1 + 2
         return 1

@@ -349,7 +349,9 @@ int lmd_force_vl_staged(int newton3, int flags, const lmd_lj* lj, int64_t n_owne
  * n_index groups it lists (e.g. the interior groups, which stage no image or
  * ghost rows, while a ghost exchange is in flight); LMD_FLAG_DEFER_EV leaves
  * the energy/virial reduction over all groups to lmd_vls_reduce_ev.  lmd_vls_refresh: rows[k] =
- * (x, y, z)[perm[k]] (perm NULL: identity) and with disp != NULL the
+ * (x, y, z)[perm[k]] (perm NULL: identity); with n_images > 0 also rows[n +
+ * k'] = the periodic image k' (position of owner[k'] + the exact shift of
+ * its code, domain.py:112-118: one launch for the whole backing); with disp != NULL the
  * largest squared displacement from build_rows max-reduced into disp[slot]
  * (disp[slot ^ 1] cleared).  lmd_vls_gather_rows (ghost rows of a
  * decomposition; with disp != NULL their displacement from build_rows is
@@ -399,7 +401,8 @@ int lmd_vls_direct(const lmd_grid* g, int newton3, int flags, const lmd_lj* lj, 
 int lmd_vls_reduce_ev(int64_t n_groups, const double* ev_scratch, lmd_stats* stats, void* stream);
 int lmd_vls_refresh(int64_t n, const int32_t* perm, const double* x, const double* y,
                     const double* z, double* rows, const double* build_rows, uint64_t* disp,
-                    int32_t slot, void* stream);
+                    int32_t slot, const lmd_box* box, int64_t n_images, const int32_t* owner,
+                    const int8_t* shift, void* stream);
 int lmd_vls_gather_rows(int64_t n, const int32_t* perm, const double* rows_in, double* rows_out,
                         const double* build_rows, uint64_t* disp, int32_t slot, void* stream);
 int lmd_vls_rows_to_legacy(int64_t n, int64_t n_owned, const double* rows, double* pos4,

@@ -189,7 +189,8 @@ _sig("lmd_vls_force", _INT, _INT, _INT, C.POINTER(LJ), _I64, _I32, _VP, _VP, _I6
 _sig("lmd_vls_direct", _INT, C.POINTER(Grid), _INT, _INT, C.POINTER(LJ), _I64, _I32, _VP, _VP,
      _VP, _VP, _VP, _VP, _I64, _I32, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP)
 _sig("lmd_vls_reduce_ev", _INT, _I64, _VP, _VP, _VP)
-_sig("lmd_vls_refresh", _INT, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _I32, _VP)
+_sig("lmd_vls_refresh", _INT, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _I32, C.POINTER(Box), _I64,
+     _VP, _VP, _VP)
 _sig("lmd_vls_gather_rows", _INT, _I64, _VP, _VP, _VP, _VP, _VP, _I32, _VP)
 _sig("lmd_vls_rows_to_legacy", _INT, _I64, _I64, _VP, _VP, _VP, _VP, _VP, _VP)
 _sig("lmd_force_vl", _INT, _INT, _INT, _INT, C.POINTER(LJ), _I64, _VP, _VP, _I64, _VP, _VP,

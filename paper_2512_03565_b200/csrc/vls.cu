@@ -1020,13 +1020,33 @@ __global__ void __launch_bounds__(kVsG, 5)
 // largest squared displacement from build[k], max-reduced into disp[slot]
 // (bit pattern of a non-negative double); disp[slot ^ 1] is cleared for the
 // next launch
+// nh > 0: threads n .. n + nh - 1 also write the periodic images (rows n ..):
+// image k' = position of owner[k'] (caller order) + the exact shift its code
+// names per axis (0 none, 1 + (hi - lo), 2 + (lo - hi): domain.py:112-118),
+// so one launch refreshes the whole backing
+struct VsImg {
+  double up[3], down[3];   // hi - lo, lo - hi per axis (rounded once, as the reference's)
+};
 __global__ void vls_refresh_kernel(long long n, const int32_t* __restrict__ perm,
                                    const double* __restrict__ x, const double* __restrict__ y,
                                    const double* __restrict__ z, double* __restrict__ rows,
                                    const double* __restrict__ build,
-                                   unsigned long long* __restrict__ disp, int slot) {
+                                   unsigned long long* __restrict__ disp, int slot, long long nh,
+                                   const int32_t* __restrict__ owner,
+                                   const int8_t* __restrict__ shift, VsImg img) {
   const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   double d2 = 0.0;
+  if (k >= n && k < n + nh) {
+    const int o = owner[k - n];
+    int sc = shift[k - n];
+    const double p[3] = {x[o], y[o], z[o]};
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+      const int d = sc % 3;
+      sc /= 3;
+      rows[3 * k + ax] = __dadd_rn(p[ax], d == 1 ? img.up[ax] : (d == 2 ? img.down[ax] : 0.0));
+    }
+  }
   if (k < n) {
     const int s = perm ? perm[k] : (int)k;
     const double px = x[s], py = y[s], pz = z[s];
@@ -1346,13 +1366,23 @@ int lmd_vls_reduce_ev(int64_t n_groups, const double* ev_scratch, lmd_stats* sta
 
 int lmd_vls_refresh(int64_t n, const int32_t* perm, const double* x, const double* y,
                     const double* z, double* rows, const double* build_rows, uint64_t* disp,
-                    int32_t slot, void* stream) {
+                    int32_t slot, const lmd_box* box, int64_t n_images, const int32_t* owner,
+                    const int8_t* shift, void* stream) {
   if (n <= 0) return LMD_OK;
   if (slot != 0 && slot != 1) return LMD_ERR_CONFIG;
   if (disp && !build_rows) return LMD_ERR_CONFIG;
+  if (n_images > 0 && (!box || !owner || !shift)) return LMD_ERR_CONFIG;
   cudaStream_t s = (cudaStream_t)stream;
-  vls_refresh_kernel<<<(unsigned)cdiv(n, 256), 256, 0, s>>>(
-      n, perm, x, y, z, rows, build_rows, (unsigned long long*)disp, slot);
+  VsImg img = {};
+  if (n_images > 0)
+    for (int ax = 0; ax < 3; ++ax) {
+      img.up[ax] = box->hi[ax] - box->lo[ax];
+      img.down[ax] = box->lo[ax] - box->hi[ax];
+    }
+  const long long total = n + (n_images > 0 ? n_images : 0);
+  vls_refresh_kernel<<<(unsigned)cdiv(total, 256), 256, 0, s>>>(
+      n, perm, x, y, z, rows, build_rows, (unsigned long long*)disp, slot,
+      n_images > 0 ? n_images : 0, owner, shift, img);
   LMD_CHECK_LAUNCH();
   return LMD_OK;
 }

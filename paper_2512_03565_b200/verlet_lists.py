@@ -232,11 +232,19 @@ class VerletListContainer:
             if track:
                 slot = 0 if self._disp_slot < 0 else self._disp_slot ^ 1
                 dp = self._disp
+            # derived periodic images move with their owners in the same launch
+            with_images = (which == "all" and nh > 0 and ghost_rows is None and ghosts is None
+                           and not self._external_halo)
             N.call("lmd_vls_refresh", n, N.ptr(self._perm), N.ptr(d.pos_x), N.ptr(d.pos_y),
                    N.ptr(d.pos_z), N.ptr(rows), N.ptr(self._build_rows) if dp is not None else None,
-                   N.ptr(dp), slot, s)
+                   N.ptr(dp), slot, N.make_box(self.box) if with_images else None,
+                   nh if with_images else 0,
+                   N.ptr(self._halo_owner) if with_images else None,
+                   N.ptr(self._halo_shift) if with_images else None, s)
             if disp:
                 self._disp_slot = slot if dp is not None else -1
+            if with_images:
+                return
         if not nh or which == "owned":
             return
         # an external ghost layer: the ghosts' displacements join the same
@@ -250,7 +258,7 @@ class VerletListContainer:
         elif ghosts is not None:
             N.call("lmd_vls_refresh", nh, N.ptr(self._hperm), N.ptr(ghosts.pos_x),
                    N.ptr(ghosts.pos_y), N.ptr(ghosts.pos_z), N.ptr(rows[n:]), N.ptr(gbuild),
-                   N.ptr(gdp), max(gslot, 0), s)
+                   N.ptr(gdp), max(gslot, 0), None, 0, None, None, s)
         else:
             N.call("lmd_halo_refresh_rows", N.make_box(self.box), nh, N.ptr(self._halo_owner),
                    N.ptr(self._halo_shift), N.ptr(d.pos_x), N.ptr(d.pos_y), N.ptr(d.pos_z),
